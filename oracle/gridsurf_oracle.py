@@ -1,0 +1,808 @@
+"""CPU oracle for one GO-Surf training step -- TEST INFRASTRUCTURE ONLY.
+
+This module is the checker, never the product: only ``tests/``,
+``__graft_entry__.smoke()`` and ``bench.py``'s CPU-baseline leg may import
+it.  The GPU path in ``paper_2206_14735_b200`` never calls into it.
+
+It restates, in plain numpy, the reference's per-iteration optimisation
+step (``gs/`` = ``/root/reference/pkg/src/gridsurf/``):
+
+    draw_ray_batch            gs/sampler.py:58-88
+    train_objective (forward) gs/renderer.py:279-468
+    dc.grad(total, params)    gs/diffcore.py:1035-1104  (hand-derived adjoints,
+                              SURVEY.md Appendix A; no generic autodiff)
+    Adam.step                 gs/optimizer.py:38-91
+
+Forward values are computed with the *same numpy operations in the same
+order* as the reference, so in both precisions every forward quantity
+(ray batch, stratified and importance depths, phi, grad-phi, colours,
+weights, loss parts) is bit-identical to the reference run on the same
+machine (pinned by ``tests/golden``).  The backward uses closed-form
+adjoints instead of the tape; it agrees with the reference to ~1e-15
+relative in double precision and to ~1e-5 (max-norm relative) in single.
+
+Parity pinning: ``tests/golden/make_golden.py`` runs the reference package
+itself and stores its outputs; ``tests/test_oracle_golden.py`` checks this
+module against them.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+SIGMA_FLOOR = 1e-12  # gs/renderer.py:42
+TRANS_FLOOR = 1e-15  # gs/renderer.py:43
+MIN_SEPARATION = 1e-9  # gs/sampler.py:32
+
+# stream tags, gs/seeds.py:14-25
+RAYS, STRATIFY, IMPORTANCE, SMOOTH = 1, 2, 3, 4
+SPHERE_INIT, NET_INIT, GRID_INIT = 7, 9, 10
+
+
+def substream(seed, tag, *indices):
+    """gs/seeds.py:28-30."""
+    return np.random.default_rng(
+        np.random.SeedSequence((int(seed), int(tag)) + tuple(int(i) for i in indices)))
+
+
+# ---------------------------------------------------------------------------
+# camera (gs/camera.py:142-171)
+
+
+def pixel_rays(intr, pixels):
+    """gs/camera.py:142-157 (float64)."""
+    px = np.atleast_2d(np.asarray(pixels, dtype=np.float64))
+    d = np.stack([(px[:, 0] - intr.cx) / intr.fx, (px[:, 1] - intr.cy) / intr.fy,
+                  np.ones(px.shape[0])], axis=1)
+    return d / np.linalg.norm(d, axis=1, keepdims=True)
+
+
+def ray_to_z_scale(intr, pixels):
+    """gs/camera.py:160-171."""
+    px = np.atleast_2d(np.asarray(pixels, dtype=np.float64))
+    d = np.stack([(px[:, 0] - intr.cx) / intr.fx, (px[:, 1] - intr.cy) / intr.fy,
+                  np.ones(px.shape[0])], axis=1)
+    return np.linalg.norm(d, axis=1)
+
+
+# ---------------------------------------------------------------------------
+# sampler (gs/sampler.py)
+
+
+class Batch:
+    """gs/sampler.py:35-55 (RayBatch)."""
+
+    def __init__(self, frame_ids, pixels, color, depth_ray, valid, dir_cam, near, far):
+        self.frame_ids, self.pixels, self.color = frame_ids, pixels, color
+        self.depth_ray, self.valid, self.dir_cam = depth_ray, valid, dir_cam
+        self.near, self.far = near, far
+
+    def __len__(self):
+        return self.frame_ids.shape[0]
+
+
+def draw_ray_batch(dataset, rng, m, near=0.01, far=8.0):
+    """gs/sampler.py:58-88."""
+    intr = dataset.intrinsics
+    f = dataset.colors.shape[0]
+    h, w = intr.height, intr.width
+    flat = rng.integers(0, f * h * w, size=m)
+    return batch_from_flat(dataset, flat, near, far)
+
+
+def batch_from_flat(dataset, flat, near=0.01, far=8.0):
+    """Deterministic part of gs/sampler.py:70-88 given the drawn flat ids."""
+    intr = dataset.intrinsics
+    h, w = intr.height, intr.width
+    m = flat.shape[0]
+    frame = flat // (h * w)
+    rem = flat % (h * w)
+    v, u = rem // w, rem % w
+    pixels = np.stack([u, v], axis=1).astype(np.float64)
+    color = dataset.colors[frame, v, u].astype(np.float64)
+    depth_z = dataset.depths[frame, v, u].astype(np.float64)
+    valid = depth_z > 0
+    scale = ray_to_z_scale(intr, pixels)
+    return Batch(frame.astype(np.int64), pixels, color, depth_z * scale, valid,
+                 pixel_rays(intr, pixels), np.full(m, near), np.full(m, far))
+
+
+def stratified_coarse(near, far, n, uniforms):
+    """gs/sampler.py:91-107."""
+    near = np.asarray(near)
+    far = np.asarray(far)
+    if np.any(far <= near):
+        raise ValueError("degenerate ray bounds")
+    steps = (np.arange(n) + uniforms) / n
+    return near[:, None] + (far - near)[:, None] * steps
+
+
+def enforce_separation(depths, min_sep=MIN_SEPARATION):
+    """gs/sampler.py:172-197."""
+    d = np.asarray(depths)
+    gaps = np.diff(d, axis=1)
+    bad_rows = np.where((gaps < min_sep).any(axis=1))[0]
+    if bad_rows.size == 0:
+        return d
+    d = d.copy()
+    k = d.shape[1]
+    for r in bad_rows:
+        row = list(d[r])
+        kept = [row[0]]
+        for x in row[1:]:
+            if x - kept[-1] >= min_sep:
+                kept.append(x)
+        while len(kept) < k:
+            diffs = np.diff(kept)
+            j = int(np.argmax(diffs))
+            kept.insert(j + 1, kept[j] + diffs[j] / 2.0)
+        d[r] = kept
+    return d
+
+
+def importance_refine_with_sources(depths, weights, near, far, uniforms):
+    """gs/sampler.py:128-169."""
+    depths = np.asarray(depths)
+    w = np.asarray(weights)[:, :-1].copy()
+    if np.any(w < 0):
+        raise ValueError("weights must be non-negative")
+    m, a = uniforms.shape
+    k = depths.shape[1]
+    total = w.sum(axis=1, keepdims=True)
+    dead = total[:, 0] <= 0.0
+    w[dead] = 1.0
+    cdf = np.cumsum(w, axis=1)
+    cdf /= cdf[:, -1:]
+    idx = np.sum(cdf[:, None, :] <= uniforms[:, :, None], axis=2)
+    idx = np.minimum(idx, w.shape[1] - 1)
+    cdf_pad = np.concatenate([np.zeros((m, 1)), cdf], axis=1)
+    lo = np.take_along_axis(cdf_pad, idx, axis=1)
+    hi = np.take_along_axis(cdf_pad, idx + 1, axis=1)
+    frac = np.where(hi > lo, (uniforms - lo) / np.maximum(hi - lo, 1e-300), 0.5)
+    d_lo = np.take_along_axis(depths, idx, axis=1)
+    d_hi = np.take_along_axis(depths, idx + 1, axis=1)
+    new = d_lo + frac * (d_hi - d_lo)
+    if np.any(dead):
+        new[dead] = near[dead, None] + uniforms[dead] * (far - near)[dead, None]
+    cat = np.concatenate([depths, new], axis=1)
+    src = np.concatenate(
+        [np.tile(np.arange(k), (m, 1)), np.full((m, a), -1, dtype=np.int64)], axis=1)
+    order = np.argsort(cat, axis=1, kind="stable")
+    merged = np.take_along_axis(cat, order, axis=1)
+    src = np.take_along_axis(src, order, axis=1)
+    out = enforce_separation(merged)
+    src = np.where(out == merged, src, -1)
+    return out, src
+
+
+# ---------------------------------------------------------------------------
+# trilinear grid (gs/diffcore.py:704-920)
+
+
+class GridBoundsError(ValueError):
+    pass
+
+
+class Level:
+    """GridGeom + features (gs/diffcore.py:704-728, gs/feature_grid.py:39-64)."""
+
+    def __init__(self, origin, voxel_size, dims, feat):
+        self.origin = np.asarray(origin, dtype=np.float64)
+        self.voxel_size = float(voxel_size)
+        self.dims = tuple(int(d) for d in dims)
+        self.feat = feat
+
+    @property
+    def n_vertices(self):
+        return self.dims[0] * self.dims[1] * self.dims[2]
+
+
+_CORNER_OFFSETS = np.array(
+    [[dx, dy, dz] for dx in (0, 1) for dy in (0, 1) for dz in (0, 1)], dtype=np.int64)
+
+
+def locate(points, lev):
+    """gs/diffcore.py:738-751."""
+    local = (points - lev.origin) / lev.voxel_size
+    dims = np.array(lev.dims)
+    eps = 1e-9 * max(lev.dims)
+    if np.any(local < -eps) or np.any(local > (dims - 1) + eps):
+        raise GridBoundsError("sample point(s) outside grid box")
+    cell = np.minimum(np.floor(local).astype(np.int64), dims - 2)
+    cell = np.maximum(cell, 0)
+    return cell, local - cell
+
+
+def corner_index(cell, lev):
+    """gs/diffcore.py:754-758 (x-major, z fastest; k = 4dx + 2dy + dz)."""
+    nx, ny, nz = lev.dims
+    flat = (cell[:, 0] * ny + cell[:, 1]) * nz + cell[:, 2]
+    offs = (_CORNER_OFFSETS[:, 0] * ny + _CORNER_OFFSETS[:, 1]) * nz + _CORNER_OFFSETS[:, 2]
+    return flat[:, None] + offs[None, :]
+
+
+def corner_weights(frac):
+    """gs/diffcore.py:761-767."""
+    fx, fy, fz = frac[:, 0], frac[:, 1], frac[:, 2]
+    wx = np.stack([1.0 - fx, fx], axis=1)
+    wy = np.stack([1.0 - fy, fy], axis=1)
+    wz = np.stack([1.0 - fz, fz], axis=1)
+    w = wx[:, :, None, None] * wy[:, None, :, None] * wz[:, None, None, :]
+    return w.reshape(frac.shape[0], 8)
+
+
+def corner_jacobian(frac):
+    """d w_k / d frac_a, (N, 8, 3): gs/diffcore.py:770-780."""
+    fx, fy, fz = frac[:, 0], frac[:, 1], frac[:, 2]
+    wx = np.stack([1.0 - fx, fx], axis=1)
+    wy = np.stack([1.0 - fy, fy], axis=1)
+    wz = np.stack([1.0 - fz, fz], axis=1)
+    sx = np.stack([-np.ones_like(fx), np.ones_like(fx)], axis=1)
+    jx = (sx[:, :, None, None] * wy[:, None, :, None] * wz[:, None, None, :]).reshape(-1, 8)
+    jy = (wx[:, :, None, None] * sx[:, None, :, None] * wz[:, None, None, :]).reshape(-1, 8)
+    jz = (wx[:, :, None, None] * wy[:, None, :, None] * sx[:, None, None, :]).reshape(-1, 8)
+    return np.stack([jx, jy, jz], axis=2)
+
+
+def gather_weighted(feat, idx8, w8):
+    """gs/diffcore.py:816-827 with numba's arithmetic: the f64 product is
+    added to the storage-dtype accumulator and rounded back per corner."""
+    dt = feat.dtype
+    out = np.zeros((idx8.shape[0], feat.shape[1]), dtype=dt)
+    for k in range(8):
+        out = (out + w8[:, k:k + 1] * feat[idx8[:, k]]).astype(dt)
+    return out
+
+
+def scatter_weighted(idx8, w8, g, n_vertices):
+    """gs/diffcore.py:830-841 (accumulated in float64, returned in g's dtype)."""
+    out = np.zeros((n_vertices, g.shape[1]), dtype=np.float64)
+    for k in range(8):
+        np.add.at(out, idx8[:, k], w8[:, k:k + 1] * g.astype(np.float64))
+    return out.astype(g.dtype)
+
+
+class LevelSample:
+    """Per-point lattice location for one level (everything grid_sample keeps)."""
+
+    def __init__(self, lev, pts):
+        cell, self.frac = locate(pts, lev)
+        self.idx8 = corner_index(cell, lev)
+        self.w8 = corner_weights(self.frac)
+        self.lev = lev
+
+    def value(self):
+        return gather_weighted(self.lev.feat, self.idx8, self.w8)
+
+    def ju(self, u):
+        """gs/diffcore.py:874-890: ju[n,k] = sum_a dw_k/dx_a u_a (world units)."""
+        J = corner_jacobian(self.frac)  # (N, 8, 3) cell units
+        return np.einsum("nka,na->nk", J, u.astype(np.float64)) / self.lev.voxel_size
+
+    def dx(self, g):
+        """gs/diffcore.py:844-871: grad_x <interp(feat, x), g>, (N, 3) in g.dtype,
+        with numba's arithmetic (storage-dtype channel products summed into a
+        float64 accumulator, per-corner rounding of the output)."""
+        dt = g.dtype
+        feat = self.lev.feat
+        fx, fy, fz = self.frac[:, 0], self.frac[:, 1], self.frac[:, 2]
+        out = np.zeros((g.shape[0], 3), dtype=dt)
+        for k in range(8):
+            rows = feat[self.idx8[:, k]]
+            acc = np.zeros(g.shape[0], dtype=np.float64)
+            for j in range(g.shape[1]):
+                acc = acc + (rows[:, j] * g[:, j]).astype(np.float64)
+            wx = fx if k & 4 else 1.0 - fx
+            wy = fy if k & 2 else 1.0 - fy
+            wz = fz if k & 1 else 1.0 - fz
+            sx = 1.0 if k & 4 else -1.0
+            sy = 1.0 if k & 2 else -1.0
+            sz = 1.0 if k & 1 else -1.0
+            out[:, 0] = (out[:, 0] + acc * sx * wy * wz).astype(dt)
+            out[:, 1] = (out[:, 1] + acc * wx * sy * wz).astype(dt)
+            out[:, 2] = (out[:, 2] + acc * wx * wy * sz).astype(dt)
+        inv_vs = 1.0 / self.lev.voxel_size
+        return (out * inv_vs).astype(dt)
+
+
+def sigmoid_raw(x):
+    """gs/diffcore.py:445-451."""
+    out = np.empty_like(x)
+    pos = x >= 0
+    out[pos] = 1.0 / (1.0 + np.exp(-x[pos]))
+    ex = np.exp(x[~pos])
+    out[~pos] = ex / (1.0 + ex)
+    return out
+
+
+# ---------------------------------------------------------------------------
+# model container
+
+
+class Params:
+    """ModelState restated (gs/renderer.py:69-105): grids coarse->fine,
+    colour grid, two DecoderNets [(W (in,out), b)], log_s, frozen poses."""
+
+    def __init__(self, levels, color, geom, color_net, log_s, lo, hi, poses):
+        self.levels, self.color = levels, color
+        self.geom, self.color_net = geom, color_net
+        self.log_s = log_s
+        self.lo = np.asarray(lo, dtype=np.float64)
+        self.hi = np.asarray(hi, dtype=np.float64)
+        self.poses = np.asarray(poses, dtype=np.float64)  # (F, 4, 4)
+
+    @property
+    def dtype(self):
+        return self.levels[0].feat.dtype
+
+    @property
+    def finest_voxel(self):
+        return min(l.voxel_size for l in self.levels)
+
+    def pose_matrices(self):
+        """gs/renderer.py:104-105 / gs/camera.py:75-80: R0 @ exp(0) = R0 and
+        the translation as stored (PoseParam.t is in the model dtype)."""
+        m = self.poses.copy()
+        m[:, :3, 3] = m[:, :3, 3].astype(self.dtype).astype(np.float64)
+        return m
+
+    def names(self):
+        """gs/optimizer.py:217-226 (no trainable poses)."""
+        n = [f"level{i}" for i in range(len(self.levels))] + ["colorgrid"]
+        for tag, net in (("geom", self.geom), ("color", self.color_net)):
+            for i in range(len(net)):
+                n += [f"{tag}_w{i}", f"{tag}_b{i}"]
+        return n + ["log_s"]
+
+    def arrays(self):
+        out = [l.feat for l in self.levels] + [self.color.feat]
+        for net in (self.geom, self.color_net):
+            for W, b in net:
+                out += [W, b]
+        return out + [self.log_s]
+
+    def lrs(self, lr_grids=1e-2, lr_decoders=1e-3):
+        """gs/optimizer.py:229-236."""
+        ng = len(self.levels) + 1
+        return [lr_grids] * ng + [lr_decoders] * (len(self.arrays()) - ng)
+
+    def copy(self):
+        cp = lambda l: Level(l.origin, l.voxel_size, l.dims, l.feat.copy())
+        return Params([cp(l) for l in self.levels], cp(self.color),
+                      [(W.copy(), b.copy()) for W, b in self.geom],
+                      [(W.copy(), b.copy()) for W, b in self.color_net],
+                      self.log_s.copy(), self.lo, self.hi, self.poses)
+
+
+def create_params(lo, hi, poses, seed=0, voxel_sizes=(0.96, 0.24, 0.06, 0.03),
+                  geom_width=4, color_voxel=None, color_width=6, dtype=np.float64,
+                  truncation=0.16):
+    """build_model(skip_init=True) restated: gs/optimizer.py:181-205,
+    MultiGrid.create gs/feature_grid.py:48-91, DecoderNet.create
+    gs/decoders.py:40-49 (same RNG streams and draw order)."""
+    lo = np.asarray(lo, dtype=np.float64)
+    hi = np.asarray(hi, dtype=np.float64)
+    rng = substream(seed, GRID_INIT)
+
+    def level(vs, width):
+        dims = np.maximum(np.ceil((hi - lo) / vs).astype(int) + 1, 2)
+        n = int(np.prod(dims))
+        feats = rng.uniform(-1e-4, 1e-4, size=(n, width)).astype(dtype)
+        return Level(lo, vs, dims, feats)
+
+    sizes = sorted(voxel_sizes, reverse=True)
+    levels = [level(vs, geom_width) for vs in sizes]
+    color = level(sizes[-1] if color_voxel is None else color_voxel, color_width)
+
+    def net(in_w, out_w, r):
+        sz = [in_w, 32, 32, out_w]
+        layers = []
+        for a, b in zip(sz[:-1], sz[1:]):
+            bound = np.sqrt(6.0 / a)
+            W = r.uniform(-bound, bound, size=(a, b)).astype(dtype)
+            layers.append((W, np.zeros(b, dtype=dtype)))
+        return layers
+
+    geom = net(geom_width * len(levels), 1, substream(seed, NET_INIT, 0))
+    cnet = net(color_width + 3, 3, substream(seed, NET_INIT, 1))
+    log_s = np.asarray(np.log(1.0 / truncation), dtype=dtype)
+    return Params(levels, color, geom, cnet, log_s, lo, hi, poses)
+
+
+def mlp_forward(layers, x):
+    """gs/decoders.py:55-63: returns (pre-activations, activations, out)."""
+    h = x
+    pre, acts = [], []
+    last = len(layers) - 1
+    for i, (W, b) in enumerate(layers):
+        a = np.matmul(h, W) + b.reshape(1, -1)
+        pre.append(a)
+        if i < last:
+            h = np.maximum(a, 0.0)
+            acts.append(h)
+        else:
+            h = a
+    return pre, acts, h
+
+
+def sample_multi(P, pts):
+    """gs/feature_grid.py:135-139."""
+    ls = [LevelSample(l, pts) for l in P.levels]
+    return ls, np.concatenate([s.value() for s in ls], axis=1)
+
+
+def phi_data(P, pts):
+    """gs/renderer.py:236-240."""
+    _, z = sample_multi(P, pts)
+    return mlp_forward(P.geom, z)[2][:, 0]
+
+
+def render_weights_data(phi, s):
+    """gs/renderer.py:162-173."""
+    sig = sigmoid_raw(s * phi)
+    ratio = sig[:, 1:] / np.maximum(sig[:, :-1], SIGMA_FLOOR)
+    om = np.concatenate(
+        [np.minimum(ratio, 1.0), np.ones((phi.shape[0], 1), dtype=phi.dtype)], axis=1)
+    trans = np.cumprod(
+        np.concatenate([np.ones((phi.shape[0], 1), dtype=phi.dtype), om[:, :-1]], axis=1),
+        axis=1)
+    return trans * (1.0 - om)
+
+
+def box_exit(origins, dirs, lo, hi):
+    """gs/renderer.py:228-233."""
+    r = np.where(np.abs(dirs) < 1e-12, 1e-12, dirs)
+    t1 = (lo - origins) / r
+    t2 = (hi - origins) / r
+    return np.min(np.maximum(t1, t2), axis=1)
+
+
+def draw_smooth_points(P, dataset, count, truncation, delta, rng):
+    """gs/renderer.py:243-276."""
+    frames, vs, us = dataset.valid_pixels
+    if frames.size == 0:
+        return None
+    pick = rng.integers(0, frames.size, size=count)
+    f, v, u = frames[pick], vs[pick], us[pick]
+    pixels = np.stack([u, v], axis=1).astype(np.float64)
+    intr = dataset.intrinsics
+    d_cam = pixel_rays(intr, pixels)
+    scale = ray_to_z_scale(intr, pixels)
+    depth_ray = dataset.depths[f, v, u] * scale + rng.uniform(-truncation, truncation, size=count)
+    mats = P.pose_matrices()[f]
+    dirs = np.einsum("nij,nj->ni", mats[:, :3, :3], d_cam)
+    x = mats[:, :3, 3] + depth_ray[:, None] * dirs
+    margin = 0.5 * P.finest_voxel
+    x = np.clip(x, P.lo + margin, P.hi - margin)
+    lo, hi = P.lo + margin, P.hi - margin
+    eps_dir = rng.normal(size=(count, 8, 3))
+    eps_dir /= np.linalg.norm(eps_dir, axis=2, keepdims=True)
+    cand = x[:, None, :] + delta * eps_dir
+    ok = ((cand >= lo) & (cand <= hi)).all(axis=2)
+    first = np.argmax(ok, axis=1)
+    xe = cand[np.arange(count), first]
+    xe = np.clip(xe, lo, hi)
+    return x, xe
+
+
+# ---------------------------------------------------------------------------
+# geometry sample pass: phi, grad phi, and its adjoint
+
+
+class GeomPass:
+    """phi and grad-phi at points, with what the backward needs.
+
+    grad phi follows gs/renderer.py:358: the MLP vjp gives g = dphi/dz
+    (ReLU masks a > 0, gs/diffcore.py:483-492) and each level adds
+    J_l^T g_l (gs/diffcore.py:946-991)."""
+
+    def __init__(self, P, pts):
+        dt = P.dtype
+        self.P = P
+        self.ls, self.z = sample_multi(P, pts)
+        (a0, a1, a2), (h0, h1), out = mlp_forward(P.geom, self.z)
+        self.phi = out[:, 0]
+        self.h0, self.h1 = h0, h1
+        self.m0 = (a0 > 0).astype(dt)
+        self.m1 = (a1 > 0).astype(dt)
+        W0, W1, W2 = (P.geom[i][0] for i in range(3))
+        ones = np.ones((self.z.shape[0], 1), dtype=dt)
+        self.d1 = np.matmul(ones, W2.T) * self.m1
+        self.d0 = np.matmul(self.d1, W1.T) * self.m0
+        self.g = np.matmul(self.d0, W0.T)
+        c = P.levels[0].feat.shape[1]
+        gphi = None
+        for l, s in enumerate(self.ls):
+            part = s.dx(self.g[:, l * c:(l + 1) * c])
+            gphi = part if gphi is None else gphi + part
+        self.gphi = gphi
+
+    def backward(self, p, u, grads):
+        """Accumulate d/dtheta of sum_n p_n phi_n + u_n . gradphi_n
+        (SURVEY.md Appendix A)."""
+        P = self.P
+        dt = P.dtype
+        c = P.levels[0].feat.shape[1]
+        W0, W1 = P.geom[0][0], P.geom[1][0]
+        pc = p.astype(dt)[:, None]
+        v = np.zeros_like(self.z)
+        for l, s in enumerate(self.ls):
+            ju = s.ju(u)  # (N,8) f64
+            gl = self.g[:, l * c:(l + 1) * c]
+            coef = s.w8 * p.astype(np.float64)[:, None] + ju
+            grads[f"level{l}"] += scatter_weighted(s.idx8, coef, gl, s.lev.n_vertices)
+            v[:, l * c:(l + 1) * c] = gather_weighted(s.lev.feat, s.idx8, ju)
+        q0 = np.matmul(v, W0) * self.m0
+        dd1 = np.matmul(q0, W1) * self.m1
+        grads["geom_w0"] += np.matmul((pc * self.z + v).T, self.d0)
+        grads["geom_w1"] += np.matmul((pc * self.h0 + q0).T, self.d1)
+        grads["geom_w2"] += (pc * self.h1 + dd1).sum(axis=0)[:, None]
+        grads["geom_b0"] += (pc * self.d0).sum(axis=0)
+        grads["geom_b1"] += (pc * self.d1).sum(axis=0)
+        grads["geom_b2"] += pc.sum(axis=0)
+
+
+# ---------------------------------------------------------------------------
+# the objective (gs/renderer.py:279-468) and its gradient
+
+
+def train_objective(P, dataset, batch, iteration, cfg, smooth_override=None,
+                    want_grads=True, inject_depths=None):
+    """One evaluation of the training objective and (optionally) all
+    parameter gradients.  Returns a dict of every intermediate.
+
+    ``inject_depths`` replaces the sampled depths (M, N) for component
+    parity (the taped pass of another implementation given our samples)."""
+    lw = cfg.weights
+    dt = P.dtype
+    m = len(batch)
+    margin = 0.5 * P.finest_voxel
+    lo_c, hi_c = P.lo + margin, P.hi - margin
+    R = {}
+
+    # ray setup: gs/renderer.py:302-317 (frozen poses, R = R0 @ I exactly)
+    uniq, inv = np.unique(batch.frame_ids, return_inverse=True)
+    R9 = P.poses[uniq, :3, :3].astype(dt).reshape(-1, 9)
+    T3 = P.poses[uniq, :3, 3].astype(dt)
+    r_sel = np.take(R9, inv, axis=0).reshape(m, 3, 3)
+    o = np.take(T3, inv, axis=0)
+    r = np.matmul(r_sel, batch.dir_cam[:, :, None].astype(dt)).reshape(m, 3)
+    o_data, r_data = o.astype(np.float64), r.astype(np.float64)
+    if cfg.fixed_far is not None:
+        far = np.full(m, float(cfg.fixed_far))
+    else:
+        far = np.minimum(box_exit(o_data, r_data, lo_c, hi_c), batch.far)
+    near = batch.near
+    far = np.maximum(far, near + 0.05)
+    R.update(o=o, r=r, far=far)
+
+    # sampling: gs/renderer.py:319-346
+    s_val = float(np.exp(P.log_s))
+    u0 = substream(cfg.seed, STRATIFY, iteration).random((m, cfg.coarse_samples))
+    depths = stratified_coarse(near, far, cfg.coarse_samples, u0)
+    R["depths0"] = depths
+
+    def phi_at(dep_rows, rows):
+        pts = o_data[rows] + dep_rows[:, None] * r_data[rows]
+        pts = np.clip(pts, lo_c, hi_c).astype(dt)
+        return phi_data(P, pts).reshape(-1).astype(np.float64)
+
+    phi_cache = None
+    R["rounds"] = []
+    for rnd in range(cfg.importance_rounds):
+        if phi_cache is None:
+            rows = np.repeat(np.arange(m), depths.shape[1])
+            phi_cache = phi_at(depths.reshape(-1), rows).reshape(m, -1)
+        w = render_weights_data(phi_cache, s_val)
+        ui = substream(cfg.seed, IMPORTANCE, iteration, rnd).random((m, cfg.importance_add))
+        prev_phi = phi_cache
+        depths, src = importance_refine_with_sources(depths, w, near, far, ui)
+        nxt = np.take_along_axis(phi_cache, np.maximum(src, 0), axis=1)
+        need_r, need_c = np.nonzero(src < 0)
+        if need_r.size:
+            nxt[need_r, need_c] = phi_at(depths[need_r, need_c], need_r)
+        phi_cache = nxt
+        R["rounds"].append(dict(phi_in=prev_phi, weights=w, depths=depths, src=src))
+    if inject_depths is not None:
+        depths = np.asarray(inject_depths, dtype=np.float64)
+    n = depths.shape[1]
+    R["depths"] = depths
+
+    # taped pass: gs/renderer.py:348-370
+    x = o.reshape(m, 1, 3) + depths[:, :, None].astype(dt) * r.reshape(m, 1, 3)
+    xf = np.minimum(np.maximum(x.reshape(m * n, 3), lo_c.astype(dt)), hi_c.astype(dt))
+    G = GeomPass(P, xf)
+    cs = LevelSample(P.color, xf)
+    fc = cs.value()
+    vdir = np.broadcast_to(r.reshape(m, 1, 3), (m, n, 3)).reshape(m * n, 3)
+    norms = np.linalg.norm(vdir, axis=-1)
+    if np.any(np.abs(norms - 1.0) > 1e-6):
+        raise ValueError("view directions must be unit length")
+    cin = np.concatenate([fc, vdir], axis=1)
+    (ca0, ca1, ca2), (ch0, ch1), cy = mlp_forward(P.color_net, cin)
+    c_flat = sigmoid_raw(cy)
+
+    phis = G.phi.reshape(m, n)
+    colors = c_flat.reshape(m, n, 3)
+    s_t = np.exp(P.log_s)  # dt 0-d
+    # alphas: gs/renderer.py:112-134
+    sig = sigmoid_raw(phis * s_t)
+    Dden = np.maximum(sig[:, :-1], dt.type(SIGMA_FLOOR))
+    ratio = sig[:, 1:] / Dden
+    head = 1.0 - np.minimum(ratio, 1.0)
+    al = np.concatenate([head, np.zeros((m, 1), dtype=dt)], axis=1)
+    # composite: gs/renderer.py:137-159
+    om = 1.0 - al
+    omc = np.maximum(om, dt.type(TRANS_FLOOR))
+    logt = np.cumsum(np.log(omc), axis=1)
+    trans = np.exp(np.concatenate([np.zeros((m, 1), dtype=dt), logt[:, :n - 1]], axis=1))
+    w = trans * al
+    dconst = depths.astype(dt)
+    chat = (w.reshape(m, n, 1) * colors).sum(axis=1)
+    dhat = (w * dconst).sum(axis=1)
+
+    # losses: gs/renderer.py:372-414
+    err = chat - batch.color.astype(dt)
+    lr_m = np.sqrt((err * err).sum(axis=1) + dt.type(1e-24))
+    l_rgb = lr_m.sum() / dt.type(m)
+    vmask = batch.valid.astype(dt)
+    n_valid = int(batch.valid.sum())
+    d_err = np.abs(dhat - batch.depth_ray.astype(dt))
+    l_d = (d_err * vmask).sum() / dt.type(max(n_valid, 1))
+    b = batch.depth_ray[:, None] - depths
+    tr_mask = (batch.valid[:, None] & (np.abs(b) <= lw.truncation)).astype(dt)
+    fs_mask = (batch.valid[:, None] & (b > lw.truncation)).astype(dt)
+    behind_mask = (batch.valid[:, None] & (b < -lw.truncation)).astype(dt)
+    b_c = b.astype(dt)
+    tr_cnt = tr_mask.sum(axis=1)
+    sdf_val = np.abs(phis - b_c) * tr_mask
+    per_ray_sdf = sdf_val.sum(axis=1) / np.maximum(tr_cnt, 1.0).astype(dt)
+    l_sdf = per_ray_sdf.sum() / dt.type(m)
+    fs_cnt = fs_mask.sum(axis=1)
+    e5 = np.exp(phis * dt.type(-lw.freespace_alpha))
+    inner = np.maximum(dt.type(0.0), e5 - dt.type(1.0))
+    fs_raw = np.maximum(inner, phis - b_c)
+    per_ray_fs = (fs_raw * fs_mask).sum(axis=1) / np.maximum(fs_cnt, 1.0).astype(dt)
+    l_fs = per_ray_fs.sum() / dt.type(m)
+    eik_mask = (fs_mask + behind_mask + (~batch.valid[:, None]).astype(dt)).clip(0, 1)
+    eik_flat = eik_mask.reshape(-1)
+    n_eik = float(max(eik_flat.sum(), 1.0))
+    gp = G.gphi
+    nrm = np.sqrt((gp * gp).sum(axis=-1) + dt.type(1e-20))
+    diff = 1.0 - nrm
+    eik_val = diff * diff
+    l_eik = (eik_val * eik_flat.astype(dt)).sum() / dt.type(n_eik)
+
+    # smoothness: gs/renderer.py:416-434
+    if smooth_override is not None:
+        smooth_pts = smooth_override
+    else:
+        rng = substream(cfg.seed, SMOOTH, iteration)
+        smooth_pts = draw_smooth_points(P, dataset, lw.smooth_count, lw.truncation,
+                                        lw.smooth_delta, rng)
+    S = None
+    if smooth_pts is None or lw.smooth == 0.0:
+        l_smooth = dt.type(0.0)
+        n_smooth = 0
+    else:
+        xs, xe = smooth_pts
+        n_smooth = xs.shape[0]
+        S = GeomPass(P, np.concatenate([xs, xe], axis=0).astype(dt))
+        dS = S.gphi[:n_smooth] - S.gphi[n_smooth:]
+        l_smooth = (dS * dS).sum() / dt.type(n_smooth)
+    R["smooth_pts"] = smooth_pts
+
+    total = (l_rgb * dt.type(lw.rgb) + l_d * dt.type(lw.depth) + l_sdf * dt.type(lw.sdf)
+             + l_fs * dt.type(lw.fs) + l_eik * dt.type(lw.eik) + l_smooth * dt.type(lw.smooth))
+    R["parts"] = {"total": float(total), "rgb": float(l_rgb), "depth": float(l_d),
+                  "sdf": float(l_sdf), "fs": float(l_fs), "eik": float(l_eik),
+                  "smooth": float(l_smooth), "s": s_val}
+    R["extras"] = {"samples_per_ray": n, "n_valid_rays": n_valid,
+                   "n_tr": int(tr_cnt.sum()), "n_fs": int(fs_cnt.sum()),
+                   "n_eik": int(eik_flat.sum()), "n_smooth": n_smooth,
+                   "empty_tr": bool(tr_cnt.sum() == 0), "empty_fs": bool(fs_cnt.sum() == 0)}
+    R.update(phi=phis, gphi=gp.reshape(m, n, 3), colors=colors, alpha=al, weights=w,
+             chat=chat, dhat=dhat, xf=xf)
+    if not want_grads:
+        return R
+
+    # ---------------- backward ----------------
+    grads = {name: np.zeros_like(a) for name, a in zip(P.names(), P.arrays())}
+    M = dt.type(m)
+    # photometric + depth seeds
+    chat_bar = (dt.type(lw.rgb) / M) * err / lr_m[:, None]
+    dhat_bar = dt.type(lw.depth) * vmask * np.sign(dhat - batch.depth_ray.astype(dt)) \
+        / dt.type(max(n_valid, 1))
+    w_bar = (chat_bar[:, None, :] * colors).sum(axis=2) + dhat_bar[:, None] * dconst
+    c_bar = w[:, :, None] * chat_bar[:, None, :]
+    T_bar = w_bar * al
+    al_bar = w_bar * trans
+    tt = T_bar * trans  # d/d logt_{i-1}
+    L_bar = np.zeros_like(al)
+    # L_bar_j = sum_{i=j+1}^{n-1} T_bar_i T_i (reverse exclusive scan)
+    L_bar[:, :n - 1] = np.flip(np.cumsum(np.flip(tt[:, 1:], axis=1), axis=1), axis=1)
+    om_bar = np.where(om >= dt.type(TRANS_FLOOR), L_bar / omc, 0.0).astype(dt)
+    al_bar = al_bar - om_bar
+    r_bar = np.where(ratio <= 1.0, -al_bar[:, :n - 1], 0.0).astype(dt)
+    sig_bar = np.zeros_like(sig)
+    sig_bar[:, 1:] += r_bar / Dden
+    D_bar = -(r_bar * sig[:, 1:]) / (Dden * Dden)
+    sig_bar[:, :-1] += np.where(sig[:, :-1] >= dt.type(SIGMA_FLOOR), D_bar, 0.0).astype(dt)
+    z_bar = sig_bar * (sig * (1.0 - sig))
+    phi_bar = z_bar * s_t
+    grads["log_s"] += np.asarray((z_bar * phis).sum() * s_t, dtype=dt)
+    # direct phi terms
+    phi_bar += (dt.type(lw.sdf) / M) * tr_mask * np.sign(phis - b_c) \
+        / np.maximum(tr_cnt, 1.0).astype(dt)[:, None]
+    dfs = np.where(inner >= phis - b_c,
+                   np.where(e5 - dt.type(1.0) > 0, e5 * dt.type(-lw.freespace_alpha), 0.0),
+                   1.0).astype(dt)
+    phi_bar += (dt.type(lw.fs) / M) * fs_mask * dfs / np.maximum(fs_cnt, 1.0).astype(dt)[:, None]
+    # eikonal
+    u = (dt.type(-2.0 * lw.eik) / dt.type(n_eik)) * (eik_flat * diff / nrm)[:, None] * gp
+    G.backward(phi_bar.reshape(-1), u.astype(dt), grads)
+    if S is not None:
+        us = np.concatenate([dS, -dS], axis=0) * (dt.type(2.0 * lw.smooth) / dt.type(n_smooth))
+        S.backward(np.zeros(2 * n_smooth, dtype=dt), us.astype(dt), grads)
+    # colour: sigma(MLP_c([fc, r])) backprop
+    cb = c_bar.reshape(m * n, 3)
+    y_bar = cb * (c_flat * (1.0 - c_flat))
+    cW = [P.color_net[i][0] for i in range(3)]
+    grads["color_w2"] += np.matmul(ch1.T, y_bar)
+    grads["color_b2"] += y_bar.sum(axis=0)
+    a1b = np.matmul(y_bar, cW[2].T) * (ca1 > 0)
+    grads["color_w1"] += np.matmul(ch0.T, a1b)
+    grads["color_b1"] += a1b.sum(axis=0)
+    a0b = np.matmul(a1b, cW[1].T) * (ca0 > 0)
+    grads["color_w0"] += np.matmul(cin.T, a0b)
+    grads["color_b0"] += a0b.sum(axis=0)
+    fc_bar = np.matmul(a0b, cW[0].T)[:, :fc.shape[1]]
+    grads["colorgrid"] += scatter_weighted(cs.idx8, cs.w8, fc_bar.astype(dt), P.color.n_vertices)
+    R["grads"] = grads
+    R["adjoints"] = dict(phi_bar=phi_bar, u=u.reshape(m, n, 3), c_bar=c_bar)
+    return R
+
+
+# ---------------------------------------------------------------------------
+# Adam (gs/optimizer.py:38-91)
+
+
+class Adam:
+    """gs/optimizer.py:58-91: per-tensor step counts, f64 math, dt storage,
+    non-finite gradient entries zeroed and counted."""
+
+    def __init__(self, arrays, lrs, beta1=0.9, beta2=0.999, eps=1e-8):
+        self.lrs = list(lrs)
+        self.beta1, self.beta2, self.eps = beta1, beta2, eps
+        self.m = [np.zeros_like(a) for a in arrays]
+        self.v = [np.zeros_like(a) for a in arrays]
+        self.t = [0] * len(arrays)
+        self.skipped = 0
+
+    def step(self, arrays, grads):
+        b1, b2, eps = self.beta1, self.beta2, self.eps
+        for i, (p, g) in enumerate(zip(arrays, grads)):
+            self.t[i] += 1
+            t = float(self.t[i])
+            c1 = 1.0 - b1 ** t
+            c2 = 1.0 - b2 ** t
+            g64 = np.asarray(g, dtype=p.dtype).astype(np.float64).reshape(p.shape)
+            bad = ~np.isfinite(g64)
+            if bad.any():
+                self.skipped += int(bad.sum())
+                g64 = np.where(bad, 0.0, g64)
+            mi = b1 * self.m[i].astype(np.float64) + (1.0 - b1) * g64
+            vi = b2 * self.v[i].astype(np.float64) + (1.0 - b2) * g64 * g64
+            self.m[i][...] = mi
+            self.v[i][...] = vi
+            p[...] = p.astype(np.float64) - self.lrs[i] * (mi / c1) / (np.sqrt(vi / c2) + eps)
+
+
+def train_step(P, opt, dataset, cfg, iteration):
+    """gs/optimizer.py:363-373: one full iteration (draw, objective, grad, Adam)."""
+    batch = draw_ray_batch(dataset, substream(cfg.seed, RAYS, iteration), cfg.batch_rays,
+                           near=cfg.near, far=cfg.max_depth)
+    R = train_objective(P, dataset, batch, iteration, cfg)
+    names = P.names()
+    opt.step(P.arrays(), [R["grads"][n] for n in names])
+    return R
