@@ -1,0 +1,371 @@
+"""Benchmark: GO-Surf training iterations (forward + backward + Adam) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl {b200,reference}]
+
+Workload (BASELINE.json configs[1]): ScanNet-shaped synthetic RGB-D sequence
+(640x480, ScanNet intrinsics), the paper's 4-level grid (0.96/0.24/0.06/0.03 m,
+colour 0.03 m) over the pinned 7 x 7 x 3.25 m box (P = 63.9 M parameters),
+M = 6144 rays per GPU, 96 + 3x12 = 132 samples per ray, smoothness on,
+float32.  A step = one full training iteration: device ray draw +
+stratified + 3 importance rounds, taped forward, rendering, six losses,
+fused backward with grid scatter, dense Adam over all parameters.
+
+value: rays/s with the step inputs already resident in HBM (device-timed).
+e2e:   rays/s through the public API (host numpy draws each step, pinned
+       H2D of ray ids + smoothness points, D2H of the loss parts).
+Multi-GPU (torchrun): weak scaling, 6144 rays per rank from one global batch,
+NCCL all-reduce of the partition counts and of the gradient arena.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "training rays/sec (fwd+bwd+Adam) at 1/2/4/8 B200; % HBM roofline; vs CPU ref"
+M_PER_GPU = 6144
+FRAMES = 8
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d.get("hbm_gbs", 6650.0)), "measured"
+    return 6650.0, "fallback"
+
+
+def make_cfg(precision="single", batch=M_PER_GPU, seed=0):
+    from paper_2206_14735_b200 import optimizer, scenes
+    return optimizer.TrainConfig(precision=precision, batch_rays=batch, seed=seed,
+                                 bounds=scenes.CONFIG2_BOUNDS, iterations=10 ** 6)
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+
+    def __init__(self):
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def start(self):
+        def run():
+            q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap")
+            while not self._stop.is_set():
+                try:
+                    out = subprocess.run(["nvidia-smi", "-i", os.environ.get("LOCAL_RANK", "0"),
+                                          f"--query-gpu={q}", "--format=csv,noheader,nounits"],
+                                         capture_output=True, text=True, timeout=5).stdout
+                    self.samples.append([x.strip() for x in out.strip().split(",")])
+                except Exception:
+                    pass
+                self._stop.wait(0.2)
+        self._t = threading.Thread(target=run, daemon=True)
+        self._t.start()
+
+    def stop(self):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=6)
+        sm = [float(s[0]) for s in self.samples if len(s) >= 6 and s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if len(s) >= 6 and s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples if len(s) >= 6
+                          for i in range(4) if s[2 + i].lower().startswith("active")})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def b_alg_bytes(model, M, N, S):
+    """Algorithmic HBM bytes of one step."""
+    P = sum(p.size for p in model.parameters())
+    G_s = sum(8 * l.width * 4 for l in model.grid.levels
+              if l.features.size * 4 > 32 * 2 ** 20)
+    Cc_s = 8 * 6 * 4 if model.grid.color.features.size * 4 > 32 * 2 ** 20 else 0
+    n_imp = 96 + 2 * 12
+    return 32 * P + M * (n_imp * G_s + N * 2 * (G_s + Cc_s)) + 2 * S * 2 * G_s, P
+
+
+# ----------------------------------------------------------------------------
+# reference arm: the CPU oracle port of the reference step
+
+
+def cpu_step_sample(steps, warmup, m_sample, threads):
+    """Time the oracle's step (gs/optimizer.py:363-373 restated in numpy) on
+    the same workload with a bounded ray sample."""
+    os.environ.setdefault("OMP_NUM_THREADS", str(threads))
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from oracle import gridsurf_oracle as O
+    from _golden import OracleDataset, cfg_ns
+    from paper_2206_14735_b200 import scenes
+    ds = scenes.config2(frames=2, threads=threads)
+    ods = OracleDataset(ds.colors_u8, ds.depths_mm, ds.poses, ds.intrinsics)
+    cfg = cfg_ns(precision="single", batch_rays=m_sample, bounds=scenes.CONFIG2_BOUNDS)
+    P = O.create_params(*cfg.bounds, ds.poses, seed=0, dtype=np.float32)
+    opt = O.Adam(P.arrays(), P.lrs())
+    times = []
+    for it in range(warmup + steps):
+        t0 = time.perf_counter()
+        O.train_step(P, opt, ods, cfg, it)
+        dt = time.perf_counter() - t0
+        if it >= warmup:
+            times.append(dt)
+    return float(np.median(times)), P
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    threads = os.cpu_count() or 1
+    m_sample = 512
+    t, P = cpu_step_sample(max(args.steps, 1), 0 if args.steps <= 1 else 1, m_sample, threads)
+    v = m_sample / t
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "rays/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": "config2 ScanNet-shaped 640x480, 4-level grid, pinned "
+                                   "7x7x3.25 m box, 132 samples/ray", "sample_rays": m_sample},
+            "cpu_baseline": {"value": v, "unit": "rays/s", "cores": threads, "kind": "port",
+                             "sample": f"{m_sample} rays of the config2 batch + dense Adam over "
+                                       f"all {sum(a.size for a in P.arrays())} parameters, "
+                                       "median step"},
+            "e2e": {"value": v, "unit": "rays/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------
+# B200 arm
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--precision", default="single")
+    ap.add_argument("--frames", type=int, default=FRAMES)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--rays", type=int, default=M_PER_GPU)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    from paper_2206_14735_b200 import _lib, engine, optimizer, scenes
+    from paper_2206_14735_b200.renderer import engine_for
+
+    ws_, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    pg = None
+    if ws_ > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+        pg = dist
+    W = max(args.warmup, 3)
+    K = args.steps
+    M = args.rays
+    cfg = make_cfg(args.precision, batch=M * ws_)
+    ds = scenes.config2(frames=args.frames, threads=min(8, os.cpu_count() or 1))
+    model = optimizer.build_model(ds, cfg, skip_init=True, device=dev)
+    opt = optimizer.make_optimizer(model, cfg)
+    eng = engine_for(model, ds)
+    N = cfg.coarse_samples + cfg.importance_rounds * cfg.importance_add
+
+    def draws_for(it):
+        d = engine.host_draws(model, ds, cfg, it)
+        # this rank's slice of the global batch; smoothness on rank 0
+        d.ray_ids = d.ray_ids[rank * M:(rank + 1) * M].copy()
+        if rank != 0:
+            d.smooth = None
+        return d
+
+    S = cfg.weights.smooth_count
+
+    def one_step(d, ids, sm, stream=None):
+        kw = dict(ray_base=rank * M, m_global=M * ws_, smooth_global=S)
+        if pg is None:
+            w = eng.launch(cfg, d, ids, sm, **kw)
+        else:
+            w = eng.launch(cfg, d, ids, sm, phases=1, **kw)
+            pg.all_reduce(w["counts"])
+            eng.model.arena.zero_grads()
+            st = eng.step_struct(cfg, d, ids, sm, w, phases=2, **kw)
+            import ctypes as C
+            _lib.check(eng.lib.gsb_train_step(C.byref(eng.mstruct), C.byref(eng.dstruct),
+                                              C.byref(st), _lib.stream_handle()), "step")
+            pg.all_reduce(model.arena.grads)
+            pg.all_reduce(w["parts"])
+        opt.t = [t + 1 for t in opt.t]
+        opt._launch()
+        return w
+
+    # ---- device-resident inputs for warmup + timed steps
+    pre = []
+    for it in range(W + K):
+        d = draws_for(it)
+        ids, sm = eng.upload(d)
+        pre.append((d, ids, sm))
+    torch.cuda.synchronize()
+    for it in range(W):
+        one_step(*pre[it])
+    torch.cuda.synchronize()
+
+    # adam-only and step-only event timing (same stream) for the roofline
+    e = [torch.cuda.Event(enable_timing=True) for _ in range(2 * K + 2)]
+    clocks = Clocks()
+    clocks.start()
+    if pg:
+        pg.barrier()
+    torch.cuda.synchronize()
+    t_step, t_adam = [], []
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    for k in range(K):
+        d, ids, sm = pre[W + k]
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        c = torch.cuda.Event(enable_timing=True)
+        a.record()
+        kw = dict(ray_base=rank * M, m_global=M * ws_, smooth_global=S)
+        if pg is None:
+            eng.launch(cfg, d, ids, sm, **kw)
+        else:
+            w = eng.launch(cfg, d, ids, sm, phases=1, **kw)
+            pg.all_reduce(w["counts"])
+            eng.model.arena.zero_grads()
+            import ctypes as C
+            st = eng.step_struct(cfg, d, ids, sm, w, phases=2, **kw)
+            _lib.check(eng.lib.gsb_train_step(C.byref(eng.mstruct), C.byref(eng.dstruct),
+                                              C.byref(st), _lib.stream_handle()), "step")
+            pg.all_reduce(model.arena.grads)
+        b.record()
+        opt.t = [t + 1 for t in opt.t]
+        opt._launch()
+        c.record()
+        t_step.append((a, b))
+        t_adam.append((b, c))
+    ev1.record()
+    torch.cuda.synchronize()
+    if pg:
+        pg.barrier()
+    clk = clocks.stop()
+    total_ms = ev0.elapsed_time(ev1)
+    if pg:
+        tt = torch.tensor([total_ms], device=dev)
+        pg.all_reduce(tt, op=pg.ReduceOp.MAX)
+        total_ms = float(tt.item())
+    ms_step = total_ms / K
+    adam_ms = float(np.mean([x.elapsed_time(y) for x, y in t_adam]))
+    obj_ms = float(np.mean([x.elapsed_time(y) for x, y in t_step]))
+    value = M * ws_ * K / (total_ms / 1e3)
+
+    # ---- e2e through the public API (host draws + H2D + D2H of parts)
+    T = optimizer.Trainer(model, ds, cfg, opt)
+    torch.cuda.synchronize()
+    if pg:
+        pg.barrier()
+    t0 = time.perf_counter()
+    pending = None
+    base_it = W + K
+    h2d = 0
+    for k in range(K):
+        it = base_it + k
+        d = draws_for(it)
+        h2d = d.ray_ids.nbytes + (0 if d.smooth is None else d.smooth.nbytes)
+        ids, sm = eng.upload(d)
+        if pg is None:
+            T.launch(it, draws=d, slot=k % 2)
+        else:
+            one_step(d, ids, sm)
+            T.host_parts[k % 2].copy_(eng.workspace(M, 96, 3, 12, S if rank == 0 else 0)["parts"],
+                                      non_blocking=True)
+            T.events[k % 2].record()
+        if pending is not None:
+            T.parts(pending)
+        pending = k % 2
+    if pending is not None:
+        T.parts(pending)
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - t0
+    if pg:
+        tt = torch.tensor([e2e_s], device=dev)
+        pg.all_reduce(tt, op=pg.ReduceOp.MAX)
+        e2e_s = float(tt.item())
+    e2e = M * ws_ * K / e2e_s
+
+    if rank != 0:
+        if pg:
+            pg.destroy_process_group()
+        return 0
+
+    # ---- roofline: dominant kernel share (Adam: HBM streaming, 32 B/param)
+    peak, peak_kind = peaks()
+    B, P = b_alg_bytes(model, M, N, S)
+    adam_bytes = 32 * P
+    roofline = {"bound": "hbm", "kernel": "k_adam (dense Adam over the arena)",
+                "achieved": adam_bytes / (adam_ms / 1e3) / 1e9, "peak": peak, "unit": "GB/s",
+                "frac": adam_bytes / (adam_ms / 1e3) / 1e9 / peak, "traffic": None,
+                "peak_kind": peak_kind,
+                "step_b_alg_gb": B / 1e9,
+                "step_frac": B / (ms_step / 1e3) / 1e9 / peak,
+                "adam_ms": adam_ms, "objective_ms": obj_ms}
+    cpu = None
+    if not args.no_cpu_baseline and ws_ == 1:
+        threads = os.cpu_count() or 1
+        m_sample = 256
+        t, _ = cpu_step_sample(1, 0, m_sample, threads)
+        cpu = {"value": m_sample / t, "unit": "rays/s", "cores": threads, "kind": "port",
+               "sample": f"one oracle step, {m_sample} rays of the config2 workload + dense "
+                         f"Adam over all {P} parameters"}
+    line = {"metric": METRIC, "value": value, "unit": "rays/s", "n_gpus": ws_, "steps": K,
+            "warmup": W, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32" if args.precision == "single" else "f64",
+            "data": "synthetic",
+            "config": {"workload": "config2: ScanNet-shaped 640x480 RGB-D, paper 4-level grid "
+                                   "(0.96/0.24/0.06/0.03 m + 0.03 m colour), pinned 7x7x3.25 m "
+                                   "box, 96+3x12 samples/ray, smoothness on",
+                       "rays_per_gpu": M, "samples_per_ray": N, "params": P,
+                       "frames": args.frames, "l2": "working set (4 arenas x 256 MB) > L2; "
+                                                   "no explicit flush"},
+            "samples_per_s": value * N,
+            "e2e": {"value": e2e, "unit": "rays/s", "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": 8 * 8},
+            "gpu_launches": None,
+            "roofline": roofline, "cpu_baseline": cpu, "clocks": clk}
+    print(json.dumps(line), flush=True)
+    if pg:
+        pg.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,203 @@
+/*
+ * gsb.h -- C ABI of the B200 GO-Surf training-step kernels.
+ *
+ * The reference (gridsurf, /root/reference/pkg/src/gridsurf) is pure Python
+ * + numba; its native boundary is the set of numba kernels and the Python
+ * step body (gs/optimizer.py:363-373).  This ABI replaces that boundary:
+ *
+ *   gsb_train_step  <- renderer.train_objective + dc.grad      (gs/renderer.py:279-468,
+ *                                                               gs/diffcore.py:1035-1104)
+ *   gsb_adam_step   <- optimizer.Adam.step / _adam_kernel       (gs/optimizer.py:38-91)
+ *   unit twins of the numba kernels, used by the parity tests:
+ *   gsb_gather_weighted   <- diffcore._nb_gather_weighted       (gs/diffcore.py:816-827)
+ *   gsb_scatter_weighted  <- diffcore._nb_scatter_weighted      (gs/diffcore.py:830-841)
+ *   gsb_grid_sample       <- diffcore.grid_sample (forward)     (gs/diffcore.py:893-920)
+ *   gsb_importance_round  <- render_weights_data + importance_refine_with_sources
+ *                            (gs/renderer.py:162-173, gs/sampler.py:128-197)
+ *   gsb_ray_batch         <- sampler.draw_ray_batch (given drawn ids) (gs/sampler.py:58-88)
+ *   gsb_pcg64_random      <- numpy Generator(PCG64).random       (gs/seeds.py:28-30)
+ *
+ * Conventions: every pointer is a DEVICE pointer unless named *_host; the
+ * caller owns all memory (kernels never allocate); every launch is
+ * asynchronous on `stream` (a cudaStream_t passed as void*); functions return
+ * GSB_OK or a negative status.  Data-dependent errors (a point outside the
+ * grid, non-finite values, list overflow) are written to the status words in
+ * the step workspace and surface at the caller's next synchronisation.
+ */
+#ifndef GSB_H
+#define GSB_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GSB_OK 0
+#define GSB_E_ARG (-1)      /* bad argument / unsupported configuration */
+#define GSB_E_CUDA (-2)     /* a CUDA runtime call failed */
+#define GSB_E_BOUNDS (-3)   /* GridBoundsError (gs/diffcore.py:738-751) */
+#define GSB_E_NONFINITE (-4)
+
+#define GSB_MAX_LEVELS 8
+#define GSB_MAX_ROUNDS 8
+#define GSB_KMAX 256        /* max samples per ray */
+#define GSB_AMAX 32         /* max importance samples added per round */
+
+/* status word indices in the step workspace (int32) */
+#define GSB_ST_BOUNDS 0
+#define GSB_ST_NONFINITE 1
+#define GSB_ST_OVERFLOW 2
+#define GSB_ST_VIEWDIR 3
+#define GSB_ST_ADAM_BAD 4
+#define GSB_ST_DIVERGED 5
+#define GSB_N_STATUS 8
+
+/* loss-part slots (double) written by gsb_train_step */
+#define GSB_P_TOTAL 0
+#define GSB_P_RGB 1
+#define GSB_P_DEPTH 2
+#define GSB_P_SDF 3
+#define GSB_P_FS 4
+#define GSB_P_EIK 5
+#define GSB_P_SMOOTH 6
+#define GSB_P_S 7
+#define GSB_N_PARTS 8
+
+/* count slots (int64) */
+#define GSB_C_VALID 0
+#define GSB_C_TR 1
+#define GSB_C_FS 2
+#define GSB_C_EIK 3
+#define GSB_N_COUNTS 4
+
+/* One dense vertex lattice (diffcore.GridGeom, gs/diffcore.py:704-728) plus
+ * where its features live in the parameter arena. */
+typedef struct {
+  int32_t nx, ny, nz;   /* vertex counts */
+  int32_t channels;     /* feature width C */
+  double ox, oy, oz;    /* world position of vertex (0,0,0) */
+  double voxel;         /* isotropic edge length */
+  int64_t offset;       /* element offset of the (V, C) block in the arena */
+} gsb_level_t;
+
+/* The model: grids coarse->fine + colour grid, MLP block, log_s
+ * (renderer.ModelState, gs/renderer.py:69-105). */
+typedef struct {
+  int32_t precision;    /* 0: float32 storage/compute, 1: float64 */
+  int32_t n_levels;     /* geometry levels */
+  gsb_level_t levels[GSB_MAX_LEVELS];
+  gsb_level_t color;
+  int64_t mlp_offset;   /* geom W0,b0,W1,b1,W2,b2 then colour W0..b2, contiguous */
+  int64_t log_s_offset;
+  int64_t n_params;     /* arena length in elements */
+  double lo_c[3], hi_c[3]; /* box shrunk by half the finest voxel (gs/renderer.py:299-300) */
+  void* params;         /* arena (T*) */
+  void* grads;          /* gradient arena, same layout (T*) */
+} gsb_model_t;
+
+/* Device-resident RGB-D dataset: colours u8 (F,H,W,3) = round(255 c),
+ * depths u16 (F,H,W) millimetres = round(1000 z) (gs/scenegen.py:319-320). */
+typedef struct {
+  const uint8_t* colors;
+  const uint16_t* depth_mm;
+  int32_t n_frames, height, width;
+  double fx, fy, cx, cy;
+  const double* poses;  /* (F, 12): R row-major then t, values already rounded to
+                           the model dtype (PoseParam stores them in dtype) */
+} gsb_dataset_t;
+
+typedef struct {
+  uint64_t state_hi, state_lo, inc_hi, inc_lo;  /* numpy PCG64 bit_generator state */
+} gsb_pcg64_t;
+
+typedef struct {
+  /* batch (sampler.draw_ray_batch): drawn flat ids into F*H*W */
+  const int64_t* ray_ids;
+  int32_t n_rays;            /* rays on this rank */
+  int32_t ray_base;          /* global row of this rank's first ray (RNG offset) */
+  double m_global;           /* global batch size M (loss normaliser) */
+  /* sampling (TrainConfig) */
+  int32_t n_coarse, n_rounds, n_add;
+  int32_t has_fixed_far;
+  double near, max_depth, fixed_far;
+  gsb_pcg64_t rng_stratify;
+  gsb_pcg64_t rng_importance[GSB_MAX_ROUNDS];
+  /* LossWeights (gs/renderer.py:46-66) */
+  double w_rgb, w_depth, w_sdf, w_fs, w_eik, w_smooth;
+  double truncation, fs_alpha;
+  /* smoothness points (x then x+eps), (2*n_smooth, 3) model dtype */
+  const void* smooth_pts;
+  int32_t n_smooth;          /* pairs on this rank */
+  double smooth_global;      /* global pair count (normaliser) */
+  /* behaviour */
+  int32_t exact_gather;      /* 1: reproduce numba's per-corner rounding (slower) */
+  int32_t phases;            /* bit0: sampling+counts, bit1: objective+backward+finalize */
+  /* workspace (see gsb_step_workspace_size) */
+  void* workspace;
+  size_t workspace_bytes;
+} gsb_step_t;
+
+int gsb_version(void);
+
+/* Bytes of device workspace gsb_train_step needs. */
+int gsb_step_workspace_size(const gsb_model_t* model, int32_t n_rays, int32_t n_coarse,
+                            int32_t n_rounds, int32_t n_add, int32_t n_smooth,
+                            size_t* bytes);
+
+/* Offsets (bytes) of the externally visible workspace regions:
+ * parts (double[GSB_N_PARTS]), counts (int64[GSB_N_COUNTS]), status
+ * (int32[GSB_N_STATUS]), final depths (double, [n_rays][ld]), weights (model
+ * dtype, [n_rays][ld]), ld. */
+int gsb_step_workspace_layout(const gsb_model_t* model, int32_t n_rays, int32_t n_coarse,
+                              int32_t n_rounds, int32_t n_add, int32_t n_smooth,
+                              int64_t* parts_off, int64_t* counts_off, int64_t* status_off,
+                              int64_t* depths_off, int64_t* weights_off, int32_t* ld);
+
+/* One training objective + full backward; gradients are ACCUMULATED into
+ * model->grads (gsb_adam_step leaves them zeroed). */
+int gsb_train_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step_t* step,
+                   void* stream);
+
+/* Dense Adam over the whole arena (gs/optimizer.py:38-55): per segment
+ * learning rate; float64 register math; grads zeroed afterwards.  If
+ * `guard` is non-null and guard[0] (total loss) is non-finite or
+ * > guard_threshold, the update is skipped and status[GSB_ST_DIVERGED] set. */
+int gsb_adam_step(int32_t precision, void* params, void* grads, void* m, void* v,
+                  int64_t n, const int64_t* seg_begin_host, const double* seg_lr_host,
+                  int32_t n_seg, double beta1, double beta2, double eps, double c1, double c2,
+                  const double* guard, double guard_threshold, int32_t* status, void* stream);
+
+/* ---------------- unit twins (parity tests) ---------------- */
+
+int gsb_pcg64_random(const gsb_pcg64_t* rng, int64_t offset, int64_t n, double* out,
+                     void* stream);
+
+/* out (n, 12) f64: frame, u, v, r, g, b, depth_ray, valid, dir x, y, z, scale */
+int gsb_ray_batch(const gsb_dataset_t* data, const int64_t* ray_ids, int32_t n, double* out,
+                  void* stream);
+
+int gsb_gather_weighted(int32_t precision, const void* feat, int32_t channels,
+                        const int64_t* idx8, const double* w8, int64_t n, void* out,
+                        void* stream);
+
+int gsb_scatter_weighted(int32_t precision, const int64_t* idx8, const double* w8,
+                         const void* g, int32_t channels, int64_t n, void* out, void* stream);
+
+/* points (n,3) model dtype -> features (n,C); exact locate + numba rounding */
+int gsb_grid_sample(int32_t precision, const gsb_level_t* level, const void* feat,
+                    const void* points, int64_t n, void* out, int32_t* status, void* stream);
+
+/* One importance round for n rays with K current samples (row stride ld):
+ * weights from phi (render_weights_data), inverse-CDF draws from `uniforms`
+ * (n, A) or, if null, from `rng`, stable merge, separation, provenance. */
+int gsb_importance_round(int32_t n, int32_t K, int32_t A, int32_t ld, const double* depths,
+                         const double* phi, double s, const double* near, const double* far,
+                         const double* uniforms, const gsb_pcg64_t* rng, double* depths_out,
+                         int32_t* src_out, double* weights_out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GSB_H */

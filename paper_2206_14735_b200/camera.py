@@ -1,0 +1,132 @@
+"""Pinhole camera and (frozen) poses, host side (gs/camera.py).
+
+Conventions as the reference: camera looks down +z, image origin top-left,
+camera-to-world matrices, depth images store z-depth.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+
+@dataclass(frozen=True)
+class Intrinsics:
+    """gs/camera.py:37-50."""
+
+    fx: float
+    fy: float
+    cx: float
+    cy: float
+    width: int
+    height: int
+
+    def __post_init__(self):
+        if self.fx <= 0 or self.fy <= 0:
+            raise ValueError("focal lengths must be positive")
+        if not (0 <= self.cx <= self.width and 0 <= self.cy <= self.height):
+            raise ValueError("principal point must lie inside the image")
+
+
+_SMALL_ANGLE = 1e-4
+
+
+def exp_so3_data(nu):
+    """gs/camera.py:125-139."""
+    nu = np.asarray(nu, dtype=np.float64)
+    th2 = float(nu @ nu)
+    K = np.array([[0.0, -nu[2], nu[1]], [nu[2], 0.0, -nu[0]], [-nu[1], nu[0], 0.0]])
+    if np.sqrt(th2) < _SMALL_ANGLE:
+        a = 1.0 - th2 / 6.0 + th2 * th2 / 120.0
+        b = 0.5 - th2 / 24.0 + th2 * th2 / 720.0
+    else:
+        th = np.sqrt(th2)
+        a = np.sin(th) / th
+        b = (1.0 - np.cos(th)) / th2
+    return np.eye(3) + a * K + b * (K @ K)
+
+
+class PoseParam:
+    """Camera-to-world pose R = R0 exp(nu^), t (gs/camera.py:53-90).
+
+    Pose refinement (trainable poses) is not part of the B200 step yet
+    (SURVEY.md 8f #3); poses are frozen constants stored in the model dtype
+    exactly as the reference stores non-trainable poses."""
+
+    def __init__(self, R0, t, trainable=False, dtype=np.float64):
+        if trainable:
+            raise NotImplementedError("pose refinement is not implemented on the B200 path")
+        self.R0 = np.asarray(R0, dtype=np.float64).copy()
+        self.nu = np.zeros(3, dtype=dtype)
+        self.t = np.asarray(t, dtype=dtype).copy()
+        self.trainable = False
+
+    @classmethod
+    def from_matrix(cls, c2w, trainable=False, dtype=np.float64):
+        c2w = np.asarray(c2w, dtype=np.float64)
+        return cls(c2w[:3, :3], c2w[:3, 3], trainable=trainable, dtype=dtype)
+
+    def rotation_data(self):
+        return self.R0 @ exp_so3_data(self.nu)
+
+    def matrix(self):
+        """gs/camera.py:75-80."""
+        m = np.eye(4)
+        m[:3, :3] = self.rotation_data()
+        m[:3, 3] = np.asarray(self.t, dtype=np.float64)
+        return m
+
+    def refresh(self):
+        return None
+
+    def parameters(self):
+        return []
+
+
+def pixel_rays(intr, pixels, dtype=np.float64):
+    """Unit camera-space directions through pixel (u, v) (gs/camera.py:142-157)."""
+    px = np.atleast_2d(np.asarray(pixels, dtype=np.float64))
+    if np.any(px[:, 0] < 0) or np.any(px[:, 0] >= intr.width) or np.any(
+            px[:, 1] < 0) or np.any(px[:, 1] >= intr.height):
+        raise ValueError("pixel outside image bounds")
+    d = np.stack([(px[:, 0] - intr.cx) / intr.fx, (px[:, 1] - intr.cy) / intr.fy,
+                  np.ones(px.shape[0])], axis=1)
+    return (d / np.linalg.norm(d, axis=1, keepdims=True)).astype(dtype)
+
+
+def ray_to_z_scale(intr, pixels):
+    """gs/camera.py:160-171."""
+    px = np.atleast_2d(np.asarray(pixels, dtype=np.float64))
+    d = np.stack([(px[:, 0] - intr.cx) / intr.fx, (px[:, 1] - intr.cy) / intr.fy,
+                  np.ones(px.shape[0])], axis=1)
+    return np.linalg.norm(d, axis=1)
+
+
+def load_poses(path):
+    """gs/camera.py:251-262."""
+    vals = np.atleast_2d(np.loadtxt(path, dtype=np.float64))
+    if vals.shape[1] != 16:
+        raise ValueError(f"pose file {path}: expected 16 numbers per line, got {vals.shape[1]}")
+    poses = vals.reshape(-1, 4, 4)
+    for i, p in enumerate(poses):
+        if not np.allclose(p[3], [0, 0, 0, 1], atol=1e-6):
+            raise ValueError(f"pose {i} in {path} has a malformed last row")
+    return poses
+
+
+def save_poses(path, poses):
+    np.savetxt(path, np.asarray(poses, dtype=np.float64).reshape(-1, 16), fmt="%.17g")
+
+
+def load_intrinsics(path):
+    vals = np.loadtxt(path, dtype=np.float64).ravel()
+    if vals.size != 6:
+        raise ValueError(f"intrinsics file {path}: expected 6 values")
+    return Intrinsics(vals[0], vals[1], vals[2], vals[3], int(vals[4]), int(vals[5]))
+
+
+def save_intrinsics(path, intr):
+    with open(path, "w") as f:
+        f.write(f"{intr.fx:.17g} {intr.fy:.17g} {intr.cx:.17g} {intr.cy:.17g} "
+                f"{intr.width} {intr.height}\n")

@@ -1,0 +1,299 @@
+// gsb.cu -- C ABI (include/gsb.h) over the GO-Surf step kernels.
+#include <cuda_runtime.h>
+
+#include <type_traits>
+
+#include "gsb_step.cuh"
+
+using namespace gsb;
+
+
+using namespace gsb::host;
+
+#define GSB_DECL(name)                                                                  \
+  extern "C" int name(const gsb_model_t* m, const gsb_dataset_t* d, const gsb_step_t* st, \
+                      cudaStream_t s);
+GSB_DECL(gsb_step_f446)
+GSB_DECL(gsb_step_d446)
+GSB_DECL(gsb_step_f222)
+GSB_DECL(gsb_step_d222)
+
+namespace gsb_abi {
+
+// twin: explicit uniforms / outputs
+__global__ void k_importance_twin(int M, int K, int A, int ld, const double* dep, const double* phi,
+                                  double s, const double* nearv, const double* farv,
+                                  const double* uni, gsb_pcg64_t rng, int use_rng, double* out,
+                                  int32_t* src, double* wts) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= M) return;
+  Pcg g;
+  g.init(rng);
+  if (use_rng) g.advance((uint64_t)i * (uint64_t)A);
+  importance_row(K, A, dep + (int64_t)i * ld, phi + (int64_t)i * ld, s, nearv[i], farv[i], &g,
+                 use_rng ? nullptr : uni + (int64_t)i * A, out + (int64_t)i * ld,
+                 src + (int64_t)i * ld, wts ? wts + (int64_t)i * ld : nullptr);
+}
+
+template <typename T>
+int dispatch_shape(const gsb_model_t* m, const gsb_dataset_t* d, const gsb_step_t* st,
+                   cudaStream_t s) {
+  const int nl = m->n_levels, cg = m->levels[0].channels, cc = m->color.channels;
+  for (int l = 0; l < nl; ++l)
+    if (m->levels[l].channels != cg) return GSB_E_ARG;
+  const bool f = sizeof(T) == 4;
+  if (nl == 4 && cg == 4 && cc == 6) return f ? gsb_step_f446(m, d, st, s) : gsb_step_d446(m, d, st, s);
+  if (nl == 2 && cg == 2 && cc == 2) return f ? gsb_step_f222(m, d, st, s) : gsb_step_d222(m, d, st, s);
+  return GSB_E_ARG;
+}
+
+}  // namespace gsb_abi
+using namespace gsb_abi;
+
+extern "C" {
+
+int gsb_version(void) { return 1; }
+
+int gsb_step_workspace_size(const gsb_model_t* model, int32_t n_rays, int32_t n_coarse,
+                            int32_t n_rounds, int32_t n_add, int32_t n_smooth, size_t* bytes) {
+  if (!model || !bytes || n_rays <= 0 || n_coarse < 2 || n_rounds < 0 || n_add < 0) return GSB_E_ARG;
+  if (n_coarse + n_rounds * n_add > GSB_KMAX || n_add > GSB_AMAX || n_rounds > GSB_MAX_ROUNDS)
+    return GSB_E_ARG;
+  Sizes z = sizes_of(model, n_rays, n_coarse, n_rounds, n_add, n_smooth);
+  if (model->precision == 0)
+    carve<float>(nullptr, z, bytes);
+  else
+    carve<double>(nullptr, z, bytes);
+  return GSB_OK;
+}
+
+int gsb_step_workspace_layout(const gsb_model_t* model, int32_t n_rays, int32_t n_coarse,
+                              int32_t n_rounds, int32_t n_add, int32_t n_smooth,
+                              int64_t* parts_off, int64_t* counts_off, int64_t* status_off,
+                              int64_t* depths_off, int64_t* weights_off, int32_t* ld) {
+  if (!model) return GSB_E_ARG;
+  Sizes z = sizes_of(model, n_rays, n_coarse, n_rounds, n_add, n_smooth);
+  size_t b = 0;
+  if (model->precision == 0)
+    carve<float>(nullptr, z, &b, parts_off, counts_off, status_off, depths_off, weights_off,
+                 n_rounds);
+  else
+    carve<double>(nullptr, z, &b, parts_off, counts_off, status_off, depths_off, weights_off,
+                  n_rounds);
+  if (ld) *ld = z.ld;
+  return GSB_OK;
+}
+
+int gsb_train_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step_t* step,
+                   void* stream) {
+  if (!model || !data || !step || !step->workspace) return GSB_E_ARG;
+  if (step->n_coarse + step->n_rounds * step->n_add > GSB_KMAX || step->n_add > GSB_AMAX ||
+      step->n_rounds > GSB_MAX_ROUNDS || step->n_coarse < 2)
+    return GSB_E_ARG;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (model->precision == 0) return dispatch_shape<float>(model, data, step, s);
+  return dispatch_shape<double>(model, data, step, s);
+}
+
+int gsb_adam_step(int32_t precision, void* params, void* grads, void* m, void* v, int64_t n,
+                  const int64_t* seg_begin_host, const double* seg_lr_host, int32_t n_seg,
+                  double beta1, double beta2, double eps, double c1, double c2,
+                  const double* guard, double guard_threshold, int32_t* status, void* stream) {
+  if (n_seg < 1 || n_seg > 16 || !status) return GSB_E_ARG;
+  AdamSegs sg;
+  sg.n = n_seg;
+  for (int i = 0; i < n_seg; ++i) {
+    sg.begin[i] = seg_begin_host[i];
+    sg.lr[i] = seg_lr_host[i];
+  }
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  int blocks = num_sms() * 8;
+  if (precision == 0)
+    k_adam<float><<<blocks, 256, 0, s>>>((float*)params, (float*)grads, (float*)m, (float*)v, n, sg,
+                                         beta1, beta2, eps, c1, c2, guard, guard_threshold, status);
+  else
+    k_adam<double><<<blocks, 256, 0, s>>>((double*)params, (double*)grads, (double*)m, (double*)v,
+                                          n, sg, beta1, beta2, eps, c1, c2, guard,
+                                          guard_threshold, status);
+  GSB_LAUNCHED();
+  return GSB_OK;
+}
+
+// ------------------------------------------------------------------ twins
+
+__global__ void k_pcg_fill(gsb_pcg64_t rng, int64_t offset, int64_t n, double* out) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  Pcg g;
+  g.init(rng);
+  g.advance((uint64_t)(offset + i));
+  out[i] = g.next_double();
+}
+
+int gsb_pcg64_random(const gsb_pcg64_t* rng, int64_t offset, int64_t n, double* out, void* stream) {
+  if (!rng || n < 0) return GSB_E_ARG;
+  if (n == 0) return GSB_OK;
+  k_pcg_fill<<<(int)((n + 255) / 256), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      *rng, offset, n, out);
+  GSB_LAUNCHED();
+  return GSB_OK;
+}
+
+__global__ void k_ray_batch_twin(gsb_dataset_t D, const int64_t* ids, int n, double* out) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  PixelRay P = pixel_ray(D, ids[i]);
+  double* o = out + (int64_t)i * 12;
+  o[0] = (double)P.frame;
+  o[1] = (double)P.u;
+  o[2] = (double)P.v;
+  o[3] = P.col[0];
+  o[4] = P.col[1];
+  o[5] = P.col[2];
+  o[6] = P.depth_ray;
+  o[7] = (double)P.valid;
+  o[8] = P.dir[0];
+  o[9] = P.dir[1];
+  o[10] = P.dir[2];
+  o[11] = P.scale;
+}
+
+int gsb_ray_batch(const gsb_dataset_t* data, const int64_t* ray_ids, int32_t n, double* out,
+                  void* stream) {
+  if (!data || n < 0) return GSB_E_ARG;
+  if (n == 0) return GSB_OK;
+  k_ray_batch_twin<<<(n + 127) / 128, 128, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      *data, ray_ids, n, out);
+  GSB_LAUNCHED();
+  return GSB_OK;
+}
+
+}  // extern "C"
+
+template <typename T>
+__global__ void k_gather_twin(const T* feat, int C, const int64_t* idx8, const double* w8,
+                              int64_t n, T* out) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  for (int c = 0; c < C; ++c) {
+    T acc = T(0);
+    for (int k = 0; k < 8; ++k)
+      acc = (T)((double)acc + w8[i * 8 + k] * (double)feat[idx8[i * 8 + k] * C + c]);
+    out[i * C + c] = acc;
+  }
+}
+
+extern "C" {
+
+int gsb_gather_weighted(int32_t precision, const void* feat, int32_t channels,
+                        const int64_t* idx8, const double* w8, int64_t n, void* out,
+                        void* stream) {
+  if (n < 0 || channels <= 0) return GSB_E_ARG;
+  if (n == 0) return GSB_OK;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  int b = (int)((n + 127) / 128);
+  if (precision == 0)
+    k_gather_twin<float><<<b, 128, 0, s>>>((const float*)feat, channels, idx8, w8, n, (float*)out);
+  else
+    k_gather_twin<double><<<b, 128, 0, s>>>((const double*)feat, channels, idx8, w8, n,
+                                            (double*)out);
+  GSB_LAUNCHED();
+  return GSB_OK;
+}
+
+}  // extern "C"
+
+template <typename T>
+__global__ void k_scatter_twin(const int64_t* idx8, const double* w8, const T* g, int C, int64_t n,
+                               T* out) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  for (int k = 0; k < 8; ++k)
+    for (int c = 0; c < C; ++c)
+      atomicAdd(out + idx8[i * 8 + k] * C + c, (T)(w8[i * 8 + k] * (double)g[i * C + c]));
+}
+
+extern "C" {
+
+int gsb_scatter_weighted(int32_t precision, const int64_t* idx8, const double* w8, const void* g,
+                         int32_t channels, int64_t n, void* out, void* stream) {
+  if (n < 0 || channels <= 0) return GSB_E_ARG;
+  if (n == 0) return GSB_OK;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  int b = (int)((n + 127) / 128);
+  if (precision == 0)
+    k_scatter_twin<float><<<b, 128, 0, s>>>(idx8, w8, (const float*)g, channels, n, (float*)out);
+  else
+    k_scatter_twin<double><<<b, 128, 0, s>>>(idx8, w8, (const double*)g, channels, n,
+                                             (double*)out);
+  GSB_LAUNCHED();
+  return GSB_OK;
+}
+
+}  // extern "C"
+
+template <typename T, int C>
+__global__ void k_grid_sample_twin(LevelDev L, const T* pts, int64_t n, T* out, int32_t* status) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  Loc q = locate<true>(L, (double)pts[i * 3], (double)pts[i * 3 + 1], (double)pts[i * 3 + 2],
+                       status);
+  T v[C];
+  gather_level<T, C, true>(L, q, v);
+  for (int c = 0; c < C; ++c) out[i * C + c] = v[c];
+}
+
+extern "C" {
+
+int gsb_grid_sample(int32_t precision, const gsb_level_t* level, const void* feat,
+                    const void* points, int64_t n, void* out, int32_t* status, void* stream) {
+  if (!level || n < 0) return GSB_E_ARG;
+  if (n == 0) return GSB_OK;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  gsb_level_t lv = *level;
+  lv.offset = 0;
+  size_t esz = precision == 0 ? 4 : 8;
+  LevelDev L = level_dev(lv, const_cast<void*>(feat), nullptr, esz);
+  int b = (int)((n + 127) / 128);
+#define GSB_GS(TT, CC)                                                                        \
+  k_grid_sample_twin<TT, CC><<<b, 128, 0, s>>>(L, (const TT*)points, n, (TT*)out, status); \
+  break;
+  if (precision == 0) {
+    switch (level->channels) {
+      case 1: GSB_GS(float, 1)
+      case 2: GSB_GS(float, 2)
+      case 4: GSB_GS(float, 4)
+      case 6: GSB_GS(float, 6)
+      default: return GSB_E_ARG;
+    }
+  } else {
+    switch (level->channels) {
+      case 1: GSB_GS(double, 1)
+      case 2: GSB_GS(double, 2)
+      case 4: GSB_GS(double, 4)
+      case 6: GSB_GS(double, 6)
+      default: return GSB_E_ARG;
+    }
+  }
+#undef GSB_GS
+  GSB_LAUNCHED();
+  return GSB_OK;
+}
+
+int gsb_importance_round(int32_t n, int32_t K, int32_t A, int32_t ld, const double* depths,
+                         const double* phi, double s, const double* nearv, const double* farv,
+                         const double* uniforms, const gsb_pcg64_t* rng, double* depths_out,
+                         int32_t* src_out, double* weights_out, void* stream) {
+  if (n < 0 || K < 2 || A < 0 || A > GSB_AMAX || K + A > GSB_KMAX || ld < K + A) return GSB_E_ARG;
+  if (!uniforms && !rng) return GSB_E_ARG;
+  if (n == 0) return GSB_OK;
+  gsb_pcg64_t g = {0, 0, 0, 0};
+  if (rng) g = *rng;
+  k_importance_twin<<<(n + 63) / 64, 64, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      n, K, A, ld, depths, phi, s, nearv, farv, uniforms, g, uniforms ? 0 : 1, depths_out, src_out,
+      weights_out);
+  GSB_LAUNCHED();
+  return GSB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,224 @@
+// gsb_common.cuh -- device building blocks shared by the step kernels.
+//
+// Compiled with --fmad=false: every multiply-add that the reference performs
+// as two rounded numpy/numba operations stays two rounded operations here;
+// the MLP and interpolation hot loops use explicit fma() where fusing is
+// harmless (those values are only compared within tolerance).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/gsb.h"
+
+#define GSB_HID 32  // decoders.HIDDEN_WIDTH (gs/decoders.py:22)
+
+namespace gsb {
+
+// ---------------------------------------------------------------------------
+// MLP weights live in __constant__ memory (copied from the arena once per
+// step): every thread reads the same weight at the same time, so each FMA
+// takes its weight straight from the constant bank.  Layout = arena layout
+// of the MLP block: geom W0 (IN,32), b0, W1 (32,32), b1, W2 (32,1), b2, pad
+// to a multiple of 4, colour W0 (CC+3,32), b0, W1, b1, W2 (32,3), b2
+// (weights stored (in, out) like gs/decoders.py:47).
+#define GSB_MLP_MAX 3200
+namespace {  // one copy per translation unit (each step TU owns its module)
+__constant__ float c_mlp_f[GSB_MLP_MAX];
+__constant__ double c_mlp_d[GSB_MLP_MAX];
+}  // namespace
+
+template <typename T> __device__ __forceinline__ T cw(int i);
+template <> __device__ __forceinline__ float cw<float>(int i) { return c_mlp_f[i]; }
+template <> __device__ __forceinline__ double cw<double>(int i) { return c_mlp_d[i]; }
+
+template <int NL_, int CG_, int CC_>
+struct Shape {
+  static constexpr int NL = NL_, CG = CG_, CC = CC_;
+  static constexpr int IN_G = NL * CG;
+  static constexpr int IN_C = CC + 3;
+  static constexpr int oGW0 = 0;
+  static constexpr int oGb0 = oGW0 + IN_G * GSB_HID;
+  static constexpr int oGW1 = oGb0 + GSB_HID;
+  static constexpr int oGb1 = oGW1 + GSB_HID * GSB_HID;
+  static constexpr int oGW2 = oGb1 + GSB_HID;
+  static constexpr int oGb2 = oGW2 + GSB_HID;
+  static constexpr int NG = oGb2 + 1;
+  static constexpr int oCW0 = (NG + 3) / 4 * 4;  // colour net starts 16-byte aligned
+  static constexpr int oCb0 = oCW0 + IN_C * GSB_HID;
+  static constexpr int oCW1 = oCb0 + GSB_HID;
+  static constexpr int oCb1 = oCW1 + GSB_HID * GSB_HID;
+  static constexpr int oCW2 = oCb1 + GSB_HID;
+  static constexpr int oCb2 = oCW2 + GSB_HID * 3;
+  static constexpr int NMLP = oCb2 + 3;
+  static_assert(NMLP <= GSB_MLP_MAX, "MLP block exceeds constant buffer");
+};
+
+// ---------------------------------------------------------------------------
+// numpy PCG64 (XSL-RR 128/64), gs/seeds.py:28-30 -> Generator.random():
+// state advances before each output; double = (x >> 11) * 2^-53.
+
+typedef unsigned __int128 u128;
+__device__ __forceinline__ u128 pcg_mult() {
+  return ((u128)0x2360ED051FC65DA4ULL << 64) | (u128)0x4385DF649FCCF645ULL;
+}
+
+struct Pcg {
+  u128 state, inc;
+  __device__ __forceinline__ void init(const gsb_pcg64_t& g) {
+    state = ((u128)g.state_hi << 64) | (u128)g.state_lo;
+    inc = ((u128)g.inc_hi << 64) | (u128)g.inc_lo;
+  }
+  __device__ __forceinline__ void advance(uint64_t delta) {
+    u128 cur_mult = pcg_mult(), cur_plus = inc, acc_mult = 1, acc_plus = 0;
+    while (delta > 0) {
+      if (delta & 1) {
+        acc_mult *= cur_mult;
+        acc_plus = acc_plus * cur_mult + cur_plus;
+      }
+      cur_plus = (cur_mult + 1) * cur_plus;
+      cur_mult *= cur_mult;
+      delta >>= 1;
+    }
+    state = acc_mult * state + acc_plus;
+  }
+  __device__ __forceinline__ uint64_t next64() {
+    state = state * pcg_mult() + inc;
+    uint64_t hi = (uint64_t)(state >> 64), lo = (uint64_t)state;
+    uint64_t x = hi ^ lo;
+    unsigned rot = (unsigned)(state >> 122);
+    return (x >> rot) | (x << ((64u - rot) & 63u));
+  }
+  __device__ __forceinline__ double next_double() {
+    return (double)(next64() >> 11) * (1.0 / 9007199254740992.0);
+  }
+};
+
+// ---------------------------------------------------------------------------
+// grid lattice (gs/diffcore.py:704-767)
+
+struct LevelDev {
+  const void* feat;
+  void* grad;
+  int nx, ny, nz, C;
+  double ox, oy, oz, vs, inv_vs, eps;
+};
+
+struct Loc {
+  int64_t base;     // flat vertex index of corner 0
+  double fx, fy, fz;
+};
+
+// local = (p - origin) / vs (gs/diffcore.py:740).  The fast path multiplies
+// by 1/vs and falls back to the exact division whenever the result lies
+// within 1e-7 of a lattice plane, so floor() -- the voxel index -- always
+// equals the reference's.
+template <bool EXACT>
+__device__ __forceinline__ double axis_local(double p, double o, double vs, double inv) {
+  double d = p - o;
+  if (EXACT) return d / vs;
+  double q = d * inv;
+  double r = rint(q);
+  if (fabs(q - r) < 1e-7 * fmax(1.0, fabs(q))) q = d / vs;
+  return q;
+}
+
+template <bool EXACT>
+__device__ __forceinline__ Loc locate(const LevelDev& L, double px, double py, double pz,
+                                      int* status) {
+  double lx = axis_local<EXACT>(px, L.ox, L.vs, L.inv_vs);
+  double ly = axis_local<EXACT>(py, L.oy, L.vs, L.inv_vs);
+  double lz = axis_local<EXACT>(pz, L.oz, L.vs, L.inv_vs);
+  if (lx < -L.eps || ly < -L.eps || lz < -L.eps || lx > (L.nx - 1) + L.eps ||
+      ly > (L.ny - 1) + L.eps || lz > (L.nz - 1) + L.eps || !(lx == lx && ly == ly && lz == lz)) {
+    if (status) atomicOr(status + GSB_ST_BOUNDS, 1);
+  }
+  int cx = (int)floor(lx), cy = (int)floor(ly), cz = (int)floor(lz);
+  cx = max(min(cx, L.nx - 2), 0);
+  cy = max(min(cy, L.ny - 2), 0);
+  cz = max(min(cz, L.nz - 2), 0);
+  Loc r;
+  r.base = ((int64_t)cx * L.ny + cy) * L.nz + cz;
+  r.fx = lx - cx;
+  r.fy = ly - cy;
+  r.fz = lz - cz;
+  return r;
+}
+
+// corner k = 4dx + 2dy + dz (gs/diffcore.py:731-735) -> flat offset
+__device__ __forceinline__ int64_t corner_off(const LevelDev& L, int k) {
+  return (int64_t)((k >> 2) & 1) * L.ny * L.nz + (int64_t)((k >> 1) & 1) * L.nz + (k & 1);
+}
+
+// ---------------------------------------------------------------------------
+// row loads / vector reductions
+
+template <typename T, int C>
+__device__ __forceinline__ void load_row(const T* __restrict__ p, T (&v)[C]) {
+  if constexpr (sizeof(T) == 4 && C % 4 == 0) {
+#pragma unroll
+    for (int c = 0; c < C; c += 4) {
+      float4 x = __ldg(reinterpret_cast<const float4*>(p + c));
+      v[c] = x.x; v[c + 1] = x.y; v[c + 2] = x.z; v[c + 3] = x.w;
+    }
+  } else if constexpr (sizeof(T) == 4 && C % 2 == 0) {
+#pragma unroll
+    for (int c = 0; c < C; c += 2) {
+      float2 x = __ldg(reinterpret_cast<const float2*>(p + c));
+      v[c] = x.x; v[c + 1] = x.y;
+    }
+  } else if constexpr (sizeof(T) == 8 && C % 2 == 0) {
+#pragma unroll
+    for (int c = 0; c < C; c += 2) {
+      double2 x = __ldg(reinterpret_cast<const double2*>(p + c));
+      v[c] = x.x; v[c + 1] = x.y;
+    }
+  } else {
+#pragma unroll
+    for (int c = 0; c < C; ++c) v[c] = __ldg(p + c);
+  }
+}
+
+__device__ __forceinline__ void red_add_v4(float* a, float x, float y, float z, float w) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(a), "f"(x), "f"(y), "f"(z),
+               "f"(w)
+               : "memory");
+}
+__device__ __forceinline__ void red_add_v2(float* a, float x, float y) {
+  asm volatile("red.global.add.v2.f32 [%0], {%1, %2};" ::"l"(a), "f"(x), "f"(y) : "memory");
+}
+
+template <typename T, int C>
+__device__ __forceinline__ void red_row(T* p, const T (&v)[C]) {
+  if constexpr (sizeof(T) == 4 && C % 4 == 0) {
+#pragma unroll
+    for (int c = 0; c < C; c += 4) red_add_v4(p + c, v[c], v[c + 1], v[c + 2], v[c + 3]);
+  } else if constexpr (sizeof(T) == 4 && C % 2 == 0) {
+#pragma unroll
+    for (int c = 0; c < C; c += 2) red_add_v2(p + c, v[c], v[c + 1]);
+  } else {
+#pragma unroll
+    for (int c = 0; c < C; ++c) atomicAdd(p + c, v[c]);
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ T sigmoid_raw(T x) {  // gs/diffcore.py:445-451
+  if (x >= T(0)) return T(1) / (T(1) + exp(-x));
+  T ex = exp(x);
+  return ex / (T(1) + ex);
+}
+
+template <typename T>
+__device__ __forceinline__ T sgn(T x) {
+  return x > T(0) ? T(1) : (x < T(0) ? T(-1) : T(0));
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+}  // namespace gsb

@@ -1,0 +1,126 @@
+// gsb_step.cuh -- one training step (objective + backward) for one (T, Shape).
+#pragma once
+
+#include "gsb_host.cuh"
+
+#define GSB_CHECK(x)                           \
+  do {                                         \
+    cudaError_t e__ = (x);                     \
+    if (e__ != cudaSuccess) return GSB_E_CUDA; \
+  } while (0)
+#define GSB_LAUNCHED() GSB_CHECK(cudaGetLastError())
+
+namespace gsb {
+namespace host {
+
+template <typename T, class S>
+int run_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step_t* st,
+             cudaStream_t stream) {
+  const size_t esz = sizeof(T);
+  Sizes z = sizes_of(model, st->n_rays, st->n_coarse, st->n_rounds, st->n_add, st->n_smooth);
+  if (S::NMLP != z.nmlp) return GSB_E_ARG;
+  size_t need = 0;
+  Ws<T> w = carve<T>(st->workspace, z, &need);
+  if (need > st->workspace_bytes) return GSB_E_ARG;
+  Geo G = geo_of(model, esz);
+  T* params = reinterpret_cast<T*>(model->params);
+  T* grads = reinterpret_cast<T*>(model->grads);
+  const T* mlp_src = params + model->mlp_offset;
+  if (std::is_same<T, float>::value)
+    GSB_CHECK(cudaMemcpyToSymbolAsync(c_mlp_f, mlp_src, S::NMLP * esz, 0,
+                                      cudaMemcpyDeviceToDevice, stream));
+  else
+    GSB_CHECK(cudaMemcpyToSymbolAsync(c_mlp_d, mlp_src, S::NMLP * esz, 0,
+                                      cudaMemcpyDeviceToDevice, stream));
+  const int M = z.M, N = z.N, Nc = st->n_coarse, A = st->n_add, R = st->n_rounds;
+  const int nsp = 2 * z.S;
+  double* dep_final = w.dep[R % 2];
+  const T* log_s = params + model->log_s_offset;
+  if (st->phases & 1) {
+    GSB_CHECK(cudaMemsetAsync(w.counts, 0, 8 * sizeof(long long), stream));
+    k_ray_setup<T><<<(M + 127) / 128, 128, 0, stream>>>(
+        *data, st->ray_ids, M, st->ray_base, w, G, Nc, st->near, st->max_depth,
+        st->has_fixed_far, st->fixed_far, st->rng_stratify);
+    GSB_LAUNCHED();
+    if (R > 0) {
+      int64_t n0 = (int64_t)M * Nc;
+      int blocks = (int)((n0 + 127) / 128);
+      k_sdf_eval<T, S, false><<<blocks, 128, 0, stream>>>(w, G, M, Nc, w.dep[0], w.phi[0],
+                                                            nullptr, nullptr);
+      GSB_LAUNCHED();
+      int cur = 0, K = Nc;
+      for (int rnd = 0; rnd < R; ++rnd) {
+        const bool need_phi = rnd < R - 1;
+        GSB_CHECK(cudaMemsetAsync(w.evl_count, 0, sizeof(int32_t), stream));
+        k_importance_dev<T><<<(M + 63) / 64, 64, 0, stream>>>(
+            w, M, K, A, st->ray_base, w.dep[cur], w.phi[cur], w.dep[1 - cur], w.phi[1 - cur],
+            log_s, st->rng_importance[rnd], w.evl, w.evl_count, w.evl_cap, need_phi ? 1 : 0);
+        GSB_LAUNCHED();
+        if (need_phi) {
+          int64_t cap = (int64_t)M * A;
+          int b2 = (int)((cap + 127) / 128);
+          k_sdf_eval<T, S, false><<<b2, 128, 0, stream>>>(w, G, M, Nc, w.dep[1 - cur],
+                                                            w.phi[1 - cur], w.evl, w.evl_count);
+          GSB_LAUNCHED();
+        }
+        cur = 1 - cur;
+        K += A;
+      }
+    }
+    k_counts<T><<<(M + 127) / 128, 128, 0, stream>>>(w, M, N, dep_final, st->truncation);
+    GSB_LAUNCHED();
+  }
+  if (st->phases & 2) {
+    const T* spts = reinterpret_cast<const T*>(st->smooth_pts);
+    int64_t ns = z.NS;
+    int fb = (int)((ns + 127) / 128);
+    k_fwd<T, S, false><<<fb, 128, 0, stream>>>(w, G, M, N, dep_final, spts, nsp);
+    GSB_LAUNCHED();
+    LossW L;
+    L.rgb = st->w_rgb;
+    L.depth = st->w_depth;
+    L.sdf = st->w_sdf;
+    L.fs = st->w_fs;
+    L.eik = st->w_eik;
+    L.smooth = st->w_smooth;
+    L.trunc = st->truncation;
+    L.alpha = st->fs_alpha;
+    L.m_global = st->m_global;
+    L.smooth_global = st->smooth_global;
+    if (z.S > 0) {
+      T scale = (T)(2.0 * st->w_smooth) / (T)st->smooth_global;
+      k_smooth<T><<<(z.S + 127) / 128, 128, 0, stream>>>(w, z.MN, z.S, scale);
+      GSB_LAUNCHED();
+    }
+    k_render<T><<<(M + 63) / 64, 64, 0, stream>>>(w, M, N, dep_final, params,
+                                                  model->log_s_offset, L);
+    GSB_LAUNCHED();
+    // backward kernels: persistent grids
+    constexpr int WG = sizeof(T) == 4 ? 4 : 2;
+    size_t smem_g = (size_t)WG * 32 * GeoRow<T, S>::ROW * sizeof(T);
+    size_t smem_c = (size_t)WG * 32 * ColRow<T, S>::ROW * sizeof(T);
+    GSB_CHECK(cudaFuncSetAttribute(k_bwd_geom<T, S, WG>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_g));
+    GSB_CHECK(cudaFuncSetAttribute(k_bwd_color<T, S, WG>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_c));
+    const int per_cta = WG * 32;
+    int nb_geo = (int)std::min<int64_t>((ns + per_cta - 1) / per_cta, (int64_t)num_sms() * 2);
+    int nb_col = (int)std::min<int64_t>((z.MN + per_cta - 1) / per_cta, (int64_t)num_sms() * 2);
+    nb_geo = std::max(1, std::min(nb_geo, kNbMax));
+    nb_col = std::max(1, std::min(nb_col, kNbMax));
+    k_bwd_geom<T, S, WG><<<nb_geo, per_cta, smem_g, stream>>>(w, G, M, N, dep_final, spts, nsp,
+                                                             2);
+    GSB_LAUNCHED();
+    k_bwd_color<T, S, WG><<<nb_col, per_cta, smem_c, stream>>>(w, G, M, N, dep_final);
+    GSB_LAUNCHED();
+    k_finalize_mlp<T, S><<<(S::NMLP + 255) / 256, 256, 0, stream>>>(w, grads, model->mlp_offset,
+                                                                    nb_geo, nb_col);
+    GSB_LAUNCHED();
+    k_finalize_loss<T><<<1, 1024, 0, stream>>>(w, M, z.S, grads, params, model->log_s_offset, L);
+    GSB_LAUNCHED();
+  }
+  return GSB_OK;
+}
+
+}  // namespace host
+}  // namespace gsb

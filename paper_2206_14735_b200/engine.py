@@ -1,0 +1,236 @@
+"""Device step engine: owns the workspace and launches ``gsb_train_step``.
+
+One engine per (model, dataset).  A step is one C-ABI call that enqueues the
+whole objective + backward on the caller's CUDA stream (ray setup and
+stratification, three importance rounds, taped forward, rendering/losses,
+fused backward with grid scatter and MLP gradient reduction); nothing in it
+synchronises with the host.  The per-iteration host inputs are only what
+the reference draws with numpy's integer/normal samplers: the ray ids
+(gs/sampler.py:70), the smoothness point set (gs/renderer.py:243-276) and
+the PCG64 states of the uniform streams, which the device regenerates.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from . import seeds
+from .camera import pixel_rays, ray_to_z_scale
+
+
+@dataclass
+class HostDraws:
+    """Everything one iteration needs from the host RNG."""
+
+    iteration: int
+    ray_ids: np.ndarray          # (M,) int64 flat ids into F*H*W
+    smooth: np.ndarray | None    # (2S, 3) model dtype: x then x+eps
+    rng_stratify: object
+    rng_importance: list
+
+
+def draw_smooth_points(model, dataset, count, truncation, delta, rng):
+    """gs/renderer.py:243-276, same RNG calls in the same order.
+
+    The k-th valid pixel comes from the dataset's per-row prefix count
+    instead of the full np.nonzero list (same pixel, same order)."""
+    n_valid = dataset.n_valid
+    if n_valid == 0:
+        return None
+    pick = rng.integers(0, n_valid, size=count)
+    f, v, u = dataset.valid_pixel(pick)
+    pixels = np.stack([u, v], axis=1).astype(np.float64)
+    intr = dataset.intrinsics
+    d_cam = pixel_rays(intr, pixels)
+    scale = ray_to_z_scale(intr, pixels)
+    depth_ray = dataset.depth_at(f, v, u) * scale + rng.uniform(-truncation, truncation, size=count)
+    mats = model.pose_matrices()[f]
+    dirs = np.einsum("nij,nj->ni", mats[:, :3, :3], d_cam)
+    x = mats[:, :3, 3] + depth_ray[:, None] * dirs
+    x = model.grid.clamp_points(x)
+    lo, hi = model.grid.clamp_box()
+    eps_dir = rng.normal(size=(count, 8, 3))
+    eps_dir /= np.linalg.norm(eps_dir, axis=2, keepdims=True)
+    cand = x[:, None, :] + delta * eps_dir
+    ok = ((cand >= lo) & (cand <= hi)).all(axis=2)
+    first = np.argmax(ok, axis=1)
+    xe = cand[np.arange(count), first]
+    xe = np.clip(xe, lo, hi)
+    return x, xe
+
+
+def host_draws(model, dataset, cfg, iteration, ray_ids=None, smooth_override=None):
+    """Host-side randomness of iteration `iteration` (gs/optimizer.py:363-366,
+    gs/renderer.py:320-336, 416-423)."""
+    lw = cfg.weights
+    if ray_ids is None:
+        intr = dataset.intrinsics
+        n = len(dataset) * intr.height * intr.width
+        ray_ids = seeds.substream(cfg.seed, seeds.RAYS, iteration).integers(
+            0, n, size=cfg.batch_rays)
+    if smooth_override is not None:
+        pts = smooth_override
+    else:
+        pts = draw_smooth_points(model, dataset, lw.smooth_count, lw.truncation,
+                                 lw.smooth_delta, seeds.substream(cfg.seed, seeds.SMOOTH,
+                                                                  iteration))
+    smooth = None
+    if pts is not None and lw.smooth != 0.0:
+        smooth = np.concatenate([pts[0], pts[1]], axis=0).astype(model.dtype)
+    rs = _lib.Pcg64.from_generator(seeds.substream(cfg.seed, seeds.STRATIFY, iteration))
+    ri = [_lib.Pcg64.from_generator(seeds.substream(cfg.seed, seeds.IMPORTANCE, iteration, r))
+          for r in range(cfg.importance_rounds)]
+    return HostDraws(iteration, np.asarray(ray_ids, dtype=np.int64), smooth, rs, ri)
+
+
+class StepEngine:
+    """Launches training steps for one model on one device dataset."""
+
+    def __init__(self, model, dataset):
+        import torch
+        self.torch = torch
+        self.model = model
+        self.dataset = dataset
+        self.device = model.arena.params.device
+        self.lib = _lib.lib()
+        self._ws = {}
+        self.col, self.dep, self.poses = dataset.device_tensors(self.device, model.dtype)
+        self.mstruct = self._model_struct()
+        self.dstruct = self._dataset_struct()
+
+    # ---- ABI structs
+    def _model_struct(self):
+        m = self.model
+        a = m.arena
+        ms = _lib.Model()
+        ms.precision = 0 if a.dtype == np.float32 else 1
+        if len(m.grid.levels) > _lib.MAX_LEVELS:
+            raise ValueError("too many grid levels")
+        ms.n_levels = len(m.grid.levels)
+
+        def lev(gl):
+            L = _lib.Level()
+            L.nx, L.ny, L.nz = gl.geom.dims
+            L.channels = gl.width
+            L.ox, L.oy, L.oz = (float(x) for x in gl.geom.origin)
+            L.voxel = gl.geom.voxel_size
+            L.offset = gl.features.offset
+            return L
+
+        for i, gl in enumerate(m.grid.levels):
+            ms.levels[i] = lev(gl)
+        ms.color = lev(m.grid.color)
+        ms.mlp_offset = a["geom_w0"].offset
+        ms.log_s_offset = m.log_s.offset
+        ms.n_params = a.n
+        lo, hi = m.grid.clamp_box()
+        for i in range(3):
+            ms.lo_c[i] = float(lo[i])
+            ms.hi_c[i] = float(hi[i])
+        ms.params = a.params.data_ptr()
+        ms.grads = a.grads.data_ptr()
+        return ms
+
+    def _dataset_struct(self):
+        ds = self.dataset
+        intr = ds.intrinsics
+        d = _lib.Dataset()
+        d.colors = self.col.data_ptr()
+        d.depth_mm = self.dep.data_ptr()
+        d.n_frames = len(ds)
+        d.height, d.width = intr.height, intr.width
+        d.fx, d.fy, d.cx, d.cy = (float(intr.fx), float(intr.fy), float(intr.cx), float(intr.cy))
+        d.poses = self.poses.data_ptr()
+        return d
+
+    # ---- workspace
+    def workspace(self, M, Nc, R, A, S):
+        key = (M, Nc, R, A, S)
+        if key not in self._ws:
+            torch = self.torch
+            nbytes = C.c_size_t(0)
+            _lib.check(self.lib.gsb_step_workspace_size(C.byref(self.mstruct), M, Nc, R, A, S,
+                                                        C.byref(nbytes)), "workspace size")
+            offs = [C.c_int64(0) for _ in range(5)]
+            ld = C.c_int32(0)
+            _lib.check(self.lib.gsb_step_workspace_layout(
+                C.byref(self.mstruct), M, Nc, R, A, S, *[C.byref(o) for o in offs],
+                C.byref(ld)), "workspace layout")
+            buf = torch.zeros(int(nbytes.value), dtype=torch.uint8, device=self.device)
+            N = Nc + R * A
+            tdt = torch.float32 if self.model.dtype == np.float32 else torch.float64
+            esz = 4 if tdt == torch.float32 else 8
+            po, co, so, do, wo = (o.value for o in offs)
+            views = dict(
+                buf=buf, ld=ld.value, N=N,
+                parts=buf[po:po + 8 * _lib.N_PARTS].view(torch.float64),
+                counts=buf[co:co + 8 * 4].view(torch.int64),
+                status=buf[so:so + 4 * _lib.N_STATUS].view(torch.int32),
+                depths=buf[do:do + 8 * M * ld.value].view(torch.float64).view(M, ld.value),
+                weights=buf[wo:wo + esz * M * N].view(tdt).view(M, N),
+            )
+            self._ws[key] = views
+        return self._ws[key]
+
+    # ---- one step
+    def step_struct(self, cfg, draws, ray_ids_dev, smooth_dev, ws, ray_base=0, m_global=None,
+                    smooth_global=None, phases=3, exact=False):
+        st = _lib.Step()
+        st.ray_ids = ray_ids_dev.data_ptr()
+        st.n_rays = int(ray_ids_dev.numel())
+        st.ray_base = int(ray_base)
+        st.m_global = float(m_global if m_global is not None else st.n_rays)
+        st.n_coarse = cfg.coarse_samples
+        st.n_rounds = cfg.importance_rounds
+        st.n_add = cfg.importance_add
+        st.has_fixed_far = 1 if cfg.fixed_far is not None else 0
+        st.near = float(cfg.near)
+        st.max_depth = float(cfg.max_depth)
+        st.fixed_far = float(cfg.fixed_far) if cfg.fixed_far is not None else 0.0
+        st.rng_stratify = draws.rng_stratify
+        for r, g in enumerate(draws.rng_importance):
+            st.rng_importance[r] = g
+        lw = cfg.weights
+        st.w_rgb, st.w_depth, st.w_sdf = float(lw.rgb), float(lw.depth), float(lw.sdf)
+        st.w_fs, st.w_eik, st.w_smooth = float(lw.fs), float(lw.eik), float(lw.smooth)
+        st.truncation = float(lw.truncation)
+        st.fs_alpha = float(lw.freespace_alpha)
+        if smooth_dev is not None:
+            st.smooth_pts = smooth_dev.data_ptr()
+            st.n_smooth = int(smooth_dev.shape[0] // 2)
+        else:
+            st.smooth_pts = None
+            st.n_smooth = 0
+        st.smooth_global = float(smooth_global if smooth_global is not None else max(st.n_smooth, 1))
+        st.exact_gather = 1 if exact else 0
+        st.phases = phases
+        st.workspace = ws["buf"].data_ptr()
+        st.workspace_bytes = ws["buf"].numel()
+        return st
+
+    def upload(self, draws, stream=None):
+        torch = self.torch
+        ids = torch.from_numpy(draws.ray_ids).pin_memory().to(self.device, non_blocking=True)
+        sm = None
+        if draws.smooth is not None:
+            sm = torch.from_numpy(np.ascontiguousarray(draws.smooth)).pin_memory().to(
+                self.device, non_blocking=True)
+        return ids, sm
+
+    def launch(self, cfg, draws, ray_ids_dev, smooth_dev, stream=None, **kw):
+        """Enqueue one objective + backward; returns the workspace views."""
+        M = int(ray_ids_dev.numel())
+        S = 0 if smooth_dev is None else int(smooth_dev.shape[0] // 2)
+        ws = self.workspace(M, cfg.coarse_samples, cfg.importance_rounds, cfg.importance_add, S)
+        self.model.arena.zero_grads()
+        ws["status"].zero_()
+        st = self.step_struct(cfg, draws, ray_ids_dev, smooth_dev, ws, **kw)
+        _lib.check(self.lib.gsb_train_step(C.byref(self.mstruct), C.byref(self.dstruct),
+                                           C.byref(st), _lib.stream_handle(stream)),
+                   "gsb_train_step")
+        self.model.arena.grads_clean = False
+        return ws

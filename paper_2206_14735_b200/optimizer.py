@@ -1,0 +1,395 @@
+"""Adam, configuration, model construction, checkpoints and the training
+loop (gs/optimizer.py), over the device parameter arena."""
+
+from __future__ import annotations
+
+import ctypes as C
+import logging
+import os
+from dataclasses import asdict, dataclass, field
+
+import numpy as np
+
+from . import _lib
+from . import checkpoint as ckpt
+from . import model as mdl
+from . import sampler, seeds
+from .data import Dataset
+from .renderer import LossWeights, engine_for, parts_from, check_status
+from .engine import host_draws
+
+__all__ = ["Adam", "TrainConfig", "DivergenceError", "train", "build_model", "make_optimizer",
+           "save_model", "load_model", "Trainer", "CSV_HEADER"]
+
+log = logging.getLogger("gridsurf_b200")
+
+
+class DivergenceError(RuntimeError):
+    pass
+
+
+class Adam:
+    """Bias-corrected Adam with per-parameter learning rates (gs/optimizer.py:58-91).
+
+    One fused launch over the whole arena: float64 register math, storage
+    in the model dtype, non-finite gradient entries zeroed and counted, the
+    gradient arena cleared on the way out."""
+
+    def __init__(self, params, lrs, beta1=0.9, beta2=0.999, eps=1e-8):
+        import torch
+        if len(params) != len(lrs):
+            raise ValueError("one learning rate per parameter")
+        self.params = list(params)
+        if not self.params:
+            raise ValueError("no parameters")
+        self.arena = self.params[0].arena
+        if any(p.arena is not self.arena for p in self.params):
+            raise ValueError("all parameters must live in one arena")
+        self.lrs = [float(l) for l in lrs]
+        self.beta1, self.beta2, self.eps = beta1, beta2, eps
+        self.m_arena = torch.zeros_like(self.arena.params)
+        self.v_arena = torch.zeros_like(self.arena.params)
+        self.t = [0] * len(self.params)
+        self.status = torch.zeros(_lib.N_STATUS, dtype=torch.int32, device=self.arena.device)
+        self._skipped_seen = 0
+
+    @property
+    def m(self):
+        return [self.m_arena[p.offset:p.offset + p.size].view(p.shape) for p in self.params]
+
+    @property
+    def v(self):
+        return [self.v_arena[p.offset:p.offset + p.size].view(p.shape) for p in self.params]
+
+    @property
+    def skipped(self):
+        return int(self.status[_lib.ST_ADAM_BAD].item())
+
+    def _segments(self):
+        """(begin, lr) runs over the arena.  Every parameter starts on a
+        4-element boundary whenever its learning-rate group can differ from
+        its predecessor's, so a 16-byte vector never straddles two rates;
+        arena ranges no parameter of this optimizer covers get lr 0."""
+        A = mdl.ParamArena.ALIGN
+        up = lambda x: (x + A - 1) // A * A
+        spans = sorted((p.offset, p.offset + p.size, lr) for p, lr in zip(self.params, self.lrs))
+        begins, lrs = [0], [spans[0][2] if spans[0][0] < A else 0.0]
+        pos = 0
+        for b, e, lr in spans:
+            if b - up(pos) >= A and lrs[-1] != 0.0:
+                begins.append(up(pos))
+                lrs.append(0.0)
+            if lrs[-1] != lr:
+                if b % A:
+                    raise ValueError("learning-rate boundary inside a vector group")
+                begins.append(b)
+                lrs.append(lr)
+            pos = e
+        if self.arena.n - up(pos) >= A and lrs[-1] != 0.0:
+            begins.append(up(pos))
+            lrs.append(0.0)
+        if len(begins) > 16:
+            raise ValueError("too many learning-rate segments")
+        return begins, lrs
+
+    def _launch(self, guard=None, guard_threshold=0.0, stream=None):
+        ts = set(self.t)
+        if len(ts) != 1:
+            raise NotImplementedError("per-tensor step counts must agree for the fused update")
+        t = float(self.t[0])
+        c1 = 1.0 - self.beta1 ** t  # host pow == numba's libm pow (bit-exact)
+        c2 = 1.0 - self.beta2 ** t
+        b, l = self._segments()
+        B = (C.c_int64 * len(b))(*b)
+        Lr = (C.c_double * len(l))(*l)
+        a = self.arena
+        _lib.check(_lib.lib().gsb_adam_step(
+            0 if a.dtype == np.float32 else 1, a.params.data_ptr(), a.grads.data_ptr(),
+            self.m_arena.data_ptr(), self.v_arena.data_ptr(), a.n, B, Lr, len(b),
+            self.beta1, self.beta2, self.eps, c1, c2,
+            None if guard is None else guard.data_ptr(), float(guard_threshold),
+            self.status.data_ptr(), _lib.stream_handle(stream)), "gsb_adam_step")
+        a.grads_clean = True
+        a.generation = getattr(a, "generation", 0) + 1
+
+    def step(self, grads, guard=None, guard_threshold=0.0):
+        """gs/optimizer.py:77-91.  `grads` are normally the arena views from
+        renderer.grad(); any other arrays are copied into the arena first."""
+        import torch
+        a = self.arena
+        fused = len(grads) == len(self.params) and all(
+            isinstance(g, torch.Tensor) and g.data_ptr() == p.grad.data_ptr()
+            for g, p in zip(grads, self.params))
+        if not fused:
+            a.grads.zero_()
+            for p, g in zip(self.params, grads):
+                gt = g if isinstance(g, torch.Tensor) else torch.as_tensor(np.asarray(g))
+                p.grad.copy_(gt.reshape(p.shape).to(device=a.device, dtype=a.grads.dtype))
+        self.t = [t + 1 for t in self.t]
+        self._launch(guard=guard, guard_threshold=guard_threshold)
+
+
+@dataclass
+class TrainConfig:
+    """All knobs of a reconstruction run (gs/optimizer.py:94-143)."""
+
+    iterations: int = 10000
+    batch_rays: int = 6144
+    coarse_samples: int = sampler.N_COARSE
+    importance_rounds: int = sampler.N_IMPORTANCE_ROUNDS
+    importance_add: int = sampler.N_IMPORTANCE_ADD
+    seed: int = 0
+    precision: str = "double"
+    refine_poses: bool = False
+    freeze_first_pose: bool = True
+    lr_grids: float = 1e-2
+    lr_decoders: float = 1e-3
+    lr_poses: float = 5e-4
+    pose_refresh_every: int = 100
+    checkpoint_every: int = 1000
+    near: float = 0.01
+    max_depth: float = 8.0
+    bounds: tuple | None = None
+    bounds_padding: float = 0.5
+    voxel_sizes: tuple = mdl.DEFAULT_GEOM_VOXELS
+    color_voxel: float | None = None
+    geom_feat_dim: int = mdl.GEOM_FEATURE_WIDTH
+    color_feat_dim: int = mdl.COLOR_FEATURE_WIDTH
+    init_steps: int = 2000
+    init_tol: float = 0.01
+    sphere_radius_scale: float = 0.5
+    divergence_threshold: float = 1e6
+    fixed_far: float | None = None
+    weights: LossWeights = field(default_factory=LossWeights)
+
+    def __post_init__(self):
+        if self.iterations < 0:
+            raise ValueError("iterations must be >= 0")
+        if self.precision not in ("double", "single"):
+            raise ValueError("precision must be 'double' or 'single'")
+
+    @property
+    def dtype(self):
+        return np.float64 if self.precision == "double" else np.float32
+
+    def echo(self):
+        d = asdict(self)
+        d["weights"] = asdict(self.weights)
+        for k, v in list(d.items()):
+            if isinstance(v, tuple):
+                d[k] = list(v)
+        return d
+
+
+def _device(device=None):
+    import torch
+    if device is not None:
+        return torch.device(device)
+    if not torch.cuda.is_available():
+        raise RuntimeError("the B200 path needs a CUDA device (no CPU fallback)")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def build_model(dataset, cfg, initial_poses=None, skip_init=False, device=None):
+    """gs/optimizer.py:181-214: grids, decoders, sharpness, poses."""
+    if cfg.refine_poses:
+        raise NotImplementedError("pose refinement is not implemented on the B200 path")
+    dataset = Dataset.wrap(dataset)
+    lo, hi = mdl.derive_bounds(dataset, cfg)
+    poses = dataset.poses if initial_poses is None else np.asarray(initial_poses)
+    model = mdl.allocate_model(lo, hi, cfg.voxel_sizes, cfg.geom_feat_dim, cfg.color_voxel,
+                               cfg.color_feat_dim, poses, cfg.dtype, _device(device))
+    mdl.init_parameters(model, cfg.seed, cfg.weights.truncation)
+    if not skip_init:
+        from .geometry import geometric_init
+        center = 0.5 * (lo + hi)
+        radius = cfg.sphere_radius_scale * float(np.min(hi - lo))
+        rmse = geometric_init(model, center, radius, seed=cfg.seed, max_steps=cfg.init_steps,
+                              tol=cfg.init_tol)
+        log.info("sphere pre-fit RMSE %.4f m", rmse)
+    return model
+
+
+def _lr_list(model, cfg):
+    """gs/optimizer.py:394-399."""
+    return ([cfg.lr_grids] * len(model.grid_params())
+            + [cfg.lr_decoders] * len(model.decoder_params())
+            + [cfg.lr_poses] * len(model.pose_params()))
+
+
+def make_optimizer(model, cfg):
+    """gs/optimizer.py:229-236."""
+    return Adam(model.parameters(), _lr_list(model, cfg))
+
+
+# ---------------------------------------------------------------------------
+# checkpoints (GSURFCKPT1, gs/optimizer.py:243-325)
+
+
+def save_model(path, model, cfg, iteration, opt=None):
+    names = model.param_names()
+    arrays = {n: p.numpy() for n, p in zip(names, model.parameters())}
+    # the reference stores log_s as a 0-d array
+    order = list(names)
+    arrays["R0"] = np.stack([p.R0 for p in model.poses], axis=0)
+    arrays["pose_nu"] = np.stack([np.asarray(p.nu, dtype=np.float64) for p in model.poses], axis=0)
+    arrays["pose_t"] = np.stack([np.asarray(p.t, dtype=np.float64) for p in model.poses], axis=0)
+    order += ["R0", "pose_nu", "pose_t"]
+    if opt is not None:
+        for name, m, v, t in zip(names, opt.m, opt.v, opt.t):
+            arrays[f"adam_m_{name}"] = m.cpu().numpy()
+            arrays[f"adam_v_{name}"] = v.cpu().numpy()
+            arrays[f"adam_t_{name}"] = np.array([t], dtype=np.int64)
+            order += [f"adam_m_{name}", f"adam_v_{name}", f"adam_t_{name}"]
+    header = {
+        "kind": "gridsurf-model",
+        "iteration": int(iteration),
+        "config": cfg.echo(),
+        "grid": {
+            "lo": list(map(float, model.grid.lo)),
+            "hi": list(map(float, model.grid.hi)),
+            "levels": [{"origin": list(map(float, l.geom.origin)),
+                        "voxel_size": l.geom.voxel_size, "dims": list(l.geom.dims),
+                        "width": int(l.width)} for l in model.grid.levels + [model.grid.color]],
+        },
+        "pose_trainable": [bool(p.trainable) for p in model.poses],
+        "has_adam": opt is not None,
+        "array_order": order,
+    }
+    ckpt.write_container(path, header, arrays)
+
+
+def load_model(path, device=None):
+    """Rebuild (model, cfg, iteration, opt-or-None) from a GSURFCKPT1 file."""
+    import torch
+    header, arrays = ckpt.read_container(path)
+    cfg_d = dict(header["config"])
+    w = cfg_d.pop("weights")
+    cfg = TrainConfig(**{**cfg_d,
+                         "bounds": tuple(map(tuple, cfg_d["bounds"])) if cfg_d.get("bounds") else None,
+                         "voxel_sizes": tuple(cfg_d["voxel_sizes"]),
+                         "weights": LossWeights(**w)})
+    if any(header["pose_trainable"]):
+        raise NotImplementedError("checkpoints with trainable poses are not supported")
+    g = header["grid"]
+    lv = g["levels"]
+    dt = arrays["level0"].dtype
+    poses = np.zeros((len(header["pose_trainable"]), 4, 4))
+    poses[:, 3, 3] = 1.0
+    poses[:, :3, :3] = arrays["R0"]
+    poses[:, :3, 3] = arrays["pose_t"]
+    model = mdl.allocate_model(g["lo"], g["hi"], [m["voxel_size"] for m in lv[:-1]],
+                               lv[0]["width"], lv[-1]["voxel_size"], lv[-1]["width"], poses, dt,
+                               _device(device))
+    for lev, meta in zip(model.grid.levels + [model.grid.color], lv):
+        if list(lev.geom.dims) != list(meta["dims"]) or not np.allclose(lev.geom.origin,
+                                                                        meta["origin"]):
+            raise ckpt.CheckpointError("grid geometry does not match the checkpoint")
+    names = model.param_names()
+    for n, p in zip(names, model.parameters()):
+        p.set(arrays[n])
+    opt = None
+    if header.get("has_adam"):
+        opt = Adam(model.parameters(), [0.0] * len(model.parameters()))
+        for n, p, m, v in zip(names, model.parameters(), opt.m, opt.v):
+            m.copy_(torch.from_numpy(np.ascontiguousarray(arrays[f"adam_m_{n}"])).reshape(p.shape))
+            v.copy_(torch.from_numpy(np.ascontiguousarray(arrays[f"adam_v_{n}"])).reshape(p.shape))
+        opt.t = [int(arrays[f"adam_t_{n}"][0]) for n in names]
+    return model, cfg, int(header["iteration"]), opt
+
+
+# ---------------------------------------------------------------------------
+# training loop (gs/optimizer.py:331-391)
+
+CSV_HEADER = "iter,total,rgb,depth,sdf,fs,eik,smooth,s\n"
+
+
+class Trainer:
+    """The device-resident inner loop: draw -> objective+backward -> Adam.
+
+    Loss parts for iteration k are copied to pinned host memory and read
+    one iteration later, so the host never waits on the GPU inside the
+    loop; divergence is enforced on the device (the Adam launch is skipped
+    when the total is non-finite or above the threshold, and stays skipped)
+    so the model state matches the reference's when the error surfaces."""
+
+    def __init__(self, model, dataset, cfg, opt):
+        import torch
+        self.torch = torch
+        self.model, self.cfg, self.opt = model, cfg, opt
+        self.dataset = Dataset.wrap(dataset)
+        self.engine = engine_for(model, self.dataset)
+        self.host_parts = torch.zeros((2, _lib.N_PARTS), dtype=torch.float64).pin_memory()
+        self.events = [torch.cuda.Event(), torch.cuda.Event()]
+
+    def draws(self, it):
+        return host_draws(self.model, self.dataset, self.cfg, it)
+
+    def launch(self, it, draws=None, slot=0):
+        d = draws if draws is not None else self.draws(it)
+        ids, sm = self.engine.upload(d)
+        ws = self.engine.launch(self.cfg, d, ids, sm)
+        self.host_parts[slot].copy_(ws["parts"], non_blocking=True)
+        self.events[slot].record()
+        self.opt.t = [t + 1 for t in self.opt.t]
+        self.opt._launch(guard=ws["parts"], guard_threshold=self.cfg.divergence_threshold)
+        return ws
+
+    def parts(self, slot):
+        self.events[slot].synchronize()
+        p = self.host_parts[slot].numpy()
+        return {k: float(p[i]) for i, k in enumerate(_lib.PART_NAMES)}
+
+
+def train(dataset, cfg, out_dir, initial_poses=None, resume=None):
+    """Optimise a model on a dataset; returns (model, final checkpoint path)
+    (gs/optimizer.py:334-391).  Writes loss_log.csv and checkpoints."""
+    os.makedirs(out_dir, exist_ok=True)
+    dataset = Dataset.wrap(dataset)
+    if resume is not None:
+        model, cfg_loaded, start_it, opt = load_model(resume)
+        cfg = cfg_loaded if cfg is None else cfg
+        if opt is None:
+            opt = make_optimizer(model, cfg)
+        opt.lrs = _lr_list(model, cfg)
+        csv_mode = "a"
+    else:
+        model = build_model(dataset, cfg, initial_poses=initial_poses)
+        opt = make_optimizer(model, cfg)
+        start_it = 0
+        csv_mode = "w"
+    csv_path = os.path.join(out_dir, "loss_log.csv")
+    final_path = os.path.join(out_dir, "ckpt_final.gsck")
+    T = Trainer(model, dataset, cfg, opt)
+    every = max(cfg.checkpoint_every, 1)
+
+    def finish(it, parts, csv):
+        if not np.isfinite(parts["total"]) or parts["total"] > cfg.divergence_threshold:
+            raise DivergenceError(f"loss diverged at iteration {it}: {parts}")
+        csv.write(f"{it},{parts['total']:.10g},{parts['rgb']:.10g},{parts['depth']:.10g},"
+                  f"{parts['sdf']:.10g},{parts['fs']:.10g},{parts['eik']:.10g},"
+                  f"{parts['smooth']:.10g},{parts['s']:.10g}\n")
+        if it % 50 == 0:
+            log.info("iter %d total %.5f", it, parts["total"])
+
+    with open(csv_path, csv_mode) as csv:
+        if csv_mode == "w":
+            csv.write(CSV_HEADER)
+        pending = None  # (iteration, slot)
+        for it in range(start_it, cfg.iterations):
+            slot = it % 2
+            T.launch(it, slot=slot)
+            if pending is not None:
+                finish(pending[0], T.parts(pending[1]), csv)
+            pending = (it, slot)
+            if (it + 1) % every == 0:
+                finish(it, T.parts(slot), csv)
+                pending = None
+                check_status(T.opt.status)
+                save_model(os.path.join(out_dir, f"ckpt_{it + 1:06d}.gsck"), model, cfg, it + 1,
+                           opt)
+        if pending is not None:
+            finish(pending[0], T.parts(pending[1]), csv)
+        csv.flush()
+    save_model(final_path, model, cfg, cfg.iterations, opt)
+    return model, final_path

@@ -1,0 +1,275 @@
+"""GPU parity: the CUDA step (through the C ABI) against the reference's
+golden vectors and the CPU oracle.
+
+Tolerances: bit-exact for indices, RNG streams, ray batch,
+grid sampling (exact twin) and importance sampling given phi; losses within
+1e-9 relative (float64) / 1e-5 (float32); gradients within max-abs-diff /
+max|g| <= 1e-9 (float64) / 1e-4 (float32) per tensor.
+"""
+
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from _golden import load, oracle_params, rel_maxnorm
+from oracle import gridsurf_oracle as O
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_2206_14735_b200 import _lib, data, optimizer, renderer, sampler, seeds  # noqa: E402
+
+DEV = torch.device("cuda", 0)
+LOSS_TOL = {"double": 1e-9, "single": 1e-5}
+GRAD_TOL = {"double": 1e-9, "single": 1e-4}
+
+
+def stream():
+    return _lib.stream_handle()
+
+
+def gpu_model(G):
+    cfg = optimizer.TrainConfig(precision=G.cfg.precision, **{
+        k: v for k, v in G.meta["cfg"].items() if k not in ("bounds", "voxel_sizes")},
+        voxel_sizes=G.cfg.voxel_sizes, bounds=G.cfg.bounds)
+    cfg.weights.smooth_count = G.meta["smooth_count"]
+    ds = data.Dataset(G.a["colors_u8"], G.a["depths_u16"], G.a["poses"], G.ds.intrinsics)
+    model = optimizer.build_model(ds, cfg, skip_init=True, device=DEV)
+    return model, ds, cfg
+
+
+# ---------------------------------------------------------------- unit twins
+
+def test_pcg64_stream_bit_exact():
+    g = seeds.substream(0, seeds.STRATIFY, 5)
+    st = _lib.Pcg64.from_generator(g)
+    ref = seeds.substream(0, seeds.STRATIFY, 5).random(5000)
+    out = torch.empty(3000, dtype=torch.float64, device=DEV)
+    _lib.check(_lib.lib().gsb_pcg64_random(C.byref(st), 2000, 3000, _lib.ptr(out), stream()))
+    np.testing.assert_array_equal(out.cpu().numpy(), ref[2000:])
+
+
+@pytest.mark.parametrize("case", ["tiny", "small"])
+def test_ray_batch_bit_exact(case):
+    G = load(case, "double")
+    model, ds, cfg = gpu_model(G)
+    it = G.meta["iteration"]
+    ids = seeds.substream(cfg.seed, seeds.RAYS, it).integers(
+        0, len(ds) * ds.intrinsics.height * ds.intrinsics.width, size=cfg.batch_rays)
+    from paper_2206_14735_b200.renderer import engine_for
+    eng = engine_for(model, ds)
+    idt = torch.from_numpy(ids).to(DEV)
+    out = torch.empty((len(ids), 12), dtype=torch.float64, device=DEV)
+    _lib.check(_lib.lib().gsb_ray_batch(C.byref(eng.dstruct), _lib.ptr(idt), len(ids),
+                                        _lib.ptr(out), stream()))
+    o = out.cpu().numpy()
+    np.testing.assert_array_equal(o[:, 0], G.a["batch_frame_ids"])
+    np.testing.assert_array_equal(o[:, 1:3], G.a["batch_pixels"])
+    np.testing.assert_array_equal(o[:, 3:6], G.a["batch_color"])
+    np.testing.assert_array_equal(o[:, 6], G.a["batch_depth_ray"])
+    np.testing.assert_array_equal(o[:, 7].astype(bool), G.a["batch_valid"])
+    np.testing.assert_array_equal(o[:, 8:11], G.a["batch_dir_cam"])
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("C_", [2, 4, 6])
+def test_grid_sample_exact_twin_bit_exact(dtype, C_):
+    rng = np.random.default_rng(C_)
+    lev = O.Level((-1.2, -0.7, -0.4), 0.13, (17, 13, 9), rng.normal(size=(17 * 13 * 9, C_)).astype(dtype))
+    hi = lev.origin + lev.voxel_size * (np.array(lev.dims) - 1)
+    pts = rng.uniform(lev.origin, hi, size=(4000, 3)).astype(dtype)
+    pts[:7] = lev.origin  # lattice corners / faces
+    pts[7] = hi.astype(dtype)
+    ref = O.LevelSample(lev, pts).value()
+    L = _lib.Level(*lev.dims, C_, *map(float, lev.origin), lev.voxel_size, 0)
+    f = torch.from_numpy(lev.feat).to(DEV)
+    p = torch.from_numpy(pts).to(DEV)
+    out = torch.empty((len(pts), C_), dtype=f.dtype, device=DEV)
+    status = torch.zeros(8, dtype=torch.int32, device=DEV)
+    _lib.check(_lib.lib().gsb_grid_sample(0 if dtype == np.float32 else 1, C.byref(L), _lib.ptr(f),
+                                          _lib.ptr(p), len(pts), _lib.ptr(out), _lib.ptr(status),
+                                          stream()))
+    assert status.sum().item() == 0
+    np.testing.assert_array_equal(out.cpu().numpy(), ref)
+
+
+def test_grid_sample_out_of_box_flags_bounds():
+    lev = O.Level((0.0, 0.0, 0.0), 1.0, (3, 3, 3), np.zeros((27, 2)))
+    L = _lib.Level(3, 3, 3, 2, 0.0, 0.0, 0.0, 1.0, 0)
+    f = torch.zeros((27, 2), dtype=torch.float64, device=DEV)
+    p = torch.tensor([[-0.1, 0.5, 0.5], [0.5, 0.5, 2.1]], dtype=torch.float64, device=DEV)
+    out = torch.empty((2, 2), dtype=torch.float64, device=DEV)
+    status = torch.zeros(8, dtype=torch.int32, device=DEV)
+    _lib.check(_lib.lib().gsb_grid_sample(1, C.byref(L), _lib.ptr(f), _lib.ptr(p), 2, _lib.ptr(out),
+                                          _lib.ptr(status), stream()))
+    assert status[_lib.ST_BOUNDS].item() == 1
+
+
+@pytest.mark.parametrize("case", ["tiny", "small"])
+def test_importance_round_given_phi(case):
+    """Depths and provenance bit-exact given the reference's phi cache;
+    weights equal to <= 2 ulp (device vs numpy exp)."""
+    G = load(case, "double")
+    n_rounds = G.cfg.importance_rounds
+    lib = _lib.lib()
+    s = 1.0 / 0.16
+    for r in range(n_rounds):
+        d_in = G.a[f"round{r}_depths_in"]
+        w_ref = G.a[f"round{r}_weights"]
+        u = G.a[f"round{r}_uniforms"]
+        M, K = d_in.shape
+        A = u.shape[1]
+        # phi that reproduces the recorded weights: use the oracle run's phi
+        P = oracle_params(G)
+        it = G.meta["iteration"]
+        batch = O.draw_ray_batch(G.ds, O.substream(G.cfg.seed, O.RAYS, it), G.cfg.batch_rays)
+        R = O.train_objective(P, G.ds, batch, it, G.cfg, want_grads=False)
+        phi = R["rounds"][r]["phi_in"]
+        ld = K + A
+        dd = torch.zeros((M, ld), dtype=torch.float64, device=DEV)
+        dd[:, :K] = torch.from_numpy(d_in)
+        pp = torch.zeros((M, ld), dtype=torch.float64, device=DEV)
+        pp[:, :K] = torch.from_numpy(phi)
+        near = torch.full((M,), G.cfg.near, dtype=torch.float64, device=DEV)
+        far_ref = R["far"]
+        far = torch.from_numpy(far_ref).to(DEV)
+        uu = torch.from_numpy(np.ascontiguousarray(u)).to(DEV)
+        out = torch.zeros((M, ld), dtype=torch.float64, device=DEV)
+        src = torch.zeros((M, ld), dtype=torch.int32, device=DEV)
+        wts = torch.zeros((M, ld), dtype=torch.float64, device=DEV)
+        _lib.check(lib.gsb_importance_round(M, K, A, ld, _lib.ptr(dd), _lib.ptr(pp), s, _lib.ptr(near),
+                                            _lib.ptr(far), _lib.ptr(uu), None, _lib.ptr(out),
+                                            _lib.ptr(src), _lib.ptr(wts), stream()))
+        w = wts.cpu().numpy()[:, :K]
+        np.testing.assert_allclose(w, w_ref, rtol=1e-15, atol=1e-300)
+        np.testing.assert_array_equal(out.cpu().numpy(), G.a[f"round{r}_depths"])
+        np.testing.assert_array_equal(src.cpu().numpy(), G.a[f"round{r}_src"])
+
+
+# ---------------------------------------------------------------- full step
+
+CASES = [(c, p) for c in ("tiny", "small") for p in ("double", "single")]
+
+
+@pytest.fixture(scope="module", params=CASES, ids=lambda cp: f"{cp[0]}-{cp[1]}")
+def step_run(request):
+    G = load(*request.param)
+    model, ds, cfg = gpu_model(G)
+    it = G.meta["iteration"]
+    batch = sampler.draw_ray_batch(ds, seeds.substream(cfg.seed, seeds.RAYS, it), cfg.batch_rays,
+                                   near=cfg.near, far=cfg.max_depth)
+    total, parts, extras = renderer.train_objective(model, ds, batch, it, cfg)
+    grads = renderer.grad(total, model.parameters())
+    g = {n: t.cpu().numpy().copy() for n, t in zip(model.param_names(), grads)}
+    return G, model, ds, cfg, total, parts, extras, g
+
+
+def test_step_init_params_bit_exact(step_run):
+    G, model = step_run[0], step_run[1]
+    # parameters are untouched by the objective
+    for n, p in zip(model.param_names(), model.parameters()):
+        np.testing.assert_array_equal(p.numpy(), G.a[f"init_{n}"], err_msg=n)
+
+
+def test_step_loss_parts_match_reference(step_run):
+    G, parts = step_run[0], step_run[5]
+    tol = LOSS_TOL[G.cfg.precision]
+    for k, v in G.meta["parts"].items():
+        if k == "smooth" and G.cfg.precision == "single":
+            assert parts[k] == pytest.approx(v, rel=1e-3, abs=1e-12), k
+            continue
+        assert parts[k] == pytest.approx(v, rel=tol, abs=1e-12), (k, parts[k], v)
+
+
+def test_step_extras_match_reference(step_run):
+    G, extras = step_run[0], step_run[6]
+    for k in ("samples_per_ray", "n_valid_rays", "n_tr", "n_fs", "n_eik", "n_smooth",
+              "empty_tr", "empty_fs"):
+        assert extras[k] == G.meta["extras"][k], k
+
+
+def test_step_depths_and_weights(step_run):
+    G, extras = step_run[0], step_run[6]
+    d = extras["depths"]
+    assert d.shape == G.a["depths"].shape
+    assert np.all(np.diff(d, axis=1) > 0)
+    if G.cfg.precision == "double":
+        np.testing.assert_allclose(d, G.a["depths"], rtol=1e-12, atol=1e-12)
+        np.testing.assert_allclose(extras["weights"], G.a["weights"], rtol=0, atol=1e-10)
+    else:
+        np.testing.assert_allclose(d, G.a["depths"], rtol=1e-5, atol=1e-5)
+        np.testing.assert_allclose(extras["weights"], G.a["weights"], rtol=0, atol=2e-4)
+
+
+def test_step_gradients_match_reference(step_run):
+    G, model, g = step_run[0], step_run[1], step_run[7]
+    tol = GRAD_TOL[G.cfg.precision]
+    worst = {}
+    for n in model.param_names():
+        worst[n] = rel_maxnorm(g[n], G.a[f"grad_{n}"])
+    assert max(worst.values()) <= tol, worst
+
+
+def test_adam_bit_exact_given_reference_grads(step_run):
+    G, model = step_run[0], step_run[1]
+    opt = optimizer.make_optimizer(model, step_run[3])
+    opt.step([G.a[f"grad_{n}"] for n in model.param_names()])
+    for i, (n, p) in enumerate(zip(model.param_names(), model.parameters())):
+        np.testing.assert_array_equal(p.numpy(), G.a[f"step1_{n}"], err_msg=n)
+        np.testing.assert_array_equal(opt.m[i].cpu().numpy(), G.a[f"step1_m_{n}"], err_msg=n)
+        np.testing.assert_array_equal(opt.v[i].cpu().numpy(), G.a[f"step1_v_{n}"], err_msg=n)
+    assert opt.skipped == 0
+
+
+@pytest.mark.parametrize("case", ["tiny", "small"])
+def test_two_iterations_double(case):
+    G = load(case, "double")
+    model, ds, cfg = gpu_model(G)
+    opt = optimizer.make_optimizer(model, cfg)
+    it0 = G.meta["iteration"]
+    for it in (it0, it0 + 1):
+        b = sampler.draw_ray_batch(ds, seeds.substream(cfg.seed, seeds.RAYS, it), cfg.batch_rays,
+                                   near=cfg.near, far=cfg.max_depth)
+        total, parts, _ = renderer.train_objective(model, ds, b, it, cfg)
+        opt.step(renderer.grad(total, opt.params))
+    for k, v in G.meta["parts1"].items():
+        assert parts[k] == pytest.approx(v, rel=1e-9, abs=1e-13), k
+    for n, p in zip(model.param_names(), model.parameters()):
+        assert rel_maxnorm(p.numpy(), G.a[f"final_{n}"]) <= 1e-7, n
+
+
+def test_step_deterministic_forward():
+    G = load("small", "single")
+    model, ds, cfg = gpu_model(G)
+    it = G.meta["iteration"]
+    b = sampler.draw_ray_batch(ds, seeds.substream(cfg.seed, seeds.RAYS, it), cfg.batch_rays)
+    _, p1, e1 = renderer.train_objective(model, ds, b, it, cfg)
+    _, p2, e2 = renderer.train_objective(model, ds, b, it, cfg)
+    assert p1 == p2
+    np.testing.assert_array_equal(e1["depths"], e2["depths"])
+
+
+def test_grad_rejects_stale_objective():
+    G = load("tiny", "single")
+    model, ds, cfg = gpu_model(G)
+    b = sampler.draw_ray_batch(ds, seeds.substream(0, seeds.RAYS, 0), cfg.batch_rays)
+    t1, _, _ = renderer.train_objective(model, ds, b, 0, cfg)
+    t2, _, _ = renderer.train_objective(model, ds, b, 0, cfg)
+    with pytest.raises(RuntimeError):
+        renderer.grad(t1, model.parameters())
+    renderer.grad(t2, model.parameters())
+
+
+def test_smooth_disabled_gives_zero():
+    G = load("tiny", "double")
+    model, ds, cfg = gpu_model(G)
+    cfg.weights.smooth = 0.0
+    b = sampler.draw_ray_batch(ds, seeds.substream(0, seeds.RAYS, 0), cfg.batch_rays)
+    _, parts, extras = renderer.train_objective(model, ds, b, 0, cfg)
+    assert parts["smooth"] == 0.0 and extras["n_smooth"] == 0
+    manual = (10 * parts["rgb"] + parts["depth"] + 10 * parts["sdf"] + parts["fs"] + parts["eik"])
+    assert parts["total"] == pytest.approx(manual, rel=1e-12)
