@@ -155,6 +155,26 @@ int gsb_step_workspace_layout(const gsb_model_t* model, int32_t n_rays, int32_t 
                               int64_t* parts_off, int64_t* counts_off, int64_t* status_off,
                               int64_t* depths_off, int64_t* weights_off, int32_t* ld);
 
+/* Byte offsets of internal workspace arrays (for parity tests / debugging). */
+#define GSB_R_PARTS 0    /* double[GSB_N_PARTS] */
+#define GSB_R_COUNTS 1   /* int64[GSB_N_COUNTS] */
+#define GSB_R_STATUS 2   /* int32[GSB_N_STATUS] */
+#define GSB_R_DEPTHS 3   /* double [n_rays][ld] final sample depths */
+#define GSB_R_WEIGHTS 4  /* T [n_rays][N] rendering weights */
+#define GSB_R_PHI 5      /* T [n_rays*N + 2*n_smooth] */
+#define GSB_R_GPHI 6     /* T [.. ][3] */
+#define GSB_R_COLOR 7    /* T [n_rays*N][3] */
+#define GSB_R_PBAR 8     /* T [n_rays*N + 2*n_smooth]  d total / d phi */
+#define GSB_R_UBAR 9     /* T [..][3]                 d total / d grad phi */
+#define GSB_R_CBAR 10    /* T [n_rays*N][3]           d total / d colour */
+#define GSB_R_RAY_O 11   /* T [n_rays][3] */
+#define GSB_R_RAY_R 12   /* T [n_rays][3] */
+#define GSB_R_RAY_FAR 13 /* double [n_rays] */
+#define GSB_N_REGIONS 14
+int gsb_step_workspace_regions(const gsb_model_t* model, int32_t n_rays, int32_t n_coarse,
+                               int32_t n_rounds, int32_t n_add, int32_t n_smooth,
+                               int64_t* offsets);
+
 /* One training objective + full backward; gradients are ACCUMULATED into
  * model->grads (gsb_adam_step leaves them zeroed). */
 int gsb_train_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step_t* step,
@@ -196,6 +216,14 @@ int gsb_importance_round(int32_t n, int32_t K, int32_t A, int32_t ld, const doub
                          const double* phi, double s, const double* near, const double* far,
                          const double* uniforms, const gsb_pcg64_t* rng, double* depths_out,
                          int32_t* src_out, double* weights_out, void* stream);
+
+/* sampler.importance_refine_with_sources (gs/sampler.py:128-169) exactly as
+ * the reference defines it: given depths (n,K), weights (n,K) and uniforms
+ * (n,A) -> merged depths (n,K+A) and provenance (-1 = new/moved). */
+int gsb_importance_refine(int32_t n, int32_t K, int32_t A, int32_t ld, const double* depths,
+                          const double* weights, const double* near, const double* far,
+                          const double* uniforms, double* depths_out, int32_t* src_out,
+                          void* stream);
 
 #ifdef __cplusplus
 }

@@ -26,7 +26,10 @@ EXPORTS = (
     "gsb_version", "gsb_step_workspace_size", "gsb_step_workspace_layout", "gsb_train_step",
     "gsb_adam_step", "gsb_pcg64_random", "gsb_ray_batch", "gsb_gather_weighted",
     "gsb_scatter_weighted", "gsb_grid_sample", "gsb_importance_round",
+    "gsb_step_workspace_regions", "gsb_importance_refine",
 )
+REGIONS = ("parts", "counts", "status", "depths", "weights", "phi", "gphi", "color", "pbar",
+           "ubar", "cbar", "ray_o", "ray_r", "ray_far")
 
 
 class Level(C.Structure):
@@ -102,6 +105,9 @@ def lib():
         "gsb_step_workspace_layout": ([C.POINTER(Model), I32, I32, I32, I32, I32,
                                        C.POINTER(I64), C.POINTER(I64), C.POINTER(I64),
                                        C.POINTER(I64), C.POINTER(I64), C.POINTER(I32)], I32),
+        "gsb_step_workspace_regions": ([C.POINTER(Model), I32, I32, I32, I32, I32,
+                                        C.POINTER(I64)], I32),
+        "gsb_importance_refine": ([I32, I32, I32, I32, P, P, P, P, P, P, P, P], I32),
         "gsb_train_step": ([C.POINTER(Model), C.POINTER(Dataset), C.POINTER(Step), P], I32),
         "gsb_adam_step": ([I32, P, P, P, P, I64, C.POINTER(I64), C.POINTER(D), I32, D, D, D, D, D,
                            P, D, P, P], I32),

@@ -22,15 +22,16 @@ namespace gsb_abi {
 
 // twin: explicit uniforms / outputs
 __global__ void k_importance_twin(int M, int K, int A, int ld, const double* dep, const double* phi,
-                                  double s, const double* nearv, const double* farv,
-                                  const double* uni, gsb_pcg64_t rng, int use_rng, double* out,
-                                  int32_t* src, double* wts) {
+                                  const double* win, double s, const double* nearv,
+                                  const double* farv, const double* uni, gsb_pcg64_t rng,
+                                  int use_rng, double* out, int32_t* src, double* wts) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= M) return;
   Pcg g;
   g.init(rng);
   if (use_rng) g.advance((uint64_t)i * (uint64_t)A);
-  importance_row(K, A, dep + (int64_t)i * ld, phi + (int64_t)i * ld, s, nearv[i], farv[i], &g,
+  importance_row(K, A, dep + (int64_t)i * ld, phi ? phi + (int64_t)i * ld : nullptr,
+                 win ? win + (int64_t)i * ld : nullptr, s, nearv[i], farv[i], &g,
                  use_rng ? nullptr : uni + (int64_t)i * A, out + (int64_t)i * ld,
                  src + (int64_t)i * ld, wts ? wts + (int64_t)i * ld : nullptr);
 }
@@ -45,6 +46,28 @@ int dispatch_shape(const gsb_model_t* m, const gsb_dataset_t* d, const gsb_step_
   if (nl == 4 && cg == 4 && cc == 6) return f ? gsb_step_f446(m, d, st, s) : gsb_step_d446(m, d, st, s);
   if (nl == 2 && cg == 2 && cc == 2) return f ? gsb_step_f222(m, d, st, s) : gsb_step_d222(m, d, st, s);
   return GSB_E_ARG;
+}
+
+template <typename T>
+void regions_of(const Sizes& z, int rounds, int64_t* o) {
+  unsigned char* base = reinterpret_cast<unsigned char*>(4096);  // never dereferenced
+  size_t b = 0;
+  Ws<T> w = carve<T>(base, z, &b);
+  auto off = [&](const void* p) { return (int64_t)(reinterpret_cast<const unsigned char*>(p) - base); };
+  o[GSB_R_PARTS] = off(w.parts);
+  o[GSB_R_COUNTS] = off(w.counts);
+  o[GSB_R_STATUS] = off(w.status);
+  o[GSB_R_DEPTHS] = off(w.dep[rounds % 2]);
+  o[GSB_R_WEIGHTS] = off(w.wts);
+  o[GSB_R_PHI] = off(w.sphi);
+  o[GSB_R_GPHI] = off(w.sgphi);
+  o[GSB_R_COLOR] = off(w.scol);
+  o[GSB_R_PBAR] = off(w.pbar);
+  o[GSB_R_UBAR] = off(w.ubar);
+  o[GSB_R_CBAR] = off(w.cbar);
+  o[GSB_R_RAY_O] = off(w.o);
+  o[GSB_R_RAY_R] = off(w.r);
+  o[GSB_R_RAY_FAR] = off(w.farv);
 }
 
 }  // namespace gsb_abi
@@ -81,6 +104,18 @@ int gsb_step_workspace_layout(const gsb_model_t* model, int32_t n_rays, int32_t 
     carve<double>(nullptr, z, &b, parts_off, counts_off, status_off, depths_off, weights_off,
                   n_rounds);
   if (ld) *ld = z.ld;
+  return GSB_OK;
+}
+
+int gsb_step_workspace_regions(const gsb_model_t* model, int32_t n_rays, int32_t n_coarse,
+                               int32_t n_rounds, int32_t n_add, int32_t n_smooth,
+                               int64_t* offsets) {
+  if (!model || !offsets) return GSB_E_ARG;
+  Sizes z = sizes_of(model, n_rays, n_coarse, n_rounds, n_add, n_smooth);
+  if (model->precision == 0)
+    regions_of<float>(z, n_rounds, offsets);
+  else
+    regions_of<double>(z, n_rounds, offsets);
   return GSB_OK;
 }
 
@@ -290,8 +325,24 @@ int gsb_importance_round(int32_t n, int32_t K, int32_t A, int32_t ld, const doub
   gsb_pcg64_t g = {0, 0, 0, 0};
   if (rng) g = *rng;
   k_importance_twin<<<(n + 63) / 64, 64, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
-      n, K, A, ld, depths, phi, s, nearv, farv, uniforms, g, uniforms ? 0 : 1, depths_out, src_out,
-      weights_out);
+      n, K, A, ld, depths, phi, nullptr, s, nearv, farv, uniforms, g, uniforms ? 0 : 1, depths_out,
+      src_out, weights_out);
+  GSB_LAUNCHED();
+  return GSB_OK;
+}
+
+int gsb_importance_refine(int32_t n, int32_t K, int32_t A, int32_t ld, const double* depths,
+                          const double* weights, const double* nearv, const double* farv,
+                          const double* uniforms, double* depths_out, int32_t* src_out,
+                          void* stream) {
+  if (n < 0 || K < 2 || A < 0 || A > GSB_AMAX || K + A > GSB_KMAX || ld < K + A || !weights ||
+      !uniforms)
+    return GSB_E_ARG;
+  if (n == 0) return GSB_OK;
+  gsb_pcg64_t g = {0, 0, 0, 0};
+  k_importance_twin<<<(n + 63) / 64, 64, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      n, K, A, ld, depths, nullptr, weights, 0.0, nearv, farv, uniforms, g, 0, depths_out,
+      src_out, nullptr);
   GSB_LAUNCHED();
   return GSB_OK;
 }

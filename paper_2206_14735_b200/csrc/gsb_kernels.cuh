@@ -410,26 +410,35 @@ static __device__ void separation_fallback(double* row, int32_t* src, int k) {
   }
 }
 
-static __device__ void importance_row(int K, int A, const double* d, const double* ph, double s,
-                               double nearv, double farv, Pcg* g, const double* uni,
-                               double* out, int32_t* src, double* wout) {
+static __device__ void importance_row(int K, int A, const double* d, const double* ph,
+                                      const double* win, double s, double nearv, double farv,
+                                      Pcg* g, const double* uni, double* out, int32_t* src,
+                                      double* wout) {
   double cdf[GSB_KMAX];
-  // render_weights_data (gs/renderer.py:162-173), sequential cumprod
-  double sig_i = sigmoid_raw(s * ph[0]);
-  double trans = 1.0, c = 0.0;
-  for (int i = 0; i < K - 1; ++i) {
-    double sig_n = sigmoid_raw(s * ph[i + 1]);
-    double den = sig_i >= 1e-12 ? sig_i : 1e-12;
-    double ratio = sig_n / den;
-    double om = ratio <= 1.0 ? ratio : 1.0;
-    double wi = trans * (1.0 - om);
-    if (wout) wout[i] = wi;
-    c = (i == 0) ? wi : c + wi;
-    cdf[i] = c;
-    trans = trans * om;
-    sig_i = sig_n;
+  double c = 0.0;
+  if (win) {  // weights given (importance_refine_with_sources signature)
+    for (int i = 0; i < K - 1; ++i) {
+      c = (i == 0) ? win[i] : c + win[i];
+      cdf[i] = c;
+    }
+  } else {
+    // render_weights_data (gs/renderer.py:162-173), sequential cumprod
+    double sig_i = sigmoid_raw(s * ph[0]);
+    double trans = 1.0;
+    for (int i = 0; i < K - 1; ++i) {
+      double sig_n = sigmoid_raw(s * ph[i + 1]);
+      double den = sig_i >= 1e-12 ? sig_i : 1e-12;
+      double ratio = sig_n / den;
+      double om = ratio <= 1.0 ? ratio : 1.0;
+      double wi = trans * (1.0 - om);
+      if (wout) wout[i] = wi;
+      c = (i == 0) ? wi : c + wi;
+      cdf[i] = c;
+      trans = trans * om;
+      sig_i = sig_n;
+    }
+    if (wout) wout[K - 1] = trans * (1.0 - 1.0);
   }
-  if (wout) wout[K - 1] = trans * (1.0 - 1.0);
   // importance_refine_with_sources (gs/sampler.py:128-169)
   bool dead = c <= 0.0;
   if (dead)
@@ -522,7 +531,7 @@ __global__ void k_importance_dev(Ws<T> w, int M, int K, int A, int ray_base,
   const double* ph = phi + (int64_t)i * w.ld;
   double* out = dep_out + (int64_t)i * w.ld;
   int32_t src[GSB_KMAX];
-  importance_row(K, A, d, ph, s, w.nearv[i], w.farv[i], &g, nullptr, out, src, nullptr);
+  importance_row(K, A, d, ph, nullptr, s, w.nearv[i], w.farv[i], &g, nullptr, out, src, nullptr);
   double* po = phi_out + (int64_t)i * w.ld;
   int nnew = 0;
   for (int t = 0; t < K + A; ++t) {

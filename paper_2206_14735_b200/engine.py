@@ -173,6 +173,19 @@ class StepEngine:
                 depths=buf[do:do + 8 * M * ld.value].view(torch.float64).view(M, ld.value),
                 weights=buf[wo:wo + esz * M * N].view(tdt).view(M, N),
             )
+            reg = (C.c_int64 * len(_lib.REGIONS))()
+            _lib.check(self.lib.gsb_step_workspace_regions(C.byref(self.mstruct), M, Nc, R, A, S,
+                                                           reg), "workspace regions")
+            views["regions"] = dict(zip(_lib.REGIONS, list(reg)))
+            NS = M * N + 2 * S
+            sizes = dict(phi=(NS,), gphi=(NS, 3), color=(M * N, 3), pbar=(NS,), ubar=(NS, 3),
+                         cbar=(M * N, 3), ray_o=(M, 3), ray_r=(M, 3))
+            for k, shp in sizes.items():
+                o = views["regions"][k]
+                n = int(np.prod(shp))
+                views[k] = buf[o:o + esz * n].view(tdt).view(*shp)
+            o = views["regions"]["ray_far"]
+            views["ray_far"] = buf[o:o + 8 * M].view(torch.float64)
             self._ws[key] = views
         return self._ws[key]
 
