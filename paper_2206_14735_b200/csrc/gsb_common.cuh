@@ -16,21 +16,10 @@
 namespace gsb {
 
 // ---------------------------------------------------------------------------
-// MLP weights live in __constant__ memory (copied from the arena once per
-// step): every thread reads the same weight at the same time, so each FMA
-// takes its weight straight from the constant bank.  Layout = arena layout
-// of the MLP block: geom W0 (IN,32), b0, W1 (32,32), b1, W2 (32,1), b2, pad
-// to a multiple of 4, colour W0 (CC+3,32), b0, W1, b1, W2 (32,3), b2
-// (weights stored (in, out) like gs/decoders.py:47).
+// MLP block layout (arena order, gs/decoders.py:40-49, weights stored (in, out)):
+// geom W0 (IN,32), b0, W1 (32,32), b1, W2 (32,1), b2, pad to a multiple of 4,
+// colour W0 (CC+3,32), b0, W1, b1, W2 (32,3), b2.
 #define GSB_MLP_MAX 3200
-namespace {  // one copy per translation unit (each step TU owns its module)
-__constant__ float c_mlp_f[GSB_MLP_MAX];
-__constant__ double c_mlp_d[GSB_MLP_MAX];
-}  // namespace
-
-template <typename T> __device__ __forceinline__ T cw(int i);
-template <> __device__ __forceinline__ float cw<float>(int i) { return c_mlp_f[i]; }
-template <> __device__ __forceinline__ double cw<double>(int i) { return c_mlp_d[i]; }
 
 template <int NL_, int CG_, int CC_>
 struct Shape {
@@ -109,18 +98,19 @@ struct Loc {
   double fx, fy, fz;
 };
 
-// local = (p - origin) / vs (gs/diffcore.py:740).  The fast path multiplies
-// by 1/vs and falls back to the exact division whenever the result lies
-// within 1e-7 of a lattice plane, so floor() -- the voxel index -- always
-// equals the reference's.
+// local = (p - origin) / vs (gs/diffcore.py:740), correctly rounded without
+// a division: with inv = RN(1/vs) (computed on the host), q = RN(d inv) is
+// within 1 ulp of d/vs, the remainder r = d - q vs is exact under an FMA, and
+// RN(q + r inv) is the correctly rounded quotient (Markstein's theorem; no
+// underflow/overflow for lattice coordinates).  So floor() -- the voxel
+// index -- always equals the reference's, at 1 DMUL + 2 DFMA per axis and no
+// slow-path call.
 template <bool EXACT>
 __device__ __forceinline__ double axis_local(double p, double o, double vs, double inv) {
-  double d = p - o;
-  if (EXACT) return d / vs;
-  double q = d * inv;
-  double r = rint(q);
-  if (fabs(q - r) < 1e-7 * fmax(1.0, fabs(q))) q = d / vs;
-  return q;
+  const double d = p - o;
+  const double q = d * inv;
+  const double r = fma(-q, vs, d);
+  return fma(r, inv, q);
 }
 
 template <bool EXACT>
@@ -207,6 +197,26 @@ __device__ __forceinline__ T sigmoid_raw(T x) {  // gs/diffcore.py:445-451
   if (x >= T(0)) return T(1) / (T(1) + exp(-x));
   T ex = exp(x);
   return ex / (T(1) + ex);
+}
+
+// Division without the IEEE slow-path subroutine call (used where values are
+// only compared within tolerance): float -> __fdividef (2 ulp), double ->
+// Newton-refined reciprocal + one remainder correction (faithful).
+__device__ __forceinline__ float fdiv(float a, float b) { return __fdividef(a, b); }
+__device__ __forceinline__ double fdiv(double a, double b) {
+  double y = (double)__frcp_rn((float)b);
+  y = fma(fma(-b, y, 1.0), y, y);
+  y = fma(fma(-b, y, 1.0), y, y);
+  const double q = a * y;
+  return fma(fma(-q, b, a), y, q);
+}
+
+// logistic function for the colour head, call-free
+template <typename T>
+__device__ __forceinline__ T sigmoid_fast(T x) {
+  if (x >= T(0)) return fdiv(T(1), T(1) + exp(-x));
+  const T ex = exp(x);
+  return fdiv(ex, T(1) + ex);
 }
 
 template <typename T>

@@ -19,6 +19,7 @@
 #include <type_traits>
 
 #include "gsb_common.cuh"
+#include "gsb_mlp.cuh"
 
 namespace gsb {
 
@@ -129,96 +130,6 @@ __device__ __forceinline__ void level_dx(const LevelDev& L, const Loc& q, const 
             (e[7] - e[5]) * (x1 * z1)) * iv;
   gr[2] += ((e[1] - e[0]) * (x0 * y0) + (e[3] - e[2]) * (x0 * y1) + (e[5] - e[4]) * (x1 * y0) +
             (e[7] - e[6]) * (x1 * y1)) * iv;
-}
-
-// ---------------------------------------------------------------------------
-// decoders (gs/decoders.py:55-99); weights from __constant__
-
-template <typename T, class S>
-__device__ __forceinline__ T geom_mlp(const T* z, T (&h0)[GSB_HID], T (&h1)[GSB_HID], uint32_t& m0,
-                                      uint32_t& m1) {
-  m0 = 0u;
-  m1 = 0u;
-#pragma unroll
-  for (int j = 0; j < GSB_HID; ++j) {
-    T a = T(0);
-#pragma unroll
-    for (int i = 0; i < S::IN_G; ++i) a = fma(z[i], cw<T>(S::oGW0 + i * GSB_HID + j), a);
-    a += cw<T>(S::oGb0 + j);
-    bool pos = a > T(0);
-    h0[j] = pos ? a : T(0);
-    m0 |= (uint32_t)pos << j;
-  }
-#pragma unroll
-  for (int j = 0; j < GSB_HID; ++j) {
-    T a = T(0);
-#pragma unroll
-    for (int i = 0; i < GSB_HID; ++i) a = fma(h0[i], cw<T>(S::oGW1 + i * GSB_HID + j), a);
-    a += cw<T>(S::oGb1 + j);
-    bool pos = a > T(0);
-    h1[j] = pos ? a : T(0);
-    m1 |= (uint32_t)pos << j;
-  }
-  T phi = T(0);
-#pragma unroll
-  for (int j = 0; j < GSB_HID; ++j) phi = fma(h1[j], cw<T>(S::oGW2 + j), phi);
-  return phi + cw<T>(S::oGb2);
-}
-
-// ReLU-MLP backward with seed 1: d1 = W2 (.) m1, d0 = (W1 d1) (.) m0, g = W0 d0
-template <typename T, class S>
-__device__ __forceinline__ void geom_delta(uint32_t m0, uint32_t m1, T (&d0)[GSB_HID],
-                                           T (&d1)[GSB_HID], T* g) {
-#pragma unroll
-  for (int j = 0; j < GSB_HID; ++j) d1[j] = ((m1 >> j) & 1u) ? cw<T>(S::oGW2 + j) : T(0);
-#pragma unroll
-  for (int i = 0; i < GSB_HID; ++i) {
-    T a = T(0);
-#pragma unroll
-    for (int j = 0; j < GSB_HID; ++j) a = fma(cw<T>(S::oGW1 + i * GSB_HID + j), d1[j], a);
-    d0[i] = ((m0 >> i) & 1u) ? a : T(0);
-  }
-#pragma unroll
-  for (int k = 0; k < S::IN_G; ++k) {
-    T a = T(0);
-#pragma unroll
-    for (int i = 0; i < GSB_HID; ++i) a = fma(cw<T>(S::oGW0 + k * GSB_HID + i), d0[i], a);
-    g[k] = a;
-  }
-}
-
-template <typename T, class S>
-__device__ __forceinline__ void color_mlp(const T* inp, T (&h0)[GSB_HID], T (&h1)[GSB_HID],
-                                          uint32_t& m0, uint32_t& m1, T (&y)[3]) {
-  m0 = 0u;
-  m1 = 0u;
-#pragma unroll
-  for (int j = 0; j < GSB_HID; ++j) {
-    T a = T(0);
-#pragma unroll
-    for (int i = 0; i < S::IN_C; ++i) a = fma(inp[i], cw<T>(S::oCW0 + i * GSB_HID + j), a);
-    a += cw<T>(S::oCb0 + j);
-    bool pos = a > T(0);
-    h0[j] = pos ? a : T(0);
-    m0 |= (uint32_t)pos << j;
-  }
-#pragma unroll
-  for (int j = 0; j < GSB_HID; ++j) {
-    T a = T(0);
-#pragma unroll
-    for (int i = 0; i < GSB_HID; ++i) a = fma(h0[i], cw<T>(S::oCW1 + i * GSB_HID + j), a);
-    a += cw<T>(S::oCb1 + j);
-    bool pos = a > T(0);
-    h1[j] = pos ? a : T(0);
-    m1 |= (uint32_t)pos << j;
-  }
-#pragma unroll
-  for (int c = 0; c < 3; ++c) {
-    T a = T(0);
-#pragma unroll
-    for (int j = 0; j < GSB_HID; ++j) a = fma(h1[j], cw<T>(S::oCW2 + j * 3 + c), a);
-    y[c] = a + cw<T>(S::oCb2 + c);
-  }
 }
 
 // ---------------------------------------------------------------------------
@@ -341,22 +252,30 @@ __global__ void k_ray_setup(gsb_dataset_t D, const int64_t* __restrict__ ids, in
 // no-grad SDF at listed samples (importance passes)
 
 template <typename T, class S, bool EXACT>
-__global__ void k_sdf_eval(Ws<T> w, Geo G, int M, int Nc, const double* __restrict__ dep,
-                           double* __restrict__ phi, const int32_t* __restrict__ list,
-                           const int32_t* __restrict__ list_count) {
-  int64_t total = list ? (int64_t)(*list_count) : (int64_t)M * Nc;
+__global__ void __launch_bounds__(128) k_sdf_eval(Ws<T> w, Geo G, int M, int Nc,
+                                                  const double* __restrict__ dep,
+                                                  double* __restrict__ phi,
+                                                  const int32_t* __restrict__ list,
+                                                  const int32_t* __restrict__ list_count,
+                                                  const T* __restrict__ mlp) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* sw = reinterpret_cast<T*>(smem_raw);
+  stage_weights<T, S>(sw, mlp, 0, S::NG);
+  __syncthreads();
+  const int64_t total = list ? (int64_t)(*list_count) : (int64_t)M * Nc;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
        t += (int64_t)gridDim.x * blockDim.x) {
     int ray, slot;
     if (list) {
-      int32_t e = list[t];
+      const int32_t e = list[t];
       ray = e / GSB_KMAX;
       slot = e % GSB_KMAX;
     } else {
-      ray = (int)(t / Nc);
-      slot = (int)(t % Nc);
+      ray = (int)((uint32_t)t / (uint32_t)Nc);
+      slot = (int)((uint32_t)t % (uint32_t)Nc);
     }
-    double d = dep[(int64_t)ray * w.ld + slot];
+    const double d = dep[(int64_t)ray * w.ld + slot];
+    // phi_at: clip(o + d r) in float64, then cast (gs/renderer.py:323-326)
     T p[3];
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
@@ -368,12 +287,15 @@ __global__ void k_sdf_eval(Ws<T> w, Geo G, int M, int Nc, const double* __restri
     T z[S::IN_G];
 #pragma unroll
     for (int l = 0; l < S::NL; ++l) {
-      Loc q = locate<EXACT>(G.lv[l], (double)p[0], (double)p[1], (double)p[2], w.status);
-      gather_level<T, S::CG, EXACT>(G.lv[l], q, z + l * S::CG);
+      const Loc q = locate<EXACT>(G.lv[l], (double)p[0], (double)p[1], (double)p[2], w.status);
+      gather_fast<T, S::CG>(G.lv[l], compact<T>(q), z + l * S::CG);
     }
     T h0[GSB_HID], h1[GSB_HID];
-    uint32_t m0, m1;
-    T f = geom_mlp<T, S>(z, h0, h1, m0, m1);
+    dense_fwd<T, S::IN_G>(sw + S::oGW0, sw + S::oGb0, z, h0);
+    relu_mask(h0);
+    dense_fwd<T, GSB_HID>(sw + S::oGW1, sw + S::oGb1, h0, h1);
+    relu_mask(h1);
+    const T f = dot32(sw + S::oGW2, h1) + sw[S::oGb2];
     phi[(int64_t)ray * w.ld + slot] = (double)f;
   }
 }
@@ -585,61 +507,104 @@ __global__ void k_counts(Ws<T> w, int M, int N, const double* __restrict__ dep, 
   }
 }
 
-// ---------------------------------------------------------------------------
 // taped forward: phi, grad phi (gs/renderer.py:356-358), colour (:360-365)
+template <typename T, class S>
+struct FwdRow {
+  static constexpr int oZ = 0;                              // z (IN_G) / colour input (IN_C)
+  static constexpr int ZP = ((S::IN_G > S::IN_C ? S::IN_G : S::IN_C) + 3) / 4 * 4;
+  static constexpr int oH = ZP;                             // hidden layer 0
+  static constexpr int oD = oH + GSB_HID;                   // delta0
+  static constexpr int ROW = oD + GSB_HID;
+};
 
 template <typename T, class S, bool EXACT>
-__global__ void __launch_bounds__(128) k_fwd(Ws<T> w, Geo G, int M, int N, const double* __restrict__ dep,
-                                             const T* __restrict__ spts, int nsp) {
-  int64_t MN = (int64_t)M * N;
-  int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+__global__ void __launch_bounds__(128) k_fwd(Ws<T> w, Geo G, int M, int N,
+                                             const double* __restrict__ dep,
+                                             const T* __restrict__ spts, int nsp,
+                                             const T* __restrict__ mlp) {
+  using R = FwdRow<T, S>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* sw = reinterpret_cast<T*>(smem_raw);
+  T* myrow = sw + (S::NMLP + 3) / 4 * 4 + (size_t)threadIdx.x * R::ROW;
+  stage_weights<T, S>(sw, mlp, 0, S::NMLP);
+  __syncthreads();
+  const int64_t MN = (int64_t)M * N;
+  const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (s >= MN + nsp) return;
   T p[3];
   int ray = -1;
   if (s < MN) {
-    ray = (int)(s / N);
-    T d = (T)dep[(int64_t)ray * w.ld + (int)(s % N)];
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-      T x = w.o[ray * 3 + a] + d * w.r[ray * 3 + a];
-      T lo = (T)G.lo[a], hi = (T)G.hi[a];
-      x = x >= lo ? x : lo;
-      x = x <= hi ? x : hi;
-      p[a] = x;
-    }
+    ray = (int)((uint32_t)s / (uint32_t)N);
+    taped_point<T>(w.o + ray * 3, w.r + ray * 3,
+                   dep[(int64_t)ray * w.ld + (int)((uint32_t)s % (uint32_t)N)], G.lo, G.hi, p);
   } else {
-    int64_t q = s - MN;
 #pragma unroll
-    for (int a = 0; a < 3; ++a) p[a] = spts[q * 3 + a];
+    for (int a = 0; a < 3; ++a) p[a] = spts[(s - MN) * 3 + a];
   }
-  T z[S::IN_G];
-  Loc loc[S::NL];
+  LocT<T> loc[S::NL];
 #pragma unroll
   for (int l = 0; l < S::NL; ++l) {
-    loc[l] = locate<EXACT>(G.lv[l], (double)p[0], (double)p[1], (double)p[2], w.status);
-    gather_level<T, S::CG, EXACT>(G.lv[l], loc[l], z + l * S::CG);
+    loc[l] = compact<T>(locate<EXACT>(G.lv[l], (double)p[0], (double)p[1], (double)p[2], w.status));
+    T f[S::CG];
+    gather_fast<T, S::CG>(G.lv[l], loc[l], f);
+#pragma unroll
+    for (int c = 0; c < S::CG; ++c) myrow[R::oZ + l * S::CG + c] = f[c];
   }
-  T h0[GSB_HID], h1[GSB_HID];
   uint32_t m0, m1;
-  T phi = geom_mlp<T, S>(z, h0, h1, m0, m1);
-  T d0[GSB_HID], d1[GSB_HID], gz[S::IN_G];
-  geom_delta<T, S>(m0, m1, d0, d1, gz);
+  T phi;
+  {
+    T h[GSB_HID];
+    dense_f_row<T, S::IN_G>(sw + S::oGW0, myrow + R::oZ, h);
+    add_bias(sw + S::oGb0, h);
+    m0 = relu_mask(h);
+    store32(myrow + R::oH, h);
+    dense_f_row<T, GSB_HID>(sw + S::oGW1, myrow + R::oH, h);
+    add_bias(sw + S::oGb1, h);
+    m1 = relu_mask(h);
+    phi = dot32(sw + S::oGW2, h) + sw[S::oGb2];
+  }
+  // grad phi: g = W0 ((W1 (W2 . m1)) . m0), then sum_l J_l^T g_l
+  T gz[S::IN_G];
+  {
+    T d[GSB_HID];
+#pragma unroll
+    for (int j = 0; j < GSB_HID; ++j) d[j] = ((m1 >> j) & 1u) ? sw[S::oGW2 + j] : T(0);
+    dense_d_row<T, GSB_HID>(sw + S::oGW1, d, m0, myrow + R::oD);
+    load32(myrow + R::oD, d);
+    dense_d_reg<T, S::IN_G>(sw + S::oGW0, d, gz);
+  }
   T gr[3] = {T(0), T(0), T(0)};
 #pragma unroll
-  for (int l = 0; l < S::NL; ++l) level_dx<T, S::CG>(G.lv[l], loc[l], gz + l * S::CG, gr);
+  for (int l = 0; l < S::NL; ++l) level_dx_fast<T, S::CG>(G.lv[l], loc[l], gz + l * S::CG, gr);
   w.sphi[s] = phi;
 #pragma unroll
   for (int a = 0; a < 3; ++a) w.sgphi[s * 3 + a] = gr[a];
   if (ray < 0) return;
-  Loc qc = locate<EXACT>(G.col, (double)p[0], (double)p[1], (double)p[2], w.status);
-  T inp[S::IN_C];
-  gather_level<T, S::CC, EXACT>(G.col, qc, inp);
+  // colour: sigmoid(MLP_c([f_c, r]))  (gs/decoders.py:86-99)
+  const Loc qc = locate<EXACT>(G.col, (double)p[0], (double)p[1], (double)p[2], w.status);
+  {
+    T f[S::CC];
+    gather_fast<T, S::CC>(G.col, compact<T>(qc), f);
 #pragma unroll
-  for (int a = 0; a < 3; ++a) inp[S::CC + a] = w.r[ray * 3 + a];
-  T y[3];
-  color_mlp<T, S>(inp, h0, h1, m0, m1, y);
+    for (int c = 0; c < S::CC; ++c) myrow[R::oZ + c] = f[c];
 #pragma unroll
-  for (int c = 0; c < 3; ++c) w.scol[s * 3 + c] = sigmoid_raw(y[c]);
+    for (int a = 0; a < 3; ++a) myrow[R::oZ + S::CC + a] = w.r[ray * 3 + a];
+  }
+  T h[GSB_HID];
+  dense_f_row<T, S::IN_C>(sw + S::oCW0, myrow + R::oZ, h);
+  add_bias(sw + S::oCb0, h);
+  relu_mask(h);
+  store32(myrow + R::oH, h);
+  dense_f_row<T, GSB_HID>(sw + S::oCW1, myrow + R::oH, h);
+  add_bias(sw + S::oCb1, h);
+  relu_mask(h);
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    T a = T(0);
+#pragma unroll
+    for (int j = 0; j < GSB_HID; ++j) a = fma(h[j], sw[S::oCW2 + j * 3 + c], a);
+    w.scol[s * 3 + c] = sigmoid_fast(a + sw[S::oCb2 + c]);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -843,39 +808,39 @@ __global__ void __launch_bounds__(64) k_render(Ws<T> w, int M, int N, const doub
 
 // ---------------------------------------------------------------------------
 // backward, geometry: grid scatter + geometry MLP weight gradients.
-// Thread per sample; each warp stages its 32 samples' outer-product factors
-// in shared memory and every lane accumulates one output column.
+// Thread per sample.  Each thread's shared-memory row holds its activations
+// and, at the end, its outer-product factors; every warp then accumulates
+// the 32 samples' outer products with lane j owning output column j.
 
 template <typename T, class S>
 struct GeoRow {
-  static constexpr int A0 = S::IN_G + 1;            // [p z + v, p]
+  static constexpr int A0 = S::IN_G + 1;            // [p z + v, p]   (z staged here)
   static constexpr int A0P = (A0 + 3) / 4 * 4;
   static constexpr int oA0 = 0;
   static constexpr int oB0 = oA0 + A0P;             // delta0
-  static constexpr int oA1 = oB0 + GSB_HID;           // [p h0 + q0, p]
+  static constexpr int oA1 = oB0 + GSB_HID;         // [p h0 + q0, p] (h0 staged here)
   static constexpr int A1P = (GSB_HID + 1 + 3) / 4 * 4;
   static constexpr int oB1 = oA1 + A1P;             // delta1
-  static constexpr int oV2 = oB1 + GSB_HID;           // p h1 + dd1 (.) m1
-  static constexpr int ROW = oV2 + GSB_HID;
+  static constexpr int oV2 = oB1 + GSB_HID;         // p h1 + dd1 (.) m1
+  static constexpr int oQ = oV2 + GSB_HID;          // q0 scratch
+  static constexpr int ROW = oQ + GSB_HID;
 };
 
 template <typename T, int C>
-__device__ __forceinline__ void scatter_level(const LevelDev& L, const Loc& q, const T* gl,
+__device__ __forceinline__ void scatter_level(const LevelDev& L, const LocT<T>& q, const T* gl,
                                               const T (&coef)[8], bool active, bool aggregate) {
-  T* Gp = reinterpret_cast<T*>(L.grad) + q.base * C;
   const unsigned full = 0xffffffffu;
   if (aggregate) {
-    // every lane of the warp shares one cell: reduce across the warp first
-    long long b0 = __shfl_sync(full, (long long)q.base, 0);
-    bool same = __all_sync(full, !active || (long long)q.base == b0);
-    if (same) {
+    // every lane shares one cell (coarse levels): reduce across the warp first
+    const int b0 = __shfl_sync(full, q.base, 0);
+    if (__all_sync(full, !active || q.base == b0)) {
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         T v[C];
 #pragma unroll
         for (int c = 0; c < C; ++c) v[c] = warp_sum(active ? gl[c] * coef[k] : T(0));
         if ((threadIdx.x & 31) == 0) {
-          T* dst = reinterpret_cast<T*>(L.grad) + (b0 + corner_off(L, k)) * C;
+          T* dst = reinterpret_cast<T*>(L.grad) + ((int64_t)b0 + corner_off(L, k)) * C;
           red_row<T, C>(dst, v);
         }
       }
@@ -883,6 +848,7 @@ __device__ __forceinline__ void scatter_level(const LevelDev& L, const Loc& q, c
     }
   }
   if (!active) return;
+  T* Gp = reinterpret_cast<T*>(L.grad) + (int64_t)q.base * C;
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
     T v[C];
@@ -892,14 +858,46 @@ __device__ __forceinline__ void scatter_level(const LevelDev& L, const Loc& q, c
   }
 }
 
+// warp outer products: acc0[i] += A0[r][i] B0[r][lane], acc1[i] += A1[r][i] B1[r][lane]
+template <typename T, int NA0, int NA0P, int NA1, int NA1P>
+__device__ __forceinline__ void warp_outer(const T* rows, int ROW, int oA0, int oB0, int oA1,
+                                           int oB1, int lane, T (&acc0)[NA0], T (&acc1)[NA1]) {
+#pragma unroll 1
+  for (int r = 0; r < 32; ++r) {
+    const T* rw = rows + (size_t)r * ROW;
+    const T b0 = rw[oB0 + lane], b1 = rw[oB1 + lane];
+#pragma unroll
+    for (int i = 0; i < NA0P; i += 4) {
+      T a0, a1, a2, a3;
+      lds4(rw + oA0 + i, a0, a1, a2, a3);
+      if (i < NA0) acc0[i] = fma(a0, b0, acc0[i]);
+      if (i + 1 < NA0) acc0[i + 1] = fma(a1, b0, acc0[i + 1]);
+      if (i + 2 < NA0) acc0[i + 2] = fma(a2, b0, acc0[i + 2]);
+      if (i + 3 < NA0) acc0[i + 3] = fma(a3, b0, acc0[i + 3]);
+    }
+#pragma unroll
+    for (int i = 0; i < NA1P; i += 4) {
+      T a0, a1, a2, a3;
+      lds4(rw + oA1 + i, a0, a1, a2, a3);
+      if (i < NA1) acc1[i] = fma(a0, b1, acc1[i]);
+      if (i + 1 < NA1) acc1[i + 1] = fma(a1, b1, acc1[i + 1]);
+      if (i + 2 < NA1) acc1[i + 2] = fma(a2, b1, acc1[i + 2]);
+      if (i + 3 < NA1) acc1[i + 3] = fma(a3, b1, acc1[i + 3]);
+    }
+  }
+}
+
 template <typename T, class S, int WARPS>
 __global__ void __launch_bounds__(WARPS * 32) k_bwd_geom(Ws<T> w, Geo G, int M, int N,
                                                         const double* __restrict__ dep,
                                                         const T* __restrict__ spts, int nsp,
-                                                        int agg_levels) {
+                                                        int agg_levels,
+                                                        const T* __restrict__ mlp) {
   using R = GeoRow<T, S>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  T* sm = reinterpret_cast<T*>(smem_raw);
+  T* sw = reinterpret_cast<T*>(smem_raw);                 // geometry weights
+  T* sm = sw + ((S::NG + 3) / 4 * 4);                      // per-warp rows
+  stage_weights<T, S>(sw, mlp, 0, S::NG);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   T* rows = sm + (size_t)wid * 32 * R::ROW;
   T* myrow = rows + (size_t)lane * R::ROW;
@@ -909,90 +907,88 @@ __global__ void __launch_bounds__(WARPS * 32) k_bwd_geom(Ws<T> w, Geo G, int M, 
   for (int i = 0; i < R::A0; ++i) acc0[i] = T(0);
 #pragma unroll
   for (int i = 0; i <= GSB_HID; ++i) acc1[i] = T(0);
+  __syncthreads();
   const int64_t nwarps = (int64_t)gridDim.x * WARPS;
   for (int64_t base = ((int64_t)blockIdx.x * WARPS + wid) * 32; base < NS; base += nwarps * 32) {
     const int64_t s = base + lane;
     const bool active = s < NS;
-    T p = T(0), u[3] = {T(0), T(0), T(0)};
-    T px = T(0), py = T(0), pz = T(0);
+    T p = T(0), u[3] = {T(0), T(0), T(0)}, pt[3];
     if (active) {
       p = w.pbar[s];
 #pragma unroll
       for (int a = 0; a < 3; ++a) u[a] = w.ubar[s * 3 + a];
-      T pt[3];
       if (s < MN) {
-        int ray = (int)(s / N);
-        T d = (T)dep[(int64_t)ray * w.ld + (int)(s % N)];
-#pragma unroll
-        for (int a = 0; a < 3; ++a) {
-          T x = w.o[ray * 3 + a] + d * w.r[ray * 3 + a];
-          T lo = (T)G.lo[a], hi = (T)G.hi[a];
-          x = x >= lo ? x : lo;
-          x = x <= hi ? x : hi;
-          pt[a] = x;
-        }
+        const int ray = (int)((uint32_t)s / (uint32_t)N);
+        taped_point<T>(w.o + ray * 3, w.r + ray * 3,
+                       dep[(int64_t)ray * w.ld + (int)((uint32_t)s % (uint32_t)N)], G.lo, G.hi, pt);
       } else {
 #pragma unroll
         for (int a = 0; a < 3; ++a) pt[a] = spts[(s - MN) * 3 + a];
       }
-      px = pt[0];
-      py = pt[1];
-      pz = pt[2];
     } else {
-      // inactive lanes evaluate a valid point (grid origin) and contribute 0
-      px = (T)G.lo[0];
-      py = (T)G.lo[1];
-      pz = (T)G.lo[2];
+      // inactive lanes evaluate a valid point and contribute zero
+#pragma unroll
+      for (int a = 0; a < 3; ++a) pt[a] = (T)G.lo[a];
     }
-    T z[S::IN_G];
-    Loc loc[S::NL];
+    LocT<T> loc[S::NL];
 #pragma unroll
     for (int l = 0; l < S::NL; ++l) {
-      loc[l] = locate<false>(G.lv[l], (double)px, (double)py, (double)pz, nullptr);
-      gather_level<T, S::CG, false>(G.lv[l], loc[l], z + l * S::CG);
+      loc[l] = compact<T>(locate<false>(G.lv[l], (double)pt[0], (double)pt[1], (double)pt[2], nullptr));
+      T f[S::CG];
+      gather_fast<T, S::CG>(G.lv[l], loc[l], f);
+#pragma unroll
+      for (int c = 0; c < S::CG; ++c) myrow[R::oA0 + l * S::CG + c] = f[c];
     }
     uint32_t m0, m1;
     {
-      T h0[GSB_HID], h1[GSB_HID];
-      geom_mlp<T, S>(z, h0, h1, m0, m1);
+      T h[GSB_HID];
+      dense_f_row<T, S::IN_G>(sw + S::oGW0, myrow + R::oA0, h);
+      add_bias(sw + S::oGb0, h);
+      m0 = relu_mask(h);
+      store32(myrow + R::oA1, h);                          // raw h0 (layer input)
+      dense_f_row<T, GSB_HID>(sw + S::oGW1, myrow + R::oA1, h);
+      add_bias(sw + S::oGb1, h);
+      m1 = relu_mask(h);
 #pragma unroll
-      for (int j = 0; j < GSB_HID; ++j) {
-        myrow[R::oA1 + j] = p * h0[j];
-        myrow[R::oV2 + j] = p * h1[j];
-      }
+      for (int j = 0; j < GSB_HID; ++j) h[j] *= p;
+      store32(myrow + R::oV2, h);                          // p h1
+      load32(myrow + R::oA1, h);
+#pragma unroll
+      for (int j = 0; j < GSB_HID; ++j) h[j] *= p;
+      store32(myrow + R::oA1, h);                          // p h0
       myrow[R::oA1 + GSB_HID] = p;
     }
     T gz[S::IN_G];
     {
-      T d0[GSB_HID], d1[GSB_HID];
-      geom_delta<T, S>(m0, m1, d0, d1, gz);
+      T d[GSB_HID];
 #pragma unroll
-      for (int j = 0; j < GSB_HID; ++j) {
-        myrow[R::oB0 + j] = d0[j];
-        myrow[R::oB1 + j] = d1[j];
-      }
+      for (int j = 0; j < GSB_HID; ++j) d[j] = ((m1 >> j) & 1u) ? sw[S::oGW2 + j] : T(0);
+      store32(myrow + R::oB1, d);                          // delta1
+      dense_d_row<T, GSB_HID>(sw + S::oGW1, d, m0, myrow + R::oB0);   // delta0
+      load32(myrow + R::oB0, d);
+      dense_d_reg<T, S::IN_G>(sw + S::oGW0, d, gz);        // g = dphi/dz
     }
-    // per level: ju, v = theta . ju, scatter g_l (p w_k + ju_k)
+    // per level: ju, v = theta . ju, scatter g_l (p w_k + ju_k)   (SURVEY Appendix A)
     T v[S::IN_G];
 #pragma unroll
     for (int l = 0; l < S::NL; ++l) {
       const LevelDev& L = G.lv[l];
-      const Loc& q = loc[l];
-      T x1 = (T)q.fx, y1 = (T)q.fy, z1 = (T)q.fz;
-      T x0 = (T)(1.0 - q.fx), y0 = (T)(1.0 - q.fy), z0 = (T)(1.0 - q.fz);
-      T iv = (T)L.inv_vs;
-      T u0 = u[0] * iv, u1 = u[1] * iv, u2 = u[2] * iv;
+      const LocT<T>& q = loc[l];
+      const T x1 = q.fx, y1 = q.fy, z1 = q.fz;
+      const T x0 = T(1) - x1, y0 = T(1) - y1, z0 = T(1) - z1;
+      const T iv = (T)L.inv_vs;
+      const T u0 = u[0] * iv, u1 = u[1] * iv, u2 = u[2] * iv;
       T coef[8];
       T vl[S::CG];
 #pragma unroll
       for (int c = 0; c < S::CG; ++c) vl[c] = T(0);
-      const T* F = reinterpret_cast<const T*>(L.feat) + q.base * S::CG;
+      const T* F = reinterpret_cast<const T*>(L.feat) + (int64_t)q.base * S::CG;
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         const int dx = (k >> 2) & 1, dy = (k >> 1) & 1, dz = k & 1;
-        T wx = dx ? x1 : x0, wy = dy ? y1 : y0, wz = dz ? z1 : z0;
-        T sx = dx ? T(1) : T(-1), sy = dy ? T(1) : T(-1), sz = dz ? T(1) : T(-1);
-        T ju = (sx * wy * wz) * u0 + (wx * sy * wz) * u1 + (wx * wy * sz) * u2;
+        const T wx = dx ? x1 : x0, wy = dy ? y1 : y0, wz = dz ? z1 : z0;
+        const T sx = dx ? T(1) : T(-1), sy = dy ? T(1) : T(-1), sz = dz ? T(1) : T(-1);
+        const T ju = (sx * wy * wz) * u0 + (wx * sy * wz) * u1 + (wx * wy * sz) * u2;
         coef[k] = p * ((wx * wy) * wz) + ju;
         T row[S::CG];
         load_row<T, S::CG>(F + corner_off(L, k) * S::CG, row);
@@ -1003,51 +999,47 @@ __global__ void __launch_bounds__(WARPS * 32) k_bwd_geom(Ws<T> w, Geo G, int M, 
       for (int c = 0; c < S::CG; ++c) v[l * S::CG + c] = vl[c];
       scatter_level<T, S::CG>(L, q, gz + l * S::CG, coef, active, l < agg_levels);
     }
+    // A0 = [p z + v, p]
 #pragma unroll
-    for (int i = 0; i < S::IN_G; ++i) myrow[R::oA0 + i] = p * z[i] + v[i];
+    for (int i = 0; i < S::IN_G; ++i) myrow[R::oA0 + i] = fma(p, myrow[R::oA0 + i], v[i]);
     myrow[R::oA0 + S::IN_G] = p;
-    // q0 = (v W0) (.) m0 ; dd1 = (q0 W1) (.) m1
+    // q0 = (v W0) (.) m0 -> A1 += q0 ; dd1 = (q0 W1) (.) m1 -> V2 += dd1
     {
       T q0[GSB_HID];
+      dense_f_reg<T, S::IN_G>(sw + S::oGW0, v, q0);
+      T a[GSB_HID];
+      load32(myrow + R::oA1, a);
 #pragma unroll
       for (int j = 0; j < GSB_HID; ++j) {
-        T a = T(0);
-#pragma unroll
-        for (int i = 0; i < S::IN_G; ++i) a = fma(v[i], cw<T>(S::oGW0 + i * GSB_HID + j), a);
-        q0[j] = ((m0 >> j) & 1u) ? a : T(0);
-        myrow[R::oA1 + j] += q0[j];
+        q0[j] = ((m0 >> j) & 1u) ? q0[j] : T(0);
+        a[j] += q0[j];
       }
+      store32(myrow + R::oA1, a);
+      store32(myrow + R::oQ, q0);
+      dense_f_row<T, GSB_HID>(sw + S::oGW1, myrow + R::oQ, q0);
+      load32(myrow + R::oV2, a);
 #pragma unroll
-      for (int j = 0; j < GSB_HID; ++j) {
-        T a = T(0);
-#pragma unroll
-        for (int i = 0; i < GSB_HID; ++i) a = fma(q0[i], cw<T>(S::oGW1 + i * GSB_HID + j), a);
-        if ((m1 >> j) & 1u) myrow[R::oV2 + j] += a;
-      }
+      for (int j = 0; j < GSB_HID; ++j) a[j] += ((m1 >> j) & 1u) ? q0[j] : T(0);
+      store32(myrow + R::oV2, a);
     }
     if (!active) {
 #pragma unroll 1
       for (int i = 0; i < R::ROW; ++i) myrow[i] = T(0);
     }
     __syncwarp();
-    // outer products over the warp's 32 samples; lane owns column `lane`
+    warp_outer<T, R::A0, R::A0P, GSB_HID + 1, R::A1P>(rows, R::ROW, R::oA0, R::oB0, R::oA1, R::oB1,
+                                                      lane, acc0, acc1);
 #pragma unroll 1
     for (int r = 0; r < 32; ++r) {
-      const T* rw = rows + (size_t)r * R::ROW;
-      T b0 = rw[R::oB0 + lane], b1 = rw[R::oB1 + lane];
-      acc2 += rw[R::oV2 + lane];
-#pragma unroll
-      for (int i = 0; i < R::A0; ++i) acc0[i] = fma(rw[R::oA0 + i], b0, acc0[i]);
-#pragma unroll
-      for (int i = 0; i <= GSB_HID; ++i) acc1[i] = fma(rw[R::oA1 + i], b1, acc1[i]);
-      accp += rw[R::oA0 + S::IN_G];
+      acc2 += rows[(size_t)r * R::ROW + R::oV2 + lane];
+      accp += rows[(size_t)r * R::ROW + R::oA0 + S::IN_G];  // db2 = sum p
     }
     __syncwarp();
   }
   // CTA reduction of the per-warp accumulators -> partial slot blockIdx.x
   __syncthreads();
-  constexpr int NGP = S::NG;  // geometry MLP parameter count
-  T* red = sm;                // [WARPS][NGP]
+  constexpr int NGP = S::NG;
+  T* red = sm;  // [WARPS][NGP]
   {
     T* mine = red + (size_t)wid * NGP;
 #pragma unroll
@@ -1078,20 +1070,25 @@ struct ColRow {
   static constexpr int A0P = (A0 + 3) / 4 * 4;
   static constexpr int oA0 = 0;
   static constexpr int oB0 = oA0 + A0P;        // a0_bar
-  static constexpr int oA1 = oB0 + GSB_HID;      // [h0, 1]
+  static constexpr int oA1 = oB0 + GSB_HID;    // [h0, 1]
   static constexpr int A1P = (GSB_HID + 1 + 3) / 4 * 4;
   static constexpr int oB1 = oA1 + A1P;        // a1_bar
-  static constexpr int oH1 = oB1 + GSB_HID;      // h1
-  static constexpr int oY = oH1 + GSB_HID;       // y_bar (3)
+  static constexpr int oH1 = oB1 + GSB_HID;    // h1
+  static constexpr int oY = oH1 + GSB_HID;     // y_bar (3)
   static constexpr int ROW = oY + 4;
 };
 
 template <typename T, class S, int WARPS>
 __global__ void __launch_bounds__(WARPS * 32) k_bwd_color(Ws<T> w, Geo G, int M, int N,
-                                                         const double* __restrict__ dep) {
+                                                         const double* __restrict__ dep,
+                                                         const T* __restrict__ mlp) {
   using R = ColRow<T, S>;
+  constexpr int CW = S::NMLP - S::oCW0;  // colour weights
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  T* sm = reinterpret_cast<T*>(smem_raw);
+  T* swc = reinterpret_cast<T*>(smem_raw);   // colour block, offsets relative to oCW0
+  T* sm = swc + ((CW + 3) / 4 * 4);
+  for (int t = threadIdx.x; t < CW; t += blockDim.x) swc[t] = mlp[S::oCW0 + t];
+  const T* sw = swc - S::oCW0;              // so that sw[S::oC*] addresses swc
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   T* rows = sm + (size_t)wid * 32 * R::ROW;
   T* myrow = rows + (size_t)lane * R::ROW;
@@ -1101,82 +1098,77 @@ __global__ void __launch_bounds__(WARPS * 32) k_bwd_color(Ws<T> w, Geo G, int M,
   for (int i = 0; i < R::A0; ++i) acc0[i] = T(0);
 #pragma unroll
   for (int i = 0; i <= GSB_HID; ++i) acc1[i] = T(0);
+  __syncthreads();
   const int64_t nwarps = (int64_t)gridDim.x * WARPS;
   for (int64_t base = ((int64_t)blockIdx.x * WARPS + wid) * 32; base < NS; base += nwarps * 32) {
     const int64_t s = base + lane;
     const bool active = s < NS;
     if (active) {
-      int ray = (int)(s / N);
-      T d = (T)dep[(int64_t)ray * w.ld + (int)(s % N)];
+      const int ray = (int)((uint32_t)s / (uint32_t)N);
       T pt[3];
+      taped_point<T>(w.o + ray * 3, w.r + ray * 3,
+                     dep[(int64_t)ray * w.ld + (int)((uint32_t)s % (uint32_t)N)], G.lo, G.hi, pt);
+      const LocT<T> q =
+          compact<T>(locate<false>(G.col, (double)pt[0], (double)pt[1], (double)pt[2], nullptr));
+      {
+        T f[S::CC];
+        gather_fast<T, S::CC>(G.col, q, f);
 #pragma unroll
-      for (int a = 0; a < 3; ++a) {
-        T x = w.o[ray * 3 + a] + d * w.r[ray * 3 + a];
-        T lo = (T)G.lo[a], hi = (T)G.hi[a];
-        x = x >= lo ? x : lo;
-        x = x <= hi ? x : hi;
-        pt[a] = x;
+        for (int c = 0; c < S::CC; ++c) myrow[R::oA0 + c] = f[c];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) myrow[R::oA0 + S::CC + a] = w.r[ray * 3 + a];
+        myrow[R::oA0 + S::IN_C] = T(1);
+#pragma unroll
+        for (int i = S::IN_C + 1; i < R::A0P; ++i) myrow[R::oA0 + i] = T(0);
       }
-      Loc q = locate<false>(G.col, (double)pt[0], (double)pt[1], (double)pt[2], nullptr);
-      T inp[S::IN_C];
-      gather_level<T, S::CC, false>(G.col, q, inp);
-#pragma unroll
-      for (int a = 0; a < 3; ++a) inp[S::CC + a] = w.r[ray * 3 + a];
-      T h0[GSB_HID], h1[GSB_HID], y[3];
       uint32_t m0, m1;
-      color_mlp<T, S>(inp, h0, h1, m0, m1, y);
       T yb[3];
+      {
+        T h[GSB_HID];
+        dense_f_row<T, S::IN_C>(sw + S::oCW0, myrow + R::oA0, h);
+        add_bias(sw + S::oCb0, h);
+        m0 = relu_mask(h);
+        store32(myrow + R::oA1, h);
+        myrow[R::oA1 + GSB_HID] = T(1);
 #pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        T cc = sigmoid_raw(y[c]);
-        yb[c] = w.cbar[s * 3 + c] * (cc * (T(1) - cc));
-        myrow[R::oY + c] = yb[c];
+        for (int i = GSB_HID + 1; i < R::A1P; ++i) myrow[R::oA1 + i] = T(0);
+        dense_f_row<T, GSB_HID>(sw + S::oCW1, myrow + R::oA1, h);
+        add_bias(sw + S::oCb1, h);
+        m1 = relu_mask(h);
+        store32(myrow + R::oH1, h);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          T a = T(0);
+#pragma unroll
+          for (int j = 0; j < GSB_HID; ++j) a = fma(h[j], sw[S::oCW2 + j * 3 + c], a);
+          const T cc = sigmoid_fast(a + sw[S::oCb2 + c]);
+          yb[c] = w.cbar[s * 3 + c] * (cc * (T(1) - cc));
+          myrow[R::oY + c] = yb[c];
+        }
+        myrow[R::oY + 3] = T(0);
       }
-#pragma unroll
-      for (int i = 0; i < S::IN_C; ++i) myrow[R::oA0 + i] = inp[i];
-      myrow[R::oA0 + S::IN_C] = T(1);
-#pragma unroll
-      for (int j = 0; j < GSB_HID; ++j) {
-        myrow[R::oA1 + j] = h0[j];
-        myrow[R::oH1 + j] = h1[j];
-      }
-      myrow[R::oA1 + GSB_HID] = T(1);
       T a1b[GSB_HID];
 #pragma unroll
       for (int j = 0; j < GSB_HID; ++j) {
         T a = T(0);
 #pragma unroll
-        for (int c = 0; c < 3; ++c) a = fma(cw<T>(S::oCW2 + j * 3 + c), yb[c], a);
+        for (int c = 0; c < 3; ++c) a = fma(sw[S::oCW2 + j * 3 + c], yb[c], a);
         a1b[j] = ((m1 >> j) & 1u) ? a : T(0);
-        myrow[R::oB1 + j] = a1b[j];
       }
-      T a0b[GSB_HID];
-#pragma unroll
-      for (int i = 0; i < GSB_HID; ++i) {
-        T a = T(0);
-#pragma unroll
-        for (int j = 0; j < GSB_HID; ++j) a = fma(cw<T>(S::oCW1 + i * GSB_HID + j), a1b[j], a);
-        a0b[i] = ((m0 >> i) & 1u) ? a : T(0);
-        myrow[R::oB0 + i] = a0b[i];
-      }
+      store32(myrow + R::oB1, a1b);
+      dense_d_row<T, GSB_HID>(sw + S::oCW1, a1b, m0, myrow + R::oB0);
+      load32(myrow + R::oB0, a1b);  // a0_bar
       T fb[S::CC];
-#pragma unroll
-      for (int c = 0; c < S::CC; ++c) {
-        T a = T(0);
-#pragma unroll
-        for (int i = 0; i < GSB_HID; ++i) a = fma(cw<T>(S::oCW0 + c * GSB_HID + i), a0b[i], a);
-        fb[c] = a;
-      }
+      dense_d_reg<T, S::CC>(sw + S::oCW0, a1b, fb);
       // colour grid scatter: theta_c[idx_k] += w_k f_bar
-      T x1 = (T)q.fx, y1 = (T)q.fy, z1 = (T)q.fz;
-      T x0 = (T)(1.0 - q.fx), y0 = (T)(1.0 - q.fy), z0 = (T)(1.0 - q.fz);
-      T* Gp = reinterpret_cast<T*>(G.col.grad) + q.base * S::CC;
+      T wk[8];
+      corner_w(q, wk);
+      T* Gp = reinterpret_cast<T*>(G.col.grad) + (int64_t)q.base * S::CC;
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
-        T wk = ((((k >> 2) & 1) ? x1 : x0) * (((k >> 1) & 1) ? y1 : y0)) * ((k & 1) ? z1 : z0);
         T vv[S::CC];
 #pragma unroll
-        for (int c = 0; c < S::CC; ++c) vv[c] = wk * fb[c];
+        for (int c = 0; c < S::CC; ++c) vv[c] = wk[k] * fb[c];
         red_row<T, S::CC>(Gp + corner_off(G.col, k) * S::CC, vv);
       }
     } else {
@@ -1184,17 +1176,18 @@ __global__ void __launch_bounds__(WARPS * 32) k_bwd_color(Ws<T> w, Geo G, int M,
       for (int i = 0; i < R::ROW; ++i) myrow[i] = T(0);
     }
     __syncwarp();
+    warp_outer<T, R::A0, R::A0P, GSB_HID + 1, R::A1P>(rows, R::ROW, R::oA0, R::oB0, R::oA1, R::oB1,
+                                                      lane, acc0, acc1);
 #pragma unroll 1
     for (int r = 0; r < 32; ++r) {
       const T* rw = rows + (size_t)r * R::ROW;
-      T b0 = rw[R::oB0 + lane], b1 = rw[R::oB1 + lane], hj = rw[R::oH1 + lane];
-#pragma unroll
-      for (int i = 0; i < R::A0; ++i) acc0[i] = fma(rw[R::oA0 + i], b0, acc0[i]);
-#pragma unroll
-      for (int i = 0; i <= GSB_HID; ++i) acc1[i] = fma(rw[R::oA1 + i], b1, acc1[i]);
-#pragma unroll
-      for (int c = 0; c < 3; ++c) acc2[c] = fma(hj, rw[R::oY + c], acc2[c]);
-      if (lane < 3) accb2 += rw[R::oY + lane];
+      const T hj = rw[R::oH1 + lane];
+      T y0, y1, y2, y3;
+      lds4(rw + R::oY, y0, y1, y2, y3);
+      acc2[0] = fma(hj, y0, acc2[0]);
+      acc2[1] = fma(hj, y1, acc2[1]);
+      acc2[2] = fma(hj, y2, acc2[2]);
+      accb2 += lane == 0 ? y0 : (lane == 1 ? y1 : (lane == 2 ? y2 : T(0)));
     }
     __syncwarp();
   }

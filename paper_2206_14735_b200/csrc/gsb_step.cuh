@@ -25,13 +25,9 @@ int run_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step
   Geo G = geo_of(model, esz);
   T* params = reinterpret_cast<T*>(model->params);
   T* grads = reinterpret_cast<T*>(model->grads);
-  const T* mlp_src = params + model->mlp_offset;
-  if (std::is_same<T, float>::value)
-    GSB_CHECK(cudaMemcpyToSymbolAsync(c_mlp_f, mlp_src, S::NMLP * esz, 0,
-                                      cudaMemcpyDeviceToDevice, stream));
-  else
-    GSB_CHECK(cudaMemcpyToSymbolAsync(c_mlp_d, mlp_src, S::NMLP * esz, 0,
-                                      cudaMemcpyDeviceToDevice, stream));
+  const T* mlp = params + model->mlp_offset;  // staged into shared memory by each CTA
+  const size_t smem_sdf = (size_t)S::NG * esz;
+  const size_t smem_fwd = ((size_t)(S::NMLP + 3) / 4 * 4 + 128 * FwdRow<T, S>::ROW) * esz;
   const int M = z.M, N = z.N, Nc = st->n_coarse, A = st->n_add, R = st->n_rounds;
   const int nsp = 2 * z.S;
   double* dep_final = w.dep[R % 2];
@@ -45,8 +41,8 @@ int run_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step
     if (R > 0) {
       int64_t n0 = (int64_t)M * Nc;
       int blocks = (int)((n0 + 127) / 128);
-      k_sdf_eval<T, S, false><<<blocks, 128, 0, stream>>>(w, G, M, Nc, w.dep[0], w.phi[0],
-                                                            nullptr, nullptr);
+      k_sdf_eval<T, S, false><<<blocks, 128, smem_sdf, stream>>>(w, G, M, Nc, w.dep[0], w.phi[0],
+                                                                   nullptr, nullptr, mlp);
       GSB_LAUNCHED();
       int cur = 0, K = Nc;
       for (int rnd = 0; rnd < R; ++rnd) {
@@ -59,8 +55,8 @@ int run_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step
         if (need_phi) {
           int64_t cap = (int64_t)M * A;
           int b2 = (int)((cap + 127) / 128);
-          k_sdf_eval<T, S, false><<<b2, 128, 0, stream>>>(w, G, M, Nc, w.dep[1 - cur],
-                                                            w.phi[1 - cur], w.evl, w.evl_count);
+          k_sdf_eval<T, S, false><<<b2, 128, smem_sdf, stream>>>(
+              w, G, M, Nc, w.dep[1 - cur], w.phi[1 - cur], w.evl, w.evl_count, mlp);
           GSB_LAUNCHED();
         }
         cur = 1 - cur;
@@ -74,7 +70,9 @@ int run_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step
     const T* spts = reinterpret_cast<const T*>(st->smooth_pts);
     int64_t ns = z.NS;
     int fb = (int)((ns + 127) / 128);
-    k_fwd<T, S, false><<<fb, 128, 0, stream>>>(w, G, M, N, dep_final, spts, nsp);
+    GSB_CHECK(cudaFuncSetAttribute(k_fwd<T, S, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)smem_fwd));
+    k_fwd<T, S, false><<<fb, 128, smem_fwd, stream>>>(w, G, M, N, dep_final, spts, nsp, mlp);
     GSB_LAUNCHED();
     LossW L;
     L.rgb = st->w_rgb;
@@ -97,8 +95,9 @@ int run_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step
     GSB_LAUNCHED();
     // backward kernels: persistent grids
     constexpr int WG = sizeof(T) == 4 ? 4 : 2;
-    size_t smem_g = (size_t)WG * 32 * GeoRow<T, S>::ROW * sizeof(T);
-    size_t smem_c = (size_t)WG * 32 * ColRow<T, S>::ROW * sizeof(T);
+    constexpr int CW = S::NMLP - S::oCW0;
+    size_t smem_g = ((size_t)(S::NG + 3) / 4 * 4 + (size_t)WG * 32 * GeoRow<T, S>::ROW) * sizeof(T);
+    size_t smem_c = ((size_t)(CW + 3) / 4 * 4 + (size_t)WG * 32 * ColRow<T, S>::ROW) * sizeof(T);
     GSB_CHECK(cudaFuncSetAttribute(k_bwd_geom<T, S, WG>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_g));
     GSB_CHECK(cudaFuncSetAttribute(k_bwd_color<T, S, WG>,
@@ -109,9 +108,9 @@ int run_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step
     nb_geo = std::max(1, std::min(nb_geo, kNbMax));
     nb_col = std::max(1, std::min(nb_col, kNbMax));
     k_bwd_geom<T, S, WG><<<nb_geo, per_cta, smem_g, stream>>>(w, G, M, N, dep_final, spts, nsp,
-                                                             2);
+                                                             2, mlp);
     GSB_LAUNCHED();
-    k_bwd_color<T, S, WG><<<nb_col, per_cta, smem_c, stream>>>(w, G, M, N, dep_final);
+    k_bwd_color<T, S, WG><<<nb_col, per_cta, smem_c, stream>>>(w, G, M, N, dep_final, mlp);
     GSB_LAUNCHED();
     k_finalize_mlp<T, S><<<(S::NMLP + 255) / 256, 256, 0, stream>>>(w, grads, model->mlp_offset,
                                                                     nb_geo, nb_col);
