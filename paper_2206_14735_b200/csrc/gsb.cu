@@ -21,20 +21,6 @@ GSB_DECL(gsb_step_d222)
 namespace gsb_abi {
 
 // twin: explicit uniforms / outputs
-__global__ void k_importance_twin(int M, int K, int A, int ld, const double* dep, const double* phi,
-                                  const double* win, double s, const double* nearv,
-                                  const double* farv, const double* uni, gsb_pcg64_t rng,
-                                  int use_rng, double* out, int32_t* src, double* wts) {
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= M) return;
-  Pcg g;
-  g.init(rng);
-  if (use_rng) g.advance((uint64_t)i * (uint64_t)A);
-  importance_row(K, A, dep + (int64_t)i * ld, phi ? phi + (int64_t)i * ld : nullptr,
-                 win ? win + (int64_t)i * ld : nullptr, s, nearv[i], farv[i], &g,
-                 use_rng ? nullptr : uni + (int64_t)i * A, out + (int64_t)i * ld,
-                 src + (int64_t)i * ld, wts ? wts + (int64_t)i * ld : nullptr);
-}
 
 template <typename T>
 int dispatch_shape(const gsb_model_t* m, const gsb_dataset_t* d, const gsb_step_t* st,
@@ -142,14 +128,23 @@ int gsb_adam_step(int32_t precision, void* params, void* grads, void* m, void* v
     sg.lr[i] = seg_lr_host[i];
   }
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  AdamConst k;
+  k.b1 = beta1;
+  k.b2 = beta2;
+  k.eps = eps;
+  k.c1 = c1;
+  k.c2 = c2;
+  k.ib1 = 1.0 - beta1;  // same rounding as numba's (1.0 - b1)
+  k.ib2 = 1.0 - beta2;
+  k.inv_c1 = 1.0 / c1;
+  k.inv_c2 = 1.0 / c2;
   int blocks = num_sms() * 8;
   if (precision == 0)
     k_adam<float><<<blocks, 256, 0, s>>>((float*)params, (float*)grads, (float*)m, (float*)v, n, sg,
-                                         beta1, beta2, eps, c1, c2, guard, guard_threshold, status);
+                                         k, guard, guard_threshold, status);
   else
     k_adam<double><<<blocks, 256, 0, s>>>((double*)params, (double*)grads, (double*)m, (double*)v,
-                                          n, sg, beta1, beta2, eps, c1, c2, guard,
-                                          guard_threshold, status);
+                                          n, sg, k, guard, guard_threshold, status);
   GSB_LAUNCHED();
   return GSB_OK;
 }
@@ -324,7 +319,7 @@ int gsb_importance_round(int32_t n, int32_t K, int32_t A, int32_t ld, const doub
   if (n == 0) return GSB_OK;
   gsb_pcg64_t g = {0, 0, 0, 0};
   if (rng) g = *rng;
-  k_importance_twin<<<(n + 63) / 64, 64, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+  k_importance_twin<<<(n + 3) / 4, 128, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
       n, K, A, ld, depths, phi, nullptr, s, nearv, farv, uniforms, g, uniforms ? 0 : 1, depths_out,
       src_out, weights_out);
   GSB_LAUNCHED();
@@ -340,7 +335,7 @@ int gsb_importance_refine(int32_t n, int32_t K, int32_t A, int32_t ld, const dou
     return GSB_E_ARG;
   if (n == 0) return GSB_OK;
   gsb_pcg64_t g = {0, 0, 0, 0};
-  k_importance_twin<<<(n + 63) / 64, 64, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+  k_importance_twin<<<(n + 3) / 4, 128, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
       n, K, A, ld, depths, nullptr, weights, 0.0, nearv, farv, uniforms, g, 0, depths_out,
       src_out, nullptr);
   GSB_LAUNCHED();

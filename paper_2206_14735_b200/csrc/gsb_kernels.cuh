@@ -332,53 +332,93 @@ static __device__ void separation_fallback(double* row, int32_t* src, int k) {
   }
 }
 
-static __device__ void importance_row(int K, int A, const double* d, const double* ph,
-                                      const double* win, double s, double nearv, double farv,
-                                      Pcg* g, const double* uni, double* out, int32_t* src,
-                                      double* wout) {
+// ---------------------------------------------------------------------------
+// one importance round, one warp per ray (render_weights_data +
+// importance_refine_with_sources + enforce_separation, gs/renderer.py:162-173,
+// gs/sampler.py:128-197).  The two float64 recurrences (cumprod of the
+// transmittance, cumsum of the CDF) run serially on lane 0 so they round
+// exactly like numpy; everything else is lane-parallel: sigmoid ratios,
+// CDF normalisation, inverse-CDF draws, the stable merge (by rank), the
+// separation test and provenance.
+
+struct ImpSmem {
+  double om[GSB_KMAX];
   double cdf[GSB_KMAX];
-  double c = 0.0;
-  if (win) {  // weights given (importance_refine_with_sources signature)
-    for (int i = 0; i < K - 1; ++i) {
-      c = (i == 0) ? win[i] : c + win[i];
-      cdf[i] = c;
+  double out[GSB_KMAX];
+  double nw[GSB_AMAX];
+  int32_t src[GSB_KMAX];
+};
+
+// d, ph: (K) input row; win: optional given weights (K); uni: optional
+// uniforms (A) else PCG64 advanced to row*A; writes out/src (K+A) in smem.
+static __device__ void importance_warp(ImpSmem& S, int K, int A, const double* __restrict__ d,
+                                const double* __restrict__ ph, const double* __restrict__ win,
+                                double s, double nearv, double farv, const gsb_pcg64_t& rng,
+                                uint64_t row, const double* __restrict__ uni,
+                                double* __restrict__ wout) {
+  const int lane = threadIdx.x & 31;
+  const unsigned full = 0xffffffffu;
+  double total;
+  if (win) {
+    if (lane == 0) {
+      double c = 0.0;
+      for (int i = 0; i < K - 1; ++i) {
+        c = (i == 0) ? win[i] : c + win[i];
+        S.cdf[i] = c;
+      }
+      total = c;
     }
   } else {
-    // render_weights_data (gs/renderer.py:162-173), sequential cumprod
-    double sig_i = sigmoid_raw(s * ph[0]);
-    double trans = 1.0;
-    for (int i = 0; i < K - 1; ++i) {
-      double sig_n = sigmoid_raw(s * ph[i + 1]);
-      double den = sig_i >= 1e-12 ? sig_i : 1e-12;
-      double ratio = sig_n / den;
-      double om = ratio <= 1.0 ? ratio : 1.0;
-      double wi = trans * (1.0 - om);
-      if (wout) wout[i] = wi;
-      c = (i == 0) ? wi : c + wi;
-      cdf[i] = c;
-      trans = trans * om;
-      sig_i = sig_n;
+    // om_i = min(sig_{i+1} / max(sig_i, 1e-12), 1)
+    for (int i = lane; i < K; i += 32) S.out[i] = sigmoid_raw(s * ph[i]);
+    __syncwarp();
+    for (int i = lane; i < K - 1; i += 32) {
+      const double den = S.out[i] >= 1e-12 ? S.out[i] : 1e-12;
+      const double ratio = S.out[i + 1] / den;
+      S.om[i] = ratio <= 1.0 ? ratio : 1.0;
     }
-    if (wout) wout[K - 1] = trans * (1.0 - 1.0);
+    __syncwarp();
+    if (lane == 0) {  // sequential cumprod / cumsum, as numpy
+      double trans = 1.0, c = 0.0;
+      for (int i = 0; i < K - 1; ++i) {
+        const double wi = trans * (1.0 - S.om[i]);
+        if (wout) wout[i] = wi;
+        c = (i == 0) ? wi : c + wi;
+        S.cdf[i] = c;
+        trans = trans * S.om[i];
+      }
+      if (wout) wout[K - 1] = trans * (1.0 - 1.0);
+      total = c;
+    }
   }
-  // importance_refine_with_sources (gs/sampler.py:128-169)
-  bool dead = c <= 0.0;
+  total = __shfl_sync(full, total, 0);
+  __syncwarp();
+  const bool dead = total <= 0.0;
   if (dead)
-    for (int i = 0; i < K - 1; ++i) cdf[i] = (double)(i + 1);
-  double last = cdf[K - 2];
-  for (int i = 0; i < K - 1; ++i) cdf[i] = cdf[i] / last;
-  double nw[GSB_AMAX];
-  int ord[GSB_AMAX];
-  for (int a = 0; a < A; ++a) {
-    double u = uni ? uni[a] : g->next_double();
-    // idx = #(cdf <= u), cdf non-decreasing -> upper bound
-    int lo = 0, hi = K - 1;
-    while (lo < hi) {
-      int mid = (lo + hi) >> 1;
-      if (cdf[mid] <= u) lo = mid + 1; else hi = mid;
+    for (int i = lane; i < K - 1; i += 32) S.cdf[i] = (double)(i + 1);
+  __syncwarp();
+  const double last = S.cdf[K - 2];
+  __syncwarp();
+  for (int i = lane; i < K - 1; i += 32) S.cdf[i] = S.cdf[i] / last;
+  __syncwarp();
+  // inverse-CDF draws, lane a < A
+  if (lane < A) {
+    double u;
+    if (uni) {
+      u = uni[lane];
+    } else {
+      Pcg g;
+      g.init(rng);
+      g.advance(row * (uint64_t)A + (uint64_t)lane);
+      u = g.next_double();
     }
-    int idx = lo < K - 2 ? lo : K - 2;
-    double clo = idx > 0 ? cdf[idx - 1] : 0.0, chi = cdf[idx];
+    int lo = 0, hi = K - 1;  // idx = #(cdf <= u): upper bound on a non-decreasing array
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (S.cdf[mid] <= u) lo = mid + 1; else hi = mid;
+    }
+    const int idx = lo < K - 2 ? lo : K - 2;
+    const double clo = idx > 0 ? S.cdf[idx - 1] : 0.0, chi = S.cdf[idx];
     double frac;
     if (chi > clo) {
       double den = chi - clo;
@@ -389,85 +429,127 @@ static __device__ void importance_row(int K, int A, const double* d, const doubl
     }
     double v = d[idx] + frac * (d[idx + 1] - d[idx]);
     if (dead) v = nearv + u * (farv - nearv);
-    nw[a] = v;
-    // stable insertion of a into ord by value
-    int t = a;
-    while (t > 0 && nw[ord[t - 1]] > v) {
-      ord[t] = ord[t - 1];
-      --t;
-    }
-    ord[t] = a;
+    S.nw[lane] = v;
   }
+  __syncwarp();
   // stable merge (np.argsort kind="stable": old columns precede new on ties)
   bool sorted = true;
-  for (int i = 0; i + 1 < K; ++i)
+  for (int i = lane; i + 1 < K; i += 32)
     if (!(d[i] <= d[i + 1])) sorted = false;
-  int n = K + A;
+  sorted = __all_sync(full, sorted);
+  const int n = K + A;
   if (sorted) {
-    int i = 0, a = 0, o = 0;
-    while (i < K || a < A) {
-      if (a >= A || (i < K && !(nw[ord[a]] < d[i]))) {
-        out[o] = d[i];
-        src[o++] = i++;
-      } else {
-        out[o] = nw[ord[a]];
-        src[o++] = -1;
-        ++a;
-      }
+    for (int i = lane; i < K; i += 32) {
+      const double di = d[i];
+      int c = 0;
+      for (int a = 0; a < A; ++a) c += S.nw[a] < di;
+      S.out[i + c] = di;
+      S.src[i + c] = i;
     }
-  } else {  // general stable insertion sort over the concatenation
+    if (lane < A) {
+      const double v = S.nw[lane];
+      int lo = 0, hi = K;  // #(old <= v)
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (d[mid] <= v) lo = mid + 1; else hi = mid;
+      }
+      int r = 0;
+      for (int b = 0; b < A; ++b) r += (S.nw[b] < v) || (S.nw[b] == v && b < lane);
+      S.out[lo + r] = v;
+      S.src[lo + r] = -1;
+    }
+  } else if (lane == 0) {  // general stable insertion sort (unsorted input rows)
     for (int t = 0; t < n; ++t) {
-      double v = t < K ? d[t] : nw[t - K];
-      int sv = t < K ? t : -1;
+      const double v = t < K ? d[t] : S.nw[t - K];
+      const int sv = t < K ? t : -1;
       int q = t;
-      while (q > 0 && out[q - 1] > v) {
-        out[q] = out[q - 1];
-        src[q] = src[q - 1];
+      while (q > 0 && S.out[q - 1] > v) {
+        S.out[q] = S.out[q - 1];
+        S.src[q] = S.src[q - 1];
         --q;
       }
-      out[q] = v;
-      src[q] = sv;
+      S.out[q] = v;
+      S.src[q] = sv;
     }
   }
+  __syncwarp();
   bool bad = false;
-  for (int i = 0; i + 1 < n; ++i)
-    if (out[i + 1] - out[i] < 1e-9) bad = true;
-  if (bad) separation_fallback(out, src, n);
+  for (int i = lane; i + 1 < n; i += 32)
+    if (S.out[i + 1] - S.out[i] < 1e-9) bad = true;
+  if (__any_sync(full, bad) && lane == 0) separation_fallback(S.out, S.src, n);
+  __syncwarp();
 }
 
 template <typename T>
-__global__ void k_importance_dev(Ws<T> w, int M, int K, int A, int ray_base,
-                                 const double* __restrict__ dep, const double* __restrict__ phi,
-                                 double* __restrict__ dep_out, double* __restrict__ phi_out,
-                                 const T* __restrict__ log_s, gsb_pcg64_t rng,
-                             int32_t* __restrict__ evl, int32_t* __restrict__ evl_count,
-                             int64_t cap, int want_list) {
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= M) return;
+__global__ void __launch_bounds__(128) k_importance_dev(Ws<T> w, int M, int K, int A, int ray_base,
+                                                        const double* __restrict__ dep,
+                                                        const double* __restrict__ phi,
+                                                        double* __restrict__ dep_out,
+                                                        double* __restrict__ phi_out,
+                                                        const T* __restrict__ log_s,
+                                                        gsb_pcg64_t rng, int32_t* __restrict__ evl,
+                                                        int32_t* __restrict__ evl_count, int64_t cap,
+                                                        int want_list) {
+  __shared__ ImpSmem smem[4];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int i = blockIdx.x * 4 + wid;
+  if (i >= M) return;  // warp-uniform
+  ImpSmem& S = smem[wid];
   // ModelState.s_value() = float(np.exp(log_s)) in the model dtype
   const double s = (double)exp(log_s[0]);
-  Pcg g;
-  g.init(rng);
-  g.advance((uint64_t)(ray_base + i) * (uint64_t)A);
   const double* d = dep + (int64_t)i * w.ld;
   const double* ph = phi + (int64_t)i * w.ld;
+  importance_warp(S, K, A, d, ph, nullptr, s, w.nearv[i], w.farv[i], rng,
+                  (uint64_t)(ray_base + i), nullptr, nullptr);
+  const int n = K + A;
   double* out = dep_out + (int64_t)i * w.ld;
-  int32_t src[GSB_KMAX];
-  importance_row(K, A, d, ph, nullptr, s, w.nearv[i], w.farv[i], &g, nullptr, out, src, nullptr);
   double* po = phi_out + (int64_t)i * w.ld;
   int nnew = 0;
-  for (int t = 0; t < K + A; ++t) {
-    if (src[t] >= 0) po[t] = ph[src[t]];
+  for (int t = lane; t < n; t += 32) {
+    out[t] = S.out[t];
+    const int sv = S.src[t];
+    if (sv >= 0) po[t] = ph[sv];
     else ++nnew;
   }
   if (!want_list) return;
-  int base = atomicAdd(evl_count, nnew);
-  if (base + nnew > cap) {
-    atomicOr(w.status + GSB_ST_OVERFLOW, 1);
+  const int tot = warp_sum(nnew);
+  int base = 0;
+  if (lane == 0) base = atomicAdd(evl_count, tot);
+  base = __shfl_sync(0xffffffffu, base, 0);
+  if (base + tot > cap) {
+    if (lane == 0) atomicOr(w.status + GSB_ST_OVERFLOW, 1);
     return;
   }
-  for (int t = 0; t < K + A; ++t)
-    if (src[t] < 0) evl[base++] = i * GSB_KMAX + t;
+  // compact the new slots in order
+  for (int t0 = 0; t0 < n; t0 += 32) {
+    const int t = t0 + lane;
+    const bool isnew = t < n && S.src[t] < 0;
+    const unsigned bal = __ballot_sync(0xffffffffu, isnew);
+    if (isnew) evl[base + __popc(bal & ((1u << lane) - 1u))] = i * GSB_KMAX + t;
+    base += __popc(bal);
+  }
+}
+
+// twin: explicit weights or phi, explicit uniforms or generator; one warp per row
+static __global__ void __launch_bounds__(128) k_importance_twin(int M, int K, int A, int ld,
+                                                         const double* dep, const double* phi,
+                                                         const double* win, double s,
+                                                         const double* nearv, const double* farv,
+                                                         const double* uni, gsb_pcg64_t rng,
+                                                         int use_rng, double* out, int32_t* src,
+                                                         double* wts) {
+  __shared__ ImpSmem smem[4];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int i = blockIdx.x * 4 + wid;
+  if (i >= M) return;
+  ImpSmem& S = smem[wid];
+  importance_warp(S, K, A, dep + (int64_t)i * ld, phi ? phi + (int64_t)i * ld : nullptr,
+                  win ? win + (int64_t)i * ld : nullptr, s, nearv[i], farv[i], rng, (uint64_t)i,
+                  use_rng ? nullptr : uni + (int64_t)i * A, wts ? wts + (int64_t)i * ld : nullptr);
+  for (int t = lane; t < K + A; t += 32) {
+    out[(int64_t)i * ld + t] = S.out[t];
+    src[(int64_t)i * ld + t] = S.src[t];
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -635,175 +717,221 @@ struct LossW {
   double rgb, depth, sdf, fs, eik, smooth, trunc, alpha, m_global, smooth_global;
 };
 
+// ---------------------------------------------------------------------------
+// rendering + losses + per-sample adjoints, one warp per ray
+// (gs/renderer.py:112-159 alphas/composite, :372-414 losses)
+
 template <typename T>
-__global__ void __launch_bounds__(64) k_render(Ws<T> w, int M, int N, const double* __restrict__ dep,
-                                               const T* __restrict__ params, int64_t log_s_off,
-                                               LossW L) {
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= M) return;
+__device__ __forceinline__ T warp_incl_scan(T x) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const T y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  return x;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_allsum(T v) {
+  return warp_sum(v);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(128) k_render(Ws<T> w, int M, int N, const double* __restrict__ dep,
+                                                const T* __restrict__ params, int64_t log_s_off,
+                                                LossW L) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  T* sig = reinterpret_cast<T*>(smem_raw) + (size_t)wid * 4 * N;
+  T* trn = sig + N;
+  T* xb = trn + N;
+  T* yb = xb + N;
+  const int ray = blockIdx.x * (blockDim.x >> 5) + wid;
+  if (ray >= M) return;  // warp-uniform
   const T s = exp(params[log_s_off]);  // ModelState.s_tensor (gs/renderer.py:83-84)
   const T SF = (T)1e-12, TF = (T)1e-15;
-  T sig[GSB_KMAX], trn[GSB_KMAX];
-  const int64_t s0 = (int64_t)i * N;
-  const double* d = dep + (int64_t)i * w.ld;
-  // ---- forward: alphas (:112-134) + composite (:137-159)
-  for (int j = 0; j < N; ++j) sig[j] = sigmoid_raw(w.sphi[s0 + j] * s);
-  T logt = T(0), ch[3] = {T(0), T(0), T(0)}, dh = T(0);
-  for (int j = 0; j < N; ++j) {
-    T al = T(0);
+  const int64_t s0 = (int64_t)ray * N;
+  const double* d = dep + (int64_t)ray * w.ld;
+  for (int j = lane; j < N; j += 32) sig[j] = sigmoid_raw(w.sphi[s0 + j] * s);
+  __syncwarp();
+  // ---- forward: alphas, transmittance (exclusive scan of log(1 - alpha)), composite
+  T carry = T(0), ch0 = T(0), ch1 = T(0), ch2 = T(0), dh = T(0);
+  for (int j0 = 0; j0 < N; j0 += 32) {
+    const int j = j0 + lane;
+    T al = T(0), Lj = T(0);
     if (j < N - 1) {
-      T den = sig[j] >= SF ? sig[j] : SF;
-      T ratio = sig[j + 1] / den;
+      const T den = sig[j] >= SF ? sig[j] : SF;
+      const T ratio = sig[j + 1] / den;
       al = T(1) - (ratio <= T(1) ? ratio : T(1));
     }
-    T om = T(1) - al;
-    T Tj = j == 0 ? T(1) : exp(logt);
-    trn[j] = Tj;
-    logt += log(om >= TF ? om : TF);
-    T wj = Tj * al;
-    w.wts[s0 + j] = wj;
-#pragma unroll
-    for (int c = 0; c < 3; ++c) ch[c] += wj * w.scol[(s0 + j) * 3 + c];
-    dh += wj * (T)d[j];
+    if (j < N) {
+      const T om = T(1) - al;
+      Lj = log(om >= TF ? om : TF);
+    }
+    const T incl = warp_incl_scan(Lj);
+    const T Tj = (j == 0) ? T(1) : exp(carry + (incl - Lj));
+    carry += __shfl_sync(0xffffffffu, incl, 31);
+    if (j < N) {
+      trn[j] = Tj;
+      const T wj = Tj * al;
+      w.wts[s0 + j] = wj;
+      const T* cj = w.scol + (s0 + j) * 3;
+      ch0 = fma(wj, cj[0], ch0);
+      ch1 = fma(wj, cj[1], ch1);
+      ch2 = fma(wj, cj[2], ch2);
+      dh = fma(wj, (T)d[j], dh);
+    }
   }
-  // ---- losses (:372-414)
-  const int valid = w.valid[i];
-  const double D = w.dray[i];
-  T err[3], q = T(0);
-#pragma unroll
-  for (int c = 0; c < 3; ++c) {
-    err[c] = ch[c] - w.col[i * 3 + c];
-    q += err[c] * err[c];
-  }
-  T lrgb = sqrt(q + (T)1e-24);
-  T dT = (T)D;
-  T lde = valid ? fabs(dh - dT) : T(0);
+  ch0 = warp_sum(ch0);
+  ch1 = warp_sum(ch1);
+  ch2 = warp_sum(ch2);
+  dh = warp_sum(dh);
+  // ---- losses
+  const int valid = w.valid[ray];
+  const double D = w.dray[ray];
+  const T err0 = ch0 - w.col[ray * 3], err1 = ch1 - w.col[ray * 3 + 1], err2 = ch2 - w.col[ray * 3 + 2];
+  const T lrgb = sqrt(((err0 * err0 + err1 * err1) + err2 * err2) + (T)1e-24);
+  const T dT = (T)D;
+  const T lde = valid ? fabs(dh - dT) : T(0);
   const long long nvalid = w.counts[GSB_C_VALID];
   const long long neik = w.counts[GSB_C_EIK];
   const T inv_nv = T(1) / (T)(nvalid > 1 ? nvalid : 1);
   const T inv_ne = T(1) / (T)(neik > 1 ? neik : 1);
-  const T ntr = (T)max(w.cnt[i * 3 + 0], 1), nfs = (T)max(w.cnt[i * 3 + 1], 1);
-  const T tr_t = (T)L.trunc;
+  const T ntr = (T)max(w.cnt[ray * 3 + 0], 1), nfs = (T)max(w.cnt[ray * 3 + 1], 1);
+  const T alpha = (T)(-L.alpha);
   T sdf = T(0), fsv = T(0), eik = T(0);
-  for (int j = 0; j < N; ++j) {
-    double b = D - d[j];
-    T bc = (T)b, ph = w.sphi[s0 + j];
-    bool tr = valid && fabs(b) <= L.trunc;
-    bool fs = valid && b > L.trunc;
-    bool bh = valid && b < -L.trunc;
+  for (int j = lane; j < N; j += 32) {
+    const double b = D - d[j];
+    const T bc = (T)b, ph = w.sphi[s0 + j];
+    const bool tr = valid && fabs(b) <= L.trunc;
+    const bool fs = valid && b > L.trunc;
+    const bool bh = valid && b < -L.trunc;
     if (tr) sdf += fabs(ph - bc);
     if (fs) {
-      T e = exp(ph * (T)(-L.alpha));
+      const T e = exp(ph * alpha);
       T inner = e - T(1);
       inner = T(0) >= inner ? T(0) : inner;
-      T lin = ph - bc;
+      const T lin = ph - bc;
       fsv += inner >= lin ? inner : lin;
     }
     if (fs || bh || !valid) {
       const T* gp = w.sgphi + (s0 + j) * 3;
-      T nn = sqrt((gp[0] * gp[0] + gp[1] * gp[1]) + gp[2] * gp[2] + (T)1e-20);
-      T df = T(1) - nn;
+      const T nn = sqrt(((gp[0] * gp[0] + gp[1] * gp[1]) + gp[2] * gp[2]) + (T)1e-20);
+      const T df = T(1) - nn;
       eik += df * df;
     }
   }
-  (void)tr_t;
-  double* part = w.ray_part + (int64_t)i * 8;
-  part[0] = (double)lrgb;
-  part[1] = (double)lde;
-  part[2] = (double)(sdf / ntr);
-  part[3] = (double)(fsv / nfs);
-  part[4] = (double)eik;
-  // ---- backward seeds (SURVEY Appendix A)
+  sdf = warp_sum(sdf);
+  fsv = warp_sum(fsv);
+  eik = warp_sum(eik);
+  // ---- backward seeds
   const T Mg = (T)L.m_global;
-  T chb[3];
-#pragma unroll
-  for (int c = 0; c < 3; ++c) chb[c] = ((T)L.rgb / Mg) * err[c] / lrgb;
+  const T chb0 = ((T)L.rgb / Mg) * err0 / lrgb, chb1 = ((T)L.rgb / Mg) * err1 / lrgb,
+          chb2 = ((T)L.rgb / Mg) * err2 / lrgb;
   const T dhb = valid ? (T)L.depth * sgn(dh - dT) * inv_nv : T(0);
   const T ksdf = ((T)L.sdf / Mg) / ntr, kfs = ((T)L.fs / Mg) / nfs;
   const T keik = (T)(-2.0 * L.eik) * inv_ne;
-  T acc = T(0);      // L_bar suffix sum
-  T carry = T(0);    // D-bar part of sigma_bar for sample j+1
-  T logs = T(0);
-  for (int j = N - 1; j >= 0; --j) {
-    const int64_t sj = s0 + j;
-    T al = T(0), ratio = T(0), den = T(1);
-    if (j < N - 1) {
-      den = sig[j] >= SF ? sig[j] : SF;
-      ratio = sig[j + 1] / den;
-      al = T(1) - (ratio <= T(1) ? ratio : T(1));
-    }
-    T om = T(1) - al;
-    T Tj = trn[j];
-    T wj = Tj * al;
-    const T* cj = w.scol + sj * 3;
-    T wbar = (chb[0] * cj[0] + chb[1] * cj[1]) + chb[2] * cj[2] + dhb * (T)d[j];
-#pragma unroll
-    for (int c = 0; c < 3; ++c) w.cbar[sj * 3 + c] = wj * chb[c];
-    T Tbar = wbar * al;
-    T Lbar = acc;
-    acc += Tbar * Tj;
-    T ombar = om >= TF ? Lbar / om : T(0);
-    T abar = wbar * Tj - ombar;
-    T sig_own = T(0);  // D-bar contribution to sigma_bar_j
-    if (j < N - 1) {
-      T rbar = ratio <= T(1) ? -abar : T(0);
-      T sbn = carry + rbar / den;  // sigma_bar_{j+1}, now complete
-      T sg = sig[j + 1];
-      T zb = sbn * (sg * (T(1) - sg));
-      // finalize sample j+1
-      {
-        const int64_t sn = sj + 1;
-        T ph = w.sphi[sn];
-        logs += zb * ph;
-        double b = D - d[j + 1];
-        T pb = zb * s;
-        if (valid && fabs(b) <= L.trunc) pb += ksdf * sgn(ph - (T)b);
-        if (valid && b > L.trunc) {
-          T e = exp(ph * (T)(-L.alpha));
-          T inner = e - T(1);
-          T inner0 = T(0) >= inner ? T(0) : inner;
-          T dfs = inner0 >= ph - (T)b ? (inner > T(0) ? e * (T)(-L.alpha) : T(0)) : T(1);
-          pb += kfs * dfs;
-        }
-        w.pbar[sn] = pb;
+  // pass A: w_bar, c_bar, T_bar T; suffix sums L_bar_j = sum_{i>j} T_bar_i T_i
+  T tot = T(0);
+  for (int j0 = 0; j0 < N; j0 += 32) {
+    const int j = j0 + lane;
+    T tt = T(0);
+    if (j < N) {
+      T al = T(0);
+      if (j < N - 1) {
+        const T den = sig[j] >= SF ? sig[j] : SF;
+        const T ratio = sig[j + 1] / den;
+        al = T(1) - (ratio <= T(1) ? ratio : T(1));
       }
-      sig_own = sig[j] >= SF ? -(rbar * sg) / (den * den) : T(0);
+      const T Tj = trn[j];
+      const T wj = Tj * al;
+      const T* cj = w.scol + (s0 + j) * 3;
+      const T wbar = ((chb0 * cj[0] + chb1 * cj[1]) + chb2 * cj[2]) + dhb * (T)d[j];
+      T* cb = w.cbar + (s0 + j) * 3;
+      cb[0] = wj * chb0;
+      cb[1] = wj * chb1;
+      cb[2] = wj * chb2;
+      tt = (wbar * al) * Tj;
+      xb[j] = wbar;  // keep w_bar for pass B
     }
-    carry = sig_own;
-    // eikonal adjoint for sample j
-    {
-      double b = D - d[j];
-      bool fs = valid && b > L.trunc, bh = valid && b < -L.trunc;
-      const T* gp = w.sgphi + sj * 3;
-      if (fs || bh || !valid) {
-        T nn = sqrt((gp[0] * gp[0] + gp[1] * gp[1]) + gp[2] * gp[2] + (T)1e-20);
-        T k = keik * (T(1) - nn) / nn;
-#pragma unroll
-        for (int c = 0; c < 3; ++c) w.ubar[sj * 3 + c] = k * gp[c];
-      } else {
-#pragma unroll
-        for (int c = 0; c < 3; ++c) w.ubar[sj * 3 + c] = T(0);
+    const T incl = warp_incl_scan(tt);
+    if (j < N) yb[j] = tot + incl;  // inclusive prefix P_j
+    tot += __shfl_sync(0xffffffffu, incl, 31);
+  }
+  __syncwarp();
+  // pass B: sigma_bar contributions (own D-bar part, and r_bar_j / D_j to j+1)
+  for (int j0 = 0; j0 < N; j0 += 32) {
+    const int j = j0 + lane;
+    T own = T(0), fwd = T(0);
+    if (j < N) {
+      T al = T(0), ratio = T(0), den = T(1);
+      if (j < N - 1) {
+        den = sig[j] >= SF ? sig[j] : SF;
+        ratio = sig[j + 1] / den;
+        al = T(1) - (ratio <= T(1) ? ratio : T(1));
       }
+      const T om = T(1) - al;
+      const T Lbar = tot - yb[j];
+      const T ombar = om >= TF ? Lbar / om : T(0);
+      const T abar = xb[j] * trn[j] - ombar;
+      if (j < N - 1) {
+        const T rbar = ratio <= T(1) ? -abar : T(0);
+        fwd = rbar / den;
+        own = sig[j] >= SF ? -(rbar * sig[j + 1]) / (den * den) : T(0);
+      }
+    }
+    __syncwarp();
+    if (j < N) {
+      xb[j] = fwd;   // contribution to sigma_bar_{j+1}
+      yb[j] = own;   // contribution to sigma_bar_j
     }
   }
-  {  // finalize sample 0
-    T sg = sig[0];
-    T zb = carry * (sg * (T(1) - sg));
-    T ph = w.sphi[s0];
+  __syncwarp();
+  // pass C: phi_bar, u (eikonal), log_s partial
+  T logs = T(0);
+  for (int j = lane; j < N; j += 32) {
+    const T sg = sig[j];
+    const T sbar = yb[j] + (j > 0 ? xb[j - 1] : T(0));
+    const T zb = sbar * (sg * (T(1) - sg));
+    const T ph = w.sphi[s0 + j];
     logs += zb * ph;
-    double b = D - d[0];
+    const double b = D - d[j];
     T pb = zb * s;
     if (valid && fabs(b) <= L.trunc) pb += ksdf * sgn(ph - (T)b);
-    if (valid && b > L.trunc) {
-      T e = exp(ph * (T)(-L.alpha));
-      T inner = e - T(1);
-      T inner0 = T(0) >= inner ? T(0) : inner;
-      T dfs = inner0 >= ph - (T)b ? (inner > T(0) ? e * (T)(-L.alpha) : T(0)) : T(1);
+    const bool fs = valid && b > L.trunc, bh = valid && b < -L.trunc;
+    if (fs) {
+      const T e = exp(ph * alpha);
+      const T inner = e - T(1);
+      const T inner0 = T(0) >= inner ? T(0) : inner;
+      const T dfs = inner0 >= ph - (T)b ? (inner > T(0) ? e * alpha : T(0)) : T(1);
       pb += kfs * dfs;
     }
-    w.pbar[s0] = pb;
+    w.pbar[s0 + j] = pb;
+    const T* gp = w.sgphi + (s0 + j) * 3;
+    T* ub = w.ubar + (s0 + j) * 3;
+    if (fs || bh || !valid) {
+      const T nn = sqrt(((gp[0] * gp[0] + gp[1] * gp[1]) + gp[2] * gp[2]) + (T)1e-20);
+      const T k = keik * (T(1) - nn) / nn;
+      ub[0] = k * gp[0];
+      ub[1] = k * gp[1];
+      ub[2] = k * gp[2];
+    } else {
+      ub[0] = T(0);
+      ub[1] = T(0);
+      ub[2] = T(0);
+    }
   }
-  part[5] = (double)logs;
+  logs = warp_sum(logs);
+  if (lane == 0) {
+    double* part = w.ray_part + (int64_t)ray * 8;
+    part[0] = (double)lrgb;
+    part[1] = (double)lde;
+    part[2] = (double)(sdf / ntr);
+    part[3] = (double)(fsv / nfs);
+    part[4] = (double)eik;
+    part[5] = (double)logs;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1286,29 +1414,72 @@ struct AdamSegs {
   int n;
 };
 
+struct AdamConst {
+  double b1, b2, eps, c1, c2, ib1, ib2, inv_c1, inv_c2;  // ib = 1 - beta
+};
+
+// Exact form (float64 storage): every operation as numba performs it.
 template <typename T>
-__device__ __forceinline__ void adam_one(T& p, T& g, T& m, T& v, double lr, double b1, double b2,
-                                         double eps, double c1, double c2, int& bad) {
+__device__ __forceinline__ void adam_exact(T& p, T& g, T& m, T& v, double lr, const AdamConst& k,
+                                           int& bad) {
   double gi = (double)g;
   if (!isfinite(gi)) {
     gi = 0.0;
     ++bad;
   }
-  double mi = b1 * (double)m + (1.0 - b1) * gi;
-  double vi = b2 * (double)v + (1.0 - b2) * gi * gi;
+  const double mi = k.b1 * (double)m + k.ib1 * gi;
+  const double vi = k.b2 * (double)v + k.ib2 * gi * gi;
   m = (T)mi;
   v = (T)vi;
-  p = (T)((double)p - lr * (mi / c1) / (sqrt(vi / c2) + eps));
+  p = (T)((double)p - lr * (mi / k.c1) / (sqrt(vi / k.c2) + k.eps));
   g = T(0);
+}
+
+// Fast form (float32 storage): m, v exactly as numba (float64 mul/add, no
+// FMA); the update uses reciprocal multiplies and Newton-refined rsqrt/rcp
+// in float64 (relative error ~1e-15), so the float32 rounding of p - update
+// equals the reference's except when the exact value sits within ~1e-15 of
+// a float32 rounding boundary.
+__device__ __forceinline__ void adam_fast(float& p, float& g, float& m, float& v, double lr,
+                                          const AdamConst& k, int& bad) {
+  double gi = (double)g;
+  if (!isfinite(gi)) {
+    gi = 0.0;
+    ++bad;
+  }
+  const double mi = k.b1 * (double)m + k.ib1 * gi;
+  const double vi = k.b2 * (double)v + k.ib2 * gi * gi;
+  m = (float)mi;
+  v = (float)vi;
+  const double q1 = mi * k.inv_c1, q2 = vi * k.inv_c2;
+  double sq;
+  if (q2 > 1e-30) {
+    double t = (double)rsqrtf((float)q2);
+    t = t * fma(-0.5 * q2, t * t, 1.5);
+    t = t * fma(-0.5 * q2, t * t, 1.5);
+    sq = q2 * t;
+    sq = fma(fma(-sq, sq, q2), 0.5 * t, sq);  // one Newton step on sqrt itself
+  } else {
+    sq = sqrt(q2);
+  }
+  const double den = sq + k.eps;
+  double y = (double)__frcp_rn((float)den);
+  y = fma(fma(-den, y, 1.0), y, y);
+  y = fma(fma(-den, y, 1.0), y, y);
+  const double num = lr * q1;
+  double q = num * y;
+  q = fma(fma(-q, den, num), y, q);
+  p = (float)((double)p - q);
+  g = 0.0f;
 }
 
 template <typename T>
 __global__ void __launch_bounds__(256) k_adam(T* __restrict__ P, T* __restrict__ Gr, T* __restrict__ Mm,
-                                              T* __restrict__ Vv, int64_t n, AdamSegs segs, double b1,
-                                              double b2, double eps, double c1, double c2,
-                                              const double* guard, double thr, int32_t* status) {
+                                              T* __restrict__ Vv, int64_t n, AdamSegs segs,
+                                              AdamConst k, const double* guard, double thr,
+                                              int32_t* status) {
   if (guard) {
-    double tot = guard[0];
+    const double tot = guard[0];
     if (!(tot == tot) || isinf(tot) || tot > thr || status[GSB_ST_DIVERGED]) {
       if (blockIdx.x == 0 && threadIdx.x == 0) status[GSB_ST_DIVERGED] = 1;
       return;
@@ -1318,35 +1489,55 @@ __global__ void __launch_bounds__(256) k_adam(T* __restrict__ P, T* __restrict__
   using Vec = typename std::conditional<sizeof(T) == 4, float4, double2>::type;
   int bad = 0;
   const int64_t nvec = n / V;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nvec;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    int64_t e = i * V;
-    int sidx = 0;
-    for (int k = 1; k < segs.n; ++k)
-      if (e >= segs.begin[k]) sidx = k;
-    double lr = segs.lr[sidx];
-    Vec p = reinterpret_cast<Vec*>(P)[i];
-    Vec g = reinterpret_cast<Vec*>(Gr)[i];
-    Vec m = reinterpret_cast<Vec*>(Mm)[i];
-    Vec v = reinterpret_cast<Vec*>(Vv)[i];
-    T* pp = reinterpret_cast<T*>(&p);
-    T* gg = reinterpret_cast<T*>(&g);
-    T* mm = reinterpret_cast<T*>(&m);
-    T* vv = reinterpret_cast<T*>(&v);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i0 < nvec; i0 += 2 * stride) {
+    // two independent vectors per iteration: more bytes in flight
+    Vec p[2], g[2], m[2], v[2];
+    double lr[2];
 #pragma unroll
-    for (int k = 0; k < V; ++k) adam_one(pp[k], gg[k], mm[k], vv[k], lr, b1, b2, eps, c1, c2, bad);
-    reinterpret_cast<Vec*>(P)[i] = p;
-    reinterpret_cast<Vec*>(Gr)[i] = g;
-    reinterpret_cast<Vec*>(Mm)[i] = m;
-    reinterpret_cast<Vec*>(Vv)[i] = v;
+    for (int u = 0; u < 2; ++u) {
+      const int64_t i = i0 + u * stride;
+      if (i >= nvec) break;
+      const int64_t e = i * V;
+      int sidx = 0;
+      for (int q = 1; q < segs.n; ++q)
+        if (e >= segs.begin[q]) sidx = q;
+      lr[u] = segs.lr[sidx];
+      p[u] = __ldcs(reinterpret_cast<const Vec*>(P) + i);
+      g[u] = __ldcs(reinterpret_cast<const Vec*>(Gr) + i);
+      m[u] = __ldcs(reinterpret_cast<const Vec*>(Mm) + i);
+      v[u] = __ldcs(reinterpret_cast<const Vec*>(Vv) + i);
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int64_t i = i0 + u * stride;
+      if (i >= nvec) break;
+      T* pp = reinterpret_cast<T*>(&p[u]);
+      T* gg = reinterpret_cast<T*>(&g[u]);
+      T* mm = reinterpret_cast<T*>(&m[u]);
+      T* vv = reinterpret_cast<T*>(&v[u]);
+#pragma unroll
+      for (int q = 0; q < V; ++q) {
+        if constexpr (sizeof(T) == 4)
+          adam_fast(pp[q], gg[q], mm[q], vv[q], lr[u], k, bad);
+        else
+          adam_exact(pp[q], gg[q], mm[q], vv[q], lr[u], k, bad);
+      }
+      __stcs(reinterpret_cast<Vec*>(P) + i, p[u]);
+      __stcs(reinterpret_cast<Vec*>(Gr) + i, g[u]);
+      __stcs(reinterpret_cast<Vec*>(Mm) + i, m[u]);
+      __stcs(reinterpret_cast<Vec*>(Vv) + i, v[u]);
+    }
   }
   // tail
-  for (int64_t e = nvec * V + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
-       e += (int64_t)gridDim.x * blockDim.x) {
+  for (int64_t e = nvec * V + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += stride) {
     int sidx = 0;
-    for (int k = 1; k < segs.n; ++k)
-      if (e >= segs.begin[k]) sidx = k;
-    adam_one(P[e], Gr[e], Mm[e], Vv[e], segs.lr[sidx], b1, b2, eps, c1, c2, bad);
+    for (int q = 1; q < segs.n; ++q)
+      if (e >= segs.begin[q]) sidx = q;
+    if constexpr (sizeof(T) == 4)
+      adam_fast(P[e], Gr[e], Mm[e], Vv[e], segs.lr[sidx], k, bad);
+    else
+      adam_exact(P[e], Gr[e], Mm[e], Vv[e], segs.lr[sidx], k, bad);
   }
   bad = warp_sum(bad);
   if ((threadIdx.x & 31) == 0 && bad) atomicAdd(status + GSB_ST_ADAM_BAD, bad);

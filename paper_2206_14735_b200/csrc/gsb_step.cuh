@@ -48,7 +48,7 @@ int run_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step
       for (int rnd = 0; rnd < R; ++rnd) {
         const bool need_phi = rnd < R - 1;
         GSB_CHECK(cudaMemsetAsync(w.evl_count, 0, sizeof(int32_t), stream));
-        k_importance_dev<T><<<(M + 63) / 64, 64, 0, stream>>>(
+        k_importance_dev<T><<<(M + 3) / 4, 128, 0, stream>>>(
             w, M, K, A, st->ray_base, w.dep[cur], w.phi[cur], w.dep[1 - cur], w.phi[1 - cur],
             log_s, st->rng_importance[rnd], w.evl, w.evl_count, w.evl_cap, need_phi ? 1 : 0);
         GSB_LAUNCHED();
@@ -90,8 +90,8 @@ int run_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step
       k_smooth<T><<<(z.S + 127) / 128, 128, 0, stream>>>(w, z.MN, z.S, scale);
       GSB_LAUNCHED();
     }
-    k_render<T><<<(M + 63) / 64, 64, 0, stream>>>(w, M, N, dep_final, params,
-                                                  model->log_s_offset, L);
+    k_render<T><<<(M + 3) / 4, 128, (size_t)4 * 4 * N * esz, stream>>>(w, M, N, dep_final, params,
+                                                                       model->log_s_offset, L);
     GSB_LAUNCHED();
     // backward kernels: persistent grids
     constexpr int WG = sizeof(T) == 4 ? 4 : 2;
