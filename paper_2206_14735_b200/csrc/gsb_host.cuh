@@ -87,8 +87,11 @@ Ws<T> carve(void* ws, const Sizes& z, size_t* bytes, int64_t* off_parts = nullpt
   w.wts = c.template take<T>(z.MN);
   w.ray_part = c.template take<double>((int64_t)z.M * 8);
   w.smooth_part = c.template take<double>(z.S > 0 ? z.S : 1);
-  w.nb_max = kNbMax;
-  w.mlp_part = c.template take<T>((int64_t)kNbMax * z.nmlp);
+  // partial weight-gradient slots: one per backward CTA (float32 path: one
+  // CTA per 128 samples), at least kNbMax for the persistent float64 kernels
+  const int64_t nb = std::max<int64_t>(kNbMax, (z.NS + 127) / 128);
+  w.nb_max = (int)nb;
+  w.mlp_part = c.template take<T>(nb * z.nmlp);
   if (bytes) *bytes = c.off;
   if (off_parts) *off_parts = (int64_t)o_parts;
   if (off_counts) *off_counts = (int64_t)o_counts;

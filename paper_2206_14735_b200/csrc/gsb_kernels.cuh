@@ -939,50 +939,84 @@ __global__ void __launch_bounds__(128) k_render(Ws<T> w, int M, int N, const dou
 // Thread per sample.  Each thread's shared-memory row holds its activations
 // and, at the end, its outer-product factors; every warp then accumulates
 // the 32 samples' outer products with lane j owning output column j.
+// One round of corner loads per sample: z = sum_k w_k theta_k and
+// v = sum_k ju_k theta_k are formed together (p, u are known up front).
 
 template <typename T, class S>
 struct GeoRow {
-  static constexpr int A0 = S::IN_G + 1;            // [p z + v, p]   (z staged here)
+  static constexpr int A0 = S::IN_G + 1;            // z, then [p z + v, p]
   static constexpr int A0P = (A0 + 3) / 4 * 4;
   static constexpr int oA0 = 0;
   static constexpr int oB0 = oA0 + A0P;             // delta0
-  static constexpr int oA1 = oB0 + GSB_HID;         // [p h0 + q0, p] (h0 staged here)
+  static constexpr int oA1 = oB0 + GSB_HID;         // h0, then [p h0 + q0, p]
   static constexpr int A1P = (GSB_HID + 1 + 3) / 4 * 4;
-  static constexpr int oB1 = oA1 + A1P;             // delta1
-  static constexpr int oV2 = oB1 + GSB_HID;         // p h1 + dd1 (.) m1
-  static constexpr int oQ = oV2 + GSB_HID;          // q0 scratch
-  static constexpr int ROW = oQ + GSB_HID;
+  static constexpr int oV2 = oA1 + A1P;             // p h1 + dd1 (.) m1
+  static constexpr int oQ = oV2 + GSB_HID;          // v (IN_G), then q0 (32)
+  static constexpr int oM = oQ + GSB_HID;           // m1 bits
+  static constexpr int ROW = oM + 4;
 };
 
+// Grid scatter theta[idx_k] += g (coef_k) for one level, reduced within the
+// warp first: samples of a ray are depth-ordered, so lanes sharing a cell
+// form contiguous runs; each run is summed with a segmented shuffle scan and
+// its first lane issues one vector red per corner.  Inactive lanes form
+// their own (empty) runs.
 template <typename T, int C>
 __device__ __forceinline__ void scatter_level(const LevelDev& L, const LocT<T>& q, const T* gl,
-                                              const T (&coef)[8], bool active, bool aggregate) {
+                                              const T (&coef)[8], bool active, bool /*unused*/) {
   const unsigned full = 0xffffffffu;
-  if (aggregate) {
-    // every lane shares one cell (coarse levels): reduce across the warp first
-    const int b0 = __shfl_sync(full, q.base, 0);
-    if (__all_sync(full, !active || q.base == b0)) {
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        T v[C];
-#pragma unroll
-        for (int c = 0; c < C; ++c) v[c] = warp_sum(active ? gl[c] * coef[k] : T(0));
-        if ((threadIdx.x & 31) == 0) {
-          T* dst = reinterpret_cast<T*>(L.grad) + ((int64_t)b0 + corner_off(L, k)) * C;
-          red_row<T, C>(dst, v);
-        }
-      }
-      return;
-    }
-  }
-  if (!active) return;
+  const int lane = threadIdx.x & 31;
+  const int key = active ? q.base : (-2 - lane);
+  const int prev = __shfl_up_sync(full, key, 1);
+  const bool head = lane == 0 || key != prev;
+  const unsigned heads = __ballot_sync(full, head);
   T* Gp = reinterpret_cast<T*>(L.grad) + (int64_t)q.base * C;
+  if (heads == full) {  // no shared cells in this warp: one red per lane
+    if (!active) return;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      T v[C];
+#pragma unroll
+      for (int c = 0; c < C; ++c) v[c] = gl[c] * coef[k];
+      red_row<T, C>(Gp + corner_off(L, k) * C, v);
+    }
+    return;
+  }
+  // end of my run (exclusive): next head after `lane`, or 32
+  const unsigned after = lane == 31 ? 0u : (heads >> (lane + 1));
+  const int run_end = after ? lane + __ffs(after) : 32;
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
     T v[C];
 #pragma unroll
-    for (int c = 0; c < C; ++c) v[c] = gl[c] * coef[k];
-    red_row<T, C>(Gp + corner_off(L, k) * C, v);
+    for (int c = 0; c < C; ++c) v[c] = active ? gl[c] * coef[k] : T(0);
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        const T y = __shfl_down_sync(full, v[c], o);
+        if (lane + o < run_end) v[c] += y;
+      }
+    }
+    if (head && active) red_row<T, C>(Gp + corner_off(L, k) * C, v);
+  }
+}
+
+// corner weights w_k and their u-directional derivatives ju_k (world units),
+// gs/diffcore.py:761-767, 874-890
+template <typename T>
+__device__ __forceinline__ void corner_w_ju(const LocT<T>& q, T iv, const T (&u)[3], T (&wk)[8],
+                                            T (&ju)[8]) {
+  const T x1 = q.fx, y1 = q.fy, z1 = q.fz;
+  const T x0 = T(1) - x1, y0 = T(1) - y1, z0 = T(1) - z1;
+  const T u0 = u[0] * iv, u1 = u[1] * iv, u2 = u[2] * iv;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int dx = (k >> 2) & 1, dy = (k >> 1) & 1, dz = k & 1;
+    const T wx = dx ? x1 : x0, wy = dy ? y1 : y0, wz = dz ? z1 : z0;
+    const T sx = dx ? T(1) : T(-1), sy = dy ? T(1) : T(-1), sz = dz ? T(1) : T(-1);
+    wk[k] = (wx * wy) * wz;
+    ju[k] = (sx * wy * wz) * u0 + (wx * sy * wz) * u1 + (wx * wy * sz) * u2;
   }
 }
 
@@ -1037,11 +1071,9 @@ __global__ void __launch_bounds__(WARPS * 32) k_bwd_geom(Ws<T> w, Geo G, int M, 
   for (int i = 0; i <= GSB_HID; ++i) acc1[i] = T(0);
   __syncthreads();
   const int64_t nwarps = (int64_t)gridDim.x * WARPS;
-  for (int64_t base = ((int64_t)blockIdx.x * WARPS + wid) * 32; base < NS; base += nwarps * 32) {
-    const int64_t s = base + lane;
-    const bool active = s < NS;
-    T p = T(0), u[3] = {T(0), T(0), T(0)}, pt[3];
-    if (active) {
+  // per-sample inputs, prefetched one batch ahead
+  auto fetch = [&](int64_t s, T& p, T (&u)[3], T (&pt)[3]) {
+    if (s < NS) {
       p = w.pbar[s];
 #pragma unroll
       for (int a = 0; a < 3; ++a) u[a] = w.ubar[s * 3 + a];
@@ -1053,20 +1085,52 @@ __global__ void __launch_bounds__(WARPS * 32) k_bwd_geom(Ws<T> w, Geo G, int M, 
 #pragma unroll
         for (int a = 0; a < 3; ++a) pt[a] = spts[(s - MN) * 3 + a];
       }
-    } else {
-      // inactive lanes evaluate a valid point and contribute zero
+    } else {  // inactive lanes evaluate a valid point and contribute zero
+      p = T(0);
 #pragma unroll
-      for (int a = 0; a < 3; ++a) pt[a] = (T)G.lo[a];
+      for (int a = 0; a < 3; ++a) {
+        u[a] = T(0);
+        pt[a] = (T)G.lo[a];
+      }
     }
+  };
+  int64_t base = ((int64_t)blockIdx.x * WARPS + wid) * 32;
+  T np, nu[3], npt[3];
+  fetch(base + lane, np, nu, npt);
+  for (; base < NS; base += nwarps * 32) {
+    const int64_t s = base + lane;
+    const bool active = s < NS;
+    T p = np, u[3] = {nu[0], nu[1], nu[2]}, pt[3] = {npt[0], npt[1], npt[2]};
+    fetch(base + nwarps * 32 + lane, np, nu, npt);
+    // ---- one pass over the corners: z (-> row), v (-> row)
     LocT<T> loc[S::NL];
 #pragma unroll
     for (int l = 0; l < S::NL; ++l) {
-      loc[l] = compact<T>(locate<false>(G.lv[l], (double)pt[0], (double)pt[1], (double)pt[2], nullptr));
-      T f[S::CG];
-      gather_fast<T, S::CG>(G.lv[l], loc[l], f);
+      const LevelDev& L = G.lv[l];
+      loc[l] = compact<T>(locate<false>(L, (double)pt[0], (double)pt[1], (double)pt[2], nullptr));
+      T wk[8], ju[8];
+      corner_w_ju(loc[l], (T)L.inv_vs, u, wk, ju);
+      const T* F = reinterpret_cast<const T*>(L.feat) + (int64_t)loc[l].base * S::CG;
+      T zl[S::CG], vl[S::CG];
 #pragma unroll
-      for (int c = 0; c < S::CG; ++c) myrow[R::oA0 + l * S::CG + c] = f[c];
+      for (int c = 0; c < S::CG; ++c) zl[c] = vl[c] = T(0);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        T row[S::CG];
+        load_row<T, S::CG>(F + corner_off(L, k) * S::CG, row);
+#pragma unroll
+        for (int c = 0; c < S::CG; ++c) {
+          zl[c] = fma(wk[k], row[c], zl[c]);
+          vl[c] = fma(ju[k], row[c], vl[c]);
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < S::CG; ++c) {
+        myrow[R::oA0 + l * S::CG + c] = zl[c];
+        myrow[R::oQ + l * S::CG + c] = vl[c];
+      }
     }
+    // ---- forward, then delta0 and g = dphi/dz
     uint32_t m0, m1;
     {
       T h[GSB_HID];
@@ -1080,87 +1144,85 @@ __global__ void __launch_bounds__(WARPS * 32) k_bwd_geom(Ws<T> w, Geo G, int M, 
 #pragma unroll
       for (int j = 0; j < GSB_HID; ++j) h[j] *= p;
       store32(myrow + R::oV2, h);                          // p h1
-      load32(myrow + R::oA1, h);
-#pragma unroll
-      for (int j = 0; j < GSB_HID; ++j) h[j] *= p;
-      store32(myrow + R::oA1, h);                          // p h0
-      myrow[R::oA1 + GSB_HID] = p;
     }
     T gz[S::IN_G];
     {
       T d[GSB_HID];
 #pragma unroll
       for (int j = 0; j < GSB_HID; ++j) d[j] = ((m1 >> j) & 1u) ? sw[S::oGW2 + j] : T(0);
-      store32(myrow + R::oB1, d);                          // delta1
       dense_d_row<T, GSB_HID>(sw + S::oGW1, d, m0, myrow + R::oB0);   // delta0
       load32(myrow + R::oB0, d);
       dense_d_reg<T, S::IN_G>(sw + S::oGW0, d, gz);        // g = dphi/dz
     }
-    // per level: ju, v = theta . ju, scatter g_l (p w_k + ju_k)
-    T v[S::IN_G];
+    // ---- grid scatter: theta_l[idx_k] += g_l (p w_k + ju_k)
 #pragma unroll
     for (int l = 0; l < S::NL; ++l) {
-      const LevelDev& L = G.lv[l];
-      const LocT<T>& q = loc[l];
-      const T x1 = q.fx, y1 = q.fy, z1 = q.fz;
-      const T x0 = T(1) - x1, y0 = T(1) - y1, z0 = T(1) - z1;
-      const T iv = (T)L.inv_vs;
-      const T u0 = u[0] * iv, u1 = u[1] * iv, u2 = u[2] * iv;
-      T coef[8];
-      T vl[S::CG];
+      T wk[8], ju[8], coef[8];
+      corner_w_ju(loc[l], (T)G.lv[l].inv_vs, u, wk, ju);
 #pragma unroll
-      for (int c = 0; c < S::CG; ++c) vl[c] = T(0);
-      const T* F = reinterpret_cast<const T*>(L.feat) + (int64_t)q.base * S::CG;
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const int dx = (k >> 2) & 1, dy = (k >> 1) & 1, dz = k & 1;
-        const T wx = dx ? x1 : x0, wy = dy ? y1 : y0, wz = dz ? z1 : z0;
-        const T sx = dx ? T(1) : T(-1), sy = dy ? T(1) : T(-1), sz = dz ? T(1) : T(-1);
-        const T ju = (sx * wy * wz) * u0 + (wx * sy * wz) * u1 + (wx * wy * sz) * u2;
-        coef[k] = p * ((wx * wy) * wz) + ju;
-        T row[S::CG];
-        load_row<T, S::CG>(F + corner_off(L, k) * S::CG, row);
-#pragma unroll
-        for (int c = 0; c < S::CG; ++c) vl[c] = fma(row[c], ju, vl[c]);
-      }
-#pragma unroll
-      for (int c = 0; c < S::CG; ++c) v[l * S::CG + c] = vl[c];
-      scatter_level<T, S::CG>(L, q, gz + l * S::CG, coef, active, l < agg_levels);
+      for (int k = 0; k < 8; ++k) coef[k] = fma(p, wk[k], ju[k]);
+      scatter_level<T, S::CG>(G.lv[l], loc[l], gz + l * S::CG, coef, active, l < agg_levels);
     }
-    // A0 = [p z + v, p]
-#pragma unroll
-    for (int i = 0; i < S::IN_G; ++i) myrow[R::oA0 + i] = fma(p, myrow[R::oA0 + i], v[i]);
-    myrow[R::oA0 + S::IN_G] = p;
-    // q0 = (v W0) (.) m0 -> A1 += q0 ; dd1 = (q0 W1) (.) m1 -> V2 += dd1
+    // ---- A0 = [p z + v, p]; q0 = (v W0) (.) m0; A1 = [p h0 + q0, p]; V2 += dd1 (.) m1
     {
       T q0[GSB_HID];
-      dense_f_reg<T, S::IN_G>(sw + S::oGW0, v, q0);
+      dense_f_row<T, S::IN_G>(sw + S::oGW0, myrow + R::oQ, q0);  // v W0
+#pragma unroll
+      for (int i = 0; i < S::IN_G; ++i)
+        myrow[R::oA0 + i] = fma(p, myrow[R::oA0 + i], myrow[R::oQ + i]);
+      myrow[R::oA0 + S::IN_G] = p;
       T a[GSB_HID];
       load32(myrow + R::oA1, a);
 #pragma unroll
       for (int j = 0; j < GSB_HID; ++j) {
         q0[j] = ((m0 >> j) & 1u) ? q0[j] : T(0);
-        a[j] += q0[j];
+        a[j] = fma(p, a[j], q0[j]);
       }
       store32(myrow + R::oA1, a);
+      myrow[R::oA1 + GSB_HID] = p;
       store32(myrow + R::oQ, q0);
-      dense_f_row<T, GSB_HID>(sw + S::oGW1, myrow + R::oQ, q0);
+      dense_f_row<T, GSB_HID>(sw + S::oGW1, myrow + R::oQ, q0);  // q0 W1
       load32(myrow + R::oV2, a);
 #pragma unroll
       for (int j = 0; j < GSB_HID; ++j) a[j] += ((m1 >> j) & 1u) ? q0[j] : T(0);
       store32(myrow + R::oV2, a);
+      reinterpret_cast<uint32_t*>(myrow + R::oM)[0] = active ? m1 : 0u;
     }
     if (!active) {
 #pragma unroll 1
-      for (int i = 0; i < R::ROW; ++i) myrow[i] = T(0);
+      for (int i = 0; i < R::oM; ++i) myrow[i] = T(0);
     }
     __syncwarp();
-    warp_outer<T, R::A0, R::A0P, GSB_HID + 1, R::A1P>(rows, R::ROW, R::oA0, R::oB0, R::oA1, R::oB1,
-                                                      lane, acc0, acc1);
+    // ---- outer products over the warp's 32 samples; lane owns column `lane`
+    {
+      const T w2l = sw[S::oGW2 + lane];
 #pragma unroll 1
-    for (int r = 0; r < 32; ++r) {
-      acc2 += rows[(size_t)r * R::ROW + R::oV2 + lane];
-      accp += rows[(size_t)r * R::ROW + R::oA0 + S::IN_G];  // db2 = sum p
+      for (int r = 0; r < 32; ++r) {
+        const T* rw = rows + (size_t)r * R::ROW;
+        const uint32_t mr = reinterpret_cast<const uint32_t*>(rw + R::oM)[0];
+        const T b0 = rw[R::oB0 + lane];
+        const T b1 = ((mr >> lane) & 1u) ? w2l : T(0);     // delta1 = W2 (.) m1
+        acc2 += rw[R::oV2 + lane];
+        accp += rw[R::oA0 + S::IN_G];                       // db2 = sum p
+#pragma unroll
+        for (int i = 0; i < R::A0P; i += 4) {
+          T a0, a1, a2, a3;
+          lds4(rw + R::oA0 + i, a0, a1, a2, a3);
+          if (i < R::A0) acc0[i] = fma(a0, b0, acc0[i]);
+          if (i + 1 < R::A0) acc0[i + 1] = fma(a1, b0, acc0[i + 1]);
+          if (i + 2 < R::A0) acc0[i + 2] = fma(a2, b0, acc0[i + 2]);
+          if (i + 3 < R::A0) acc0[i + 3] = fma(a3, b0, acc0[i + 3]);
+        }
+#pragma unroll
+        for (int i = 0; i < R::A1P; i += 4) {
+          T a0, a1, a2, a3;
+          lds4(rw + R::oA1 + i, a0, a1, a2, a3);
+          if (i <= GSB_HID) acc1[i] = fma(a0, b1, acc1[i]);
+          if (i + 1 <= GSB_HID) acc1[i + 1] = fma(a1, b1, acc1[i + 1]);
+          if (i + 2 <= GSB_HID) acc1[i + 2] = fma(a2, b1, acc1[i + 2]);
+          if (i + 3 <= GSB_HID) acc1[i + 3] = fma(a3, b1, acc1[i + 3]);
+        }
+      }
     }
     __syncwarp();
   }
@@ -1181,7 +1243,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_bwd_geom(Ws<T> w, Geo G, int M, 
   }
   __syncthreads();
   T* out = w.mlp_part + (size_t)blockIdx.x * S::NMLP;
-  for (int t = threadIdx.x; t < NGP; t += blockDim.x) {
+  for (int t = threadIdx.x; t < NGP; t += WARPS * 32) {
     T a = T(0);
 #pragma unroll
     for (int k = 0; k < WARPS; ++k) a += red[(size_t)k * NGP + t];
@@ -1338,7 +1400,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_bwd_color(Ws<T> w, Geo G, int M,
   }
   __syncthreads();
   T* out = w.mlp_part + (size_t)blockIdx.x * S::NMLP + S::NG;
-  for (int t = threadIdx.x; t < NCP; t += blockDim.x) {
+  for (int t = threadIdx.x; t < NCP; t += WARPS * 32) {
     T a = T(0);
 #pragma unroll
     for (int k = 0; k < WARPS; ++k) a += red[(size_t)k * NCP + t];
@@ -1349,14 +1411,28 @@ __global__ void __launch_bounds__(WARPS * 32) k_bwd_color(Ws<T> w, Geo G, int M,
 // ---------------------------------------------------------------------------
 // deterministic finalization
 
+// sum of the per-CTA partial weight gradients, fixed order (deterministic):
+// block = 32 parameters x 8 warps; warp w sums slots w, w+8, ...; then the 8
+// warp partials are added in warp order
 template <typename T, class S>
-__global__ void k_finalize_mlp(Ws<T> w, T* grads, int64_t mlp_off, int nb_geo, int nb_col) {
-  int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= S::NMLP) return;
-  int nb = t < S::NG ? nb_geo : nb_col;
+__global__ void __launch_bounds__(256) k_finalize_mlp(Ws<T> w, T* grads, int64_t mlp_off,
+                                                      int nb_geo, int nb_col) {
+  __shared__ double red[8][33];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int t = blockIdx.x * 32 + lane;
   double a = 0.0;
-  for (int b = 0; b < nb; ++b) a += (double)w.mlp_part[(size_t)b * S::NMLP + t];
-  grads[mlp_off + t] += (T)a;
+  if (t < S::NMLP) {
+    const int nb = t < S::NG ? nb_geo : nb_col;
+    for (int b = wid; b < nb; b += 8) a += (double)w.mlp_part[(size_t)b * S::NMLP + t];
+  }
+  red[wid][lane] = a;
+  __syncthreads();
+  if (wid == 0 && t < S::NMLP) {
+    double tot = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) tot += red[k][lane];
+    grads[mlp_off + t] += (T)tot;
+  }
 }
 
 template <typename T>

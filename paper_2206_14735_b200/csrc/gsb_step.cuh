@@ -2,6 +2,7 @@
 #pragma once
 
 #include "gsb_host.cuh"
+#include "gsb_fast.cuh"
 
 #define GSB_CHECK(x)                           \
   do {                                         \
@@ -26,6 +27,10 @@ int run_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step
   T* params = reinterpret_cast<T*>(model->params);
   T* grads = reinterpret_cast<T*>(model->grads);
   const T* mlp = params + model->mlp_offset;  // staged into shared memory by each CTA
+  constexpr bool F32 = sizeof(T) == 4;  // float32: constant-bank weights + tensor-core outer products
+  if constexpr (F32)
+    GSB_CHECK(cudaMemcpyToSymbolAsync(c_w4, mlp, S::NMLP * esz, 0, cudaMemcpyDeviceToDevice,
+                                      stream));
   const size_t smem_sdf = (size_t)S::NG * esz;
   const size_t smem_fwd = ((size_t)(S::NMLP + 3) / 4 * 4 + 128 * FwdRow<T, S>::ROW) * esz;
   const int M = z.M, N = z.N, Nc = st->n_coarse, A = st->n_add, R = st->n_rounds;
@@ -41,8 +46,12 @@ int run_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step
     if (R > 0) {
       int64_t n0 = (int64_t)M * Nc;
       int blocks = (int)((n0 + 127) / 128);
-      k_sdf_eval<T, S, false><<<blocks, 128, smem_sdf, stream>>>(w, G, M, Nc, w.dep[0], w.phi[0],
-                                                                   nullptr, nullptr, mlp);
+      if constexpr (F32)
+        k_sdf_eval_f<S><<<blocks, 128, 0, stream>>>(w, G, M, Nc, w.dep[0], w.phi[0], nullptr,
+                                                     nullptr);
+      else
+        k_sdf_eval<T, S, false><<<blocks, 128, smem_sdf, stream>>>(w, G, M, Nc, w.dep[0],
+                                                                   w.phi[0], nullptr, nullptr, mlp);
       GSB_LAUNCHED();
       int cur = 0, K = Nc;
       for (int rnd = 0; rnd < R; ++rnd) {
@@ -55,8 +64,12 @@ int run_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step
         if (need_phi) {
           int64_t cap = (int64_t)M * A;
           int b2 = (int)((cap + 127) / 128);
-          k_sdf_eval<T, S, false><<<b2, 128, smem_sdf, stream>>>(
-              w, G, M, Nc, w.dep[1 - cur], w.phi[1 - cur], w.evl, w.evl_count, mlp);
+          if constexpr (F32)
+            k_sdf_eval_f<S><<<b2, 128, 0, stream>>>(w, G, M, Nc, w.dep[1 - cur], w.phi[1 - cur],
+                                                     w.evl, w.evl_count);
+          else
+            k_sdf_eval<T, S, false><<<b2, 128, smem_sdf, stream>>>(
+                w, G, M, Nc, w.dep[1 - cur], w.phi[1 - cur], w.evl, w.evl_count, mlp);
           GSB_LAUNCHED();
         }
         cur = 1 - cur;
@@ -70,9 +83,13 @@ int run_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step
     const T* spts = reinterpret_cast<const T*>(st->smooth_pts);
     int64_t ns = z.NS;
     int fb = (int)((ns + 127) / 128);
-    GSB_CHECK(cudaFuncSetAttribute(k_fwd<T, S, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)smem_fwd));
-    k_fwd<T, S, false><<<fb, 128, smem_fwd, stream>>>(w, G, M, N, dep_final, spts, nsp, mlp);
+    if constexpr (F32) {
+      k_fwd_f<S><<<fb, 128, 0, stream>>>(w, G, M, N, dep_final, spts, nsp);
+    } else {
+      GSB_CHECK(cudaFuncSetAttribute(k_fwd<T, S, false>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fwd));
+      k_fwd<T, S, false><<<fb, 128, smem_fwd, stream>>>(w, G, M, N, dep_final, spts, nsp, mlp);
+    }
     GSB_LAUNCHED();
     LossW L;
     L.rgb = st->w_rgb;
@@ -95,24 +112,39 @@ int run_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step
     GSB_LAUNCHED();
     // backward kernels: persistent grids
     constexpr int WG = sizeof(T) == 4 ? 4 : 2;
-    constexpr int CW = S::NMLP - S::oCW0;
-    size_t smem_g = ((size_t)(S::NG + 3) / 4 * 4 + (size_t)WG * 32 * GeoRow<T, S>::ROW) * sizeof(T);
-    size_t smem_c = ((size_t)(CW + 3) / 4 * 4 + (size_t)WG * 32 * ColRow<T, S>::ROW) * sizeof(T);
-    GSB_CHECK(cudaFuncSetAttribute(k_bwd_geom<T, S, WG>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_g));
-    GSB_CHECK(cudaFuncSetAttribute(k_bwd_color<T, S, WG>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_c));
     const int per_cta = WG * 32;
     int nb_geo = (int)std::min<int64_t>((ns + per_cta - 1) / per_cta, (int64_t)num_sms() * 2);
     int nb_col = (int)std::min<int64_t>((z.MN + per_cta - 1) / per_cta, (int64_t)num_sms() * 2);
     nb_geo = std::max(1, std::min(nb_geo, kNbMax));
     nb_col = std::max(1, std::min(nb_col, kNbMax));
-    k_bwd_geom<T, S, WG><<<nb_geo, per_cta, smem_g, stream>>>(w, G, M, N, dep_final, spts, nsp,
-                                                             2, mlp);
-    GSB_LAUNCHED();
-    k_bwd_color<T, S, WG><<<nb_col, per_cta, smem_c, stream>>>(w, G, M, N, dep_final, mlp);
-    GSB_LAUNCHED();
-    k_finalize_mlp<T, S><<<(S::NMLP + 255) / 256, 256, 0, stream>>>(w, grads, model->mlp_offset,
+    if constexpr (F32) {
+      nb_geo = (int)((ns + per_cta - 1) / per_cta);     // one 32-sample batch per warp
+      nb_col = (int)((z.MN + per_cta - 1) / per_cta);
+      const size_t smem_g = (size_t)WG * 32 * GeoRowF<S>::ROW * esz;
+      const size_t smem_c = (size_t)WG * 32 * ColRowF<S>::ROW * esz;
+      GSB_CHECK(cudaFuncSetAttribute(k_bwd_geom_f<S, WG>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_g));
+      GSB_CHECK(cudaFuncSetAttribute(k_bwd_color_f<S, WG>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_c));
+      k_bwd_geom_f<S, WG><<<nb_geo, per_cta, smem_g, stream>>>(w, G, M, N, dep_final, spts, nsp, 2);
+      GSB_LAUNCHED();
+      k_bwd_color_f<S, WG><<<nb_col, per_cta, smem_c, stream>>>(w, G, M, N, dep_final);
+      GSB_LAUNCHED();
+    } else {
+      constexpr int CW = S::NMLP - S::oCW0;
+      size_t smem_g = ((size_t)(S::NG + 3) / 4 * 4 + (size_t)WG * 32 * GeoRow<T, S>::ROW) * esz;
+      size_t smem_c = ((size_t)(CW + 3) / 4 * 4 + (size_t)WG * 32 * ColRow<T, S>::ROW) * esz;
+      GSB_CHECK(cudaFuncSetAttribute(k_bwd_geom<T, S, WG>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_g));
+      GSB_CHECK(cudaFuncSetAttribute(k_bwd_color<T, S, WG>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_c));
+      k_bwd_geom<T, S, WG><<<nb_geo, per_cta, smem_g, stream>>>(w, G, M, N, dep_final, spts, nsp,
+                                                               2, mlp);
+      GSB_LAUNCHED();
+      k_bwd_color<T, S, WG><<<nb_col, per_cta, smem_c, stream>>>(w, G, M, N, dep_final, mlp);
+      GSB_LAUNCHED();
+    }
+    k_finalize_mlp<T, S><<<(S::NMLP + 31) / 32, 256, 0, stream>>>(w, grads, model->mlp_offset,
                                                                     nb_geo, nb_col);
     GSB_LAUNCHED();
     k_finalize_loss<T><<<1, 1024, 0, stream>>>(w, M, z.S, grads, params, model->log_s_offset, L);
