@@ -625,18 +625,12 @@ __global__ void __launch_bounds__(WARPS * 32) k_bwd_color_f(Ws<float> w, Geo G, 
     store32(myrow + R::oB0, a0b);
     float fb[S::CC];
     cdense_t<S::CC, S::oCW0>(a0b, fb);
-    if (active) {  // colour grid scatter: theta_c[idx_k] += w_k f_bar
+    {  // colour grid scatter: theta_c[idx_k] += w_k f_bar (warp-segmented)
       float wk[8];
       corner_w(q, wk);
-      float* Gp = reinterpret_cast<float*>(G.col.grad) + (int64_t)q.base * S::CC;
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        float vv[S::CC];
-#pragma unroll
-        for (int c = 0; c < S::CC; ++c) vv[c] = wk[k] * fb[c];
-        red_row<float, S::CC>(Gp + corner_off(G.col, k) * S::CC, vv);
-      }
-    } else {
+      scatter_level<float, S::CC>(G.col, q, fb, wk, active, false);
+    }
+    if (!active) {
 #pragma unroll 1
       for (int i = 0; i < R::ROW; ++i) myrow[i] = 0.f;
     }
