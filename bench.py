@@ -53,27 +53,66 @@ def make_cfg(precision="single", batch=M_PER_GPU, seed=0):
 
 
 class Clocks:
-    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+    """SM clock + throttle-reason sampling during the timed region
+    (B200_PROFILING.md clocks line): NVML in-process every 20 ms (nvidia-smi
+    spawns are too slow for a sub-second region), nvidia-smi as fallback."""
+
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
 
     def __init__(self):
-        self.samples = []
+        self.samples = []  # (sm_mhz, max_mhz, set of reasons)
         self._stop = threading.Event()
         self._t = None
 
+    def _nvml(self):
+        import pynvml as N
+        N.nvmlInit()
+        idx = int(os.environ.get("LOCAL_RANK", "0"))
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+        if vis:
+            idx = int(vis.split(",")[idx])
+        h = N.nvmlDeviceGetHandleByIndex(idx)
+        bits = {"hw_slowdown": N.nvmlClocksEventReasonHwSlowdown,
+                "hw_thermal_slowdown": N.nvmlClocksEventReasonHwThermalSlowdown,
+                "sw_thermal_slowdown": N.nvmlClocksEventReasonSwThermalSlowdown,
+                "sw_power_cap": N.nvmlClocksEventReasonSwPowerCap}
+        mx = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
+
+        def read():
+            sm = N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)
+            r = N.nvmlDeviceGetCurrentClocksEventReasons(h)
+            return sm, mx, {k for k, b in bits.items() if r & b}
+        return read
+
+    def _smi(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+
+        def read():
+            out = subprocess.run(["nvidia-smi", "-i", os.environ.get("LOCAL_RANK", "0"),
+                                  f"--query-gpu={q}", "--format=csv,noheader,nounits"],
+                                 capture_output=True, text=True, timeout=5).stdout
+            f = [x.strip() for x in out.strip().split(",")]
+            return (float(f[0]), float(f[1]),
+                    {self.NAMES[i] for i in range(4) if f[2 + i].lower().startswith("active")})
+        return read
+
     def start(self):
+        try:
+            read = self._nvml()
+            read()
+            period = 0.02
+        except Exception:
+            read, period = self._smi(), 0.2
+
         def run():
-            q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
-                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-                 "clocks_event_reasons.sw_power_cap")
             while not self._stop.is_set():
                 try:
-                    out = subprocess.run(["nvidia-smi", "-i", os.environ.get("LOCAL_RANK", "0"),
-                                          f"--query-gpu={q}", "--format=csv,noheader,nounits"],
-                                         capture_output=True, text=True, timeout=5).stdout
-                    self.samples.append([x.strip() for x in out.strip().split(",")])
+                    self.samples.append(read())
                 except Exception:
                     pass
-                self._stop.wait(0.2)
+                self._stop.wait(period)
         self._t = threading.Thread(target=run, daemon=True)
         self._t.start()
 
@@ -81,11 +120,9 @@ class Clocks:
         self._stop.set()
         if self._t:
             self._t.join(timeout=6)
-        sm = [float(s[0]) for s in self.samples if len(s) >= 6 and s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if len(s) >= 6 and s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples if len(s) >= 6
-                          for i in range(4) if s[2 + i].lower().startswith("active")})
+        sm = [s[0] for s in self.samples]
+        mx = [s[1] for s in self.samples]
+        reasons = sorted(set().union(*[s[2] for s in self.samples])) if self.samples else []
         return {"sm_mhz": float(np.median(sm)) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
                 "samples": len(self.samples)}
@@ -106,6 +143,64 @@ def b_alg_bytes(model, M, N, S):
     Cc_s = 8 * 6 * 4 if model.grid.color.features.size * 4 > 32 * 2 ** 20 else 0
     n_imp = 96 + 2 * 12
     return 32 * P + M * (n_imp * G_s + N * 2 * (G_s + Cc_s)) + 2 * S * 2 * G_s, P
+
+
+HID, IN_G, IN_C = 32, 16, 9
+MAC_GEO_FWD = IN_G * HID + HID * HID + HID                       # 1568
+MAC_DELTA = HID * HID + HID * IN_G                                # dphi/dz chain
+MAC_COL_FWD = IN_C * HID + HID * HID + HID * 3
+MAC_GEO_BWD = MAC_GEO_FWD + MAC_DELTA + IN_G * HID + HID * HID + IN_G * HID + HID * HID + HID
+MAC_COL_BWD = MAC_COL_FWD + 3 * HID + HID * HID + HID * 6 + (IN_C + 1) * HID + HID * HID + HID * 3
+FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12                 # nominal FMA peak
+
+
+def traffic_of(kernel):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel` from
+    the committed ncu --set full summary (profiles/traffic.json), else None."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as f:
+        d = json.load(f)
+    for k, v in d.get("kernels", {}).items():
+        if k.startswith(kernel):
+            return v
+    return None
+
+
+def kernel_table(model, kt, K, M, N, S, P, peak_hbm):
+    """Per-kernel algorithmic work over live CUDA-event times."""
+    G_s = sum(8 * l.width * 4 for l in model.grid.levels if l.features.size * 4 > 32 * 2 ** 20)
+    Cc_s = 8 * 6 * 4 if model.grid.color.features.size * 4 > 32 * 2 ** 20 else 0
+    n_imp = 96 + 2 * 12
+    NS = M * N + 2 * S
+    work = {  # kernel: (bytes, MACs) per step
+        "k_adam": (32 * P, 0),
+        "k_sdf_eval": (M * n_imp * G_s, M * n_imp * MAC_GEO_FWD),
+        "k_fwd": (NS * G_s + M * N * Cc_s, NS * (MAC_GEO_FWD + MAC_DELTA) + M * N * MAC_COL_FWD),
+        "k_bwd_geom_f": (NS * G_s, NS * MAC_GEO_BWD),
+        "k_bwd_color_f": (M * N * Cc_s, M * N * MAC_COL_BWD),
+    }
+    rows = []
+    for name, (ms, n) in sorted(kt.items(), key=lambda x: -x[1][0]):
+        t = ms / K / 1e3
+        b, mac = work.get(name, (0, 0))
+        hbm = b / t / 1e9 if t > 0 else 0.0
+        fl = 2 * mac / t / 1e12 if t > 0 else 0.0
+        compute = mac > 0 and 2 * mac / (FP32_PEAK_TFLOPS * 1e12) > b / (peak_hbm * 1e9)
+        r = {"kernel": name, "ms_per_step": ms / K, "launches_per_step": n / K,
+             "alg_bytes": b, "alg_flops": 2 * mac, "hbm_gbs": hbm, "tflops": fl}
+        if compute:
+            r.update(bound="tensor", achieved=fl, peak=FP32_PEAK_TFLOPS, unit="TFLOP/s",
+                     frac=fl / FP32_PEAK_TFLOPS,
+                     peak_kind="nominal fp32 FMA peak 148 SM x 128 FMA/clk x 2 x 1.965 GHz "
+                               "(fp32 MLP work; 3xTF32 mma.sync measured at the same "
+                               "effective rate, tools/mb_layers.cu)")
+        else:
+            r.update(bound="hbm", achieved=hbm, peak=peak_hbm, unit="GB/s",
+                     frac=hbm / peak_hbm, peak_kind="measured (MEASURED_PEAKS.json hbm_gbs)")
+        rows.append(r)
+    return rows
 
 
 # ----------------------------------------------------------------------------
@@ -140,7 +235,8 @@ def run_reference(args):
     if rank != 0:
         return 0
     threads = os.cpu_count() or 1
-    m_sample = 512
+    # bounded sample per step so that K steps stay within a few minutes
+    m_sample = 512 if args.steps <= 20 else 256 if args.steps <= 50 else 128
     t, P = cpu_step_sample(max(args.steps, 1), 0 if args.steps <= 1 else 1, m_sample, threads)
     v = m_sample / t
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "rays/s",
@@ -166,7 +262,7 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--precision", default="single")
@@ -246,6 +342,7 @@ def main():
         pg.barrier()
     torch.cuda.synchronize()
     t_step, t_adam = [], []
+    launches0 = eng.lib.gsb_launch_count()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     ev0.record()
@@ -275,6 +372,7 @@ def main():
         t_adam.append((b, c))
     ev1.record()
     torch.cuda.synchronize()
+    launches = int(eng.lib.gsb_launch_count() - launches0)
     if pg:
         pg.barrier()
     clk = clocks.stop()
@@ -287,6 +385,15 @@ def main():
     adam_ms = float(np.mean([x.elapsed_time(y) for x, y in t_adam]))
     obj_ms = float(np.mean([x.elapsed_time(y) for x, y in t_step]))
     value = M * ws_ * K / (total_ms / 1e3)
+
+    # ---- per-kernel live timing (CUDA events between launches on the step
+    # stream, gsb_timing_enable); a separate pass so `value` carries no markers
+    eng.lib.gsb_timing_enable(1)
+    for k in range(K):
+        one_step(*pre[W + k])
+    torch.cuda.synchronize()
+    eng.lib.gsb_timing_enable(0)
+    kt = _lib.kernel_times()
 
     # ---- e2e through the public API (host draws + H2D + D2H of parts)
     T = optimizer.Trainer(model, ds, cfg, opt)
@@ -327,21 +434,26 @@ def main():
             pg.destroy_process_group()
         return 0
 
-    # ---- roofline: dominant kernel share (Adam: HBM streaming, 32 B/param)
+    # ---- roofline of the dominant kernel + per-kernel table
     peak, peak_kind = peaks()
     B, P = b_alg_bytes(model, M, N, S)
-    adam_bytes = 32 * P
-    roofline = {"bound": "hbm", "kernel": "k_adam (dense Adam over the arena)",
-                "achieved": adam_bytes / (adam_ms / 1e3) / 1e9, "peak": peak, "unit": "GB/s",
-                "frac": adam_bytes / (adam_ms / 1e3) / 1e9 / peak, "traffic": None,
-                "peak_kind": peak_kind,
+    table = kernel_table(model, kt, K, M, N, S, P, peak)
+    dom = max(table, key=lambda r: r["ms_per_step"])
+    roofline = {"bound": dom["bound"], "kernel": dom["kernel"], "achieved": dom["achieved"],
+                "peak": dom["peak"], "unit": dom["unit"], "frac": dom["frac"],
+                "traffic": None, "peak_kind": dom["peak_kind"],
+                "share_of_step": dom["ms_per_step"] / ms_step,
                 "step_b_alg_gb": B / 1e9,
-                "step_frac": B / (ms_step / 1e3) / 1e9 / peak,
-                "adam_ms": adam_ms, "objective_ms": obj_ms}
+                "step_hbm_frac": B / (ms_step / 1e3) / 1e9 / peak,
+                "objective_ms": obj_ms, "adam_ms": adam_ms,
+                "kernels": table}
+    tr = traffic_of(dom["kernel"])
+    if tr is not None:
+        roofline["traffic"] = tr
     cpu = None
     if not args.no_cpu_baseline and ws_ == 1:
         threads = os.cpu_count() or 1
-        m_sample = 256
+        m_sample = 2048  # ~10-20 s of CPU work
         t, _ = cpu_step_sample(1, 0, m_sample, threads)
         cpu = {"value": m_sample / t, "unit": "rays/s", "cores": threads, "kind": "port",
                "sample": f"one oracle step, {m_sample} rays of the config2 workload + dense "
@@ -359,7 +471,7 @@ def main():
             "samples_per_s": value * N,
             "e2e": {"value": e2e, "unit": "rays/s", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": 8 * 8},
-            "gpu_launches": None,
+            "gpu_launches": launches,
             "roofline": roofline, "cpu_baseline": cpu, "clocks": clk}
     print(json.dumps(line), flush=True)
     if pg:

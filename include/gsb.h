@@ -141,6 +141,18 @@ typedef struct {
 
 int gsb_version(void);
 
+/* Number of kernels this library has launched in the process (all entry
+ * points).  Bench/diagnostic counter; no reference counterpart. */
+uint64_t gsb_launch_count(void);
+
+/* Opt-in per-kernel timing for benchmarks: while enabled, gsb_train_step and
+ * gsb_adam_step record a CUDA event on their stream after every launch.
+ * gsb_timing_collect synchronises, returns per-kernel-name total milliseconds
+ * and launch counts (names: max_kernels x 64 chars), and resets the marks. */
+int gsb_timing_enable(int32_t on);
+int gsb_timing_collect(int32_t max_kernels, char* names, double* total_ms, int64_t* launches,
+                       int32_t* n_kernels);
+
 /* Bytes of device workspace gsb_train_step needs. */
 int gsb_step_workspace_size(const gsb_model_t* model, int32_t n_rays, int32_t n_coarse,
                             int32_t n_rounds, int32_t n_add, int32_t n_smooth,

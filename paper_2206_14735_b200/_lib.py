@@ -26,7 +26,8 @@ EXPORTS = (
     "gsb_version", "gsb_step_workspace_size", "gsb_step_workspace_layout", "gsb_train_step",
     "gsb_adam_step", "gsb_pcg64_random", "gsb_ray_batch", "gsb_gather_weighted",
     "gsb_scatter_weighted", "gsb_grid_sample", "gsb_importance_round",
-    "gsb_step_workspace_regions", "gsb_importance_refine",
+    "gsb_step_workspace_regions", "gsb_importance_refine", "gsb_launch_count",
+    "gsb_timing_enable", "gsb_timing_collect",
 )
 REGIONS = ("parts", "counts", "status", "depths", "weights", "phi", "gphi", "color", "pbar",
            "ubar", "cbar", "ray_o", "ray_r", "ray_far")
@@ -101,6 +102,9 @@ def lib():
     P, I32, I64, D, SZ = C.c_void_p, C.c_int32, C.c_int64, C.c_double, C.c_size_t
     sig = {
         "gsb_version": ([], I32),
+        "gsb_launch_count": ([], C.c_uint64),
+        "gsb_timing_enable": ([I32], I32),
+        "gsb_timing_collect": ([I32, C.c_char_p, C.POINTER(D), C.POINTER(I64), C.POINTER(I32)], I32),
         "gsb_step_workspace_size": ([C.POINTER(Model), I32, I32, I32, I32, I32, C.POINTER(SZ)], I32),
         "gsb_step_workspace_layout": ([C.POINTER(Model), I32, I32, I32, I32, I32,
                                        C.POINTER(I64), C.POINTER(I64), C.POINTER(I64),
@@ -144,3 +148,18 @@ def stream_handle(stream=None):
     import torch
     s = stream if stream is not None else torch.cuda.current_stream()
     return C.c_void_p(s.cuda_stream)
+
+
+def kernel_times(max_kernels=32):
+    """Collect gsb_timing marks -> {kernel name: (total_ms, launches)}."""
+    L = lib()
+    names = C.create_string_buffer(64 * max_kernels)
+    ms = (C.c_double * max_kernels)()
+    cnt = (C.c_int64 * max_kernels)()
+    n = C.c_int32(0)
+    check(L.gsb_timing_collect(max_kernels, names, ms, cnt, C.byref(n)), "timing_collect")
+    out = {}
+    for k in range(n.value):
+        nm = names.raw[64 * k:64 * k + 64].split(b"\0", 1)[0].decode()
+        out[nm] = (float(ms[k]), int(cnt[k]))
+    return out

@@ -5,6 +5,44 @@
 
 #include "gsb_step.cuh"
 
+#include <atomic>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+namespace gsb {
+namespace host {
+static std::atomic<unsigned long long> g_launches{0};
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+// per-kernel timing: an event after every production launch; the duration of
+// a launch is the gap to the previous mark (the call's start mark or the
+// previous kernel) on the same stream
+struct Mark {
+  const char* name;
+  cudaEvent_t ev;
+};
+static std::mutex g_tm;
+static bool g_timing = false;
+static std::vector<Mark> g_marks;
+static std::vector<cudaEvent_t> g_pool;
+
+void timing_point(const char* name, cudaStream_t s) {
+  if (!g_timing) return;
+  std::lock_guard<std::mutex> lk(g_tm);
+  cudaEvent_t e;
+  if (g_pool.empty()) {
+    if (cudaEventCreate(&e) != cudaSuccess) return;
+  } else {
+    e = g_pool.back();
+    g_pool.pop_back();
+  }
+  cudaEventRecord(e, s);
+  g_marks.push_back({name, e});
+}
+}  // namespace host
+}  // namespace gsb
+
 using namespace gsb;
 
 
@@ -62,6 +100,44 @@ using namespace gsb_abi;
 extern "C" {
 
 int gsb_version(void) { return 1; }
+
+uint64_t gsb_launch_count(void) { return gsb::host::g_launches.load(); }
+
+int gsb_timing_enable(int32_t on) {
+  std::lock_guard<std::mutex> lk(gsb::host::g_tm);
+  gsb::host::g_timing = on != 0;
+  return GSB_OK;
+}
+
+int gsb_timing_collect(int32_t max_kernels, char* names, double* total_ms, int64_t* launches,
+                       int32_t* n_kernels) {
+  using namespace gsb::host;
+  if (max_kernels <= 0 || !names || !total_ms || !launches || !n_kernels) return GSB_E_ARG;
+  std::lock_guard<std::mutex> lk(g_tm);
+  if (!g_marks.empty() && cudaEventSynchronize(g_marks.back().ev) != cudaSuccess) return GSB_E_CUDA;
+  int n = 0;
+  for (size_t i = 1; i < g_marks.size(); ++i) {
+    if (!g_marks[i].name) continue;  // start mark of a call
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, g_marks[i - 1].ev, g_marks[i].ev) != cudaSuccess) return GSB_E_CUDA;
+    int k = 0;
+    while (k < n && std::strncmp(names + 64 * k, g_marks[i].name, 63) != 0) ++k;
+    if (k == n) {
+      if (n == max_kernels) continue;
+      std::strncpy(names + 64 * k, g_marks[i].name, 63);
+      names[64 * k + 63] = 0;
+      total_ms[k] = 0.0;
+      launches[k] = 0;
+      ++n;
+    }
+    total_ms[k] += ms;
+    launches[k] += 1;
+  }
+  for (auto& m : g_marks) g_pool.push_back(m.ev);
+  g_marks.clear();
+  *n_kernels = n;
+  return GSB_OK;
+}
 
 int gsb_step_workspace_size(const gsb_model_t* model, int32_t n_rays, int32_t n_coarse,
                             int32_t n_rounds, int32_t n_add, int32_t n_smooth, size_t* bytes) {
@@ -139,6 +215,7 @@ int gsb_adam_step(int32_t precision, void* params, void* grads, void* m, void* v
   k.inv_c1 = 1.0 / c1;
   k.inv_c2 = 1.0 / c2;
   int blocks = num_sms() * 8;
+  timing_point(nullptr, s);
   if (precision == 0)
     k_adam<float><<<blocks, 256, 0, s>>>((float*)params, (float*)grads, (float*)m, (float*)v, n, sg,
                                          k, guard, guard_threshold, status);
@@ -146,6 +223,7 @@ int gsb_adam_step(int32_t precision, void* params, void* grads, void* m, void* v
     k_adam<double><<<blocks, 256, 0, s>>>((double*)params, (double*)grads, (double*)m, (double*)v,
                                           n, sg, k, guard, guard_threshold, status);
   GSB_LAUNCHED();
+  timing_point("k_adam", s);
   return GSB_OK;
 }
 

@@ -12,6 +12,12 @@ namespace host {
 
 constexpr int kNbMax = 1024;  // max CTAs of the backward kernels (partials slots)
 
+// kernels launched by this library (process-wide; gsb_launch_count)
+void note_launch();
+// opt-in per-kernel CUDA-event timing (gsb_timing_enable): records an event on
+// `s` after each production launch; name == nullptr marks the start of a call
+void timing_point(const char* name, cudaStream_t s);
+
 inline int num_sms() {
   static int n = 0;
   if (n == 0) {

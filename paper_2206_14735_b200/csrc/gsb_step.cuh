@@ -9,7 +9,17 @@
     cudaError_t e__ = (x);                     \
     if (e__ != cudaSuccess) return GSB_E_CUDA; \
   } while (0)
-#define GSB_LAUNCHED() GSB_CHECK(cudaGetLastError())
+#define GSB_LAUNCHED()         \
+  do {                         \
+    gsb::host::note_launch(); \
+    GSB_CHECK(cudaGetLastError()); \
+  } while (0)
+
+#define GSB_LAUNCHED_T(name)                  \
+  do {                                        \
+    GSB_LAUNCHED();                           \
+    gsb::host::timing_point(name, stream);    \
+  } while (0)
 
 namespace gsb {
 namespace host {
@@ -18,6 +28,7 @@ template <typename T, class S>
 int run_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step_t* st,
              cudaStream_t stream) {
   const size_t esz = sizeof(T);
+  timing_point(nullptr, stream);
   Sizes z = sizes_of(model, st->n_rays, st->n_coarse, st->n_rounds, st->n_add, st->n_smooth);
   if (S::NMLP != z.nmlp) return GSB_E_ARG;
   size_t need = 0;
@@ -42,7 +53,7 @@ int run_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step
     k_ray_setup<T><<<(M + 127) / 128, 128, 0, stream>>>(
         *data, st->ray_ids, M, st->ray_base, w, G, Nc, st->near, st->max_depth,
         st->has_fixed_far, st->fixed_far, st->rng_stratify);
-    GSB_LAUNCHED();
+    GSB_LAUNCHED_T("k_ray_setup");
     if (R > 0) {
       int64_t n0 = (int64_t)M * Nc;
       int blocks = (int)((n0 + 127) / 128);
@@ -52,7 +63,7 @@ int run_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step
       else
         k_sdf_eval<T, S, false><<<blocks, 128, smem_sdf, stream>>>(w, G, M, Nc, w.dep[0],
                                                                    w.phi[0], nullptr, nullptr, mlp);
-      GSB_LAUNCHED();
+      GSB_LAUNCHED_T("k_sdf_eval");
       int cur = 0, K = Nc;
       for (int rnd = 0; rnd < R; ++rnd) {
         const bool need_phi = rnd < R - 1;
@@ -60,7 +71,7 @@ int run_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step
         k_importance_dev<T><<<(M + 3) / 4, 128, 0, stream>>>(
             w, M, K, A, st->ray_base, w.dep[cur], w.phi[cur], w.dep[1 - cur], w.phi[1 - cur],
             log_s, st->rng_importance[rnd], w.evl, w.evl_count, w.evl_cap, need_phi ? 1 : 0);
-        GSB_LAUNCHED();
+        GSB_LAUNCHED_T("k_importance_dev");
         if (need_phi) {
           int64_t cap = (int64_t)M * A;
           int b2 = (int)((cap + 127) / 128);
@@ -70,14 +81,14 @@ int run_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step
           else
             k_sdf_eval<T, S, false><<<b2, 128, smem_sdf, stream>>>(
                 w, G, M, Nc, w.dep[1 - cur], w.phi[1 - cur], w.evl, w.evl_count, mlp);
-          GSB_LAUNCHED();
+          GSB_LAUNCHED_T("k_sdf_eval");
         }
         cur = 1 - cur;
         K += A;
       }
     }
     k_counts<T><<<(M + 127) / 128, 128, 0, stream>>>(w, M, N, dep_final, st->truncation);
-    GSB_LAUNCHED();
+    GSB_LAUNCHED_T("k_counts");
   }
   if (st->phases & 2) {
     const T* spts = reinterpret_cast<const T*>(st->smooth_pts);
@@ -90,7 +101,7 @@ int run_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fwd));
       k_fwd<T, S, false><<<fb, 128, smem_fwd, stream>>>(w, G, M, N, dep_final, spts, nsp, mlp);
     }
-    GSB_LAUNCHED();
+    GSB_LAUNCHED_T("k_fwd");
     LossW L;
     L.rgb = st->w_rgb;
     L.depth = st->w_depth;
@@ -105,11 +116,11 @@ int run_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step
     if (z.S > 0) {
       T scale = (T)(2.0 * st->w_smooth) / (T)st->smooth_global;
       k_smooth<T><<<(z.S + 127) / 128, 128, 0, stream>>>(w, z.MN, z.S, scale);
-      GSB_LAUNCHED();
+      GSB_LAUNCHED_T("k_smooth");
     }
     k_render<T><<<(M + 3) / 4, 128, (size_t)4 * 4 * N * esz, stream>>>(w, M, N, dep_final, params,
                                                                        model->log_s_offset, L);
-    GSB_LAUNCHED();
+    GSB_LAUNCHED_T("k_render");
     // backward kernels: persistent grids
     constexpr int WG = sizeof(T) == 4 ? 4 : 2;
     const int per_cta = WG * 32;
@@ -127,9 +138,9 @@ int run_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step
       GSB_CHECK(cudaFuncSetAttribute(k_bwd_color_f<S, WG>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_c));
       k_bwd_geom_f<S, WG><<<nb_geo, per_cta, smem_g, stream>>>(w, G, M, N, dep_final, spts, nsp, 2);
-      GSB_LAUNCHED();
+      GSB_LAUNCHED_T("k_bwd_geom_f");
       k_bwd_color_f<S, WG><<<nb_col, per_cta, smem_c, stream>>>(w, G, M, N, dep_final);
-      GSB_LAUNCHED();
+      GSB_LAUNCHED_T("k_bwd_color_f");
     } else {
       constexpr int CW = S::NMLP - S::oCW0;
       size_t smem_g = ((size_t)(S::NG + 3) / 4 * 4 + (size_t)WG * 32 * GeoRow<T, S>::ROW) * esz;
@@ -140,15 +151,15 @@ int run_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_c));
       k_bwd_geom<T, S, WG><<<nb_geo, per_cta, smem_g, stream>>>(w, G, M, N, dep_final, spts, nsp,
                                                                2, mlp);
-      GSB_LAUNCHED();
+      GSB_LAUNCHED_T("k_bwd_geom");
       k_bwd_color<T, S, WG><<<nb_col, per_cta, smem_c, stream>>>(w, G, M, N, dep_final, mlp);
-      GSB_LAUNCHED();
+      GSB_LAUNCHED_T("k_bwd_color");
     }
     k_finalize_mlp<T, S><<<(S::NMLP + 31) / 32, 256, 0, stream>>>(w, grads, model->mlp_offset,
                                                                     nb_geo, nb_col);
-    GSB_LAUNCHED();
+    GSB_LAUNCHED_T("k_finalize_mlp");
     k_finalize_loss<T><<<1, 1024, 0, stream>>>(w, M, z.S, grads, params, model->log_s_offset, L);
-    GSB_LAUNCHED();
+    GSB_LAUNCHED_T("k_finalize_loss");
   }
   return GSB_OK;
 }

@@ -97,11 +97,17 @@ class Dataset:
         row = np.searchsorted(cum, k, side="right")
         before = np.where(row > 0, cum[np.maximum(row - 1, 0)], 0)
         r = k - before
-        h = self.intrinsics.height
+        h, wd = self.intrinsics.height, self.intrinsics.width
         f, v = row // h, row % h
-        mask = self.depths_mm[f, v] > 0  # (n, W)
-        csum = np.cumsum(mask, axis=1)
-        u = np.argmax(csum > r[:, None], axis=1)
+        # rows without missing depth: the r-th valid pixel is u = r; only
+        # partial rows need the in-row prefix scan
+        cnt = cum[row] - before
+        u = r.copy()
+        part = np.flatnonzero(cnt < wd)
+        if part.size:
+            mask = self.depths_mm[f[part], v[part]] > 0  # (n_part, W)
+            csum = np.cumsum(mask, axis=1, dtype=np.int32)
+            u[part] = np.argmax(csum > r[part, None], axis=1)
         return f.astype(np.int64), v.astype(np.int64), u.astype(np.int64)
 
     @property

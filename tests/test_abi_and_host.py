@@ -18,7 +18,7 @@ HEADER = os.path.join(ROOT, "include", "gsb.h")
 def declared_functions():
     src = open(HEADER).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\bint\s+(gsb_\w+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(?:int|uint64_t)\s+(gsb_\w+)\s*\(", src)))
 
 
 def test_header_declarations_match_binding():
