@@ -178,8 +178,8 @@ def kernel_table(model, kt, K, M, N, S, P, peak_hbm):
         "k_adam": (32 * P, 0),
         "k_sdf_eval": (M * n_imp * G_s, M * n_imp * MAC_GEO_FWD),
         "k_fwd": (NS * G_s + M * N * Cc_s, NS * (MAC_GEO_FWD + MAC_DELTA) + M * N * MAC_COL_FWD),
-        "k_bwd_geom_f": (NS * G_s, NS * MAC_GEO_BWD),
-        "k_bwd_color_f": (M * N * Cc_s, M * N * MAC_COL_BWD),
+        "k_bwd_geom": (NS * G_s, NS * MAC_GEO_BWD),
+        "k_bwd_color": (M * N * Cc_s, M * N * MAC_COL_BWD),
     }
     rows = []
     for name, (ms, n) in sorted(kt.items(), key=lambda x: -x[1][0]):

@@ -53,6 +53,7 @@ struct Ws {
   double* ray_part;     // [M][8]
   double* smooth_part;  // [S]
   T* mlp_part;          // [nb_max][NMLP]
+  uint4* wfrag;         // float32: per-lane tf32 hi/lo B fragments of the MLP (gsb_tc.cuh)
   int nb_max;
   long long* counts;
   double* parts;

@@ -2,7 +2,7 @@
 #pragma once
 
 #include "gsb_host.cuh"
-#include "gsb_fast.cuh"
+#include "gsb_tc.cuh"
 
 #define GSB_CHECK(x)                           \
   do {                                         \
@@ -38,10 +38,13 @@ int run_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step
   T* params = reinterpret_cast<T*>(model->params);
   T* grads = reinterpret_cast<T*>(model->grads);
   const T* mlp = params + model->mlp_offset;  // staged into shared memory by each CTA
-  constexpr bool F32 = sizeof(T) == 4;  // float32: constant-bank weights + tensor-core outer products
-  if constexpr (F32)
-    GSB_CHECK(cudaMemcpyToSymbolAsync(c_w4, mlp, S::NMLP * esz, 0, cudaMemcpyDeviceToDevice,
-                                      stream));
+  constexpr bool F32 = sizeof(T) == 4;  // float32: decoders on the tensor cores (gsb_tc.cuh)
+  constexpr int TW = 4;                  // warps per CTA of the float32 sample kernels
+  const float* mlp32 = reinterpret_cast<const float*>(mlp);
+  if constexpr (F32) {
+    tc::k_wfrag<S><<<tc::Fr<S>::NALL, 32, 0, stream>>>(mlp32, w.wfrag);
+    GSB_LAUNCHED_T("k_wfrag");
+  }
   const size_t smem_sdf = (size_t)S::NG * esz;
   const size_t smem_fwd = ((size_t)(S::NMLP + 3) / 4 * 4 + 128 * FwdRow<T, S>::ROW) * esz;
   const int M = z.M, N = z.N, Nc = st->n_coarse, A = st->n_add, R = st->n_rounds;
@@ -57,10 +60,13 @@ int run_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step
     if (R > 0) {
       int64_t n0 = (int64_t)M * Nc;
       int blocks = (int)((n0 + 127) / 128);
-      if constexpr (F32)
-        k_sdf_eval_f<S><<<blocks, 128, 0, stream>>>(w, G, M, Nc, w.dep[0], w.phi[0], nullptr,
-                                                     nullptr);
-      else
+      if constexpr (F32) {
+        GSB_CHECK(cudaFuncSetAttribute(tc::k_sdf_eval_tc<S, TW>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)tc::SdfTc<S, TW>::smem()));
+        tc::k_sdf_eval_tc<S, TW><<<blocks, TW * 32, tc::SdfTc<S, TW>::smem(), stream>>>(
+            w, G, M, Nc, mlp32, w.dep[0], w.phi[0], nullptr, nullptr);
+      } else
         k_sdf_eval<T, S, false><<<blocks, 128, smem_sdf, stream>>>(w, G, M, Nc, w.dep[0],
                                                                    w.phi[0], nullptr, nullptr, mlp);
       GSB_LAUNCHED_T("k_sdf_eval");
@@ -76,8 +82,8 @@ int run_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step
           int64_t cap = (int64_t)M * A;
           int b2 = (int)((cap + 127) / 128);
           if constexpr (F32)
-            k_sdf_eval_f<S><<<b2, 128, 0, stream>>>(w, G, M, Nc, w.dep[1 - cur], w.phi[1 - cur],
-                                                     w.evl, w.evl_count);
+            tc::k_sdf_eval_tc<S, TW><<<b2, TW * 32, tc::SdfTc<S, TW>::smem(), stream>>>(
+                w, G, M, Nc, mlp32, w.dep[1 - cur], w.phi[1 - cur], w.evl, w.evl_count);
           else
             k_sdf_eval<T, S, false><<<b2, 128, smem_sdf, stream>>>(
                 w, G, M, Nc, w.dep[1 - cur], w.phi[1 - cur], w.evl, w.evl_count, mlp);
@@ -95,7 +101,10 @@ int run_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step
     int64_t ns = z.NS;
     int fb = (int)((ns + 127) / 128);
     if constexpr (F32) {
-      k_fwd_f<S><<<fb, 128, 0, stream>>>(w, G, M, N, dep_final, spts, nsp);
+      GSB_CHECK(cudaFuncSetAttribute(tc::k_fwd_tc<S, TW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)tc::FwdTc<S, TW>::smem()));
+      tc::k_fwd_tc<S, TW><<<(int)((ns + TW * 32 - 1) / (TW * 32)), TW * 32, tc::FwdTc<S, TW>::smem(),
+                            stream>>>(w, G, M, N, mlp32, dep_final, spts, nsp);
     } else {
       GSB_CHECK(cudaFuncSetAttribute(k_fwd<T, S, false>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fwd));
@@ -131,16 +140,17 @@ int run_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step
     if constexpr (F32) {
       nb_geo = (int)((ns + per_cta - 1) / per_cta);     // one 32-sample batch per warp
       nb_col = (int)((z.MN + per_cta - 1) / per_cta);
-      const size_t smem_g = (size_t)WG * 32 * GeoRowF<S>::ROW * esz;
-      const size_t smem_c = (size_t)WG * 32 * ColRowF<S>::ROW * esz;
-      GSB_CHECK(cudaFuncSetAttribute(k_bwd_geom_f<S, WG>,
+      const size_t smem_g = tc::GeoTc<S, WG>::smem();
+      const size_t smem_c = tc::ColTc<S, WG>::smem();
+      GSB_CHECK(cudaFuncSetAttribute(tc::k_bwd_geom_tc<S, WG>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_g));
-      GSB_CHECK(cudaFuncSetAttribute(k_bwd_color_f<S, WG>,
+      GSB_CHECK(cudaFuncSetAttribute(tc::k_bwd_color_tc<S, WG>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_c));
-      k_bwd_geom_f<S, WG><<<nb_geo, per_cta, smem_g, stream>>>(w, G, M, N, dep_final, spts, nsp, 2);
-      GSB_LAUNCHED_T("k_bwd_geom_f");
-      k_bwd_color_f<S, WG><<<nb_col, per_cta, smem_c, stream>>>(w, G, M, N, dep_final);
-      GSB_LAUNCHED_T("k_bwd_color_f");
+      tc::k_bwd_geom_tc<S, WG><<<nb_geo, per_cta, smem_g, stream>>>(w, G, M, N, mlp32, dep_final,
+                                                                    spts, nsp, 2);
+      GSB_LAUNCHED_T("k_bwd_geom");
+      tc::k_bwd_color_tc<S, WG><<<nb_col, per_cta, smem_c, stream>>>(w, G, M, N, mlp32, dep_final);
+      GSB_LAUNCHED_T("k_bwd_color");
     } else {
       constexpr int CW = S::NMLP - S::oCW0;
       size_t smem_g = ((size_t)(S::NG + 3) / 4 * 4 + (size_t)WG * 32 * GeoRow<T, S>::ROW) * esz;

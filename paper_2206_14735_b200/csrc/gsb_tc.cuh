@@ -1,0 +1,1033 @@
+// gsb_tc.cuh -- float32 taped pass with the decoders on the tensor cores.
+//
+// Work split: a warp owns 32 samples.  Per-sample
+// scalar work -- point, grid location, trilinear gather, grad-phi assembly,
+// grid scatter -- runs lane-per-sample.  The MLP layers run as chains of
+// mma.sync m16n8k8 TF32 in 3xTF32 split precision (hi*hi + hi*lo + lo*hi,
+// ~fp32 accuracy), activations resident in registers as accumulator ("D")
+// fragments: lane (g = lane/4, t = lane%4) of m-tile mt holds samples
+// 16mt+g (r = 0,1) and 16mt+g+8 (r = 2,3) at features 8nn+2t+(r&1).
+//
+// Chaining without shuffles: the A operand of k-step kk wants features
+// {slot t, slot t+4} of block kk; we *define* slot t <-> feature 2t and slot
+// t+4 <-> feature 2t+1, so the D fragment of feature block kk is the A
+// fragment {d0, d2, d1, d3}, and the weight (B) fragments are built with the
+// same permutation of their contraction index once per step (k_wfrag), split
+// into tf32 hi/lo, and staged in shared memory per CTA.
+//
+// tools/mb_layers.cu measured this form at 84-101% of the fp32 FFMA peak
+// (effective) already at 1-2 CTAs/SM with ~10x fewer issued instructions
+// and ~10x less code than the unrolled-FFMA kernels (gsb_fast.cuh), whose
+// 100-190 KB of SASS thrashed the instruction cache.
+#pragma once
+
+#include "gsb_fast.cuh"
+
+namespace gsb {
+namespace tc {
+
+constexpr int kFragMax = 128;  // B fragments per model (446 shape: 100)
+
+// B-fragment ids (each = 32 lanes x uint4 {hi0, hi1, lo0, lo1})
+template <class S>
+struct Fr {
+  static constexpr int KG = (S::IN_G + 7) / 8;  // geometry input k-steps
+  static constexpr int KC = (S::IN_C + 7) / 8;  // colour input k-steps
+  static constexpr int NCC = (S::CC + 7) / 8;   // colour-feature gradient n-tiles
+  static constexpr int G_W0 = 0;                // z W0        KG x 4
+  static constexpr int G_W1 = G_W0 + KG * 4;    // h0 W1       4 x 4
+  static constexpr int G_W1T = G_W1 + 16;       // d1 W1^T     4 x 4
+  static constexpr int G_W0T = G_W1T + 16;      // d0 W0^T     4 x KG
+  static constexpr int NGEO = G_W0T + 4 * KG;
+  static constexpr int C_W0 = NGEO;             // inp W0c     KC x 4
+  static constexpr int C_W1 = C_W0 + KC * 4;    // h0c W1c     4 x 4
+  static constexpr int C_W2 = C_W1 + 16;        // h1c W2c     4 x 1
+  static constexpr int C_W2T = C_W2 + 4;        // ybar W2c^T  1 x 4
+  static constexpr int C_W1T = C_W2T + 4;       // a1b W1c^T   4 x 4
+  static constexpr int C_W0T = C_W1T + 16;      // a0b W0c^T   4 x NCC
+  static constexpr int NALL = C_W0T + 4 * NCC;
+  static_assert(NALL <= kFragMax, "fragment buffer");
+};
+
+// One block per fragment id, one thread per lane.  Contraction index k of
+// fragment (kk, nn): b0 <-> k = 8kk+2t, b1 <-> k = 8kk+2t+1; output n = 8nn+g.
+template <class S>
+__global__ void __launch_bounds__(32) k_wfrag(const float* __restrict__ mlp, uint4* __restrict__ out) {
+  using F = Fr<S>;
+  const int id = blockIdx.x, lane = threadIdx.x, g = lane >> 2, t = lane & 3;
+  int oW, rows, cols, NN, li, lim;
+  bool tr;
+  if (id < F::G_W1) {
+    oW = S::oGW0; rows = S::IN_G; cols = GSB_HID; tr = false; NN = 4; li = id - F::G_W0; lim = 0;
+  } else if (id < F::G_W1T) {
+    oW = S::oGW1; rows = GSB_HID; cols = GSB_HID; tr = false; NN = 4; li = id - F::G_W1; lim = 0;
+  } else if (id < F::G_W0T) {
+    oW = S::oGW1; rows = GSB_HID; cols = GSB_HID; tr = true; NN = 4; li = id - F::G_W1T; lim = GSB_HID;
+  } else if (id < F::C_W0) {
+    oW = S::oGW0; rows = S::IN_G; cols = GSB_HID; tr = true; NN = F::KG; li = id - F::G_W0T; lim = S::IN_G;
+  } else if (id < F::C_W1) {
+    oW = S::oCW0; rows = S::IN_C; cols = GSB_HID; tr = false; NN = 4; li = id - F::C_W0; lim = 0;
+  } else if (id < F::C_W2) {
+    oW = S::oCW1; rows = GSB_HID; cols = GSB_HID; tr = false; NN = 4; li = id - F::C_W1; lim = 0;
+  } else if (id < F::C_W2T) {
+    oW = S::oCW2; rows = GSB_HID; cols = 3; tr = false; NN = 1; li = id - F::C_W2; lim = 0;
+  } else if (id < F::C_W1T) {
+    oW = S::oCW2; rows = GSB_HID; cols = 3; tr = true; NN = 4; li = id - F::C_W2T; lim = GSB_HID;
+  } else if (id < F::C_W0T) {
+    oW = S::oCW1; rows = GSB_HID; cols = GSB_HID; tr = true; NN = 4; li = id - F::C_W1T; lim = GSB_HID;
+  } else {
+    oW = S::oCW0; rows = S::IN_C; cols = GSB_HID; tr = true; NN = F::NCC; li = id - F::C_W0T; lim = S::CC;
+  }
+  const int kk = li / NN, nn = li % NN;
+  const int n = 8 * nn + g;
+  float b[2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int k = 8 * kk + 2 * t + h;
+    float v = 0.f;
+    if (!tr) {
+      if (k < rows && n < cols) v = mlp[oW + k * cols + n];  // W[k][n]
+    } else {
+      if (n < lim && k < cols) v = mlp[oW + n * cols + k];   // W^T[k][n] = W[n][k]
+    }
+    b[h] = v;
+  }
+  uint32_t h0, l0, h1, l1;
+  split_tf32(b[0], h0, l0);
+  split_tf32(b[1], h1, l1);
+  out[id * 32 + lane] = make_uint4(h0, h1, l0, l1);
+}
+
+// ---------------------------------------------------------------------------
+// fragment helpers
+
+__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+
+// A operand from the D fragment of feature block kk
+__device__ __forceinline__ void a_from_d(const float (&x)[4], uint32_t (&ah)[4], uint32_t (&al)[4]) {
+  split_tf32(x[0], ah[0], al[0]);
+  split_tf32(x[2], ah[1], al[1]);
+  split_tf32(x[1], ah[2], al[2]);
+  split_tf32(x[3], ah[3], al[3]);
+}
+
+// A operand from sample-major shared rows (features at off + 8kk + {2t, 2t+1})
+template <int ROW>
+__device__ __forceinline__ void a_from_rows(const float* rows, int off, int m0, int kk,
+                                            uint32_t (&ah)[4], uint32_t (&al)[4]) {
+  const int lane = lane_id(), g = lane >> 2, t = lane & 3;
+  const float2 u = *reinterpret_cast<const float2*>(rows + (m0 + g) * ROW + off + 8 * kk + 2 * t);
+  const float2 v = *reinterpret_cast<const float2*>(rows + (m0 + g + 8) * ROW + off + 8 * kk + 2 * t);
+  split_tf32(u.x, ah[0], al[0]);
+  split_tf32(v.x, ah[1], al[1]);
+  split_tf32(u.y, ah[2], al[2]);
+  split_tf32(v.y, ah[3], al[3]);
+}
+
+// Y[mt][nn] += A(mt, kk) B(kk, nn); B fragments at fr[(kk*NN + nn)*32 + lane]
+template <int MT, int KK, int NN, class AF>
+__device__ __forceinline__ void mma_layer(const AF& afrag, const uint4* fr, float (&Y)[MT][NN][4]) {
+  const int lane = lane_id();
+#pragma unroll
+  for (int kk = 0; kk < KK; ++kk) {
+    uint32_t ah[MT][4], al[MT][4];
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) afrag(mt, kk, ah[mt], al[mt]);
+#pragma unroll
+    for (int nn = 0; nn < NN; ++nn) {
+      const uint4 b = fr[(kk * NN + nn) * 32 + lane];
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) mma3(Y[mt][nn], ah[mt], al[mt], b.x, b.y, b.z, b.w);
+    }
+  }
+}
+
+template <int MT, int NN>
+__device__ __forceinline__ void fill_cols(float (&Y)[MT][NN][4], const float* v) {
+  const int t = lane_id() & 3;
+#pragma unroll
+  for (int nn = 0; nn < NN; ++nn) {
+    const float2 b = *reinterpret_cast<const float2*>(v + 8 * nn + 2 * t);
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) {
+      Y[mt][nn][0] = b.x;
+      Y[mt][nn][1] = b.y;
+      Y[mt][nn][2] = b.x;
+      Y[mt][nn][3] = b.y;
+    }
+  }
+}
+
+template <int MT, int NN>
+__device__ __forceinline__ void zero_d(float (&Y)[MT][NN][4]) {
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+    for (int nn = 0; nn < NN; ++nn)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) Y[mt][nn][r] = 0.f;
+}
+
+// ReLU in place (relu_m semantics: pos ? h : 0), returns the mask bits
+// (bit mt*16 + nn*4 + r)
+template <int MT>
+__device__ __forceinline__ uint32_t relu_d(float (&Y)[MT][4][4]) {
+  uint32_t m = 0u;
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+    for (int nn = 0; nn < 4; ++nn)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const bool pos = Y[mt][nn][r] > 0.f;
+        Y[mt][nn][r] = pos ? Y[mt][nn][r] : 0.f;
+        m |= (uint32_t)pos << (mt * 16 + nn * 4 + r);
+      }
+  return m;
+}
+
+template <int MT>
+__device__ __forceinline__ void mask_d(float (&Y)[MT][4][4], uint32_t m) {
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+    for (int nn = 0; nn < 4; ++nn)
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+        Y[mt][nn][r] = ((m >> (mt * 16 + nn * 4 + r)) & 1u) ? Y[mt][nn][r] : 0.f;
+}
+
+// delta1 = m1 ? W2[col] : 0 (D form)
+template <int MT>
+__device__ __forceinline__ void delta1_d(float (&Y)[MT][4][4], uint32_t m1, const float* w2) {
+  const int t = lane_id() & 3;
+#pragma unroll
+  for (int nn = 0; nn < 4; ++nn) {
+    const float2 w = *reinterpret_cast<const float2*>(w2 + 8 * nn + 2 * t);
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+        Y[mt][nn][r] = ((m1 >> (mt * 16 + nn * 4 + r)) & 1u) ? ((r & 1) ? w.y : w.x) : 0.f;
+  }
+}
+
+// D fragments -> sample-major rows (features at off + 8nn + {2t, 2t+1})
+template <int ROW, int MT, int NN>
+__device__ __forceinline__ void store_d(const float (&Y)[MT][NN][4], float* rows, int off) {
+  const int lane = lane_id(), g = lane >> 2, t = lane & 3;
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+    for (int nn = 0; nn < NN; ++nn) {
+      *reinterpret_cast<float2*>(rows + (16 * mt + g) * ROW + off + 8 * nn + 2 * t) =
+          make_float2(Y[mt][nn][0], Y[mt][nn][1]);
+      *reinterpret_cast<float2*>(rows + (16 * mt + g + 8) * ROW + off + 8 * nn + 2 * t) =
+          make_float2(Y[mt][nn][2], Y[mt][nn][3]);
+    }
+}
+
+// per-sample 32-bit feature mask of a D-form layer for rows g / g+8 of m-tile mt
+// (OR over the quad); valid in every lane of the quad
+__device__ __forceinline__ uint32_t row_mask(uint32_t m, int mt, int half) {
+  const int t = lane_id() & 3;
+  uint32_t r = 0u;
+#pragma unroll
+  for (int nn = 0; nn < 4; ++nn)
+#pragma unroll
+    for (int c = 0; c < 2; ++c)
+      r |= ((m >> (mt * 16 + nn * 4 + 2 * half + c)) & 1u) << (8 * nn + 2 * t + c);
+  r |= __shfl_xor_sync(0xffffffffu, r, 1);
+  r |= __shfl_xor_sync(0xffffffffu, r, 2);
+  return r;
+}
+
+// phi = h1 . W2 + b2 for rows g, g+8 of each m-tile (quad reduction)
+template <int MT>
+__device__ __forceinline__ void phi_d(const float (&h1)[MT][4][4], const float* w2, float b2,
+                                      float (&phi)[MT][2]) {
+  const int t = lane_id() & 3;
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt) {
+    float s0 = 0.f, s1 = 0.f;
+#pragma unroll
+    for (int nn = 0; nn < 4; ++nn) {
+      const float2 w = *reinterpret_cast<const float2*>(w2 + 8 * nn + 2 * t);
+      s0 = fmaf(h1[mt][nn][0], w.x, s0);
+      s0 = fmaf(h1[mt][nn][1], w.y, s0);
+      s1 = fmaf(h1[mt][nn][2], w.x, s1);
+      s1 = fmaf(h1[mt][nn][3], w.y, s1);
+    }
+    s0 += __shfl_xor_sync(0xffffffffu, s0, 1);
+    s1 += __shfl_xor_sync(0xffffffffu, s1, 1);
+    s0 += __shfl_xor_sync(0xffffffffu, s0, 2);
+    s1 += __shfl_xor_sync(0xffffffffu, s1, 2);
+    phi[mt][0] = s0 + b2;
+    phi[mt][1] = s1 + b2;
+  }
+}
+
+// vector block layouts (float offsets in svec; each segment padded to 8)
+struct GVec {
+  static constexpr int b0 = 0, b1 = 32, w2 = 64, b2 = 96, N = 104;
+};
+struct CVec {
+  static constexpr int b0 = 0, b1 = 32, b2 = 64, N = 72;
+};
+
+template <class S>
+__device__ __forceinline__ void stage_gvec(float* svec, const float* __restrict__ mlp, int threads) {
+  for (int i = threadIdx.x; i < GVec::N; i += threads) {
+    float v = 0.f;
+    if (i < 32) v = mlp[S::oGb0 + i];
+    else if (i < 64) v = mlp[S::oGb1 + i - 32];
+    else if (i < 96) v = mlp[S::oGW2 + i - 64];
+    else if (i == 96) v = mlp[S::oGb2];
+    svec[i] = v;
+  }
+}
+template <class S>
+__device__ __forceinline__ void stage_cvec(float* svec, const float* __restrict__ mlp, int threads) {
+  for (int i = threadIdx.x; i < CVec::N; i += threads) {
+    float v = 0.f;
+    if (i < 32) v = mlp[S::oCb0 + i];
+    else if (i < 64) v = mlp[S::oCb1 + i - 32];
+    else if (i < 67) v = mlp[S::oCb2 + i - 64];
+    svec[i] = v;
+  }
+}
+
+template <int WARPS>
+__device__ __forceinline__ void stage_frags(uint4* sfr, const uint4* __restrict__ gfr, int first,
+                                            int count) {
+  for (int i = threadIdx.x; i < count * 32; i += WARPS * 32) sfr[i] = gfr[first * 32 + i];
+}
+
+// ---------------------------------------------------------------------------
+// no-grad SDF at listed samples (importance passes, gs/renderer.py:330-340)
+
+template <class S, int WARPS>
+struct SdfTc {
+  using F = Fr<S>;
+  static constexpr int ROW = 24;  // z (8 KG) ; phi at 16
+  static constexpr int NFR = F::G_W1T;  // G_W0, G_W1
+  static constexpr size_t smem() {
+    return (size_t)NFR * 32 * 16 + GVec::N * 4 + (size_t)WARPS * 32 * ROW * 4;
+  }
+  static_assert(8 * F::KG <= 16, "row layout");
+};
+
+template <class S, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32) k_sdf_eval_tc(Ws<float> w, Geo G, int M, int Nc,
+                                                            const float* __restrict__ mlp,
+                                                            const double* __restrict__ dep,
+                                                            double* __restrict__ phi,
+                                                            const int32_t* __restrict__ list,
+                                                            const int32_t* __restrict__ list_count) {
+  using K = SdfTc<S, WARPS>;
+  using F = Fr<S>;
+  constexpr int ROW = K::ROW;
+  extern __shared__ uint4 smem4[];
+  uint4* sfr = smem4;
+  float* svec = reinterpret_cast<float*>(sfr + K::NFR * 32);
+  float* rows_all = svec + GVec::N;
+  const int lane = lane_id(), wid = threadIdx.x >> 5, g = lane >> 2;
+  const int64_t total = list ? (int64_t)(*list_count) : (int64_t)M * Nc;
+  if ((int64_t)blockIdx.x * WARPS * 32 >= total) return;  // block-uniform
+  stage_frags<WARPS>(sfr, w.wfrag, F::G_W0, K::NFR);
+  stage_gvec<S>(svec, mlp, WARPS * 32);
+  __syncthreads();
+  float* rows = rows_all + wid * 32 * ROW;
+  const int64_t base = ((int64_t)blockIdx.x * WARPS + wid) * 32;
+  if (base >= total) return;  // warp-uniform; no block barrier below
+  const int64_t s = base + lane;
+  const bool act = s < total;
+  int ray = 0, slot = 0;
+  if (act) {
+    if (list) {
+      const int32_t e = list[s];
+      ray = e / GSB_KMAX;
+      slot = e % GSB_KMAX;
+    } else {
+      ray = (int)((uint32_t)s / (uint32_t)Nc);
+      slot = (int)((uint32_t)s % (uint32_t)Nc);
+    }
+  }
+  {
+    const double d = act ? dep[(int64_t)ray * w.ld + slot] : 0.0;
+    float p[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      double x = w.od[ray * 3 + a] + d * w.rd[ray * 3 + a];
+      x = x >= G.lo[a] ? x : G.lo[a];
+      x = x <= G.hi[a] ? x : G.hi[a];
+      p[a] = (float)x;
+    }
+    float z[8 * F::KG];
+#pragma unroll
+    for (int i = S::IN_G; i < 8 * F::KG; ++i) z[i] = 0.f;
+#pragma unroll
+    for (int l = 0; l < S::NL; ++l) {
+      const Loc q = locate<false>(G.lv[l], (double)p[0], (double)p[1], (double)p[2],
+                                  act ? w.status : nullptr);
+      gather_fast<float, S::CG>(G.lv[l], compact<float>(q), z + l * S::CG);
+    }
+    float* my = rows + lane * ROW;
+#pragma unroll
+    for (int i = 0; i < 8 * F::KG; i += 2) *reinterpret_cast<float2*>(my + i) = make_float2(z[i], z[i + 1]);
+  }
+  __syncwarp();
+  float h0[2][4][4], h1[2][4][4];
+  fill_cols(h0, svec + GVec::b0);
+  mma_layer<2, F::KG, 4>(
+      [&](int mt, int kk, uint32_t (&ah)[4], uint32_t (&al)[4]) { a_from_rows<ROW>(rows, 0, 16 * mt, kk, ah, al); },
+      sfr + (F::G_W0 - F::G_W0) * 32, h0);
+  relu_d(h0);
+  fill_cols(h1, svec + GVec::b1);
+  mma_layer<2, 4, 4>([&](int mt, int kk, uint32_t (&ah)[4], uint32_t (&al)[4]) { a_from_d(h0[mt][kk], ah, al); },
+                     sfr + (F::G_W1 - F::G_W0) * 32, h1);
+  relu_d(h1);
+  float ph[2][2];
+  phi_d(h1, svec + GVec::w2, svec[GVec::b2], ph);
+  __syncwarp();
+  if ((lane & 3) == 0) {
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt) {
+      rows[(16 * mt + g) * ROW + 16] = ph[mt][0];
+      rows[(16 * mt + g + 8) * ROW + 16] = ph[mt][1];
+    }
+  }
+  __syncwarp();
+  if (act) phi[(int64_t)ray * w.ld + slot] = (double)rows[lane * ROW + 16];
+}
+
+// ---------------------------------------------------------------------------
+// taped forward: phi, grad phi (gs/renderer.py:356-358), colour (:360-365)
+
+template <class S, int WARPS>
+struct FwdTc {
+  using F = Fr<S>;
+  static constexpr int ROW = 40;
+  static constexpr int oZ = 0;    // z, later dphi/dz (16)
+  static constexpr int oC = 16;   // colour input [f_c, r] (16), later phi at oC
+  static constexpr int oY = 32;   // colour (8 columns)
+  static constexpr int NFR = F::C_W2T;  // geometry (all) + colour forward
+  static constexpr int VEC = GVec::N + CVec::N;
+  static constexpr size_t smem() {
+    return (size_t)NFR * 32 * 16 + VEC * 4 + (size_t)WARPS * 32 * ROW * 4;
+  }
+  static_assert(8 * F::KG <= 16 && 8 * F::KC <= 16 && ROW % 32 == 8, "row layout");
+};
+
+template <class S, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32) k_fwd_tc(Ws<float> w, Geo G, int M, int N,
+                                                       const float* __restrict__ mlp,
+                                                       const double* __restrict__ dep,
+                                                       const float* __restrict__ spts, int nsp) {
+  using K = FwdTc<S, WARPS>;
+  using F = Fr<S>;
+  constexpr int ROW = K::ROW;
+  extern __shared__ uint4 smem4[];
+  uint4* sfr = smem4;
+  float* gvec = reinterpret_cast<float*>(sfr + K::NFR * 32);
+  float* cvec = gvec + GVec::N;
+  float* rows_all = cvec + CVec::N;
+  const int lane = lane_id(), wid = threadIdx.x >> 5, g = lane >> 2;
+  const int64_t MN = (int64_t)M * N, NS = MN + nsp;
+  if ((int64_t)blockIdx.x * WARPS * 32 >= NS) return;
+  stage_frags<WARPS>(sfr, w.wfrag, 0, K::NFR);
+  stage_gvec<S>(gvec, mlp, WARPS * 32);
+  stage_cvec<S>(cvec, mlp, WARPS * 32);
+  __syncthreads();
+  float* rows = rows_all + wid * 32 * ROW;
+  const int64_t base = ((int64_t)blockIdx.x * WARPS + wid) * 32;
+  if (base >= NS) return;
+  const int64_t s = base + lane;
+  const bool act = s < NS;
+  float p[3];
+  int ray = -1;
+  if (act && s < MN) {
+    ray = (int)((uint32_t)s / (uint32_t)N);
+    taped_point<float>(w.o + ray * 3, w.r + ray * 3,
+                       dep[(int64_t)ray * w.ld + (int)((uint32_t)s % (uint32_t)N)], G.lo, G.hi, p);
+  } else if (act) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) p[a] = spts[(s - MN) * 3 + a];
+  } else {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) p[a] = (float)G.lo[a];
+  }
+  LocT<float> loc[S::NL];
+  {
+    float* my = rows + lane * ROW;
+    float z[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) z[i] = 0.f;
+#pragma unroll
+    for (int l = 0; l < S::NL; ++l) {
+      loc[l] = compact<float>(locate<false>(G.lv[l], (double)p[0], (double)p[1], (double)p[2],
+                                            act ? w.status : nullptr));
+      gather_fast<float, S::CG>(G.lv[l], loc[l], z + l * S::CG);
+    }
+#pragma unroll
+    for (int i = 0; i < 16; i += 2) *reinterpret_cast<float2*>(my + K::oZ + i) = make_float2(z[i], z[i + 1]);
+    // colour input: grid features + view direction; smoothness points
+    // (ray < 0) evaluate a harmless colour that is not stored
+    const int cr = ray < 0 ? 0 : ray;
+    const Loc qc = locate<false>(G.col, (double)p[0], (double)p[1], (double)p[2], nullptr);
+    float inp[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) inp[i] = 0.f;
+    gather_fast<float, S::CC>(G.col, compact<float>(qc), inp);
+#pragma unroll
+    for (int a = 0; a < 3; ++a) inp[S::CC + a] = w.r[cr * 3 + a];
+#pragma unroll
+    for (int i = 0; i < 16; i += 2) *reinterpret_cast<float2*>(my + K::oC + i) = make_float2(inp[i], inp[i + 1]);
+  }
+  __syncwarp();
+  // ---- colour: sigmoid(MLP_c([f_c, r]))  (gs/decoders.py:86-99)
+  {
+    float c0[2][4][4], c1[2][4][4], y[2][1][4];
+    fill_cols(c0, cvec + CVec::b0);
+    mma_layer<2, F::KC, 4>(
+        [&](int mt, int kk, uint32_t (&ah)[4], uint32_t (&al)[4]) { a_from_rows<ROW>(rows, K::oC, 16 * mt, kk, ah, al); },
+        sfr + F::C_W0 * 32, c0);
+    relu_d(c0);
+    fill_cols(c1, cvec + CVec::b1);
+    mma_layer<2, 4, 4>([&](int mt, int kk, uint32_t (&ah)[4], uint32_t (&al)[4]) { a_from_d(c0[mt][kk], ah, al); },
+                       sfr + F::C_W1 * 32, c1);
+    relu_d(c1);
+    fill_cols(y, cvec + CVec::b2);
+    mma_layer<2, 4, 1>([&](int mt, int kk, uint32_t (&ah)[4], uint32_t (&al)[4]) { a_from_d(c1[mt][kk], ah, al); },
+                       sfr + F::C_W2 * 32, y);
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) y[mt][0][r] = sigmoid_fast(y[mt][0][r]);
+    store_d<ROW>(y, rows, K::oY);
+  }
+  // ---- geometry: phi and dphi/dz = W0 ((W1 (W2 . m1)) . m0)
+  {
+    float h0[2][4][4], h1[2][4][4];
+    fill_cols(h0, gvec + GVec::b0);
+    mma_layer<2, F::KG, 4>(
+        [&](int mt, int kk, uint32_t (&ah)[4], uint32_t (&al)[4]) { a_from_rows<ROW>(rows, K::oZ, 16 * mt, kk, ah, al); },
+        sfr + F::G_W0 * 32, h0);
+    const uint32_t m0 = relu_d(h0);
+    fill_cols(h1, gvec + GVec::b1);
+    mma_layer<2, 4, 4>([&](int mt, int kk, uint32_t (&ah)[4], uint32_t (&al)[4]) { a_from_d(h0[mt][kk], ah, al); },
+                       sfr + F::G_W1 * 32, h1);
+    const uint32_t m1 = relu_d(h1);
+    float ph[2][2];
+    phi_d(h1, gvec + GVec::w2, gvec[GVec::b2], ph);
+    // delta chain (h0 and h1 registers reused)
+    delta1_d(h1, m1, gvec + GVec::w2);
+    zero_d(h0);
+    mma_layer<2, 4, 4>([&](int mt, int kk, uint32_t (&ah)[4], uint32_t (&al)[4]) { a_from_d(h1[mt][kk], ah, al); },
+                       sfr + F::G_W1T * 32, h0);
+    mask_d(h0, m0);
+    float gz[2][F::KG][4];
+    zero_d(gz);
+    mma_layer<2, 4, F::KG>([&](int mt, int kk, uint32_t (&ah)[4], uint32_t (&al)[4]) { a_from_d(h0[mt][kk], ah, al); },
+                           sfr + F::G_W0T * 32, gz);
+    __syncwarp();  // every lane's z / colour-input reads are done
+    store_d<ROW>(gz, rows, K::oZ);
+    if ((lane & 3) == 0) {
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) {
+        rows[(16 * mt + g) * ROW + K::oC] = ph[mt][0];
+        rows[(16 * mt + g + 8) * ROW + K::oC] = ph[mt][1];
+      }
+    }
+  }
+  __syncwarp();
+  if (!act) return;
+  const float* my = rows + lane * ROW;
+  float gr[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+  for (int l = 0; l < S::NL; ++l) level_dx_fast<float, S::CG>(G.lv[l], loc[l], my + K::oZ + l * S::CG, gr);
+  w.sphi[s] = my[K::oC];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) w.sgphi[s * 3 + a] = gr[a];
+  if (ray >= 0) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) w.scol[s * 3 + c] = my[K::oY + c];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// backward, geometry: grid scatter + MLP weight grads
+
+template <class S, int WARPS>
+struct GeoTc {
+  using F = Fr<S>;
+  static constexpr int ROW = 136;
+  static constexpr int oZ = 0;     // z, later dphi/dz (16)
+  static constexpr int oV = 16;    // v = sum_k ju_k theta_k (16)
+  static constexpr int oA0 = 32;   // p z + v (16)
+  static constexpr int oP = 48;    // p
+  static constexpr int oM = 49;    // m1 bits
+  static constexpr int oB0 = 56;   // delta0 (32)
+  static constexpr int oA1 = 88;   // p h0 + q0 (32)
+  static constexpr int NFR = F::NGEO;
+  static constexpr size_t smem_rows() { return (size_t)WARPS * 32 * ROW * 4; }
+  static constexpr size_t smem() { return (size_t)NFR * 32 * 16 + GVec::N * 4 + smem_rows(); }
+  static_assert(oA1 + GSB_HID <= ROW && ROW % 32 == 8 && S::IN_G <= 16, "row layout");
+};
+
+template <class S, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32) k_bwd_geom_tc(Ws<float> w, Geo G, int M, int N,
+                                                            const float* __restrict__ mlp,
+                                                            const double* __restrict__ dep,
+                                                            const float* __restrict__ spts, int nsp,
+                                                            int agg_levels) {
+  using K = GeoTc<S, WARPS>;
+  using F = Fr<S>;
+  constexpr int ROW = K::ROW;
+  extern __shared__ uint4 smem4[];
+  uint4* sfr = smem4;
+  float* gvec = reinterpret_cast<float*>(sfr + K::NFR * 32);
+  float* rows_all = gvec + GVec::N;
+  const int lane = lane_id(), wid = threadIdx.x >> 5, g = lane >> 2, t = lane & 3;
+  stage_frags<WARPS>(sfr, w.wfrag, F::G_W0, K::NFR);
+  stage_gvec<S>(gvec, mlp, WARPS * 32);
+  __syncthreads();
+  float* rows = rows_all + wid * 32 * ROW;
+  float* myrow = rows + lane * ROW;
+  const int64_t MN = (int64_t)M * N, NS = MN + nsp;
+  const int64_t s = ((int64_t)blockIdx.x * WARPS + wid) * 32 + lane;
+  const bool active = s < NS;
+  // ---- per sample: point, z and v in one pass over the corners
+  float p = 0.f, u[3] = {0.f, 0.f, 0.f};
+  LocT<float> loc[S::NL];
+  {
+    float pt[3];
+    if (active) {
+      p = w.pbar[s];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) u[a] = w.ubar[s * 3 + a];
+      if (s < MN) {
+        const int ray = (int)((uint32_t)s / (uint32_t)N);
+        taped_point<float>(w.o + ray * 3, w.r + ray * 3,
+                           dep[(int64_t)ray * w.ld + (int)((uint32_t)s % (uint32_t)N)], G.lo, G.hi, pt);
+      } else {
+#pragma unroll
+        for (int a = 0; a < 3; ++a) pt[a] = spts[(s - MN) * 3 + a];
+      }
+    } else {
+#pragma unroll
+      for (int a = 0; a < 3; ++a) pt[a] = (float)G.lo[a];
+    }
+    float z[16], v[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) z[i] = v[i] = 0.f;
+#pragma unroll
+    for (int l = 0; l < S::NL; ++l) {
+      const LevelDev& L = G.lv[l];
+      loc[l] = compact<float>(locate<false>(L, (double)pt[0], (double)pt[1], (double)pt[2], nullptr));
+      float wk[8], ju[8];
+      corner_w_ju(loc[l], (float)L.inv_vs, u, wk, ju);
+      const float* Fp = reinterpret_cast<const float*>(L.feat) + (int64_t)loc[l].base * S::CG;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        float row[S::CG];
+        load_row<float, S::CG>(Fp + corner_off(L, k) * S::CG, row);
+#pragma unroll
+        for (int c = 0; c < S::CG; ++c) {
+          z[l * S::CG + c] = fmaf(wk[k], row[c], z[l * S::CG + c]);
+          v[l * S::CG + c] = fmaf(ju[k], row[c], v[l * S::CG + c]);
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 16; i += 2) {
+      *reinterpret_cast<float2*>(myrow + K::oZ + i) = make_float2(z[i], z[i + 1]);
+      *reinterpret_cast<float2*>(myrow + K::oV + i) = make_float2(v[i], v[i + 1]);
+      *reinterpret_cast<float2*>(myrow + K::oA0 + i) =
+          make_float2(fmaf(p, z[i], v[i]), fmaf(p, z[i + 1], v[i + 1]));
+    }
+    myrow[K::oP] = p;
+  }
+  __syncwarp();
+  // ---- MLP on the tensor cores (both m-tiles of the warp's 32 samples)
+  float pr[2][2];  // p of rows g, g+8 per m-tile
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt) {
+    pr[mt][0] = rows[(16 * mt + g) * ROW + K::oP];
+    pr[mt][1] = rows[(16 * mt + g + 8) * ROW + K::oP];
+  }
+  float accb0[4][2], accb1[4][2], accw2[4][2];  // column partial sums (cols 8nn+2t+c)
+  float h0[2][4][4], h1[2][4][4];
+  fill_cols(h0, gvec + GVec::b0);
+  mma_layer<2, F::KG, 4>(
+      [&](int mt, int kk, uint32_t (&ah)[4], uint32_t (&al)[4]) { a_from_rows<ROW>(rows, K::oZ, 16 * mt, kk, ah, al); },
+      sfr + F::G_W0 * 32, h0);
+  const uint32_t m0 = relu_d(h0);
+  fill_cols(h1, gvec + GVec::b1);
+  mma_layer<2, 4, 4>([&](int mt, int kk, uint32_t (&ah)[4], uint32_t (&al)[4]) { a_from_d(h0[mt][kk], ah, al); },
+                     sfr + F::G_W1 * 32, h1);
+  const uint32_t m1 = relu_d(h1);
+  // dW2 += p h1 (column sums); per-sample m1 masks for the dW1 outer product
+#pragma unroll
+  for (int nn = 0; nn < 4; ++nn)
+#pragma unroll
+    for (int c = 0; c < 2; ++c)
+      accw2[nn][c] = pr[0][0] * h1[0][nn][c] + pr[0][1] * h1[0][nn][2 + c] + pr[1][0] * h1[1][nn][c] +
+                     pr[1][1] * h1[1][nn][2 + c];
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int hf = 0; hf < 2; ++hf) {
+      const uint32_t rm = row_mask(m1, mt, hf);
+      if (t == 0) reinterpret_cast<uint32_t*>(rows + (16 * mt + g + 8 * hf) * ROW + K::oM)[0] = rm;
+    }
+  // q0 = (v W0) . m0 ; A1 = p h0 + q0 ; dd1 = (q0 W1) . m1 -> dW2
+  {
+    float q0[2][4][4];
+    zero_d(q0);
+    mma_layer<2, F::KG, 4>(
+        [&](int mt, int kk, uint32_t (&ah)[4], uint32_t (&al)[4]) { a_from_rows<ROW>(rows, K::oV, 16 * mt, kk, ah, al); },
+        sfr + F::G_W0 * 32, q0);
+    mask_d(q0, m0);
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nn = 0; nn < 4; ++nn)
+#pragma unroll
+        for (int r = 0; r < 4; ++r) h0[mt][nn][r] = fmaf(pr[mt][r >> 1], h0[mt][nn][r], q0[mt][nn][r]);
+    store_d<ROW>(h0, rows, K::oA1);
+    zero_d(h1);
+    mma_layer<2, 4, 4>([&](int mt, int kk, uint32_t (&ah)[4], uint32_t (&al)[4]) { a_from_d(q0[mt][kk], ah, al); },
+                       sfr + F::G_W1 * 32, h1);
+    mask_d(h1, m1);
+#pragma unroll
+    for (int nn = 0; nn < 4; ++nn)
+#pragma unroll
+      for (int c = 0; c < 2; ++c)
+        accw2[nn][c] += h1[0][nn][c] + h1[0][nn][2 + c] + h1[1][nn][c] + h1[1][nn][2 + c];
+  }
+  // delta1 = m1 . W2 -> db1 = sum p delta1 ; delta0 = (delta1 W1^T) . m0 -> rows, db0 ;
+  // dphi/dz = delta0 W0^T -> rows (scatter)
+  delta1_d(h1, m1, gvec + GVec::w2);
+#pragma unroll
+  for (int nn = 0; nn < 4; ++nn)
+#pragma unroll
+    for (int c = 0; c < 2; ++c)
+      accb1[nn][c] = pr[0][0] * h1[0][nn][c] + pr[0][1] * h1[0][nn][2 + c] + pr[1][0] * h1[1][nn][c] +
+                     pr[1][1] * h1[1][nn][2 + c];
+  zero_d(h0);
+  mma_layer<2, 4, 4>([&](int mt, int kk, uint32_t (&ah)[4], uint32_t (&al)[4]) { a_from_d(h1[mt][kk], ah, al); },
+                     sfr + F::G_W1T * 32, h0);
+  mask_d(h0, m0);
+#pragma unroll
+  for (int nn = 0; nn < 4; ++nn)
+#pragma unroll
+    for (int c = 0; c < 2; ++c)
+      accb0[nn][c] = pr[0][0] * h0[0][nn][c] + pr[0][1] * h0[0][nn][2 + c] + pr[1][0] * h0[1][nn][c] +
+                     pr[1][1] * h0[1][nn][2 + c];
+  store_d<ROW>(h0, rows, K::oB0);
+  {
+    float gz[2][F::KG][4];
+    zero_d(gz);
+    mma_layer<2, 4, F::KG>([&](int mt, int kk, uint32_t (&ah)[4], uint32_t (&al)[4]) { a_from_d(h0[mt][kk], ah, al); },
+                           sfr + F::G_W0T * 32, gz);
+    __syncwarp();  // z reads (first layer) are done in every lane
+    store_d<ROW>(gz, rows, K::oZ);
+  }
+  __syncwarp();
+  // ---- grid scatter: theta_l[idx_k] += g_l (p w_k + ju_k)
+#pragma unroll
+  for (int l = 0; l < S::NL; ++l) {
+    float wk[8], ju[8], coef[8];
+    corner_w_ju(loc[l], (float)G.lv[l].inv_vs, u, wk, ju);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) coef[k] = fmaf(p, wk[k], ju[k]);
+    scatter_level<float, S::CG>(G.lv[l], loc[l], myrow + K::oZ + l * S::CG, coef, active, l < agg_levels);
+  }
+  // ---- outer products over the warp's samples: dW0 += A0^T delta0, dW1 += A1^T delta1
+  float d0[4][4], d1[2][4][4];
+#pragma unroll
+  for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      d0[nt][c] = 0.f;
+      d1[0][nt][c] = 0.f;
+      d1[1][nt][c] = 0.f;
+    }
+  const float w2l = gvec[GVec::w2 + lane];
+#pragma unroll
+  for (int ks = 0; ks < 4; ++ks) {
+    const int k0 = ks * 8;
+    const uint32_t mk0 = reinterpret_cast<const uint32_t*>(rows + (k0 + t) * ROW + K::oM)[0];
+    const uint32_t mk1 = reinterpret_cast<const uint32_t*>(rows + (k0 + t + 4) * ROW + K::oM)[0];
+    uint32_t ah[4], al[4];
+    frag_a(rows, ROW, K::oA0, k0, 0, ah, al);
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) {
+      uint32_t bh0, bh1, bl0, bl1;
+      frag_b(rows, ROW, K::oB0, k0, nt * 8, bh0, bh1, bl0, bl1);
+      mma3(d0[nt], ah, al, bh0, bh1, bl0, bl1);
+    }
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt) {
+      frag_a(rows, ROW, K::oA1, k0, mt * 16, ah, al);
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) {
+        const int n = nt * 8 + g;
+        const float w2n = __shfl_sync(0xffffffffu, w2l, n);
+        const float b0v = ((mk0 >> n) & 1u) ? w2n : 0.f;
+        const float b1v = ((mk1 >> n) & 1u) ? w2n : 0.f;
+        uint32_t bh0, bh1, bl0, bl1;
+        split_tf32(b0v, bh0, bl0);
+        split_tf32(b1v, bh1, bl1);
+        mma3(d1[mt][nt], ah, al, bh0, bh1, bl0, bl1);
+      }
+    }
+  }
+  // column sums over the warp: reduce the 8 lanes sharing t
+#pragma unroll
+  for (int nn = 0; nn < 4; ++nn)
+#pragma unroll
+    for (int c = 0; c < 2; ++c)
+#pragma unroll
+      for (int o = 4; o < 32; o <<= 1) {
+        accb0[nn][c] += __shfl_xor_sync(0xffffffffu, accb0[nn][c], o);
+        accb1[nn][c] += __shfl_xor_sync(0xffffffffu, accb1[nn][c], o);
+        accw2[nn][c] += __shfl_xor_sync(0xffffffffu, accw2[nn][c], o);
+      }
+  float accp = p;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) accp += __shfl_xor_sync(0xffffffffu, accp, o);
+  // ---- CTA reduction -> partial slot blockIdx.x (geometry block of the MLP)
+  __syncthreads();
+  constexpr int NGP = S::NG;
+  float* red = rows_all;  // [WARPS][NGP] over the (now free) rows
+  {
+    float* mine = red + (size_t)wid * NGP;
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) frag_d_store(d0[nt], mine + S::oGW0, 0, nt * 8, S::IN_G);
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) frag_d_store(d1[mt][nt], mine + S::oGW1, mt * 16, nt * 8, GSB_HID);
+    if (g == 0) {
+#pragma unroll
+      for (int nn = 0; nn < 4; ++nn)
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          mine[S::oGb0 + 8 * nn + 2 * t + c] = accb0[nn][c];
+          mine[S::oGb1 + 8 * nn + 2 * t + c] = accb1[nn][c];
+          mine[S::oGW2 + 8 * nn + 2 * t + c] = accw2[nn][c];
+        }
+    }
+    if (lane == 0) mine[S::oGb2] = accp;
+  }
+  __syncthreads();
+  float* out = w.mlp_part + (size_t)blockIdx.x * S::NMLP;
+  for (int i = threadIdx.x; i < NGP; i += WARPS * 32) {
+    float a = 0.f;
+#pragma unroll
+    for (int k = 0; k < WARPS; ++k) a += red[(size_t)k * NGP + i];
+    out[i] = a;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// backward, colour
+
+template <class S, int WARPS>
+struct ColTc {
+  using F = Fr<S>;
+  static constexpr int ROW = 168;
+  static constexpr int oA0 = 0;     // [inp (IN_C), 1, 0...] (16)
+  static constexpr int oB0 = 16;    // a0_bar (32)
+  static constexpr int oA1 = 48;    // h0c (32)
+  static constexpr int oB1 = 80;    // a1_bar (32)
+  static constexpr int oH1 = 112;   // h1c (32)
+  static constexpr int oY = 144;    // y_bar (8 columns, 3 used)
+  static constexpr int oFB = 152;   // f_bar (8 columns, CC used)
+  static constexpr int NFR = F::NALL - F::NGEO;
+  static constexpr size_t smem_rows() { return (size_t)WARPS * 32 * ROW * 4; }
+  static constexpr size_t smem() { return (size_t)NFR * 32 * 16 + CVec::N * 4 + smem_rows(); }
+  static_assert(oFB + 8 <= ROW && ROW % 32 == 8 && S::IN_C + 1 <= 16 && S::CC <= 8, "row layout");
+};
+
+template <class S, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32) k_bwd_color_tc(Ws<float> w, Geo G, int M, int N,
+                                                             const float* __restrict__ mlp,
+                                                             const double* __restrict__ dep) {
+  using K = ColTc<S, WARPS>;
+  using F = Fr<S>;
+  constexpr int ROW = K::ROW;
+  extern __shared__ uint4 smem4[];
+  uint4* sfr = smem4;  // fragment ids F::C_W0.. at index (id - NGEO)
+  float* cvec = reinterpret_cast<float*>(sfr + K::NFR * 32);
+  float* rows_all = cvec + CVec::N;
+  const int lane = lane_id(), wid = threadIdx.x >> 5, g = lane >> 2, t = lane & 3;
+  stage_frags<WARPS>(sfr, w.wfrag, F::NGEO, K::NFR);
+  stage_cvec<S>(cvec, mlp, WARPS * 32);
+  __syncthreads();
+  const uint4* fr = sfr - F::NGEO * 32;  // index by global fragment id
+  float* rows = rows_all + wid * 32 * ROW;
+  float* myrow = rows + lane * ROW;
+  const int64_t NS = (int64_t)M * N;
+  const int64_t base = ((int64_t)blockIdx.x * WARPS + wid) * 32;
+  const int64_t s = base + lane;
+  const bool active = s < NS;
+  const int ray = active ? (int)((uint32_t)s / (uint32_t)N) : 0;
+  LocT<float> q;
+  {
+    float pt[3];
+    taped_point<float>(w.o + ray * 3, w.r + ray * 3,
+                       active ? dep[(int64_t)ray * w.ld + (int)((uint32_t)s % (uint32_t)N)] : 0.0,
+                       G.lo, G.hi, pt);
+    q = compact<float>(locate<false>(G.col, (double)pt[0], (double)pt[1], (double)pt[2], nullptr));
+    float inp[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) inp[i] = 0.f;
+    gather_fast<float, S::CC>(G.col, q, inp);
+#pragma unroll
+    for (int a = 0; a < 3; ++a) inp[S::CC + a] = w.r[ray * 3 + a];
+    inp[S::IN_C] = 1.f;  // ones column: db0c rides on the dW0c outer product
+#pragma unroll
+    for (int i = 0; i < 16; i += 2) *reinterpret_cast<float2*>(myrow + K::oA0 + i) = make_float2(inp[i], inp[i + 1]);
+  }
+  __syncwarp();
+  // ---- forward (masks, h0c, h1c) and y_bar = cbar * y (1 - y)
+  float c0[2][4][4], c1[2][4][4];
+  fill_cols(c0, cvec + CVec::b0);
+  mma_layer<2, F::KC, 4>(
+      [&](int mt, int kk, uint32_t (&ah)[4], uint32_t (&al)[4]) { a_from_rows<ROW>(rows, K::oA0, 16 * mt, kk, ah, al); },
+      fr + F::C_W0 * 32, c0);
+  const uint32_t m0 = relu_d(c0);
+  store_d<ROW>(c0, rows, K::oA1);
+  fill_cols(c1, cvec + CVec::b1);
+  mma_layer<2, 4, 4>([&](int mt, int kk, uint32_t (&ah)[4], uint32_t (&al)[4]) { a_from_d(c0[mt][kk], ah, al); },
+                     fr + F::C_W1 * 32, c1);
+  const uint32_t m1 = relu_d(c1);
+  store_d<ROW>(c1, rows, K::oH1);
+  float yb[2][1][4];
+  fill_cols(yb, cvec + CVec::b2);
+  mma_layer<2, 4, 1>([&](int mt, int kk, uint32_t (&ah)[4], uint32_t (&al)[4]) { a_from_d(c1[mt][kk], ah, al); },
+                     fr + F::C_W2 * 32, yb);
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int col = 2 * t + (r & 1);
+      const int64_t sr = base + 16 * mt + g + 8 * (r >> 1);
+      const float cc = sigmoid_fast(yb[mt][0][r]);
+      yb[mt][0][r] = (col < 3 && sr < NS) ? w.cbar[sr * 3 + col] * (cc * (1.f - cc)) : 0.f;
+    }
+  store_d<ROW>(yb, rows, K::oY);
+  // a1_bar = (y_bar W2c^T) . m1 ; a0_bar = (a1_bar W1c^T) . m0 ; f_bar = a0_bar W0c^T
+  zero_d(c1);
+  mma_layer<2, 1, 4>([&](int mt, int kk, uint32_t (&ah)[4], uint32_t (&al)[4]) { a_from_d(yb[mt][kk], ah, al); },
+                     fr + F::C_W2T * 32, c1);
+  mask_d(c1, m1);
+  store_d<ROW>(c1, rows, K::oB1);
+  zero_d(c0);
+  mma_layer<2, 4, 4>([&](int mt, int kk, uint32_t (&ah)[4], uint32_t (&al)[4]) { a_from_d(c1[mt][kk], ah, al); },
+                     fr + F::C_W1T * 32, c0);
+  mask_d(c0, m0);
+  store_d<ROW>(c0, rows, K::oB0);
+  {
+    float fb[2][F::NCC][4];
+    zero_d(fb);
+    mma_layer<2, 4, F::NCC>([&](int mt, int kk, uint32_t (&ah)[4], uint32_t (&al)[4]) { a_from_d(c0[mt][kk], ah, al); },
+                            fr + F::C_W0T * 32, fb);
+    store_d<ROW>(fb, rows, K::oFB);
+  }
+  __syncwarp();
+  {  // colour grid scatter: theta_c[idx_k] += w_k f_bar (warp-segmented)
+    float wk[8];
+    corner_w(q, wk);
+    scatter_level<float, S::CC>(G.col, q, myrow + K::oFB, wk, active, false);
+  }
+  // ---- outer products: e0 = [inp,1]^T a0b, e1 = h0c^T a1b, e2 = h1c^T y_bar
+  float e0[4][4], e1[2][4][4], e2[2][4];
+#pragma unroll
+  for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      e0[nt][c] = 0.f;
+      e1[0][nt][c] = 0.f;
+      e1[1][nt][c] = 0.f;
+    }
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) e2[mt][c] = 0.f;
+#pragma unroll
+  for (int ks = 0; ks < 4; ++ks) {
+    const int k0 = ks * 8;
+    uint32_t ah[4], al[4];
+    frag_a(rows, ROW, K::oA0, k0, 0, ah, al);
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) {
+      uint32_t bh0, bh1, bl0, bl1;
+      frag_b(rows, ROW, K::oB0, k0, nt * 8, bh0, bh1, bl0, bl1);
+      mma3(e0[nt], ah, al, bh0, bh1, bl0, bl1);
+    }
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt) {
+      frag_a(rows, ROW, K::oA1, k0, mt * 16, ah, al);
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) {
+        uint32_t bh0, bh1, bl0, bl1;
+        frag_b(rows, ROW, K::oB1, k0, nt * 8, bh0, bh1, bl0, bl1);
+        mma3(e1[mt][nt], ah, al, bh0, bh1, bl0, bl1);
+      }
+      frag_a(rows, ROW, K::oH1, k0, mt * 16, ah, al);
+      uint32_t bh0, bh1, bl0, bl1;
+      frag_b(rows, ROW, K::oY, k0, 0, bh0, bh1, bl0, bl1);
+      mma3(e2[mt], ah, al, bh0, bh1, bl0, bl1);
+    }
+  }
+  float acc_b1 = 0.f, acc_b2 = 0.f;
+#pragma unroll 4
+  for (int r = 0; r < 32; ++r) {
+    const float* rw = rows + (size_t)r * ROW;
+    acc_b1 += rw[K::oB1 + lane];                       // db1 = sum a1_bar
+    acc_b2 += lane < 3 ? rw[K::oY + lane] : 0.f;        // db2 = sum y_bar
+  }
+  __syncthreads();
+  constexpr int NCP = S::NMLP - S::NG;
+  float* red = rows_all;
+  {
+    float* mine = red + (size_t)wid * NCP;
+    const int o = S::NG;
+    if (lane < S::oCW0 - S::NG) mine[lane] = 0.f;  // alignment padding
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) frag_d_store(e0[nt], mine + (S::oCW0 - o), 0, nt * 8, S::IN_C + 1);
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) frag_d_store(e1[mt][nt], mine + (S::oCW1 - o), mt * 16, nt * 8, GSB_HID);
+    mine[S::oCb1 - o + lane] = acc_b1;
+    if (lane < 3) mine[S::oCb2 - o + lane] = acc_b2;
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt) {
+      const int r0 = mt * 16 + g, r1 = r0 + 8, c = 2 * t;
+      if (c < 3) {
+        mine[S::oCW2 - o + r0 * 3 + c] = e2[mt][0];
+        mine[S::oCW2 - o + r1 * 3 + c] = e2[mt][2];
+      }
+      if (c + 1 < 3) {
+        mine[S::oCW2 - o + r0 * 3 + c + 1] = e2[mt][1];
+        mine[S::oCW2 - o + r1 * 3 + c + 1] = e2[mt][3];
+      }
+    }
+  }
+  __syncthreads();
+  float* out = w.mlp_part + (size_t)blockIdx.x * S::NMLP + S::NG;
+  for (int i = threadIdx.x; i < NCP; i += WARPS * 32) {
+    float a = 0.f;
+#pragma unroll
+    for (int k = 0; k < WARPS; ++k) a += red[(size_t)k * NCP + i];
+    out[i] = a;
+  }
+}
+
+}  // namespace tc
+}  // namespace gsb
