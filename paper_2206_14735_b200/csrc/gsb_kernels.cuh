@@ -986,13 +986,19 @@ __device__ __forceinline__ void scatter_level(const LevelDev& L, const LocT<T>& 
   // end of my run (exclusive): next head after `lane`, or 32
   const unsigned after = lane == 31 ? 0u : (heads >> (lane + 1));
   const int run_end = after ? lane + __ffs(after) : 32;
+  // scan steps bounded by the warp's longest run (fine levels: 1-2 lanes)
+  const int maxrun = (int)__reduce_max_sync(full, head ? (unsigned)(run_end - lane) : 0u);
+  T gv[C];
+#pragma unroll
+  for (int c = 0; c < C; ++c) gv[c] = active ? gl[c] : T(0);
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
     T v[C];
 #pragma unroll
-    for (int c = 0; c < C; ++c) v[c] = active ? gl[c] * coef[k] : T(0);
+    for (int c = 0; c < C; ++c) v[c] = gv[c] * coef[k];
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
+      if (o >= maxrun) break;
 #pragma unroll
       for (int c = 0; c < C; ++c) {
         const T y = __shfl_down_sync(full, v[c], o);

@@ -42,7 +42,8 @@ int run_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step
   constexpr int TW = 4;                  // warps per CTA of the float32 sample kernels
   const float* mlp32 = reinterpret_cast<const float*>(mlp);
   if constexpr (F32) {
-    tc::k_wfrag<S><<<tc::Fr<S>::NALL, 32, 0, stream>>>(mlp32, w.wfrag);
+    static_assert(tc::kFragBufU4 == 4096 + 44, "workspace carve");
+    tc::k_wfrag<S><<<tc::Fr<S>::NALL + 1, 32, 0, stream>>>(mlp32, w.wfrag);
     GSB_LAUNCHED_T("k_wfrag");
   }
   const size_t smem_sdf = (size_t)S::NG * esz;

@@ -27,6 +27,58 @@ namespace gsb {
 namespace tc {
 
 constexpr int kFragMax = 128;  // B fragments per model (446 shape: 100)
+constexpr int kVecBase = kFragMax * 32;  // uint4 index of the vector block in the buffer
+
+// vector block (floats; segments padded to 8): geometry b0, b1, W2, b2 then
+// colour b0c, b1c, b2c
+struct GVec {
+  static constexpr int b0 = 0, b1 = 32, w2 = 64, b2 = 96, N = 104;
+};
+struct CVec {
+  static constexpr int b0 = 0, b1 = 32, b2 = 64, N = 72;
+};
+constexpr int kFragBufU4 = kVecBase + (GVec::N + CVec::N) / 4;
+
+// ---- one-shot TMA bulk staging (cp.async.bulk + mbarrier transaction count)
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  }
+}
+// thread 0: stage fragments [first, first + count) to sfr and `nvec` floats of
+// the vector block (from float offset voff) to svec; all threads later mbar_wait
+__device__ __forceinline__ void stage_async(uint64_t* bar, uint4* sfr, const uint4* gbuf, int first,
+                                            int count, float* svec, int voff, int nvec) {
+  if (threadIdx.x == 0) {
+    const uint32_t fb = (uint32_t)count * 32u * 16u, vb = (uint32_t)nvec * 4u;
+    mbar_expect(bar, fb + vb);
+    bulk_g2s(sfr, gbuf + first * 32, fb, bar);
+    bulk_g2s(svec, reinterpret_cast<const float*>(gbuf + kVecBase) + voff, vb, bar);
+  }
+}
 
 // B-fragment ids (each = 32 lanes x uint4 {hi0, hi1, lo0, lo1})
 template <class S>
@@ -55,6 +107,25 @@ template <class S>
 __global__ void __launch_bounds__(32) k_wfrag(const float* __restrict__ mlp, uint4* __restrict__ out) {
   using F = Fr<S>;
   const int id = blockIdx.x, lane = threadIdx.x, g = lane >> 2, t = lane & 3;
+  if (id == F::NALL) {  // bias / W2 vectors: geometry block then colour block
+    float* v = reinterpret_cast<float*>(out + kVecBase);
+    for (int i = lane; i < GVec::N + CVec::N; i += 32) {
+      float x = 0.f;
+      if (i < GVec::N) {
+        if (i < 32) x = mlp[S::oGb0 + i];
+        else if (i < 64) x = mlp[S::oGb1 + i - 32];
+        else if (i < 96) x = mlp[S::oGW2 + i - 64];
+        else if (i == 96) x = mlp[S::oGb2];
+      } else {
+        const int j = i - GVec::N;
+        if (j < 32) x = mlp[S::oCb0 + j];
+        else if (j < 64) x = mlp[S::oCb1 + j - 32];
+        else if (j < 67) x = mlp[S::oCb2 + j - 64];
+      }
+      v[i] = x;
+    }
+    return;
+  }
   int oW, rows, cols, NN, li, lim;
   bool tr;
   if (id < F::G_W1) {
@@ -267,42 +338,6 @@ __device__ __forceinline__ void phi_d(const float (&h1)[MT][4][4], const float* 
   }
 }
 
-// vector block layouts (float offsets in svec; each segment padded to 8)
-struct GVec {
-  static constexpr int b0 = 0, b1 = 32, w2 = 64, b2 = 96, N = 104;
-};
-struct CVec {
-  static constexpr int b0 = 0, b1 = 32, b2 = 64, N = 72;
-};
-
-template <class S>
-__device__ __forceinline__ void stage_gvec(float* svec, const float* __restrict__ mlp, int threads) {
-  for (int i = threadIdx.x; i < GVec::N; i += threads) {
-    float v = 0.f;
-    if (i < 32) v = mlp[S::oGb0 + i];
-    else if (i < 64) v = mlp[S::oGb1 + i - 32];
-    else if (i < 96) v = mlp[S::oGW2 + i - 64];
-    else if (i == 96) v = mlp[S::oGb2];
-    svec[i] = v;
-  }
-}
-template <class S>
-__device__ __forceinline__ void stage_cvec(float* svec, const float* __restrict__ mlp, int threads) {
-  for (int i = threadIdx.x; i < CVec::N; i += threads) {
-    float v = 0.f;
-    if (i < 32) v = mlp[S::oCb0 + i];
-    else if (i < 64) v = mlp[S::oCb1 + i - 32];
-    else if (i < 67) v = mlp[S::oCb2 + i - 64];
-    svec[i] = v;
-  }
-}
-
-template <int WARPS>
-__device__ __forceinline__ void stage_frags(uint4* sfr, const uint4* __restrict__ gfr, int first,
-                                            int count) {
-  for (int i = threadIdx.x; i < count * 32; i += WARPS * 32) sfr[i] = gfr[first * 32 + i];
-}
-
 // ---------------------------------------------------------------------------
 // no-grad SDF at listed samples (importance passes, gs/renderer.py:330-340)
 
@@ -334,9 +369,10 @@ __global__ void __launch_bounds__(WARPS * 32) k_sdf_eval_tc(Ws<float> w, Geo G, 
   const int lane = lane_id(), wid = threadIdx.x >> 5, g = lane >> 2;
   const int64_t total = list ? (int64_t)(*list_count) : (int64_t)M * Nc;
   if ((int64_t)blockIdx.x * WARPS * 32 >= total) return;  // block-uniform
-  stage_frags<WARPS>(sfr, w.wfrag, F::G_W0, K::NFR);
-  stage_gvec<S>(svec, mlp, WARPS * 32);
+  __shared__ __align__(8) uint64_t s_bar;
+  if (threadIdx.x == 0) mbar_init(&s_bar);
   __syncthreads();
+  stage_async(&s_bar, sfr, w.wfrag, F::G_W0, K::NFR, svec, 0, GVec::N);
   float* rows = rows_all + wid * 32 * ROW;
   const int64_t base = ((int64_t)blockIdx.x * WARPS + wid) * 32;
   if (base >= total) return;  // warp-uniform; no block barrier below
@@ -376,6 +412,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_sdf_eval_tc(Ws<float> w, Geo G, 
 #pragma unroll
     for (int i = 0; i < 8 * F::KG; i += 2) *reinterpret_cast<float2*>(my + i) = make_float2(z[i], z[i + 1]);
   }
+  mbar_wait(&s_bar, 0);
   __syncwarp();
   float h0[2][4][4], h1[2][4][4];
   fill_cols(h0, svec + GVec::b0);
@@ -435,10 +472,10 @@ __global__ void __launch_bounds__(WARPS * 32) k_fwd_tc(Ws<float> w, Geo G, int M
   const int lane = lane_id(), wid = threadIdx.x >> 5, g = lane >> 2;
   const int64_t MN = (int64_t)M * N, NS = MN + nsp;
   if ((int64_t)blockIdx.x * WARPS * 32 >= NS) return;
-  stage_frags<WARPS>(sfr, w.wfrag, 0, K::NFR);
-  stage_gvec<S>(gvec, mlp, WARPS * 32);
-  stage_cvec<S>(cvec, mlp, WARPS * 32);
+  __shared__ __align__(8) uint64_t s_bar;
+  if (threadIdx.x == 0) mbar_init(&s_bar);
   __syncthreads();
+  stage_async(&s_bar, sfr, w.wfrag, 0, K::NFR, gvec, 0, GVec::N + CVec::N);
   float* rows = rows_all + wid * 32 * ROW;
   const int64_t base = ((int64_t)blockIdx.x * WARPS + wid) * 32;
   if (base >= NS) return;
@@ -484,6 +521,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_fwd_tc(Ws<float> w, Geo G, int M
 #pragma unroll
     for (int i = 0; i < 16; i += 2) *reinterpret_cast<float2*>(my + K::oC + i) = make_float2(inp[i], inp[i + 1]);
   }
+  mbar_wait(&s_bar, 0);
   __syncwarp();
   // ---- colour: sigmoid(MLP_c([f_c, r]))  (gs/decoders.py:86-99)
   {
@@ -589,9 +627,10 @@ __global__ void __launch_bounds__(WARPS * 32) k_bwd_geom_tc(Ws<float> w, Geo G, 
   float* gvec = reinterpret_cast<float*>(sfr + K::NFR * 32);
   float* rows_all = gvec + GVec::N;
   const int lane = lane_id(), wid = threadIdx.x >> 5, g = lane >> 2, t = lane & 3;
-  stage_frags<WARPS>(sfr, w.wfrag, F::G_W0, K::NFR);
-  stage_gvec<S>(gvec, mlp, WARPS * 32);
+  __shared__ __align__(8) uint64_t s_bar;
+  if (threadIdx.x == 0) mbar_init(&s_bar);
   __syncthreads();
+  stage_async(&s_bar, sfr, w.wfrag, F::G_W0, K::NFR, gvec, 0, GVec::N);
   float* rows = rows_all + wid * 32 * ROW;
   float* myrow = rows + lane * ROW;
   const int64_t MN = (int64_t)M * N, NS = MN + nsp;
@@ -648,6 +687,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_bwd_geom_tc(Ws<float> w, Geo G, 
     }
     myrow[K::oP] = p;
   }
+  mbar_wait(&s_bar, 0);
   __syncwarp();
   // ---- MLP on the tensor cores (both m-tiles of the warp's 32 samples)
   float pr[2][2];  // p of rows g, g+8 per m-tile
@@ -864,9 +904,10 @@ __global__ void __launch_bounds__(WARPS * 32) k_bwd_color_tc(Ws<float> w, Geo G,
   float* cvec = reinterpret_cast<float*>(sfr + K::NFR * 32);
   float* rows_all = cvec + CVec::N;
   const int lane = lane_id(), wid = threadIdx.x >> 5, g = lane >> 2, t = lane & 3;
-  stage_frags<WARPS>(sfr, w.wfrag, F::NGEO, K::NFR);
-  stage_cvec<S>(cvec, mlp, WARPS * 32);
+  __shared__ __align__(8) uint64_t s_bar;
+  if (threadIdx.x == 0) mbar_init(&s_bar);
   __syncthreads();
+  stage_async(&s_bar, sfr, w.wfrag, F::NGEO, K::NFR, cvec, GVec::N, CVec::N);
   const uint4* fr = sfr - F::NGEO * 32;  // index by global fragment id
   float* rows = rows_all + wid * 32 * ROW;
   float* myrow = rows + lane * ROW;
@@ -892,6 +933,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_bwd_color_tc(Ws<float> w, Geo G,
 #pragma unroll
     for (int i = 0; i < 16; i += 2) *reinterpret_cast<float2*>(myrow + K::oA0 + i) = make_float2(inp[i], inp[i + 1]);
   }
+  mbar_wait(&s_bar, 0);
   __syncwarp();
   // ---- forward (masks, h0c, h1c) and y_bar = cbar * y (1 - y)
   float c0[2][4][4], c1[2][4][4];
