@@ -204,13 +204,44 @@ __device__ __forceinline__ void mma_layer(const AF& afrag, const uint4* fr, floa
     uint32_t ah[MT][4], al[MT][4];
 #pragma unroll
     for (int mt = 0; mt < MT; ++mt) afrag(mt, kk, ah[mt], al[mt]);
+    uint4 b[NN];
 #pragma unroll
-    for (int nn = 0; nn < NN; ++nn) {
-      const uint4 b = fr[(kk * NN + nn) * 32 + lane];
+    for (int nn = 0; nn < NN; ++nn) b[nn] = fr[(kk * NN + nn) * 32 + lane];
+    // three passes (lo*hi, hi*lo, hi*hi), each sweeping the MT x NN independent
+    // accumulators, so consecutive MMAs never wait on each other
 #pragma unroll
-      for (int mt = 0; mt < MT; ++mt) mma3(Y[mt][nn], ah[mt], al[mt], b.x, b.y, b.z, b.w);
-    }
+    for (int nn = 0; nn < NN; ++nn)
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) mma_tf32(Y[mt][nn], al[mt], b[nn].x, b[nn].y);
+#pragma unroll
+    for (int nn = 0; nn < NN; ++nn)
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) mma_tf32(Y[mt][nn], ah[mt], b[nn].z, b[nn].w);
+#pragma unroll
+    for (int nn = 0; nn < NN; ++nn)
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) mma_tf32(Y[mt][nn], ah[mt], b[nn].x, b[nn].y);
   }
+}
+
+// D[mt][nt] += A[mt] B[nt] in 3xTF32, pass-interleaved over the MT x NT tiles
+template <int MT, int NT>
+__device__ __forceinline__ void mma3_sweep(float (&D)[MT][NT][4], const uint32_t (&ah)[MT][4],
+                                           const uint32_t (&al)[MT][4], const uint32_t (&bh0)[NT],
+                                           const uint32_t (&bh1)[NT], const uint32_t (&bl0)[NT],
+                                           const uint32_t (&bl1)[NT]) {
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) mma_tf32(D[mt][nt], al[mt], bh0[nt], bh1[nt]);
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) mma_tf32(D[mt][nt], ah[mt], bl0[nt], bl1[nt]);
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) mma_tf32(D[mt][nt], ah[mt], bh0[nt], bh1[nt]);
 }
 
 template <int MT, int NN>
@@ -295,6 +326,23 @@ __device__ __forceinline__ void store_d(const float (&Y)[MT][NN][4], float* rows
           make_float2(Y[mt][nn][0], Y[mt][nn][1]);
       *reinterpret_cast<float2*>(rows + (16 * mt + g + 8) * ROW + off + 8 * nn + 2 * t) =
           make_float2(Y[mt][nn][2], Y[mt][nn][3]);
+    }
+}
+
+// sample-major rows -> D fragments (inverse of store_d)
+template <int ROW, int MT, int NN>
+__device__ __forceinline__ void load_d(float (&Y)[MT][NN][4], const float* rows, int off) {
+  const int lane = lane_id(), g = lane >> 2, t = lane & 3;
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+    for (int nn = 0; nn < NN; ++nn) {
+      const float2 a = *reinterpret_cast<const float2*>(rows + (16 * mt + g) * ROW + off + 8 * nn + 2 * t);
+      const float2 b = *reinterpret_cast<const float2*>(rows + (16 * mt + g + 8) * ROW + off + 8 * nn + 2 * t);
+      Y[mt][nn][0] = a.x;
+      Y[mt][nn][1] = a.y;
+      Y[mt][nn][2] = b.x;
+      Y[mt][nn][3] = b.y;
     }
 }
 
@@ -607,10 +655,11 @@ struct GeoTc {
   static constexpr int oM = 49;    // m1 bits
   static constexpr int oB0 = 56;   // delta0 (32)
   static constexpr int oA1 = 88;   // p h0 + q0 (32)
+  static constexpr int oL = 120;   // grid locations, 4 per level (base bits, fx, fy, fz)
   static constexpr int NFR = F::NGEO;
   static constexpr size_t smem_rows() { return (size_t)WARPS * 32 * ROW * 4; }
   static constexpr size_t smem() { return (size_t)NFR * 32 * 16 + GVec::N * 4 + smem_rows(); }
-  static_assert(oA1 + GSB_HID <= ROW && ROW % 32 == 8 && S::IN_G <= 16, "row layout");
+  static_assert(oL + 4 * S::NL <= ROW && ROW % 32 == 8 && S::IN_G <= 16, "row layout");
 };
 
 template <class S, int WARPS>
@@ -636,10 +685,10 @@ __global__ void __launch_bounds__(WARPS * 32) k_bwd_geom_tc(Ws<float> w, Geo G, 
   const int64_t MN = (int64_t)M * N, NS = MN + nsp;
   const int64_t s = ((int64_t)blockIdx.x * WARPS + wid) * 32 + lane;
   const bool active = s < NS;
-  // ---- per sample: point, z and v in one pass over the corners
-  float p = 0.f, u[3] = {0.f, 0.f, 0.f};
-  LocT<float> loc[S::NL];
+  // ---- per sample: point, z and v in one pass over the corners; the grid
+  // locations wait in the row (registers are the MLP phase's)
   {
+    float p = 0.f, u[3] = {0.f, 0.f, 0.f};
     float pt[3];
     if (active) {
       p = w.pbar[s];
@@ -663,10 +712,11 @@ __global__ void __launch_bounds__(WARPS * 32) k_bwd_geom_tc(Ws<float> w, Geo G, 
 #pragma unroll
     for (int l = 0; l < S::NL; ++l) {
       const LevelDev& L = G.lv[l];
-      loc[l] = compact<float>(locate<false>(L, (double)pt[0], (double)pt[1], (double)pt[2], nullptr));
+      const LocT<float> lq = compact<float>(locate<false>(L, (double)pt[0], (double)pt[1], (double)pt[2], nullptr));
+      *reinterpret_cast<float4*>(myrow + K::oL + 4 * l) = make_float4(__int_as_float(lq.base), lq.fx, lq.fy, lq.fz);
       float wk[8], ju[8];
-      corner_w_ju(loc[l], (float)L.inv_vs, u, wk, ju);
-      const float* Fp = reinterpret_cast<const float*>(L.feat) + (int64_t)loc[l].base * S::CG;
+      corner_w_ju(lq, (float)L.inv_vs, u, wk, ju);
+      const float* Fp = reinterpret_cast<const float*>(L.feat) + (int64_t)lq.base * S::CG;
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         float row[S::CG];
@@ -706,6 +756,14 @@ __global__ void __launch_bounds__(WARPS * 32) k_bwd_geom_tc(Ws<float> w, Geo G, 
   fill_cols(h1, gvec + GVec::b1);
   mma_layer<2, 4, 4>([&](int mt, int kk, uint32_t (&ah)[4], uint32_t (&al)[4]) { a_from_d(h0[mt][kk], ah, al); },
                      sfr + F::G_W1 * 32, h1);
+  // A1 = p h0 (+ q0 below) parked in the row so h0 dies here
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int nn = 0; nn < 4; ++nn)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) h0[mt][nn][r] *= pr[mt][r >> 1];
+  store_d<ROW>(h0, rows, K::oA1);
   const uint32_t m1 = relu_d(h1);
   // dW2 += p h1 (column sums); per-sample m1 masks for the dW1 outer product
 #pragma unroll
@@ -729,12 +787,13 @@ __global__ void __launch_bounds__(WARPS * 32) k_bwd_geom_tc(Ws<float> w, Geo G, 
         [&](int mt, int kk, uint32_t (&ah)[4], uint32_t (&al)[4]) { a_from_rows<ROW>(rows, K::oV, 16 * mt, kk, ah, al); },
         sfr + F::G_W0 * 32, q0);
     mask_d(q0, m0);
+    load_d<ROW>(h0, rows, K::oA1);
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
       for (int nn = 0; nn < 4; ++nn)
 #pragma unroll
-        for (int r = 0; r < 4; ++r) h0[mt][nn][r] = fmaf(pr[mt][r >> 1], h0[mt][nn][r], q0[mt][nn][r]);
+        for (int r = 0; r < 4; ++r) h0[mt][nn][r] += q0[mt][nn][r];
     store_d<ROW>(h0, rows, K::oA1);
     zero_d(h1);
     mma_layer<2, 4, 4>([&](int mt, int kk, uint32_t (&ah)[4], uint32_t (&al)[4]) { a_from_d(q0[mt][kk], ah, al); },
@@ -776,53 +835,55 @@ __global__ void __launch_bounds__(WARPS * 32) k_bwd_geom_tc(Ws<float> w, Geo G, 
   }
   __syncwarp();
   // ---- grid scatter: theta_l[idx_k] += g_l (p w_k + ju_k)
+  const float p = myrow[K::oP];
+  float u[3] = {0.f, 0.f, 0.f};
+  if (active) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) u[a] = w.ubar[s * 3 + a];
+  }
 #pragma unroll
   for (int l = 0; l < S::NL; ++l) {
+    const float4 lv = *reinterpret_cast<const float4*>(myrow + K::oL + 4 * l);
+    LocT<float> lq;
+    lq.base = __float_as_int(lv.x);
+    lq.fx = lv.y;
+    lq.fy = lv.z;
+    lq.fz = lv.w;
     float wk[8], ju[8], coef[8];
-    corner_w_ju(loc[l], (float)G.lv[l].inv_vs, u, wk, ju);
+    corner_w_ju(lq, (float)G.lv[l].inv_vs, u, wk, ju);
 #pragma unroll
     for (int k = 0; k < 8; ++k) coef[k] = fmaf(p, wk[k], ju[k]);
-    scatter_level<float, S::CG>(G.lv[l], loc[l], myrow + K::oZ + l * S::CG, coef, active, l < agg_levels);
+    scatter_level<float, S::CG>(G.lv[l], lq, myrow + K::oZ + l * S::CG, coef, active, l < agg_levels);
   }
   // ---- outer products over the warp's samples: dW0 += A0^T delta0, dW1 += A1^T delta1
-  float d0[4][4], d1[2][4][4];
-#pragma unroll
-  for (int nt = 0; nt < 4; ++nt)
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      d0[nt][c] = 0.f;
-      d1[0][nt][c] = 0.f;
-      d1[1][nt][c] = 0.f;
-    }
+  float d0[1][4][4], d1[2][4][4];
+  zero_d(d0);
+  zero_d(d1);
   const float w2l = gvec[GVec::w2 + lane];
 #pragma unroll
   for (int ks = 0; ks < 4; ++ks) {
     const int k0 = ks * 8;
     const uint32_t mk0 = reinterpret_cast<const uint32_t*>(rows + (k0 + t) * ROW + K::oM)[0];
     const uint32_t mk1 = reinterpret_cast<const uint32_t*>(rows + (k0 + t + 4) * ROW + K::oM)[0];
-    uint32_t ah[4], al[4];
-    frag_a(rows, ROW, K::oA0, k0, 0, ah, al);
+    uint32_t ah[2][4], al[2][4], bh0[4], bh1[4], bl0[4], bl1[4];
+    {  // dW0 += A0^T delta0
+      uint32_t a1h[1][4], a1l[1][4];
+      frag_a(rows, ROW, K::oA0, k0, 0, a1h[0], a1l[0]);
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) frag_b(rows, ROW, K::oB0, k0, nt * 8, bh0[nt], bh1[nt], bl0[nt], bl1[nt]);
+      mma3_sweep(d0, a1h, a1l, bh0, bh1, bl0, bl1);
+    }
+    // dW1 += A1^T delta1, delta1[k][n] = m1_k(n) ? W2[n] : 0
 #pragma unroll
     for (int nt = 0; nt < 4; ++nt) {
-      uint32_t bh0, bh1, bl0, bl1;
-      frag_b(rows, ROW, K::oB0, k0, nt * 8, bh0, bh1, bl0, bl1);
-      mma3(d0[nt], ah, al, bh0, bh1, bl0, bl1);
+      const int n = nt * 8 + g;
+      const float w2n = __shfl_sync(0xffffffffu, w2l, n);
+      split_tf32(((mk0 >> n) & 1u) ? w2n : 0.f, bh0[nt], bl0[nt]);
+      split_tf32(((mk1 >> n) & 1u) ? w2n : 0.f, bh1[nt], bl1[nt]);
     }
 #pragma unroll
-    for (int mt = 0; mt < 2; ++mt) {
-      frag_a(rows, ROW, K::oA1, k0, mt * 16, ah, al);
-#pragma unroll
-      for (int nt = 0; nt < 4; ++nt) {
-        const int n = nt * 8 + g;
-        const float w2n = __shfl_sync(0xffffffffu, w2l, n);
-        const float b0v = ((mk0 >> n) & 1u) ? w2n : 0.f;
-        const float b1v = ((mk1 >> n) & 1u) ? w2n : 0.f;
-        uint32_t bh0, bh1, bl0, bl1;
-        split_tf32(b0v, bh0, bl0);
-        split_tf32(b1v, bh1, bl1);
-        mma3(d1[mt][nt], ah, al, bh0, bh1, bl0, bl1);
-      }
-    }
+    for (int mt = 0; mt < 2; ++mt) frag_a(rows, ROW, K::oA1, k0, mt * 16, ah[mt], al[mt]);
+    mma3_sweep(d1, ah, al, bh0, bh1, bl0, bl1);
   }
   // column sums over the warp: reduce the 8 lanes sharing t
 #pragma unroll
@@ -845,7 +906,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_bwd_geom_tc(Ws<float> w, Geo G, 
   {
     float* mine = red + (size_t)wid * NGP;
 #pragma unroll
-    for (int nt = 0; nt < 4; ++nt) frag_d_store(d0[nt], mine + S::oGW0, 0, nt * 8, S::IN_G);
+    for (int nt = 0; nt < 4; ++nt) frag_d_store(d0[0][nt], mine + S::oGW0, 0, nt * 8, S::IN_G);
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
@@ -987,43 +1048,34 @@ __global__ void __launch_bounds__(WARPS * 32) k_bwd_color_tc(Ws<float> w, Geo G,
     scatter_level<float, S::CC>(G.col, q, myrow + K::oFB, wk, active, false);
   }
   // ---- outer products: e0 = [inp,1]^T a0b, e1 = h0c^T a1b, e2 = h1c^T y_bar
-  float e0[4][4], e1[2][4][4], e2[2][4];
-#pragma unroll
-  for (int nt = 0; nt < 4; ++nt)
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      e0[nt][c] = 0.f;
-      e1[0][nt][c] = 0.f;
-      e1[1][nt][c] = 0.f;
-    }
-#pragma unroll
-  for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-    for (int c = 0; c < 4; ++c) e2[mt][c] = 0.f;
+  float e0[1][4][4], e1[2][4][4], e2[2][1][4];
+  zero_d(e0);
+  zero_d(e1);
+  zero_d(e2);
 #pragma unroll
   for (int ks = 0; ks < 4; ++ks) {
     const int k0 = ks * 8;
-    uint32_t ah[4], al[4];
-    frag_a(rows, ROW, K::oA0, k0, 0, ah, al);
+    uint32_t ah[2][4], al[2][4], bh0[4], bh1[4], bl0[4], bl1[4];
+    {  // dW0c (+ db0c via the ones column) += [inp,1]^T a0b
+      uint32_t a1h[1][4], a1l[1][4];
+      frag_a(rows, ROW, K::oA0, k0, 0, a1h[0], a1l[0]);
 #pragma unroll
-    for (int nt = 0; nt < 4; ++nt) {
-      uint32_t bh0, bh1, bl0, bl1;
-      frag_b(rows, ROW, K::oB0, k0, nt * 8, bh0, bh1, bl0, bl1);
-      mma3(e0[nt], ah, al, bh0, bh1, bl0, bl1);
+      for (int nt = 0; nt < 4; ++nt) frag_b(rows, ROW, K::oB0, k0, nt * 8, bh0[nt], bh1[nt], bl0[nt], bl1[nt]);
+      mma3_sweep(e0, a1h, a1l, bh0, bh1, bl0, bl1);
     }
+    // dW1c += h0c^T a1b
 #pragma unroll
-    for (int mt = 0; mt < 2; ++mt) {
-      frag_a(rows, ROW, K::oA1, k0, mt * 16, ah, al);
+    for (int mt = 0; mt < 2; ++mt) frag_a(rows, ROW, K::oA1, k0, mt * 16, ah[mt], al[mt]);
 #pragma unroll
-      for (int nt = 0; nt < 4; ++nt) {
-        uint32_t bh0, bh1, bl0, bl1;
-        frag_b(rows, ROW, K::oB1, k0, nt * 8, bh0, bh1, bl0, bl1);
-        mma3(e1[mt][nt], ah, al, bh0, bh1, bl0, bl1);
-      }
-      frag_a(rows, ROW, K::oH1, k0, mt * 16, ah, al);
-      uint32_t bh0, bh1, bl0, bl1;
-      frag_b(rows, ROW, K::oY, k0, 0, bh0, bh1, bl0, bl1);
-      mma3(e2[mt], ah, al, bh0, bh1, bl0, bl1);
+    for (int nt = 0; nt < 4; ++nt) frag_b(rows, ROW, K::oB1, k0, nt * 8, bh0[nt], bh1[nt], bl0[nt], bl1[nt]);
+    mma3_sweep(e1, ah, al, bh0, bh1, bl0, bl1);
+    // dW2c += h1c^T y_bar
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt) frag_a(rows, ROW, K::oH1, k0, mt * 16, ah[mt], al[mt]);
+    {
+      uint32_t yh0[1], yh1[1], yl0[1], yl1[1];
+      frag_b(rows, ROW, K::oY, k0, 0, yh0[0], yh1[0], yl0[0], yl1[0]);
+      mma3_sweep(e2, ah, al, yh0, yh1, yl0, yl1);
     }
   }
   float acc_b1 = 0.f, acc_b2 = 0.f;
@@ -1041,7 +1093,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_bwd_color_tc(Ws<float> w, Geo G,
     const int o = S::NG;
     if (lane < S::oCW0 - S::NG) mine[lane] = 0.f;  // alignment padding
 #pragma unroll
-    for (int nt = 0; nt < 4; ++nt) frag_d_store(e0[nt], mine + (S::oCW0 - o), 0, nt * 8, S::IN_C + 1);
+    for (int nt = 0; nt < 4; ++nt) frag_d_store(e0[0][nt], mine + (S::oCW0 - o), 0, nt * 8, S::IN_C + 1);
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
@@ -1052,12 +1104,12 @@ __global__ void __launch_bounds__(WARPS * 32) k_bwd_color_tc(Ws<float> w, Geo G,
     for (int mt = 0; mt < 2; ++mt) {
       const int r0 = mt * 16 + g, r1 = r0 + 8, c = 2 * t;
       if (c < 3) {
-        mine[S::oCW2 - o + r0 * 3 + c] = e2[mt][0];
-        mine[S::oCW2 - o + r1 * 3 + c] = e2[mt][2];
+        mine[S::oCW2 - o + r0 * 3 + c] = e2[mt][0][0];
+        mine[S::oCW2 - o + r1 * 3 + c] = e2[mt][0][2];
       }
       if (c + 1 < 3) {
-        mine[S::oCW2 - o + r0 * 3 + c + 1] = e2[mt][1];
-        mine[S::oCW2 - o + r1 * 3 + c + 1] = e2[mt][3];
+        mine[S::oCW2 - o + r0 * 3 + c + 1] = e2[mt][0][1];
+        mine[S::oCW2 - o + r1 * 3 + c + 1] = e2[mt][0][3];
       }
     }
   }
