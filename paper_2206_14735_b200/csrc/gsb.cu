@@ -214,7 +214,17 @@ int gsb_adam_step(int32_t precision, void* params, void* grads, void* m, void* v
   k.ib2 = 1.0 - beta2;
   k.inv_c1 = 1.0 / c1;
   k.inv_c2 = 1.0 / c2;
-  int blocks = num_sms() * 8;
+  // persistent grid: exactly the resident blocks (no partial last wave)
+  static int resident[2] = {0, 0};
+  int& res = resident[precision == 0 ? 0 : 1];
+  if (res == 0) {
+    if (precision == 0)
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&res, k_adam<float>, 256, 0);
+    else
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&res, k_adam<double>, 256, 0);
+    if (res <= 0) res = 1;
+  }
+  int blocks = num_sms() * res;
   timing_point(nullptr, s);
   if (precision == 0)
     k_adam<float><<<blocks, 256, 0, s>>>((float*)params, (float*)grads, (float*)m, (float*)v, n, sg,

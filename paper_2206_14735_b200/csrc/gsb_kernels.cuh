@@ -1536,7 +1536,9 @@ __device__ __forceinline__ void adam_fast(float& p, float& g, float& m, float& v
   v = (float)vi;
   const double q1 = mi * k.inv_c1, q2 = vi * k.inv_c2;
   double sq;
-  if (q2 > 1e-30) {
+  if (q2 == 0.0) {  // never-touched parameter: sqrt(0) = 0 exactly
+    sq = 0.0;
+  } else if (q2 > 1e-30) {
     double t = (double)rsqrtf((float)q2);
     t = t * fma(-0.5 * q2, t * t, 1.5);
     t = t * fma(-0.5 * q2, t * t, 1.5);
