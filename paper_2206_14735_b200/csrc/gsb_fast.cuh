@@ -116,6 +116,13 @@ __device__ __forceinline__ void split_tf32(float x, uint32_t& hi, uint32_t& lo) 
   hi = tf32_of(x);
   lo = tf32_of(x - __uint_as_float(hi));
 }
+// per-use split (3 integer/FP ops instead of two emulated cvt.rna): hi rounds
+// the mantissa half-away at bit 13, lo = x - hi is exact and goes to the MMA
+// raw (the tensor core ignores its low 13 bits): |x - hi - lo_tf32| <= 2^-21 |x|
+__device__ __forceinline__ void split_fast(float x, uint32_t& hi, uint32_t& lo) {
+  hi = (__float_as_uint(x) + 0x1000u) & 0xffffe000u;
+  lo = __float_as_uint(x - __uint_as_float(hi));
+}
 __device__ __forceinline__ void mma_tf32(float (&d)[4], const uint32_t (&a)[4], uint32_t b0,
                                          uint32_t b1) {
   asm("mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
@@ -139,18 +146,18 @@ __device__ __forceinline__ void frag_a(const float* rows, int ROW, int off, int 
   const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   const float* r0 = rows + (k0 + t) * ROW + off + m0 + g;
   const float* r1 = rows + (k0 + t + 4) * ROW + off + m0 + g;
-  split_tf32(r0[0], ah[0], al[0]);
-  split_tf32(r0[8], ah[1], al[1]);
-  split_tf32(r1[0], ah[2], al[2]);
-  split_tf32(r1[8], ah[3], al[3]);
+  split_fast(r0[0], ah[0], al[0]);
+  split_fast(r0[8], ah[1], al[1]);
+  split_fast(r1[0], ah[2], al[2]);
+  split_fast(r1[8], ah[3], al[3]);
 }
 // B fragment (samples x outputs) from rows: b0 = row[k0+t][n0+g], b1 = row[k0+t+4][n0+g]
 __device__ __forceinline__ void frag_b(const float* rows, int ROW, int off, int k0, int n0,
                                        uint32_t& bh0, uint32_t& bh1, uint32_t& bl0,
                                        uint32_t& bl1) {
   const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
-  split_tf32(rows[(k0 + t) * ROW + off + n0 + g], bh0, bl0);
-  split_tf32(rows[(k0 + t + 4) * ROW + off + n0 + g], bh1, bl1);
+  split_fast(rows[(k0 + t) * ROW + off + n0 + g], bh0, bl0);
+  split_fast(rows[(k0 + t + 4) * ROW + off + n0 + g], bh1, bl1);
 }
 
 // scatter D fragments of an (m-tile, n-tile) into a row-major [rows][32] block

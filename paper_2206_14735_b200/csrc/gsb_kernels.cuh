@@ -988,24 +988,29 @@ __device__ __forceinline__ void scatter_level(const LevelDev& L, const LocT<T>& 
   const int run_end = after ? lane + __ffs(after) : 32;
   // scan steps bounded by the warp's longest run (fine levels: 1-2 lanes)
   const int maxrun = (int)__reduce_max_sync(full, head ? (unsigned)(run_end - lane) : 0u);
-  T gv[C];
+  // all 8 corners x C channels scan together (8C independent shuffle chains)
+  T v[8][C];
 #pragma unroll
-  for (int c = 0; c < C; ++c) gv[c] = active ? gl[c] : T(0);
+  for (int c = 0; c < C; ++c) {
+    const T gc = active ? gl[c] : T(0);
 #pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    T v[C];
+    for (int k = 0; k < 8; ++k) v[k][c] = gc * coef[k];
+  }
 #pragma unroll
-    for (int c = 0; c < C; ++c) v[c] = gv[c] * coef[k];
+  for (int o = 1; o < 32; o <<= 1) {
+    if (o >= maxrun) break;
+    const bool take = lane + o < run_end;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      if (o >= maxrun) break;
+    for (int k = 0; k < 8; ++k)
 #pragma unroll
       for (int c = 0; c < C; ++c) {
-        const T y = __shfl_down_sync(full, v[c], o);
-        if (lane + o < run_end) v[c] += y;
+        const T y = __shfl_down_sync(full, v[k][c], o);
+        if (take) v[k][c] += y;
       }
-    }
-    if (head && active) red_row<T, C>(Gp + corner_off(L, k) * C, v);
+  }
+  if (head && active) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) red_row<T, C>(Gp + corner_off(L, k) * C, v[k]);
   }
 }
 

@@ -176,10 +176,10 @@ __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 
 // A operand from the D fragment of feature block kk
 __device__ __forceinline__ void a_from_d(const float (&x)[4], uint32_t (&ah)[4], uint32_t (&al)[4]) {
-  split_tf32(x[0], ah[0], al[0]);
-  split_tf32(x[2], ah[1], al[1]);
-  split_tf32(x[1], ah[2], al[2]);
-  split_tf32(x[3], ah[3], al[3]);
+  split_fast(x[0], ah[0], al[0]);
+  split_fast(x[2], ah[1], al[1]);
+  split_fast(x[1], ah[2], al[2]);
+  split_fast(x[3], ah[3], al[3]);
 }
 
 // A operand from sample-major shared rows (features at off + 8kk + {2t, 2t+1})
@@ -189,10 +189,10 @@ __device__ __forceinline__ void a_from_rows(const float* rows, int off, int m0, 
   const int lane = lane_id(), g = lane >> 2, t = lane & 3;
   const float2 u = *reinterpret_cast<const float2*>(rows + (m0 + g) * ROW + off + 8 * kk + 2 * t);
   const float2 v = *reinterpret_cast<const float2*>(rows + (m0 + g + 8) * ROW + off + 8 * kk + 2 * t);
-  split_tf32(u.x, ah[0], al[0]);
-  split_tf32(v.x, ah[1], al[1]);
-  split_tf32(u.y, ah[2], al[2]);
-  split_tf32(v.y, ah[3], al[3]);
+  split_fast(u.x, ah[0], al[0]);
+  split_fast(v.x, ah[1], al[1]);
+  split_fast(u.y, ah[2], al[2]);
+  split_fast(v.y, ah[3], al[3]);
 }
 
 // Y[mt][nn] += A(mt, kk) B(kk, nn); B fragments at fr[(kk*NN + nn)*32 + lane]
@@ -878,8 +878,8 @@ __global__ void __launch_bounds__(WARPS * 32) k_bwd_geom_tc(Ws<float> w, Geo G, 
     for (int nt = 0; nt < 4; ++nt) {
       const int n = nt * 8 + g;
       const float w2n = __shfl_sync(0xffffffffu, w2l, n);
-      split_tf32(((mk0 >> n) & 1u) ? w2n : 0.f, bh0[nt], bl0[nt]);
-      split_tf32(((mk1 >> n) & 1u) ? w2n : 0.f, bh1[nt], bl1[nt]);
+      split_fast(((mk0 >> n) & 1u) ? w2n : 0.f, bh0[nt], bl0[nt]);
+      split_fast(((mk1 >> n) & 1u) ? w2n : 0.f, bh1[nt], bl1[nt]);
     }
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt) frag_a(rows, ROW, K::oA1, k0, mt * 16, ah[mt], al[mt]);

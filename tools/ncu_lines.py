@@ -5,6 +5,7 @@ import subprocess
 import sys
 
 rep, top = sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else 15
+col = sys.argv[3] if len(sys.argv) > 3 else "Warp Stall Sampling (All Samples)"
 raw = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
                      capture_output=True, text=True).stdout
 cur_file = fn = hdr = None
@@ -19,7 +20,7 @@ for r in csv.reader(raw.splitlines()):
         continue
     if r and r[0] == "Line No":
         hdr = r
-        si = hdr.index("Warp Stall Sampling (All Samples)")
+        si = hdr.index(col)
         continue
     if not r or hdr is None or not r[0].isdigit() or r[2] != "-":
         continue
