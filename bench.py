@@ -274,7 +274,7 @@ def main():
         return run_reference(args)
 
     import torch
-    from paper_2206_14735_b200 import _lib, engine, optimizer, scenes
+    from paper_2206_14735_b200 import _lib, engine, optimizer, parallel, scenes
     from paper_2206_14735_b200.renderer import engine_for
 
     ws_, rank, local = dist_env()
@@ -295,30 +295,21 @@ def main():
     eng = engine_for(model, ds)
     N = cfg.coarse_samples + cfg.importance_rounds * cfg.importance_add
 
+    dp = parallel.DataParallelStep(eng, pg) if pg is not None else None
+
     def draws_for(it):
-        d = engine.host_draws(model, ds, cfg, it)
-        # this rank's slice of the global batch; smoothness on rank 0
-        d.ray_ids = d.ray_ids[rank * M:(rank + 1) * M].copy()
-        if rank != 0:
-            d.smooth = None
-        return d
+        """Host draws of the global batch; this rank's shard (rank 0: smoothness)."""
+        return parallel.shard_draws(engine.host_draws(model, ds, cfg, it), rank, ws_)
 
     S = cfg.weights.smooth_count
 
-    def one_step(d, ids, sm, stream=None):
-        kw = dict(ray_base=rank * M, m_global=M * ws_, smooth_global=S)
-        if pg is None:
-            w = eng.launch(cfg, d, ids, sm, **kw)
-        else:
-            w = eng.launch(cfg, d, ids, sm, phases=1, **kw)
-            pg.all_reduce(w["counts"])
-            eng.model.arena.zero_grads()
-            st = eng.step_struct(cfg, d, ids, sm, w, phases=2, **kw)
-            import ctypes as C
-            _lib.check(eng.lib.gsb_train_step(C.byref(eng.mstruct), C.byref(eng.dstruct),
-                                              C.byref(st), _lib.stream_handle()), "step")
-            pg.all_reduce(model.arena.grads)
-            pg.all_reduce(w["parts"])
+    def objective(d, kw, ids, sm):
+        if dp is None:
+            return eng.launch(cfg, d, ids, sm, **kw)
+        return dp(cfg, d, ids, sm, **kw)
+
+    def one_step(d, kw, ids, sm):
+        w = objective(d, kw, ids, sm)
         opt.t = [t + 1 for t in opt.t]
         opt._launch()
         return w
@@ -326,16 +317,15 @@ def main():
     # ---- device-resident inputs for warmup + timed steps
     pre = []
     for it in range(W + K):
-        d = draws_for(it)
+        d, kw = draws_for(it)
         ids, sm = eng.upload(d)
-        pre.append((d, ids, sm))
+        pre.append((d, kw, ids, sm))
     torch.cuda.synchronize()
     for it in range(W):
         one_step(*pre[it])
     torch.cuda.synchronize()
 
-    # adam-only and step-only event timing (same stream) for the roofline
-    e = [torch.cuda.Event(enable_timing=True) for _ in range(2 * K + 2)]
+    # timed region: objective and Adam event pairs on the step stream
     clocks = Clocks()
     clocks.start()
     if pg:
@@ -347,23 +337,11 @@ def main():
     ev1 = torch.cuda.Event(enable_timing=True)
     ev0.record()
     for k in range(K):
-        d, ids, sm = pre[W + k]
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)
         c = torch.cuda.Event(enable_timing=True)
         a.record()
-        kw = dict(ray_base=rank * M, m_global=M * ws_, smooth_global=S)
-        if pg is None:
-            eng.launch(cfg, d, ids, sm, **kw)
-        else:
-            w = eng.launch(cfg, d, ids, sm, phases=1, **kw)
-            pg.all_reduce(w["counts"])
-            eng.model.arena.zero_grads()
-            import ctypes as C
-            st = eng.step_struct(cfg, d, ids, sm, w, phases=2, **kw)
-            _lib.check(eng.lib.gsb_train_step(C.byref(eng.mstruct), C.byref(eng.dstruct),
-                                              C.byref(st), _lib.stream_handle()), "step")
-            pg.all_reduce(model.arena.grads)
+        objective(*pre[W + k])
         b.record()
         opt.t = [t + 1 for t in opt.t]
         opt._launch()
@@ -406,15 +384,14 @@ def main():
     h2d = 0
     for k in range(K):
         it = base_it + k
-        d = draws_for(it)
+        d, kw = draws_for(it)
         h2d = d.ray_ids.nbytes + (0 if d.smooth is None else d.smooth.nbytes)
-        ids, sm = eng.upload(d)
         if pg is None:
             T.launch(it, draws=d, slot=k % 2)
         else:
-            one_step(d, ids, sm)
-            T.host_parts[k % 2].copy_(eng.workspace(M, 96, 3, 12, S if rank == 0 else 0)["parts"],
-                                      non_blocking=True)
+            ids, sm = eng.upload(d)
+            w = one_step(d, kw, ids, sm)
+            T.host_parts[k % 2].copy_(w["parts"], non_blocking=True)
             T.events[k % 2].record()
         if pending is not None:
             T.parts(pending)

@@ -547,15 +547,26 @@ class GeomPass:
 
 
 def train_objective(P, dataset, batch, iteration, cfg, smooth_override=None,
-                    want_grads=True, inject_depths=None):
+                    want_grads=True, inject_depths=None, shard=None):
     """One evaluation of the training objective and (optionally) all
     parameter gradients.  Returns a dict of every intermediate.
 
     ``inject_depths`` replaces the sampled depths (M, N) for component
-    parity (the taped pass of another implementation given our samples)."""
+    parity (the taped pass of another implementation given our samples).
+
+    ``shard`` (data-parallel restatement; not in the
+    reference): dict with ``row_base`` and ``m_global`` (this batch is rows
+    [row_base, row_base + m) of a global batch: the stratify / importance
+    uniforms are those rows of the global draws), optional global
+    normalisers ``n_valid`` / ``n_eik`` / ``n_smooth``, and ``smooth``
+    (False: this shard owns no smoothness points).  The shard's parts and
+    gradients then sum over shards to the unsharded step."""
     lw = cfg.weights
     dt = P.dtype
     m = len(batch)
+    sh = shard or {}
+    row0 = int(sh.get("row_base", 0))
+    m_glob = int(sh.get("m_global", m))
     margin = 0.5 * P.finest_voxel
     lo_c, hi_c = P.lo + margin, P.hi - margin
     R = {}
@@ -578,7 +589,7 @@ def train_objective(P, dataset, batch, iteration, cfg, smooth_override=None,
 
     # sampling: gs/renderer.py:319-346
     s_val = float(np.exp(P.log_s))
-    u0 = substream(cfg.seed, STRATIFY, iteration).random((m, cfg.coarse_samples))
+    u0 = substream(cfg.seed, STRATIFY, iteration).random((m_glob, cfg.coarse_samples))[row0:row0 + m]
     depths = stratified_coarse(near, far, cfg.coarse_samples, u0)
     R["depths0"] = depths
 
@@ -594,7 +605,8 @@ def train_objective(P, dataset, batch, iteration, cfg, smooth_override=None,
             rows = np.repeat(np.arange(m), depths.shape[1])
             phi_cache = phi_at(depths.reshape(-1), rows).reshape(m, -1)
         w = render_weights_data(phi_cache, s_val)
-        ui = substream(cfg.seed, IMPORTANCE, iteration, rnd).random((m, cfg.importance_add))
+        ui = substream(cfg.seed, IMPORTANCE, iteration, rnd).random(
+            (m_glob, cfg.importance_add))[row0:row0 + m]
         prev_phi = phi_cache
         depths, src = importance_refine_with_sources(depths, w, near, far, ui)
         nxt = np.take_along_axis(phi_cache, np.maximum(src, 0), axis=1)
@@ -644,11 +656,12 @@ def train_objective(P, dataset, batch, iteration, cfg, smooth_override=None,
     # losses: gs/renderer.py:372-414
     err = chat - batch.color.astype(dt)
     lr_m = np.sqrt((err * err).sum(axis=1) + dt.type(1e-24))
-    l_rgb = lr_m.sum() / dt.type(m)
+    l_rgb = lr_m.sum() / dt.type(m_glob)
     vmask = batch.valid.astype(dt)
     n_valid = int(batch.valid.sum())
+    nv_norm = int(sh.get("n_valid", n_valid))
     d_err = np.abs(dhat - batch.depth_ray.astype(dt))
-    l_d = (d_err * vmask).sum() / dt.type(max(n_valid, 1))
+    l_d = (d_err * vmask).sum() / dt.type(max(nv_norm, 1))
     b = batch.depth_ray[:, None] - depths
     tr_mask = (batch.valid[:, None] & (np.abs(b) <= lw.truncation)).astype(dt)
     fs_mask = (batch.valid[:, None] & (b > lw.truncation)).astype(dt)
@@ -657,16 +670,16 @@ def train_objective(P, dataset, batch, iteration, cfg, smooth_override=None,
     tr_cnt = tr_mask.sum(axis=1)
     sdf_val = np.abs(phis - b_c) * tr_mask
     per_ray_sdf = sdf_val.sum(axis=1) / np.maximum(tr_cnt, 1.0).astype(dt)
-    l_sdf = per_ray_sdf.sum() / dt.type(m)
+    l_sdf = per_ray_sdf.sum() / dt.type(m_glob)
     fs_cnt = fs_mask.sum(axis=1)
     e5 = np.exp(phis * dt.type(-lw.freespace_alpha))
     inner = np.maximum(dt.type(0.0), e5 - dt.type(1.0))
     fs_raw = np.maximum(inner, phis - b_c)
     per_ray_fs = (fs_raw * fs_mask).sum(axis=1) / np.maximum(fs_cnt, 1.0).astype(dt)
-    l_fs = per_ray_fs.sum() / dt.type(m)
+    l_fs = per_ray_fs.sum() / dt.type(m_glob)
     eik_mask = (fs_mask + behind_mask + (~batch.valid[:, None]).astype(dt)).clip(0, 1)
     eik_flat = eik_mask.reshape(-1)
-    n_eik = float(max(eik_flat.sum(), 1.0))
+    n_eik = float(max(sh.get("n_eik", eik_flat.sum()), 1.0))
     gp = G.gphi
     nrm = np.sqrt((gp * gp).sum(axis=-1) + dt.type(1e-20))
     diff = 1.0 - nrm
@@ -681,15 +694,16 @@ def train_objective(P, dataset, batch, iteration, cfg, smooth_override=None,
         smooth_pts = draw_smooth_points(P, dataset, lw.smooth_count, lw.truncation,
                                         lw.smooth_delta, rng)
     S = None
-    if smooth_pts is None or lw.smooth == 0.0:
+    if smooth_pts is None or lw.smooth == 0.0 or not sh.get("smooth", True):
         l_smooth = dt.type(0.0)
         n_smooth = 0
     else:
         xs, xe = smooth_pts
         n_smooth = xs.shape[0]
+        n_sm_norm = int(sh.get("n_smooth", n_smooth))
         S = GeomPass(P, np.concatenate([xs, xe], axis=0).astype(dt))
         dS = S.gphi[:n_smooth] - S.gphi[n_smooth:]
-        l_smooth = (dS * dS).sum() / dt.type(n_smooth)
+        l_smooth = (dS * dS).sum() / dt.type(n_sm_norm)
     R["smooth_pts"] = smooth_pts
 
     total = (l_rgb * dt.type(lw.rgb) + l_d * dt.type(lw.depth) + l_sdf * dt.type(lw.sdf)
@@ -708,11 +722,11 @@ def train_objective(P, dataset, batch, iteration, cfg, smooth_override=None,
 
     # ---------------- backward ----------------
     grads = {name: np.zeros_like(a) for name, a in zip(P.names(), P.arrays())}
-    M = dt.type(m)
+    M = dt.type(m_glob)
     # photometric + depth seeds
     chat_bar = (dt.type(lw.rgb) / M) * err / lr_m[:, None]
     dhat_bar = dt.type(lw.depth) * vmask * np.sign(dhat - batch.depth_ray.astype(dt)) \
-        / dt.type(max(n_valid, 1))
+        / dt.type(max(nv_norm, 1))
     w_bar = (chat_bar[:, None, :] * colors).sum(axis=2) + dhat_bar[:, None] * dconst
     c_bar = w[:, :, None] * chat_bar[:, None, :]
     T_bar = w_bar * al
@@ -742,7 +756,7 @@ def train_objective(P, dataset, batch, iteration, cfg, smooth_override=None,
     u = (dt.type(-2.0 * lw.eik) / dt.type(n_eik)) * (eik_flat * diff / nrm)[:, None] * gp
     G.backward(phi_bar.reshape(-1), u.astype(dt), grads)
     if S is not None:
-        us = np.concatenate([dS, -dS], axis=0) * (dt.type(2.0 * lw.smooth) / dt.type(n_smooth))
+        us = np.concatenate([dS, -dS], axis=0) * (dt.type(2.0 * lw.smooth) / dt.type(n_sm_norm))
         S.backward(np.zeros(2 * n_smooth, dtype=dt), us.astype(dt), grads)
     # colour: sigma(MLP_c([fc, r])) backprop
     cb = c_bar.reshape(m * n, 3)

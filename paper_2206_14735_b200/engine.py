@@ -234,16 +234,20 @@ class StepEngine:
                 self.device, non_blocking=True)
         return ids, sm
 
-    def launch(self, cfg, draws, ray_ids_dev, smooth_dev, stream=None, **kw):
-        """Enqueue one objective + backward; returns the workspace views."""
+    def launch(self, cfg, draws, ray_ids_dev, smooth_dev, stream=None, fresh=True, **kw):
+        """Enqueue one objective + backward; returns the workspace views.
+        ``fresh=False`` continues a step in the same workspace (phase 2 after
+        a phase-1 launch and the count all-reduce): status words are kept."""
         M = int(ray_ids_dev.numel())
         S = 0 if smooth_dev is None else int(smooth_dev.shape[0] // 2)
         ws = self.workspace(M, cfg.coarse_samples, cfg.importance_rounds, cfg.importance_add, S)
         self.model.arena.zero_grads()
-        ws["status"].zero_()
+        if fresh:
+            ws["status"].zero_()
         st = self.step_struct(cfg, draws, ray_ids_dev, smooth_dev, ws, **kw)
         _lib.check(self.lib.gsb_train_step(C.byref(self.mstruct), C.byref(self.dstruct),
                                            C.byref(st), _lib.stream_handle(stream)),
                    "gsb_train_step")
-        self.model.arena.grads_clean = False
+        if kw.get("phases", 3) & 2:
+            self.model.arena.grads_clean = False
         return ws

@@ -1,0 +1,143 @@
+"""Ray-sharded data parallelism on CPU: the package's
+DataParallelStep / shard_draws driven over a gloo world of 2, with the
+oracle standing in for the device step of each rank.  The all-reduced
+gradients and loss parts must equal the unsharded step."""
+
+import os
+import socket
+import sys
+from types import SimpleNamespace
+
+import numpy as np
+import pytest
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+sys.path.insert(0, ROOT)
+sys.path.insert(0, HERE)
+
+
+def test_shard_rows_partition():
+    from paper_2206_14735_b200.parallel import shard_rows
+    for m in (1, 7, 64, 6144, 6145):
+        for world in (1, 2, 3, 8):
+            blocks = [shard_rows(m, r, world) for r in range(world)]
+            assert blocks[0][0] == 0 and blocks[-1][1] == m
+            assert all(blocks[i][1] == blocks[i + 1][0] for i in range(world - 1))
+            sizes = [b - a for a, b in blocks]
+            assert max(sizes) - min(sizes) <= 1
+
+
+def test_shard_draws_slices_rays_and_keeps_smoothness_on_rank0():
+    from paper_2206_14735_b200.engine import HostDraws
+    from paper_2206_14735_b200.parallel import shard_draws
+    d = HostDraws(3, np.arange(10, dtype=np.int64) * 7, np.ones((8, 3), np.float32), None, [])
+    d0, kw0 = shard_draws(d, 0, 3)
+    d2, kw2 = shard_draws(d, 2, 3)
+    assert list(d0.ray_ids) == [0, 7, 14, 21] and d0.smooth is not None
+    assert list(d2.ray_ids) == [49, 56, 63] and d2.smooth is None
+    assert kw0 == dict(ray_base=0, m_global=10, smooth_global=4)
+    assert kw2 == dict(ray_base=7, m_global=10, smooth_global=4)
+    assert d2.iteration == 3
+
+
+def _sub_batch(b, lo, hi):
+    from oracle import gridsurf_oracle as O
+    m = len(b)
+
+    def cut(x):
+        return x[lo:hi] if isinstance(x, np.ndarray) and x.shape[:1] == (m,) else x
+    return O.Batch(*(cut(getattr(b, k)) for k in
+                     ("frame_ids", "pixels", "color", "depth_ray", "valid", "dir_cam", "near", "far")))
+
+
+class OracleEngine:
+    """Stand-in for StepEngine on CPU: phase 1 = sampling + local partition
+    counts, phase 2 = objective + backward with the global normalisers read
+    back from the (all-reduced) counts; gradients land in a flat arena."""
+
+    def __init__(self, torch, G, P, cfg, batch, it):
+        self.torch, self.G, self.P, self.cfg, self.batch, self.it = torch, G, P, cfg, batch, it
+        n = sum(a.size for a in P.arrays())
+        self.model = SimpleNamespace(arena=SimpleNamespace(grads=torch.zeros(n, dtype=torch.float64)))
+        self.ws = dict(counts=torch.zeros(4, dtype=torch.int64),
+                       parts=torch.zeros(8, dtype=torch.float64))
+
+    def launch(self, cfg, draws, ids, sm, phases=3, fresh=True, ray_base=0, m_global=None,
+               smooth_global=None):
+        from oracle import gridsurf_oracle as O
+        lo, hi = ray_base, ray_base + len(ids)
+        sub = _sub_batch(self.batch, lo, hi)
+        shard = dict(row_base=lo, m_global=m_global, smooth=sm is not None)
+        if phases == 1:
+            R = O.train_objective(self.P, self.G.ds, sub, self.it, self.cfg, want_grads=False,
+                                  shard=shard)
+            e = R["extras"]
+            self.ws["counts"][:] = self.torch.tensor(
+                [e["n_valid_rays"], e["n_tr"], e["n_fs"], e["n_eik"]], dtype=self.torch.int64)
+            return self.ws
+        c = self.ws["counts"].tolist()
+        shard.update(n_valid=c[0], n_eik=c[3], n_smooth=smooth_global)
+        R = O.train_objective(self.P, self.G.ds, sub, self.it, self.cfg, shard=shard)
+        flat = np.concatenate([R["grads"][n].reshape(-1) for n in self.P.names()])
+        self.model.arena.grads.copy_(self.torch.from_numpy(flat))
+        names = ("total", "rgb", "depth", "sdf", "fs", "eik", "smooth", "s")
+        self.ws["parts"][:] = self.torch.tensor([R["parts"][k] for k in names], dtype=self.torch.float64)
+        return self.ws
+
+
+def _worker(rank, world, port, out):
+    import torch
+    import torch.distributed as dist
+    from _golden import load, oracle_params
+    from oracle import gridsurf_oracle as O
+    from paper_2206_14735_b200.engine import HostDraws
+    from paper_2206_14735_b200.parallel import DataParallelStep, shard_draws
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    try:
+        G = load("tiny", "double")
+        P = oracle_params(G)
+        cfg = G.cfg
+        it = G.meta["iteration"]
+        rng = O.substream(cfg.seed, O.RAYS, it)
+        intr = G.ds.intrinsics
+        flat = rng.integers(0, G.ds.colors.shape[0] * intr.height * intr.width, size=cfg.batch_rays)
+        batch = O.batch_from_flat(G.ds, flat)
+        draws = HostDraws(it, flat, np.zeros((2, 3)), None, [])  # smoothness drawn by the oracle
+        d, kw = shard_draws(draws, rank, world)
+        kw["smooth_global"] = cfg.weights.smooth_count
+        eng = OracleEngine(torch, G, P, cfg, batch, it)
+        ws = DataParallelStep(eng, dist)(cfg, d, d.ray_ids, d.smooth, **kw)
+        if rank == 0:
+            R = O.train_objective(P, G.ds, batch, it, cfg)
+            ref = np.concatenate([R["grads"][n].reshape(-1) for n in P.names()])
+            got = eng.model.arena.grads.numpy()
+            names = ("total", "rgb", "depth", "sdf", "fs", "eik", "smooth", "s")
+            np.savez(out, got=got, ref=ref, parts=ws["parts"].numpy(),
+                     ref_parts=np.array([R["parts"][k] for k in names]),
+                     counts=ws["counts"].numpy(),
+                     ref_counts=np.array([R["extras"]["n_valid_rays"], R["extras"]["n_tr"],
+                                          R["extras"]["n_fs"], R["extras"]["n_eik"]]))
+    finally:
+        dist.destroy_process_group()
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+@pytest.mark.timeout(600)
+def test_data_parallel_gloo_world2_equals_unsharded(tmp_path):
+    import torch.multiprocessing as mp
+    out = str(tmp_path / "dp.npz")
+    mp.spawn(_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    z = np.load(out)
+    # counts are integers: exact; parts / gradients: float64 summation order only
+    assert (z["counts"] == z["ref_counts"]).all()
+    np.testing.assert_allclose(z["parts"], z["ref_parts"], rtol=1e-12, atol=1e-15)
+    scale = np.abs(z["ref"]).max()
+    assert np.abs(z["got"] - z["ref"]).max() <= 1e-12 * scale
