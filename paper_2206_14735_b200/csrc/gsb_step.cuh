@@ -139,16 +139,17 @@ int run_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step
     nb_geo = std::max(1, std::min(nb_geo, kNbMax));
     nb_col = std::max(1, std::min(nb_col, kNbMax));
     if constexpr (F32) {
-      nb_geo = (int)((ns + per_cta - 1) / per_cta);     // one 32-sample batch per warp
+      constexpr int WGEO = 4;                          // one 32-sample batch per warp
+      nb_geo = (int)((ns + WGEO * 32 - 1) / (WGEO * 32));
       nb_col = (int)((z.MN + per_cta - 1) / per_cta);
-      const size_t smem_g = tc::GeoTc<S, WG>::smem();
+      const size_t smem_g = tc::GeoTc<S, WGEO>::smem();
       const size_t smem_c = tc::ColTc<S, WG>::smem();
-      GSB_CHECK(cudaFuncSetAttribute(tc::k_bwd_geom_tc<S, WG>,
+      GSB_CHECK(cudaFuncSetAttribute(tc::k_bwd_geom_tc<S, WGEO>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_g));
       GSB_CHECK(cudaFuncSetAttribute(tc::k_bwd_color_tc<S, WG>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_c));
-      tc::k_bwd_geom_tc<S, WG><<<nb_geo, per_cta, smem_g, stream>>>(w, G, M, N, mlp32, dep_final,
-                                                                    spts, nsp, 2);
+      tc::k_bwd_geom_tc<S, WGEO><<<nb_geo, WGEO * 32, smem_g, stream>>>(w, G, M, N, mlp32,
+                                                                        dep_final, spts, nsp, 2);
       GSB_LAUNCHED_T("k_bwd_geom");
       tc::k_bwd_color_tc<S, WG><<<nb_col, per_cta, smem_c, stream>>>(w, G, M, N, mlp32, dep_final);
       GSB_LAUNCHED_T("k_bwd_color");

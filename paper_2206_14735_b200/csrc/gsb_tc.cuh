@@ -174,6 +174,23 @@ __global__ void __launch_bounds__(32) k_wfrag(const float* __restrict__ mlp, uin
 
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 
+// value barrier: the compiler cannot see through it, so work that depends on
+// it is recomputed instead of kept live (and spilled) across the MLP phase
+__device__ __forceinline__ float opaque(float x) {
+  float y;
+  asm volatile("mov.b32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+template <typename T>
+__device__ __forceinline__ LocT<T> opaque(const LocT<T>& q) {
+  LocT<T> r;
+  r.base = __float_as_int(opaque(__int_as_float(q.base)));
+  r.fx = opaque(q.fx);
+  r.fy = opaque(q.fy);
+  r.fz = opaque(q.fz);
+  return r;
+}
+
 // A operand from the D fragment of feature block kk
 __device__ __forceinline__ void a_from_d(const float (&x)[4], uint32_t (&ah)[4], uint32_t (&al)[4]) {
   split_fast(x[0], ah[0], al[0]);
@@ -571,58 +588,59 @@ __global__ void __launch_bounds__(WARPS * 32) k_fwd_tc(Ws<float> w, Geo G, int M
   }
   mbar_wait(&s_bar, 0);
   __syncwarp();
-  // ---- colour: sigmoid(MLP_c([f_c, r]))  (gs/decoders.py:86-99)
-  {
-    float c0[2][4][4], c1[2][4][4], y[2][1][4];
-    fill_cols(c0, cvec + CVec::b0);
-    mma_layer<2, F::KC, 4>(
-        [&](int mt, int kk, uint32_t (&ah)[4], uint32_t (&al)[4]) { a_from_rows<ROW>(rows, K::oC, 16 * mt, kk, ah, al); },
-        sfr + F::C_W0 * 32, c0);
-    relu_d(c0);
-    fill_cols(c1, cvec + CVec::b1);
-    mma_layer<2, 4, 4>([&](int mt, int kk, uint32_t (&ah)[4], uint32_t (&al)[4]) { a_from_d(c0[mt][kk], ah, al); },
-                       sfr + F::C_W1 * 32, c1);
-    relu_d(c1);
-    fill_cols(y, cvec + CVec::b2);
-    mma_layer<2, 4, 1>([&](int mt, int kk, uint32_t (&ah)[4], uint32_t (&al)[4]) { a_from_d(c1[mt][kk], ah, al); },
-                       sfr + F::C_W2 * 32, y);
+  // MLP phases one m-tile (16 samples) at a time: half the live fragments
+  // (occupancy), B fragments re-read from shared memory per m-tile
+#pragma unroll 1
+  for (int mt = 0; mt < 2; ++mt) {
+    float* rm = rows + 16 * mt * ROW;
+    // ---- colour: sigmoid(MLP_c([f_c, r]))  (gs/decoders.py:86-99)
+    {
+      float c0[1][4][4], c1[1][4][4], y[1][1][4];
+      fill_cols(c0, cvec + CVec::b0);
+      mma_layer<1, F::KC, 4>(
+          [&](int, int kk, uint32_t (&ah)[4], uint32_t (&al)[4]) { a_from_rows<ROW>(rm, K::oC, 0, kk, ah, al); },
+          sfr + F::C_W0 * 32, c0);
+      relu_d(c0);
+      fill_cols(c1, cvec + CVec::b1);
+      mma_layer<1, 4, 4>([&](int, int kk, uint32_t (&ah)[4], uint32_t (&al)[4]) { a_from_d(c0[0][kk], ah, al); },
+                         sfr + F::C_W1 * 32, c1);
+      relu_d(c1);
+      fill_cols(y, cvec + CVec::b2);
+      mma_layer<1, 4, 1>([&](int, int kk, uint32_t (&ah)[4], uint32_t (&al)[4]) { a_from_d(c1[0][kk], ah, al); },
+                         sfr + F::C_W2 * 32, y);
 #pragma unroll
-    for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-      for (int r = 0; r < 4; ++r) y[mt][0][r] = sigmoid_fast(y[mt][0][r]);
-    store_d<ROW>(y, rows, K::oY);
-  }
-  // ---- geometry: phi and dphi/dz = W0 ((W1 (W2 . m1)) . m0)
-  {
-    float h0[2][4][4], h1[2][4][4];
-    fill_cols(h0, gvec + GVec::b0);
-    mma_layer<2, F::KG, 4>(
-        [&](int mt, int kk, uint32_t (&ah)[4], uint32_t (&al)[4]) { a_from_rows<ROW>(rows, K::oZ, 16 * mt, kk, ah, al); },
-        sfr + F::G_W0 * 32, h0);
-    const uint32_t m0 = relu_d(h0);
-    fill_cols(h1, gvec + GVec::b1);
-    mma_layer<2, 4, 4>([&](int mt, int kk, uint32_t (&ah)[4], uint32_t (&al)[4]) { a_from_d(h0[mt][kk], ah, al); },
-                       sfr + F::G_W1 * 32, h1);
-    const uint32_t m1 = relu_d(h1);
-    float ph[2][2];
-    phi_d(h1, gvec + GVec::w2, gvec[GVec::b2], ph);
-    // delta chain (h0 and h1 registers reused)
-    delta1_d(h1, m1, gvec + GVec::w2);
-    zero_d(h0);
-    mma_layer<2, 4, 4>([&](int mt, int kk, uint32_t (&ah)[4], uint32_t (&al)[4]) { a_from_d(h1[mt][kk], ah, al); },
-                       sfr + F::G_W1T * 32, h0);
-    mask_d(h0, m0);
-    float gz[2][F::KG][4];
-    zero_d(gz);
-    mma_layer<2, 4, F::KG>([&](int mt, int kk, uint32_t (&ah)[4], uint32_t (&al)[4]) { a_from_d(h0[mt][kk], ah, al); },
-                           sfr + F::G_W0T * 32, gz);
-    __syncwarp();  // every lane's z / colour-input reads are done
-    store_d<ROW>(gz, rows, K::oZ);
-    if ((lane & 3) == 0) {
-#pragma unroll
-      for (int mt = 0; mt < 2; ++mt) {
-        rows[(16 * mt + g) * ROW + K::oC] = ph[mt][0];
-        rows[(16 * mt + g + 8) * ROW + K::oC] = ph[mt][1];
+      for (int r = 0; r < 4; ++r) y[0][0][r] = sigmoid_fast(y[0][0][r]);
+      store_d<ROW>(y, rm, K::oY);
+    }
+    // ---- geometry: phi and dphi/dz = W0 ((W1 (W2 . m1)) . m0)
+    {
+      float h0[1][4][4], h1[1][4][4];
+      fill_cols(h0, gvec + GVec::b0);
+      mma_layer<1, F::KG, 4>(
+          [&](int, int kk, uint32_t (&ah)[4], uint32_t (&al)[4]) { a_from_rows<ROW>(rm, K::oZ, 0, kk, ah, al); },
+          sfr + F::G_W0 * 32, h0);
+      const uint32_t m0 = relu_d(h0);
+      fill_cols(h1, gvec + GVec::b1);
+      mma_layer<1, 4, 4>([&](int, int kk, uint32_t (&ah)[4], uint32_t (&al)[4]) { a_from_d(h0[0][kk], ah, al); },
+                         sfr + F::G_W1 * 32, h1);
+      const uint32_t m1 = relu_d(h1);
+      float ph[1][2];
+      phi_d(h1, gvec + GVec::w2, gvec[GVec::b2], ph);
+      // delta chain (h0 and h1 registers reused)
+      delta1_d(h1, m1, gvec + GVec::w2);
+      zero_d(h0);
+      mma_layer<1, 4, 4>([&](int, int kk, uint32_t (&ah)[4], uint32_t (&al)[4]) { a_from_d(h1[0][kk], ah, al); },
+                         sfr + F::G_W1T * 32, h0);
+      mask_d(h0, m0);
+      float gz[1][F::KG][4];
+      zero_d(gz);
+      mma_layer<1, 4, F::KG>([&](int, int kk, uint32_t (&ah)[4], uint32_t (&al)[4]) { a_from_d(h0[0][kk], ah, al); },
+                             sfr + F::G_W0T * 32, gz);
+      __syncwarp();  // every lane's z / colour-input reads of this m-tile are done
+      store_d<ROW>(gz, rm, K::oZ);
+      if ((lane & 3) == 0) {
+        rm[g * ROW + K::oC] = ph[0][0];
+        rm[(g + 8) * ROW + K::oC] = ph[0][1];
       }
     }
   }
@@ -647,19 +665,18 @@ __global__ void __launch_bounds__(WARPS * 32) k_fwd_tc(Ws<float> w, Geo G, int M
 template <class S, int WARPS>
 struct GeoTc {
   using F = Fr<S>;
-  static constexpr int ROW = 136;
+  static constexpr int ROW = 104;  // 6 warps x 13 KB + 25 KB weights: 2 CTAs = 12 warps / SM
   static constexpr int oZ = 0;     // z, later dphi/dz (16)
-  static constexpr int oV = 16;    // v = sum_k ju_k theta_k (16)
-  static constexpr int oA0 = 32;   // p z + v (16)
-  static constexpr int oP = 48;    // p
-  static constexpr int oM = 49;    // m1 bits
-  static constexpr int oB0 = 56;   // delta0 (32)
-  static constexpr int oA1 = 88;   // p h0 + q0 (32)
-  static constexpr int oL = 120;   // grid locations, 4 per level (base bits, fx, fy, fz)
+  static constexpr int oA0 = 16;   // p z + v (16)
+  static constexpr int oP = 32;    // p
+  static constexpr int oM = 33;    // m1 bits
+  static constexpr int oB0 = 40;   // delta0 (32)
+  static constexpr int oV = oB0;   // v = sum_k ju_k theta_k (16): consumed before delta0 lands
+  static constexpr int oA1 = 72;   // p h0 + q0 (32)
   static constexpr int NFR = F::NGEO;
   static constexpr size_t smem_rows() { return (size_t)WARPS * 32 * ROW * 4; }
   static constexpr size_t smem() { return (size_t)NFR * 32 * 16 + GVec::N * 4 + smem_rows(); }
-  static_assert(oL + 4 * S::NL <= ROW && ROW % 32 == 8 && S::IN_G <= 16, "row layout");
+  static_assert(oA1 + GSB_HID <= ROW && ROW % 32 == 8 && S::IN_G <= 16, "row layout");
 };
 
 template <class S, int WARPS>
@@ -685,8 +702,8 @@ __global__ void __launch_bounds__(WARPS * 32) k_bwd_geom_tc(Ws<float> w, Geo G, 
   const int64_t MN = (int64_t)M * N, NS = MN + nsp;
   const int64_t s = ((int64_t)blockIdx.x * WARPS + wid) * 32 + lane;
   const bool active = s < NS;
-  // ---- per sample: point, z and v in one pass over the corners; the grid
-  // locations wait in the row (registers are the MLP phase's)
+  // ---- per sample: point, z and v in one pass over the corners
+  LocT<float> loc[S::NL];
   {
     float p = 0.f, u[3] = {0.f, 0.f, 0.f};
     float pt[3];
@@ -713,7 +730,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_bwd_geom_tc(Ws<float> w, Geo G, 
     for (int l = 0; l < S::NL; ++l) {
       const LevelDev& L = G.lv[l];
       const LocT<float> lq = compact<float>(locate<false>(L, (double)pt[0], (double)pt[1], (double)pt[2], nullptr));
-      *reinterpret_cast<float4*>(myrow + K::oL + 4 * l) = make_float4(__int_as_float(lq.base), lq.fx, lq.fy, lq.fz);
+      loc[l] = lq;
       float wk[8], ju[8];
       corner_w_ju(lq, (float)L.inv_vs, u, wk, ju);
       const float* Fp = reinterpret_cast<const float*>(L.feat) + (int64_t)lq.base * S::CG;
@@ -739,99 +756,88 @@ __global__ void __launch_bounds__(WARPS * 32) k_bwd_geom_tc(Ws<float> w, Geo G, 
   }
   mbar_wait(&s_bar, 0);
   __syncwarp();
-  // ---- MLP on the tensor cores (both m-tiles of the warp's 32 samples)
-  float pr[2][2];  // p of rows g, g+8 per m-tile
-#pragma unroll
-  for (int mt = 0; mt < 2; ++mt) {
-    pr[mt][0] = rows[(16 * mt + g) * ROW + K::oP];
-    pr[mt][1] = rows[(16 * mt + g + 8) * ROW + K::oP];
-  }
+  // ---- MLP on the tensor cores, one m-tile (16 samples) at a time
   float accb0[4][2], accb1[4][2], accw2[4][2];  // column partial sums (cols 8nn+2t+c)
-  float h0[2][4][4], h1[2][4][4];
-  fill_cols(h0, gvec + GVec::b0);
-  mma_layer<2, F::KG, 4>(
-      [&](int mt, int kk, uint32_t (&ah)[4], uint32_t (&al)[4]) { a_from_rows<ROW>(rows, K::oZ, 16 * mt, kk, ah, al); },
-      sfr + F::G_W0 * 32, h0);
-  const uint32_t m0 = relu_d(h0);
-  fill_cols(h1, gvec + GVec::b1);
-  mma_layer<2, 4, 4>([&](int mt, int kk, uint32_t (&ah)[4], uint32_t (&al)[4]) { a_from_d(h0[mt][kk], ah, al); },
-                     sfr + F::G_W1 * 32, h1);
-  // A1 = p h0 (+ q0 below) parked in the row so h0 dies here
-#pragma unroll
-  for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-    for (int nn = 0; nn < 4; ++nn)
-#pragma unroll
-      for (int r = 0; r < 4; ++r) h0[mt][nn][r] *= pr[mt][r >> 1];
-  store_d<ROW>(h0, rows, K::oA1);
-  const uint32_t m1 = relu_d(h1);
-  // dW2 += p h1 (column sums); per-sample m1 masks for the dW1 outer product
 #pragma unroll
   for (int nn = 0; nn < 4; ++nn)
 #pragma unroll
-    for (int c = 0; c < 2; ++c)
-      accw2[nn][c] = pr[0][0] * h1[0][nn][c] + pr[0][1] * h1[0][nn][2 + c] + pr[1][0] * h1[1][nn][c] +
-                     pr[1][1] * h1[1][nn][2 + c];
+    for (int c = 0; c < 2; ++c) accb0[nn][c] = accb1[nn][c] = accw2[nn][c] = 0.f;
+#pragma unroll 1
+  for (int mt = 0; mt < 2; ++mt) {
+    float* rm = rows + 16 * mt * ROW;
+    const float pg[2] = {rm[g * ROW + K::oP], rm[(g + 8) * ROW + K::oP]};  // p of rows g, g+8
+    float h0[1][4][4], h1[1][4][4];
+    fill_cols(h0, gvec + GVec::b0);
+    mma_layer<1, F::KG, 4>(
+        [&](int, int kk, uint32_t (&ah)[4], uint32_t (&al)[4]) { a_from_rows<ROW>(rm, K::oZ, 0, kk, ah, al); },
+        sfr + F::G_W0 * 32, h0);
+    const uint32_t m0 = relu_d(h0);
+    fill_cols(h1, gvec + GVec::b1);
+    mma_layer<1, 4, 4>([&](int, int kk, uint32_t (&ah)[4], uint32_t (&al)[4]) { a_from_d(h0[0][kk], ah, al); },
+                       sfr + F::G_W1 * 32, h1);
+    // A1 = p h0 (+ q0 below) parked in the row so h0 dies here
 #pragma unroll
-  for (int mt = 0; mt < 2; ++mt)
+    for (int nn = 0; nn < 4; ++nn)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) h0[0][nn][r] *= pg[r >> 1];
+    store_d<ROW>(h0, rm, K::oA1);
+    const uint32_t m1 = relu_d(h1);
+    // dW2 += p h1 (column sums); per-sample m1 masks for the dW1 outer product
+#pragma unroll
+    for (int nn = 0; nn < 4; ++nn)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) accw2[nn][c] += pg[0] * h1[0][nn][c] + pg[1] * h1[0][nn][2 + c];
 #pragma unroll
     for (int hf = 0; hf < 2; ++hf) {
-      const uint32_t rm = row_mask(m1, mt, hf);
-      if (t == 0) reinterpret_cast<uint32_t*>(rows + (16 * mt + g + 8 * hf) * ROW + K::oM)[0] = rm;
+      const uint32_t msk = row_mask(m1, 0, hf);
+      if (t == 0) reinterpret_cast<uint32_t*>(rm + (g + 8 * hf) * ROW + K::oM)[0] = msk;
     }
-  // q0 = (v W0) . m0 ; A1 = p h0 + q0 ; dd1 = (q0 W1) . m1 -> dW2
-  {
-    float q0[2][4][4];
-    zero_d(q0);
-    mma_layer<2, F::KG, 4>(
-        [&](int mt, int kk, uint32_t (&ah)[4], uint32_t (&al)[4]) { a_from_rows<ROW>(rows, K::oV, 16 * mt, kk, ah, al); },
-        sfr + F::G_W0 * 32, q0);
-    mask_d(q0, m0);
-    load_d<ROW>(h0, rows, K::oA1);
-#pragma unroll
-    for (int mt = 0; mt < 2; ++mt)
+    // q0 = (v W0) . m0 ; A1 = p h0 + q0 ; dd1 = (q0 W1) . m1 -> dW2
+    {
+      float q0[1][4][4];
+      zero_d(q0);
+      mma_layer<1, F::KG, 4>(
+          [&](int, int kk, uint32_t (&ah)[4], uint32_t (&al)[4]) { a_from_rows<ROW>(rm, K::oV, 0, kk, ah, al); },
+          sfr + F::G_W0 * 32, q0);
+      mask_d(q0, m0);
+      load_d<ROW>(h0, rm, K::oA1);
 #pragma unroll
       for (int nn = 0; nn < 4; ++nn)
 #pragma unroll
-        for (int r = 0; r < 4; ++r) h0[mt][nn][r] += q0[mt][nn][r];
-    store_d<ROW>(h0, rows, K::oA1);
-    zero_d(h1);
-    mma_layer<2, 4, 4>([&](int mt, int kk, uint32_t (&ah)[4], uint32_t (&al)[4]) { a_from_d(q0[mt][kk], ah, al); },
-                       sfr + F::G_W1 * 32, h1);
-    mask_d(h1, m1);
+        for (int r = 0; r < 4; ++r) h0[0][nn][r] += q0[0][nn][r];
+      store_d<ROW>(h0, rm, K::oA1);
+      zero_d(h1);
+      mma_layer<1, 4, 4>([&](int, int kk, uint32_t (&ah)[4], uint32_t (&al)[4]) { a_from_d(q0[0][kk], ah, al); },
+                         sfr + F::G_W1 * 32, h1);
+      mask_d(h1, m1);
+#pragma unroll
+      for (int nn = 0; nn < 4; ++nn)
+#pragma unroll
+        for (int c = 0; c < 2; ++c) accw2[nn][c] += h1[0][nn][c] + h1[0][nn][2 + c];
+    }
+    // delta1 = m1 . W2 -> db1 = sum p delta1 ; delta0 = (delta1 W1^T) . m0 -> rows, db0 ;
+    // dphi/dz = delta0 W0^T -> rows (scatter)
+    delta1_d(h1, m1, gvec + GVec::w2);
 #pragma unroll
     for (int nn = 0; nn < 4; ++nn)
 #pragma unroll
-      for (int c = 0; c < 2; ++c)
-        accw2[nn][c] += h1[0][nn][c] + h1[0][nn][2 + c] + h1[1][nn][c] + h1[1][nn][2 + c];
-  }
-  // delta1 = m1 . W2 -> db1 = sum p delta1 ; delta0 = (delta1 W1^T) . m0 -> rows, db0 ;
-  // dphi/dz = delta0 W0^T -> rows (scatter)
-  delta1_d(h1, m1, gvec + GVec::w2);
+      for (int c = 0; c < 2; ++c) accb1[nn][c] += pg[0] * h1[0][nn][c] + pg[1] * h1[0][nn][2 + c];
+    zero_d(h0);
+    mma_layer<1, 4, 4>([&](int, int kk, uint32_t (&ah)[4], uint32_t (&al)[4]) { a_from_d(h1[0][kk], ah, al); },
+                       sfr + F::G_W1T * 32, h0);
+    mask_d(h0, m0);
 #pragma unroll
-  for (int nn = 0; nn < 4; ++nn)
+    for (int nn = 0; nn < 4; ++nn)
 #pragma unroll
-    for (int c = 0; c < 2; ++c)
-      accb1[nn][c] = pr[0][0] * h1[0][nn][c] + pr[0][1] * h1[0][nn][2 + c] + pr[1][0] * h1[1][nn][c] +
-                     pr[1][1] * h1[1][nn][2 + c];
-  zero_d(h0);
-  mma_layer<2, 4, 4>([&](int mt, int kk, uint32_t (&ah)[4], uint32_t (&al)[4]) { a_from_d(h1[mt][kk], ah, al); },
-                     sfr + F::G_W1T * 32, h0);
-  mask_d(h0, m0);
-#pragma unroll
-  for (int nn = 0; nn < 4; ++nn)
-#pragma unroll
-    for (int c = 0; c < 2; ++c)
-      accb0[nn][c] = pr[0][0] * h0[0][nn][c] + pr[0][1] * h0[0][nn][2 + c] + pr[1][0] * h0[1][nn][c] +
-                     pr[1][1] * h0[1][nn][2 + c];
-  store_d<ROW>(h0, rows, K::oB0);
-  {
-    float gz[2][F::KG][4];
+      for (int c = 0; c < 2; ++c) accb0[nn][c] += pg[0] * h0[0][nn][c] + pg[1] * h0[0][nn][2 + c];
+    __syncwarp();  // v reads of this m-tile are done: delta0 takes its slot
+    store_d<ROW>(h0, rm, K::oB0);
+    float gz[1][F::KG][4];
     zero_d(gz);
-    mma_layer<2, 4, F::KG>([&](int mt, int kk, uint32_t (&ah)[4], uint32_t (&al)[4]) { a_from_d(h0[mt][kk], ah, al); },
+    mma_layer<1, 4, F::KG>([&](int, int kk, uint32_t (&ah)[4], uint32_t (&al)[4]) { a_from_d(h0[0][kk], ah, al); },
                            sfr + F::G_W0T * 32, gz);
-    __syncwarp();  // z reads (first layer) are done in every lane
-    store_d<ROW>(gz, rows, K::oZ);
+    __syncwarp();  // z reads of this m-tile are done
+    store_d<ROW>(gz, rm, K::oZ);
   }
   __syncwarp();
   // ---- grid scatter: theta_l[idx_k] += g_l (p w_k + ju_k)
@@ -839,16 +845,11 @@ __global__ void __launch_bounds__(WARPS * 32) k_bwd_geom_tc(Ws<float> w, Geo G, 
   float u[3] = {0.f, 0.f, 0.f};
   if (active) {
 #pragma unroll
-    for (int a = 0; a < 3; ++a) u[a] = w.ubar[s * 3 + a];
+    for (int a = 0; a < 3; ++a) u[a] = opaque(w.ubar[s * 3 + a]);
   }
 #pragma unroll
   for (int l = 0; l < S::NL; ++l) {
-    const float4 lv = *reinterpret_cast<const float4*>(myrow + K::oL + 4 * l);
-    LocT<float> lq;
-    lq.base = __float_as_int(lv.x);
-    lq.fx = lv.y;
-    lq.fy = lv.z;
-    lq.fz = lv.w;
+    const LocT<float> lq = opaque(loc[l]);
     float wk[8], ju[8], coef[8];
     corner_w_ju(lq, (float)G.lv[l].inv_vs, u, wk, ju);
 #pragma unroll
