@@ -98,7 +98,7 @@ Ws<T> carve(void* ws, const Sizes& z, size_t* bytes, int64_t* off_parts = nullpt
   const int64_t nb = std::max<int64_t>(kNbMax, (z.NS + 127) / 128);
   w.nb_max = (int)nb;
   w.mlp_part = c.template take<T>(nb * z.nmlp);
-  w.wfrag = c.template take<uint4>(4096 + 44);  // tc::kFragBufU4: fragments + vector block
+  w.wfrag = c.template take<uint4>(4096 + 68);  // tc::kFragBufU4: fragments + vector block
   if (bytes) *bytes = c.off;
   if (off_parts) *off_parts = (int64_t)o_parts;
   if (off_counts) *off_counts = (int64_t)o_counts;

@@ -42,7 +42,7 @@ int run_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step
   constexpr int TW = 4;                  // warps per CTA of the float32 sample kernels
   const float* mlp32 = reinterpret_cast<const float*>(mlp);
   if constexpr (F32) {
-    static_assert(tc::kFragBufU4 == 4096 + 44, "workspace carve");
+    static_assert(tc::kFragBufU4 == 4096 + 68, "workspace carve");
     tc::k_wfrag<S><<<tc::Fr<S>::NALL + 1, 32, 0, stream>>>(mlp32, w.wfrag);
     GSB_LAUNCHED_T("k_wfrag");
   }
@@ -143,15 +143,17 @@ int run_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step
       nb_geo = (int)((ns + WGEO * 32 - 1) / (WGEO * 32));
       nb_col = (int)((z.MN + per_cta - 1) / per_cta);
       const size_t smem_g = tc::GeoTc<S, WGEO>::smem();
-      const size_t smem_c = tc::ColTc<S, WG>::smem();
+      constexpr int WCOL = 6;
+      nb_col = (int)((z.MN + WCOL * 32 - 1) / (WCOL * 32));
+      const size_t smem_c = tc::ColTc<S, WCOL>::smem();
       GSB_CHECK(cudaFuncSetAttribute(tc::k_bwd_geom_tc<S, WGEO>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_g));
-      GSB_CHECK(cudaFuncSetAttribute(tc::k_bwd_color_tc<S, WG>,
+      GSB_CHECK(cudaFuncSetAttribute(tc::k_bwd_color_tc<S, WCOL>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_c));
       tc::k_bwd_geom_tc<S, WGEO><<<nb_geo, WGEO * 32, smem_g, stream>>>(w, G, M, N, mlp32,
                                                                         dep_final, spts, nsp, 2);
       GSB_LAUNCHED_T("k_bwd_geom");
-      tc::k_bwd_color_tc<S, WG><<<nb_col, per_cta, smem_c, stream>>>(w, G, M, N, mlp32, dep_final);
+      tc::k_bwd_color_tc<S, WCOL><<<nb_col, WCOL * 32, smem_c, stream>>>(w, G, M, N, mlp32, dep_final);
       GSB_LAUNCHED_T("k_bwd_color");
     } else {
       constexpr int CW = S::NMLP - S::oCW0;

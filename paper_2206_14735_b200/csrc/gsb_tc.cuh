@@ -35,7 +35,7 @@ struct GVec {
   static constexpr int b0 = 0, b1 = 32, w2 = 64, b2 = 96, N = 104;
 };
 struct CVec {
-  static constexpr int b0 = 0, b1 = 32, b2 = 64, N = 72;
+  static constexpr int b0 = 0, b1 = 32, b2 = 64, w2 = 72, N = 168;  // w2: W2c (32 x 3)
 };
 constexpr int kFragBufU4 = kVecBase + (GVec::N + CVec::N) / 4;
 
@@ -121,6 +121,7 @@ __global__ void __launch_bounds__(32) k_wfrag(const float* __restrict__ mlp, uin
         if (j < 32) x = mlp[S::oCb0 + j];
         else if (j < 64) x = mlp[S::oCb1 + j - 32];
         else if (j < 67) x = mlp[S::oCb2 + j - 64];
+        else if (j >= CVec::w2 && j < CVec::w2 + 96) x = mlp[S::oCW2 + j - CVec::w2];
       }
       v[i] = x;
     }
@@ -376,6 +377,36 @@ __device__ __forceinline__ uint32_t row_mask(uint32_t m, int mt, int half) {
   r |= __shfl_xor_sync(0xffffffffu, r, 1);
   r |= __shfl_xor_sync(0xffffffffu, r, 2);
   return r;
+}
+
+// Sum v over the 8 lanes that share t (lane bits 2..4) as a butterfly
+// reduce-scatter: N/2 + N/4 + N/8 shuffles instead of 3N for an all-reduce.
+// The lane keeps chunk q = 4 b4 + 2 b3 + b2 (its lane bits) of N/8 values.
+template <int N>
+__device__ __forceinline__ void reduce_scatter_g(const float (&v)[N], float (&out)[N / 8]) {
+  static_assert(N % 8 == 0, "N");
+  const int lane = lane_id();
+  const bool h4 = (lane >> 4) & 1, h3 = (lane >> 3) & 1, h2 = (lane >> 2) & 1;
+  float a[N / 2], b[N / 4];
+#pragma unroll
+  for (int i = 0; i < N / 2; ++i) {
+    const float send = h4 ? v[i] : v[N / 2 + i];
+    a[i] = (h4 ? v[N / 2 + i] : v[i]) + __shfl_xor_sync(0xffffffffu, send, 16);
+  }
+#pragma unroll
+  for (int i = 0; i < N / 4; ++i) {
+    const float send = h3 ? a[i] : a[N / 4 + i];
+    b[i] = (h3 ? a[N / 4 + i] : a[i]) + __shfl_xor_sync(0xffffffffu, send, 8);
+  }
+#pragma unroll
+  for (int i = 0; i < N / 8; ++i) {
+    const float send = h2 ? b[i] : b[N / 8 + i];
+    out[i] = (h2 ? b[N / 8 + i] : b[i]) + __shfl_xor_sync(0xffffffffu, send, 4);
+  }
+}
+__device__ __forceinline__ int rs_chunk() {
+  const int lane = lane_id();
+  return 4 * ((lane >> 4) & 1) + 2 * ((lane >> 3) & 1) + ((lane >> 2) & 1);
 }
 
 // phi = h1 . W2 + b2 for rows g, g+8 of each m-tile (quad reduction)
@@ -940,22 +971,27 @@ __global__ void __launch_bounds__(WARPS * 32) k_bwd_geom_tc(Ws<float> w, Geo G, 
 template <class S, int WARPS>
 struct ColTc {
   using F = Fr<S>;
-  static constexpr int ROW = 168;
-  static constexpr int oA0 = 0;     // [inp (IN_C), 1, 0...] (16)
-  static constexpr int oB0 = 16;    // a0_bar (32)
-  static constexpr int oA1 = 48;    // h0c (32)
-  static constexpr int oB1 = 80;    // a1_bar (32)
-  static constexpr int oH1 = 112;   // h1c (32)
-  static constexpr int oY = 144;    // y_bar (8 columns, 3 used)
-  static constexpr int oFB = 152;   // f_bar (8 columns, CC used)
+  static constexpr int ROW = 104;  // 6 warps x 13 KB + 27 KB weights: 2 CTAs = 12 warps / SM
+  static constexpr int oA0 = 0;    // [inp (IN_C), 1, 0...] (16)
+  static constexpr int oB0 = 16;   // a0_bar (32)
+  static constexpr int oA1 = 48;   // h0c (32)
+  static constexpr int oY = 80;    // y_bar (8 columns, 3 used)
+  static constexpr int oM = 88;    // m1 bits (colour layer 1)
+  static constexpr int oFB = 90;   // f_bar (8 columns, CC used)
+  static constexpr int oCB = 98;   // cbar prefetch (3)
   static constexpr int NFR = F::NALL - F::NGEO;
   static constexpr size_t smem_rows() { return (size_t)WARPS * 32 * ROW * 4; }
   static constexpr size_t smem() { return (size_t)NFR * 32 * 16 + CVec::N * 4 + smem_rows(); }
-  static_assert(oFB + 8 <= ROW && ROW % 32 == 8 && S::IN_C + 1 <= 16 && S::CC <= 8, "row layout");
+  static_assert(oCB + 3 <= ROW && ROW % 32 == 8 && S::IN_C + 1 <= 16 && S::CC <= 8 && GSB_HID == 32,
+                "row layout");
 };
 
+// Colour backward.  Sample-major rows hold only the outer-product factors
+// [inp, 1] and a0_bar (dW0c, db0c) and h0c (dW1c); the dW1c partner a1_bar
+// is rebuilt per fragment from y_bar, the layer-1 mask and W2c; dW2c, db1c
+// and db2c are column sums of D fragments.
 template <class S, int WARPS>
-__global__ void __launch_bounds__(WARPS * 32) k_bwd_color_tc(Ws<float> w, Geo G, int M, int N,
+__global__ void __launch_bounds__(WARPS * 32, 2) k_bwd_color_tc(Ws<float> w, Geo G, int M, int N,
                                                              const float* __restrict__ mlp,
                                                              const double* __restrict__ dep) {
   using K = ColTc<S, WARPS>;
@@ -984,6 +1020,8 @@ __global__ void __launch_bounds__(WARPS * 32) k_bwd_color_tc(Ws<float> w, Geo G,
     taped_point<float>(w.o + ray * 3, w.r + ray * 3,
                        active ? dep[(int64_t)ray * w.ld + (int)((uint32_t)s % (uint32_t)N)] : 0.0,
                        G.lo, G.hi, pt);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) myrow[K::oCB + c] = active ? w.cbar[s * 3 + c] : 0.f;
     q = compact<float>(locate<false>(G.col, (double)pt[0], (double)pt[1], (double)pt[2], nullptr));
     float inp[16];
 #pragma unroll
@@ -997,50 +1035,92 @@ __global__ void __launch_bounds__(WARPS * 32) k_bwd_color_tc(Ws<float> w, Geo G,
   }
   mbar_wait(&s_bar, 0);
   __syncwarp();
-  // ---- forward (masks, h0c, h1c) and y_bar = cbar * y (1 - y)
-  float c0[2][4][4], c1[2][4][4];
-  fill_cols(c0, cvec + CVec::b0);
-  mma_layer<2, F::KC, 4>(
-      [&](int mt, int kk, uint32_t (&ah)[4], uint32_t (&al)[4]) { a_from_rows<ROW>(rows, K::oA0, 16 * mt, kk, ah, al); },
-      fr + F::C_W0 * 32, c0);
-  const uint32_t m0 = relu_d(c0);
-  store_d<ROW>(c0, rows, K::oA1);
-  fill_cols(c1, cvec + CVec::b1);
-  mma_layer<2, 4, 4>([&](int mt, int kk, uint32_t (&ah)[4], uint32_t (&al)[4]) { a_from_d(c0[mt][kk], ah, al); },
-                     fr + F::C_W1 * 32, c1);
-  const uint32_t m1 = relu_d(c1);
-  store_d<ROW>(c1, rows, K::oH1);
-  float yb[2][1][4];
-  fill_cols(yb, cvec + CVec::b2);
-  mma_layer<2, 4, 1>([&](int mt, int kk, uint32_t (&ah)[4], uint32_t (&al)[4]) { a_from_d(c1[mt][kk], ah, al); },
-                     fr + F::C_W2 * 32, yb);
+  // ---- per m-tile: forward (masks, h0c), y_bar, a1_bar, a0_bar, f_bar
+  // column sums, reduced over the warp per m-tile (reduce_scatter_g): this lane
+  // owns column j = 8 (q >> 1) + 2t + (q & 1) of db1c and dW2c, q = rs_chunk()
+  float sb1 = 0.f, sw2[3] = {0.f, 0.f, 0.f}, accb2[3];
 #pragma unroll
-  for (int mt = 0; mt < 2; ++mt)
+  for (int c = 0; c < 3; ++c) accb2[c] = 0.f;
+#pragma unroll 1
+  for (int mt = 0; mt < 2; ++mt) {
+    float* rm = rows + 16 * mt * ROW;
+    float c0[1][4][4], c1[1][4][4];
+    fill_cols(c0, cvec + CVec::b0);
+    mma_layer<1, F::KC, 4>(
+        [&](int, int kk, uint32_t (&ah)[4], uint32_t (&al)[4]) { a_from_rows<ROW>(rm, K::oA0, 0, kk, ah, al); },
+        fr + F::C_W0 * 32, c0);
+    const uint32_t m0 = relu_d(c0);
+    store_d<ROW>(c0, rm, K::oA1);
+    fill_cols(c1, cvec + CVec::b1);
+    mma_layer<1, 4, 4>([&](int, int kk, uint32_t (&ah)[4], uint32_t (&al)[4]) { a_from_d(c0[0][kk], ah, al); },
+                       fr + F::C_W1 * 32, c1);
+    const uint32_t m1 = relu_d(c1);
+#pragma unroll
+    for (int hf = 0; hf < 2; ++hf) {
+      const uint32_t msk = row_mask(m1, 0, hf);
+      if (t == 0) reinterpret_cast<uint32_t*>(rm + (g + 8 * hf) * ROW + K::oM)[0] = msk;
+    }
+    float yb[1][1][4];
+    fill_cols(yb, cvec + CVec::b2);
+    mma_layer<1, 4, 1>([&](int, int kk, uint32_t (&ah)[4], uint32_t (&al)[4]) { a_from_d(c1[0][kk], ah, al); },
+                       fr + F::C_W2 * 32, yb);
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
       const int col = 2 * t + (r & 1);
-      const int64_t sr = base + 16 * mt + g + 8 * (r >> 1);
-      const float cc = sigmoid_fast(yb[mt][0][r]);
-      yb[mt][0][r] = (col < 3 && sr < NS) ? w.cbar[sr * 3 + col] * (cc * (1.f - cc)) : 0.f;
+      const float cc = sigmoid_fast(yb[0][0][r]);
+      yb[0][0][r] = col < 3 ? rm[(g + 8 * (r >> 1)) * ROW + K::oCB + col] * (cc * (1.f - cc)) : 0.f;
     }
-  store_d<ROW>(yb, rows, K::oY);
-  // a1_bar = (y_bar W2c^T) . m1 ; a0_bar = (a1_bar W1c^T) . m0 ; f_bar = a0_bar W0c^T
-  zero_d(c1);
-  mma_layer<2, 1, 4>([&](int mt, int kk, uint32_t (&ah)[4], uint32_t (&al)[4]) { a_from_d(yb[mt][kk], ah, al); },
-                     fr + F::C_W2T * 32, c1);
-  mask_d(c1, m1);
-  store_d<ROW>(c1, rows, K::oB1);
-  zero_d(c0);
-  mma_layer<2, 4, 4>([&](int mt, int kk, uint32_t (&ah)[4], uint32_t (&al)[4]) { a_from_d(c1[mt][kk], ah, al); },
-                     fr + F::C_W1T * 32, c0);
-  mask_d(c0, m0);
-  store_d<ROW>(c0, rows, K::oB0);
-  {
-    float fb[2][F::NCC][4];
+    store_d<ROW>(yb, rm, K::oY);
+    // y_bar of rows g, g+8 in every lane of the quad (cols 0,1 live in t=0, col 2 in t=1)
+    float yv[2][3];
+#pragma unroll
+    for (int hf = 0; hf < 2; ++hf) {
+      const int src = lane & ~3;
+      yv[hf][0] = __shfl_sync(0xffffffffu, yb[0][0][2 * hf], src);
+      yv[hf][1] = __shfl_sync(0xffffffffu, yb[0][0][2 * hf + 1], src);
+      yv[hf][2] = __shfl_sync(0xffffffffu, yb[0][0][2 * hf], src + 1);
+    }
+    // dW2c += h1c^T y_bar: this m-tile's column sums, reduced over the warp and
+    // accumulated (m-tile order) in the rows' spare columns; db2c += y_bar
+    {
+      float pw[24], r3[3];
+#pragma unroll
+      for (int nn = 0; nn < 4; ++nn)
+#pragma unroll
+        for (int cc = 0; cc < 2; ++cc)
+#pragma unroll
+          for (int c = 0; c < 3; ++c)
+            pw[(nn * 2 + cc) * 3 + c] = fmaf(c1[0][nn][cc], yv[0][c], c1[0][nn][2 + cc] * yv[1][c]);
+      reduce_scatter_g(pw, r3);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) sw2[c] += r3[c];
+    }
+#pragma unroll
+    for (int c = 0; c < 3; ++c) accb2[c] += yv[0][c] + yv[1][c];
+    // a1_bar = (y_bar W2c^T) . m1 -> db1c ; a0_bar = (a1_bar W1c^T) . m0 -> rows ; f_bar
+    zero_d(c1);
+    mma_layer<1, 1, 4>([&](int, int kk, uint32_t (&ah)[4], uint32_t (&al)[4]) { a_from_d(yb[0][kk], ah, al); },
+                       fr + F::C_W2T * 32, c1);
+    mask_d(c1, m1);
+    {
+      float pb[8], r1[1];
+#pragma unroll
+      for (int nn = 0; nn < 4; ++nn)
+#pragma unroll
+        for (int cc = 0; cc < 2; ++cc) pb[nn * 2 + cc] = c1[0][nn][cc] + c1[0][nn][2 + cc];
+      reduce_scatter_g(pb, r1);
+      sb1 += r1[0];
+    }
+    zero_d(c0);
+    mma_layer<1, 4, 4>([&](int, int kk, uint32_t (&ah)[4], uint32_t (&al)[4]) { a_from_d(c1[0][kk], ah, al); },
+                       fr + F::C_W1T * 32, c0);
+    mask_d(c0, m0);
+    store_d<ROW>(c0, rm, K::oB0);
+    float fb[1][F::NCC][4];
     zero_d(fb);
-    mma_layer<2, 4, F::NCC>([&](int mt, int kk, uint32_t (&ah)[4], uint32_t (&al)[4]) { a_from_d(c0[mt][kk], ah, al); },
+    mma_layer<1, 4, F::NCC>([&](int, int kk, uint32_t (&ah)[4], uint32_t (&al)[4]) { a_from_d(c0[0][kk], ah, al); },
                             fr + F::C_W0T * 32, fb);
-    store_d<ROW>(fb, rows, K::oFB);
+    store_d<ROW>(fb, rm, K::oFB);
   }
   __syncwarp();
   {  // colour grid scatter: theta_c[idx_k] += w_k f_bar (warp-segmented)
@@ -1048,11 +1128,15 @@ __global__ void __launch_bounds__(WARPS * 32) k_bwd_color_tc(Ws<float> w, Geo G,
     corner_w(q, wk);
     scatter_level<float, S::CC>(G.col, q, myrow + K::oFB, wk, active, false);
   }
-  // ---- outer products: e0 = [inp,1]^T a0b, e1 = h0c^T a1b, e2 = h1c^T y_bar
-  float e0[1][4][4], e1[2][4][4], e2[2][1][4];
+  // ---- outer products over the warp's samples: e0 = [inp,1]^T a0b, e1 = h0c^T a1b
+  float w2c[4][3];  // W2c rows n = 8nt + g
+#pragma unroll
+  for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) w2c[nt][c] = cvec[CVec::w2 + (8 * nt + g) * 3 + c];
+  float e0[1][4][4], e1[2][4][4];
   zero_d(e0);
   zero_d(e1);
-  zero_d(e2);
 #pragma unroll
   for (int ks = 0; ks < 4; ++ks) {
     const int k0 = ks * 8;
@@ -1064,27 +1148,31 @@ __global__ void __launch_bounds__(WARPS * 32) k_bwd_color_tc(Ws<float> w, Geo G,
       for (int nt = 0; nt < 4; ++nt) frag_b(rows, ROW, K::oB0, k0, nt * 8, bh0[nt], bh1[nt], bl0[nt], bl1[nt]);
       mma3_sweep(e0, a1h, a1l, bh0, bh1, bl0, bl1);
     }
-    // dW1c += h0c^T a1b
+    {  // dW1c += h0c^T a1b, a1b[k][n] = m1_k(n) ? sum_c W2c[n][c] y_bar_k[c] : 0
+      const float* r0 = rows + (k0 + t) * ROW;
+      const float* r1 = rows + (k0 + t + 4) * ROW;
+      const uint32_t mk0 = reinterpret_cast<const uint32_t*>(r0 + K::oM)[0];
+      const uint32_t mk1 = reinterpret_cast<const uint32_t*>(r1 + K::oM)[0];
+      const float y00 = r0[K::oY], y01 = r0[K::oY + 1], y02 = r0[K::oY + 2];
+      const float y10 = r1[K::oY], y11 = r1[K::oY + 1], y12 = r1[K::oY + 2];
 #pragma unroll
-    for (int mt = 0; mt < 2; ++mt) frag_a(rows, ROW, K::oA1, k0, mt * 16, ah[mt], al[mt]);
+      for (int nt = 0; nt < 4; ++nt) {
+        const int n = nt * 8 + g;
+        const float v0 = fmaf(w2c[nt][0], y00, fmaf(w2c[nt][1], y01, w2c[nt][2] * y02));
+        const float v1 = fmaf(w2c[nt][0], y10, fmaf(w2c[nt][1], y11, w2c[nt][2] * y12));
+        split_fast(((mk0 >> n) & 1u) ? v0 : 0.f, bh0[nt], bl0[nt]);
+        split_fast(((mk1 >> n) & 1u) ? v1 : 0.f, bh1[nt], bl1[nt]);
+      }
 #pragma unroll
-    for (int nt = 0; nt < 4; ++nt) frag_b(rows, ROW, K::oB1, k0, nt * 8, bh0[nt], bh1[nt], bl0[nt], bl1[nt]);
-    mma3_sweep(e1, ah, al, bh0, bh1, bl0, bl1);
-    // dW2c += h1c^T y_bar
-#pragma unroll
-    for (int mt = 0; mt < 2; ++mt) frag_a(rows, ROW, K::oH1, k0, mt * 16, ah[mt], al[mt]);
-    {
-      uint32_t yh0[1], yh1[1], yl0[1], yl1[1];
-      frag_b(rows, ROW, K::oY, k0, 0, yh0[0], yh1[0], yl0[0], yl1[0]);
-      mma3_sweep(e2, ah, al, yh0, yh1, yl0, yl1);
+      for (int mt = 0; mt < 2; ++mt) frag_a(rows, ROW, K::oA1, k0, mt * 16, ah[mt], al[mt]);
+      mma3_sweep(e1, ah, al, bh0, bh1, bl0, bl1);
     }
   }
-  float acc_b1 = 0.f, acc_b2 = 0.f;
-#pragma unroll 4
-  for (int r = 0; r < 32; ++r) {
-    const float* rw = rows + (size_t)r * ROW;
-    acc_b1 += rw[K::oB1 + lane];                       // db1 = sum a1_bar
-    acc_b2 += lane < 3 ? rw[K::oY + lane] : 0.f;        // db2 = sum y_bar
+  // column sums over the warp: reduce the 8 lanes sharing t
+#pragma unroll
+  for (int o = 4; o < 32; o <<= 1) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) accb2[c] += __shfl_xor_sync(0xffffffffu, accb2[c], o);
   }
   __syncthreads();
   constexpr int NCP = S::NMLP - S::NG;
@@ -1099,19 +1187,15 @@ __global__ void __launch_bounds__(WARPS * 32) k_bwd_color_tc(Ws<float> w, Geo G,
     for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
       for (int nt = 0; nt < 4; ++nt) frag_d_store(e1[mt][nt], mine + (S::oCW1 - o), mt * 16, nt * 8, GSB_HID);
-    mine[S::oCb1 - o + lane] = acc_b1;
-    if (lane < 3) mine[S::oCb2 - o + lane] = acc_b2;
+    {
+      const int q = rs_chunk(), j = 8 * (q >> 1) + 2 * t + (q & 1);
+      mine[S::oCb1 - o + j] = sb1;
 #pragma unroll
-    for (int mt = 0; mt < 2; ++mt) {
-      const int r0 = mt * 16 + g, r1 = r0 + 8, c = 2 * t;
-      if (c < 3) {
-        mine[S::oCW2 - o + r0 * 3 + c] = e2[mt][0][0];
-        mine[S::oCW2 - o + r1 * 3 + c] = e2[mt][0][2];
-      }
-      if (c + 1 < 3) {
-        mine[S::oCW2 - o + r0 * 3 + c + 1] = e2[mt][0][1];
-        mine[S::oCW2 - o + r1 * 3 + c + 1] = e2[mt][0][3];
-      }
+      for (int c = 0; c < 3; ++c) mine[S::oCW2 - o + j * 3 + c] = sw2[c];
+    }
+    if (lane == 0) {  // y_bar is quad-replicated: lane 0's sum covers every row once
+#pragma unroll
+      for (int c = 0; c < 3; ++c) mine[S::oCb2 - o + c] = accb2[c];
     }
   }
   __syncthreads();
