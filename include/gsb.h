@@ -201,6 +201,28 @@ int gsb_adam_step(int32_t precision, void* params, void* grads, void* m, void* v
                   int32_t n_seg, double beta1, double beta2, double eps, double c1, double c2,
                   const double* guard, double guard_threshold, int32_t* status, void* stream);
 
+/* ---------------- geometry on point lists ---------------- */
+
+/* Bytes of device workspace gsb_sdf_points / gsb_sdf_fit_step need for up to
+ * n_points points. */
+int gsb_sdf_workspace_size(const gsb_model_t* model, int64_t n_points, size_t* bytes);
+
+/* phi at n points (model dtype, (n, 3) -> (n,)), no grad: the geometry decoder
+ * on the multi-level grid (renderer._phi_data / decoders.decode_sdf on
+ * feature_grid.sample_multi, gs/renderer.py:236-240, gs/decoders.py:79-83). */
+int gsb_sdf_points(const gsb_model_t* model, const void* points, int64_t n, void* phi_out,
+                   void* workspace, size_t workspace_bytes, void* stream);
+
+/* One step of the sphere pre-fit (decoders.geometric_init inner loop,
+ * gs/decoders.py:160-167): points = n_batch uniform points then n_anchor
+ * anchors, targets their SDF (model dtype).  ADDS d/dtheta [mean_batch (phi-t)^2
+ * + mean_anchor (phi-t)^2] into the geometry levels' and geometry decoder's
+ * gradients (caller zeroes them); colour gradients are untouched.  The loss
+ * (double) is written to *loss_out (device pointer, may be NULL). */
+int gsb_sdf_fit_step(const gsb_model_t* model, const void* points, const void* targets,
+                     int64_t n_batch, int64_t n_anchor, void* workspace, size_t workspace_bytes,
+                     double* loss_out, void* stream);
+
 /* ---------------- unit twins (parity tests) ---------------- */
 
 int gsb_pcg64_random(const gsb_pcg64_t* rng, int64_t offset, int64_t n, double* out,

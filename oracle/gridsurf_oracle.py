@@ -812,6 +812,65 @@ class Adam:
             p[...] = p.astype(np.float64) - self.lrs[i] * (mi / c1) / (np.sqrt(vi / c2) + eps)
 
 
+class InitError(RuntimeError):
+    """gs/decoders.py InitError."""
+
+
+def geometric_init(P, center, radius, seed=0, max_steps=2000, tol=0.01, batch=4096,
+                   lr_grid=1e-2, lr_net=1e-3, info=None):
+    """gs/decoders.py:102-177: fit the geometry levels + decoder to a sphere SDF
+    with Adam on uniform in-box batches plus 13 anchors; early exit on the
+    held-out RMSE checks (step >= 100, every 50 steps); final 10k check."""
+    dt = P.dtype
+    center = np.asarray(center, dtype=np.float64)
+    lo = P.lo + 0.5 * P.finest_voxel
+    hi = P.hi - 0.5 * P.finest_voxel
+    if np.any(center - radius < P.lo) or np.any(center + radius > P.hi):
+        raise ValueError("sphere must fit inside the grid box")
+    L = len(P.levels)
+    names = [f"level{i}" for i in range(L)] + [f"geom_{k}{i}" for i in range(3) for k in ("w", "b")]
+    arrays = [P.levels[i].feat for i in range(L)] + [P.geom[i][j] for i in range(3) for j in (0, 1)]
+    opt = Adam(arrays, [lr_grid] * L + [lr_net] * 6)
+
+    def sdf(x):
+        return np.linalg.norm(x - center, axis=1, keepdims=True) - radius
+
+    axes = np.concatenate([np.eye(3), -np.eye(3)], axis=0)
+    anchors = np.clip(np.concatenate([center[None, :], center + radius * axes,
+                                      center + 2.0 * radius * axes]), lo, hi)
+    anchor_target = sdf(anchors).astype(dt)
+
+    def rmse(n_pts, idx):
+        pts = substream(seed, SPHERE_INIT, 10_000 + idx).uniform(lo, hi, size=(n_pts, 3))
+        phi = phi_data(P, pts.astype(dt))[:, None]
+        return float(np.sqrt(np.mean((phi - sdf(pts)) ** 2)))
+
+    def anchor_err():
+        phi = phi_data(P, anchors.astype(dt))[:, None]
+        return float(np.max(np.abs(phi - sdf(anchors))))
+
+    steps = 0
+    for step in range(max_steps):
+        pts = substream(seed, SPHERE_INIT, step).uniform(lo, hi, size=(batch, 3))
+        target = sdf(pts).astype(dt)
+        grads = {n: np.zeros_like(a) for n, a in zip(names, arrays)}
+        for x, t, n in ((pts.astype(dt), target, batch), (anchors.astype(dt), anchor_target, len(anchors))):
+            G = GeomPass(P, x)
+            g = dt.type(1.0) / dt.type(n)  # mean vjp, then mul vjp: g*err + g*err
+            pe = g * (G.phi - t[:, 0])
+            G.backward(pe + pe, np.zeros((x.shape[0], 3), dtype=dt), grads)
+        opt.step(arrays, [grads[n] for n in names])
+        steps += 1
+        if step >= 100 and step % 50 == 0 and rmse(2048, step) < 0.8 * tol and anchor_err() < 0.8 * tol:
+            break
+    final = rmse(10_000, -1)
+    if info is not None:
+        info["steps"] = steps
+    if final >= tol:
+        raise InitError(f"sphere pre-fit RMSE {final:.4f} m did not reach {tol} m within {max_steps} steps")
+    return final
+
+
 def train_step(P, opt, dataset, cfg, iteration):
     """gs/optimizer.py:363-373: one full iteration (draw, objective, grad, Adam)."""
     batch = draw_ray_batch(dataset, substream(cfg.seed, RAYS, iteration), cfg.batch_rays,

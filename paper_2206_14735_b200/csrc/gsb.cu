@@ -55,6 +55,15 @@ GSB_DECL(gsb_step_f446)
 GSB_DECL(gsb_step_d446)
 GSB_DECL(gsb_step_f222)
 GSB_DECL(gsb_step_d222)
+#define GSB_DECL_SDF(tag)                                                                       \
+  extern "C" int gsb_step_##tag##_sdf_points(const gsb_model_t*, const void*, int64_t, void*,  \
+                                             void*, size_t, cudaStream_t);                     \
+  extern "C" int gsb_step_##tag##_sdf_fit(const gsb_model_t*, const void*, const void*, int64_t, \
+                                          int64_t, void*, size_t, double*, cudaStream_t);
+GSB_DECL_SDF(f446)
+GSB_DECL_SDF(d446)
+GSB_DECL_SDF(f222)
+GSB_DECL_SDF(d222)
 
 namespace gsb_abi {
 
@@ -70,6 +79,16 @@ int dispatch_shape(const gsb_model_t* m, const gsb_dataset_t* d, const gsb_step_
   if (nl == 4 && cg == 4 && cc == 6) return f ? gsb_step_f446(m, d, st, s) : gsb_step_d446(m, d, st, s);
   if (nl == 2 && cg == 2 && cc == 2) return f ? gsb_step_f222(m, d, st, s) : gsb_step_d222(m, d, st, s);
   return GSB_E_ARG;
+}
+
+// shape tag of a model: 0 = (4,4,6), 1 = (2,2,2), -1 unsupported
+inline int shape_tag(const gsb_model_t* m) {
+  const int nl = m->n_levels, cg = m->levels[0].channels, cc = m->color.channels;
+  for (int l = 0; l < nl; ++l)
+    if (m->levels[l].channels != cg) return -1;
+  if (nl == 4 && cg == 4 && cc == 6) return 0;
+  if (nl == 2 && cg == 2 && cc == 2) return 1;
+  return -1;
 }
 
 template <typename T>
@@ -137,6 +156,55 @@ int gsb_timing_collect(int32_t max_kernels, char* names, double* total_ms, int64
   g_marks.clear();
   *n_kernels = n;
   return GSB_OK;
+}
+
+int gsb_sdf_workspace_size(const gsb_model_t* model, int64_t n_points, size_t* bytes) {
+  if (!model || !bytes || n_points <= 0) return GSB_E_ARG;
+  const int nmlp = nmlp_of(model);
+  if (model->precision == 0)
+    carve_sdf<float>(nullptr, n_points, nmlp, bytes);
+  else
+    carve_sdf<double>(nullptr, n_points, nmlp, bytes);
+  return GSB_OK;
+}
+
+int gsb_sdf_points(const gsb_model_t* model, const void* points, int64_t n, void* phi_out,
+                   void* workspace, size_t workspace_bytes, void* stream) {
+  if (!model || !points || !phi_out || !workspace) return GSB_E_ARG;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const bool f = model->precision == 0;
+  switch (shape_tag(model)) {
+    case 0:
+      return f ? gsb_step_f446_sdf_points(model, points, n, phi_out, workspace, workspace_bytes, s)
+               : gsb_step_d446_sdf_points(model, points, n, phi_out, workspace, workspace_bytes, s);
+    case 1:
+      return f ? gsb_step_f222_sdf_points(model, points, n, phi_out, workspace, workspace_bytes, s)
+               : gsb_step_d222_sdf_points(model, points, n, phi_out, workspace, workspace_bytes, s);
+    default:
+      return GSB_E_ARG;
+  }
+}
+
+int gsb_sdf_fit_step(const gsb_model_t* model, const void* points, const void* targets,
+                     int64_t n_batch, int64_t n_anchor, void* workspace, size_t workspace_bytes,
+                     double* loss_out, void* stream) {
+  if (!model || !points || !targets || !workspace) return GSB_E_ARG;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const bool f = model->precision == 0;
+  switch (shape_tag(model)) {
+    case 0:
+      return f ? gsb_step_f446_sdf_fit(model, points, targets, n_batch, n_anchor, workspace,
+                                       workspace_bytes, loss_out, s)
+               : gsb_step_d446_sdf_fit(model, points, targets, n_batch, n_anchor, workspace,
+                                       workspace_bytes, loss_out, s);
+    case 1:
+      return f ? gsb_step_f222_sdf_fit(model, points, targets, n_batch, n_anchor, workspace,
+                                       workspace_bytes, loss_out, s)
+               : gsb_step_d222_sdf_fit(model, points, targets, n_batch, n_anchor, workspace,
+                                       workspace_bytes, loss_out, s);
+    default:
+      return GSB_E_ARG;
+  }
 }
 
 int gsb_step_workspace_size(const gsb_model_t* model, int32_t n_rays, int32_t n_coarse,

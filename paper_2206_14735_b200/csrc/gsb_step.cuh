@@ -178,5 +178,130 @@ int run_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step
   return GSB_OK;
 }
 
+// ---------------------------------------------------------------------------
+// geometry-only evaluation / fit on point lists: the sphere pre-fit
+// (decoders.geometric_init, gs/decoders.py:102-177) and dense SDF queries.
+// They reuse the taped kernels with zero rays: every sample is a "point"
+// sample (the smoothness-point path), so phi is exactly the step's phi.
+
+template <typename T>
+Ws<T> carve_sdf(void* ws, int64_t n, int nmlp, size_t* bytes) {
+  Carver<T> c;
+  c.base = reinterpret_cast<unsigned char*>(ws);
+  Ws<T> w{};
+  w.ld = 1;
+  w.status = c.template take<int32_t>(GSB_N_STATUS);
+  w.parts = c.template take<double>(16);       // [0]: fit loss
+  w.o = c.template take<T>(4);                 // dummy ray for the (unused) colour branch
+  w.r = c.template take<T>(4);
+  w.sphi = c.template take<T>(n);
+  w.sgphi = c.template take<T>(n * 3);
+  w.pbar = c.template take<T>(n);
+  w.ubar = c.template take<T>(n * 3);
+  const int64_t nb = std::max<int64_t>(kNbMax, (n + 127) / 128);
+  w.nb_max = (int)nb;
+  w.mlp_part = c.template take<T>(nb * nmlp);
+  w.wfrag = c.template take<uint4>(4096 + 68);
+  if (bytes) *bytes = c.off;
+  return w;
+}
+
+// p_bar = d/dphi [mean_batch (phi - t)^2 + mean_anchor (phi - t)^2] with the
+// reference's vjp arithmetic: g = 1/n, then g*err + g*err (gs/diffcore.py:354-572)
+template <typename T>
+__global__ void k_fit_seed(Ws<T> w, const T* __restrict__ target, int64_t nb, int64_t na) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= nb + na) return;
+  const T inv = T(1) / (T)(i < nb ? nb : na);
+  const T err = w.sphi[i] - target[i];
+  const T g = inv * err;
+  w.pbar[i] = g + g;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) w.ubar[i * 3 + a] = T(0);
+  atomicAdd(&w.parts[0], (double)(err * err) * (double)inv);
+}
+
+template <typename T, class S>
+int sdf_forward(const gsb_model_t* model, Ws<T>& w, const T* pts, int64_t n, cudaStream_t stream) {
+  const size_t esz = sizeof(T);
+  Geo G = geo_of(model, esz);
+  const T* mlp = reinterpret_cast<const T*>(model->params) + model->mlp_offset;
+  const int blocks = (int)((n + 127) / 128);
+  if constexpr (sizeof(T) == 4) {
+    constexpr int TW = 4;
+    tc::k_wfrag<S><<<tc::Fr<S>::NALL + 1, 32, 0, stream>>>(mlp, w.wfrag);
+    GSB_LAUNCHED_T("k_wfrag");
+    GSB_CHECK(cudaFuncSetAttribute(tc::k_fwd_tc<S, TW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)tc::FwdTc<S, TW>::smem()));
+    tc::k_fwd_tc<S, TW><<<blocks, TW * 32, tc::FwdTc<S, TW>::smem(), stream>>>(w, G, 0, 1, mlp, nullptr,
+                                                                             pts, (int)n);
+  } else {
+    const size_t smem_fwd = ((size_t)(S::NMLP + 3) / 4 * 4 + 128 * FwdRow<T, S>::ROW) * esz;
+    GSB_CHECK(cudaFuncSetAttribute(k_fwd<T, S, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)smem_fwd));
+    k_fwd<T, S, false><<<blocks, 128, smem_fwd, stream>>>(w, G, 0, 1, nullptr, pts, (int)n, mlp);
+  }
+  GSB_LAUNCHED_T("k_fwd");
+  return GSB_OK;
+}
+
+template <typename T, class S>
+int run_sdf_points(const gsb_model_t* model, const void* points, int64_t n, void* phi_out, void* ws,
+                   size_t ws_bytes, cudaStream_t stream) {
+  if (S::NMLP != nmlp_of(model) || n <= 0 || n > INT32_MAX) return GSB_E_ARG;
+  timing_point(nullptr, stream);
+  size_t need = 0;
+  Ws<T> w = carve_sdf<T>(ws, n, S::NMLP, &need);
+  if (need > ws_bytes) return GSB_E_ARG;
+  w.sphi = reinterpret_cast<T*>(phi_out);
+  GSB_CHECK(cudaMemsetAsync(w.status, 0, GSB_N_STATUS * sizeof(int32_t), stream));
+  return sdf_forward<T, S>(model, w, reinterpret_cast<const T*>(points), n, stream);
+}
+
+template <typename T, class S>
+int run_sdf_fit(const gsb_model_t* model, const void* points, const void* targets, int64_t nb,
+                int64_t na, void* ws, size_t ws_bytes, double* loss_out, cudaStream_t stream) {
+  const int64_t n = nb + na;
+  if (S::NMLP != nmlp_of(model) || nb <= 0 || na < 0 || n > INT32_MAX) return GSB_E_ARG;
+  timing_point(nullptr, stream);
+  size_t need = 0;
+  Ws<T> w = carve_sdf<T>(ws, n, S::NMLP, &need);
+  if (need > ws_bytes) return GSB_E_ARG;
+  GSB_CHECK(cudaMemsetAsync(w.status, 0, GSB_N_STATUS * sizeof(int32_t), stream));
+  GSB_CHECK(cudaMemsetAsync(w.parts, 0, 16 * sizeof(double), stream));
+  const T* pts = reinterpret_cast<const T*>(points);
+  int rc = sdf_forward<T, S>(model, w, pts, n, stream);
+  if (rc != GSB_OK) return rc;
+  k_fit_seed<T><<<(int)((n + 255) / 256), 256, 0, stream>>>(w, reinterpret_cast<const T*>(targets), nb, na);
+  GSB_LAUNCHED_T("k_fit_seed");
+  Geo G = geo_of(model, sizeof(T));
+  T* grads = reinterpret_cast<T*>(model->grads);
+  const T* mlp = reinterpret_cast<const T*>(model->params) + model->mlp_offset;
+  int nb_geo;
+  if constexpr (sizeof(T) == 4) {
+    constexpr int WGEO = 4;
+    nb_geo = (int)((n + WGEO * 32 - 1) / (WGEO * 32));
+    const size_t smem_g = tc::GeoTc<S, WGEO>::smem();
+    GSB_CHECK(cudaFuncSetAttribute(tc::k_bwd_geom_tc<S, WGEO>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_g));
+    tc::k_bwd_geom_tc<S, WGEO><<<nb_geo, WGEO * 32, smem_g, stream>>>(w, G, 0, 1, mlp, nullptr, pts,
+                                                                      (int)n, 2);
+  } else {
+    constexpr int WG = 2;
+    nb_geo = (int)std::min<int64_t>((n + WG * 32 - 1) / (WG * 32), (int64_t)num_sms() * 2);
+    nb_geo = std::max(1, std::min(nb_geo, kNbMax));
+    const size_t smem_g = ((size_t)(S::NG + 3) / 4 * 4 + (size_t)WG * 32 * GeoRow<T, S>::ROW) * sizeof(T);
+    GSB_CHECK(cudaFuncSetAttribute(k_bwd_geom<T, S, WG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)smem_g));
+    k_bwd_geom<T, S, WG><<<nb_geo, WG * 32, smem_g, stream>>>(w, G, 0, 1, nullptr, pts, (int)n, 2, mlp);
+  }
+  GSB_LAUNCHED_T("k_bwd_geom");
+  k_finalize_mlp<T, S><<<(S::NMLP + 31) / 32, 256, 0, stream>>>(w, grads, model->mlp_offset, nb_geo, 0);
+  GSB_LAUNCHED_T("k_finalize_mlp");
+  if (loss_out)
+    GSB_CHECK(cudaMemcpyAsync(loss_out, w.parts, sizeof(double), cudaMemcpyDeviceToDevice, stream));
+  return GSB_OK;
+}
+
 }  // namespace host
 }  // namespace gsb

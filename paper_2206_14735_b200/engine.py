@@ -87,6 +87,39 @@ def host_draws(model, dataset, cfg, iteration, ray_ids=None, smooth_override=Non
     return HostDraws(iteration, np.asarray(ray_ids, dtype=np.int64), smooth, rs, ri)
 
 
+def model_struct(m):
+    """gsb_model_t of a ModelState (arena pointers, level descriptors)."""
+    a = m.arena
+    ms = _lib.Model()
+    ms.precision = 0 if a.dtype == np.float32 else 1
+    if len(m.grid.levels) > _lib.MAX_LEVELS:
+        raise ValueError("too many grid levels")
+    ms.n_levels = len(m.grid.levels)
+
+    def lev(gl):
+        L = _lib.Level()
+        L.nx, L.ny, L.nz = gl.geom.dims
+        L.channels = gl.width
+        L.ox, L.oy, L.oz = (float(x) for x in gl.geom.origin)
+        L.voxel = gl.geom.voxel_size
+        L.offset = gl.features.offset
+        return L
+
+    for i, gl in enumerate(m.grid.levels):
+        ms.levels[i] = lev(gl)
+    ms.color = lev(m.grid.color)
+    ms.mlp_offset = a["geom_w0"].offset
+    ms.log_s_offset = m.log_s.offset
+    ms.n_params = a.n
+    lo, hi = m.grid.clamp_box()
+    for i in range(3):
+        ms.lo_c[i] = float(lo[i])
+        ms.hi_c[i] = float(hi[i])
+    ms.params = a.params.data_ptr()
+    ms.grads = a.grads.data_ptr()
+    return ms
+
+
 class StepEngine:
     """Launches training steps for one model on one device dataset."""
 
@@ -104,36 +137,7 @@ class StepEngine:
 
     # ---- ABI structs
     def _model_struct(self):
-        m = self.model
-        a = m.arena
-        ms = _lib.Model()
-        ms.precision = 0 if a.dtype == np.float32 else 1
-        if len(m.grid.levels) > _lib.MAX_LEVELS:
-            raise ValueError("too many grid levels")
-        ms.n_levels = len(m.grid.levels)
-
-        def lev(gl):
-            L = _lib.Level()
-            L.nx, L.ny, L.nz = gl.geom.dims
-            L.channels = gl.width
-            L.ox, L.oy, L.oz = (float(x) for x in gl.geom.origin)
-            L.voxel = gl.geom.voxel_size
-            L.offset = gl.features.offset
-            return L
-
-        for i, gl in enumerate(m.grid.levels):
-            ms.levels[i] = lev(gl)
-        ms.color = lev(m.grid.color)
-        ms.mlp_offset = a["geom_w0"].offset
-        ms.log_s_offset = m.log_s.offset
-        ms.n_params = a.n
-        lo, hi = m.grid.clamp_box()
-        for i in range(3):
-            ms.lo_c[i] = float(lo[i])
-            ms.hi_c[i] = float(hi[i])
-        ms.params = a.params.data_ptr()
-        ms.grads = a.grads.data_ptr()
-        return ms
+        return model_struct(self.model)
 
     def _dataset_struct(self):
         ds = self.dataset
