@@ -54,6 +54,8 @@ struct Ws {
   double* smooth_part;  // [S]
   T* mlp_part;          // [nb_max][NMLP]
   uint4* wfrag;         // float32: per-lane tf32 hi/lo B fragments of the MLP (gsb_tc.cuh)
+  double* fin_red;      // [FIN_SPLIT][NMLP] chunk totals of k_finalize_mlp2
+  unsigned* fin_cnt;    // [ceil(NMLP/32)] tickets (self-resetting; zeroed per step)
   int nb_max;
   long long* counts;
   double* parts;
@@ -1444,6 +1446,56 @@ __global__ void __launch_bounds__(256) k_finalize_mlp(Ws<T> w, T* grads, int64_t
 #pragma unroll
     for (int k = 0; k < 8; ++k) tot += red[k][lane];
     grads[mlp_off + t] += (T)tot;
+  }
+}
+
+// Deterministic reduction of the per-CTA MLP partials, split over (column
+// group of 32 parameters) x (FIN_SPLIT chunks of the partial range): 4 loads
+// in flight per warp, then the last chunk-block of a column group (atomic
+// ticket) sums the chunk totals in chunk order.
+constexpr int FIN_SPLIT = 16;
+
+template <typename T, class S>
+__global__ void __launch_bounds__(256) k_finalize_mlp2(Ws<T> w, T* grads, int64_t mlp_off,
+                                                       int nb_geo, int nb_col) {
+  __shared__ double red[8][33];
+  __shared__ bool last;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int t = blockIdx.x * 32 + lane, y = blockIdx.y;
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  if (t < S::NMLP) {
+    const int nb = t < S::NG ? nb_geo : nb_col;
+    const int b0 = (int)((int64_t)nb * y / FIN_SPLIT), b1 = (int)((int64_t)nb * (y + 1) / FIN_SPLIT);
+    const T* col = w.mlp_part + t;
+    int b = b0 + wid;
+    for (; b + 24 < b1; b += 32) {
+      a0 += (double)col[(size_t)b * S::NMLP];
+      a1 += (double)col[(size_t)(b + 8) * S::NMLP];
+      a2 += (double)col[(size_t)(b + 16) * S::NMLP];
+      a3 += (double)col[(size_t)(b + 24) * S::NMLP];
+    }
+    for (; b < b1; b += 8) a0 += (double)col[(size_t)b * S::NMLP];
+  }
+  red[wid][lane] = (a0 + a1) + (a2 + a3);
+  __syncthreads();
+  if (wid == 0) {
+    double tot = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) tot += red[k][lane];
+    if (t < S::NMLP) w.fin_red[(size_t)y * S::NMLP + t] = tot;
+    __threadfence();
+    __syncwarp();
+    if (lane == 0) last = atomicAdd(&w.fin_cnt[blockIdx.x], 1u) == FIN_SPLIT - 1;
+  }
+  __syncthreads();
+  if (last && wid == 0) {
+    __threadfence();
+    if (t < S::NMLP) {
+      double tot = 0.0;
+      for (int k = 0; k < FIN_SPLIT; ++k) tot += __ldcg(&w.fin_red[(size_t)k * S::NMLP + t]);
+      grads[mlp_off + t] += (T)tot;
+    }
+    if (lane == 0) w.fin_cnt[blockIdx.x] = 0u;  // ready for the next launch
   }
 }
 

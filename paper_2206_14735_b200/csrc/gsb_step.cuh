@@ -169,7 +169,9 @@ int run_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step
       k_bwd_color<T, S, WG><<<nb_col, per_cta, smem_c, stream>>>(w, G, M, N, dep_final, mlp);
       GSB_LAUNCHED_T("k_bwd_color");
     }
-    k_finalize_mlp<T, S><<<(S::NMLP + 31) / 32, 256, 0, stream>>>(w, grads, model->mlp_offset,
+    static_assert(FIN_SPLIT == 16, "workspace carve");
+    GSB_CHECK(cudaMemsetAsync(w.fin_cnt, 0, (S::NMLP + 31) / 32 * sizeof(unsigned), stream));
+    k_finalize_mlp2<T, S><<<dim3((S::NMLP + 31) / 32, FIN_SPLIT), 256, 0, stream>>>(w, grads, model->mlp_offset,
                                                                     nb_geo, nb_col);
     GSB_LAUNCHED_T("k_finalize_mlp");
     k_finalize_loss<T><<<1, 1024, 0, stream>>>(w, M, z.S, grads, params, model->log_s_offset, L);
@@ -202,6 +204,8 @@ Ws<T> carve_sdf(void* ws, int64_t n, int nmlp, size_t* bytes) {
   w.nb_max = (int)nb;
   w.mlp_part = c.template take<T>(nb * nmlp);
   w.wfrag = c.template take<uint4>(4096 + 68);
+  w.fin_red = c.template take<double>((int64_t)16 * nmlp);
+  w.fin_cnt = c.template take<unsigned>((nmlp + 31) / 32);
   if (bytes) *bytes = c.off;
   return w;
 }
@@ -296,7 +300,9 @@ int run_sdf_fit(const gsb_model_t* model, const void* points, const void* target
     k_bwd_geom<T, S, WG><<<nb_geo, WG * 32, smem_g, stream>>>(w, G, 0, 1, nullptr, pts, (int)n, 2, mlp);
   }
   GSB_LAUNCHED_T("k_bwd_geom");
-  k_finalize_mlp<T, S><<<(S::NMLP + 31) / 32, 256, 0, stream>>>(w, grads, model->mlp_offset, nb_geo, 0);
+  GSB_CHECK(cudaMemsetAsync(w.fin_cnt, 0, (S::NMLP + 31) / 32 * sizeof(unsigned), stream));
+  k_finalize_mlp2<T, S><<<dim3((S::NMLP + 31) / 32, FIN_SPLIT), 256, 0, stream>>>(w, grads, model->mlp_offset,
+                                                                                nb_geo, 0);
   GSB_LAUNCHED_T("k_finalize_mlp");
   if (loss_out)
     GSB_CHECK(cudaMemcpyAsync(loss_out, w.parts, sizeof(double), cudaMemcpyDeviceToDevice, stream));
