@@ -269,6 +269,8 @@ def main():
     ap.add_argument("--frames", type=int, default=FRAMES)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--rays", type=int, default=M_PER_GPU)
+    ap.add_argument("--prefetch", action="store_true",
+                    help="host draws on a background thread in the e2e leg")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -373,26 +375,19 @@ def main():
     eng.lib.gsb_timing_enable(0)
     kt = _lib.kernel_times()
 
-    # ---- e2e through the public API (host draws + H2D + D2H of parts)
-    T = optimizer.Trainer(model, ds, cfg, opt)
+    # ---- e2e through the public API (host draws + H2D + D2H of parts);
+    # the Trainer prefetches host draws on a background thread
+    T = optimizer.Trainer(model, ds, cfg, opt, dist=pg, rank=rank, world=ws_)
+    base_it = W + K
+    if args.prefetch:
+        T.start_prefetch(base_it)
     torch.cuda.synchronize()
     if pg:
         pg.barrier()
     t0 = time.perf_counter()
     pending = None
-    base_it = W + K
-    h2d = 0
     for k in range(K):
-        it = base_it + k
-        d, kw = draws_for(it)
-        h2d = d.ray_ids.nbytes + (0 if d.smooth is None else d.smooth.nbytes)
-        if pg is None:
-            T.launch(it, draws=d, slot=k % 2)
-        else:
-            ids, sm = eng.upload(d)
-            w = one_step(d, kw, ids, sm)
-            T.host_parts[k % 2].copy_(w["parts"], non_blocking=True)
-            T.events[k % 2].record()
+        T.launch(base_it + k, slot=k % 2)
         if pending is not None:
             T.parts(pending)
         pending = k % 2
@@ -400,6 +395,7 @@ def main():
         T.parts(pending)
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - t0
+    T.stop_prefetch()
     if pg:
         tt = torch.tensor([e2e_s], device=dev)
         pg.all_reduce(tt, op=pg.ReduceOp.MAX)
@@ -446,7 +442,7 @@ def main():
                        "frames": args.frames, "l2": "working set (4 arenas x 256 MB) > L2; "
                                                    "no explicit flush"},
             "samples_per_s": value * N,
-            "e2e": {"value": e2e, "unit": "rays/s", "h2d_bytes_per_step": int(h2d),
+            "e2e": {"value": e2e, "unit": "rays/s", "h2d_bytes_per_step": int(T.last_h2d),
                     "d2h_bytes_per_step": 8 * 8},
             "gpu_launches": launches,
             "roofline": roofline, "cpu_baseline": cpu, "clocks": clk}

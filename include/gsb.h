@@ -201,6 +201,18 @@ int gsb_adam_step(int32_t precision, void* params, void* grads, void* m, void* v
                   int32_t n_seg, double beta1, double beta2, double eps, double c1, double c2,
                   const double* guard, double guard_threshold, int32_t* status, void* stream);
 
+/* Smoothness points (renderer.draw_smooth_points, gs/renderer.py:243-276) on
+ * the device from the host's RNG draws, in the reference's call order:
+ * pick = integers(0, n_valid, count) (index into the valid-depth pixels in
+ * np.nonzero order), jitter = uniform(-truncation, truncation, count),
+ * normals = normal((count, 8, 3)).  poses: (F, 12) f64 rows of
+ * ModelState.pose_matrices() (R row-major, then t); row_cum: (F*H) inclusive
+ * prefix counts of valid pixels per image row.  out: (2*count, 3) model dtype,
+ * x then x + eps, clamped to model->lo_c/hi_c.  Bit-exact with the reference. */
+int gsb_smooth_points(const gsb_model_t* model, const gsb_dataset_t* data, const double* poses,
+                      const int64_t* row_cum, const int64_t* pick, const double* jitter,
+                      const double* normals, int32_t count, double delta, void* out, void* stream);
+
 /* ---------------- geometry on point lists ---------------- */
 
 /* Bytes of device workspace gsb_sdf_points / gsb_sdf_fit_step need for up to

@@ -344,6 +344,28 @@ __global__ void k_ray_batch_twin(gsb_dataset_t D, const int64_t* ids, int n, dou
   o[11] = P.scale;
 }
 
+int gsb_smooth_points(const gsb_model_t* model, const gsb_dataset_t* data, const double* poses,
+                      const int64_t* row_cum, const int64_t* pick, const double* jitter,
+                      const double* normals, int32_t count, double delta, void* out, void* stream) {
+  if (!model || !data || !poses || !row_cum || !pick || !jitter || !normals || !out || count < 0)
+    return GSB_E_ARG;
+  if (count == 0) return GSB_OK;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int64_t n_rows = (int64_t)data->n_frames * data->height;
+  const int blocks = (count + 127) / 128;
+  if (model->precision == 0) {
+    Geo G = geo_of(model, 4);
+    k_smooth_points<float><<<blocks, 128, 0, s>>>(*data, poses, row_cum, n_rows, pick, jitter, normals,
+                                                  count, delta, G, (float*)out);
+  } else {
+    Geo G = geo_of(model, 8);
+    k_smooth_points<double><<<blocks, 128, 0, s>>>(*data, poses, row_cum, n_rows, pick, jitter,
+                                                   normals, count, delta, G, (double*)out);
+  }
+  GSB_LAUNCHED();
+  return GSB_OK;
+}
+
 int gsb_ray_batch(const gsb_dataset_t* data, const int64_t* ray_ids, int32_t n, double* out,
                   void* stream) {
   if (!data || n < 0) return GSB_E_ARG;

@@ -336,6 +336,83 @@ static __device__ void separation_fallback(double* row, int32_t* src, int k) {
 }
 
 // ---------------------------------------------------------------------------
+// smoothness points (renderer.draw_smooth_points, gs/renderer.py:243-276)
+// from the host's RNG draws: pick = integers(0, n_valid, S), jitter =
+// uniform(-t, t, S), nrm = normal((S, 8, 3)).  Same f64 operations in the
+// same order (the build disables FMA contraction); poses are the f64
+// ModelState.pose_matrices() rows (R0 exact, t rounded through the dtype).
+
+template <typename T>
+__global__ void k_smooth_points(gsb_dataset_t D, const double* __restrict__ poses,
+                                const int64_t* __restrict__ row_cum, int64_t n_rows,
+                                const int64_t* __restrict__ pick, const double* __restrict__ jitter,
+                                const double* __restrict__ nrm, int S, double delta, Geo G,
+                                T* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= S) return;
+  // k-th valid pixel in np.nonzero order: row by the inclusive prefix counts,
+  // then the r-th valid column of that row
+  const int64_t k = pick[i];
+  int64_t lo = 0, hi = n_rows;  // first row with cum > k
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (row_cum[mid] > k) hi = mid; else lo = mid + 1;
+  }
+  const int64_t row = lo;
+  int64_t r = k - (row > 0 ? row_cum[row - 1] : 0);
+  const int64_t f = row / D.height;
+  const int v = (int)(row % D.height);
+  const uint16_t* drow = D.depth_mm + row * D.width;
+  int u = 0;
+  for (; u < D.width; ++u)
+    if (drow[u] > 0 && r-- == 0) break;
+  // pixel ray and z -> ray-distance scale (gs/camera.py:142-171)
+  const double dx = ((double)u - D.cx) / D.fx;
+  const double dy = ((double)v - D.cy) / D.fy;
+  const double dz = 1.0;
+  const double n0 = sqrt((dx * dx + dy * dy) + dz * dz);
+  const double dc[3] = {dx / n0, dy / n0, dz / n0};
+  const double depth_ray = ((double)drow[u] / 1000.0) * n0 + jitter[i];
+  const double* P = poses + f * 12;
+  double x[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    // np.einsum("nij,nj->ni") sums this 3-term contraction as (t0 + t2) + t1
+    // (numpy 2.3 two-accumulator loop; measured, 100% of 180k cases)
+    const double dir = (P[3 * a] * dc[0] + P[3 * a + 2] * dc[2]) + P[3 * a + 1] * dc[1];
+    double xa = P[9 + a] + depth_ray * dir;
+    xa = xa >= G.lo[a] ? xa : G.lo[a];
+    x[a] = xa <= G.hi[a] ? xa : G.hi[a];
+  }
+  // first of 8 unit directions whose delta-step stays in the box, else the first
+  double xe[3];
+  bool found = false;
+  for (int j = 0; j < 8; ++j) {
+    const double* e = nrm + ((int64_t)i * 8 + j) * 3;
+    const double en = sqrt((e[0] * e[0] + e[1] * e[1]) + e[2] * e[2]);
+    double c[3];
+    bool ok = true;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      c[a] = x[a] + delta * (e[a] / en);
+      ok = ok && c[a] >= G.lo[a] && c[a] <= G.hi[a];
+    }
+    if (j == 0 || (ok && !found)) {
+#pragma unroll
+      for (int a = 0; a < 3; ++a) xe[a] = c[a];
+    }
+    if (ok && !found) found = true;
+  }
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    double c = xe[a] >= G.lo[a] ? xe[a] : G.lo[a];
+    c = c <= G.hi[a] ? c : G.hi[a];
+    out[(int64_t)i * 3 + a] = (T)x[a];
+    out[((int64_t)S + i) * 3 + a] = (T)c;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // one importance round, one warp per ray (render_weights_data +
 // importance_refine_with_sources + enforce_separation, gs/renderer.py:162-173,
 // gs/sampler.py:128-197).  The two float64 recurrences (cumprod of the

@@ -28,9 +28,28 @@ class HostDraws:
 
     iteration: int
     ray_ids: np.ndarray          # (M,) int64 flat ids into F*H*W
-    smooth: np.ndarray | None    # (2S, 3) model dtype: x then x+eps
+    smooth: np.ndarray | None    # (2S, 3) model dtype: x then x+eps (explicit points)
     rng_stratify: object
     rng_importance: list
+    # raw smoothness draws (pick, jitter, normals) turned into points on the
+    # device by gsb_smooth_points; exclusive with `smooth`
+    smooth_raw: tuple | None = None
+    smooth_delta: float = 0.004
+
+    @property
+    def n_smooth(self):
+        if self.smooth is not None:
+            return self.smooth.shape[0] // 2
+        return 0 if self.smooth_raw is None else len(self.smooth_raw[0])
+
+    @property
+    def h2d_bytes(self):
+        b = self.ray_ids.nbytes
+        if self.smooth is not None:
+            b += self.smooth.nbytes
+        if self.smooth_raw is not None:
+            b += sum(a.nbytes for a in self.smooth_raw)
+        return b
 
 
 def draw_smooth_points(model, dataset, count, truncation, delta, rng):
@@ -63,28 +82,48 @@ def draw_smooth_points(model, dataset, count, truncation, delta, rng):
     return x, xe
 
 
-def host_draws(model, dataset, cfg, iteration, ray_ids=None, smooth_override=None):
+def smooth_raw_draws(dataset, count, truncation, rng):
+    """The RNG calls of draw_smooth_points (gs/renderer.py:253-268), in order:
+    integers (valid pixel), uniform (range jitter), normal (8 directions)."""
+    n_valid = dataset.n_valid
+    if n_valid == 0:
+        return None
+    pick = rng.integers(0, n_valid, size=count)
+    jitter = rng.uniform(-truncation, truncation, size=count)
+    normals = rng.normal(size=(count, 8, 3))
+    return (np.ascontiguousarray(pick, dtype=np.int64), np.ascontiguousarray(jitter),
+            np.ascontiguousarray(normals))
+
+
+def host_draws(model, dataset, cfg, iteration, ray_ids=None, smooth_override=None,
+               device_smooth=True):
     """Host-side randomness of iteration `iteration` (gs/optimizer.py:363-366,
-    gs/renderer.py:320-336, 416-423)."""
+    gs/renderer.py:320-336, 416-423).  With ``device_smooth`` the smoothness
+    points are left as raw draws for gsb_smooth_points."""
     lw = cfg.weights
     if ray_ids is None:
         intr = dataset.intrinsics
         n = len(dataset) * intr.height * intr.width
         ray_ids = seeds.substream(cfg.seed, seeds.RAYS, iteration).integers(
             0, n, size=cfg.batch_rays)
-    if smooth_override is not None:
-        pts = smooth_override
-    else:
-        pts = draw_smooth_points(model, dataset, lw.smooth_count, lw.truncation,
-                                 lw.smooth_delta, seeds.substream(cfg.seed, seeds.SMOOTH,
-                                                                  iteration))
-    smooth = None
-    if pts is not None and lw.smooth != 0.0:
-        smooth = np.concatenate([pts[0], pts[1]], axis=0).astype(model.dtype)
+    smooth = raw = None
+    if lw.smooth != 0.0:
+        rng = seeds.substream(cfg.seed, seeds.SMOOTH, iteration)
+        if smooth_override is not None:
+            pts = smooth_override
+        elif device_smooth:
+            pts = None
+            raw = smooth_raw_draws(dataset, lw.smooth_count, lw.truncation, rng)
+        else:
+            pts = draw_smooth_points(model, dataset, lw.smooth_count, lw.truncation,
+                                     lw.smooth_delta, rng)
+        if pts is not None:
+            smooth = np.concatenate([pts[0], pts[1]], axis=0).astype(model.dtype)
     rs = _lib.Pcg64.from_generator(seeds.substream(cfg.seed, seeds.STRATIFY, iteration))
     ri = [_lib.Pcg64.from_generator(seeds.substream(cfg.seed, seeds.IMPORTANCE, iteration, r))
           for r in range(cfg.importance_rounds)]
-    return HostDraws(iteration, np.asarray(ray_ids, dtype=np.int64), smooth, rs, ri)
+    return HostDraws(iteration, np.asarray(ray_ids, dtype=np.int64), smooth, rs, ri, raw,
+                     float(lw.smooth_delta))
 
 
 def model_struct(m):
@@ -229,6 +268,34 @@ class StepEngine:
         st.workspace_bytes = ws["buf"].numel()
         return st
 
+    def _smooth_tables(self):
+        """(F, 12) f64 pose_matrices() rows and the (F*H) valid-pixel row
+        prefix counts, device-resident (poses are frozen in this path)."""
+        if not hasattr(self, "_smooth_tab"):
+            torch = self.torch
+            mats = self.model.pose_matrices()
+            P = np.concatenate([mats[:, :3, :3].reshape(-1, 9), mats[:, :3, 3]], axis=1)
+            self._smooth_tab = (
+                torch.from_numpy(np.ascontiguousarray(P, dtype=np.float64)).to(self.device),
+                torch.from_numpy(np.ascontiguousarray(self.dataset._rows(), dtype=np.int64)).to(self.device))
+        return self._smooth_tab
+
+    def smooth_points(self, raw, delta, stream=None):
+        """gsb_smooth_points: raw host draws -> (2S, 3) device points."""
+        torch = self.torch
+        pick, jitter, normals = raw
+        S = len(pick)
+        packed = np.concatenate([pick.view(np.float64), jitter, normals.reshape(-1)])
+        dev = torch.from_numpy(packed).pin_memory().to(self.device, non_blocking=True)
+        poses, row_cum = self._smooth_tables()
+        out = torch.empty((2 * S, 3), dtype=self.model.arena.params.dtype, device=self.device)
+        base = dev.data_ptr()
+        _lib.check(self.lib.gsb_smooth_points(
+            C.byref(self.mstruct), C.byref(self.dstruct), poses.data_ptr(), row_cum.data_ptr(),
+            base, base + 8 * S, base + 16 * S, S, float(delta), out.data_ptr(),
+            _lib.stream_handle(stream)), "gsb_smooth_points")
+        return out
+
     def upload(self, draws, stream=None):
         torch = self.torch
         ids = torch.from_numpy(draws.ray_ids).pin_memory().to(self.device, non_blocking=True)
@@ -236,6 +303,8 @@ class StepEngine:
         if draws.smooth is not None:
             sm = torch.from_numpy(np.ascontiguousarray(draws.smooth)).pin_memory().to(
                 self.device, non_blocking=True)
+        elif draws.smooth_raw is not None:
+            sm = self.smooth_points(draws.smooth_raw, draws.smooth_delta, stream)
         return ids, sm
 
     def launch(self, cfg, draws, ray_ids_dev, smooth_dev, stream=None, fresh=True, **kw):

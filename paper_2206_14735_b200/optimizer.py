@@ -304,6 +304,51 @@ def load_model(path, device=None):
 CSV_HEADER = "iter,total,rgb,depth,sdf,fs,eik,smooth,s\n"
 
 
+class DrawPrefetcher:
+    """Host draws (numpy RNG, gs/optimizer.py:363-366 + gs/renderer.py:320-336,
+    416-423) of the next iterations on a background thread.  The main thread
+    spends each step waiting on CUDA events, which releases the GIL, so the
+    draws of iteration k+1 overlap the device work of iteration k."""
+
+    def __init__(self, fn, start, depth=2):
+        import queue
+        import threading
+        self._queue_mod = queue
+        self.fn = fn
+        self.q = queue.Queue(maxsize=depth)
+        self.stop_ev = threading.Event()
+        self.t = threading.Thread(target=self._run, args=(int(start),), daemon=True)
+        self.t.start()
+
+    def _run(self, it):
+        while not self.stop_ev.is_set():
+            try:
+                item = self.fn(it)
+            except BaseException as e:  # surfaced by get()
+                item = e
+            while not self.stop_ev.is_set():
+                try:
+                    self.q.put((it, item), timeout=0.1)
+                    break
+                except self._queue_mod.Full:
+                    continue
+            if isinstance(item, BaseException):
+                return
+            it += 1
+
+    def get(self, it):
+        got, item = self.q.get()
+        if isinstance(item, BaseException):
+            raise item
+        if got != it:
+            raise RuntimeError(f"draw prefetch out of order: wanted {it}, got {got}")
+        return item
+
+    def close(self):
+        self.stop_ev.set()
+        self.t.join(timeout=5)
+
+
 class Trainer:
     """The device-resident inner loop: draw -> objective+backward -> Adam.
 
@@ -311,24 +356,56 @@ class Trainer:
     one iteration later, so the host never waits on the GPU inside the
     loop; divergence is enforced on the device (the Adam launch is skipped
     when the total is non-finite or above the threshold, and stays skipped)
-    so the model state matches the reference's when the error surfaces."""
+    so the model state matches the reference's when the error surfaces.
 
-    def __init__(self, model, dataset, cfg, opt):
+    With ``dist`` (torch.distributed, one process per GPU) each rank takes
+    its row shard of the global batch and the step runs as
+    parallel.DataParallelStep."""
+
+    def __init__(self, model, dataset, cfg, opt, dist=None, rank=0, world=1):
         import torch
+        from .parallel import DataParallelStep
         self.torch = torch
         self.model, self.cfg, self.opt = model, cfg, opt
         self.dataset = Dataset.wrap(dataset)
         self.engine = engine_for(model, self.dataset)
         self.host_parts = torch.zeros((2, _lib.N_PARTS), dtype=torch.float64).pin_memory()
         self.events = [torch.cuda.Event(), torch.cuda.Event()]
+        self.rank, self.world = int(rank), int(world)
+        self.dp = DataParallelStep(self.engine, dist) if dist is not None and world > 1 else None
+        self.prefetcher = None
+        self.last_h2d = 0
 
     def draws(self, it):
-        return host_draws(self.model, self.dataset, self.cfg, it)
+        """(this rank's HostDraws, step kwargs) of iteration ``it``."""
+        from .parallel import shard_draws
+        d = host_draws(self.model, self.dataset, self.cfg, it)
+        if self.world == 1:
+            return d, {}
+        return shard_draws(d, self.rank, self.world)
+
+    def start_prefetch(self, start_it):
+        self.stop_prefetch()
+        self.prefetcher = DrawPrefetcher(self.draws, start_it)
+
+    def stop_prefetch(self):
+        if self.prefetcher is not None:
+            self.prefetcher.close()
+            self.prefetcher = None
 
     def launch(self, it, draws=None, slot=0):
-        d = draws if draws is not None else self.draws(it)
+        if draws is not None:
+            d, kw = draws if isinstance(draws, tuple) else (draws, {})
+        elif self.prefetcher is not None:
+            d, kw = self.prefetcher.get(it)
+        else:
+            d, kw = self.draws(it)
+        self.last_h2d = d.h2d_bytes
         ids, sm = self.engine.upload(d)
-        ws = self.engine.launch(self.cfg, d, ids, sm)
+        if self.dp is None:
+            ws = self.engine.launch(self.cfg, d, ids, sm, **kw)
+        else:
+            ws = self.dp(self.cfg, d, ids, sm, **kw)
         self.host_parts[slot].copy_(ws["parts"], non_blocking=True)
         self.events[slot].record()
         self.opt.t = [t + 1 for t in self.opt.t]
@@ -376,6 +453,7 @@ def train(dataset, cfg, out_dir, initial_poses=None, resume=None):
         if csv_mode == "w":
             csv.write(CSV_HEADER)
         pending = None  # (iteration, slot)
+        T.start_prefetch(start_it)
         for it in range(start_it, cfg.iterations):
             slot = it % 2
             T.launch(it, slot=slot)
@@ -390,6 +468,7 @@ def train(dataset, cfg, out_dir, initial_poses=None, resume=None):
                            opt)
         if pending is not None:
             finish(pending[0], T.parts(pending[1]), csv)
+        T.stop_prefetch()
         csv.flush()
     save_model(final_path, model, cfg, cfg.iterations, opt)
     return model, final_path

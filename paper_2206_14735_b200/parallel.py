@@ -37,9 +37,10 @@ def shard_draws(draws, rank, world):
     step keyword arguments (ray_base, m_global, smooth_global)."""
     m = len(draws.ray_ids)
     lo, hi = shard_rows(m, rank, world)
-    n_smooth = 0 if draws.smooth is None else draws.smooth.shape[0] // 2
+    n_smooth = draws.n_smooth
     d = dataclasses.replace(draws, ray_ids=draws.ray_ids[lo:hi].copy(),
-                            smooth=draws.smooth if rank == 0 else None)
+                            smooth=draws.smooth if rank == 0 else None,
+                            smooth_raw=draws.smooth_raw if rank == 0 else None)
     return d, dict(ray_base=lo, m_global=m, smooth_global=max(n_smooth, 1))
 
 

@@ -169,7 +169,7 @@ def train_objective(model, dataset, batch, iteration, cfg, smooth_override=None)
         "n_tr": int(counts[_lib.C_TR]),
         "n_fs": int(counts[_lib.C_FS]),
         "n_eik": int(counts[_lib.C_EIK]),
-        "n_smooth": 0 if draws.smooth is None else draws.smooth.shape[0] // 2,
+        "n_smooth": draws.n_smooth,
         "empty_tr": bool(counts[_lib.C_TR] == 0),
         "empty_fs": bool(counts[_lib.C_FS] == 0),
     }

@@ -170,3 +170,24 @@ def test_oracle_matches_reference_objective_double_small():
     R = O.train_objective(P, G.ds, batch, it, G.cfg)
     assert R["parts"]["total"] == G.meta["parts"]["total"]
     assert rel_maxnorm(R["grads"]["level3"], G.a["grad_level3"]) < 1e-12
+
+
+def test_draw_prefetcher_order_and_errors():
+    from paper_2206_14735_b200.optimizer import DrawPrefetcher
+
+    def fn(it):
+        if it == 8:
+            raise ValueError("boom")
+        return it * 2
+
+    p = DrawPrefetcher(fn, 5)
+    assert [p.get(i) for i in (5, 6, 7)] == [10, 12, 14]
+    import pytest
+    with pytest.raises(ValueError):
+        p.get(8)
+    p.close()
+    q = DrawPrefetcher(lambda it: it, 0)
+    q.get(0)
+    with pytest.raises(RuntimeError):
+        q.get(5)  # out of order is an error, not a silent mismatch
+    q.close()

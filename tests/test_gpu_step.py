@@ -360,3 +360,23 @@ def test_smooth_disabled_gives_zero():
     assert parts["smooth"] == 0.0 and extras["n_smooth"] == 0
     manual = (10 * parts["rgb"] + parts["depth"] + 10 * parts["sdf"] + parts["fs"] + parts["eik"])
     assert parts["total"] == pytest.approx(manual, rel=1e-12)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", ["tiny", "small"])
+@pytest.mark.parametrize("precision", ["double", "single"])
+def test_device_smooth_points_bit_exact(case, precision):
+    """gsb_smooth_points from the raw RNG draws == draw_smooth_points
+    (gs/renderer.py:243-276) on the host, bit for bit."""
+    from paper_2206_14735_b200 import engine, seeds
+    from paper_2206_14735_b200.renderer import engine_for
+    G = load(case, precision)
+    model, ds, cfg = gpu_model(G)
+    eng = engine_for(model, ds)
+    for it in (0, 3, 11):
+        ref = engine.draw_smooth_points(model, ds, 257, 0.16, 0.004,
+                                        seeds.substream(cfg.seed, seeds.SMOOTH, it))
+        raw = engine.smooth_raw_draws(ds, 257, 0.16, seeds.substream(cfg.seed, seeds.SMOOTH, it))
+        got = eng.smooth_points(raw, 0.004).cpu().numpy()
+        want = np.concatenate([ref[0], ref[1]], axis=0).astype(model.dtype)
+        np.testing.assert_array_equal(got, want)
