@@ -306,6 +306,8 @@ def main():
     S = cfg.weights.smooth_count
 
     def objective(d, kw, ids, sm):
+        if isinstance(sm, tuple):  # device-resident raw smoothness draws: part of the step
+            sm = eng.smooth_points_dev(*sm)
         if dp is None:
             return eng.launch(cfg, d, ids, sm, **kw)
         return dp(cfg, d, ids, sm, **kw)
@@ -320,7 +322,10 @@ def main():
     pre = []
     for it in range(W + K):
         d, kw = draws_for(it)
-        ids, sm = eng.upload(d)
+        ids = torch.from_numpy(d.ray_ids).to(dev)
+        sm = None
+        if d.smooth_raw is not None:
+            sm = (eng.upload_smooth_raw(d.smooth_raw), d.n_smooth, d.smooth_delta)
         pre.append((d, kw, ids, sm))
     torch.cuda.synchronize()
     for it in range(W):

@@ -207,11 +207,15 @@ int gsb_adam_step(int32_t precision, void* params, void* grads, void* m, void* v
  * np.nonzero order), jitter = uniform(-truncation, truncation, count),
  * normals = normal((count, 8, 3)).  poses: (F, 12) f64 rows of
  * ModelState.pose_matrices() (R row-major, then t); row_cum: (F*H) inclusive
- * prefix counts of valid pixels per image row.  out: (2*count, 3) model dtype,
- * x then x + eps, clamped to model->lo_c/hi_c.  Bit-exact with the reference. */
+ * prefix counts of valid pixels per image row; valid_u: (F*H, W) int16, row r's
+ * valid columns in increasing order in its first row_cum[r]-row_cum[r-1]
+ * entries (the per-row compaction of Dataset.valid_pixels, gs/scenegen.py:281-287).
+ * out: (2*count, 3) model dtype, x then x + eps, clamped to model->lo_c/hi_c.
+ * Bit-exact with the reference. */
 int gsb_smooth_points(const gsb_model_t* model, const gsb_dataset_t* data, const double* poses,
-                      const int64_t* row_cum, const int64_t* pick, const double* jitter,
-                      const double* normals, int32_t count, double delta, void* out, void* stream);
+                      const int64_t* row_cum, const int16_t* valid_u, const int64_t* pick,
+                      const double* jitter, const double* normals, int32_t count, double delta,
+                      void* out, void* stream);
 
 /* ---------------- geometry on point lists ---------------- */
 

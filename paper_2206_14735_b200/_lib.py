@@ -105,7 +105,7 @@ def lib():
         "gsb_version": ([], I32),
         "gsb_launch_count": ([], C.c_uint64),
         "gsb_sdf_workspace_size": ([C.POINTER(Model), I64, C.POINTER(SZ)], I32),
-        "gsb_smooth_points": ([C.POINTER(Model), C.POINTER(Dataset), P, P, P, P, P, I32, D, P, P], I32),
+        "gsb_smooth_points": ([C.POINTER(Model), C.POINTER(Dataset), P, P, P, P, P, P, I32, D, P, P], I32),
         "gsb_sdf_points": ([C.POINTER(Model), P, I64, P, P, SZ, P], I32),
         "gsb_sdf_fit_step": ([C.POINTER(Model), P, P, I64, I64, P, SZ, P, P], I32),
         "gsb_timing_enable": ([I32], I32),

@@ -345,9 +345,11 @@ __global__ void k_ray_batch_twin(gsb_dataset_t D, const int64_t* ids, int n, dou
 }
 
 int gsb_smooth_points(const gsb_model_t* model, const gsb_dataset_t* data, const double* poses,
-                      const int64_t* row_cum, const int64_t* pick, const double* jitter,
-                      const double* normals, int32_t count, double delta, void* out, void* stream) {
-  if (!model || !data || !poses || !row_cum || !pick || !jitter || !normals || !out || count < 0)
+                      const int64_t* row_cum, const int16_t* valid_u, const int64_t* pick,
+                      const double* jitter, const double* normals, int32_t count, double delta,
+                      void* out, void* stream) {
+  if (!model || !data || !poses || !row_cum || !valid_u || !pick || !jitter || !normals || !out ||
+      count < 0)
     return GSB_E_ARG;
   if (count == 0) return GSB_OK;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
@@ -355,12 +357,12 @@ int gsb_smooth_points(const gsb_model_t* model, const gsb_dataset_t* data, const
   const int blocks = (count + 127) / 128;
   if (model->precision == 0) {
     Geo G = geo_of(model, 4);
-    k_smooth_points<float><<<blocks, 128, 0, s>>>(*data, poses, row_cum, n_rows, pick, jitter, normals,
-                                                  count, delta, G, (float*)out);
+    k_smooth_points<float><<<blocks, 128, 0, s>>>(*data, poses, row_cum, n_rows, valid_u, pick, jitter,
+                                                  normals, count, delta, G, (float*)out);
   } else {
     Geo G = geo_of(model, 8);
-    k_smooth_points<double><<<blocks, 128, 0, s>>>(*data, poses, row_cum, n_rows, pick, jitter,
-                                                   normals, count, delta, G, (double*)out);
+    k_smooth_points<double><<<blocks, 128, 0, s>>>(*data, poses, row_cum, n_rows, valid_u, pick,
+                                                   jitter, normals, count, delta, G, (double*)out);
   }
   GSB_LAUNCHED();
   return GSB_OK;

@@ -345,6 +345,7 @@ static __device__ void separation_fallback(double* row, int32_t* src, int k) {
 template <typename T>
 __global__ void k_smooth_points(gsb_dataset_t D, const double* __restrict__ poses,
                                 const int64_t* __restrict__ row_cum, int64_t n_rows,
+                                const int16_t* __restrict__ valid_u,
                                 const int64_t* __restrict__ pick, const double* __restrict__ jitter,
                                 const double* __restrict__ nrm, int S, double delta, Geo G,
                                 T* __restrict__ out) {
@@ -359,13 +360,11 @@ __global__ void k_smooth_points(gsb_dataset_t D, const double* __restrict__ pose
     if (row_cum[mid] > k) hi = mid; else lo = mid + 1;
   }
   const int64_t row = lo;
-  int64_t r = k - (row > 0 ? row_cum[row - 1] : 0);
+  const int64_t r = k - (row > 0 ? row_cum[row - 1] : 0);
   const int64_t f = row / D.height;
   const int v = (int)(row % D.height);
   const uint16_t* drow = D.depth_mm + row * D.width;
-  int u = 0;
-  for (; u < D.width; ++u)
-    if (drow[u] > 0 && r-- == 0) break;
+  const int u = valid_u[row * D.width + r];  // r-th valid column (per-row compacted index)
   // pixel ray and z -> ray-distance scale (gs/camera.py:142-171)
   const double dx = ((double)u - D.cx) / D.fx;
   const double dy = ((double)v - D.cy) / D.fy;

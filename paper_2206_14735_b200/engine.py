@@ -275,26 +275,39 @@ class StepEngine:
             torch = self.torch
             mats = self.model.pose_matrices()
             P = np.concatenate([mats[:, :3, :3].reshape(-1, 9), mats[:, :3, 3]], axis=1)
+            ds = self.dataset
+            mask = (ds.depths_mm > 0).reshape(-1, ds.depths_mm.shape[-1])
+            # per-row compaction: row r's valid columns, in order, come first
+            if mask.shape[1] >= 1 << 15:
+                raise ValueError("image width exceeds the int16 valid-column index")
+            valid_u = np.argsort(~mask, axis=1, kind="stable").astype(np.int16)
             self._smooth_tab = (
                 torch.from_numpy(np.ascontiguousarray(P, dtype=np.float64)).to(self.device),
-                torch.from_numpy(np.ascontiguousarray(self.dataset._rows(), dtype=np.int64)).to(self.device))
+                torch.from_numpy(np.ascontiguousarray(ds._rows(), dtype=np.int64)).to(self.device),
+                torch.from_numpy(np.ascontiguousarray(valid_u)).to(self.device))
         return self._smooth_tab
+
+    def upload_smooth_raw(self, raw):
+        """Raw smoothness draws -> one device buffer [pick | jitter | normals]."""
+        pick, jitter, normals = raw
+        packed = np.concatenate([pick.view(np.float64), jitter, normals.reshape(-1)])
+        return self.torch.from_numpy(packed).pin_memory().to(self.device, non_blocking=True)
+
+    def smooth_points_dev(self, raw_dev, count, delta, stream=None):
+        """gsb_smooth_points on device-resident raw draws -> (2S, 3) points."""
+        poses, row_cum, valid_u = self._smooth_tables()
+        out = self.torch.empty((2 * count, 3), dtype=self.model.arena.params.dtype,
+                               device=self.device)
+        base = raw_dev.data_ptr()
+        _lib.check(self.lib.gsb_smooth_points(
+            C.byref(self.mstruct), C.byref(self.dstruct), poses.data_ptr(), row_cum.data_ptr(),
+            valid_u.data_ptr(), base, base + 8 * count, base + 16 * count, count, float(delta),
+            out.data_ptr(), _lib.stream_handle(stream)), "gsb_smooth_points")
+        return out
 
     def smooth_points(self, raw, delta, stream=None):
         """gsb_smooth_points: raw host draws -> (2S, 3) device points."""
-        torch = self.torch
-        pick, jitter, normals = raw
-        S = len(pick)
-        packed = np.concatenate([pick.view(np.float64), jitter, normals.reshape(-1)])
-        dev = torch.from_numpy(packed).pin_memory().to(self.device, non_blocking=True)
-        poses, row_cum = self._smooth_tables()
-        out = torch.empty((2 * S, 3), dtype=self.model.arena.params.dtype, device=self.device)
-        base = dev.data_ptr()
-        _lib.check(self.lib.gsb_smooth_points(
-            C.byref(self.mstruct), C.byref(self.dstruct), poses.data_ptr(), row_cum.data_ptr(),
-            base, base + 8 * S, base + 16 * S, S, float(delta), out.data_ptr(),
-            _lib.stream_handle(stream)), "gsb_smooth_points")
-        return out
+        return self.smooth_points_dev(self.upload_smooth_raw(raw), len(raw[0]), delta, stream)
 
     def upload(self, draws, stream=None):
         torch = self.torch
