@@ -239,6 +239,44 @@ int gsb_sdf_fit_step(const gsb_model_t* model, const void* points, const void* t
                      int64_t n_batch, int64_t n_anchor, void* workspace, size_t workspace_bytes,
                      double* loss_out, void* stream);
 
+/* ---------------- mesh extraction and metrics (gs/mesher.py) ---------------- */
+
+/* Dense SDF volume (mesher.sdf_volume, gs/mesher.py:114-133): vertex (i,j,k)
+ * at lo + (i,j,k) * resolution (f64, then the model dtype), phi stored as
+ * float32 in vol[(i * ny + j) * nz + k]. */
+int gsb_sdf_volume_workspace_size(const gsb_model_t* model, size_t* bytes);
+int gsb_sdf_volume(const gsb_model_t* model, const double* lo_host, double resolution, int64_t nx,
+                   int64_t ny, int64_t nz, float* vol, void* workspace, size_t workspace_bytes,
+                   void* stream);
+
+/* Marching cubes (mesher.mesh_from_sdf, gs/mesher.py:136-146) with the
+ * generated 256-case table (mc_table.py; table = packed int8 ntri[256] |
+ * tri[256][16] | edge corners[12][2], device).  gsb_mc_count writes the
+ * triangle total (int64) and the volume min/max (2 floats) to device memory;
+ * gsb_mc_emit then writes 3 f64 vertices per triangle (verts: 9 * total). */
+int gsb_mc_workspace_size(int64_t nx, int64_t ny, int64_t nz, size_t* bytes);
+int gsb_mc_count(const float* vol, int64_t nx, int64_t ny, int64_t nz, float level, const int8_t* table,
+                 void* workspace, size_t workspace_bytes, int64_t* total, float* minmax, void* stream);
+int gsb_mc_emit(const float* vol, int64_t nx, int64_t ny, int64_t nz, float level, double ox, double oy,
+                double oz, double resolution, const int8_t* table, void* workspace,
+                size_t workspace_bytes, double* verts, void* stream);
+
+/* Exact nearest neighbour from each query into ref (mesher.nearest_neighbors,
+ * gs/mesher.py:302-363): the same cell hash (lo, cell, dims computed by the
+ * caller as the reference does), ring order and early-out, so distances and
+ * tie-broken indices equal the reference's. */
+int gsb_nn_workspace_size(int64_t n_ref, int64_t nx, int64_t ny, int64_t nz, size_t* bytes);
+int gsb_nearest_neighbors(const double* query, int64_t nq, const double* ref, int64_t nr,
+                          const double* lo_host, double cell, int64_t nx, int64_t ny, int64_t nz,
+                          void* workspace, size_t workspace_bytes, double* out_d, int64_t* out_i,
+                          void* stream);
+
+/* Min-z buffer of a mesh in one camera (mesher._raster_zbuffer,
+ * gs/mesher.py:198-229): u, v, z per vertex (f64, device), faces (F, 3) int64;
+ * zbuf (height, width) f64 = +inf where nothing is drawn. */
+int gsb_raster_zbuffer(const double* u, const double* v, const double* z, const int64_t* faces,
+                       int64_t n_faces, int32_t height, int32_t width, double* zbuf, void* stream);
+
 /* ---------------- unit twins (parity tests) ---------------- */
 
 int gsb_pcg64_random(const gsb_pcg64_t* rng, int64_t offset, int64_t n, double* out,

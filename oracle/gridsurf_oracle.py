@@ -879,3 +879,51 @@ def train_step(P, opt, dataset, cfg, iteration):
     names = P.names()
     opt.step(P.arrays(), [R["grads"][n] for n in names])
     return R
+
+
+# ---------------------------------------------------------------------------
+# marching cubes (test infrastructure): numpy restatement of the device
+# kernel over the generated 256-case table (paper_2206_14735_b200/mc_table.py),
+# standing in for skimage.measure.marching_cubes, which is not installed here.
+# Cells in C order, triangles in table order, three vertices per triangle;
+# vertex = origin-free grid coordinates scaled by spacing (as skimage).
+
+
+def marching_cubes(vol, level=0.0, spacing=(1.0, 1.0, 1.0), table=None):
+    if table is None:
+        import importlib.util
+        import os
+        here = os.path.dirname(os.path.abspath(__file__))
+        spec = importlib.util.spec_from_file_location(
+            "mc_table", os.path.join(here, "..", "paper_2206_14735_b200", "mc_table.py"))
+        mod = importlib.util.module_from_spec(spec)
+        spec.loader.exec_module(mod)
+        table = (mod.TABLE, mod.NTRI, mod.EDGE_CORNERS)
+    tab, ntri, edges = table
+    vol = np.asarray(vol, dtype=np.float32)
+    nx, ny, nz = vol.shape
+    corners = np.array([[(k >> 2) & 1, (k >> 1) & 1, k & 1] for k in range(8)])
+    idx = np.zeros((nx - 1, ny - 1, nz - 1), dtype=np.int64)
+    vals = []
+    for k, (dx, dy, dz) in enumerate(corners):
+        v = vol[dx:nx - 1 + dx, dy:ny - 1 + dy, dz:nz - 1 + dz]
+        vals.append(v)
+        idx |= (v < np.float32(level)).astype(np.int64) << k
+    cells = np.flatnonzero(ntri[idx.reshape(-1)] > 0)
+    verts = []
+    for c in cells:
+        i, r = divmod(int(c), (ny - 1) * (nz - 1))
+        j, k = divmod(r, nz - 1)
+        m = idx[i, j, k]
+        for q in range(3 * int(ntri[m])):
+            e = tab[m, q]
+            a, b = edges[e]
+            va = float(vals[a][i, j, k])
+            vb = float(vals[b][i, j, k])
+            t = (float(np.float32(level)) - va) / (vb - va)
+            pa = np.array([i, j, k]) + corners[a]
+            pb = np.array([i, j, k]) + corners[b]
+            verts.append([(pa[d] + t * (pb[d] - pa[d])) * spacing[d] for d in range(3)])
+    verts = np.asarray(verts, dtype=np.float64).reshape(-1, 3)
+    faces = np.arange(len(verts), dtype=np.int64).reshape(-1, 3)
+    return verts, faces

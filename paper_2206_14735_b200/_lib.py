@@ -29,6 +29,8 @@ EXPORTS = (
     "gsb_step_workspace_regions", "gsb_importance_refine", "gsb_launch_count",
     "gsb_timing_enable", "gsb_timing_collect",
     "gsb_sdf_workspace_size", "gsb_sdf_points", "gsb_sdf_fit_step", "gsb_smooth_points",
+    "gsb_sdf_volume_workspace_size", "gsb_sdf_volume", "gsb_mc_workspace_size", "gsb_mc_count",
+    "gsb_mc_emit", "gsb_nn_workspace_size", "gsb_nearest_neighbors", "gsb_raster_zbuffer",
 )
 REGIONS = ("parts", "counts", "status", "depths", "weights", "phi", "gphi", "color", "pbar",
            "ubar", "cbar", "ray_o", "ray_r", "ray_far")
@@ -105,6 +107,14 @@ def lib():
         "gsb_version": ([], I32),
         "gsb_launch_count": ([], C.c_uint64),
         "gsb_sdf_workspace_size": ([C.POINTER(Model), I64, C.POINTER(SZ)], I32),
+        "gsb_sdf_volume_workspace_size": ([C.POINTER(Model), C.POINTER(SZ)], I32),
+        "gsb_sdf_volume": ([C.POINTER(Model), P, D, I64, I64, I64, P, P, SZ, P], I32),
+        "gsb_mc_workspace_size": ([I64, I64, I64, C.POINTER(SZ)], I32),
+        "gsb_mc_count": ([P, I64, I64, I64, C.c_float, P, P, SZ, P, P, P], I32),
+        "gsb_mc_emit": ([P, I64, I64, I64, C.c_float, D, D, D, D, P, P, SZ, P, P], I32),
+        "gsb_nn_workspace_size": ([I64, I64, I64, I64, C.POINTER(SZ)], I32),
+        "gsb_raster_zbuffer": ([P, P, P, P, I64, I32, I32, P, P], I32),
+        "gsb_nearest_neighbors": ([P, I64, P, I64, P, D, I64, I64, I64, P, SZ, P, P, P], I32),
         "gsb_smooth_points": ([C.POINTER(Model), C.POINTER(Dataset), P, P, P, P, P, P, I32, D, P, P], I32),
         "gsb_sdf_points": ([C.POINTER(Model), P, I64, P, P, SZ, P], I32),
         "gsb_sdf_fit_step": ([C.POINTER(Model), P, P, I64, I64, P, SZ, P, P], I32),

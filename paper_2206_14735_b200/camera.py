@@ -130,3 +130,14 @@ def save_intrinsics(path, intr):
     with open(path, "w") as f:
         f.write(f"{intr.fx:.17g} {intr.fy:.17g} {intr.cx:.17g} {intr.cy:.17g} "
                 f"{intr.width} {intr.height}\n")
+
+
+def project(intr, c2w, points):
+    """World points into one camera -> (u, v, z_cam) (gs/camera.py:201-210):
+    p_cam = (p - t) R, pixel = f * p / z + c (z guarded away from 0)."""
+    c2w = np.asarray(c2w, dtype=np.float64)
+    R, t = c2w[:3, :3], c2w[:3, 3]
+    pc = (np.asarray(points, dtype=np.float64) - t) @ R
+    z = pc[:, 2]
+    safe = np.where(np.abs(z) > 1e-12, z, 1e-12)
+    return intr.fx * pc[:, 0] / safe + intr.cx, intr.fy * pc[:, 1] / safe + intr.cy, z

@@ -4,6 +4,7 @@
 #include <type_traits>
 
 #include "gsb_step.cuh"
+#include "gsb_mesh.cuh"
 
 #include <atomic>
 #include <cstring>
@@ -60,6 +61,13 @@ GSB_DECL(gsb_step_d222)
                                              void*, size_t, cudaStream_t);                     \
   extern "C" int gsb_step_##tag##_sdf_fit(const gsb_model_t*, const void*, const void*, int64_t, \
                                           int64_t, void*, size_t, double*, cudaStream_t);
+#define GSB_DECL_VOL(tag)                                                                          \
+  extern "C" int gsb_step_##tag##_sdf_volume(const gsb_model_t*, const double*, double, int64_t, int64_t, \
+                                             int64_t, float*, void*, size_t, cudaStream_t);
+GSB_DECL_VOL(f446)
+GSB_DECL_VOL(d446)
+GSB_DECL_VOL(f222)
+GSB_DECL_VOL(d222)
 GSB_DECL_SDF(f446)
 GSB_DECL_SDF(d446)
 GSB_DECL_SDF(f222)
@@ -183,6 +191,190 @@ int gsb_sdf_points(const gsb_model_t* model, const void* points, int64_t n, void
     default:
       return GSB_E_ARG;
   }
+}
+
+int gsb_sdf_volume_workspace_size(const gsb_model_t* model, size_t* bytes) {
+  if (!model || !bytes) return GSB_E_ARG;
+  const int nmlp = nmlp_of(model);
+  *bytes = model->precision == 0 ? sdf_volume_ws<float>(nmlp) : sdf_volume_ws<double>(nmlp);
+  return GSB_OK;
+}
+
+int gsb_sdf_volume(const gsb_model_t* model, const double* lo_host, double resolution, int64_t nx,
+                   int64_t ny, int64_t nz, float* vol, void* workspace, size_t workspace_bytes,
+                   void* stream) {
+  if (!model || !lo_host || !vol || !workspace || !(resolution > 0.0)) return GSB_E_ARG;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const bool f = model->precision == 0;
+  switch (shape_tag(model)) {
+    case 0:
+      return f ? gsb_step_f446_sdf_volume(model, lo_host, resolution, nx, ny, nz, vol, workspace,
+                                          workspace_bytes, s)
+               : gsb_step_d446_sdf_volume(model, lo_host, resolution, nx, ny, nz, vol, workspace,
+                                          workspace_bytes, s);
+    case 1:
+      return f ? gsb_step_f222_sdf_volume(model, lo_host, resolution, nx, ny, nz, vol, workspace,
+                                          workspace_bytes, s)
+               : gsb_step_d222_sdf_volume(model, lo_host, resolution, nx, ny, nz, vol, workspace,
+                                          workspace_bytes, s);
+    default:
+      return GSB_E_ARG;
+  }
+}
+
+// ---- marching cubes
+static size_t mc_layout(int64_t cells, size_t* o_counts, size_t* o_offsets, size_t* o_mm, size_t* o_tmp,
+                        size_t* tmp_bytes) {
+  size_t tb = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tb, (const int32_t*)nullptr, (int32_t*)nullptr, (int)cells);
+  size_t off = 0;
+  *o_counts = off;
+  off = align_up(off + (size_t)cells * 4);
+  *o_offsets = off;
+  off = align_up(off + (size_t)cells * 4);
+  *o_mm = off;
+  off = align_up(off + 16);
+  *o_tmp = off;
+  off = align_up(off + tb);
+  *tmp_bytes = tb;
+  return off;
+}
+
+int gsb_mc_workspace_size(int64_t nx, int64_t ny, int64_t nz, size_t* bytes) {
+  if (!bytes || nx < 2 || ny < 2 || nz < 2) return GSB_E_ARG;
+  const int64_t cells = (nx - 1) * (ny - 1) * (nz - 1);
+  if (cells >= INT32_MAX) return GSB_E_ARG;
+  size_t a, b, c, d, t;
+  *bytes = mc_layout(cells, &a, &b, &c, &d, &t);
+  return GSB_OK;
+}
+
+__global__ void k_mc_total(const int32_t* counts, const int32_t* offsets, int64_t cells, const int* mm,
+                           int64_t* total, float* minmax) {
+  total[0] = (int64_t)offsets[cells - 1] + counts[cells - 1];
+  for (int q = 0; q < 2; ++q) {
+    const int i = mm[q];
+    minmax[q] = __int_as_float(i >= 0 ? i : i ^ 0x7fffffff);
+  }
+}
+
+int gsb_mc_count(const float* vol, int64_t nx, int64_t ny, int64_t nz, float level, const int8_t* table,
+                 void* workspace, size_t workspace_bytes, int64_t* total, float* minmax, void* stream) {
+  if (!vol || !table || !workspace || !total || !minmax || nx < 2 || ny < 2 || nz < 2) return GSB_E_ARG;
+  const int64_t cells = (nx - 1) * (ny - 1) * (nz - 1);
+  if (cells >= INT32_MAX) return GSB_E_ARG;
+  size_t oc, oo, om, ot, tb;
+  if (mc_layout(cells, &oc, &oo, &om, &ot, &tb) > workspace_bytes) return GSB_E_ARG;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  unsigned char* w = reinterpret_cast<unsigned char*>(workspace);
+  int32_t* counts = reinterpret_cast<int32_t*>(w + oc);
+  int32_t* offsets = reinterpret_cast<int32_t*>(w + oo);
+  int* mm = reinterpret_cast<int*>(w + om);
+  const int init[2] = {INT_MAX, INT_MIN};
+  GSB_CHECK(cudaMemcpyAsync(mm, init, sizeof(init), cudaMemcpyHostToDevice, s));
+  mesh::k_mc_count<<<(int)((cells + 255) / 256), 256, 0, s>>>(vol, nx, ny, nz, level, table, counts, mm);
+  GSB_LAUNCHED();
+  GSB_CHECK(cub::DeviceScan::ExclusiveSum(w + ot, tb, counts, offsets, (int)cells, s));
+  k_mc_total<<<1, 1, 0, s>>>(counts, offsets, cells, mm, total, minmax);
+  GSB_LAUNCHED();
+  return GSB_OK;
+}
+
+int gsb_mc_emit(const float* vol, int64_t nx, int64_t ny, int64_t nz, float level, double ox, double oy,
+                double oz, double resolution, const int8_t* table, void* workspace, size_t workspace_bytes,
+                double* verts, void* stream) {
+  if (!vol || !table || !workspace || !verts || nx < 2 || ny < 2 || nz < 2) return GSB_E_ARG;
+  const int64_t cells = (nx - 1) * (ny - 1) * (nz - 1);
+  size_t oc, oo, om, ot, tb;
+  if (mc_layout(cells, &oc, &oo, &om, &ot, &tb) > workspace_bytes) return GSB_E_ARG;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  unsigned char* w = reinterpret_cast<unsigned char*>(workspace);
+  mesh::k_mc_emit<<<(int)((cells + 255) / 256), 256, 0, s>>>(
+      vol, nx, ny, nz, level, ox, oy, oz, resolution, table, reinterpret_cast<const int32_t*>(w + oc),
+      reinterpret_cast<const int32_t*>(w + oo), verts);
+  GSB_LAUNCHED();
+  return GSB_OK;
+}
+
+// ---- exact nearest neighbours
+static size_t nn_layout(int64_t nr, int64_t ncells, size_t o[6], size_t* tmp_bytes, int* bits) {
+  int b = 1;
+  while (b < 63 && (int64_t(1) << b) < ncells) ++b;
+  *bits = b;
+  size_t tb = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, tb, (const int64_t*)nullptr, (int64_t*)nullptr,
+                                  (const int64_t*)nullptr, (int64_t*)nullptr, (int)nr, 0, b);
+  size_t off = 0;
+  for (int k = 0; k < 4; ++k) {
+    o[k] = off;
+    off = align_up(off + (size_t)nr * 8);
+  }
+  o[4] = off;
+  off = align_up(off + (size_t)(ncells + 1) * 8);
+  o[5] = off;
+  off = align_up(off + tb);
+  *tmp_bytes = tb;
+  return off;
+}
+
+int gsb_nn_workspace_size(int64_t n_ref, int64_t nx, int64_t ny, int64_t nz, size_t* bytes) {
+  if (!bytes || n_ref <= 0 || n_ref >= INT32_MAX || nx <= 0 || ny <= 0 || nz <= 0) return GSB_E_ARG;
+  size_t o[6], tb;
+  int bits;
+  *bytes = nn_layout(n_ref, nx * ny * nz, o, &tb, &bits);
+  return GSB_OK;
+}
+
+int gsb_nearest_neighbors(const double* query, int64_t nq, const double* ref, int64_t nr, const double* lo_host,
+                          double cell, int64_t nx, int64_t ny, int64_t nz, void* workspace,
+                          size_t workspace_bytes, double* out_d, int64_t* out_i, void* stream) {
+  if (!query || !ref || !lo_host || !workspace || !out_d || !out_i || nr <= 0 || nq < 0 || !(cell > 0.0))
+    return GSB_E_ARG;
+  const int64_t ncells = nx * ny * nz;
+  size_t o[6], tb;
+  int bits;
+  if (nn_layout(nr, ncells, o, &tb, &bits) > workspace_bytes) return GSB_E_ARG;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  unsigned char* w = reinterpret_cast<unsigned char*>(workspace);
+  int64_t* cid = reinterpret_cast<int64_t*>(w + o[0]);
+  int64_t* idx = reinterpret_cast<int64_t*>(w + o[1]);
+  int64_t* scid = reinterpret_cast<int64_t*>(w + o[2]);
+  int64_t* order = reinterpret_cast<int64_t*>(w + o[3]);
+  int64_t* starts = reinterpret_cast<int64_t*>(w + o[4]);
+  mesh::k_nn_cells<<<(int)((nr + 255) / 256), 256, 0, s>>>(ref, nr, lo_host[0], lo_host[1], lo_host[2], cell,
+                                                           nx, ny, nz, cid, idx);
+  GSB_LAUNCHED();
+  GSB_CHECK(cub::DeviceRadixSort::SortPairs(w + o[5], tb, cid, scid, idx, order, (int)nr, 0, bits, s));
+  mesh::k_nn_starts<<<(int)((ncells + 1 + 255) / 256), 256, 0, s>>>(scid, nr, ncells, starts);
+  GSB_LAUNCHED();
+  if (nq > 0) {
+    mesh::k_nn_query<<<(int)((nq + 127) / 128), 128, 0, s>>>(query, nq, ref, order, starts, lo_host[0],
+                                                             lo_host[1], lo_host[2], cell, nx, ny, nz,
+                                                             out_d, out_i);
+    GSB_LAUNCHED();
+  }
+  return GSB_OK;
+}
+
+__global__ void k_fill_u64(unsigned long long* p, int64_t n, unsigned long long v) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) p[i] = v;
+}
+
+int gsb_raster_zbuffer(const double* u, const double* v, const double* z, const int64_t* faces,
+                       int64_t n_faces, int32_t height, int32_t width, double* zbuf, void* stream) {
+  if (!u || !v || !z || !faces || !zbuf || height <= 0 || width <= 0 || n_faces < 0) return GSB_E_ARG;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int64_t np = (int64_t)height * width;
+  unsigned long long* zb = reinterpret_cast<unsigned long long*>(zbuf);
+  k_fill_u64<<<(int)((np + 255) / 256), 256, 0, s>>>(zb, np, 0x7ff0000000000000ull);  // +inf
+  GSB_LAUNCHED();
+  if (n_faces > 0) {
+    mesh::k_raster_zbuffer<<<(int)((n_faces + 127) / 128), 128, 0, s>>>(u, v, z, faces, n_faces, height,
+                                                                        width, zb);
+    GSB_LAUNCHED();
+  }
+  return GSB_OK;
 }
 
 int gsb_sdf_fit_step(const gsb_model_t* model, const void* points, const void* targets,

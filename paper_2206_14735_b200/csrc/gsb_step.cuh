@@ -187,7 +187,7 @@ int run_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step
 // sample (the smoothness-point path), so phi is exactly the step's phi.
 
 template <typename T>
-Ws<T> carve_sdf(void* ws, int64_t n, int nmlp, size_t* bytes) {
+Ws<T> carve_sdf(void* ws, int64_t n, int nmlp, size_t* bytes, bool grad = true) {
   Carver<T> c;
   c.base = reinterpret_cast<unsigned char*>(ws);
   Ws<T> w{};
@@ -198,9 +198,9 @@ Ws<T> carve_sdf(void* ws, int64_t n, int nmlp, size_t* bytes) {
   w.r = c.template take<T>(4);
   w.sphi = c.template take<T>(n);
   w.sgphi = c.template take<T>(n * 3);
-  w.pbar = c.template take<T>(n);
-  w.ubar = c.template take<T>(n * 3);
-  const int64_t nb = std::max<int64_t>(kNbMax, (n + 127) / 128);
+  w.pbar = c.template take<T>(grad ? n : 1);
+  w.ubar = c.template take<T>(grad ? n * 3 : 1);
+  const int64_t nb = grad ? std::max<int64_t>(kNbMax, (n + 127) / 128) : 1;
   w.nb_max = (int)nb;
   w.mlp_part = c.template take<T>(nb * nmlp);
   w.wfrag = c.template take<uint4>(4096 + 68);
@@ -255,7 +255,7 @@ int run_sdf_points(const gsb_model_t* model, const void* points, int64_t n, void
   if (S::NMLP != nmlp_of(model) || n <= 0 || n > INT32_MAX) return GSB_E_ARG;
   timing_point(nullptr, stream);
   size_t need = 0;
-  Ws<T> w = carve_sdf<T>(ws, n, S::NMLP, &need);
+  Ws<T> w = carve_sdf<T>(ws, n, S::NMLP, &need, false);
   if (need > ws_bytes) return GSB_E_ARG;
   w.sphi = reinterpret_cast<T*>(phi_out);
   GSB_CHECK(cudaMemsetAsync(w.status, 0, GSB_N_STATUS * sizeof(int32_t), stream));
@@ -306,6 +306,64 @@ int run_sdf_fit(const gsb_model_t* model, const void* points, const void* target
   GSB_LAUNCHED_T("k_finalize_mlp");
   if (loss_out)
     GSB_CHECK(cudaMemcpyAsync(loss_out, w.parts, sizeof(double), cudaMemcpyDeviceToDevice, stream));
+  return GSB_OK;
+}
+
+// ---- dense SDF volume (mesher.sdf_volume, gs/mesher.py:114-133): vertex
+// (i, j, k) at lo + (i, j, k) * res in f64 (numpy's lo + arange * res), cast
+// to the dtype, decoded in chunks of kVolChunk points; float32 output
+constexpr int64_t kVolChunk = int64_t(1) << 22;
+
+template <typename T>
+__global__ void k_grid_points(double lx, double ly, double lz, double res, int64_t ny, int64_t nz,
+                              int64_t start, int64_t count, T* __restrict__ out) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= count) return;
+  const int64_t g = start + t;
+  const int64_t k = g % nz, j = (g / nz) % ny, i = g / (ny * nz);
+  out[t * 3] = (T)(lx + (double)i * res);
+  out[t * 3 + 1] = (T)(ly + (double)j * res);
+  out[t * 3 + 2] = (T)(lz + (double)k * res);
+}
+
+template <typename T>
+__global__ void k_to_f32(const T* __restrict__ in, int64_t n, float* __restrict__ out) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t < n) out[t] = (float)in[t];
+}
+
+template <typename T>
+size_t sdf_volume_ws(int nmlp) {
+  size_t b = 0;
+  carve_sdf<T>(nullptr, kVolChunk, nmlp, &b, false);
+  return align_up(b) + align_up((size_t)kVolChunk * 3 * sizeof(T)) + align_up((size_t)kVolChunk * sizeof(T));
+}
+
+template <typename T, class S>
+int run_sdf_volume(const gsb_model_t* model, const double* lo, double res, int64_t nx, int64_t ny,
+                   int64_t nz, float* vol, void* ws, size_t ws_bytes, cudaStream_t stream) {
+  if (S::NMLP != nmlp_of(model) || nx <= 0 || ny <= 0 || nz <= 0) return GSB_E_ARG;
+  if (ws_bytes < sdf_volume_ws<T>(S::NMLP)) return GSB_E_ARG;
+  size_t b = 0;
+  unsigned char* base = reinterpret_cast<unsigned char*>(ws);
+  Ws<T> w = carve_sdf<T>(base, kVolChunk, S::NMLP, &b, false);
+  T* pts = reinterpret_cast<T*>(base + align_up(b));
+  T* phi = reinterpret_cast<T*>(base + align_up(b) + align_up((size_t)kVolChunk * 3 * sizeof(T)));
+  GSB_CHECK(cudaMemsetAsync(w.status, 0, GSB_N_STATUS * sizeof(int32_t), stream));
+  const int64_t total = nx * ny * nz;
+  for (int64_t s0 = 0; s0 < total; s0 += kVolChunk) {
+    const int64_t n = std::min(kVolChunk, total - s0);
+    k_grid_points<T><<<(int)((n + 255) / 256), 256, 0, stream>>>(lo[0], lo[1], lo[2], res, ny, nz, s0, n,
+                                                                pts);
+    GSB_LAUNCHED_T("k_grid_points");
+    w.sphi = sizeof(T) == 4 ? reinterpret_cast<T*>(vol + s0) : phi;
+    const int rc = sdf_forward<T, S>(model, w, pts, n, stream);
+    if (rc != GSB_OK) return rc;
+    if (sizeof(T) != 4) {
+      k_to_f32<T><<<(int)((n + 255) / 256), 256, 0, stream>>>(phi, n, vol + s0);
+      GSB_LAUNCHED_T("k_to_f32");
+    }
+  }
   return GSB_OK;
 }
 

@@ -25,3 +25,10 @@ extern "C" int GSB_CAT(GSB_ENTRY, _sdf_fit)(const gsb_model_t* m, const void* pt
   return gsb::host::run_sdf_fit<GSB_T, gsb::Shape<GSB_NL, GSB_CG, GSB_CC>>(m, pts, tgt, nb, na, ws,
                                                                            ws_bytes, loss, s);
 }
+
+extern "C" int GSB_CAT(GSB_ENTRY, _sdf_volume)(const gsb_model_t* m, const double* lo, double res,
+                                               int64_t nx, int64_t ny, int64_t nz, float* vol, void* ws,
+                                               size_t ws_bytes, cudaStream_t s) {
+  return gsb::host::run_sdf_volume<GSB_T, gsb::Shape<GSB_NL, GSB_CG, GSB_CC>>(m, lo, res, nx, ny, nz, vol,
+                                                                              ws, ws_bytes, s);
+}
