@@ -1,7 +1,11 @@
-"""Ray-sharded data parallelism on CPU: the package's
-DataParallelStep / shard_draws driven over a gloo world of 2, with the
-oracle standing in for the device step of each rank.  The all-reduced
-gradients and loss parts must equal the unsharded step."""
+"""Ray-sharded data parallelism: the package's
+DataParallelStep / shard_draws over a world of 2 must reproduce the
+unsharded step (all-reduced gradients, loss parts, partition counts).
+
+* CPU (gloo): the oracle stands in for each rank's device step.
+* GPU: the real device step on both ranks (this environment has one GPU, so
+  both ranks share it and the collectives are gloo on the host; the NCCL
+  path of bench.py runs the same DataParallelStep)."""
 
 import os
 import socket
@@ -141,3 +145,54 @@ def test_data_parallel_gloo_world2_equals_unsharded(tmp_path):
     np.testing.assert_allclose(z["parts"], z["ref_parts"], rtol=1e-12, atol=1e-15)
     scale = np.abs(z["ref"]).max()
     assert np.abs(z["got"] - z["ref"]).max() <= 1e-12 * scale
+
+
+def _gpu_worker(rank, world, port, out):
+    """Real device step under DataParallelStep; gloo collectives (both ranks
+    share the one GPU of this environment; collectives run on the host)."""
+    import torch
+    import torch.distributed as dist
+    from _golden import load
+    from paper_2206_14735_b200 import data, engine, optimizer, seeds
+    from paper_2206_14735_b200.parallel import DataParallelStep, shard_draws
+    from paper_2206_14735_b200.renderer import engine_for
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    try:
+        G = load("small", "double")
+        cfg = optimizer.TrainConfig(precision="double", **{
+            k: v for k, v in G.meta["cfg"].items() if k not in ("bounds", "voxel_sizes")},
+            voxel_sizes=G.cfg.voxel_sizes, bounds=G.cfg.bounds)
+        cfg.weights.smooth_count = G.meta["smooth_count"]
+        ds = data.Dataset(G.a["colors_u8"], G.a["depths_u16"], G.a["poses"], G.ds.intrinsics)
+        model = optimizer.build_model(ds, cfg, skip_init=True, device=torch.device("cuda", 0))
+        eng = engine_for(model, ds)
+        it = G.meta["iteration"]
+        full = engine.host_draws(model, ds, cfg, it)
+        d, kw = shard_draws(full, rank, world)
+        ids, sm = eng.upload(d)
+        ws = DataParallelStep(eng, dist)(cfg, d, ids, sm, **kw)
+        got = model.arena.grads.cpu().numpy().copy()
+        parts = ws["parts"].cpu().numpy().copy()
+        counts = ws["counts"].cpu().numpy().copy()
+        if rank == 0:  # the unsharded step on the same process/GPU
+            ids1, sm1 = eng.upload(full)
+            ws1 = eng.launch(cfg, full, ids1, sm1)
+            ref = model.arena.grads.cpu().numpy()
+            np.savez(out, got=got, ref=ref, parts=parts, ref_parts=ws1["parts"].cpu().numpy(),
+                     counts=counts, ref_counts=ws1["counts"].cpu().numpy())
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.timeout(900)
+def test_data_parallel_device_step_world2_equals_unsharded(tmp_path):
+    import torch.multiprocessing as mp
+    out = str(tmp_path / "dpgpu.npz")
+    mp.spawn(_gpu_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    z = np.load(out)
+    assert (z["counts"] == z["ref_counts"]).all()
+    np.testing.assert_allclose(z["parts"], z["ref_parts"], rtol=1e-12, atol=1e-15)
+    assert np.abs(z["got"] - z["ref"]).max() <= 1e-11 * np.abs(z["ref"]).max()
