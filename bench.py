@@ -46,10 +46,21 @@ def peaks():
     return 6650.0, "fallback"
 
 
-def make_cfg(precision="single", batch=M_PER_GPU, seed=0):
+def make_cfg(precision="single", batch=M_PER_GPU, seed=0, config=2, coarse=96, smooth=True):
+    """config 2 (BASELINE configs[1]) or 4 (configs[3]); c5's axes: the ray
+    batch, the coarse samples (N = coarse + 3 x 12) and smoothness on/off."""
     from paper_2206_14735_b200 import optimizer, scenes
-    return optimizer.TrainConfig(precision=precision, batch_rays=batch, seed=seed,
-                                 bounds=scenes.CONFIG2_BOUNDS, iterations=10 ** 6)
+    kw = dict(precision=precision, batch_rays=batch, seed=seed, iterations=10 ** 6,
+              coarse_samples=coarse)
+    if config == 4:
+        kw.update(bounds=scenes.CONFIG4_BOUNDS, voxel_sizes=scenes.CONFIG4_VOXELS,
+                  color_voxel=scenes.CONFIG4_COLOR_VOXEL)
+    else:
+        kw.update(bounds=scenes.CONFIG2_BOUNDS)
+    cfg = optimizer.TrainConfig(**kw)
+    if not smooth:
+        cfg.weights.smooth = 0.0
+    return cfg
 
 
 class Clocks:
@@ -141,7 +152,7 @@ def b_alg_bytes(model, M, N, S):
     G_s = sum(8 * l.width * 4 for l in model.grid.levels
               if l.features.size * 4 > 32 * 2 ** 20)
     Cc_s = 8 * 6 * 4 if model.grid.color.features.size * 4 > 32 * 2 ** 20 else 0
-    n_imp = 96 + 2 * 12
+    n_imp = N - 12  # coarse + 2 x 12 evaluated (the last round's 12 are not)
     return 32 * P + M * (n_imp * G_s + N * 2 * (G_s + Cc_s)) + 2 * S * 2 * G_s, P
 
 
@@ -152,6 +163,17 @@ MAC_COL_FWD = IN_C * HID + HID * HID + HID * 3
 MAC_GEO_BWD = MAC_GEO_FWD + MAC_DELTA + IN_G * HID + HID * HID + IN_G * HID + HID * HID + HID
 MAC_COL_BWD = MAC_COL_FWD + 3 * HID + HID * HID + HID * 6 + (IN_C + 1) * HID + HID * HID + HID * 3
 FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12                 # nominal FMA peak
+
+
+def workload_name(args, N):
+    sm = "off" if args.no_smooth else "on"
+    if args.config == 4:
+        return (f"config4: 10 m synthetic room, 640x480 RGB-D, 4-level grid "
+                f"(0.96/0.24/0.06/0.02 m + 0.02 m colour), 11 m box, "
+                f"{args.coarse}+3x12 samples/ray, smoothness {sm}")
+    return (f"config2: ScanNet-shaped 640x480 RGB-D, paper 4-level grid "
+            f"(0.96/0.24/0.06/0.03 m + 0.03 m colour), pinned 7x7x3.25 m box, "
+            f"{args.coarse}+3x12 samples/ray, smoothness {sm}")
 
 
 def traffic_of(kernel):
@@ -172,7 +194,7 @@ def kernel_table(model, kt, K, M, N, S, P, peak_hbm):
     """Per-kernel algorithmic work over live CUDA-event times."""
     G_s = sum(8 * l.width * 4 for l in model.grid.levels if l.features.size * 4 > 32 * 2 ** 20)
     Cc_s = 8 * 6 * 4 if model.grid.color.features.size * 4 > 32 * 2 ** 20 else 0
-    n_imp = 96 + 2 * 12
+    n_imp = N - 12  # coarse + 2 x 12 evaluated (the last round's 12 are not)
     NS = M * N + 2 * S
     work = {  # kernel: (bytes, MACs) per step
         "k_adam": (32 * P, 0),
@@ -269,6 +291,10 @@ def main():
     ap.add_argument("--frames", type=int, default=FRAMES)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--rays", type=int, default=M_PER_GPU)
+    ap.add_argument("--config", type=int, default=2, choices=[2, 4],
+                    help="2: ScanNet-shaped room (headline); 4: 10 m scene, 0.02 m grid (P = 1.7 B)")
+    ap.add_argument("--coarse", type=int, default=96, help="coarse samples per ray (c5 sweep)")
+    ap.add_argument("--no-smooth", action="store_true", help="lambda_smooth = 0 (c5 sweep)")
     ap.add_argument("--prefetch", action="store_true",
                     help="host draws on a background thread in the e2e leg")
     args = ap.parse_args()
@@ -290,8 +316,12 @@ def main():
     W = max(args.warmup, 3)
     K = args.steps
     M = args.rays
-    cfg = make_cfg(args.precision, batch=M * ws_)
-    ds = scenes.config2(frames=args.frames, threads=min(8, os.cpu_count() or 1))
+    cfg = make_cfg(args.precision, batch=M * ws_, config=args.config, coarse=args.coarse,
+                   smooth=not args.no_smooth)
+    if args.config == 4:
+        ds = scenes.config4(frames=args.frames, threads=min(8, os.cpu_count() or 1))
+    else:
+        ds = scenes.config2(frames=args.frames, threads=min(8, os.cpu_count() or 1))
     model = optimizer.build_model(ds, cfg, skip_init=True, device=dev)
     opt = optimizer.make_optimizer(model, cfg)
     eng = engine_for(model, ds)
@@ -303,7 +333,7 @@ def main():
         """Host draws of the global batch; this rank's shard (rank 0: smoothness)."""
         return parallel.shard_draws(engine.host_draws(model, ds, cfg, it), rank, ws_)
 
-    S = cfg.weights.smooth_count
+    S = cfg.weights.smooth_count if cfg.weights.smooth != 0.0 else 0
 
     def objective(d, kw, ids, sm):
         if isinstance(sm, tuple):  # device-resident raw smoothness draws: part of the step
@@ -440,12 +470,10 @@ def main():
             "warmup": W, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32" if args.precision == "single" else "f64",
             "data": "synthetic",
-            "config": {"workload": "config2: ScanNet-shaped 640x480 RGB-D, paper 4-level grid "
-                                   "(0.96/0.24/0.06/0.03 m + 0.03 m colour), pinned 7x7x3.25 m "
-                                   "box, 96+3x12 samples/ray, smoothness on",
+            "config": {"workload": workload_name(args, N),
                        "rays_per_gpu": M, "samples_per_ray": N, "params": P,
-                       "frames": args.frames, "l2": "working set (4 arenas x 256 MB) > L2; "
-                                                   "no explicit flush"},
+                       "frames": args.frames, "l2": f"working set (params/grad/m/v arenas = {4 * P * model.arena.params.element_size() / 1e9:.2f} GB) "
+                             "> L2 (126 MB); no explicit flush"},
             "samples_per_s": value * N,
             "e2e": {"value": e2e, "unit": "rays/s", "h2d_bytes_per_step": int(T.last_h2d),
                     "d2h_bytes_per_step": 8 * 8},
