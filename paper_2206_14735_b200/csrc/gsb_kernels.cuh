@@ -568,7 +568,7 @@ __global__ void __launch_bounds__(128) k_importance_dev(Ws<T> w, int M, int K, i
                                                         const T* __restrict__ log_s,
                                                         gsb_pcg64_t rng, int32_t* __restrict__ evl,
                                                         int32_t* __restrict__ evl_count, int64_t cap,
-                                                        int want_list) {
+                                                        int want_list, int count_final, double trunc) {
   __shared__ ImpSmem smem[4];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int i = blockIdx.x * 4 + wid;
@@ -589,6 +589,32 @@ __global__ void __launch_bounds__(128) k_importance_dev(Ws<T> w, int M, int K, i
     const int sv = S.src[t];
     if (sv >= 0) po[t] = ph[sv];
     else ++nnew;
+  }
+  if (count_final) {  // partition counts of the final samples (as k_counts)
+    const int valid = w.valid[i];
+    const double D = w.dray[i];
+    int ntr = 0, nfs = 0, neik = 0;
+    for (int t = lane; t < n; t += 32) {
+      const double b = D - S.out[t];
+      const bool tr = valid && fabs(b) <= trunc;
+      const bool fs = valid && b > trunc;
+      const bool bh = valid && b < -trunc;
+      ntr += tr;
+      nfs += fs;
+      neik += (fs || bh || !valid);
+    }
+    ntr = warp_sum(ntr);
+    nfs = warp_sum(nfs);
+    neik = warp_sum(neik);
+    if (lane == 0) {
+      w.cnt[i * 3 + 0] = ntr;
+      w.cnt[i * 3 + 1] = nfs;
+      w.cnt[i * 3 + 2] = neik;
+      atomicAdd((unsigned long long*)&w.counts[GSB_C_VALID], (unsigned long long)valid);
+      atomicAdd((unsigned long long*)&w.counts[GSB_C_TR], (unsigned long long)ntr);
+      atomicAdd((unsigned long long*)&w.counts[GSB_C_FS], (unsigned long long)nfs);
+      atomicAdd((unsigned long long*)&w.counts[GSB_C_EIK], (unsigned long long)neik);
+    }
   }
   if (!want_list) return;
   const int tot = warp_sum(nnew);

@@ -77,7 +77,8 @@ int run_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step
         GSB_CHECK(cudaMemsetAsync(w.evl_count, 0, sizeof(int32_t), stream));
         k_importance_dev<T><<<(M + 3) / 4, 128, 0, stream>>>(
             w, M, K, A, st->ray_base, w.dep[cur], w.phi[cur], w.dep[1 - cur], w.phi[1 - cur],
-            log_s, st->rng_importance[rnd], w.evl, w.evl_count, w.evl_cap, need_phi ? 1 : 0);
+            log_s, st->rng_importance[rnd], w.evl, w.evl_count, w.evl_cap, need_phi ? 1 : 0,
+            rnd == R - 1 ? 1 : 0, st->truncation);
         GSB_LAUNCHED_T("k_importance_dev");
         if (need_phi) {
           int64_t cap = (int64_t)M * A;
@@ -94,8 +95,10 @@ int run_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step
         K += A;
       }
     }
-    k_counts<T><<<(M + 127) / 128, 128, 0, stream>>>(w, M, N, dep_final, st->truncation);
-    GSB_LAUNCHED_T("k_counts");
+    if (R == 0) {  // otherwise counted by the last importance round
+      k_counts<T><<<(M + 127) / 128, 128, 0, stream>>>(w, M, N, dep_final, st->truncation);
+      GSB_LAUNCHED_T("k_counts");
+    }
   }
   if (st->phases & 2) {
     const T* spts = reinterpret_cast<const T*>(st->smooth_pts);
