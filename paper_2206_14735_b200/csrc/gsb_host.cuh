@@ -101,6 +101,8 @@ Ws<T> carve(void* ws, const Sizes& z, size_t* bytes, int64_t* off_parts = nullpt
   w.wfrag = c.template take<uint4>(4096 + 68);  // tc::kFragBufU4: fragments + vector block
   w.fin_red = c.template take<double>((int64_t)16 * z.nmlp);  // FIN_SPLIT x NMLP
   w.fin_cnt = c.template take<unsigned>((z.nmlp + 31) / 32);
+  w.loss_red = c.template take<double>((int64_t)((std::max(z.M, z.S) + 255) / 256 + 1) * 8);
+  w.loss_cnt = c.template take<unsigned>(4);
   if (bytes) *bytes = c.off;
   if (off_parts) *off_parts = (int64_t)o_parts;
   if (off_counts) *off_counts = (int64_t)o_counts;

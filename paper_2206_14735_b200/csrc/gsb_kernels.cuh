@@ -56,6 +56,8 @@ struct Ws {
   uint4* wfrag;         // float32: per-lane tf32 hi/lo B fragments of the MLP (gsb_tc.cuh)
   double* fin_red;      // [FIN_SPLIT][NMLP] chunk totals of k_finalize_mlp2
   unsigned* fin_cnt;    // [ceil(NMLP/32)] tickets (self-resetting; zeroed per step)
+  double* loss_red;     // [ceil(max(M, S) / 256)][8] block partials of k_finalize_loss
+  unsigned* loss_cnt;   // its ticket (zeroed per step)
   int nb_max;
   long long* counts;
   double* parts;
@@ -1601,49 +1603,65 @@ __global__ void __launch_bounds__(256) k_finalize_mlp2(Ws<T> w, T* grads, int64_
   }
 }
 
+// Loss parts and the log_s gradient from the per-ray / per-smoothness-pair
+// partials: one thread per item over many blocks, block partials in a
+// scratch array, and the last block (atomic ticket) sums them in block order.
 template <typename T>
-__global__ void k_finalize_loss(Ws<T> w, int M, int S, T* grads, const T* params, int64_t log_s_off,
-                                LossW L) {
-  __shared__ double red[7][32];
+__global__ void __launch_bounds__(256) k_finalize_loss(Ws<T> w, int M, int S, T* grads, const T* params,
+                                                       int64_t log_s_off, LossW L) {
+  __shared__ double red[7][8];
+  __shared__ bool last;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int i = blockIdx.x * 256 + tid;
   double acc[7] = {0, 0, 0, 0, 0, 0, 0};
-  for (int i = threadIdx.x; i < M; i += blockDim.x) {
+  if (i < M) {
     const double* p = w.ray_part + (int64_t)i * 8;
 #pragma unroll
-    for (int k = 0; k < 6; ++k) acc[k] += p[k];
+    for (int k = 0; k < 6; ++k) acc[k] = p[k];
   }
-  for (int j = threadIdx.x; j < S; j += blockDim.x) acc[6] += w.smooth_part[j];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (i < S) acc[6] = w.smooth_part[i];
 #pragma unroll
   for (int k = 0; k < 7; ++k) {
-    double v = warp_sum(acc[k]);
+    const double v = warp_sum(acc[k]);
     if (lane == 0) red[k][wid] = v;
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    double tot[7] = {0, 0, 0, 0, 0, 0, 0};
-    for (int k = 0; k < 7; ++k)
-      for (int q = 0; q < (int)(blockDim.x >> 5); ++q) tot[k] += red[k][q];
-    const T sT = exp(params[log_s_off]);
-    const double s = (double)sT;
-    long long nv = w.counts[GSB_C_VALID], ne = w.counts[GSB_C_EIK];
-    double rgb = tot[0] / L.m_global;
-    double dep = tot[1] / (double)(nv > 1 ? nv : 1);
-    double sdf = tot[2] / L.m_global;
-    double fs = tot[3] / L.m_global;
-    double eik = tot[4] / (double)(ne > 1 ? ne : 1);
-    double sm = L.smooth > 0.0 && S > 0 ? tot[6] / L.smooth_global : 0.0;
-    w.parts[GSB_P_RGB] = rgb;
-    w.parts[GSB_P_DEPTH] = dep;
-    w.parts[GSB_P_SDF] = sdf;
-    w.parts[GSB_P_FS] = fs;
-    w.parts[GSB_P_EIK] = eik;
-    w.parts[GSB_P_SMOOTH] = sm;
-    w.parts[GSB_P_S] = s;
-    w.parts[GSB_P_TOTAL] = L.rgb * rgb + L.depth * dep + L.sdf * sdf + L.fs * fs + L.eik * eik +
-                           L.smooth * sm;
-    // d total / d log_s = s * sum z_bar phi (exp vjp)
-    grads[log_s_off] += (T)(tot[5] * s);
+  if (tid < 7) {
+    double t = 0.0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) t += red[tid][q];
+    w.loss_red[blockIdx.x * 8 + tid] = t;
   }
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) last = atomicAdd(w.loss_cnt, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last || tid != 0) return;
+  __threadfence();
+  double tot[7] = {0, 0, 0, 0, 0, 0, 0};
+  for (int blk = 0; blk < (int)gridDim.x; ++blk)
+    for (int k = 0; k < 7; ++k) tot[k] += __ldcg(&w.loss_red[blk * 8 + k]);
+  *w.loss_cnt = 0u;  // ready for the next launch
+  const T sT = exp(params[log_s_off]);
+  const double s = (double)sT;
+  long long nv = w.counts[GSB_C_VALID], ne = w.counts[GSB_C_EIK];
+  double rgb = tot[0] / L.m_global;
+  double dep = tot[1] / (double)(nv > 1 ? nv : 1);
+  double sdf = tot[2] / L.m_global;
+  double fs = tot[3] / L.m_global;
+  double eik = tot[4] / (double)(ne > 1 ? ne : 1);
+  double sm = L.smooth > 0.0 && S > 0 ? tot[6] / L.smooth_global : 0.0;
+  w.parts[GSB_P_RGB] = rgb;
+  w.parts[GSB_P_DEPTH] = dep;
+  w.parts[GSB_P_SDF] = sdf;
+  w.parts[GSB_P_FS] = fs;
+  w.parts[GSB_P_EIK] = eik;
+  w.parts[GSB_P_SMOOTH] = sm;
+  w.parts[GSB_P_S] = s;
+  w.parts[GSB_P_TOTAL] = L.rgb * rgb + L.depth * dep + L.sdf * sdf + L.fs * fs + L.eik * eik +
+                         L.smooth * sm;
+  // d total / d log_s = s * sum z_bar phi (exp vjp)
+  grads[log_s_off] += (T)(tot[5] * s);
 }
 
 // ---------------------------------------------------------------------------

@@ -177,7 +177,9 @@ int run_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step
     k_finalize_mlp2<T, S><<<dim3((S::NMLP + 31) / 32, FIN_SPLIT), 256, 0, stream>>>(w, grads, model->mlp_offset,
                                                                     nb_geo, nb_col);
     GSB_LAUNCHED_T("k_finalize_mlp");
-    k_finalize_loss<T><<<1, 1024, 0, stream>>>(w, M, z.S, grads, params, model->log_s_offset, L);
+    GSB_CHECK(cudaMemsetAsync(w.loss_cnt, 0, sizeof(unsigned), stream));
+    k_finalize_loss<T><<<(std::max(M, z.S) + 255) / 256, 256, 0, stream>>>(w, M, z.S, grads, params,
+                                                                         model->log_s_offset, L);
     GSB_LAUNCHED_T("k_finalize_loss");
   }
   return GSB_OK;
