@@ -108,6 +108,17 @@ typedef struct {
                            the model dtype (PoseParam stores them in dtype) */
 } gsb_dataset_t;
 
+/* Camera poses under refinement (camera.PoseParam, gs/camera.py:53-90): frame f
+ * has base rotation R0_f (f64) and, when trainable, nu_f / t_f in the
+ * parameter arena (gs/optimizer.py:217-226 names them nu{f}, t{f}). */
+typedef struct {
+  int32_t n_frames;
+  const double* R0;          /* (F, 9) row-major, device */
+  const int64_t* nu_offset;  /* (F) element offset of nu_f in the arena, -1: frozen (nu = 0) */
+  const int64_t* t_offset;   /* (F) element offset of t_f, -1: frozen (t_fixed) */
+  const double* t_fixed;     /* (F, 3) translations of frozen frames (dtype-rounded), device */
+} gsb_pose_t;
+
 typedef struct {
   uint64_t state_hi, state_lo, inc_hi, inc_lo;  /* numpy PCG64 bit_generator state */
 } gsb_pcg64_t;
@@ -191,6 +202,25 @@ int gsb_step_workspace_regions(const gsb_model_t* model, int32_t n_rays, int32_t
  * model->grads (gsb_adam_step leaves them zeroed). */
 int gsb_train_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step_t* step,
                    void* stream);
+
+/* Pose refinement.
+ * gsb_pose_table: realised poses of the current parameters: table (F, 12) =
+ *   R0c exp_so3(nu) evaluated in the model dtype as the reference's graph does
+ *   (PoseParam.rotation, gs/camera.py:68-70, 96-122) and t -- the ray table
+ *   gsb_dataset_t.poses expects -- and table_f64 (F, 12) = R0 exp_so3_data(nu)
+ *   in float64 (PoseParam.matrix, gs/camera.py:75-80), the smoothness-point table.
+ * gsb_pose_grad: after gsb_train_step (same model / data / step arguments),
+ *   ACCUMULATES d total / d nu_f and d total / d t_f of every trainable frame
+ *   into model->grads: the tracked-point cotangent of each taped sample (phi,
+ *   grad-phi Hessian block, colour; gs/diffcore.py:893-991), the clip mask,
+ *   x = o + d r, r = R dir_cam per frame, and the exp_so3 adjoint.  Scratch:
+ *   gsb_pose_scratch_size bytes. */
+int gsb_pose_table(const gsb_model_t* model, const gsb_pose_t* pose, double* table, double* table_f64,
+                   void* stream);
+int gsb_pose_scratch_size(const gsb_model_t* model, int32_t n_rays, int32_t n_coarse, int32_t n_rounds,
+                          int32_t n_add, size_t* bytes);
+int gsb_pose_grad(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step_t* step,
+                  const gsb_pose_t* pose, void* scratch, size_t scratch_bytes, void* stream);
 
 /* Dense Adam over the whole arena (gs/optimizer.py:38-55): per segment
  * learning rate; float64 register math; grads zeroed afterwards.  If

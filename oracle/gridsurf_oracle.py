@@ -319,17 +319,98 @@ def sigmoid_raw(x):
 # model container
 
 
+# ---------------------------------------------------------------------------
+# poses: Rodrigues map (gs/camera.py:93-139) and its adjoint
+
+SMALL_ANGLE = 1e-4  # gs/camera.py:93
+
+
+def exp_so3_data(nu):
+    """gs/camera.py:125-139 (plain f64)."""
+    nu = np.asarray(nu, dtype=np.float64)
+    th2 = float(nu @ nu)
+    K = np.array([[0.0, -nu[2], nu[1]], [nu[2], 0.0, -nu[0]], [-nu[1], nu[0], 0.0]])
+    if np.sqrt(th2) < SMALL_ANGLE:
+        a = 1.0 - th2 / 6.0 + th2 * th2 / 120.0
+        b = 0.5 - th2 / 24.0 + th2 * th2 / 720.0
+    else:
+        th = np.sqrt(th2)
+        a = np.sin(th) / th
+        b = (1.0 - np.cos(th)) / th2
+    return np.eye(3) + a * K + b * (K @ K)
+
+
+def exp_so3_graph(nu):
+    """gs/camera.py:96-122 evaluated as the graph does, in nu's dtype.
+    Returns E and what the adjoint needs."""
+    dt = nu.dtype
+    z = np.zeros(1, dtype=dt)
+    n0, n1, n2 = nu[0:1], nu[1:2], nu[2:3]
+    K = np.concatenate([z, -n2, n1, n2, z, -n0, -n1, n0, z]).reshape(3, 3)
+    K2 = np.matmul(K, K)
+    th2 = (nu * nu).sum()
+    small = float(np.sqrt(th2.item())) < SMALL_ANGLE
+    if small:
+        a = 1.0 + th2 * (-1.0 / 6.0) + th2 * th2 * (1.0 / 120.0)
+        b = 0.5 + th2 * (-1.0 / 24.0) + th2 * th2 * (1.0 / 720.0)
+        th = None
+    else:
+        th = np.sqrt(th2)
+        a = np.sin(th) / th
+        b = (dt.type(1.0) - np.cos(th)) / th2
+    a, b = np.asarray(a, dtype=dt), np.asarray(b, dtype=dt)
+    E = np.eye(3, dtype=dt) + a.reshape(1, 1) * K + b.reshape(1, 1) * K2
+    return E, dict(K=K, K2=K2, th2=th2, th=th, a=a, b=b, small=small)
+
+
+def exp_so3_adjoint(nu, aux, Ebar):
+    """d/dnu of <E(nu), Ebar> through the graph of gs/camera.py:96-122."""
+    dt = nu.dtype
+    K, K2, th2, th, a, b = (aux[k] for k in ("K", "K2", "th2", "th", "a", "b"))
+    abar = (Ebar * K).sum()
+    bbar = (Ebar * K2).sum()
+    K2bar = b * Ebar
+    Kbar = a * Ebar + np.matmul(K2bar, K.T) + np.matmul(K.T, K2bar)
+    if aux["small"]:
+        th2bar = abar * (dt.type(-1.0 / 6.0) + dt.type(2.0 / 120.0) * th2) \
+            + bbar * (dt.type(-1.0 / 24.0) + dt.type(2.0 / 720.0) * th2)
+    else:
+        s, c = np.sin(th), np.cos(th)
+        thbar = abar * (c / th - s / (th * th)) + bbar * (s / th2)
+        th2bar = thbar / (dt.type(2.0) * th) - bbar * (dt.type(1.0) - c) / (th2 * th2)
+    nubar = dt.type(2.0) * nu * th2bar
+    nubar = nubar + np.array([Kbar[2, 1] - Kbar[1, 2], Kbar[0, 2] - Kbar[2, 0],
+                              Kbar[1, 0] - Kbar[0, 1]], dtype=dt)
+    return nubar.astype(dt)
+
+
+def pair_hessian(v, frac):
+    """gs/diffcore.py:783-804: off-diagonal trilinear Hessian (cell units)."""
+    fx, fy, fz = frac[:, 0], frac[:, 1], frac[:, 2]
+    h12 = (1.0 - fz) * (v[:, 0] + v[:, 6] - v[:, 2] - v[:, 4]) + fz * (v[:, 1] + v[:, 7] - v[:, 3] - v[:, 5])
+    h13 = (1.0 - fy) * (v[:, 0] + v[:, 5] - v[:, 1] - v[:, 4]) + fy * (v[:, 2] + v[:, 7] - v[:, 3] - v[:, 6])
+    h23 = (1.0 - fx) * (v[:, 0] + v[:, 3] - v[:, 1] - v[:, 2]) + fx * (v[:, 4] + v[:, 7] - v[:, 5] - v[:, 6])
+    return h12, h13, h23
+
+
 class Params:
     """ModelState restated (gs/renderer.py:69-105): grids coarse->fine,
     colour grid, two DecoderNets [(W (in,out), b)], log_s, frozen poses."""
 
-    def __init__(self, levels, color, geom, color_net, log_s, lo, hi, poses):
+    def __init__(self, levels, color, geom, color_net, log_s, lo, hi, poses, trainable=None):
         self.levels, self.color = levels, color
         self.geom, self.color_net = geom, color_net
         self.log_s = log_s
         self.lo = np.asarray(lo, dtype=np.float64)
         self.hi = np.asarray(hi, dtype=np.float64)
         self.poses = np.asarray(poses, dtype=np.float64)  # (F, 4, 4)
+        # PoseParam (gs/camera.py:53-90): R0 f64, nu / t in the model dtype
+        F = self.poses.shape[0]
+        dt = self.dtype
+        self.trainable = np.zeros(F, dtype=bool) if trainable is None else np.asarray(trainable, bool)
+        self.R0 = self.poses[:, :3, :3].copy()
+        self.nu = [np.zeros(3, dtype=dt) for _ in range(F)]
+        self.t = [self.poses[i, :3, 3].astype(dt) for i in range(F)]
 
     @property
     def dtype(self):
@@ -340,43 +421,63 @@ class Params:
         return min(l.voxel_size for l in self.levels)
 
     def pose_matrices(self):
-        """gs/renderer.py:104-105 / gs/camera.py:75-80: R0 @ exp(0) = R0 and
-        the translation as stored (PoseParam.t is in the model dtype)."""
-        m = self.poses.copy()
-        m[:, :3, 3] = m[:, :3, 3].astype(self.dtype).astype(np.float64)
+        """gs/renderer.py:104-105 / gs/camera.py:75-80: R0 @ exp_so3_data(nu)
+        (f64) and the translation as stored (PoseParam.t is in the model dtype)."""
+        m = np.zeros((len(self.nu), 4, 4))
+        m[:, 3, 3] = 1.0
+        for i in range(len(self.nu)):
+            m[i, :3, :3] = self.R0[i] @ exp_so3_data(self.nu[i])
+            m[i, :3, 3] = np.asarray(self.t[i], dtype=np.float64)
         return m
 
     def names(self):
-        """gs/optimizer.py:217-226 (no trainable poses)."""
+        """gs/optimizer.py:217-226."""
         n = [f"level{i}" for i in range(len(self.levels))] + ["colorgrid"]
         for tag, net in (("geom", self.geom), ("color", self.color_net)):
             for i in range(len(net)):
                 n += [f"{tag}_w{i}", f"{tag}_b{i}"]
-        return n + ["log_s"]
+        n.append("log_s")
+        for i in np.nonzero(self.trainable)[0]:
+            n += [f"nu{i}", f"t{i}"]
+        return n
 
     def arrays(self):
         out = [l.feat for l in self.levels] + [self.color.feat]
         for net in (self.geom, self.color_net):
             for W, b in net:
                 out += [W, b]
-        return out + [self.log_s]
+        out.append(self.log_s)
+        for i in np.nonzero(self.trainable)[0]:
+            out += [self.nu[i], self.t[i]]
+        return out
 
-    def lrs(self, lr_grids=1e-2, lr_decoders=1e-3):
+    def lrs(self, lr_grids=1e-2, lr_decoders=1e-3, lr_poses=5e-4):
         """gs/optimizer.py:229-236."""
         ng = len(self.levels) + 1
-        return [lr_grids] * ng + [lr_decoders] * (len(self.arrays()) - ng)
+        npose = 2 * int(self.trainable.sum())
+        return [lr_grids] * ng + [lr_decoders] * (len(self.arrays()) - ng - npose) + [lr_poses] * npose
+
+    def refresh_poses(self):
+        """PoseParam.refresh, gs/camera.py:82-87: fold exp(nu) into R0, zero nu."""
+        for i in np.nonzero(self.trainable)[0]:
+            self.R0[i] = self.R0[i] @ exp_so3_data(self.nu[i])
+            self.nu[i][...] = 0.0
 
     def copy(self):
         cp = lambda l: Level(l.origin, l.voxel_size, l.dims, l.feat.copy())
-        return Params([cp(l) for l in self.levels], cp(self.color),
-                      [(W.copy(), b.copy()) for W, b in self.geom],
-                      [(W.copy(), b.copy()) for W, b in self.color_net],
-                      self.log_s.copy(), self.lo, self.hi, self.poses)
+        P = Params([cp(l) for l in self.levels], cp(self.color),
+                   [(W.copy(), b.copy()) for W, b in self.geom],
+                   [(W.copy(), b.copy()) for W, b in self.color_net],
+                   self.log_s.copy(), self.lo, self.hi, self.poses, self.trainable)
+        P.R0 = self.R0.copy()
+        P.nu = [a.copy() for a in self.nu]
+        P.t = [a.copy() for a in self.t]
+        return P
 
 
 def create_params(lo, hi, poses, seed=0, voxel_sizes=(0.96, 0.24, 0.06, 0.03),
                   geom_width=4, color_voxel=None, color_width=6, dtype=np.float64,
-                  truncation=0.16):
+                  truncation=0.16, refine_poses=False, freeze_first_pose=True):
     """build_model(skip_init=True) restated: gs/optimizer.py:181-205,
     MultiGrid.create gs/feature_grid.py:48-91, DecoderNet.create
     gs/decoders.py:40-49 (same RNG streams and draw order)."""
@@ -406,7 +507,9 @@ def create_params(lo, hi, poses, seed=0, voxel_sizes=(0.96, 0.24, 0.06, 0.03),
     geom = net(geom_width * len(levels), 1, substream(seed, NET_INIT, 0))
     cnet = net(color_width + 3, 3, substream(seed, NET_INIT, 1))
     log_s = np.asarray(np.log(1.0 / truncation), dtype=dtype)
-    return Params(levels, color, geom, cnet, log_s, lo, hi, poses)
+    F = np.asarray(poses).shape[0]
+    trainable = [refine_poses and not (freeze_first_pose and i == 0) for i in range(F)]
+    return Params(levels, color, geom, cnet, log_s, lo, hi, poses, trainable)
 
 
 def mlp_forward(layers, x):
@@ -571,13 +674,9 @@ def train_objective(P, dataset, batch, iteration, cfg, smooth_override=None,
     lo_c, hi_c = P.lo + margin, P.hi - margin
     R = {}
 
-    # ray setup: gs/renderer.py:302-317 (frozen poses, R = R0 @ I exactly)
-    uniq, inv = np.unique(batch.frame_ids, return_inverse=True)
-    R9 = P.poses[uniq, :3, :3].astype(dt).reshape(-1, 9)
-    T3 = P.poses[uniq, :3, 3].astype(dt)
-    r_sel = np.take(R9, inv, axis=0).reshape(m, 3, 3)
-    o = np.take(T3, inv, axis=0)
-    r = np.matmul(r_sel, batch.dir_cam[:, :, None].astype(dt)).reshape(m, 3)
+    # ray setup: gs/renderer.py:302-317; R = R0 @ exp_so3(nu) in the model
+    # dtype (gs/camera.py:68-70, exactly R0 for nu = 0)
+    uniq, inv, pose_aux, o, r = realised_rays(P, batch)
     o_data, r_data = o.astype(np.float64), r.astype(np.float64)
     if cfg.fixed_far is not None:
         far = np.full(m, float(cfg.fixed_far))
@@ -622,7 +721,8 @@ def train_objective(P, dataset, batch, iteration, cfg, smooth_override=None,
 
     # taped pass: gs/renderer.py:348-370
     x = o.reshape(m, 1, 3) + depths[:, :, None].astype(dt) * r.reshape(m, 1, 3)
-    xf = np.minimum(np.maximum(x.reshape(m * n, 3), lo_c.astype(dt)), hi_c.astype(dt))
+    xu = x.reshape(m * n, 3)
+    xf = np.minimum(np.maximum(xu, lo_c.astype(dt)), hi_c.astype(dt))
     G = GeomPass(P, xf)
     cs = LevelSample(P.color, xf)
     fc = cs.value()
@@ -770,11 +870,123 @@ def train_objective(P, dataset, batch, iteration, cfg, smooth_override=None,
     a0b = np.matmul(a1b, cW[1].T) * (ca0 > 0)
     grads["color_w0"] += np.matmul(cin.T, a0b)
     grads["color_b0"] += a0b.sum(axis=0)
-    fc_bar = np.matmul(a0b, cW[0].T)[:, :fc.shape[1]]
+    in_bar = np.matmul(a0b, cW[0].T)
+    fc_bar = in_bar[:, :fc.shape[1]]
     grads["colorgrid"] += scatter_weighted(cs.idx8, cs.w8, fc_bar.astype(dt), P.color.n_vertices)
+    if P.trainable[uniq].any():
+        R["pose"] = pose_backward(P, G, cs, phi_bar.reshape(-1), u.astype(dt), fc_bar.astype(dt),
+                      in_bar[:, fc.shape[1]:].astype(dt), xu, lo_c, hi_c, depths, batch, uniq, inv,
+                      pose_aux, m, n, grads)
     R["grads"] = grads
     R["adjoints"] = dict(phi_bar=phi_bar, u=u.reshape(m, n, 3), c_bar=c_bar)
     return R
+
+
+def realised_rays(P, batch):
+    """gs/renderer.py:302-309: per unique frame R = R0 @ exp_so3(nu) in the
+    model dtype (gs/camera.py:68-70, exactly R0 for nu = 0), o = t, r = R dir_cam."""
+    dt = P.dtype
+    m = len(batch)
+    uniq, inv = np.unique(batch.frame_ids, return_inverse=True)
+    pose_aux = []
+    R9 = np.empty((len(uniq), 9), dtype=dt)
+    for j, f in enumerate(uniq):
+        E, aux = exp_so3_graph(P.nu[f])
+        R0c = P.R0[f].astype(dt)
+        R9[j] = np.matmul(R0c, E).reshape(9)
+        pose_aux.append((R0c, aux))
+    T3 = np.stack([P.t[f] for f in uniq]).astype(dt)
+    r_sel = np.take(R9, inv, axis=0).reshape(m, 3, 3)
+    o = np.take(T3, inv, axis=0)
+    r = np.matmul(r_sel, batch.dir_cam[:, :, None].astype(dt)).reshape(m, 3)
+    return uniq, inv, pose_aux, o, r
+
+
+def pose_grads_given(P, batch, depths, phi_bar, u, c_bar, lo_c, hi_c):
+    """Component restatement: the pose gradients of a step whose sampled
+    depths and loss adjoints (phi_bar (M, N), u (M, N, 3), c_bar (M, N, 3))
+    are given -- the taped point / colour recomputation plus pose_backward."""
+    dt = P.dtype
+    m, n = depths.shape
+    uniq, inv, pose_aux, o, r = realised_rays(P, batch)
+    x = o.reshape(m, 1, 3) + depths[:, :, None].astype(dt) * r.reshape(m, 1, 3)
+    xu = x.reshape(m * n, 3)
+    xf = np.minimum(np.maximum(xu, lo_c.astype(dt)), hi_c.astype(dt))
+    G = GeomPass(P, xf)
+    cs = LevelSample(P.color, xf)
+    fc = cs.value()
+    vdir = np.broadcast_to(r.reshape(m, 1, 3), (m, n, 3)).reshape(m * n, 3)
+    cin = np.concatenate([fc, vdir], axis=1)
+    (ca0, ca1, ca2), _, cy = mlp_forward(P.color_net, cin)
+    c_flat = sigmoid_raw(cy)
+    cW = [P.color_net[i][0] for i in range(3)]
+    y_bar = c_bar.reshape(m * n, 3).astype(dt) * (c_flat * (1.0 - c_flat))
+    a1b = np.matmul(y_bar, cW[2].T) * (ca1 > 0)
+    a0b = np.matmul(a1b, cW[1].T) * (ca0 > 0)
+    in_bar = np.matmul(a0b, cW[0].T)
+    grads = {nm: np.zeros_like(a) for nm, a in zip(P.names(), P.arrays())
+             if nm.startswith("nu") or (nm[0] == "t" and nm[1:].isdigit())}
+    inter = pose_backward(P, G, cs, np.asarray(phi_bar, dt).reshape(-1), np.asarray(u, dt).reshape(-1, 3),
+                          in_bar[:, :fc.shape[1]].astype(dt), in_bar[:, fc.shape[1]:].astype(dt), xu, lo_c,
+                          hi_c, depths, batch, uniq, inv, pose_aux, m, n, grads)
+    return grads, inter
+
+
+def pose_backward(P, G, cs, p, u, fc_bar, vdir_bar, xu, lo_c, hi_c, depths, batch, uniq, inv,
+                  pose_aux, m, n, grads):
+    """Gradients of the trainable poses.
+
+    Per taped sample the cotangent of the tracked point xf collects
+    (gs/renderer.py:352-365, gs/diffcore.py:893-991):
+      * phi:        J_l^T zbar_l with zbar = phi_bar * g (grid_sample vjp);
+      * grad phi:   the in-cell Hessian block, u against (h12, h13, h23) of
+                    the per-corner contraction theta_k . g_l (_grid_dx_op vjp,
+                    gs/diffcore.py:971-978; g is piecewise constant in z);
+      * colour:     J_c^T fc_bar.
+    The clip passes it where lo <= x <= hi (maximum/minimum ties,
+    gs/diffcore.py:506-529); x = o + d r gives o_bar = sum_n x_bar and
+    r_bar = sum_n d x_bar + view-direction cotangents; r = R dir_cam,
+    index_select per frame, R = R0 exp_so3(nu) (gs/camera.py:68-70)."""
+    dt = P.dtype
+    c = P.levels[0].feat.shape[1]
+    zbar = p.astype(dt)[:, None] * G.g
+    xb = None
+    for l, s in enumerate(G.ls):
+        gl = G.g[:, l * c:(l + 1) * c]
+        part = s.dx(zbar[:, l * c:(l + 1) * c])
+        # per-corner contraction, as _nb_dx_forward's gc (f64 accumulator)
+        gc = np.zeros((gl.shape[0], 8))
+        for k in range(8):
+            rows = s.lev.feat[s.idx8[:, k]]
+            for j in range(c):
+                gc[:, k] = gc[:, k] + (rows[:, j] * gl[:, j]).astype(np.float64)
+        h12, h13, h23 = pair_hessian(gc, s.frac)
+        vs2 = s.lev.voxel_size * s.lev.voxel_size
+        ua = u.astype(np.float64)
+        hx = np.empty_like(u)
+        hx[:, 0] = (h12 * ua[:, 1] + h13 * ua[:, 2]) / vs2
+        hx[:, 1] = (h12 * ua[:, 0] + h23 * ua[:, 2]) / vs2
+        hx[:, 2] = (h13 * ua[:, 0] + h23 * ua[:, 1]) / vs2
+        part = part + hx
+        xb = part if xb is None else xb + part
+    xb = xb + cs.dx(fc_bar)
+    inside = (xu >= lo_c.astype(dt)) & (xu <= hi_c.astype(dt))
+    xb = np.where(inside, xb, dt.type(0.0)).astype(dt).reshape(m, n, 3)
+    o_bar = xb.sum(axis=1)
+    r_bar = (xb * depths[:, :, None].astype(dt)).sum(axis=1) + vdir_bar.reshape(m, n, 3).sum(axis=1)
+    Rsel_bar = r_bar[:, :, None] * batch.dir_cam.astype(dt)[:, None, :]
+    R9_bar = np.zeros((len(uniq), 3, 3), dtype=dt)
+    T3_bar = np.zeros((len(uniq), 3), dtype=dt)
+    np.add.at(R9_bar, inv, Rsel_bar)
+    np.add.at(T3_bar, inv, o_bar)
+    for j, f in enumerate(uniq):
+        if not P.trainable[f]:
+            continue
+        R0c, aux = pose_aux[j]
+        Ebar = np.matmul(R0c.T, R9_bar[j])
+        grads[f"nu{f}"] += exp_so3_adjoint(P.nu[f], aux, Ebar)
+        grads[f"t{f}"] += T3_bar[j]
+    return dict(xbar=xb, vdir_bar=vdir_bar.reshape(m, n, 3), o_bar=o_bar, r_bar=r_bar)
 
 
 # ---------------------------------------------------------------------------
@@ -878,6 +1090,8 @@ def train_step(P, opt, dataset, cfg, iteration):
     R = train_objective(P, dataset, batch, iteration, cfg)
     names = P.names()
     opt.step(P.arrays(), [R["grads"][n] for n in names])
+    if P.trainable.any() and (iteration + 1) % cfg.pose_refresh_every == 0:
+        P.refresh_poses()
     return R
 
 

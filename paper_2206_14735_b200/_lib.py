@@ -31,6 +31,7 @@ EXPORTS = (
     "gsb_sdf_workspace_size", "gsb_sdf_points", "gsb_sdf_fit_step", "gsb_smooth_points",
     "gsb_sdf_volume_workspace_size", "gsb_sdf_volume", "gsb_mc_workspace_size", "gsb_mc_count",
     "gsb_mc_emit", "gsb_nn_workspace_size", "gsb_nearest_neighbors", "gsb_raster_zbuffer",
+    "gsb_pose_table", "gsb_pose_scratch_size", "gsb_pose_grad",
 )
 REGIONS = ("parts", "counts", "status", "depths", "weights", "phi", "gphi", "color", "pbar",
            "ubar", "cbar", "ray_o", "ray_r", "ray_far")
@@ -55,6 +56,11 @@ class Dataset(C.Structure):
                 ("n_frames", C.c_int32), ("height", C.c_int32), ("width", C.c_int32),
                 ("fx", C.c_double), ("fy", C.c_double), ("cx", C.c_double), ("cy", C.c_double),
                 ("poses", C.c_void_p)]
+
+
+class Pose(C.Structure):
+    _fields_ = [("n_frames", C.c_int32), ("R0", C.c_void_p), ("nu_offset", C.c_void_p),
+                ("t_offset", C.c_void_p), ("t_fixed", C.c_void_p)]
 
 
 class Pcg64(C.Structure):
@@ -117,6 +123,10 @@ def lib():
         "gsb_nearest_neighbors": ([P, I64, P, I64, P, D, I64, I64, I64, P, SZ, P, P, P], I32),
         "gsb_smooth_points": ([C.POINTER(Model), C.POINTER(Dataset), P, P, P, P, P, P, I32, D, P, P], I32),
         "gsb_sdf_points": ([C.POINTER(Model), P, I64, P, P, SZ, P], I32),
+        "gsb_pose_table": ([C.POINTER(Model), C.POINTER(Pose), P, P, P], I32),
+        "gsb_pose_scratch_size": ([C.POINTER(Model), I32, I32, I32, I32, C.POINTER(SZ)], I32),
+        "gsb_pose_grad": ([C.POINTER(Model), C.POINTER(Dataset), C.POINTER(Step), C.POINTER(Pose), P, SZ,
+                           P], I32),
         "gsb_sdf_fit_step": ([C.POINTER(Model), P, P, I64, I64, P, SZ, P, P], I32),
         "gsb_timing_enable": ([I32], I32),
         "gsb_timing_collect": ([I32, C.c_char_p, C.POINTER(D), C.POINTER(I64), C.POINTER(I32)], I32),

@@ -1,4 +1,4 @@
-"""Pinhole camera and (frozen) poses, host side (gs/camera.py).
+"""Pinhole camera and poses, host side (gs/camera.py).
 
 Conventions as the reference: camera looks down +z, image origin top-left,
 camera-to-world matrices, depth images store z-depth.
@@ -50,38 +50,57 @@ def exp_so3_data(nu):
 class PoseParam:
     """Camera-to-world pose R = R0 exp(nu^), t (gs/camera.py:53-90).
 
-    Pose refinement (trainable poses) is not part of the B200 step yet
-    (SURVEY.md 8f #3); poses are frozen constants stored in the model dtype
-    exactly as the reference stores non-trainable poses."""
+    Frozen poses keep nu = 0 and t as host arrays in the model dtype, exactly
+    as the reference stores non-trainable poses.  Trainable poses (pose
+    refinement) hold nu and t as views into the parameter
+    arena (``Param``), so the fused Adam updates them with the rest; R0 stays
+    on the host (f64) and is folded by ``refresh``."""
 
-    def __init__(self, R0, t, trainable=False, dtype=np.float64):
-        if trainable:
-            raise NotImplementedError("pose refinement is not implemented on the B200 path")
+    def __init__(self, R0, t, trainable=False, dtype=np.float64, nu_param=None, t_param=None):
         self.R0 = np.asarray(R0, dtype=np.float64).copy()
-        self.nu = np.zeros(3, dtype=dtype)
-        self.t = np.asarray(t, dtype=dtype).copy()
-        self.trainable = False
+        self.version = 0  # bumped by refresh (device copies of R0 follow it)
+        self.trainable = bool(trainable)
+        if self.trainable:
+            if nu_param is None or t_param is None:
+                raise ValueError("trainable poses live in the parameter arena (nu_param, t_param)")
+            self.nu, self.t = nu_param, t_param
+            self.t.set(np.asarray(t, dtype=dtype))
+        else:
+            self.nu = np.zeros(3, dtype=dtype)
+            self.t = np.asarray(t, dtype=dtype).copy()
 
     @classmethod
-    def from_matrix(cls, c2w, trainable=False, dtype=np.float64):
+    def from_matrix(cls, c2w, trainable=False, dtype=np.float64, nu_param=None, t_param=None):
         c2w = np.asarray(c2w, dtype=np.float64)
-        return cls(c2w[:3, :3], c2w[:3, 3], trainable=trainable, dtype=dtype)
+        return cls(c2w[:3, :3], c2w[:3, 3], trainable=trainable, dtype=dtype, nu_param=nu_param,
+                   t_param=t_param)
+
+    def nu_data(self):
+        return self.nu.numpy() if self.trainable else self.nu
+
+    def t_data(self):
+        return self.t.numpy() if self.trainable else self.t
 
     def rotation_data(self):
-        return self.R0 @ exp_so3_data(self.nu)
+        return self.R0 @ exp_so3_data(self.nu_data())
 
     def matrix(self):
         """gs/camera.py:75-80."""
         m = np.eye(4)
         m[:3, :3] = self.rotation_data()
-        m[:3, 3] = np.asarray(self.t, dtype=np.float64)
+        m[:3, 3] = np.asarray(self.t_data(), dtype=np.float64)
         return m
 
     def refresh(self):
-        return None
+        """Fold exp(nu) into R0 and zero nu (gs/camera.py:82-87)."""
+        if not self.trainable:
+            return
+        self.R0 = self.R0 @ exp_so3_data(self.nu_data())
+        self.nu.set(np.zeros(3))
+        self.version += 1
 
     def parameters(self):
-        return []
+        return [self.nu, self.t] if self.trainable else []
 
 
 def pixel_rays(intr, pixels, dtype=np.float64):

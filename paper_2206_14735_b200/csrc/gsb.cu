@@ -64,6 +64,13 @@ GSB_DECL(gsb_step_d222)
 #define GSB_DECL_VOL(tag)                                                                          \
   extern "C" int gsb_step_##tag##_sdf_volume(const gsb_model_t*, const double*, double, int64_t, int64_t, \
                                              int64_t, float*, void*, size_t, cudaStream_t);
+#define GSB_DECL_POSE(tag)                                                                      \
+  extern "C" int gsb_step_##tag##_pose_grad(const gsb_model_t*, const gsb_dataset_t*, const gsb_step_t*, \
+                                            const gsb_pose_t*, void*, size_t, cudaStream_t);
+GSB_DECL_POSE(f446)
+GSB_DECL_POSE(d446)
+GSB_DECL_POSE(f222)
+GSB_DECL_POSE(d222)
 GSB_DECL_VOL(f446)
 GSB_DECL_VOL(d446)
 GSB_DECL_VOL(f222)
@@ -188,6 +195,48 @@ int gsb_sdf_points(const gsb_model_t* model, const void* points, int64_t n, void
     case 1:
       return f ? gsb_step_f222_sdf_points(model, points, n, phi_out, workspace, workspace_bytes, s)
                : gsb_step_d222_sdf_points(model, points, n, phi_out, workspace, workspace_bytes, s);
+    default:
+      return GSB_E_ARG;
+  }
+}
+
+int gsb_pose_table(const gsb_model_t* model, const gsb_pose_t* pose, double* table, double* table_f64,
+                   void* stream) {
+  if (!model || !pose || !table || !table_f64 || pose->n_frames < 0) return GSB_E_ARG;
+  if (pose->n_frames == 0) return GSB_OK;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int b = (pose->n_frames + 127) / 128;
+  if (model->precision == 0)
+    k_pose_table<float><<<b, 128, 0, s>>>(*pose, reinterpret_cast<const float*>(model->params), table, table_f64);
+  else
+    k_pose_table<double><<<b, 128, 0, s>>>(*pose, reinterpret_cast<const double*>(model->params), table,
+                                           table_f64);
+  note_launch();
+  timing_point("k_pose_table", s);
+  return cudaGetLastError() == cudaSuccess ? GSB_OK : GSB_E_CUDA;
+}
+
+int gsb_pose_scratch_size(const gsb_model_t* model, int32_t n_rays, int32_t n_coarse, int32_t n_rounds,
+                          int32_t n_add, size_t* bytes) {
+  if (!model || !bytes || n_rays < 0) return GSB_E_ARG;
+  const Sizes z = sizes_of(model, n_rays, n_coarse, n_rounds, n_add, 0);
+  *bytes = model->precision == 0 ? pose_scratch_bytes<float>(z) : pose_scratch_bytes<double>(z);
+  return GSB_OK;
+}
+
+int gsb_pose_grad(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step_t* step,
+                  const gsb_pose_t* pose, void* scratch, size_t scratch_bytes, void* stream) {
+  if (!model || !data || !step || !pose || !scratch) return GSB_E_ARG;
+  if (pose->n_frames != data->n_frames) return GSB_E_ARG;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const bool f = model->precision == 0;
+  switch (shape_tag(model)) {
+    case 0:
+      return f ? gsb_step_f446_pose_grad(model, data, step, pose, scratch, scratch_bytes, s)
+               : gsb_step_d446_pose_grad(model, data, step, pose, scratch, scratch_bytes, s);
+    case 1:
+      return f ? gsb_step_f222_pose_grad(model, data, step, pose, scratch, scratch_bytes, s)
+               : gsb_step_d222_pose_grad(model, data, step, pose, scratch, scratch_bytes, s);
     default:
       return GSB_E_ARG;
   }

@@ -3,6 +3,10 @@
 
 #include "gsb_host.cuh"
 #include "gsb_tc.cuh"
+#include "gsb_t5.cuh"
+#include "gsb_pose.cuh"
+
+#include <cstdlib>
 
 #define GSB_CHECK(x)                           \
   do {                                         \
@@ -22,6 +26,37 @@
   } while (0)
 
 namespace gsb {
+
+// GSB_T5=0 selects the mma.sync form of the no-grad SDF kernel (A/B runs)
+inline bool use_t5() {
+  static const int v = [] {
+    const char* e = std::getenv("GSB_T5");
+    return e ? std::atoi(e) : 1;
+  }();
+  return v != 0;
+}
+inline int sm_count() {
+  static const int v = [] {
+    int dev = 0, n = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n > 0 ? n : 148;
+  }();
+  return v;
+}
+// persistent tcgen05 SDF evaluation over `cap` (upper bound of) samples
+template <class S>
+inline cudaError_t launch_sdf_t5(Ws<float> w, Geo G, int M, int Nc, const double* dep, double* phi,
+                                 const int32_t* list, const int32_t* list_count, int64_t cap,
+                                 cudaStream_t stream) {
+  const int64_t tiles = (cap + t5::kTile - 1) / t5::kTile;
+  const int grid = (int)std::min<int64_t>(tiles, (int64_t)sm_count() * t5::kCtaPerSm);
+  if (grid <= 0) return cudaSuccess;
+  t5::k_sdf_eval_t5<S><<<grid, t5::kTile, t5::SdfT5::smem(), stream>>>(w, G, M, Nc, dep, phi, list,
+                                                                        list_count);
+  return cudaGetLastError();
+}
+
 namespace host {
 
 template <typename T, class S>
@@ -42,8 +77,8 @@ int run_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step
   constexpr int TW = 4;                  // warps per CTA of the float32 sample kernels
   const float* mlp32 = reinterpret_cast<const float*>(mlp);
   if constexpr (F32) {
-    static_assert(tc::kFragBufU4 == 4096 + 68, "workspace carve");
-    tc::k_wfrag<S><<<tc::Fr<S>::NALL + 1, 32, 0, stream>>>(mlp32, w.wfrag);
+    static_assert(tc::kFragBufU4 == 4096 + 68 + 768, "workspace carve");
+    tc::k_wfrag<S><<<tc::Fr<S>::NALL + 5, 32, 0, stream>>>(mlp32, w.wfrag);
     GSB_LAUNCHED_T("k_wfrag");
   }
   const size_t smem_sdf = (size_t)S::NG * esz;
@@ -62,11 +97,15 @@ int run_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step
       int64_t n0 = (int64_t)M * Nc;
       int blocks = (int)((n0 + 127) / 128);
       if constexpr (F32) {
-        GSB_CHECK(cudaFuncSetAttribute(tc::k_sdf_eval_tc<S, TW>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)tc::SdfTc<S, TW>::smem()));
-        tc::k_sdf_eval_tc<S, TW><<<blocks, TW * 32, tc::SdfTc<S, TW>::smem(), stream>>>(
-            w, G, M, Nc, mlp32, w.dep[0], w.phi[0], nullptr, nullptr);
+        if (use_t5()) {
+          GSB_CHECK(launch_sdf_t5<S>(w, G, M, Nc, w.dep[0], w.phi[0], nullptr, nullptr, n0, stream));
+        } else {
+          GSB_CHECK(cudaFuncSetAttribute(tc::k_sdf_eval_tc<S, TW>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)tc::SdfTc<S, TW>::smem()));
+          tc::k_sdf_eval_tc<S, TW><<<blocks, TW * 32, tc::SdfTc<S, TW>::smem(), stream>>>(
+              w, G, M, Nc, mlp32, w.dep[0], w.phi[0], nullptr, nullptr);
+        }
       } else
         k_sdf_eval<T, S, false><<<blocks, 128, smem_sdf, stream>>>(w, G, M, Nc, w.dep[0],
                                                                    w.phi[0], nullptr, nullptr, mlp);
@@ -83,10 +122,14 @@ int run_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step
         if (need_phi) {
           int64_t cap = (int64_t)M * A;
           int b2 = (int)((cap + 127) / 128);
-          if constexpr (F32)
-            tc::k_sdf_eval_tc<S, TW><<<b2, TW * 32, tc::SdfTc<S, TW>::smem(), stream>>>(
-                w, G, M, Nc, mlp32, w.dep[1 - cur], w.phi[1 - cur], w.evl, w.evl_count);
-          else
+          if constexpr (F32) {
+            if (use_t5())
+              GSB_CHECK(launch_sdf_t5<S>(w, G, M, Nc, w.dep[1 - cur], w.phi[1 - cur], w.evl, w.evl_count,
+                                         cap, stream));
+            else
+              tc::k_sdf_eval_tc<S, TW><<<b2, TW * 32, tc::SdfTc<S, TW>::smem(), stream>>>(
+                  w, G, M, Nc, mlp32, w.dep[1 - cur], w.phi[1 - cur], w.evl, w.evl_count);
+          } else
             k_sdf_eval<T, S, false><<<b2, 128, smem_sdf, stream>>>(
                 w, G, M, Nc, w.dep[1 - cur], w.phi[1 - cur], w.evl, w.evl_count, mlp);
           GSB_LAUNCHED_T("k_sdf_eval");
@@ -208,7 +251,7 @@ Ws<T> carve_sdf(void* ws, int64_t n, int nmlp, size_t* bytes, bool grad = true) 
   const int64_t nb = grad ? std::max<int64_t>(kNbMax, (n + 127) / 128) : 1;
   w.nb_max = (int)nb;
   w.mlp_part = c.template take<T>(nb * nmlp);
-  w.wfrag = c.template take<uint4>(4096 + 68);
+  w.wfrag = c.template take<uint4>(4096 + 68 + 768);
   w.fin_red = c.template take<double>((int64_t)16 * nmlp);
   w.fin_cnt = c.template take<unsigned>((nmlp + 31) / 32);
   if (bytes) *bytes = c.off;
@@ -238,7 +281,7 @@ int sdf_forward(const gsb_model_t* model, Ws<T>& w, const T* pts, int64_t n, cud
   const int blocks = (int)((n + 127) / 128);
   if constexpr (sizeof(T) == 4) {
     constexpr int TW = 4;
-    tc::k_wfrag<S><<<tc::Fr<S>::NALL + 1, 32, 0, stream>>>(mlp, w.wfrag);
+    tc::k_wfrag<S><<<tc::Fr<S>::NALL + 5, 32, 0, stream>>>(mlp, w.wfrag);
     GSB_LAUNCHED_T("k_wfrag");
     GSB_CHECK(cudaFuncSetAttribute(tc::k_fwd_tc<S, TW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)tc::FwdTc<S, TW>::smem()));
@@ -369,6 +412,37 @@ int run_sdf_volume(const gsb_model_t* model, const double* lo, double res, int64
       GSB_LAUNCHED_T("k_to_f32");
     }
   }
+  return GSB_OK;
+}
+
+// pose gradients of the step just run on (model, data, st): SURVEY.md 8f #3
+template <typename T, class S>
+int run_pose_grad(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step_t* st,
+                  const gsb_pose_t* pose, void* scratch, size_t scratch_bytes, cudaStream_t stream) {
+  if (S::NMLP != nmlp_of(model)) return GSB_E_ARG;
+  const Sizes z = sizes_of(model, st->n_rays, st->n_coarse, st->n_rounds, st->n_add, st->n_smooth);
+  if (pose_scratch_bytes<T>(z) > scratch_bytes) return GSB_E_ARG;
+  size_t need = 0;
+  Ws<T> w = carve<T>(st->workspace, z, &need);
+  if (need > st->workspace_bytes) return GSB_E_ARG;
+  if (z.M == 0) return GSB_OK;
+  const Geo G = geo_of(model, sizeof(T));
+  const T* params = reinterpret_cast<const T*>(model->params);
+  T* grads = reinterpret_cast<T*>(model->grads);
+  const double* dep = w.dep[st->n_rounds % 2];
+  T* xbar = reinterpret_cast<T*>(scratch);
+  double* rbar = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(scratch) +
+                                           ((size_t)z.MN * 6 * sizeof(T) + 255) / 256 * 256);
+  using R = FwdRow<T, S>;
+  const size_t smem = ((size_t)(S::NMLP + 3) / 4 * 4 + 128 * R::ROW) * sizeof(T);
+  GSB_CHECK(cudaFuncSetAttribute(k_pose_xbar<T, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k_pose_xbar<T, S><<<(int)((z.MN + 127) / 128), 128, smem, stream>>>(w, G, z.M, z.N, dep,
+                                                                      params + model->mlp_offset, xbar);
+  GSB_LAUNCHED_T("k_pose_xbar");
+  k_pose_ray<T><<<(z.M + 3) / 4, 128, 0, stream>>>(w, z.M, z.N, dep, xbar, rbar);
+  GSB_LAUNCHED_T("k_pose_ray");
+  k_pose_frames<T><<<pose->n_frames, 256, 0, stream>>>(*data, st->ray_ids, z.M, *pose, params, rbar, grads);
+  GSB_LAUNCHED_T("k_pose_frames");
   return GSB_OK;
 }
 

@@ -32,3 +32,10 @@ extern "C" int GSB_CAT(GSB_ENTRY, _sdf_volume)(const gsb_model_t* m, const doubl
   return gsb::host::run_sdf_volume<GSB_T, gsb::Shape<GSB_NL, GSB_CG, GSB_CC>>(m, lo, res, nx, ny, nz, vol,
                                                                               ws, ws_bytes, s);
 }
+
+extern "C" int GSB_CAT(GSB_ENTRY, _pose_grad)(const gsb_model_t* m, const gsb_dataset_t* d, const gsb_step_t* st,
+                                              const gsb_pose_t* pose, void* scratch, size_t scratch_bytes,
+                                              cudaStream_t s) {
+  return gsb::host::run_pose_grad<GSB_T, gsb::Shape<GSB_NL, GSB_CG, GSB_CC>>(m, d, st, pose, scratch,
+                                                                             scratch_bytes, s);
+}

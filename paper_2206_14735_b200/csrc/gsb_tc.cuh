@@ -37,7 +37,20 @@ struct GVec {
 struct CVec {
   static constexpr int b0 = 0, b1 = 32, b2 = 64, w2 = 72, N = 168;  // w2: W2c (32 x 3)
 };
-constexpr int kFragBufU4 = kVecBase + (GVec::N + CVec::N) / 4;
+// tcgen05 operand block (gsb_t5.cuh): geometry W0 / W1 as B operands (out x in,
+// canonical K-major, no swizzle), tf32 hi and lo tiles; float offsets
+struct UmmaW {
+  static constexpr int W0H = 0, W0L = 512, W1H = 1024, W1L = 2048, N = 3072;
+};
+constexpr int kUmmaBaseU4 = kVecBase + (GVec::N + CVec::N) / 4;
+constexpr int kFragBufU4 = kUmmaBaseU4 + UmmaW::N / 4;
+
+// element (r, k) of an [R x K] fp32 operand tile: core matrices of 8 rows x
+// 4 k (16-byte rows, 128 B), K-adjacent core matrices 128 B apart (LBO), 8-row
+// groups K/4 core matrices apart (SBO = 32 K bytes)
+__host__ __device__ __forceinline__ int kmaj(int r, int k, int K) {
+  return (r >> 3) * (K / 4) * 32 + (k >> 2) * 32 + (r & 7) * 4 + (k & 3);
+}
 
 // ---- one-shot TMA bulk staging (cp.async.bulk + mbarrier transaction count)
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -107,6 +120,22 @@ template <class S>
 __global__ void __launch_bounds__(32) k_wfrag(const float* __restrict__ mlp, uint4* __restrict__ out) {
   using F = Fr<S>;
   const int id = blockIdx.x, lane = threadIdx.x, g = lane >> 2, t = lane & 3;
+  if (id > F::NALL) {  // tcgen05 B tiles: 1 W0 hi, 2 W0 lo, 3 W1 hi, 4 W1 lo
+    const int tile = id - F::NALL - 1, lo = tile & 1;
+    const bool l1 = tile >= 2;
+    const int K = l1 ? GSB_HID : 8 * F::KG, rows = l1 ? GSB_HID : S::IN_G;
+    const int oW = l1 ? S::oGW1 : S::oGW0;
+    float* o = reinterpret_cast<float*>(out + kUmmaBaseU4) + (l1 ? (lo ? UmmaW::W1L : UmmaW::W1H)
+                                                                  : (lo ? UmmaW::W0L : UmmaW::W0H));
+    for (int i = lane; i < GSB_HID * K; i += 32) {
+      const int n = i / K, k = i % K;  // B[n][k] = W[k][n]
+      const float v = k < rows ? mlp[oW + k * GSB_HID + n] : 0.f;
+      uint32_t h, l;
+      split_tf32(v, h, l);
+      o[kmaj(n, k, K)] = __uint_as_float(lo ? l : h);
+    }
+    return;
+  }
   if (id == F::NALL) {  // bias / W2 vectors: geometry block then colour block
     float* v = reinterpret_cast<float*>(out + kVecBase);
     for (int i = lane; i < GVec::N + CVec::N; i += 32) {

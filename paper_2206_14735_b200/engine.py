@@ -170,9 +170,56 @@ class StepEngine:
         self.device = model.arena.params.device
         self.lib = _lib.lib()
         self._ws = {}
-        self.col, self.dep, self.poses = dataset.device_tensors(self.device, model.dtype)
+        self.col, self.dep, _ = dataset.device_tensors(self.device, model.dtype)
         self.mstruct = self._model_struct()
+        self._init_poses()
         self.dstruct = self._dataset_struct()
+
+    # ---- poses
+    def _init_poses(self):
+        """Ray pose table (F, 12) from the MODEL's poses: R0c exp_so3(nu) and t in
+        the model dtype (gs/renderer.py:218-225), and the f64 PoseParam.matrix
+        table for the smoothness points.  Frozen poses: computed once here.
+        Trainable poses (pose refinement): gsb_pose_table refreshes both from
+        the arena every step (``pose_tables``)."""
+        torch = self.torch
+        model = self.model
+        dt = model.dtype
+        F = len(model.poses)
+        R0 = np.stack([p.R0 for p in model.poses]).reshape(F, 9)
+        tab = np.zeros((F, 12))
+        tab[:, :9] = R0.astype(dt).astype(np.float64)
+        tab[:, 9:] = np.stack([np.asarray(p.t_data(), dtype=dt) for p in model.poses]).astype(np.float64)
+        mats = model.pose_matrices()
+        tab64 = np.concatenate([mats[:, :3, :3].reshape(-1, 9), mats[:, :3, 3]], axis=1)
+        self.pose_tab = torch.from_numpy(np.ascontiguousarray(tab)).to(self.device)
+        self.pose_tab64 = torch.from_numpy(np.ascontiguousarray(tab64)).to(self.device)
+        self.refine = model.refine_poses
+        if not self.refine:
+            return
+        off = lambda p, q: (q.offset if p.trainable else -1)
+        self._pose_dev = dict(
+            R0=torch.from_numpy(np.ascontiguousarray(R0)).to(self.device),
+            nu_off=torch.tensor([off(p, p.nu) for p in model.poses], dtype=torch.int64, device=self.device),
+            t_off=torch.tensor([off(p, p.t) for p in model.poses], dtype=torch.int64, device=self.device),
+            t_fixed=self.pose_tab[:, 9:].contiguous())
+        self._pose_ver = tuple(p.version for p in model.poses)
+        d = self._pose_dev
+        self.pstruct = _lib.Pose(F, d["R0"].data_ptr(), d["nu_off"].data_ptr(), d["t_off"].data_ptr(),
+                                 d["t_fixed"].data_ptr())
+
+    def pose_tables(self, stream=None):
+        """Refresh the pose tables from the current R0 / nu / t (pose refinement)."""
+        if self.refine:
+            ver = tuple(p.version for p in self.model.poses)
+            if ver != self._pose_ver:  # a PoseParam.refresh folded nu into R0 on the host
+                R0 = np.stack([p.R0 for p in self.model.poses]).reshape(-1, 9)
+                self._pose_dev["R0"].copy_(self.torch.from_numpy(np.ascontiguousarray(R0)))
+                self._pose_ver = ver
+            _lib.check(self.lib.gsb_pose_table(C.byref(self.mstruct), C.byref(self.pstruct),
+                                               self.pose_tab.data_ptr(), self.pose_tab64.data_ptr(),
+                                               _lib.stream_handle(stream)), "gsb_pose_table")
+
 
     # ---- ABI structs
     def _model_struct(self):
@@ -187,7 +234,7 @@ class StepEngine:
         d.n_frames = len(ds)
         d.height, d.width = intr.height, intr.width
         d.fx, d.fy, d.cx, d.cy = (float(intr.fx), float(intr.fy), float(intr.cx), float(intr.cy))
-        d.poses = self.poses.data_ptr()
+        d.poses = self.pose_tab.data_ptr()
         return d
 
     # ---- workspace
@@ -270,11 +317,10 @@ class StepEngine:
 
     def _smooth_tables(self):
         """(F, 12) f64 pose_matrices() rows and the (F*H) valid-pixel row
-        prefix counts, device-resident (poses are frozen in this path)."""
+        prefix counts, device-resident (the pose table is the engine's, kept
+        current by ``pose_tables`` under pose refinement)."""
         if not hasattr(self, "_smooth_tab"):
             torch = self.torch
-            mats = self.model.pose_matrices()
-            P = np.concatenate([mats[:, :3, :3].reshape(-1, 9), mats[:, :3, 3]], axis=1)
             ds = self.dataset
             mask = (ds.depths_mm > 0).reshape(-1, ds.depths_mm.shape[-1])
             # per-row compaction: row r's valid columns, in order, come first
@@ -282,7 +328,7 @@ class StepEngine:
                 raise ValueError("image width exceeds the int16 valid-column index")
             valid_u = np.argsort(~mask, axis=1, kind="stable").astype(np.int16)
             self._smooth_tab = (
-                torch.from_numpy(np.ascontiguousarray(P, dtype=np.float64)).to(self.device),
+                self.pose_tab64,
                 torch.from_numpy(np.ascontiguousarray(ds._rows(), dtype=np.int64)).to(self.device),
                 torch.from_numpy(np.ascontiguousarray(valid_u)).to(self.device))
         return self._smooth_tab
@@ -311,6 +357,7 @@ class StepEngine:
 
     def upload(self, draws, stream=None):
         torch = self.torch
+        self.pose_tables(stream)
         ids = torch.from_numpy(draws.ray_ids).pin_memory().to(self.device, non_blocking=True)
         sm = None
         if draws.smooth is not None:
@@ -331,9 +378,28 @@ class StepEngine:
         if fresh:
             ws["status"].zero_()
         st = self.step_struct(cfg, draws, ray_ids_dev, smooth_dev, ws, **kw)
+        phases = kw.get("phases", 3)
+        if fresh and phases & 1:
+            self.pose_tables(stream)
         _lib.check(self.lib.gsb_train_step(C.byref(self.mstruct), C.byref(self.dstruct),
                                            C.byref(st), _lib.stream_handle(stream)),
                    "gsb_train_step")
-        if kw.get("phases", 3) & 2:
+        if phases & 2:
             self.model.arena.grads_clean = False
+            if self.refine:
+                self._pose_grad(cfg, st, M, stream)
         return ws
+
+    def _pose_grad(self, cfg, st, M, stream):
+        key = ("pose", M, cfg.coarse_samples, cfg.importance_rounds, cfg.importance_add)
+        if key not in self._ws:
+            nbytes = C.c_size_t(0)
+            _lib.check(self.lib.gsb_pose_scratch_size(C.byref(self.mstruct), M, cfg.coarse_samples,
+                                                      cfg.importance_rounds, cfg.importance_add,
+                                                      C.byref(nbytes)), "pose scratch size")
+            self._ws[key] = self.torch.empty(max(int(nbytes.value), 1), dtype=self.torch.uint8,
+                                             device=self.device)
+        buf = self._ws[key]
+        _lib.check(self.lib.gsb_pose_grad(C.byref(self.mstruct), C.byref(self.dstruct), C.byref(st),
+                                          C.byref(self.pstruct), buf.data_ptr(), buf.numel(),
+                                          _lib.stream_handle(stream)), "gsb_pose_grad")

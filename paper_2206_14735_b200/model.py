@@ -10,7 +10,7 @@ Arena layout (elements of the model dtype):
     level0 (V0, C) | level1 | ... | colour grid (Vc, Cc)      each 16-byte aligned
     MLP block: geom W0 b0 W1 b1 W2 b2 | pad to 4 | colour W0 b0 W1 b1 W2 b2
                (this exact layout is copied into __constant__ memory per step)
-    log_s
+    log_s | pose nu0 t0 nu1 t1 ... (trainable frames only)
 """
 
 from __future__ import annotations
@@ -219,7 +219,14 @@ class ModelState:
         return self.geom_net.parameters() + self.color_net.parameters() + [self.log_s]
 
     def pose_params(self):
-        return []
+        out = []
+        for p in self.poses:
+            out.extend(p.parameters())
+        return out
+
+    @property
+    def refine_poses(self):
+        return any(p.trainable for p in self.poses)
 
     def parameters(self):
         return self.grid_params() + self.decoder_params() + self.pose_params()
@@ -233,7 +240,11 @@ class ModelState:
         for tag, net in (("geom", self.geom_net), ("color", self.color_net)):
             for i in range(len(net.layers)):
                 names += [f"{tag}_w{i}", f"{tag}_b{i}"]
-        return names + ["log_s"]
+        names.append("log_s")
+        for i, p in enumerate(self.poses):
+            if p.trainable:
+                names += [f"nu{i}", f"t{i}"]
+        return names
 
 
 def level_dims(lo, hi, voxel_size):
@@ -246,8 +257,10 @@ def level_dims(lo, hi, voxel_size):
 
 
 def allocate_model(lo, hi, voxel_sizes, geom_width, color_voxel, color_width, poses, dtype,
-                   device):
-    """Create the arena and the container objects (values all zero)."""
+                   device, trainable=None):
+    """Create the arena and the container objects (values all zero except the
+    pose translations).  ``trainable[f]``: frame f's pose is refined (its nu
+    and t join the arena after log_s, gs/optimizer.py:217-226)."""
     lo = np.asarray(lo, dtype=np.float64)
     hi = np.asarray(hi, dtype=np.float64)
     sizes = sorted(voxel_sizes, reverse=True)  # coarse first (gs/feature_grid.py:87)
@@ -264,13 +277,20 @@ def allocate_model(lo, hi, voxel_sizes, geom_width, color_voxel, color_width, po
             specs.append((f"{tag}_w{i}", (a, b), f"mlp_{tag}"))
             specs.append((f"{tag}_b{i}", (b,), f"mlp_{tag}"))
     specs.append(("log_s", (), "log_s"))
+    trainable = [False] * len(poses) if trainable is None else [bool(t) for t in trainable]
+    for i, tr in enumerate(trainable):
+        if tr:
+            specs += [(f"nu{i}", (3,), "pose"), (f"t{i}", (3,), "pose")]
     arena = ParamArena(specs, dtype, device)
     levels = [GridLevel(g, arena[f"level{i}"]) for i, g in enumerate(geoms)]
     color = GridLevel(cgeom, arena["colorgrid"])
     grid = MultiGrid(levels, color, lo, hi)
     geom_net = DecoderNet([(arena[f"geom_w{i}"], arena[f"geom_b{i}"]) for i in range(3)])
     color_net = DecoderNet([(arena[f"color_w{i}"], arena[f"color_b{i}"]) for i in range(3)])
-    pose_objs = [PoseParam.from_matrix(p, trainable=False, dtype=dtype) for p in poses]
+    pose_objs = [PoseParam.from_matrix(p, trainable=tr, dtype=dtype,
+                                       nu_param=arena[f"nu{i}"] if tr else None,
+                                       t_param=arena[f"t{i}"] if tr else None)
+                 for i, (p, tr) in enumerate(zip(poses, trainable))]
     return ModelState(grid, geom_net, color_net, arena["log_s"], pose_objs, arena)
 
 

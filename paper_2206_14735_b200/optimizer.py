@@ -192,13 +192,12 @@ def _device(device=None):
 
 def build_model(dataset, cfg, initial_poses=None, skip_init=False, device=None):
     """gs/optimizer.py:181-214: grids, decoders, sharpness, poses."""
-    if cfg.refine_poses:
-        raise NotImplementedError("pose refinement is not implemented on the B200 path")
     dataset = Dataset.wrap(dataset)
     lo, hi = mdl.derive_bounds(dataset, cfg)
     poses = dataset.poses if initial_poses is None else np.asarray(initial_poses)
+    trainable = [cfg.refine_poses and not (cfg.freeze_first_pose and i == 0) for i in range(len(poses))]
     model = mdl.allocate_model(lo, hi, cfg.voxel_sizes, cfg.geom_feat_dim, cfg.color_voxel,
-                               cfg.color_feat_dim, poses, cfg.dtype, _device(device))
+                               cfg.color_feat_dim, poses, cfg.dtype, _device(device), trainable=trainable)
     mdl.init_parameters(model, cfg.seed, cfg.weights.truncation)
     if not skip_init:
         from .geometry import geometric_init
@@ -232,8 +231,8 @@ def save_model(path, model, cfg, iteration, opt=None):
     # the reference stores log_s as a 0-d array
     order = list(names)
     arrays["R0"] = np.stack([p.R0 for p in model.poses], axis=0)
-    arrays["pose_nu"] = np.stack([np.asarray(p.nu, dtype=np.float64) for p in model.poses], axis=0)
-    arrays["pose_t"] = np.stack([np.asarray(p.t, dtype=np.float64) for p in model.poses], axis=0)
+    arrays["pose_nu"] = np.stack([np.asarray(p.nu_data(), dtype=np.float64) for p in model.poses], axis=0)
+    arrays["pose_t"] = np.stack([np.asarray(p.t_data(), dtype=np.float64) for p in model.poses], axis=0)
     order += ["R0", "pose_nu", "pose_t"]
     if opt is not None:
         for name, m, v, t in zip(names, opt.m, opt.v, opt.t):
@@ -269,8 +268,6 @@ def load_model(path, device=None):
                          "bounds": tuple(map(tuple, cfg_d["bounds"])) if cfg_d.get("bounds") else None,
                          "voxel_sizes": tuple(cfg_d["voxel_sizes"]),
                          "weights": LossWeights(**w)})
-    if any(header["pose_trainable"]):
-        raise NotImplementedError("checkpoints with trainable poses are not supported")
     g = header["grid"]
     lv = g["levels"]
     dt = arrays["level0"].dtype
@@ -280,7 +277,7 @@ def load_model(path, device=None):
     poses[:, :3, 3] = arrays["pose_t"]
     model = mdl.allocate_model(g["lo"], g["hi"], [m["voxel_size"] for m in lv[:-1]],
                                lv[0]["width"], lv[-1]["voxel_size"], lv[-1]["width"], poses, dt,
-                               _device(device))
+                               _device(device), trainable=header["pose_trainable"])
     for lev, meta in zip(model.grid.levels + [model.grid.color], lv):
         if list(lev.geom.dims) != list(meta["dims"]) or not np.allclose(lev.geom.origin,
                                                                         meta["origin"]):
@@ -410,6 +407,9 @@ class Trainer:
         self.events[slot].record()
         self.opt.t = [t + 1 for t in self.opt.t]
         self.opt._launch(guard=ws["parts"], guard_threshold=self.cfg.divergence_threshold)
+        if self.engine.refine and (it + 1) % self.cfg.pose_refresh_every == 0:
+            for p in self.model.poses:  # gs/optimizer.py:374-376
+                p.refresh()
         return ws
 
     def parts(self, slot):

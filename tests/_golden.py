@@ -52,7 +52,8 @@ def cfg_ns(**kw):
              importance_add=12, seed=0, precision="double", near=0.01, max_depth=8.0,
              bounds=None, bounds_padding=0.5, voxel_sizes=(0.96, 0.24, 0.06, 0.03),
              color_voxel=None, geom_feat_dim=4, color_feat_dim=6, fixed_far=None,
-             lr_grids=1e-2, lr_decoders=1e-3, lr_poses=5e-4)
+             lr_grids=1e-2, lr_decoders=1e-3, lr_poses=5e-4, refine_poses=False,
+             freeze_first_pose=True, pose_refresh_every=100)
     d.update(kw)
     d.setdefault("weights", weights_ns())
     return SimpleNamespace(**d)
