@@ -171,6 +171,8 @@ def workload_name(args, N):
         return (f"config4: 10 m synthetic room, 640x480 RGB-D, 4-level grid "
                 f"(0.96/0.24/0.06/0.02 m + 0.02 m colour), 11 m box, "
                 f"{args.coarse}+3x12 samples/ray, smoothness {sm}")
+    if args.refine_poses:
+        sm += ", pose refinement on"
     return (f"config2: ScanNet-shaped 640x480 RGB-D, paper 4-level grid "
             f"(0.96/0.24/0.06/0.03 m + 0.03 m colour), pinned 7x7x3.25 m box, "
             f"{args.coarse}+3x12 samples/ray, smoothness {sm}")
@@ -295,6 +297,8 @@ def main():
                     help="2: ScanNet-shaped room (headline); 4: 10 m scene, 0.02 m grid (P = 1.7 B)")
     ap.add_argument("--coarse", type=int, default=96, help="coarse samples per ray (c5 sweep)")
     ap.add_argument("--no-smooth", action="store_true", help="lambda_smooth = 0 (c5 sweep)")
+    ap.add_argument("--refine-poses", action="store_true",
+                    help="pose refinement on (refine_poses=True, frame 0 frozen; not the headline)")
     ap.add_argument("--prefetch", action="store_true",
                     help="host draws on a background thread in the e2e leg")
     args = ap.parse_args()
@@ -318,6 +322,7 @@ def main():
     M = args.rays
     cfg = make_cfg(args.precision, batch=M * ws_, config=args.config, coarse=args.coarse,
                    smooth=not args.no_smooth)
+    cfg.refine_poses = bool(args.refine_poses)
     if args.config == 4:
         ds = scenes.config4(frames=args.frames, threads=min(8, os.cpu_count() or 1))
     else:

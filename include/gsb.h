@@ -119,6 +119,30 @@ typedef struct {
   const double* t_fixed;     /* (F, 3) translations of frozen frames (dtype-rounded), device */
 } gsb_pose_t;
 
+/* Analytic CSG scene (scenegen.AnalyticScene, gs/scenegen.py:41-155) flattened
+ * into a postfix program: op (0 PUSH prim k | 1 NEG | 2 MIN over the top n).
+ * prim row: type (0 sphere, 1 box), centre[3], radius | half[3], albedo[3],
+ * albedo2[3], checker (m, 0 = solid). */
+#define GSB_SCENE_MAX_PRIMS 16
+#define GSB_SCENE_MAX_OPS 32
+#define GSB_SCENE_MAX_STACK 8
+typedef struct {
+  int32_t n_prims, n_ops;
+  double prim[GSB_SCENE_MAX_PRIMS][16];
+  int32_t op[GSB_SCENE_MAX_OPS][2];
+  double light[3];       /* unit, from the light toward the scene */
+  double background[3];  /* RGB of rays that miss */
+} gsb_scene_t;
+
+/* Depth corruptions of scenegen.render_dataset (gs/scenegen.py:328-343). */
+typedef struct {
+  int32_t rect[4];       /* x0, y0, x1, y1 pixel rectangle zeroed in every frame (x1 <= x0: none) */
+  double world_c[3];     /* world-space ball ... */
+  double world_r;        /* ... of this radius (<= 0: none) */
+  int32_t has_box;       /* world-space box lo..hi */
+  double box_lo[3], box_hi[3];
+} gsb_render_opts_t;
+
 typedef struct {
   uint64_t state_hi, state_lo, inc_hi, inc_lo;  /* numpy PCG64 bit_generator state */
 } gsb_pcg64_t;
@@ -221,6 +245,19 @@ int gsb_pose_scratch_size(const gsb_model_t* model, int32_t n_rays, int32_t n_co
                           int32_t n_add, size_t* bytes);
 int gsb_pose_grad(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step_t* step,
                   const gsb_pose_t* pose, void* scratch, size_t scratch_bytes, void* stream);
+
+/* Synthetic RGB-D frames: scenegen._render_frame
+ * (gs/scenegen.py:290-325) for n_frames camera-to-world poses (device, (F, 16)
+ * row-major f64), one thread per pixel: pixel rays, sphere tracing (tol 1e-6,
+ * 256 steps, max_t), Lambert shading, optional Gaussian depth noise
+ * sigma0 z^2 with the caller's standard normals (device (F, H, W) f64, drawn
+ * from seeds.substream(seed, DEPTH_NOISE, f) on the host) and dropouts;
+ * writes u8 colours (F, H, W, 3) = round(255 c) and u16 depth (F, H, W) =
+ * round(1000 z) straight into the device dataset layout. */
+int gsb_render_frames(const gsb_scene_t* scene, const double* poses, int32_t n_frames, int32_t height,
+                      int32_t width, double fx, double fy, double cx, double cy, double max_t,
+                      const double* noise, double sigma0, const gsb_render_opts_t* opts, uint8_t* colors,
+                      uint16_t* depth_mm, void* stream);
 
 /* Dense Adam over the whole arena (gs/optimizer.py:38-55): per segment
  * learning rate; float64 register math; grads zeroed afterwards.  If

@@ -31,7 +31,7 @@ EXPORTS = (
     "gsb_sdf_workspace_size", "gsb_sdf_points", "gsb_sdf_fit_step", "gsb_smooth_points",
     "gsb_sdf_volume_workspace_size", "gsb_sdf_volume", "gsb_mc_workspace_size", "gsb_mc_count",
     "gsb_mc_emit", "gsb_nn_workspace_size", "gsb_nearest_neighbors", "gsb_raster_zbuffer",
-    "gsb_pose_table", "gsb_pose_scratch_size", "gsb_pose_grad",
+    "gsb_pose_table", "gsb_pose_scratch_size", "gsb_pose_grad", "gsb_render_frames",
 )
 REGIONS = ("parts", "counts", "status", "depths", "weights", "phi", "gphi", "color", "pbar",
            "ubar", "cbar", "ray_o", "ray_r", "ray_far")
@@ -56,6 +56,21 @@ class Dataset(C.Structure):
                 ("n_frames", C.c_int32), ("height", C.c_int32), ("width", C.c_int32),
                 ("fx", C.c_double), ("fy", C.c_double), ("cx", C.c_double), ("cy", C.c_double),
                 ("poses", C.c_void_p)]
+
+
+SCENE_MAX_PRIMS, SCENE_MAX_OPS, SCENE_MAX_STACK = 16, 32, 8
+
+
+class Scene(C.Structure):
+    _fields_ = [("n_prims", C.c_int32), ("n_ops", C.c_int32),
+                ("prim", (C.c_double * 16) * SCENE_MAX_PRIMS),
+                ("op", (C.c_int32 * 2) * SCENE_MAX_OPS),
+                ("light", C.c_double * 3), ("background", C.c_double * 3)]
+
+
+class RenderOpts(C.Structure):
+    _fields_ = [("rect", C.c_int32 * 4), ("world_c", C.c_double * 3), ("world_r", C.c_double),
+                ("has_box", C.c_int32), ("box_lo", C.c_double * 3), ("box_hi", C.c_double * 3)]
 
 
 class Pose(C.Structure):
@@ -123,6 +138,8 @@ def lib():
         "gsb_nearest_neighbors": ([P, I64, P, I64, P, D, I64, I64, I64, P, SZ, P, P, P], I32),
         "gsb_smooth_points": ([C.POINTER(Model), C.POINTER(Dataset), P, P, P, P, P, P, I32, D, P, P], I32),
         "gsb_sdf_points": ([C.POINTER(Model), P, I64, P, P, SZ, P], I32),
+        "gsb_render_frames": ([C.POINTER(Scene), P, I32, I32, I32, D, D, D, D, D, P, D,
+                               C.POINTER(RenderOpts), P, P, P], I32),
         "gsb_pose_table": ([C.POINTER(Model), C.POINTER(Pose), P, P, P], I32),
         "gsb_pose_scratch_size": ([C.POINTER(Model), I32, I32, I32, I32, C.POINTER(SZ)], I32),
         "gsb_pose_grad": ([C.POINTER(Model), C.POINTER(Dataset), C.POINTER(Step), C.POINTER(Pose), P, SZ,

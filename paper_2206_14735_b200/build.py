@@ -8,6 +8,7 @@ ctypes; it is built in-tree so it travels with the repo snapshot.
 
 from __future__ import annotations
 
+import glob
 import os
 import subprocess
 import sys
@@ -17,8 +18,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 SRC = os.path.join(CSRC, "gsb.cu")
 INST = os.path.join(CSRC, "gsb_step_inst.cu")
-DEPS = [os.path.join(CSRC, f) for f in ("gsb_common.cuh", "gsb_kernels.cuh", "gsb_host.cuh",
-                                        "gsb_step.cuh", "gsb_step_inst.cu")] + [
+DEPS = sorted(glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(CSRC, "*.cu"))) + [
     os.path.join(ROOT, "include", "gsb.h")]
 OUT = os.path.join(HERE, "_gsb.so")
 OBJDIR = os.path.join(ROOT, "build", "obj")

@@ -5,6 +5,7 @@
 
 #include "gsb_step.cuh"
 #include "gsb_mesh.cuh"
+#include "gsb_scene.cuh"
 
 #include <atomic>
 #include <cstring>
@@ -198,6 +199,40 @@ int gsb_sdf_points(const gsb_model_t* model, const void* points, int64_t n, void
     default:
       return GSB_E_ARG;
   }
+}
+
+int gsb_render_frames(const gsb_scene_t* scene, const double* poses, int32_t n_frames, int32_t height,
+                      int32_t width, double fx, double fy, double cx, double cy, double max_t,
+                      const double* noise, double sigma0, const gsb_render_opts_t* opts, uint8_t* colors,
+                      uint16_t* depth_mm, void* stream) {
+  if (!scene || !poses || !opts || !colors || !depth_mm || n_frames < 0 || height <= 0 || width <= 0)
+    return GSB_E_ARG;
+  if (scene->n_prims < 1 || scene->n_prims > GSB_SCENE_MAX_PRIMS || scene->n_ops < 1 ||
+      scene->n_ops > GSB_SCENE_MAX_OPS)
+    return GSB_E_ARG;
+  int sp = 0;  // validate the program: indices, stack depth, one result
+  for (int i = 0; i < scene->n_ops; ++i) {
+    const int op = scene->op[i][0], arg = scene->op[i][1];
+    if (op == 0) {
+      if (arg < 0 || arg >= scene->n_prims || ++sp > GSB_SCENE_MAX_STACK) return GSB_E_ARG;
+    } else if (op == 1) {
+      if (sp < 1) return GSB_E_ARG;
+    } else if (op == 2) {
+      if (arg < 1 || arg > sp) return GSB_E_ARG;
+      sp -= arg - 1;
+    } else {
+      return GSB_E_ARG;
+    }
+  }
+  if (sp != 1 || (sigma0 > 0.0 && !noise)) return GSB_E_ARG;
+  const int64_t n = (int64_t)n_frames * height * width;
+  if (n == 0) return GSB_OK;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  k_render_frames<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(*scene, poses, n, height, width, fx, fy, cx, cy,
+                                                              max_t, noise, sigma0, *opts, colors, depth_mm);
+  note_launch();
+  timing_point("k_render_frames", s);
+  return cudaGetLastError() == cudaSuccess ? GSB_OK : GSB_E_CUDA;
 }
 
 int gsb_pose_table(const gsb_model_t* model, const gsb_pose_t* pose, double* table, double* table_f64,
