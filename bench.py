@@ -347,10 +347,16 @@ def main():
             return eng.launch(cfg, d, ids, sm, **kw)
         return dp(cfg, d, ids, sm, **kw)
 
+    def adam_step():
+        opt.t = [t + 1 for t in opt.t]
+        if dp is None:
+            opt._launch()
+        else:
+            dp.adam(opt)  # sharded Adam + all-gather (parallel.py)
+
     def one_step(d, kw, ids, sm):
         w = objective(d, kw, ids, sm)
-        opt.t = [t + 1 for t in opt.t]
-        opt._launch()
+        adam_step()
         return w
 
     # ---- device-resident inputs for warmup + timed steps
@@ -385,8 +391,7 @@ def main():
         a.record()
         objective(*pre[W + k])
         b.record()
-        opt.t = [t + 1 for t in opt.t]
-        opt._launch()
+        adam_step()
         c.record()
         t_step.append((a, b))
         t_adam.append((b, c))

@@ -91,6 +91,7 @@ class ParamArena:
     """Parameters / gradients as single device buffers with named views."""
 
     ALIGN = 4  # elements; 16 B for float32 rows and vector Adam
+    TOTAL_ALIGN = 256
 
     def __init__(self, specs, dtype, device):
         """specs: list of (name, shape, group) with group in {"grid", "mlp", "log_s"}."""
@@ -112,7 +113,10 @@ class ParamArena:
             self.order.append(name)
             off += n
             prev_group = group
-        self.n = (off + self.ALIGN - 1) // self.ALIGN * self.ALIGN
+        # padded to a multiple of TOTAL_ALIGN so a data-parallel world of up
+        # to 64 ranks splits the arena into equal 16-byte-aligned shards
+        # (reduce-scatter / sharded Adam / all-gather, parallel.py)
+        self.n = (off + self.TOTAL_ALIGN - 1) // self.TOTAL_ALIGN * self.TOTAL_ALIGN
         tdt = _torch_dtype(dtype)
         self.params = torch.zeros(self.n, dtype=tdt, device=device)
         self.grads = torch.zeros(self.n, dtype=tdt, device=device)

@@ -92,20 +92,39 @@ class Adam:
             raise ValueError("too many learning-rate segments")
         return begins, lrs
 
-    def _launch(self, guard=None, guard_threshold=0.0, stream=None):
+    def _segments_in(self, lo, hi):
+        """The learning-rate runs of arena range [lo, hi), relative to lo."""
+        b, l = self._segments()
+        begins, lrs = [0], [0.0]
+        for x, lr in zip(b, l):
+            if x <= lo:
+                lrs[0] = lr
+            elif x < hi:
+                begins.append(x - lo)
+                lrs.append(lr)
+        return begins, lrs
+
+    def _launch(self, guard=None, guard_threshold=0.0, stream=None, lo=0, hi=None):
+        """One fused update of arena range [lo, hi) (default: all of it;
+        a data-parallel rank updates its own shard, parallel.py)."""
         ts = set(self.t)
         if len(ts) != 1:
             raise NotImplementedError("per-tensor step counts must agree for the fused update")
         t = float(self.t[0])
         c1 = 1.0 - self.beta1 ** t  # host pow == numba's libm pow (bit-exact)
         c2 = 1.0 - self.beta2 ** t
-        b, l = self._segments()
+        a = self.arena
+        hi = a.n if hi is None else int(hi)
+        lo = int(lo)
+        if lo % mdl.ParamArena.ALIGN or (hi - lo) % mdl.ParamArena.ALIGN or not 0 <= lo <= hi <= a.n:
+            raise ValueError("Adam range must be 16-byte aligned inside the arena")
+        b, l = self._segments_in(lo, hi) if (lo, hi) != (0, a.n) else self._segments()
         B = (C.c_int64 * len(b))(*b)
         Lr = (C.c_double * len(l))(*l)
-        a = self.arena
+        esz = a.params.element_size()
         _lib.check(_lib.lib().gsb_adam_step(
-            0 if a.dtype == np.float32 else 1, a.params.data_ptr(), a.grads.data_ptr(),
-            self.m_arena.data_ptr(), self.v_arena.data_ptr(), a.n, B, Lr, len(b),
+            0 if a.dtype == np.float32 else 1, a.params.data_ptr() + lo * esz, a.grads.data_ptr() + lo * esz,
+            self.m_arena.data_ptr() + lo * esz, self.v_arena.data_ptr() + lo * esz, hi - lo, B, Lr, len(b),
             self.beta1, self.beta2, self.eps, c1, c2,
             None if guard is None else guard.data_ptr(), float(guard_threshold),
             self.status.data_ptr(), _lib.stream_handle(stream)), "gsb_adam_step")
@@ -406,7 +425,10 @@ class Trainer:
         self.host_parts[slot].copy_(ws["parts"], non_blocking=True)
         self.events[slot].record()
         self.opt.t = [t + 1 for t in self.opt.t]
-        self.opt._launch(guard=ws["parts"], guard_threshold=self.cfg.divergence_threshold)
+        if self.dp is None:
+            self.opt._launch(guard=ws["parts"], guard_threshold=self.cfg.divergence_threshold)
+        else:
+            self.dp.adam(self.opt, guard=ws["parts"], guard_threshold=self.cfg.divergence_threshold)
         if self.engine.refine and (it + 1) % self.cfg.pose_refresh_every == 0:
             for p in self.model.poses:  # gs/optimizer.py:374-376
                 p.refresh()

@@ -9,8 +9,13 @@ points:
 1. after sampling (phase 1): all-reduce of the partition counts, because the
    depth and eikonal normalisers (n_valid, n_eik; gs/renderer.py:372-414)
    are global and n_eik depends on the sampled depths;
-2. after the backward (phase 2): all-reduce of the gradient arena (and of the
-   additive loss parts), then every rank runs the same Adam.
+2. after the backward (phase 2): the gradient arena is reduce-scattered
+   (each rank receives the global sum of its 1/N shard), every rank runs Adam
+   on its shard only, and the updated parameters are all-gathered -- the
+   wire bytes of one all-reduce, with Adam's HBM bytes divided by N (ZeRO-1;
+   Adam m / v are valid on the owning rank, ``gather_adam_state`` assembles
+   them for a checkpoint).  ``shard_adam=False`` keeps the all-reduce +
+   replicated Adam form.
 
 Rank 0 owns the smoothness points; every loss keeps its global normaliser
 (``m_global``, ``smooth_global``)."""
@@ -51,19 +56,72 @@ class DataParallelStep:
     ``model.arena.grads`` tensor); ``dist`` is ``torch.distributed`` with an
     initialised process group (NCCL on GPUs, gloo in the CPU tests)."""
 
-    def __init__(self, engine, dist, group=None):
+    def __init__(self, engine, dist, group=None, shard_adam=True):
         self.engine = engine
         self.dist = dist
         self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.nccl = dist.get_backend(group) == "nccl"
+        self.shard_adam = bool(shard_adam) and self.world > 1
+        self._inplace_ok = True  # NCCL in-place reduce-scatter / all-gather accepted
+
+    def shard(self, n):
+        """This rank's arena range [lo, hi) (n is a multiple of 4 x world)."""
+        chunk = n // self.world
+        if chunk * self.world != n or chunk % 4:
+            raise ValueError("arena length must split into equal 16-byte-aligned shards")
+        return self.rank * chunk, (self.rank + 1) * chunk
 
     def __call__(self, cfg, draws, ids, sm, **kw):
         eng = self.engine
         ws = eng.launch(cfg, draws, ids, sm, phases=1, **kw)
         self.dist.all_reduce(ws["counts"], group=self.group)            # exchange 1
         ws = eng.launch(cfg, draws, ids, sm, phases=2, fresh=False, **kw)
-        self.dist.all_reduce(eng.model.arena.grads, group=self.group)   # exchange 2
+        g = eng.model.arena.grads                                       # exchange 2
+        done = False
+        if self.shard_adam and self.nccl and self._inplace_ok:
+            lo, hi = self.shard(g.numel())
+            try:
+                self.dist.reduce_scatter_tensor(g[lo:hi], g, group=self.group)  # in place
+                done = True
+            except (RuntimeError, ValueError):  # argument check refused the aliasing
+                self._inplace_ok = False
+        if not done:  # gloo has no reduce-scatter: the sum everywhere, the shard is a slice
+            self.dist.all_reduce(g, group=self.group)
         parts = ws["parts"]
         s = parts[S_SLOT].clone()
         self.dist.all_reduce(parts, group=self.group)
         parts[S_SLOT] = s
         return ws
+
+    def adam(self, opt, **kw):
+        """The optimizer step after ``__call__``: sharded update + all-gather."""
+        if not self.shard_adam:
+            opt._launch(**kw)
+            return
+        a = opt.arena
+        lo, hi = self.shard(a.n)
+        opt._launch(lo=lo, hi=hi, **kw)       # zeroes grads[lo:hi]
+        a.grads[:lo].zero_()                  # partial sums of the other shards
+        a.grads[hi:].zero_()
+        self._all_gather(a.params, lo, hi)
+
+    def _all_gather(self, t, lo, hi):
+        if self.nccl and self._inplace_ok:
+            try:
+                self.dist.all_gather_into_tensor(t, t[lo:hi], group=self.group)  # in place
+                return
+            except (RuntimeError, ValueError):
+                self._inplace_ok = False
+        n = hi - lo
+        parts = [t[r * n:(r + 1) * n] for r in range(self.world)]
+        self.dist.all_gather(parts, t[lo:hi].clone(), group=self.group)
+
+    def gather_adam_state(self, opt):
+        """Assemble the full Adam m / v on every rank (e.g. before save_model)."""
+        if not self.shard_adam:
+            return
+        lo, hi = self.shard(opt.arena.n)
+        self._all_gather(opt.m_arena, lo, hi)
+        self._all_gather(opt.v_arena, lo, hi)

@@ -196,3 +196,171 @@ def test_data_parallel_device_step_world2_equals_unsharded(tmp_path):
     assert (z["counts"] == z["ref_counts"]).all()
     np.testing.assert_allclose(z["parts"], z["ref_parts"], rtol=1e-12, atol=1e-15)
     assert np.abs(z["got"] - z["ref"]).max() <= 1e-11 * np.abs(z["ref"]).max()
+
+
+class _FakeArena:
+    def __init__(self, torch, n):
+        self.n = n
+        self.params = torch.linspace(-1.0, 1.0, n, dtype=torch.float64)
+        self.grads = torch.zeros(n, dtype=torch.float64)
+
+
+class _TorchAdam:
+    """Adam restated in torch (gs/optimizer.py:38-55) over an arena range,
+    standing in for gsb_adam_step in the CPU choreography test."""
+
+    def __init__(self, torch, arena, lr=1e-2):
+        self.arena, self.lr, self.t = arena, lr, [0]
+        self.m_arena = torch.zeros_like(arena.params)
+        self.v_arena = torch.zeros_like(arena.params)
+
+    def _launch(self, lo=0, hi=None, **kw):
+        a = self.arena
+        hi = a.n if hi is None else hi
+        t = float(self.t[0])
+        g = a.grads[lo:hi]
+        m = self.m_arena[lo:hi]
+        v = self.v_arena[lo:hi]
+        m.mul_(0.9).add_(0.1 * g)
+        v.mul_(0.999).add_(0.001 * g * g)
+        a.params[lo:hi] -= self.lr * (m / (1 - 0.9 ** t)) / ((v / (1 - 0.999 ** t)).sqrt() + 1e-8)
+        g.zero_()
+
+
+class _FakeStepEngine:
+    def __init__(self, torch, arena, rank):
+        import types
+        self.torch, self.rank = torch, rank
+        self.model = types.SimpleNamespace(arena=arena)
+        self.ws = dict(counts=torch.zeros(4, dtype=torch.int64), parts=torch.zeros(8, dtype=torch.float64))
+
+    def launch(self, cfg, draws, ids, sm, phases=3, fresh=True, it=0, **kw):
+        if phases == 1:
+            self.ws["counts"][:] = self.torch.tensor([1, 2, 3, 4]) * (self.rank + 1)
+            return self.ws
+        a = self.model.arena
+        gen = self.torch.Generator().manual_seed(1000 * kw.get("step", 0) + self.rank)
+        a.grads += self.torch.randn(a.n, generator=gen, dtype=self.torch.float64)
+        self.ws["parts"][:] = float(self.rank + 1)
+        return self.ws
+
+
+def _shard_worker(rank, world, port, out, steps, n):
+    import torch
+    import torch.distributed as dist
+    from paper_2206_14735_b200.parallel import DataParallelStep
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    try:
+        arena = _FakeArena(torch, n)
+        opt = _TorchAdam(torch, arena)
+        dp = DataParallelStep(_FakeStepEngine(torch, arena, rank), dist)
+        assert dp.shard_adam
+        for k in range(steps):
+            ws = dp(None, None, None, None, step=k)
+            opt.t = [k + 1]
+            dp.adam(opt)
+            assert float(arena.grads.abs().max()) == 0.0
+        dp.gather_adam_state(opt)
+        if rank == 0:
+            np.savez(out, params=arena.params.numpy(), m=opt.m_arena.numpy(), v=opt.v_arena.numpy(),
+                     counts=ws["counts"].numpy(), parts=ws["parts"].numpy())
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_sharded_adam_gloo_world2_equals_replicated(tmp_path):
+    """reduce-scatter -> Adam on the rank's shard -> all-gather (parallel.py)
+    gives the replicated all-reduce + full Adam result, parameters and the
+    gathered moments alike (gloo: the reduce-scatter falls back to all-reduce)."""
+    import torch
+    import torch.multiprocessing as mp
+    out, steps, n, world = str(tmp_path / "shard.npz"), 3, 1024, 2
+    mp.spawn(_shard_worker, args=(world, _free_port(), out, steps, n), nprocs=world, join=True)
+    z = np.load(out)
+    arena = _FakeArena(torch, n)
+    opt = _TorchAdam(torch, arena)
+    for k in range(steps):
+        for r in range(world):
+            gen = torch.Generator().manual_seed(1000 * k + r)
+            arena.grads += torch.randn(n, generator=gen, dtype=torch.float64)
+        opt.t = [k + 1]
+        opt._launch()
+    np.testing.assert_allclose(z["params"], arena.params.numpy(), rtol=0, atol=1e-15)
+    np.testing.assert_allclose(z["m"], opt.m_arena.numpy(), rtol=0, atol=1e-15)
+    np.testing.assert_allclose(z["v"], opt.v_arena.numpy(), rtol=0, atol=1e-15)
+    assert list(z["counts"]) == [3, 6, 9, 12]
+    assert z["parts"][0] == 3.0 and z["parts"][7] == 1.0  # s slot is not summed
+
+
+def test_adam_segments_in_range():
+    """Learning-rate runs of a shard, relative to its start."""
+    from paper_2206_14735_b200.optimizer import Adam
+    a = Adam.__new__(Adam)
+    a._segments = lambda: ([0, 64, 128, 200], [0.01, 0.001, 0.0005, 0.0])
+    assert a._segments_in(0, 64) == ([0], [0.01])
+    assert a._segments_in(32, 160) == ([0, 32, 96], [0.01, 0.001, 0.0005])
+    assert a._segments_in(128, 256) == ([0, 72], [0.0005, 0.0])
+    assert a._segments_in(200, 256) == ([0], [0.0])
+
+
+def _gpu_adam_worker(rank, world, port, out):
+    """Two device steps + sharded gsb_adam_step on each rank (gloo collectives,
+    both ranks on the one GPU), against the 1-process step + full Adam."""
+    import torch
+    import torch.distributed as dist
+    from _golden import load
+    from paper_2206_14735_b200 import data, engine, optimizer
+    from paper_2206_14735_b200.parallel import DataParallelStep, shard_draws
+    from paper_2206_14735_b200.renderer import engine_for
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    try:
+        G = load("small", "double")
+        cfg = optimizer.TrainConfig(precision="double", **{
+            k: v for k, v in G.meta["cfg"].items() if k not in ("bounds", "voxel_sizes")},
+            voxel_sizes=G.cfg.voxel_sizes, bounds=G.cfg.bounds)
+        cfg.weights.smooth_count = G.meta["smooth_count"]
+        ds = data.Dataset(G.a["colors_u8"], G.a["depths_u16"], G.a["poses"], G.ds.intrinsics)
+        res = []
+        for sharded in (True, False):
+            model = optimizer.build_model(ds, cfg, skip_init=True, device=torch.device("cuda", 0))
+            opt = optimizer.make_optimizer(model, cfg)
+            eng = engine_for(model, ds)
+            dp = DataParallelStep(eng, dist) if sharded else None
+            for it in range(2):
+                full = engine.host_draws(model, ds, cfg, it)
+                if sharded:
+                    d, kw = shard_draws(full, rank, world)
+                    ids, sm = eng.upload(d)
+                    dp(cfg, d, ids, sm, **kw)
+                    opt.t = [t + 1 for t in opt.t]
+                    dp.adam(opt)
+                else:
+                    ids, sm = eng.upload(full)
+                    eng.launch(cfg, full, ids, sm)
+                    opt.t = [t + 1 for t in opt.t]
+                    opt._launch()
+            if sharded:
+                dp.gather_adam_state(opt)
+            torch.cuda.synchronize()
+            res.append((model.arena.params.cpu().numpy().copy(), opt.m_arena.cpu().numpy().copy()))
+        if rank == 0:
+            np.savez(out, p_sh=res[0][0], m_sh=res[0][1], p_1=res[1][0], m_1=res[1][1])
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.timeout(900)
+def test_sharded_adam_device_world2_equals_single(tmp_path):
+    import torch.multiprocessing as mp
+    out = str(tmp_path / "shadam.npz")
+    mp.spawn(_gpu_adam_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    z = np.load(out)
+    # sharded gradients are a float64 sum in another order: Adam amplifies
+    # last-bit differences of near-zero gradients only up to lr
+    assert np.abs(z["p_sh"] - z["p_1"]).max() <= 1e-9
+    assert np.abs(z["m_sh"] - z["m_1"]).max() <= 1e-9 * max(np.abs(z["m_1"]).max(), 1e-300)
