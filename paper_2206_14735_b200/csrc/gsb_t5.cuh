@@ -184,10 +184,12 @@ __global__ void __launch_bounds__(kTile) k_sdf_eval_t5(Ws<float> w, Geo G, int M
   const uint32_t w1h = smem_u32(sw + tc::UmmaW::W1H), w1l = smem_u32(sw + tc::UmmaW::W1L);
   uint32_t phase = 0;
   bool staged = false;
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  // one tile's lane-per-sample inputs: (ray, slot) and z at the sample point
+  auto gather = [&](int64_t tile, float (&z)[8 * KG], int& ray, int& slot, bool& act) {
     const int64_t s = tile * kTile + tid;
-    const bool act = s < total;
-    int ray = 0, slot = 0;
+    act = s < total;
+    ray = 0;
+    slot = 0;
     if (act) {
       if (list) {
         const int32_t e = list[s];
@@ -198,27 +200,29 @@ __global__ void __launch_bounds__(kTile) k_sdf_eval_t5(Ws<float> w, Geo G, int M
         slot = (int)((uint32_t)s % (uint32_t)Nc);
       }
     }
-    {
-      const double d = act ? dep[(int64_t)ray * w.ld + slot] : 0.0;
-      float p[3];
+    const double d = act ? dep[(int64_t)ray * w.ld + slot] : 0.0;
+    float p[3];
 #pragma unroll
-      for (int a = 0; a < 3; ++a) {
-        double x = w.od[ray * 3 + a] + d * w.rd[ray * 3 + a];
-        x = x >= G.lo[a] ? x : G.lo[a];
-        x = x <= G.hi[a] ? x : G.hi[a];
-        p[a] = (float)x;
-      }
-      float z[8 * KG];
-#pragma unroll
-      for (int i = S::IN_G; i < 8 * KG; ++i) z[i] = 0.f;
-#pragma unroll
-      for (int l = 0; l < S::NL; ++l) {
-        const Loc q = locate<false>(G.lv[l], (double)p[0], (double)p[1], (double)p[2],
-                                    act ? w.status : nullptr);
-        gather_fast<float, S::CG>(G.lv[l], compact<float>(q), z + l * S::CG);
-      }
-      store_a<KG>(tl, z);
+    for (int a = 0; a < 3; ++a) {
+      double x = w.od[ray * 3 + a] + d * w.rd[ray * 3 + a];
+      x = x >= G.lo[a] ? x : G.lo[a];
+      x = x <= G.hi[a] ? x : G.hi[a];
+      p[a] = (float)x;
     }
+#pragma unroll
+    for (int i = S::IN_G; i < 8 * KG; ++i) z[i] = 0.f;
+#pragma unroll
+    for (int l = 0; l < S::NL; ++l) {
+      const Loc q = locate<false>(G.lv[l], (double)p[0], (double)p[1], (double)p[2], act ? w.status : nullptr);
+      gather_fast<float, S::CG>(G.lv[l], compact<float>(q), z + l * S::CG);
+    }
+  };
+  float z[8 * KG];
+  int ray, slot;
+  bool act;
+  gather(blockIdx.x, z, ray, slot, act);
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    store_a<KG>(tl, z);
     cta_sync_tmem();
     if (!staged) {
       tc::mbar_wait(&s_bar[0], 0);
@@ -228,6 +232,10 @@ __global__ void __launch_bounds__(kTile) k_sdf_eval_t5(Ws<float> w, Geo G, int M
       issue_layer<KG>(tmem, w0h, w0l);
       commit(&s_bar[1]);
     }
+    // software pipeline: the next tile's gathers overlap this tile's MMAs
+    const int cur_ray = ray, cur_slot = slot;
+    const bool cur_act = act;
+    if (tile + gridDim.x < ntiles) gather(tile + gridDim.x, z, ray, slot, act);
     tc::mbar_wait(&s_bar[1], phase);
     phase ^= 1u;
     fence_after();
@@ -248,7 +256,7 @@ __global__ void __launch_bounds__(kTile) k_sdf_eval_t5(Ws<float> w, Geo G, int M
     float acc = svec[tc::GVec::b2];
 #pragma unroll
     for (int n = 0; n < 32; ++n) acc = fmaf(fmaxf(h[n] + svec[tc::GVec::b1 + n], 0.f), svec[tc::GVec::w2 + n], acc);
-    if (act) phi[(int64_t)ray * w.ld + slot] = (double)acc;
+    if (cur_act) phi[(int64_t)cur_ray * w.ld + cur_slot] = (double)acc;
   }
   fence_before();
   __syncthreads();
