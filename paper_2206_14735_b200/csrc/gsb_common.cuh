@@ -6,6 +6,7 @@
 // harmless (those values are only compared within tolerance).
 #pragma once
 
+#include "gsb_pcg_tables.cuh"
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -58,16 +59,17 @@ struct Pcg {
     state = ((u128)g.state_hi << 64) | (u128)g.state_lo;
     inc = ((u128)g.inc_hi << 64) | (u128)g.inc_lo;
   }
+  // jump ahead by delta draws: for each set bit k, state -> M_k state + inc P_k
+  // (gsb_pcg_tables.cuh; exact mod 2^128, equal to square-and-multiply)
   __device__ __forceinline__ void advance(uint64_t delta) {
-    u128 cur_mult = pcg_mult(), cur_plus = inc, acc_mult = 1, acc_plus = 0;
-    while (delta > 0) {
+    u128 acc_mult = 1, acc_plus = 0;
+    for (int k = 0; delta != 0; ++k, delta >>= 1) {
       if (delta & 1) {
-        acc_mult *= cur_mult;
-        acc_plus = acc_plus * cur_mult + cur_plus;
+        const u128 Mk = ((u128)kPcgMultPow[k][0] << 64) | (u128)kPcgMultPow[k][1];
+        const u128 Pk = ((u128)kPcgPlusPow[k][0] << 64) | (u128)kPcgPlusPow[k][1];
+        acc_mult *= Mk;
+        acc_plus = acc_plus * Mk + inc * Pk;
       }
-      cur_plus = (cur_mult + 1) * cur_plus;
-      cur_mult *= cur_mult;
-      delta >>= 1;
     }
     state = acc_mult * state + acc_plus;
   }
