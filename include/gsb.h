@@ -172,6 +172,11 @@ typedef struct {
   /* workspace (see gsb_step_workspace_size) */
   void* workspace;
   size_t workspace_bytes;
+  /* pose refinement: the gsb_pose_grad scratch (gsb_pose_scratch_size bytes),
+   * or NULL.  In float32 mode the step then also leaves each taped sample's
+   * dphi/dz and colour-input cotangent there for gsb_pose_grad. */
+  void* pose_work;
+  size_t pose_work_bytes;
 } gsb_step_t;
 
 int gsb_version(void);

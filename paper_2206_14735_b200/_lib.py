@@ -105,7 +105,8 @@ class Step(C.Structure):
                 ("smooth_pts", C.c_void_p), ("n_smooth", C.c_int32),
                 ("smooth_global", C.c_double),
                 ("exact_gather", C.c_int32), ("phases", C.c_int32),
-                ("workspace", C.c_void_p), ("workspace_bytes", C.c_size_t)]
+                ("workspace", C.c_void_p), ("workspace_bytes", C.c_size_t),
+                ("pose_work", C.c_void_p), ("pose_work_bytes", C.c_size_t)]
 
 
 class GsbError(RuntimeError):

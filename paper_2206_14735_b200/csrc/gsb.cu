@@ -255,7 +255,8 @@ int gsb_pose_scratch_size(const gsb_model_t* model, int32_t n_rays, int32_t n_co
                           int32_t n_add, size_t* bytes) {
   if (!model || !bytes || n_rays < 0) return GSB_E_ARG;
   const Sizes z = sizes_of(model, n_rays, n_coarse, n_rounds, n_add, 0);
-  *bytes = model->precision == 0 ? pose_scratch_bytes<float>(z) : pose_scratch_bytes<double>(z);
+  const int in_g = model->n_levels * model->levels[0].channels;
+  *bytes = model->precision == 0 ? pose_scratch_bytes<float>(z, in_g) : pose_scratch_bytes<double>(z, in_g);
   return GSB_OK;
 }
 

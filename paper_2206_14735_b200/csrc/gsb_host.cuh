@@ -56,6 +56,8 @@ Ws<T> carve(void* ws, const Sizes& z, size_t* bytes, int64_t* off_parts = nullpt
   Carver<T> c;
   c.base = reinterpret_cast<unsigned char*>(ws);
   Ws<T> w;
+  w.pose_g = nullptr;
+  w.pose_fb = nullptr;
   w.ld = z.ld;
   // small, externally visible blocks first
   size_t o_parts = c.off;

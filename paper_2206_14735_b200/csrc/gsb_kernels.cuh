@@ -54,6 +54,8 @@ struct Ws {
   double* smooth_part;  // [S]
   T* mlp_part;          // [nb_max][NMLP]
   uint4* wfrag;         // float32: per-lane tf32 hi/lo B fragments of the MLP (gsb_tc.cuh)
+  T* pose_g;            // pose refinement, float32: [MN][IN_G] dphi/dz (k_fwd_tc), or null
+  T* pose_fb;           // pose refinement, float32: [MN][12] colour-input cotangent (k_bwd_color_tc)
   double* fin_red;      // [FIN_SPLIT][NMLP] chunk totals of k_finalize_mlp2
   unsigned* fin_cnt;    // [ceil(NMLP/32)] tickets (self-resetting; zeroed per step)
   double* loss_red;     // [ceil(max(M, S) / 256)][8] block partials of k_finalize_loss

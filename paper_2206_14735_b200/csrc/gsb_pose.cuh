@@ -306,9 +306,76 @@ __global__ void __launch_bounds__(128) k_pose_xbar(Ws<T> w, Geo G, int M, int N,
   }
 }
 
-// warp per ray: rbar[ray] = (o_bar[3], r_bar[3]) in f64
+// float32 form: the step's k_fwd_tc left dphi/dz (w.pose_g) and k_bwd_color_tc
+// the colour-input cotangent (w.pose_fb: f_bar, then the view-direction
+// part); only the per-corner contractions remain (no MLP recomputation)
+template <class S>
+__global__ void __launch_bounds__(128) k_pose_fast(Ws<float> w, Geo G, int M, int N,
+                                                   const double* __restrict__ dep, float* __restrict__ xbar) {
+  const int64_t MN = (int64_t)M * N;
+  const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (s >= MN) return;
+  const int ray = (int)(s / N), j = (int)(s % N);
+  float p[3];
+  bool inside[3];
+  {
+    const float d = (float)dep[(int64_t)ray * w.ld + j];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      float x = w.o[ray * 3 + a] + d * w.r[ray * 3 + a];
+      const float l = (float)G.lo[a], h = (float)G.hi[a];
+      inside[a] = x >= l && x <= h;
+      x = x >= l ? x : l;
+      x = x <= h ? x : h;
+      p[a] = x;
+    }
+  }
+  const double pb = (double)w.pbar[s];
+  const double u[3] = {(double)w.ubar[s * 3], (double)w.ubar[s * 3 + 1], (double)w.ubar[s * 3 + 2]};
+  double xb[3] = {0.0, 0.0, 0.0};
+  const float* gz = w.pose_g + s * S::IN_G;
+#pragma unroll
+  for (int l = 0; l < S::NL; ++l) {
+    const LevelDev& L = G.lv[l];
+    const Loc q = locate<false>(L, (double)p[0], (double)p[1], (double)p[2], nullptr);
+    float g[S::CG];
+#pragma unroll
+    for (int c = 0; c < S::CG; ++c) g[c] = gz[l * S::CG + c];
+    double e[8], gr[3], h[3];
+    corner_contract<float, S::CG>(L, q.base, g, e);
+    corner_grad_hess(e, q.fx, q.fy, q.fz, gr, h);
+    const double iv = L.inv_vs, iv2 = 1.0 / (L.vs * L.vs);
+    xb[0] += gr[0] * iv * pb + (h[0] * u[1] + h[1] * u[2]) * iv2;
+    xb[1] += gr[1] * iv * pb + (h[0] * u[0] + h[2] * u[2]) * iv2;
+    xb[2] += gr[2] * iv * pb + (h[1] * u[0] + h[2] * u[1]) * iv2;
+  }
+  const float* fb = w.pose_fb + s * 12;
+  {
+    const Loc qc = locate<false>(G.col, (double)p[0], (double)p[1], (double)p[2], nullptr);
+    float f[S::CC];
+#pragma unroll
+    for (int c = 0; c < S::CC; ++c) f[c] = fb[c];
+    double e[8], gr[3], h[3];
+    corner_contract<float, S::CC>(G.col, qc.base, f, e);
+    corner_grad_hess(e, qc.fx, qc.fy, qc.fz, gr, h);
+#pragma unroll
+    for (int a = 0; a < 3; ++a) xb[a] += gr[a] * G.col.inv_vs;
+  }
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    xbar[s * 6 + a] = inside[a] ? (float)xb[a] : 0.f;
+    xbar[s * 6 + 3 + a] = fb[S::CC + a];
+  }
+}
+
+// warp per ray: o_bar = sum x_bar, r_bar = sum d x_bar + vdir_bar, then (lane 0)
+// R_bar = r_bar dir_cam^T (gs/renderer.py:307-309): rbar[ray] = (R_bar[9],
+// o_bar[3], frame) in f64, stride kRbar
+constexpr int kRbar = 16;
+
 template <typename T>
-__global__ void __launch_bounds__(128) k_pose_ray(Ws<T> w, int M, int N, const double* __restrict__ dep,
+__global__ void __launch_bounds__(128) k_pose_ray(Ws<T> w, gsb_dataset_t D, const int64_t* __restrict__ ids,
+                                                  int M, int N, const double* __restrict__ dep,
                                                   const T* __restrict__ xbar, double* __restrict__ rbar) {
   const int lane = threadIdx.x & 31;
   const int ray = blockIdx.x * 4 + (threadIdx.x >> 5);
@@ -329,39 +396,40 @@ __global__ void __launch_bounds__(128) k_pose_ray(Ws<T> w, int M, int N, const d
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v[i] += __shfl_xor_sync(0xffffffffu, v[i], o);
   }
-  if (lane == 0)
+  if (lane != 0) return;
+  const int64_t hw = (int64_t)D.height * D.width;
+  const int64_t flat = ids[ray];
+  const int64_t rem = flat % hw;
+  const int pv = (int)(rem / D.width), pu = (int)(rem % D.width);
+  // dir_cam (gs/camera.py:142-157) cast to the dtype (gs/renderer.py:308)
+  const double dx = ((double)pu - D.cx) / D.fx, dy = ((double)pv - D.cy) / D.fy;
+  const double nrm = sqrt((dx * dx + dy * dy) + 1.0);
+  const T dc[3] = {(T)(dx / nrm), (T)(dy / nrm), (T)(1.0 / nrm)};
+  double* o = rbar + (int64_t)ray * kRbar;
 #pragma unroll
-    for (int i = 0; i < 6; ++i) rbar[(int64_t)ray * 6 + i] = v[i];
+  for (int a = 0; a < 3; ++a) {
+#pragma unroll
+    for (int b = 0; b < 3; ++b) o[a * 3 + b] = v[3 + a] * (double)dc[b];
+    o[9 + a] = v[a];
+  }
+  o[12] = (double)(flat / hw);
 }
 
 // block per frame: R_bar, t_bar over the frame's rays, exp_so3 adjoint
 template <typename T>
-__global__ void __launch_bounds__(256) k_pose_frames(gsb_dataset_t D, const int64_t* __restrict__ ids, int M,
-                                                     gsb_pose_t P, const T* __restrict__ params,
+__global__ void __launch_bounds__(256) k_pose_frames(int M, gsb_pose_t P, const T* __restrict__ params,
                                                      const double* __restrict__ rbar, T* __restrict__ grads) {
   const int f = blockIdx.x;
   const int64_t no = P.nu_offset[f], to = P.t_offset[f];
   if (no < 0 && to < 0) return;
-  const int64_t hw = (int64_t)D.height * D.width;
   double acc[12];
 #pragma unroll
   for (int i = 0; i < 12; ++i) acc[i] = 0.0;
   for (int i = threadIdx.x; i < M; i += blockDim.x) {
-    const int64_t flat = ids[i];
-    if (flat / hw != f) continue;
-    const int64_t rem = flat % hw;
-    const int v = (int)(rem / D.width), u = (int)(rem % D.width);
-    // dir_cam (gs/camera.py:142-157) cast to the dtype (gs/renderer.py:308)
-    const double dx = ((double)u - D.cx) / D.fx, dy = ((double)v - D.cy) / D.fy;
-    const double nrm = sqrt((dx * dx + dy * dy) + 1.0);
-    const T dc[3] = {(T)(dx / nrm), (T)(dy / nrm), (T)(1.0 / nrm)};
+    const double* r = rbar + (int64_t)i * kRbar;
+    if ((int)r[12] != f) continue;
 #pragma unroll
-    for (int a = 0; a < 3; ++a) {
-      const double rb = rbar[(int64_t)i * 6 + 3 + a];
-#pragma unroll
-      for (int b = 0; b < 3; ++b) acc[a * 3 + b] += rb * (double)dc[b];
-      acc[9 + a] += rbar[(int64_t)i * 6 + a];
-    }
+    for (int k = 0; k < 12; ++k) acc[k] += r[k];
   }
   __shared__ double red[8][12];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -404,10 +472,31 @@ __global__ void __launch_bounds__(256) k_pose_frames(gsb_dataset_t D, const int6
 
 namespace host {
 
+// pose scratch: [xbar MN x 6 T][rbar M x kRbar f64] and, float32, the step's
+// per-sample [dphi/dz MN x IN_G][colour-input cotangent MN x 12]
+struct PoseLayout {
+  size_t xbar, rbar, g, fb, total;
+};
 template <typename T>
-inline size_t pose_scratch_bytes(const Sizes& z) {
-  const size_t a = ((size_t)z.MN * 6 * sizeof(T) + 255) / 256 * 256;
-  return a + (size_t)z.M * 6 * sizeof(double);
+inline PoseLayout pose_layout(const Sizes& z, int in_g) {
+  auto up = [](size_t x) { return (x + 255) / 256 * 256; };
+  PoseLayout L;
+  L.xbar = 0;
+  L.rbar = up((size_t)z.MN * 6 * sizeof(T));
+  size_t o = up(L.rbar + (size_t)z.M * kRbar * sizeof(double));
+  L.g = L.fb = 0;
+  if (sizeof(T) == 4) {
+    L.g = o;
+    o = up(o + (size_t)z.MN * in_g * 4);
+    L.fb = o;
+    o = up(o + (size_t)z.MN * 12 * 4);
+  }
+  L.total = o;
+  return L;
+}
+template <typename T>
+inline size_t pose_scratch_bytes(const Sizes& z, int in_g) {
+  return pose_layout<T>(z, in_g).total;
 }
 
 }  // namespace host

@@ -77,6 +77,13 @@ int run_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step
   constexpr int TW = 4;                  // warps per CTA of the float32 sample kernels
   const float* mlp32 = reinterpret_cast<const float*>(mlp);
   if constexpr (F32) {
+    if (st->pose_work) {  // pose refinement: keep dphi/dz and colour-input cotangents
+      const PoseLayout PL = pose_layout<T>(z, S::IN_G);
+      if (PL.total > st->pose_work_bytes) return GSB_E_ARG;
+      unsigned char* sc = reinterpret_cast<unsigned char*>(st->pose_work);
+      w.pose_g = reinterpret_cast<T*>(sc + PL.g);
+      w.pose_fb = reinterpret_cast<T*>(sc + PL.fb);
+    }
     static_assert(tc::kFragBufU4 == 4096 + 68 + 768, "workspace carve");
     tc::k_wfrag<S><<<tc::Fr<S>::NALL + 5, 32, 0, stream>>>(mlp32, w.wfrag);
     GSB_LAUNCHED_T("k_wfrag");
@@ -421,7 +428,8 @@ int run_pose_grad(const gsb_model_t* model, const gsb_dataset_t* data, const gsb
                   const gsb_pose_t* pose, void* scratch, size_t scratch_bytes, cudaStream_t stream) {
   if (S::NMLP != nmlp_of(model)) return GSB_E_ARG;
   const Sizes z = sizes_of(model, st->n_rays, st->n_coarse, st->n_rounds, st->n_add, st->n_smooth);
-  if (pose_scratch_bytes<T>(z) > scratch_bytes) return GSB_E_ARG;
+  const PoseLayout PL = pose_layout<T>(z, S::IN_G);
+  if (PL.total > scratch_bytes) return GSB_E_ARG;
   size_t need = 0;
   Ws<T> w = carve<T>(st->workspace, z, &need);
   if (need > st->workspace_bytes) return GSB_E_ARG;
@@ -430,18 +438,31 @@ int run_pose_grad(const gsb_model_t* model, const gsb_dataset_t* data, const gsb
   const T* params = reinterpret_cast<const T*>(model->params);
   T* grads = reinterpret_cast<T*>(model->grads);
   const double* dep = w.dep[st->n_rounds % 2];
-  T* xbar = reinterpret_cast<T*>(scratch);
-  double* rbar = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(scratch) +
-                                           ((size_t)z.MN * 6 * sizeof(T) + 255) / 256 * 256);
-  using R = FwdRow<T, S>;
-  const size_t smem = ((size_t)(S::NMLP + 3) / 4 * 4 + 128 * R::ROW) * sizeof(T);
-  GSB_CHECK(cudaFuncSetAttribute(k_pose_xbar<T, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k_pose_xbar<T, S><<<(int)((z.MN + 127) / 128), 128, smem, stream>>>(w, G, z.M, z.N, dep,
-                                                                      params + model->mlp_offset, xbar);
-  GSB_LAUNCHED_T("k_pose_xbar");
-  k_pose_ray<T><<<(z.M + 3) / 4, 128, 0, stream>>>(w, z.M, z.N, dep, xbar, rbar);
+  unsigned char* sc = reinterpret_cast<unsigned char*>(scratch);
+  T* xbar = reinterpret_cast<T*>(sc + PL.xbar);
+  double* rbar = reinterpret_cast<double*>(sc + PL.rbar);
+  bool fast = false;
+  if constexpr (sizeof(T) == 4) {
+    // the step stored dphi/dz and the colour-input cotangents in this scratch
+    fast = st->pose_work == scratch;
+    if (fast) {
+      w.pose_g = reinterpret_cast<T*>(sc + PL.g);
+      w.pose_fb = reinterpret_cast<T*>(sc + PL.fb);
+      k_pose_fast<S><<<(int)((z.MN + 127) / 128), 128, 0, stream>>>(w, G, z.M, z.N, dep, xbar);
+      GSB_LAUNCHED_T("k_pose_fast");
+    }
+  }
+  if (!fast) {
+    using R = FwdRow<T, S>;
+    const size_t smem = ((size_t)(S::NMLP + 3) / 4 * 4 + 128 * R::ROW) * sizeof(T);
+    GSB_CHECK(cudaFuncSetAttribute(k_pose_xbar<T, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_pose_xbar<T, S><<<(int)((z.MN + 127) / 128), 128, smem, stream>>>(w, G, z.M, z.N, dep,
+                                                                        params + model->mlp_offset, xbar);
+    GSB_LAUNCHED_T("k_pose_xbar");
+  }
+  k_pose_ray<T><<<(z.M + 3) / 4, 128, 0, stream>>>(w, *data, st->ray_ids, z.M, z.N, dep, xbar, rbar);
   GSB_LAUNCHED_T("k_pose_ray");
-  k_pose_frames<T><<<pose->n_frames, 256, 0, stream>>>(*data, st->ray_ids, z.M, *pose, params, rbar, grads);
+  k_pose_frames<T><<<pose->n_frames, 256, 0, stream>>>(z.M, *pose, params, rbar, grads);
   GSB_LAUNCHED_T("k_pose_frames");
   return GSB_OK;
 }

@@ -716,6 +716,10 @@ __global__ void __launch_bounds__(WARPS * 32) k_fwd_tc(Ws<float> w, Geo G, int M
   if (ray >= 0) {
 #pragma unroll
     for (int c = 0; c < 3; ++c) w.scol[s * 3 + c] = my[K::oY + c];
+    if (w.pose_g) {  // pose refinement: keep dphi/dz for gsb_pose_grad (gsb_pose.cuh)
+#pragma unroll
+      for (int i = 0; i < S::IN_G; ++i) w.pose_g[s * S::IN_G + i] = my[K::oZ + i];
+    }
   }
 }
 
@@ -1156,6 +1160,19 @@ __global__ void __launch_bounds__(WARPS * 32, 2) k_bwd_color_tc(Ws<float> w, Geo
     float wk[8];
     corner_w(q, wk);
     scatter_level<float, S::CC>(G.col, q, myrow + K::oFB, wk, active, false);
+  }
+  if (w.pose_fb && active) {  // pose refinement: f_bar and the view-direction cotangent
+    float* o = w.pose_fb + s * 12;
+#pragma unroll
+    for (int c = 0; c < S::CC; ++c) o[c] = myrow[K::oFB + c];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {  // (a0_bar W0c^T) at the view-direction inputs
+      const float* wr = mlp + S::oCW0 + (S::CC + a) * GSB_HID;
+      float acc = 0.f;
+#pragma unroll
+      for (int jj = 0; jj < GSB_HID; ++jj) acc = fmaf(myrow[K::oB0 + jj], __ldg(wr + jj), acc);
+      o[S::CC + a] = acc;
+    }
   }
   // ---- outer products over the warp's samples: e0 = [inp,1]^T a0b, e1 = h0c^T a1b
   float w2c[4][3];  // W2c rows n = 8nt + g

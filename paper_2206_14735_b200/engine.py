@@ -379,6 +379,9 @@ class StepEngine:
             ws["status"].zero_()
         st = self.step_struct(cfg, draws, ray_ids_dev, smooth_dev, ws, **kw)
         phases = kw.get("phases", 3)
+        if self.refine:
+            buf = self._pose_scratch(cfg, M)
+            st.pose_work, st.pose_work_bytes = buf.data_ptr(), buf.numel()
         if fresh and phases & 1:
             self.pose_tables(stream)
         _lib.check(self.lib.gsb_train_step(C.byref(self.mstruct), C.byref(self.dstruct),
@@ -390,7 +393,7 @@ class StepEngine:
                 self._pose_grad(cfg, st, M, stream)
         return ws
 
-    def _pose_grad(self, cfg, st, M, stream):
+    def _pose_scratch(self, cfg, M):
         key = ("pose", M, cfg.coarse_samples, cfg.importance_rounds, cfg.importance_add)
         if key not in self._ws:
             nbytes = C.c_size_t(0)
@@ -399,7 +402,10 @@ class StepEngine:
                                                       C.byref(nbytes)), "pose scratch size")
             self._ws[key] = self.torch.empty(max(int(nbytes.value), 1), dtype=self.torch.uint8,
                                              device=self.device)
-        buf = self._ws[key]
+        return self._ws[key]
+
+    def _pose_grad(self, cfg, st, M, stream):
+        buf = self._pose_scratch(cfg, M)
         _lib.check(self.lib.gsb_pose_grad(C.byref(self.mstruct), C.byref(self.dstruct), C.byref(st),
                                           C.byref(self.pstruct), buf.data_ptr(), buf.numel(),
                                           _lib.stream_handle(stream)), "gsb_pose_grad")
