@@ -310,12 +310,19 @@ def main():
     from paper_2206_14735_b200.renderer import engine_for
 
     ws_, rank, local = dist_env()
+    local = local % max(torch.cuda.device_count(), 1)  # (functional smoke runs may share a GPU)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     pg = None
     if ws_ > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        # GSB_DIST_BACKEND=gloo only for functional smoke runs of the N > 1 path
+        # on fewer GPUs than ranks (host collectives; not a measurement)
+        backend = os.environ.get("GSB_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
         pg = dist
     W = max(args.warmup, 3)
     K = args.steps
