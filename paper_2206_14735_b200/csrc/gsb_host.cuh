@@ -56,6 +56,7 @@ Ws<T> carve(void* ws, const Sizes& z, size_t* bytes, int64_t* off_parts = nullpt
   Carver<T> c;
   c.base = reinterpret_cast<unsigned char*>(ws);
   Ws<T> w;
+  w.mlp_slots = 0;
   w.pose_g = nullptr;
   w.pose_fb = nullptr;
   w.ld = z.ld;

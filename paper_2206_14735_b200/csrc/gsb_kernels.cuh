@@ -54,6 +54,7 @@ struct Ws {
   double* smooth_part;  // [S]
   T* mlp_part;          // [nb_max][NMLP]
   uint4* wfrag;         // float32: per-lane tf32 hi/lo B fragments of the MLP (gsb_tc.cuh)
+  int mlp_slots;        // float32 taped backward: >0 = CTAs red.add into slot blockIdx % mlp_slots
   T* pose_g;            // pose refinement, float32: [MN][IN_G] dphi/dz (k_fwd_tc), or null
   T* pose_fb;           // pose refinement, float32: [MN][12] colour-input cotangent (k_bwd_color_tc)
   double* fin_red;      // [FIN_SPLIT][NMLP] chunk totals of k_finalize_mlp2

@@ -203,11 +203,18 @@ int run_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_g));
       GSB_CHECK(cudaFuncSetAttribute(tc::k_bwd_color_tc<S, WCOL>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_c));
+      // MLP partials: red.add into kMlpSlots L2-resident rows instead of one row per CTA
+      constexpr int kMlpSlots = 64;
+      static_assert(kMlpSlots <= kNbMax, "workspace carve");
+      w.mlp_slots = kMlpSlots;
+      GSB_CHECK(cudaMemsetAsync(w.mlp_part, 0, (size_t)kMlpSlots * S::NMLP * sizeof(T), stream));
       tc::k_bwd_geom_tc<S, WGEO><<<nb_geo, WGEO * 32, smem_g, stream>>>(w, G, M, N, mlp32,
                                                                         dep_final, spts, nsp, 2);
       GSB_LAUNCHED_T("k_bwd_geom");
       tc::k_bwd_color_tc<S, WCOL><<<nb_col, WCOL * 32, smem_c, stream>>>(w, G, M, N, mlp32, dep_final);
       GSB_LAUNCHED_T("k_bwd_color");
+      nb_geo = std::min(nb_geo, kMlpSlots);
+      nb_col = std::min(nb_col, kMlpSlots);
     } else {
       constexpr int CW = S::NMLP - S::oCW0;
       size_t smem_g = ((size_t)(S::NG + 3) / 4 * 4 + (size_t)WG * 32 * GeoRow<T, S>::ROW) * esz;

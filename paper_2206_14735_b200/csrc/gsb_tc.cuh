@@ -989,12 +989,16 @@ __global__ void __launch_bounds__(WARPS * 32) k_bwd_geom_tc(Ws<float> w, Geo G, 
     if (lane == 0) mine[S::oGb2] = accp;
   }
   __syncthreads();
-  float* out = w.mlp_part + (size_t)blockIdx.x * S::NMLP;
+  const int slot = w.mlp_slots > 0 ? (int)(blockIdx.x % (unsigned)w.mlp_slots) : (int)blockIdx.x;
+  float* out = w.mlp_part + (size_t)slot * S::NMLP;
   for (int i = threadIdx.x; i < NGP; i += WARPS * 32) {
     float a = 0.f;
 #pragma unroll
     for (int k = 0; k < WARPS; ++k) a += red[(size_t)k * NGP + i];
-    out[i] = a;
+    if (w.mlp_slots > 0)
+      atomicAdd(out + i, a);  // few L2-resident slots instead of one partial row per CTA
+    else
+      out[i] = a;
   }
 }
 
@@ -1245,12 +1249,16 @@ __global__ void __launch_bounds__(WARPS * 32, 2) k_bwd_color_tc(Ws<float> w, Geo
     }
   }
   __syncthreads();
-  float* out = w.mlp_part + (size_t)blockIdx.x * S::NMLP + S::NG;
+  const int slot = w.mlp_slots > 0 ? (int)(blockIdx.x % (unsigned)w.mlp_slots) : (int)blockIdx.x;
+  float* out = w.mlp_part + (size_t)slot * S::NMLP + S::NG;
   for (int i = threadIdx.x; i < NCP; i += WARPS * 32) {
     float a = 0.f;
 #pragma unroll
     for (int k = 0; k < WARPS; ++k) a += red[(size_t)k * NCP + i];
-    out[i] = a;
+    if (w.mlp_slots > 0)
+      atomicAdd(out + i, a);
+    else
+      out[i] = a;
   }
 }
 
