@@ -178,14 +178,17 @@ def workload_name(args, N):
             f"{args.coarse}+3x12 samples/ray, smoothness {sm}")
 
 
-def traffic_of(kernel):
+def traffic_of(kernel, workload):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel` from
-    the committed ncu --set full summary (profiles/traffic.json), else None."""
+    the committed ncu --set full summary (profiles/traffic.json) of the same
+    workload (its "workload" key), else None."""
     p = os.path.join(ROOT, "profiles", "traffic.json")
     if not os.path.exists(p):
         return None
     with open(p) as f:
         d = json.load(f)
+    if d.get("workload") != workload:
+        return None
     for k, v in d.get("kernels", {}).items():
         if k.startswith(kernel):
             return v
@@ -472,7 +475,7 @@ def main():
                 "step_hbm_frac": B / (ms_step / 1e3) / 1e9 / peak,
                 "objective_ms": obj_ms, "adam_ms": adam_ms,
                 "kernels": table}
-    tr = traffic_of(dom["kernel"])
+    tr = traffic_of(dom["kernel"], f"config{args.config}" + ("-pose" if args.refine_poses else ""))
     if tr is not None:
         roofline["traffic"] = tr
     cpu = None
