@@ -27,14 +27,17 @@
 
 namespace gsb {
 
-// GSB_T5=0 selects the mma.sync form of the no-grad SDF kernel (A/B runs)
-inline bool use_t5() {
+// no-grad SDF kernel form (A/B runs): GSB_T5=0 mma.sync everywhere, 1 tcgen05
+// everywhere, 2 (default, measured best) tcgen05 for the coarse pass (590 k samples,
+// ~10 tiles per persistent CTA) and mma.sync for the 74 k-sample importance passes
+inline int t5_mode() {
   static const int v = [] {
     const char* e = std::getenv("GSB_T5");
-    return e ? std::atoi(e) : 1;
+    return e ? std::atoi(e) : 2;
   }();
-  return v != 0;
+  return v;
 }
+inline bool use_t5(bool coarse = true) { return t5_mode() == 1 || (t5_mode() == 2 && coarse); }
 inline int sm_count() {
   static const int v = [] {
     int dev = 0, n = 0;
@@ -130,7 +133,7 @@ int run_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step
           int64_t cap = (int64_t)M * A;
           int b2 = (int)((cap + 127) / 128);
           if constexpr (F32) {
-            if (use_t5())
+            if (use_t5(false))
               GSB_CHECK(launch_sdf_t5<S>(w, G, M, Nc, w.dep[1 - cur], w.phi[1 - cur], w.evl, w.evl_count,
                                          cap, stream));
             else
