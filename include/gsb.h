@@ -177,6 +177,13 @@ typedef struct {
    * dphi/dz and colour-input cotangent there for gsb_pose_grad. */
   void* pose_work;
   size_t pose_work_bytes;
+  /* deterministic scatter mode (validation): gsb_det_scratch_size bytes, or
+   * NULL.  The grid-gradient scatters then record (row, value) entries that
+   * are stably sorted by row and summed in sample order, so the gradients are
+   * bit-reproducible run to run (the default mode uses warp-aggregated
+   * atomics).  MLP partials are then per-CTA rows reduced in a fixed order. */
+  void* det_work;
+  size_t det_work_bytes;
 } gsb_step_t;
 
 int gsb_version(void);
@@ -244,6 +251,8 @@ int gsb_train_step(const gsb_model_t* model, const gsb_dataset_t* data, const gs
  *   grad-phi Hessian block, colour; gs/diffcore.py:893-991), the clip mask,
  *   x = o + d r, r = R dir_cam per frame, and the exp_so3 adjoint.  Scratch:
  *   gsb_pose_scratch_size bytes. */
+int gsb_det_scratch_size(const gsb_model_t* model, int32_t n_rays, int32_t n_coarse, int32_t n_rounds,
+                         int32_t n_add, int32_t n_smooth, size_t* bytes);
 int gsb_pose_table(const gsb_model_t* model, const gsb_pose_t* pose, double* table, double* table_f64,
                    void* stream);
 int gsb_pose_scratch_size(const gsb_model_t* model, int32_t n_rays, int32_t n_coarse, int32_t n_rounds,

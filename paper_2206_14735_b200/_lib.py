@@ -31,7 +31,7 @@ EXPORTS = (
     "gsb_sdf_workspace_size", "gsb_sdf_points", "gsb_sdf_fit_step", "gsb_smooth_points",
     "gsb_sdf_volume_workspace_size", "gsb_sdf_volume", "gsb_mc_workspace_size", "gsb_mc_count",
     "gsb_mc_emit", "gsb_nn_workspace_size", "gsb_nearest_neighbors", "gsb_raster_zbuffer",
-    "gsb_pose_table", "gsb_pose_scratch_size", "gsb_pose_grad", "gsb_render_frames",
+    "gsb_pose_table", "gsb_pose_scratch_size", "gsb_pose_grad", "gsb_render_frames", "gsb_det_scratch_size",
 )
 REGIONS = ("parts", "counts", "status", "depths", "weights", "phi", "gphi", "color", "pbar",
            "ubar", "cbar", "ray_o", "ray_r", "ray_far")
@@ -106,7 +106,8 @@ class Step(C.Structure):
                 ("smooth_global", C.c_double),
                 ("exact_gather", C.c_int32), ("phases", C.c_int32),
                 ("workspace", C.c_void_p), ("workspace_bytes", C.c_size_t),
-                ("pose_work", C.c_void_p), ("pose_work_bytes", C.c_size_t)]
+                ("pose_work", C.c_void_p), ("pose_work_bytes", C.c_size_t),
+                ("det_work", C.c_void_p), ("det_work_bytes", C.c_size_t)]
 
 
 class GsbError(RuntimeError):
@@ -141,6 +142,7 @@ def lib():
         "gsb_sdf_points": ([C.POINTER(Model), P, I64, P, P, SZ, P], I32),
         "gsb_render_frames": ([C.POINTER(Scene), P, I32, I32, I32, D, D, D, D, D, P, D,
                                C.POINTER(RenderOpts), P, P, P], I32),
+        "gsb_det_scratch_size": ([C.POINTER(Model), I32, I32, I32, I32, I32, C.POINTER(SZ)], I32),
         "gsb_pose_table": ([C.POINTER(Model), C.POINTER(Pose), P, P, P], I32),
         "gsb_pose_scratch_size": ([C.POINTER(Model), I32, I32, I32, I32, C.POINTER(SZ)], I32),
         "gsb_pose_grad": ([C.POINTER(Model), C.POINTER(Dataset), C.POINTER(Step), C.POINTER(Pose), P, SZ,

@@ -251,6 +251,15 @@ int gsb_pose_table(const gsb_model_t* model, const gsb_pose_t* pose, double* tab
   return cudaGetLastError() == cudaSuccess ? GSB_OK : GSB_E_CUDA;
 }
 
+int gsb_det_scratch_size(const gsb_model_t* model, int32_t n_rays, int32_t n_coarse, int32_t n_rounds,
+                         int32_t n_add, int32_t n_smooth, size_t* bytes) {
+  if (!model || !bytes || n_rays < 0) return GSB_E_ARG;
+  const Sizes z = sizes_of(model, n_rays, n_coarse, n_rounds, n_add, n_smooth);
+  *bytes = model->precision == 0 ? det_layout<float>(z, model->n_levels).total
+                                 : det_layout<double>(z, model->n_levels).total;
+  return GSB_OK;
+}
+
 int gsb_pose_scratch_size(const gsb_model_t* model, int32_t n_rays, int32_t n_coarse, int32_t n_rounds,
                           int32_t n_add, size_t* bytes) {
   if (!model || !bytes || n_rays < 0) return GSB_E_ARG;

@@ -55,6 +55,8 @@ struct Ws {
   T* mlp_part;          // [nb_max][NMLP]
   uint4* wfrag;         // float32: per-lane tf32 hi/lo B fragments of the MLP (gsb_tc.cuh)
   int mlp_slots;        // float32 taped backward: >0 = CTAs red.add into slot blockIdx % mlp_slots
+  uint64_t* det_keys;   // deterministic scatter mode: [NS][NL+1][8] grad-row addresses, or null
+  T* det_vals;          // ... and their [8] values (C used); reduced in sample order (k_det_reduce)
   T* pose_g;            // pose refinement, float32: [MN][IN_G] dphi/dz (k_fwd_tc), or null
   T* pose_fb;           // pose refinement, float32: [MN][12] colour-input cotangent (k_bwd_color_tc)
   double* fin_red;      // [FIN_SPLIT][NMLP] chunk totals of k_finalize_mlp2
@@ -1071,9 +1073,32 @@ struct GeoRow {
 // form contiguous runs; each run is summed with a segmented shuffle scan and
 // its first lane issues one vector red per corner.  Inactive lanes form
 // their own (empty) runs.
+// Deterministic mode: entry slot (sample, level) records its 8 corner rows
+// (address key + C values); k_det_reduce sums each row's entries in slot
+// order after a stable sort, so the result does not depend on scheduling.
+template <typename T, int C>
+__device__ __forceinline__ void det_put(uint64_t* keys, T* vals, int64_t slot, const LevelDev& L,
+                                        int64_t base, const T* gl, const T (&coef)[8], bool active) {
+  if (!active) return;  // unused slots keep the ~0 key they were initialised with
+  T* Gp = reinterpret_cast<T*>(L.grad) + base * C;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int64_t e = slot * 8 + k;
+    keys[e] = (uint64_t)(uintptr_t)(Gp + corner_off(L, k) * C);
+#pragma unroll
+    for (int c = 0; c < C; ++c) vals[e * 8 + c] = gl[c] * coef[k];
+  }
+}
+
 template <typename T, int C>
 __device__ __forceinline__ void scatter_level(const LevelDev& L, const LocT<T>& q, const T* gl,
-                                              const T (&coef)[8], bool active, bool /*unused*/) {
+                                              const T (&coef)[8], bool active, bool /*unused*/,
+                                              uint64_t* dkeys = nullptr, T* dvals = nullptr,
+                                              int64_t dslot = 0) {
+  if (dkeys) {
+    det_put<T, C>(dkeys, dvals, dslot, L, (int64_t)q.base, gl, coef, active);
+    return;
+  }
   const unsigned full = 0xffffffffu;
   const int lane = threadIdx.x & 31;
   const int key = active ? q.base : (-2 - lane);
@@ -1282,7 +1307,8 @@ __global__ void __launch_bounds__(WARPS * 32) k_bwd_geom(Ws<T> w, Geo G, int M, 
       corner_w_ju(loc[l], (T)G.lv[l].inv_vs, u, wk, ju);
 #pragma unroll
       for (int k = 0; k < 8; ++k) coef[k] = fma(p, wk[k], ju[k]);
-      scatter_level<T, S::CG>(G.lv[l], loc[l], gz + l * S::CG, coef, active, l < agg_levels);
+      scatter_level<T, S::CG>(G.lv[l], loc[l], gz + l * S::CG, coef, active, l < agg_levels, w.det_keys,
+                              w.det_vals, s * (S::NL + 1) + l);
     }
     // ---- A0 = [p z + v, p]; q0 = (v W0) (.) m0; A1 = [p h0 + q0, p]; V2 += dd1 (.) m1
     {
@@ -1474,13 +1500,18 @@ __global__ void __launch_bounds__(WARPS * 32) k_bwd_color(Ws<T> w, Geo G, int M,
       // colour grid scatter: theta_c[idx_k] += w_k f_bar
       T wk[8];
       corner_w(q, wk);
-      T* Gp = reinterpret_cast<T*>(G.col.grad) + (int64_t)q.base * S::CC;
+      if (w.det_keys) {
+        det_put<T, S::CC>(w.det_keys, w.det_vals, s * (S::NL + 1) + S::NL, G.col, (int64_t)q.base, fb, wk,
+                          true);
+      } else {
+        T* Gp = reinterpret_cast<T*>(G.col.grad) + (int64_t)q.base * S::CC;
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        T vv[S::CC];
+        for (int k = 0; k < 8; ++k) {
+          T vv[S::CC];
 #pragma unroll
-        for (int c = 0; c < S::CC; ++c) vv[c] = wk[k] * fb[c];
-        red_row<T, S::CC>(Gp + corner_off(G.col, k) * S::CC, vv);
+          for (int c = 0; c < S::CC; ++c) vv[c] = wk[k] * fb[c];
+          red_row<T, S::CC>(Gp + corner_off(G.col, k) * S::CC, vv);
+        }
       }
     } else {
 #pragma unroll 1
@@ -1806,6 +1837,36 @@ __global__ void __launch_bounds__(256) k_adam(T* __restrict__ P, T* __restrict__
   }
   bad = warp_sum(bad);
   if ((threadIdx.x & 31) == 0 && bad) atomicAdd(status + GSB_ST_ADAM_BAD, bad);
+}
+
+// ---------------------------------------------------------------------------
+// deterministic scatter mode: sum each grad row's entries in (sample, level,
+// corner) order -- the entries were stably sorted by row address
+
+static __global__ void k_det_iota(int32_t* idx, int64_t n) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) idx[i] = (int32_t)i;
+}
+
+template <typename T>
+__global__ void k_det_reduce(const uint64_t* __restrict__ keys, const int32_t* __restrict__ order,
+                             const T* __restrict__ vals, int64_t n, int C_geo, int C_col,
+                             uintptr_t col_lo, uintptr_t col_hi) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint64_t key = keys[i];
+  if (key == ~0ull || (i > 0 && keys[i - 1] == key)) return;  // run heads only
+  const int C = (key >= col_lo && key < col_hi) ? C_col : C_geo;
+  T acc[8];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) acc[c] = T(0);
+  for (int64_t j = i; j < n && keys[j] == key; ++j) {
+    const T* v = vals + (int64_t)order[j] * 8;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) acc[c] += v[c];
+  }
+  T* row = reinterpret_cast<T*>((uintptr_t)key);
+  for (int c = 0; c < C; ++c) row[c] += acc[c];
 }
 
 }  // namespace gsb

@@ -6,6 +6,8 @@
 #include "gsb_t5.cuh"
 #include "gsb_pose.cuh"
 
+#include <cub/cub.cuh>
+
 #include <cstdlib>
 
 #define GSB_CHECK(x)                           \
@@ -47,6 +49,36 @@ inline int sm_count() {
   }();
   return v;
 }
+// deterministic scatter scratch: entries (sample slot, level, corner)
+struct DetLayout {
+  int64_t n;
+  size_t keys_in, keys_out, idx_in, idx_out, vals, temp, temp_bytes, total;
+};
+template <typename T>
+inline DetLayout det_layout(const host::Sizes& z, int nl) {
+  auto up = [](size_t x) { return (x + 255) / 256 * 256; };
+  DetLayout L;
+  L.n = ((int64_t)z.NS + 64) * (nl + 1) * 8;
+  size_t o = 0;
+  L.keys_in = o;
+  o = up(o + (size_t)L.n * 8);
+  L.keys_out = o;
+  o = up(o + (size_t)L.n * 8);
+  L.idx_in = o;
+  o = up(o + (size_t)L.n * 4);
+  L.idx_out = o;
+  o = up(o + (size_t)L.n * 4);
+  L.vals = o;
+  o = up(o + (size_t)L.n * 8 * sizeof(T));
+  L.temp_bytes = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, L.temp_bytes, (const uint64_t*)nullptr, (uint64_t*)nullptr,
+                                  (const int32_t*)nullptr, (int32_t*)nullptr, (int)L.n);
+  L.temp = o;
+  o = up(o + L.temp_bytes);
+  L.total = o;
+  return L;
+}
+
 // persistent tcgen05 SDF evaluation over `cap` (upper bound of) samples
 template <class S>
 inline cudaError_t launch_sdf_t5(Ws<float> w, Geo G, int M, int Nc, const double* dep, double* phi,
@@ -79,6 +111,14 @@ int run_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step
   constexpr bool F32 = sizeof(T) == 4;  // float32: decoders on the tensor cores (gsb_tc.cuh)
   constexpr int TW = 4;                  // warps per CTA of the float32 sample kernels
   const float* mlp32 = reinterpret_cast<const float*>(mlp);
+  DetLayout DL{};
+  if (st->det_work && (st->phases & 2)) {  // deterministic scatter: entries instead of atomics
+    DL = det_layout<T>(z, S::NL);
+    if (DL.total > st->det_work_bytes || DL.n > INT32_MAX) return GSB_E_ARG;
+    unsigned char* db = reinterpret_cast<unsigned char*>(st->det_work);
+    w.det_keys = reinterpret_cast<uint64_t*>(db + DL.keys_in);
+    w.det_vals = reinterpret_cast<T*>(db + DL.vals);
+  }
   if constexpr (F32) {
     if (st->pose_work) {  // pose refinement: keep dphi/dz and colour-input cotangents
       const PoseLayout PL = pose_layout<T>(z, S::IN_G);
@@ -187,6 +227,8 @@ int run_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step
     k_render<T><<<(M + 3) / 4, 128, (size_t)4 * 4 * N * esz, stream>>>(w, M, N, dep_final, params,
                                                                        model->log_s_offset, L);
     GSB_LAUNCHED_T("k_render");
+    if (w.det_keys)  // every slot starts empty (~0 sorts last and is skipped)
+      GSB_CHECK(cudaMemsetAsync(w.det_keys, 0xff, (size_t)DL.n * 8, stream));
     // backward kernels: persistent grids
     constexpr int WG = sizeof(T) == 4 ? 4 : 2;
     const int per_cta = WG * 32;
@@ -209,15 +251,18 @@ int run_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step
       // MLP partials: red.add into kMlpSlots L2-resident rows instead of one row per CTA
       constexpr int kMlpSlots = 64;
       static_assert(kMlpSlots <= kNbMax, "workspace carve");
-      w.mlp_slots = kMlpSlots;
-      GSB_CHECK(cudaMemsetAsync(w.mlp_part, 0, (size_t)kMlpSlots * S::NMLP * sizeof(T), stream));
+      w.mlp_slots = w.det_keys ? 0 : kMlpSlots;  // deterministic mode: per-CTA rows
+      if (w.mlp_slots)
+        GSB_CHECK(cudaMemsetAsync(w.mlp_part, 0, (size_t)kMlpSlots * S::NMLP * sizeof(T), stream));
       tc::k_bwd_geom_tc<S, WGEO><<<nb_geo, WGEO * 32, smem_g, stream>>>(w, G, M, N, mlp32,
                                                                         dep_final, spts, nsp, 2);
       GSB_LAUNCHED_T("k_bwd_geom");
       tc::k_bwd_color_tc<S, WCOL><<<nb_col, WCOL * 32, smem_c, stream>>>(w, G, M, N, mlp32, dep_final);
       GSB_LAUNCHED_T("k_bwd_color");
-      nb_geo = std::min(nb_geo, kMlpSlots);
-      nb_col = std::min(nb_col, kMlpSlots);
+      if (w.mlp_slots) {
+        nb_geo = std::min(nb_geo, kMlpSlots);
+        nb_col = std::min(nb_col, kMlpSlots);
+      }
     } else {
       constexpr int CW = S::NMLP - S::oCW0;
       size_t smem_g = ((size_t)(S::NG + 3) / 4 * 4 + (size_t)WG * 32 * GeoRow<T, S>::ROW) * esz;
@@ -231,6 +276,23 @@ int run_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step
       GSB_LAUNCHED_T("k_bwd_geom");
       k_bwd_color<T, S, WG><<<nb_col, per_cta, smem_c, stream>>>(w, G, M, N, dep_final, mlp);
       GSB_LAUNCHED_T("k_bwd_color");
+    }
+    if (w.det_keys) {  // stable sort by grad row, then per-row sums in (sample, level, corner) order
+      unsigned char* db = reinterpret_cast<unsigned char*>(st->det_work);
+      int32_t* idx_in = reinterpret_cast<int32_t*>(db + DL.idx_in);
+      int32_t* idx_out = reinterpret_cast<int32_t*>(db + DL.idx_out);
+      uint64_t* keys_out = reinterpret_cast<uint64_t*>(db + DL.keys_out);
+      const int nb = (int)((DL.n + 255) / 256);
+      k_det_iota<<<nb, 256, 0, stream>>>(idx_in, DL.n);
+      GSB_LAUNCHED_T("k_det_iota");
+      size_t tb = DL.temp_bytes;
+      GSB_CHECK(cub::DeviceRadixSort::SortPairs(db + DL.temp, tb, w.det_keys, keys_out, idx_in, idx_out,
+                                                (int)DL.n, 0, 64, stream));
+      GSB_LAUNCHED_T("cub_radix_sort");
+      const uintptr_t col_lo = reinterpret_cast<uintptr_t>(G.col.grad);
+      const uintptr_t col_hi = col_lo + (uintptr_t)G.col.nx * G.col.ny * G.col.nz * G.col.C * sizeof(T);
+      k_det_reduce<T><<<nb, 256, 0, stream>>>(keys_out, idx_out, w.det_vals, DL.n, S::CG, S::CC, col_lo, col_hi);
+      GSB_LAUNCHED_T("k_det_reduce");
     }
     static_assert(FIN_SPLIT == 16, "workspace carve");
     GSB_CHECK(cudaMemsetAsync(w.fin_cnt, 0, (S::NMLP + 31) / 32 * sizeof(unsigned), stream));

@@ -918,7 +918,8 @@ __global__ void __launch_bounds__(WARPS * 32) k_bwd_geom_tc(Ws<float> w, Geo G, 
     corner_w_ju(lq, (float)G.lv[l].inv_vs, u, wk, ju);
 #pragma unroll
     for (int k = 0; k < 8; ++k) coef[k] = fmaf(p, wk[k], ju[k]);
-    scatter_level<float, S::CG>(G.lv[l], lq, myrow + K::oZ + l * S::CG, coef, active, l < agg_levels);
+    scatter_level<float, S::CG>(G.lv[l], lq, myrow + K::oZ + l * S::CG, coef, active, l < agg_levels,
+                                w.det_keys, w.det_vals, s * (S::NL + 1) + l);
   }
   // ---- outer products over the warp's samples: dW0 += A0^T delta0, dW1 += A1^T delta1
   float d0[1][4][4], d1[2][4][4];
@@ -1163,7 +1164,8 @@ __global__ void __launch_bounds__(WARPS * 32, 2) k_bwd_color_tc(Ws<float> w, Geo
   {  // colour grid scatter: theta_c[idx_k] += w_k f_bar (warp-segmented)
     float wk[8];
     corner_w(q, wk);
-    scatter_level<float, S::CC>(G.col, q, myrow + K::oFB, wk, active, false);
+    scatter_level<float, S::CC>(G.col, q, myrow + K::oFB, wk, active, false, w.det_keys, w.det_vals,
+                                s * (S::NL + 1) + S::NL);
   }
   if (w.pose_fb && active) {  // pose refinement: f_bar and the view-direction cotangent
     float* o = w.pose_fb + s * 12;

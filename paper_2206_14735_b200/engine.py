@@ -172,6 +172,8 @@ class StepEngine:
         self._ws = {}
         self.col, self.dep, _ = dataset.device_tensors(self.device, model.dtype)
         self.mstruct = self._model_struct()
+        # deterministic scatter mode (validation): bit-reproducible grid gradients
+        self.deterministic = False
         self._init_poses()
         self.dstruct = self._dataset_struct()
 
@@ -382,6 +384,9 @@ class StepEngine:
         if self.refine:
             buf = self._pose_scratch(cfg, M)
             st.pose_work, st.pose_work_bytes = buf.data_ptr(), buf.numel()
+        if self.deterministic:
+            buf = self._det_scratch(cfg, M, S)
+            st.det_work, st.det_work_bytes = buf.data_ptr(), buf.numel()
         if fresh and phases & 1:
             self.pose_tables(stream)
         _lib.check(self.lib.gsb_train_step(C.byref(self.mstruct), C.byref(self.dstruct),
@@ -392,6 +397,17 @@ class StepEngine:
             if self.refine:
                 self._pose_grad(cfg, st, M, stream)
         return ws
+
+    def _det_scratch(self, cfg, M, S):
+        key = ("det", M, cfg.coarse_samples, cfg.importance_rounds, cfg.importance_add, S)
+        if key not in self._ws:
+            nbytes = C.c_size_t(0)
+            _lib.check(self.lib.gsb_det_scratch_size(C.byref(self.mstruct), M, cfg.coarse_samples,
+                                                     cfg.importance_rounds, cfg.importance_add, S,
+                                                     C.byref(nbytes)), "det scratch size")
+            self._ws[key] = self.torch.empty(max(int(nbytes.value), 1), dtype=self.torch.uint8,
+                                             device=self.device)
+        return self._ws[key]
 
     def _pose_scratch(self, cfg, M):
         key = ("pose", M, cfg.coarse_samples, cfg.importance_rounds, cfg.importance_add)

@@ -137,9 +137,13 @@ def parts_from(ws):
     return {k: float(p[i]) for i, k in enumerate(_lib.PART_NAMES)}
 
 
-def train_objective(model, dataset, batch, iteration, cfg, smooth_override=None):
+def train_objective(model, dataset, batch, iteration, cfg, smooth_override=None, deterministic=None):
     """Evaluate the objective for one ray batch and its full gradient
     (gs/renderer.py:279-468 + gs/diffcore.py:1035).
+
+    ``deterministic`` (not in the reference): True switches the grid-gradient
+    scatters to the sorted, sample-ordered reduction (bit-reproducible run to
+    run, for validation); None keeps the engine's current mode.
 
     Returns (total Objective, parts dict of floats, extras dict)."""
     from .data import Dataset
@@ -151,6 +155,8 @@ def train_objective(model, dataset, batch, iteration, cfg, smooth_override=None)
     if near != cfg.near or far != cfg.max_depth:
         cfg = _with(cfg, near=near, max_depth=far)
     eng = engine_for(model, dataset)
+    if deterministic is not None:
+        eng.deterministic = bool(deterministic)
     draws = host_draws(model, dataset, cfg, iteration, ray_ids=batch_ray_ids(batch, dataset),
                        smooth_override=smooth_override)
     ids, sm = eng.upload(draws)

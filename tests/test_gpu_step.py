@@ -380,3 +380,29 @@ def test_device_smooth_points_bit_exact(case, precision):
         got = eng.smooth_points(raw, 0.004).cpu().numpy()
         want = np.concatenate([ref[0], ref[1]], axis=0).astype(model.dtype)
         np.testing.assert_array_equal(got, want)
+
+
+@pytest.mark.parametrize("precision", ["single", "double"])
+def test_deterministic_scatter_mode(precision):
+    """Deterministic scatter mode (north star: 'a deterministic segmented-
+    reduction mode for validation'): grid gradients bit-identical run to run,
+    and equal to the default (atomic) mode within float summation order."""
+    G = load("small", precision)
+    model, ds, cfg = gpu_model(G)
+    it = G.meta["iteration"]
+    b = sampler.draw_ray_batch(ds, seeds.substream(cfg.seed, seeds.RAYS, it), cfg.batch_rays,
+                               near=cfg.near, far=cfg.max_depth)
+    runs = []
+    for det in (True, True, False):
+        total, parts, _ = renderer.train_objective(model, ds, b, it, cfg, deterministic=det)
+        g = renderer.grad(total, model.parameters())
+        runs.append((parts, [t.cpu().numpy().copy() for t in g]))
+    (p1, g1), (p2, g2), (p3, g3) = runs
+    assert p1 == p2
+    for n, a, bb, c in zip(model.param_names(), g1, g2, g3):
+        np.testing.assert_array_equal(a, bb, err_msg=n)
+        tol = 1e-12 if precision == "double" else 2e-5
+        assert np.abs(a - c).max() <= tol * max(np.abs(c).max(), 1e-30), n
+    if precision == "double":  # and against the reference's own gradients
+        for n, a in zip(model.param_names(), g1):
+            assert rel_maxnorm(a, G.a[f"grad_{n}"]) <= GRAD_TOL[precision], n
