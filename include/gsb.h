@@ -168,7 +168,9 @@ typedef struct {
   double smooth_global;      /* global pair count (normaliser) */
   /* behaviour */
   int32_t exact_gather;      /* 1: reproduce numba's per-corner rounding (slower) */
-  int32_t phases;            /* bit0: sampling+counts, bit1: objective+backward+finalize */
+  int32_t phases;            /* bit0: sampling+counts, bit1: objective+backward+finalize;
+                                bit2 / bit3 with bit1: only part A (taped forward, render,
+                                geometry backward) / only part B (colour backward, finalize) */
   /* workspace (see gsb_step_workspace_size) */
   void* workspace;
   size_t workspace_bytes;

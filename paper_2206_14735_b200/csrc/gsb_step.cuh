@@ -194,9 +194,14 @@ int run_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step
     }
   }
   if (st->phases & 2) {
+    // bit 2 / bit 3 split the backward phase for communication overlap: part A
+    // = taped forward, render, geometry backward (the geometry grids' grads are
+    // final after it); part B = colour backward and the finalize kernels
+    const bool runA = (st->phases & 12) != 8, runB = (st->phases & 12) != 4;
     const T* spts = reinterpret_cast<const T*>(st->smooth_pts);
     int64_t ns = z.NS;
     int fb = (int)((ns + 127) / 128);
+    if (runA) {
     if constexpr (F32) {
       GSB_CHECK(cudaFuncSetAttribute(tc::k_fwd_tc<S, TW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)tc::FwdTc<S, TW>::smem()));
@@ -208,6 +213,7 @@ int run_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step
       k_fwd<T, S, false><<<fb, 128, smem_fwd, stream>>>(w, G, M, N, dep_final, spts, nsp, mlp);
     }
     GSB_LAUNCHED_T("k_fwd");
+    }
     LossW L;
     L.rgb = st->w_rgb;
     L.depth = st->w_depth;
@@ -219,16 +225,18 @@ int run_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step
     L.alpha = st->fs_alpha;
     L.m_global = st->m_global;
     L.smooth_global = st->smooth_global;
-    if (z.S > 0) {
-      T scale = (T)(2.0 * st->w_smooth) / (T)st->smooth_global;
-      k_smooth<T><<<(z.S + 127) / 128, 128, 0, stream>>>(w, z.MN, z.S, scale);
-      GSB_LAUNCHED_T("k_smooth");
+    if (runA) {
+      if (z.S > 0) {
+        T scale = (T)(2.0 * st->w_smooth) / (T)st->smooth_global;
+        k_smooth<T><<<(z.S + 127) / 128, 128, 0, stream>>>(w, z.MN, z.S, scale);
+        GSB_LAUNCHED_T("k_smooth");
+      }
+      k_render<T><<<(M + 3) / 4, 128, (size_t)4 * 4 * N * esz, stream>>>(w, M, N, dep_final, params,
+                                                                         model->log_s_offset, L);
+      GSB_LAUNCHED_T("k_render");
+      if (w.det_keys)  // every slot starts empty (~0 sorts last and is skipped)
+        GSB_CHECK(cudaMemsetAsync(w.det_keys, 0xff, (size_t)DL.n * 8, stream));
     }
-    k_render<T><<<(M + 3) / 4, 128, (size_t)4 * 4 * N * esz, stream>>>(w, M, N, dep_final, params,
-                                                                       model->log_s_offset, L);
-    GSB_LAUNCHED_T("k_render");
-    if (w.det_keys)  // every slot starts empty (~0 sorts last and is skipped)
-      GSB_CHECK(cudaMemsetAsync(w.det_keys, 0xff, (size_t)DL.n * 8, stream));
     // backward kernels: persistent grids
     constexpr int WG = sizeof(T) == 4 ? 4 : 2;
     const int per_cta = WG * 32;
@@ -252,13 +260,17 @@ int run_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step
       constexpr int kMlpSlots = 64;
       static_assert(kMlpSlots <= kNbMax, "workspace carve");
       w.mlp_slots = w.det_keys ? 0 : kMlpSlots;  // deterministic mode: per-CTA rows
-      if (w.mlp_slots)
-        GSB_CHECK(cudaMemsetAsync(w.mlp_part, 0, (size_t)kMlpSlots * S::NMLP * sizeof(T), stream));
-      tc::k_bwd_geom_tc<S, WGEO><<<nb_geo, WGEO * 32, smem_g, stream>>>(w, G, M, N, mlp32,
-                                                                        dep_final, spts, nsp, 2);
-      GSB_LAUNCHED_T("k_bwd_geom");
-      tc::k_bwd_color_tc<S, WCOL><<<nb_col, WCOL * 32, smem_c, stream>>>(w, G, M, N, mlp32, dep_final);
-      GSB_LAUNCHED_T("k_bwd_color");
+      if (runA) {
+        if (w.mlp_slots)
+          GSB_CHECK(cudaMemsetAsync(w.mlp_part, 0, (size_t)kMlpSlots * S::NMLP * sizeof(T), stream));
+        tc::k_bwd_geom_tc<S, WGEO><<<nb_geo, WGEO * 32, smem_g, stream>>>(w, G, M, N, mlp32,
+                                                                          dep_final, spts, nsp, 2);
+        GSB_LAUNCHED_T("k_bwd_geom");
+      }
+      if (runB) {
+        tc::k_bwd_color_tc<S, WCOL><<<nb_col, WCOL * 32, smem_c, stream>>>(w, G, M, N, mlp32, dep_final);
+        GSB_LAUNCHED_T("k_bwd_color");
+      }
       if (w.mlp_slots) {
         nb_geo = std::min(nb_geo, kMlpSlots);
         nb_col = std::min(nb_col, kMlpSlots);
@@ -271,12 +283,17 @@ int run_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_g));
       GSB_CHECK(cudaFuncSetAttribute(k_bwd_color<T, S, WG>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_c));
-      k_bwd_geom<T, S, WG><<<nb_geo, per_cta, smem_g, stream>>>(w, G, M, N, dep_final, spts, nsp,
-                                                               2, mlp);
-      GSB_LAUNCHED_T("k_bwd_geom");
-      k_bwd_color<T, S, WG><<<nb_col, per_cta, smem_c, stream>>>(w, G, M, N, dep_final, mlp);
-      GSB_LAUNCHED_T("k_bwd_color");
+      if (runA) {
+        k_bwd_geom<T, S, WG><<<nb_geo, per_cta, smem_g, stream>>>(w, G, M, N, dep_final, spts, nsp,
+                                                                 2, mlp);
+        GSB_LAUNCHED_T("k_bwd_geom");
+      }
+      if (runB) {
+        k_bwd_color<T, S, WG><<<nb_col, per_cta, smem_c, stream>>>(w, G, M, N, dep_final, mlp);
+        GSB_LAUNCHED_T("k_bwd_color");
+      }
     }
+    if (!runB) return GSB_OK;  // part A only: the caller overlaps the geometry-grid exchange
     if (w.det_keys) {  // stable sort by grad row, then per-row sums in (sample, level, corner) order
       unsigned char* db = reinterpret_cast<unsigned char*>(st->det_work);
       int32_t* idx_in = reinterpret_cast<int32_t*>(db + DL.idx_in);

@@ -376,7 +376,8 @@ class StepEngine:
         M = int(ray_ids_dev.numel())
         S = 0 if smooth_dev is None else int(smooth_dev.shape[0] // 2)
         ws = self.workspace(M, cfg.coarse_samples, cfg.importance_rounds, cfg.importance_add, S)
-        self.model.arena.zero_grads()
+        if kw.get("phases", 3) & 12 != 8:  # part B continues part A's gradients
+            self.model.arena.zero_grads()
         if fresh:
             ws["status"].zero_()
         st = self.step_struct(cfg, draws, ray_ids_dev, smooth_dev, ws, **kw)
@@ -394,7 +395,7 @@ class StepEngine:
                    "gsb_train_step")
         if phases & 2:
             self.model.arena.grads_clean = False
-            if self.refine:
+            if self.refine and (phases & 12) != 4:  # after the whole backward (or its part B)
                 self._pose_grad(cfg, st, M, stream)
         return ws
 

@@ -15,7 +15,10 @@ points:
    wire bytes of one all-reduce, with Adam's HBM bytes divided by N (ZeRO-1;
    Adam m / v are valid on the owning rank, ``gather_adam_state`` assembles
    them for a checkpoint).  ``shard_adam=False`` keeps the all-reduce +
-   replicated Adam form.
+   replicated Adam form.  With NCCL the backward runs in two launches and
+   the geometry grids' reduce-scatter (their gradients are final after the
+   geometry backward) overlaps the colour backward on NCCL's stream; the
+   rest of the arena follows.
 
 Rank 0 owns the smoothness points; every loss keeps its global normaliser
 (``m_global``, ``smooth_global``)."""
@@ -56,7 +59,7 @@ class DataParallelStep:
     ``model.arena.grads`` tensor); ``dist`` is ``torch.distributed`` with an
     initialised process group (NCCL on GPUs, gloo in the CPU tests)."""
 
-    def __init__(self, engine, dist, group=None, shard_adam=True):
+    def __init__(self, engine, dist, group=None, shard_adam=True, overlap=True):
         self.engine = engine
         self.dist = dist
         self.group = group
@@ -65,6 +68,34 @@ class DataParallelStep:
         self.nccl = dist.get_backend(group) == "nccl"
         self.shard_adam = bool(shard_adam) and self.world > 1
         self._inplace_ok = True  # NCCL in-place reduce-scatter / all-gather accepted
+        self.overlap = overlap
+
+    def chunks(self, n):
+        """Arena chunks exchanged separately: [(0, a), (a, n)] with a the end of
+        the geometry grids rounded down to 4 x world (overlap form), else [(0, n)]."""
+        eng = self.engine
+        q = 4 * self.world
+        a = 0
+        # overlap="always": the two-chunk form on any backend (tests run it on gloo)
+        if (self.overlap and (self.nccl or self.overlap == "always") and self.shard_adam
+                and not getattr(eng, "deterministic", False)):
+            try:
+                a = int(eng.model.arena["colorgrid"].offset) // q * q
+            except (KeyError, AttributeError, TypeError):
+                a = 0
+        if 0 < a < n and (n - a) % q == 0:
+            return [(0, a), (a, n)]
+        return [(0, n)]
+
+    def shards(self, n):
+        """This rank's [lo, hi) in every chunk."""
+        out = []
+        for c0, c1 in self.chunks(n):
+            chunk = (c1 - c0) // self.world
+            if chunk * self.world != c1 - c0 or chunk % 4:
+                raise ValueError("arena chunks must split into equal 16-byte-aligned shards")
+            out.append((c0 + self.rank * chunk, c0 + (self.rank + 1) * chunk))
+        return out
 
     def shard(self, n):
         """This rank's arena range [lo, hi) (n is a multiple of 4 x world)."""
@@ -77,23 +108,41 @@ class DataParallelStep:
         eng = self.engine
         ws = eng.launch(cfg, draws, ids, sm, phases=1, **kw)
         self.dist.all_reduce(ws["counts"], group=self.group)            # exchange 1
-        ws = eng.launch(cfg, draws, ids, sm, phases=2, fresh=False, **kw)
         g = eng.model.arena.grads                                       # exchange 2
-        done = False
-        if self.shard_adam and self.nccl and self._inplace_ok:
-            lo, hi = self.shard(g.numel())
-            try:
-                self.dist.reduce_scatter_tensor(g[lo:hi], g, group=self.group)  # in place
-                done = True
-            except (RuntimeError, ValueError):  # argument check refused the aliasing
-                self._inplace_ok = False
-        if not done:  # gloo has no reduce-scatter: the sum everywhere, the shard is a slice
-            self.dist.all_reduce(g, group=self.group)
+        chunks = self.chunks(g.numel()) if self.shard_adam else [(0, g.numel())]
+        if len(chunks) == 2:  # geometry-grid reduce-scatter under the colour backward
+            eng.launch(cfg, draws, ids, sm, phases=2 | 4, fresh=False, **kw)
+            works = [self._reduce_scatter(g, *chunks[0], async_op=True)]
+            ws = eng.launch(cfg, draws, ids, sm, phases=2 | 8, fresh=False, **kw)
+            works.append(self._reduce_scatter(g, *chunks[1], async_op=True))
+            for wk in works:
+                if wk is not None:
+                    wk.wait()
+        else:
+            ws = eng.launch(cfg, draws, ids, sm, phases=2, fresh=False, **kw)
+            if self.shard_adam:
+                self._reduce_scatter(g, *chunks[0])
+            else:
+                self.dist.all_reduce(g, group=self.group)
         parts = ws["parts"]
         s = parts[S_SLOT].clone()
         self.dist.all_reduce(parts, group=self.group)
         parts[S_SLOT] = s
         return ws
+
+    def _reduce_scatter(self, g, c0, c1, async_op=False):
+        """Sum of chunk [c0, c1) into this rank's shard of it (NCCL in place);
+        gloo has no reduce-scatter: the chunk's sum everywhere."""
+        t = g[c0:c1]
+        if self.nccl and self._inplace_ok:
+            chunk = (c1 - c0) // self.world
+            lo = self.rank * chunk
+            try:
+                return self.dist.reduce_scatter_tensor(t[lo:lo + chunk], t, group=self.group,
+                                                       async_op=async_op)
+            except (RuntimeError, ValueError):  # argument check refused the aliasing
+                self._inplace_ok = False
+        return self.dist.all_reduce(t, group=self.group, async_op=async_op)
 
     def adam(self, opt, **kw):
         """The optimizer step after ``__call__``: sharded update + all-gather."""
@@ -101,11 +150,16 @@ class DataParallelStep:
             opt._launch(**kw)
             return
         a = opt.arena
-        lo, hi = self.shard(a.n)
-        opt._launch(lo=lo, hi=hi, **kw)       # zeroes grads[lo:hi]
-        a.grads[:lo].zero_()                  # partial sums of the other shards
-        a.grads[hi:].zero_()
-        self._all_gather(a.params, lo, hi)
+        mine = self.shards(a.n)
+        for lo, hi in mine:  # Adam zeroes grads[lo:hi]; the divergence guard gates every range
+            opt._launch(lo=lo, hi=hi, **kw)
+        prev = 0
+        for lo, hi in mine:  # partial sums of the other ranks' shards
+            a.grads[prev:lo].zero_()
+            prev = hi
+        a.grads[prev:].zero_()
+        for (c0, c1), (lo, hi) in zip(self.chunks(a.n), mine):
+            self._all_gather(a.params[c0:c1], lo - c0, hi - c0)
 
     def _all_gather(self, t, lo, hi):
         if self.nccl and self._inplace_ok:
@@ -122,6 +176,6 @@ class DataParallelStep:
         """Assemble the full Adam m / v on every rank (e.g. before save_model)."""
         if not self.shard_adam:
             return
-        lo, hi = self.shard(opt.arena.n)
-        self._all_gather(opt.m_arena, lo, hi)
-        self._all_gather(opt.v_arena, lo, hi)
+        for (c0, c1), (lo, hi) in zip(self.chunks(opt.arena.n), self.shards(opt.arena.n)):
+            self._all_gather(opt.m_arena[c0:c1], lo - c0, hi - c0)
+            self._all_gather(opt.v_arena[c0:c1], lo - c0, hi - c0)

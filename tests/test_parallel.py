@@ -204,6 +204,10 @@ class _FakeArena:
         self.params = torch.linspace(-1.0, 1.0, n, dtype=torch.float64)
         self.grads = torch.zeros(n, dtype=torch.float64)
 
+    def __getitem__(self, name):  # the "colorgrid" parameter starts at element 300
+        from types import SimpleNamespace
+        return SimpleNamespace(offset=300)
+
 
 class _TorchAdam:
     """Adam restated in torch (gs/optimizer.py:38-55) over an arena range,
@@ -232,6 +236,7 @@ class _FakeStepEngine:
         import types
         self.torch, self.rank = torch, rank
         self.model = types.SimpleNamespace(arena=arena)
+        self.split = 300  # "colorgrid" offset of the fake arena
         self.ws = dict(counts=torch.zeros(4, dtype=torch.int64), parts=torch.zeros(8, dtype=torch.float64))
 
     def launch(self, cfg, draws, ids, sm, phases=3, fresh=True, it=0, **kw):
@@ -240,12 +245,19 @@ class _FakeStepEngine:
             return self.ws
         a = self.model.arena
         gen = self.torch.Generator().manual_seed(1000 * kw.get("step", 0) + self.rank)
-        a.grads += self.torch.randn(a.n, generator=gen, dtype=self.torch.float64)
+        full = self.torch.randn(a.n, generator=gen, dtype=self.torch.float64)
+        cut = self.split  # split backward: part A writes [0, cut), part B the rest
+        if phases & 12 == 4:
+            a.grads[:cut] += full[:cut]
+        elif phases & 12 == 8:
+            a.grads[cut:] += full[cut:]
+        else:
+            a.grads += full
         self.ws["parts"][:] = float(self.rank + 1)
         return self.ws
 
 
-def _shard_worker(rank, world, port, out, steps, n):
+def _shard_worker(rank, world, port, out, steps, n, overlap):
     import torch
     import torch.distributed as dist
     from paper_2206_14735_b200.parallel import DataParallelStep
@@ -253,8 +265,9 @@ def _shard_worker(rank, world, port, out, steps, n):
     try:
         arena = _FakeArena(torch, n)
         opt = _TorchAdam(torch, arena)
-        dp = DataParallelStep(_FakeStepEngine(torch, arena, rank), dist)
+        dp = DataParallelStep(_FakeStepEngine(torch, arena, rank), dist, overlap=overlap)
         assert dp.shard_adam
+        assert len(dp.chunks(n)) == (2 if overlap == "always" else 1)
         for k in range(steps):
             ws = dp(None, None, None, None, step=k)
             opt.t = [k + 1]
@@ -270,14 +283,15 @@ def _shard_worker(rank, world, port, out, steps, n):
 
 
 @pytest.mark.timeout(300)
-def test_sharded_adam_gloo_world2_equals_replicated(tmp_path):
+@pytest.mark.parametrize("overlap", [True, "always"])
+def test_sharded_adam_gloo_world2_equals_replicated(tmp_path, overlap):
     """reduce-scatter -> Adam on the rank's shard -> all-gather (parallel.py)
     gives the replicated all-reduce + full Adam result, parameters and the
     gathered moments alike (gloo: the reduce-scatter falls back to all-reduce)."""
     import torch
     import torch.multiprocessing as mp
     out, steps, n, world = str(tmp_path / "shard.npz"), 3, 1024, 2
-    mp.spawn(_shard_worker, args=(world, _free_port(), out, steps, n), nprocs=world, join=True)
+    mp.spawn(_shard_worker, args=(world, _free_port(), out, steps, n, overlap), nprocs=world, join=True)
     z = np.load(out)
     arena = _FakeArena(torch, n)
     opt = _TorchAdam(torch, arena)
@@ -328,7 +342,7 @@ def _gpu_adam_worker(rank, world, port, out):
             model = optimizer.build_model(ds, cfg, skip_init=True, device=torch.device("cuda", 0))
             opt = optimizer.make_optimizer(model, cfg)
             eng = engine_for(model, ds)
-            dp = DataParallelStep(eng, dist) if sharded else None
+            dp = DataParallelStep(eng, dist, overlap="always") if sharded else None
             for it in range(2):
                 full = engine.host_draws(model, ds, cfg, it)
                 if sharded:
