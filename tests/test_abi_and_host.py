@@ -191,3 +191,27 @@ def test_draw_prefetcher_order_and_errors():
     with pytest.raises(RuntimeError):
         q.get(5)  # out of order is an error, not a silent mismatch
     q.close()
+
+
+def test_product_path_fails_loudly_without_extension(monkeypatch, tmp_path):
+    """No CPU fallback: with the CUDA extension absent the library loader and
+    a model build raise instead of computing anything on the host."""
+    from paper_2206_14735_b200 import _lib
+    monkeypatch.setattr(_lib, "_lib", None)
+    monkeypatch.setattr(_lib, "LIB_PATH", str(tmp_path / "missing_gsb.so"))
+    with pytest.raises(_lib.GsbError):
+        _lib.lib()
+
+
+def test_build_model_refuses_cpu_device():
+    """The step has no host implementation: build_model needs CUDA."""
+    import torch
+    from paper_2206_14735_b200 import optimizer
+    if torch.cuda.is_available():
+        pytest.skip("CUDA present")
+    G = load("tiny", "single")
+    cfg = optimizer.TrainConfig(precision="single", batch_rays=8)
+    from paper_2206_14735_b200 import data
+    ds = data.Dataset(G.a["colors_u8"], G.a["depths_u16"], G.a["poses"], G.ds.intrinsics)
+    with pytest.raises(RuntimeError, match="CUDA"):
+        optimizer.build_model(ds, cfg, skip_init=True)
