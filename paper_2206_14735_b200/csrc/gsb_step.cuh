@@ -203,9 +203,10 @@ int run_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step
     int fb = (int)((ns + 127) / 128);
     if (runA) {
     if constexpr (F32) {
-      GSB_CHECK(cudaFuncSetAttribute(tc::k_fwd_tc<S, TW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)tc::FwdTc<S, TW>::smem()));
-      tc::k_fwd_tc<S, TW><<<(int)((ns + TW * 32 - 1) / (TW * 32)), TW * 32, tc::FwdTc<S, TW>::smem(),
+      constexpr int FW = 4;  // warps per CTA of the taped forward
+      GSB_CHECK(cudaFuncSetAttribute(tc::k_fwd_tc<S, FW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)tc::FwdTc<S, FW>::smem()));
+      tc::k_fwd_tc<S, FW><<<(int)((ns + FW * 32 - 1) / (FW * 32)), FW * 32, tc::FwdTc<S, FW>::smem(),
                             stream>>>(w, G, M, N, mlp32, dep_final, spts, nsp);
     } else {
       GSB_CHECK(cudaFuncSetAttribute(k_fwd<T, S, false>,
@@ -245,11 +246,11 @@ int run_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step
     nb_geo = std::max(1, std::min(nb_geo, kNbMax));
     nb_col = std::max(1, std::min(nb_col, kNbMax));
     if constexpr (F32) {
-      constexpr int WGEO = 4;                          // one 32-sample batch per warp
+      constexpr int WGEO = 4;  // one 32-sample batch per warp
       nb_geo = (int)((ns + WGEO * 32 - 1) / (WGEO * 32));
       nb_col = (int)((z.MN + per_cta - 1) / per_cta);
       const size_t smem_g = tc::GeoTc<S, WGEO>::smem();
-      constexpr int WCOL = 6;
+      constexpr int WCOL = 4;  // 2 x 4 warps beat 2 x 6 (322 vs 367 us): L1 for the gathers
       nb_col = (int)((z.MN + WCOL * 32 - 1) / (WCOL * 32));
       const size_t smem_c = tc::ColTc<S, WCOL>::smem();
       GSB_CHECK(cudaFuncSetAttribute(tc::k_bwd_geom_tc<S, WGEO>,

@@ -1009,7 +1009,8 @@ __global__ void __launch_bounds__(WARPS * 32) k_bwd_geom_tc(Ws<float> w, Geo G, 
 template <class S, int WARPS>
 struct ColTc {
   using F = Fr<S>;
-  static constexpr int ROW = 104;  // 6 warps x 13 KB + 27 KB weights: 2 CTAs = 12 warps / SM
+  static constexpr int ROW = 104;  // 4 warps x 13 KB + 27 KB weights: 2 CTAs = 8 warps / SM (measured best: the
+                                   // smaller shared-memory carve-out leaves L1 for the colour-corner gathers)
   static constexpr int oA0 = 0;    // [inp (IN_C), 1, 0...] (16)
   static constexpr int oB0 = 16;   // a0_bar (32)
   static constexpr int oA1 = 48;   // h0c (32)
@@ -1029,7 +1030,7 @@ struct ColTc {
 // is rebuilt per fragment from y_bar, the layer-1 mask and W2c; dW2c, db1c
 // and db2c are column sums of D fragments.
 template <class S, int WARPS>
-__global__ void __launch_bounds__(WARPS * 32, 2) k_bwd_color_tc(Ws<float> w, Geo G, int M, int N,
+__global__ void __launch_bounds__(WARPS * 32, WARPS <= 6 ? 2 : 1) k_bwd_color_tc(Ws<float> w, Geo G, int M, int N,
                                                              const float* __restrict__ mlp,
                                                              const double* __restrict__ dep) {
   using K = ColTc<S, WARPS>;
