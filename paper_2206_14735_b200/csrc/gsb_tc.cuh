@@ -17,11 +17,11 @@
 //
 // tools/mb_layers.cu measured this form at 84-101% of the fp32 FFMA peak
 // (effective) already at 1-2 CTAs/SM with ~10x fewer issued instructions
-// and ~10x less code than the unrolled-FFMA kernels (gsb_fast.cuh), whose
+// and ~10x less code than the unrolled-FFMA kernels (round-1 history), whose
 // 100-190 KB of SASS thrashed the instruction cache.
 #pragma once
 
-#include "gsb_fast.cuh"
+#include "gsb_mma.cuh"
 
 namespace gsb {
 namespace tc {
