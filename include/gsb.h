@@ -167,7 +167,8 @@ typedef struct {
   int32_t n_smooth;          /* pairs on this rank */
   double smooth_global;      /* global pair count (normaliser) */
   /* behaviour */
-  int32_t exact_gather;      /* 1: reproduce numba's per-corner rounding (slower) */
+  int32_t exact_gather;      /* reserved (0): the step gathers with FMAs; the per-corner
+                                rounding of numba is gsb_gather_weighted (exact twin) */
   int32_t phases;            /* bit0: sampling+counts, bit1: objective+backward+finalize;
                                 bit2 / bit3 with bit1: only part A (taped forward, render,
                                 geometry backward) / only part B (colour backward, finalize) */
