@@ -147,9 +147,10 @@ def test_data_parallel_gloo_world2_equals_unsharded(tmp_path):
     assert np.abs(z["got"] - z["ref"]).max() <= 1e-12 * scale
 
 
-def _gpu_worker(rank, world, port, out):
+def _gpu_worker(rank, world, port, out, precision="double", refine=False):
     """Real device step under DataParallelStep; gloo collectives (both ranks
-    share the one GPU of this environment; collectives run on the host)."""
+    share the one GPU of this environment; collectives run on the host).
+    ``refine``: pose refinement on (per-rank partial pose gradients)."""
     import torch
     import torch.distributed as dist
     from _golden import load
@@ -159,10 +160,10 @@ def _gpu_worker(rank, world, port, out):
 
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
     try:
-        G = load("small", "double")
-        cfg = optimizer.TrainConfig(precision="double", **{
+        G = load("small", precision)
+        cfg = optimizer.TrainConfig(precision=precision, **{
             k: v for k, v in G.meta["cfg"].items() if k not in ("bounds", "voxel_sizes")},
-            voxel_sizes=G.cfg.voxel_sizes, bounds=G.cfg.bounds)
+            voxel_sizes=G.cfg.voxel_sizes, bounds=G.cfg.bounds, refine_poses=refine)
         cfg.weights.smooth_count = G.meta["smooth_count"]
         ds = data.Dataset(G.a["colors_u8"], G.a["depths_u16"], G.a["poses"], G.ds.intrinsics)
         model = optimizer.build_model(ds, cfg, skip_init=True, device=torch.device("cuda", 0))
@@ -188,10 +189,11 @@ def _gpu_worker(rank, world, port, out):
 
 @pytest.mark.gpu
 @pytest.mark.timeout(900)
-def test_data_parallel_device_step_world2_equals_unsharded(tmp_path):
+@pytest.mark.parametrize("refine", [False, True])
+def test_data_parallel_device_step_world2_equals_unsharded(tmp_path, refine):
     import torch.multiprocessing as mp
     out = str(tmp_path / "dpgpu.npz")
-    mp.spawn(_gpu_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    mp.spawn(_gpu_worker, args=(2, _free_port(), out, "double", refine), nprocs=2, join=True)
     z = np.load(out)
     assert (z["counts"] == z["ref_counts"]).all()
     np.testing.assert_allclose(z["parts"], z["ref_parts"], rtol=1e-12, atol=1e-15)
