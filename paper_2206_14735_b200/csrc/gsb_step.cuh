@@ -128,7 +128,7 @@ int run_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step
       w.pose_fb = reinterpret_cast<T*>(sc + PL.fb);
     }
     static_assert(tc::kFragBufU4 == 4096 + 68 + 768, "workspace carve");
-    tc::k_wfrag<S><<<tc::Fr<S>::NALL + 5, 32, 0, stream>>>(mlp32, w.wfrag);
+    tc::k_wfrag<S><<<tc::Fr<S>::NALL + 5, 128, 0, stream>>>(mlp32, w.wfrag);
     GSB_LAUNCHED_T("k_wfrag");
   }
   const size_t smem_sdf = (size_t)S::NG * esz;
@@ -378,7 +378,7 @@ int sdf_forward(const gsb_model_t* model, Ws<T>& w, const T* pts, int64_t n, cud
   const int blocks = (int)((n + 127) / 128);
   if constexpr (sizeof(T) == 4) {
     constexpr int TW = 4;
-    tc::k_wfrag<S><<<tc::Fr<S>::NALL + 5, 32, 0, stream>>>(mlp, w.wfrag);
+    tc::k_wfrag<S><<<tc::Fr<S>::NALL + 5, 128, 0, stream>>>(mlp, w.wfrag);
     GSB_LAUNCHED_T("k_wfrag");
     GSB_CHECK(cudaFuncSetAttribute(tc::k_fwd_tc<S, TW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)tc::FwdTc<S, TW>::smem()));

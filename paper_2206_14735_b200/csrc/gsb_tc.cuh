@@ -117,9 +117,9 @@ struct Fr {
 // One block per fragment id, one thread per lane.  Contraction index k of
 // fragment (kk, nn): b0 <-> k = 8kk+2t, b1 <-> k = 8kk+2t+1; output n = 8nn+g.
 template <class S>
-__global__ void __launch_bounds__(32) k_wfrag(const float* __restrict__ mlp, uint4* __restrict__ out) {
+__global__ void __launch_bounds__(128) k_wfrag(const float* __restrict__ mlp, uint4* __restrict__ out) {
   using F = Fr<S>;
-  const int id = blockIdx.x, lane = threadIdx.x, g = lane >> 2, t = lane & 3;
+  const int id = blockIdx.x, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   if (id > F::NALL) {  // tcgen05 B tiles: 1 W0 hi, 2 W0 lo, 3 W1 hi, 4 W1 lo
     const int tile = id - F::NALL - 1, lo = tile & 1;
     const bool l1 = tile >= 2;
@@ -127,7 +127,7 @@ __global__ void __launch_bounds__(32) k_wfrag(const float* __restrict__ mlp, uin
     const int oW = l1 ? S::oGW1 : S::oGW0;
     float* o = reinterpret_cast<float*>(out + kUmmaBaseU4) + (l1 ? (lo ? UmmaW::W1L : UmmaW::W1H)
                                                                   : (lo ? UmmaW::W0L : UmmaW::W0H));
-    for (int i = lane; i < GSB_HID * K; i += 32) {
+    for (int i = threadIdx.x; i < GSB_HID * K; i += blockDim.x) {
       const int n = i / K, k = i % K;  // B[n][k] = W[k][n]
       const float v = k < rows ? mlp[oW + k * GSB_HID + n] : 0.f;
       uint32_t h, l;
@@ -136,6 +136,7 @@ __global__ void __launch_bounds__(32) k_wfrag(const float* __restrict__ mlp, uin
     }
     return;
   }
+  if (threadIdx.x >= 32) return;  // fragments and vectors: one warp per block
   if (id == F::NALL) {  // bias / W2 vectors: geometry block then colour block
     float* v = reinterpret_cast<float*>(out + kVecBase);
     for (int i = lane; i < GVec::N + CVec::N; i += 32) {
