@@ -55,6 +55,8 @@ def make_cfg(precision="single", batch=M_PER_GPU, seed=0, config=2, coarse=96, s
     if config == 4:
         kw.update(bounds=scenes.CONFIG4_BOUNDS, voxel_sizes=scenes.CONFIG4_VOXELS,
                   color_voxel=scenes.CONFIG4_COLOR_VOXEL)
+    elif config == 1:
+        pass  # the reference's defaults: 4-level grid, bounds derived from the frames
     else:
         kw.update(bounds=scenes.CONFIG2_BOUNDS)
     cfg = optimizer.TrainConfig(**kw)
@@ -167,6 +169,10 @@ FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12                 # nominal FMA 
 
 def workload_name(args, N):
     sm = "off" if args.no_smooth else "on"
+    if args.config == 1:
+        return (f"config1: sphere-in-box room, 20 RGB-D frames 160x120, default 4-level grid "
+                f"(0.96/0.24/0.06/0.03 m), derived bounds, {args.rays} rays, "
+                f"{args.coarse}+3x12 samples/ray, smoothness {sm}")
     if args.config == 4:
         return (f"config4: 10 m synthetic room, 640x480 RGB-D, 4-level grid "
                 f"(0.96/0.24/0.06/0.02 m + 0.02 m colour), 11 m box, "
@@ -296,8 +302,9 @@ def main():
     ap.add_argument("--frames", type=int, default=FRAMES)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--rays", type=int, default=M_PER_GPU)
-    ap.add_argument("--config", type=int, default=2, choices=[2, 4],
-                    help="2: ScanNet-shaped room (headline); 4: 10 m scene, 0.02 m grid (P = 1.7 B)")
+    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 4],
+                    help="2: ScanNet-shaped room (headline); 1: sphere-in-box 20 x 160x120, M = 1024 "
+                         "(the reference's CPU-runnable case); 4: 10 m scene, 0.02 m grid (P = 1.7 B)")
     ap.add_argument("--coarse", type=int, default=96, help="coarse samples per ray (c5 sweep)")
     ap.add_argument("--no-smooth", action="store_true", help="lambda_smooth = 0 (c5 sweep)")
     ap.add_argument("--refine-poses", action="store_true",
@@ -335,6 +342,8 @@ def main():
     cfg.refine_poses = bool(args.refine_poses)
     if args.config == 4:
         ds = scenes.config4(frames=args.frames, threads=min(8, os.cpu_count() or 1))
+    elif args.config == 1:
+        ds = scenes.config1(frames=20)
     else:
         ds = scenes.config2(frames=args.frames, threads=min(8, os.cpu_count() or 1))
     model = optimizer.build_model(ds, cfg, skip_init=True, device=dev)
