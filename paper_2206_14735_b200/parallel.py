@@ -15,10 +15,12 @@ points:
    wire bytes of one all-reduce, with Adam's HBM bytes divided by N (ZeRO-1;
    Adam m / v are valid on the owning rank, ``gather_adam_state`` assembles
    them for a checkpoint).  ``shard_adam=False`` keeps the all-reduce +
-   replicated Adam form.  With NCCL the backward runs in two launches and
-   the geometry grids' reduce-scatter (their gradients are final after the
-   geometry backward) overlaps the colour backward on NCCL's stream; the
-   rest of the arena follows.
+   replicated Adam form.  ``overlap=True`` (NCCL, opt-in) runs the backward in
+   two launches and issues the geometry grids' reduce-scatter (their
+   gradients are final after the geometry backward) under the colour
+   backward; off by default: the colour backward fills the register file, so
+   concurrent kernels cannot share its SMs (a single-GPU overlap of Adam with
+   it measured slower), and this run has no multi-GPU box to measure on.
 
 Rank 0 owns the smoothness points; every loss keeps its global normaliser
 (``m_global``, ``smooth_global``)."""
@@ -59,7 +61,7 @@ class DataParallelStep:
     ``model.arena.grads`` tensor); ``dist`` is ``torch.distributed`` with an
     initialised process group (NCCL on GPUs, gloo in the CPU tests)."""
 
-    def __init__(self, engine, dist, group=None, shard_adam=True, overlap=True):
+    def __init__(self, engine, dist, group=None, shard_adam=True, overlap=False):
         self.engine = engine
         self.dist = dist
         self.group = group
