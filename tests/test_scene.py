@@ -73,3 +73,28 @@ def test_device_render_dataset_is_a_dataset():
     np.testing.assert_array_equal(ds.colors_u8, host.colors_u8)
     np.testing.assert_array_equal(ds.depths_mm, host.depths_mm)
     assert ds.n_valid == host.n_valid
+
+
+def test_scene_program_flattening_and_validation():
+    """The CSG tree becomes a postfix program (Complement -> NEG, Union -> MIN
+    over its children in order); the library rejects malformed programs
+    before launching anything (no GPU needed)."""
+    import ctypes as C
+    from paper_2206_14735_b200 import _lib, scenes
+    S = scenes.scene_program(scenes.sphere_in_box())
+    ops = [(S.op[i][0], S.op[i][1]) for i in range(S.n_ops)]
+    assert ops == [(0, 0), (1, 0), (0, 1), (2, 2)]
+    assert S.prim[0][0] == 1.0 and S.prim[1][0] == 0.0  # room box, then the ball
+    assert S.prim[0][13] == 0.25  # checker size of the room
+    L = _lib.lib()
+    O = _lib.RenderOpts()
+    dummy = C.c_void_p(16)
+    bad = scenes.scene_program(scenes.scannet_room())
+    bad.op[bad.n_ops - 1][1] = 9  # MIN over more entries than the stack holds
+    rc = L.gsb_render_frames(C.byref(bad), dummy, 1, 4, 4, 1.0, 1.0, 2.0, 2.0, 8.0, None, 0.0, C.byref(O),
+                             dummy, dummy, None)
+    assert rc == -1  # GSB_E_ARG
+    S.n_ops = 3  # leaves two entries on the stack
+    rc = L.gsb_render_frames(C.byref(S), dummy, 1, 4, 4, 1.0, 1.0, 2.0, 2.0, 8.0, None, 0.0, C.byref(O),
+                             dummy, dummy, None)
+    assert rc == -1
