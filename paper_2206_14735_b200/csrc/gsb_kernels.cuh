@@ -850,7 +850,7 @@ __device__ __forceinline__ T warp_allsum(T v) {
 }
 
 template <typename T>
-__global__ void __launch_bounds__(128) k_render(Ws<T> w, int M, int N, const double* __restrict__ dep,
+__global__ void __launch_bounds__(128, 11) k_render(Ws<T> w, int M, int N, const double* __restrict__ dep,
                                                 const T* __restrict__ params, int64_t log_s_off,
                                                 LossW L) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
