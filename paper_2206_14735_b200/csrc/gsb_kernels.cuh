@@ -201,60 +201,73 @@ __device__ __forceinline__ PixelRay pixel_ray(const gsb_dataset_t& D, int64_t fl
 }
 
 template <typename T>
-__global__ void k_ray_setup(gsb_dataset_t D, const int64_t* __restrict__ ids, int M, int ray_base,
-                            Ws<T> w, Geo G, int Nc, double nearv, double max_depth, int has_ff,
-                            double ff, gsb_pcg64_t rng) {
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= M) return;
-  PixelRay P = pixel_ray(D, ids[i]);
-  const double* pose = D.poses + P.frame * 12;
-  T r[3];
-  rotate<T>(pose, P.dir[0], P.dir[1], P.dir[2], r);
-  T o[3] = {(T)pose[9], (T)pose[10], (T)pose[11]};
-  double od[3], rd[3];
-#pragma unroll
-  for (int a = 0; a < 3; ++a) {
-    w.o[i * 3 + a] = o[a];
-    w.r[i * 3 + a] = r[a];
-    od[a] = (double)o[a];
-    rd[a] = (double)r[a];
-    w.od[i * 3 + a] = od[a];
-    w.rd[i * 3 + a] = rd[a];
-    w.col[i * 3 + a] = (T)P.col[a];
-  }
-  // decode_color's unit view-direction check (gs/decoders.py:96-98), in dtype
-  T n2 = (r[0] * r[0] + r[1] * r[1]) + r[2] * r[2];
-  if (fabs((double)sqrt(n2) - 1.0) > 1e-6) atomicOr(w.status + GSB_ST_VIEWDIR, 1);
-  w.dray[i] = P.depth_ray;
-  w.valid[i] = P.valid;
-  double farv;
-  if (has_ff) {
-    farv = ff;
-  } else {  // _box_exit, gs/renderer.py:228-233
-    double ex = 0.0;
+__global__ void __launch_bounds__(128) k_ray_setup(gsb_dataset_t D, const int64_t* __restrict__ ids, int M,
+                                                   int ray_base, Ws<T> w, Geo G, int Nc, double nearv,
+                                                   double max_depth, int has_ff, double ff, gsb_pcg64_t rng) {
+  // 32 rays per block: threads 0..31 set the rays up, then all 128 threads
+  // fill the stratified depths, 4 threads per ray (each jumps its own PCG
+  // stream to its first sample)
+  __shared__ double s_near[32], s_span[32];
+  const int t = threadIdx.x;
+  const int i = blockIdx.x * 32 + t;
+  if (t < 32 && i < M) {
+    PixelRay P = pixel_ray(D, ids[i]);
+    const double* pose = D.poses + P.frame * 12;
+    T r[3];
+    rotate<T>(pose, P.dir[0], P.dir[1], P.dir[2], r);
+    T o[3] = {(T)pose[9], (T)pose[10], (T)pose[11]};
+    double od[3], rd[3];
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
-      double rr = fabs(rd[a]) < 1e-12 ? 1e-12 : rd[a];
-      double t1 = (G.lo[a] - od[a]) / rr;
-      double t2 = (G.hi[a] - od[a]) / rr;
-      double tm = t1 >= t2 ? t1 : t2;
-      ex = (a == 0 || tm < ex) ? tm : ex;
+      w.o[i * 3 + a] = o[a];
+      w.r[i * 3 + a] = r[a];
+      od[a] = (double)o[a];
+      rd[a] = (double)r[a];
+      w.od[i * 3 + a] = od[a];
+      w.rd[i * 3 + a] = rd[a];
+      w.col[i * 3 + a] = (T)P.col[a];
     }
-    farv = ex <= max_depth ? ex : max_depth;
+    // decode_color's unit view-direction check (gs/decoders.py:96-98), in dtype
+    T n2 = (r[0] * r[0] + r[1] * r[1]) + r[2] * r[2];
+    if (fabs((double)sqrt(n2) - 1.0) > 1e-6) atomicOr(w.status + GSB_ST_VIEWDIR, 1);
+    w.dray[i] = P.depth_ray;
+    w.valid[i] = P.valid;
+    double farv;
+    if (has_ff) {
+      farv = ff;
+    } else {  // _box_exit, gs/renderer.py:228-233
+      double ex = 0.0;
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        double rr = fabs(rd[a]) < 1e-12 ? 1e-12 : rd[a];
+        double t1 = (G.lo[a] - od[a]) / rr;
+        double t2 = (G.hi[a] - od[a]) / rr;
+        double tm = t1 >= t2 ? t1 : t2;
+        ex = (a == 0 || tm < ex) ? tm : ex;
+      }
+      farv = ex <= max_depth ? ex : max_depth;
+    }
+    double nf = nearv + 0.05;
+    farv = farv >= nf ? farv : nf;
+    w.nearv[i] = nearv;
+    w.farv[i] = farv;
+    s_near[t] = nearv;
+    s_span[t] = farv - nearv;
   }
-  double nf = nearv + 0.05;
-  farv = farv >= nf ? farv : nf;
-  w.nearv[i] = nearv;
-  w.farv[i] = farv;
-  // stratified_coarse (gs/sampler.py:91-107) with uniform row (ray_base+i)
+  __syncthreads();
+  // stratified_coarse (gs/sampler.py:91-107) with uniform row (ray_base + ray)
+  const int rl = t >> 2, q = t & 3, ray = blockIdx.x * 32 + rl;
+  if (ray >= M) return;
+  const int chunk = (Nc + 3) / 4, j0 = q * chunk, j1 = min(Nc, j0 + chunk);
+  if (j0 >= j1) return;
   Pcg g;
   g.init(rng);
-  g.advance((uint64_t)(ray_base + i) * (uint64_t)Nc);
-  double span = farv - nearv;
-  double* dep = w.dep[0] + (int64_t)i * w.ld;
-  for (int j = 0; j < Nc; ++j) {
+  g.advance((uint64_t)(ray_base + ray) * (uint64_t)Nc + (uint64_t)j0);
+  const double nv = s_near[rl], span = s_span[rl];
+  double* dep = w.dep[0] + (int64_t)ray * w.ld;
+  for (int j = j0; j < j1; ++j) {
     double u = g.next_double();
-    dep[j] = nearv + span * (((double)j + u) / (double)Nc);
+    dep[j] = nv + span * (((double)j + u) / (double)Nc);
   }
 }
 
