@@ -3,7 +3,7 @@ import ctypes as C
 import sys
 import os
 import numpy as np
-HERE = os.path.dirname(os.path.abspath(__file__))
+HERE = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests")
 sys.path.insert(0, os.path.dirname(HERE)); sys.path.insert(0, HERE)
 import torch
 from test_pose import golden, _device_setup, _intr
