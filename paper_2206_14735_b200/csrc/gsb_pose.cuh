@@ -417,7 +417,7 @@ __global__ void __launch_bounds__(128) k_pose_ray(Ws<T> w, gsb_dataset_t D, cons
 
 // block per frame: R_bar, t_bar over the frame's rays, exp_so3 adjoint
 template <typename T>
-__global__ void __launch_bounds__(256) k_pose_frames(int M, gsb_pose_t P, const T* __restrict__ params,
+__global__ void __launch_bounds__(1024) k_pose_frames(int M, gsb_pose_t P, const T* __restrict__ params,
                                                      const double* __restrict__ rbar, T* __restrict__ grads) {
   const int f = blockIdx.x;
   const int64_t no = P.nu_offset[f], to = P.t_offset[f];
@@ -431,7 +431,7 @@ __global__ void __launch_bounds__(256) k_pose_frames(int M, gsb_pose_t P, const 
 #pragma unroll
     for (int k = 0; k < 12; ++k) acc[k] += r[k];
   }
-  __shared__ double red[8][12];
+  __shared__ double red[32][12];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 #pragma unroll
   for (int i = 0; i < 12; ++i) {

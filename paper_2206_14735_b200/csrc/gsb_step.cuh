@@ -552,7 +552,7 @@ int run_pose_grad(const gsb_model_t* model, const gsb_dataset_t* data, const gsb
   }
   k_pose_ray<T><<<(z.M + 3) / 4, 128, 0, stream>>>(w, *data, st->ray_ids, z.M, z.N, dep, xbar, rbar);
   GSB_LAUNCHED_T("k_pose_ray");
-  k_pose_frames<T><<<pose->n_frames, 256, 0, stream>>>(z.M, *pose, params, rbar, grads);
+  k_pose_frames<T><<<pose->n_frames, 1024, 0, stream>>>(z.M, *pose, params, rbar, grads);
   GSB_LAUNCHED_T("k_pose_frames");
   return GSB_OK;
 }
