@@ -47,6 +47,11 @@ def exp_so3_data(nu):
     return np.eye(3) + a * K + b * (K @ K)
 
 
+# the graph form's values (gs/camera.py:96-122): the device step evaluates the
+# graph itself (gsb_pose_table); on the host the array form serves both
+exp_so3 = exp_so3_data
+
+
 class PoseParam:
     """Camera-to-world pose R = R0 exp(nu^), t (gs/camera.py:53-90).
 
@@ -160,3 +165,44 @@ def project(intr, c2w, points):
     z = pc[:, 2]
     safe = np.where(np.abs(z) > 1e-12, z, 1e-12)
     return intr.fx * pc[:, 0] / safe + intr.cx, intr.fy * pc[:, 1] / safe + intr.cy, z
+
+
+def backproject(intr, pose, pixels):
+    """World-space rays through pixels of one camera (gs/camera.py:174-210):
+    (origins, unit directions) as (N, 3) arrays; `pose` is a PoseParam or a
+    4x4 camera-to-world matrix."""
+    if isinstance(pose, PoseParam):
+        m = pose.matrix()
+    else:
+        m = np.asarray(pose, dtype=np.float64)
+    d_cam = pixel_rays(intr, pixels)
+    dirs = d_cam @ m[:3, :3].T
+    origins = np.broadcast_to(m[:3, 3], dirs.shape).copy()
+    return origins, dirs
+
+
+def pose_errors(estimated, ground_truth):
+    """Mean translation error (m) and mean geodesic rotation error (degrees)
+    between two (F, 4, 4) camera-to-world stacks (gs/camera.py:213-227)."""
+    est = np.asarray(estimated, dtype=np.float64)
+    gt = np.asarray(ground_truth, dtype=np.float64)
+    if est.shape != gt.shape:
+        raise ValueError("pose count mismatch")
+    trans = np.linalg.norm(est[:, :3, 3] - gt[:, :3, 3], axis=1)
+    rel = np.einsum("fij,fik->fjk", est[:, :3, :3], gt[:, :3, :3])  # R_est^T R_gt
+    cos = np.clip((np.trace(rel, axis1=1, axis2=2) - 1.0) / 2.0, -1.0, 1.0)
+    return float(trans.mean()), float(np.degrees(np.arccos(cos)).mean())
+
+
+def perturb_pose(c2w, trans_mag, rot_mag_deg, rng):
+    """A pose offset by exactly `trans_mag` metres and `rot_mag_deg` degrees in
+    random directions (gs/camera.py:230-243): the translation direction, then
+    the rotation axis, each drawn as a normalised 3-vector of normals."""
+    out = np.asarray(c2w, dtype=np.float64).copy()
+    step = rng.normal(size=3)
+    step /= np.linalg.norm(step)
+    axis = rng.normal(size=3)
+    axis /= np.linalg.norm(axis)
+    out[:3, 3] += trans_mag * step
+    out[:3, :3] = out[:3, :3] @ exp_so3_data(axis * np.radians(rot_mag_deg))
+    return out

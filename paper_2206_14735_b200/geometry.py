@@ -18,6 +18,11 @@ import numpy as np
 from . import _lib, seeds
 
 
+from .model import HIDDEN_WIDTH, DecoderNet  # noqa: E402,F401  (gs/decoders.py:22-76)
+
+N_HIDDEN = 2  # hidden ReLU layers of each decoder (gs/decoders.py:23)
+
+
 class InitError(RuntimeError):
     """Geometric initialization failed to reach tolerance in budget."""
 

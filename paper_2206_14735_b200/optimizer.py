@@ -209,6 +209,11 @@ def _device(device=None):
     return torch.device("cuda", torch.cuda.current_device())
 
 
+def derive_bounds(dataset, cfg):
+    """gs/optimizer.py:146-178 (model.derive_bounds)."""
+    return mdl.derive_bounds(Dataset.wrap(dataset), cfg)
+
+
 def build_model(dataset, cfg, initial_poses=None, skip_init=False, device=None):
     """gs/optimizer.py:181-214: grids, decoders, sharpness, poses."""
     dataset = Dataset.wrap(dataset)

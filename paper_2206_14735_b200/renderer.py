@@ -15,6 +15,7 @@ import numpy as np
 
 from . import _lib
 from .engine import StepEngine, draw_smooth_points, host_draws
+from .model import ModelState  # noqa: F401  (gs/renderer.py:69-105)
 from .sampler import batch_ray_ids
 
 __all__ = ["LossWeights", "train_objective", "grad", "Objective", "draw_smooth_points",
@@ -195,3 +196,20 @@ def _with(cfg, **kw):
     for k, v in kw.items():
         setattr(c, k, v)
     return c
+
+
+def realized_pose_arrays(model, frames):
+    """gs/renderer.py:218-225: rows R (U, 9) and t (U, 3) of the given frames,
+    in the model dtype, as the step realises them (R0 exp_so3(nu), t)."""
+    frames = np.asarray(frames, dtype=np.int64).reshape(-1)
+    dt = model.dtype
+    R = np.stack([(model.poses[f].R0.astype(dt) @ _exp_dt(model.poses[f].nu_data(), dt)).reshape(9)
+                  for f in frames]) if len(frames) else np.zeros((0, 9), dt)
+    T = np.stack([np.asarray(model.poses[f].t_data(), dtype=dt) for f in frames]) if len(frames) \
+        else np.zeros((0, 3), dt)
+    return R.astype(dt), T.astype(dt)
+
+
+def _exp_dt(nu, dt):
+    from .camera import exp_so3_data
+    return exp_so3_data(np.asarray(nu, dtype=np.float64)).astype(dt)

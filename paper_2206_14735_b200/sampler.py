@@ -87,3 +87,38 @@ def stratified_coarse(near, far, n, uniforms):
         raise ValueError("degenerate ray bounds")
     steps = (np.arange(n) + uniforms) / n
     return near[:, None] + (far - near)[:, None] * steps
+
+
+def importance_refine_with_sources(depths, weights, near, far, uniforms):
+    """gs/sampler.py:128-169 on the device (gsb_importance_refine): invert the
+    piecewise-constant weight CDF, merge stably, enforce the 1e-9 separation.
+    Returns ((M, K + A) depths, (M, K + A) int64 provenance, -1 = new/moved)."""
+    import torch
+
+    from . import _lib
+    d = np.ascontiguousarray(depths, dtype=np.float64)
+    M, K = d.shape
+    A = np.asarray(uniforms).shape[1]
+    if K + A > _lib.KMAX or A > _lib.AMAX:
+        raise ValueError("too many samples per ray for the device kernel")
+    dev = torch.device("cuda", torch.cuda.current_device())
+    ld = K + A
+    T = lambda a: torch.from_numpy(np.array(a, dtype=np.float64)).to(dev)  # a writable copy
+    dd = torch.zeros((M, ld), dtype=torch.float64, device=dev)
+    dd[:, :K] = T(d)
+    ww = torch.zeros((M, ld), dtype=torch.float64, device=dev)
+    ww[:, :K] = T(weights)
+    nt, ft, ut = T(np.broadcast_to(near, (M,))), T(np.broadcast_to(far, (M,))), T(uniforms)
+    out = torch.zeros((M, ld), dtype=torch.float64, device=dev)
+    src = torch.zeros((M, ld), dtype=torch.int32, device=dev)
+    if M:
+        _lib.check(_lib.lib().gsb_importance_refine(M, K, A, ld, dd.data_ptr(), ww.data_ptr(), nt.data_ptr(),
+                                                    ft.data_ptr(), ut.data_ptr(), out.data_ptr(),
+                                                    src.data_ptr(), _lib.stream_handle()),
+                   "gsb_importance_refine")
+    return out.cpu().numpy(), src.cpu().numpy().astype(np.int64)
+
+
+def importance_refine(depths, weights, near, far, uniforms):
+    """gs/sampler.py:110-125."""
+    return importance_refine_with_sources(depths, weights, near, far, uniforms)[0]

@@ -406,3 +406,18 @@ def test_deterministic_scatter_mode(precision):
     if precision == "double":  # and against the reference's own gradients
         for n, a in zip(model.param_names(), g1):
             assert rel_maxnorm(a, G.a[f"grad_{n}"]) <= GRAD_TOL[precision], n
+
+
+def test_sampler_importance_refine_public_api():
+    """sampler.importance_refine_with_sources (the reference's public name)
+    runs gsb_importance_refine and reproduces the recorded reference rounds."""
+    G = load("small", "double")
+    R = _rounds_inputs(G, 0)
+    for r in range(G.cfg.importance_rounds):
+        d_in = G.a[f"round{r}_depths_in"]
+        out, src = sampler.importance_refine_with_sources(d_in, G.a[f"round{r}_weights"], G.cfg.near,
+                                                          R["far"], G.a[f"round{r}_uniforms"])
+        np.testing.assert_array_equal(out, G.a[f"round{r}_depths"])
+        np.testing.assert_array_equal(src, G.a[f"round{r}_src"])
+        np.testing.assert_array_equal(sampler.importance_refine(d_in, G.a[f"round{r}_weights"], G.cfg.near,
+                                                                R["far"], G.a[f"round{r}_uniforms"]), out)
