@@ -421,3 +421,22 @@ def test_sampler_importance_refine_public_api():
         np.testing.assert_array_equal(src, G.a[f"round{r}_src"])
         np.testing.assert_array_equal(sampler.importance_refine(d_in, G.a[f"round{r}_weights"], G.cfg.near,
                                                                 R["far"], G.a[f"round{r}_uniforms"]), out)
+
+
+@pytest.mark.parametrize("precision", ["double", "single"])
+def test_feature_grid_sample_public_api(precision):
+    """feature_grid.sample / sample_multi (gs/feature_grid.py:120-139) run the
+    exact device twin: bit-identical to the numba gather restated by the oracle."""
+    from paper_2206_14735_b200 import feature_grid
+    G = load("small", precision)
+    model, ds, cfg = gpu_model(G)
+    P = oracle_params(G)
+    rng = np.random.default_rng(5)
+    lo, hi = model.grid.clamp_box()
+    pts = (lo + rng.random((500, 3)) * (hi - lo)).astype(G.dtype)
+    got = feature_grid.sample_multi(model.grid, pts)
+    _, ref = O.sample_multi(P, pts)
+    np.testing.assert_array_equal(got, ref)
+    np.testing.assert_array_equal(feature_grid.sample(model.grid.color, pts), O.LevelSample(P.color, pts).value())
+    with pytest.raises(renderer.GridBoundsError):
+        feature_grid.sample(model.grid.levels[0], np.array([[1e3, 0.0, 0.0]]))

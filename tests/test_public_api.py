@@ -17,12 +17,15 @@ REF_SRC = "/root/reference/pkg/src"
 
 # reference module -> package module
 PAIRS = {"optimizer": "optimizer", "renderer": "renderer", "sampler": "sampler", "camera": "camera",
-         "scenegen": "scenes", "seeds": "seeds", "checkpoint": "checkpoint", "decoders": "geometry"}
+         "scenegen": "scenes", "seeds": "seeds", "checkpoint": "checkpoint", "decoders": "geometry",
+         "feature_grid": "feature_grid"}
 # names deliberately not mirrored: graph-level (dc.Tensor) helpers the fused step replaces
 NOT_MIRRORED = {"renderer": {"alphas", "composite", "render_weights_data", "loss_rgb_depth", "loss_sdf_fs",
                              "loss_eikonal"},
                 "sampler": {"enforce_separation"},
-                "decoders": {"decode_sdf", "decode_color"}}
+                "decoders": {"decode_sdf", "decode_color"},
+                # analysis helpers of the reference's own autodiff tests
+                "feature_grid": {"sample_jacobian", "sample_hessian_xx", "sample_hessian_xtheta"}}
 
 
 def _reference(name):
