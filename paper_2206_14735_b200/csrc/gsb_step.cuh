@@ -40,6 +40,15 @@ inline int t5_mode() {
   return v;
 }
 inline bool use_t5(bool coarse = true) { return t5_mode() == 1 || (t5_mode() == 2 && coarse); }
+// taped forward form: GSB_T5_FWD=0 mma.sync (tc::k_fwd_tc); k > 0 tcgen05
+// (t5::k_fwd_t5) with k CTAs per SM (3 or 4; register cap 170 / 128)
+inline int t5_fwd_mode() {
+  static const int v = [] {
+    const char* e = std::getenv("GSB_T5_FWD");
+    return e ? std::atoi(e) : 4;
+  }();
+  return v;
+}
 inline int sm_count() {
   static const int v = [] {
     int dev = 0, n = 0;
@@ -127,8 +136,8 @@ int run_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step
       w.pose_g = reinterpret_cast<T*>(sc + PL.g);
       w.pose_fb = reinterpret_cast<T*>(sc + PL.fb);
     }
-    static_assert(tc::kFragBufU4 == 4096 + 68 + 768, "workspace carve");
-    tc::k_wfrag<S><<<tc::Fr<S>::NALL + 5, 128, 0, stream>>>(mlp32, w.wfrag);
+    static_assert(tc::kFragBufU4 == 4096 + 68 + 2304, "workspace carve");
+    tc::k_wfrag<S><<<tc::Fr<S>::NALL + 1 + tc::UmmaW::kTiles, 128, 0, stream>>>(mlp32, w.wfrag);
     GSB_LAUNCHED_T("k_wfrag");
   }
   const size_t smem_sdf = (size_t)S::NG * esz;
@@ -204,10 +213,21 @@ int run_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step
     if (runA) {
     if constexpr (F32) {
       constexpr int FW = 4;  // warps per CTA of the taped forward
-      GSB_CHECK(cudaFuncSetAttribute(tc::k_fwd_tc<S, FW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)tc::FwdTc<S, FW>::smem()));
-      tc::k_fwd_tc<S, FW><<<(int)((ns + FW * 32 - 1) / (FW * 32)), FW * 32, tc::FwdTc<S, FW>::smem(),
-                            stream>>>(w, G, M, N, mlp32, dep_final, spts, nsp);
+      if (const int cps = t5_fwd_mode(); cps > 0) {
+        const int64_t tiles = (ns + t5::kTile - 1) / t5::kTile;
+        const int grid = (int)std::min<int64_t>(tiles, (int64_t)sm_count() * (cps == 3 ? 3 : 4));
+        if (grid > 0) {
+          if (cps == 3)
+            t5::k_fwd_t5<S, 3><<<grid, t5::kTile, t5::FwdT5::smem(), stream>>>(w, G, M, N, dep_final, spts, nsp);
+          else
+            t5::k_fwd_t5<S, 4><<<grid, t5::kTile, t5::FwdT5::smem(), stream>>>(w, G, M, N, dep_final, spts, nsp);
+        }
+      } else {
+        GSB_CHECK(cudaFuncSetAttribute(tc::k_fwd_tc<S, FW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)tc::FwdTc<S, FW>::smem()));
+        tc::k_fwd_tc<S, FW><<<(int)((ns + FW * 32 - 1) / (FW * 32)), FW * 32, tc::FwdTc<S, FW>::smem(),
+                              stream>>>(w, G, M, N, mlp32, dep_final, spts, nsp);
+      }
     } else {
       GSB_CHECK(cudaFuncSetAttribute(k_fwd<T, S, false>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fwd));
@@ -348,7 +368,7 @@ Ws<T> carve_sdf(void* ws, int64_t n, int nmlp, size_t* bytes, bool grad = true) 
   const int64_t nb = grad ? std::max<int64_t>(kNbMax, (n + 127) / 128) : 1;
   w.nb_max = (int)nb;
   w.mlp_part = c.template take<T>(nb * nmlp);
-  w.wfrag = c.template take<uint4>(4096 + 68 + 768);
+  w.wfrag = c.template take<uint4>(4096 + 68 + 2304);
   w.fin_red = c.template take<double>((int64_t)16 * nmlp);
   w.fin_cnt = c.template take<unsigned>((nmlp + 31) / 32);
   if (bytes) *bytes = c.off;
@@ -378,7 +398,7 @@ int sdf_forward(const gsb_model_t* model, Ws<T>& w, const T* pts, int64_t n, cud
   const int blocks = (int)((n + 127) / 128);
   if constexpr (sizeof(T) == 4) {
     constexpr int TW = 4;
-    tc::k_wfrag<S><<<tc::Fr<S>::NALL + 5, 128, 0, stream>>>(mlp, w.wfrag);
+    tc::k_wfrag<S><<<tc::Fr<S>::NALL + 1 + tc::UmmaW::kTiles, 128, 0, stream>>>(mlp, w.wfrag);
     GSB_LAUNCHED_T("k_wfrag");
     GSB_CHECK(cudaFuncSetAttribute(tc::k_fwd_tc<S, TW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)tc::FwdTc<S, TW>::smem()));

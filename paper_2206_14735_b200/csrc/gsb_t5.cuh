@@ -26,19 +26,23 @@ constexpr int kTile = 128;         // samples per CTA = TMEM lanes
 constexpr int kCtaPerSm = 4;       // 128 TMEM columns each: 4 x 128 = 512
 constexpr uint32_t kCols = 128;
 
-// kind::tf32, D f32, A/B K-major, N = 32, M = 128
-constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((32u >> 3) << 17) | ((128u >> 4) << 24);
+// kind::tf32, D f32, A/B K-major, M = 128, N = 32 (or 16)
+__host__ __device__ constexpr uint32_t idesc(uint32_t n) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((n >> 3) << 17) | ((128u >> 4) << 24);
+}
+constexpr uint32_t kIdesc = idesc(32);
 
 // shared-memory matrix descriptor, SWIZZLE_NONE, descriptor version 1 (sm_100)
 __device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
   return (uint64_t)((addr >> 4) & 0x3FFFu) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
          ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | ((uint64_t)1 << 46);
 }
+template <uint32_t NN = 32>
 __device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a, uint64_t b, uint32_t acc) {
   asm volatile(
       "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d),
-      "r"(a), "l"(b), "r"(kIdesc), "r"(acc));
+      "r"(a), "l"(b), "r"(idesc(NN)), "r"(acc));
 }
 __device__ __forceinline__ void commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
@@ -95,6 +99,18 @@ __device__ __forceinline__ void ld32(uint32_t ta, float (&v)[32]) {
 #pragma unroll
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
+__device__ __forceinline__ void ld16(uint32_t ta, float (&v)[16]) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(ta)
+      : "memory");
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
 // hi = x rounded to tf32 (half away at bit 13); lo = x - hi exact (the tensor
 // core reads its top 19 bits)
 __device__ __forceinline__ void split2(float x, float& hi, float& lo) {
@@ -121,16 +137,16 @@ __device__ __forceinline__ void store_a(uint32_t tl, const float* x) {
   }
 }
 
-// D[0, 32) = A (TMEM) x B (smem tiles bh / bl, K = 8 KS), 3xTF32
-template <int KS>
+// D[0, NN) = A (TMEM) x B (smem tiles bh / bl, NN x K, K = 8 KS), 3xTF32
+template <int KS, uint32_t NN = 32>
 __device__ __forceinline__ void issue_layer(uint32_t tmem, uint32_t bh, uint32_t bl) {
   constexpr uint32_t sbo = KS * 8 * 32;  // 8 rows x K fp32
 #pragma unroll
   for (int kk = 0; kk < KS; ++kk) {
     const uint32_t off = kk * 256;  // two 128-byte core matrices per k-step of 8
-    mma_ts(tmem, tmem + 64 + kk * 8, sdesc(bh + off, 128, sbo), kk > 0 ? 1u : 0u);
-    mma_ts(tmem, tmem + 32 + kk * 8, sdesc(bl + off, 128, sbo), 1u);
-    mma_ts(tmem, tmem + 32 + kk * 8, sdesc(bh + off, 128, sbo), 1u);
+    mma_ts<NN>(tmem, tmem + 64 + kk * 8, sdesc(bh + off, 128, sbo), kk > 0 ? 1u : 0u);
+    mma_ts<NN>(tmem, tmem + 32 + kk * 8, sdesc(bl + off, 128, sbo), 1u);
+    mma_ts<NN>(tmem, tmem + 32 + kk * 8, sdesc(bh + off, 128, sbo), 1u);
   }
 }
 
@@ -257,6 +273,196 @@ __global__ void __launch_bounds__(kTile) k_sdf_eval_t5(Ws<float> w, Geo G, int M
 #pragma unroll
     for (int n = 0; n < 32; ++n) acc = fmaf(fmaxf(h[n] + svec[tc::GVec::b1 + n], 0.f), svec[tc::GVec::w2 + n], acc);
     if (cur_act) phi[(int64_t)cur_ray * w.ld + cur_slot] = (double)acc;
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kCols) : "memory");
+}
+
+
+// ---------------------------------------------------------------------------
+// taped forward (same contract as tc::k_fwd_tc): per sample phi, dphi/dx and
+// colour, plus dphi/dz for pose refinement.  Six chained tcgen05 layers per
+// 128-sample tile: z W0, h0 W1, delta1 W1^T, delta0 W0^T (N = 16), then the
+// colour decoder [f_c, r] W0c, h0c W1c; the 32 -> 1 / 32 -> 3 heads and the
+// grid-space gradient are per-lane epilogues.  The next tile's gathers
+// overlap the last MMA.
+
+struct FwdT5 {
+  static constexpr size_t smem() { return (size_t)(tc::UmmaW::N + tc::GVec::N + tc::CVec::N) * 4; }
+};
+
+template <class S, int CPS>
+__global__ void __launch_bounds__(kTile, CPS) k_fwd_t5(Ws<float> w, Geo G, int M, int N,
+                                                 const double* __restrict__ dep,
+                                                 const float* __restrict__ spts, int nsp) {
+  using F = tc::Fr<S>;
+  using U = tc::UmmaW;
+  constexpr int KG = F::KG, KC = F::KC;
+  static_assert(8 * KG <= 16 && 8 * KC <= 16, "input widths");
+  extern __shared__ __align__(128) float t5_smem[];
+  float* sw = t5_smem;
+  const float* gvec = t5_smem + U::N;
+  const float* cvec = gvec + tc::GVec::N;
+  __shared__ __align__(8) uint64_t s_bar[2];
+  __shared__ uint32_t s_tmem;
+  const int64_t MN = (int64_t)M * N, NS = MN + nsp;
+  const int64_t ntiles = (NS + kTile - 1) / kTile;
+  if ((int64_t)blockIdx.x >= ntiles) return;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&s_tmem)),
+                 "r"(kCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  if (tid == 0) {
+    tc::mbar_init(&s_bar[0]);
+    tc::mbar_init(&s_bar[1]);
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  if (tid == 0) {
+    constexpr uint32_t wb = U::N * 4, vb = (tc::GVec::N + tc::CVec::N) * 4;
+    tc::mbar_expect(&s_bar[0], wb + vb);
+    tc::bulk_g2s(sw, w.wfrag + tc::kUmmaBaseU4, wb, &s_bar[0]);
+    tc::bulk_g2s(t5_smem + U::N, reinterpret_cast<const float*>(w.wfrag + tc::kVecBase), vb, &s_bar[0]);
+  }
+  const uint32_t tmem = s_tmem;
+  const uint32_t tl = tmem + ((uint32_t)(warp * 32) << 16);
+  auto sa = [&](int off) { return smem_u32(sw + off); };
+  uint32_t phase = 0;
+  auto run = [&](auto issue) {  // all lanes' A stores -> one thread issues -> wait for D
+    cta_sync_tmem();
+    if (tid == 0) {
+      issue();
+      commit(&s_bar[1]);
+    }
+  };
+  auto wait_d = [&]() {
+    tc::mbar_wait(&s_bar[1], phase);
+    phase ^= 1u;
+    fence_after();
+  };
+  // lane-per-sample inputs of one tile
+  int64_t s;
+  int ray;
+  bool act;
+  LocT<float> loc[S::NL];
+  float z[8 * KG], inp[8 * KC];
+  auto gather = [&](int64_t tile) {
+    s = tile * kTile + tid;
+    act = s < NS;
+    ray = -1;
+    float p[3];
+    if (act && s < MN) {
+      ray = (int)((uint32_t)s / (uint32_t)N);
+      taped_point<float>(w.o + ray * 3, w.r + ray * 3,
+                         dep[(int64_t)ray * w.ld + (int)((uint32_t)s % (uint32_t)N)], G.lo, G.hi, p);
+    } else if (act) {
+#pragma unroll
+      for (int a = 0; a < 3; ++a) p[a] = spts[(s - MN) * 3 + a];
+    } else {
+#pragma unroll
+      for (int a = 0; a < 3; ++a) p[a] = (float)G.lo[a];
+    }
+#pragma unroll
+    for (int i = 0; i < 8 * KG; ++i) z[i] = 0.f;
+#pragma unroll
+    for (int l = 0; l < S::NL; ++l) {
+      loc[l] = compact<float>(locate<false>(G.lv[l], (double)p[0], (double)p[1], (double)p[2],
+                                            act ? w.status : nullptr));
+      gather_fast<float, S::CG>(G.lv[l], loc[l], z + l * S::CG);
+    }
+    const int cr = ray < 0 ? 0 : ray;  // smoothness points: harmless colour, not stored
+    const Loc qc = locate<false>(G.col, (double)p[0], (double)p[1], (double)p[2], nullptr);
+#pragma unroll
+    for (int i = 0; i < 8 * KC; ++i) inp[i] = 0.f;
+    gather_fast<float, S::CC>(G.col, compact<float>(qc), inp);
+#pragma unroll
+    for (int a = 0; a < 3; ++a) inp[S::CC + a] = w.r[cr * 3 + a];
+  };
+  gather(blockIdx.x);
+  tc::mbar_wait(&s_bar[0], 0);
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    float h[32];
+    uint32_t m0 = 0u;
+    // ---- geometry layer 0 / 1 (gs/decoders.py:40-60)
+    store_a<KG>(tl, z);
+    run([&] { issue_layer<KG>(tmem, sa(U::W0H), sa(U::W0L)); });
+    wait_d();
+    ld32(tl, h);
+#pragma unroll
+    for (int n = 0; n < 32; ++n) {
+      const float v = h[n] + gvec[tc::GVec::b0 + n];
+      const bool pos = v > 0.f;
+      h[n] = pos ? v : 0.f;
+      m0 |= (uint32_t)pos << n;
+    }
+    store_a<4>(tl, h);
+    run([&] { issue_layer<4>(tmem, sa(U::W1H), sa(U::W1L)); });
+    wait_d();
+    ld32(tl, h);
+    float phi = gvec[tc::GVec::b2];
+#pragma unroll
+    for (int n = 0; n < 32; ++n) {
+      const float v = h[n] + gvec[tc::GVec::b1 + n];
+      const bool pos = v > 0.f;
+      phi = fmaf(pos ? v : 0.f, gvec[tc::GVec::w2 + n], phi);
+      h[n] = pos ? gvec[tc::GVec::w2 + n] : 0.f;  // delta1
+    }
+    // ---- dphi/dz = W0 ((W1 delta1) . m0)
+    store_a<4>(tl, h);
+    run([&] { issue_layer<4>(tmem, sa(U::W1NH), sa(U::W1NL)); });
+    wait_d();
+    ld32(tl, h);
+#pragma unroll
+    for (int n = 0; n < 32; ++n) h[n] = ((m0 >> n) & 1u) ? h[n] : 0.f;
+    store_a<4>(tl, h);
+    run([&] { issue_layer<4, 16>(tmem, sa(U::W0NH), sa(U::W0NL)); });
+    wait_d();
+    float gz[16];
+    ld16(tl, gz);
+    float gr[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+    for (int l = 0; l < S::NL; ++l) level_dx_fast<float, S::CG>(G.lv[l], loc[l], gz + l * S::CG, gr);
+    // ---- colour: sigmoid(MLP_c([f_c, r]))  (gs/decoders.py:86-99)
+    store_a<KC>(tl, inp);
+    run([&] { issue_layer<KC>(tmem, sa(U::C0H), sa(U::C0L)); });
+    wait_d();
+    ld32(tl, h);
+#pragma unroll
+    for (int n = 0; n < 32; ++n) h[n] = fmaxf(h[n] + cvec[tc::CVec::b0 + n], 0.f);
+    store_a<4>(tl, h);
+    run([&] { issue_layer<4>(tmem, sa(U::C1H), sa(U::C1L)); });
+    const int64_t cs = s;
+    const int cray = ray;
+    const bool cact = act;
+    if (tile + gridDim.x < ntiles) gather(tile + gridDim.x);  // overlaps the last MMA
+    wait_d();
+    ld32(tl, h);
+    float y[3] = {cvec[tc::CVec::b2], cvec[tc::CVec::b2 + 1], cvec[tc::CVec::b2 + 2]};
+#pragma unroll
+    for (int n = 0; n < 32; ++n) {
+      const float v = fmaxf(h[n] + cvec[tc::CVec::b1 + n], 0.f);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) y[c] = fmaf(v, cvec[tc::CVec::w2 + n * 3 + c], y[c]);
+    }
+    if (cact) {
+      w.sphi[cs] = phi;
+#pragma unroll
+      for (int a = 0; a < 3; ++a) w.sgphi[cs * 3 + a] = gr[a];
+      if (cray >= 0) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) w.scol[cs * 3 + c] = sigmoid_fast(y[c]);
+        if (w.pose_g) {
+#pragma unroll
+          for (int i = 0; i < S::IN_G; ++i) w.pose_g[cs * S::IN_G + i] = gz[i];
+        }
+      }
+    }
   }
   fence_before();
   __syncthreads();

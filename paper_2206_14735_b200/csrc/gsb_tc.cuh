@@ -40,7 +40,13 @@ struct CVec {
 // tcgen05 operand block (gsb_t5.cuh): geometry W0 / W1 as B operands (out x in,
 // canonical K-major, no swizzle), tf32 hi and lo tiles; float offsets
 struct UmmaW {
-  static constexpr int W0H = 0, W0L = 512, W1H = 1024, W1L = 2048, N = 3072;
+  // geometry W0^T, W1^T (forward), W1, W0 (delta chain: B[n][k] = W[n][k]),
+  // colour W0c^T, W1c^T; hi then lo tile each
+  static constexpr int W0H = 0, W0L = 512, W1H = 1024, W1L = 2048;
+  static constexpr int W1NH = 3072, W1NL = 4096, W0NH = 5120, W0NL = 5632;
+  static constexpr int C0H = 6144, C0L = 6656, C1H = 7168, C1L = 8192;
+  static constexpr int N = 9216;
+  static constexpr int kTiles = 12;
 };
 constexpr int kUmmaBaseU4 = kVecBase + (GVec::N + CVec::N) / 4;
 constexpr int kFragBufU4 = kUmmaBaseU4 + UmmaW::N / 4;
@@ -120,16 +126,28 @@ template <class S>
 __global__ void __launch_bounds__(128) k_wfrag(const float* __restrict__ mlp, uint4* __restrict__ out) {
   using F = Fr<S>;
   const int id = blockIdx.x, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
-  if (id > F::NALL) {  // tcgen05 B tiles: 1 W0 hi, 2 W0 lo, 3 W1 hi, 4 W1 lo
-    const int tile = id - F::NALL - 1, lo = tile & 1;
-    const bool l1 = tile >= 2;
-    const int K = l1 ? GSB_HID : 8 * F::KG, rows = l1 ? GSB_HID : S::IN_G;
-    const int oW = l1 ? S::oGW1 : S::oGW0;
-    float* o = reinterpret_cast<float*>(out + kUmmaBaseU4) + (l1 ? (lo ? UmmaW::W1L : UmmaW::W1H)
-                                                                  : (lo ? UmmaW::W0L : UmmaW::W0H));
-    for (int i = threadIdx.x; i < GSB_HID * K; i += blockDim.x) {
-      const int n = i / K, k = i % K;  // B[n][k] = W[k][n]
-      const float v = k < rows ? mlp[oW + k * GSB_HID + n] : 0.f;
+  if (id > F::NALL) {  // tcgen05 B tiles (UmmaW), hi / lo per matrix
+    const int tile = id - F::NALL - 1, lo = tile & 1, mat = tile >> 1;
+    // mat: 0 W0^T, 1 W1^T, 2 W1, 3 W0, 4 W0c^T, 5 W1c^T.  B[n][k] with K contiguous
+    int oW, K, Nn, rows, off;
+    bool tr;  // true: B[n][k] = W[k][n] (W stored (in, out) row-major, 32 columns)
+    switch (mat) {
+      case 0: oW = S::oGW0; K = 8 * F::KG; Nn = GSB_HID; rows = S::IN_G; tr = true; off = lo ? UmmaW::W0L : UmmaW::W0H; break;
+      case 1: oW = S::oGW1; K = GSB_HID; Nn = GSB_HID; rows = GSB_HID; tr = true; off = lo ? UmmaW::W1L : UmmaW::W1H; break;
+      case 2: oW = S::oGW1; K = GSB_HID; Nn = GSB_HID; rows = GSB_HID; tr = false; off = lo ? UmmaW::W1NL : UmmaW::W1NH; break;
+      case 3: oW = S::oGW0; K = GSB_HID; Nn = 16; rows = S::IN_G; tr = false; off = lo ? UmmaW::W0NL : UmmaW::W0NH; break;
+      case 4: oW = S::oCW0; K = 8 * F::KC; Nn = GSB_HID; rows = S::IN_C; tr = true; off = lo ? UmmaW::C0L : UmmaW::C0H; break;
+      default: oW = S::oCW1; K = GSB_HID; Nn = GSB_HID; rows = GSB_HID; tr = true; off = lo ? UmmaW::C1L : UmmaW::C1H; break;
+    }
+    float* o = reinterpret_cast<float*>(out + kUmmaBaseU4) + off;
+    for (int i = threadIdx.x; i < Nn * K; i += blockDim.x) {
+      const int n = i / K, k = i % K;
+      float v = 0.f;
+      if (tr) {
+        if (k < rows) v = mlp[oW + k * GSB_HID + n];
+      } else {
+        if (n < rows) v = mlp[oW + n * GSB_HID + k];  // W rows are the outputs here
+      }
       uint32_t h, l;
       split_tf32(v, h, l);
       o[kmaj(n, k, K)] = __uint_as_float(lo ? l : h);
