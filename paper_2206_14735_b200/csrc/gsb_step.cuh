@@ -42,6 +42,14 @@ inline int t5_mode() {
 inline bool use_t5(bool coarse = true) { return t5_mode() == 1 || (t5_mode() == 2 && coarse); }
 // taped forward form: GSB_T5_FWD=0 mma.sync (tc::k_fwd_tc); k > 0 tcgen05
 // (t5::k_fwd_t5) with k CTAs per SM (3 or 4; register cap 170 / 128)
+// geometry backward form: GSB_T5_BWD=1 (default) tcgen05 (t5::k_bwd_geom_t5), 0 mma.sync
+inline bool use_t5_bwd() {
+  static const bool v = [] {
+    const char* e = std::getenv("GSB_T5_BWD");
+    return e ? std::atoi(e) != 0 : true;
+  }();
+  return v;
+}
 inline int t5_fwd_mode() {
   static const int v = [] {
     const char* e = std::getenv("GSB_T5_FWD");
@@ -284,8 +292,16 @@ int run_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step
       if (runA) {
         if (w.mlp_slots)
           GSB_CHECK(cudaMemsetAsync(w.mlp_part, 0, (size_t)kMlpSlots * S::NMLP * sizeof(T), stream));
-        tc::k_bwd_geom_tc<S, WGEO><<<nb_geo, WGEO * 32, smem_g, stream>>>(w, G, M, N, mlp32,
-                                                                          dep_final, spts, nsp, 2);
+        if (use_t5_bwd()) {
+          const size_t smem_t5 = t5::GeoT5::smem();
+          GSB_CHECK(cudaFuncSetAttribute(t5::k_bwd_geom_t5<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem_t5));
+          t5::k_bwd_geom_t5<S><<<(int)((ns + t5::kTile - 1) / t5::kTile), t5::kTile, smem_t5, stream>>>(
+              w, G, M, N, dep_final, spts, nsp, 2);
+        } else {
+          tc::k_bwd_geom_tc<S, WGEO><<<nb_geo, WGEO * 32, smem_g, stream>>>(w, G, M, N, mlp32,
+                                                                            dep_final, spts, nsp, 2);
+        }
         GSB_LAUNCHED_T("k_bwd_geom");
       }
       if (runB) {

@@ -470,5 +470,321 @@ __global__ void __launch_bounds__(kTile, CPS) k_fwd_t5(Ws<float> w, Geo G, int M
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kCols) : "memory");
 }
 
+
+// ---------------------------------------------------------------------------
+// geometry backward (same contract as tc::k_bwd_geom_tc): the six
+// sample-major layers on tcgen05, two independent layers per commit
+//   S1: z W0 -> h0, m0          | v W0 -> q0 = (v W0) . m0
+//   S2: h0 W1 -> h1, m1         | q0 W1 -> dd1 = (q0 W1) . m1
+//   S3: delta1 W1^T -> delta0 = (.) . m0
+//   S4: delta0 W0^T -> dphi/dz (N = 16, stays in TMEM until the scatter)
+// column sums (db0, db1, dW2) as warp butterfly reduce-scatters; the
+// weight-gradient outer products (contraction over samples) stay on
+// mma.sync over the sample-major rows, as in the tc kernel.  256 TMEM
+// columns: D0 [0,32), D1 [32,64), A1 hi/lo [64,128), A2 hi/lo [128,192);
+// 78 KB shared memory: 2 CTAs per SM (3 CTAs with 128 columns, 5 MMA rounds
+// and a 168-register cap measured slower: 432 vs 390 us).
+
+struct GeoT5 {
+  static constexpr int ROW = 104;  // 104 % 32 = 8: fragment loads conflict-free (88 measured slower)
+  static constexpr int oA0 = 16, oM = 33, oB0 = 40, oA1 = 72;  // p z + v, m1 bits, delta0, p h0 + q0
+  static constexpr int NW = tc::UmmaW::W0NL + 512;              // geometry tiles only
+  static constexpr uint32_t kCols2 = 256;
+  static constexpr size_t smem() { return (size_t)(NW + tc::GVec::N) * 4 + (size_t)kTile * ROW * 4; }
+};
+
+// x (W columns) as tf32 hi / lo to TMEM columns chi / clo of this warp's lanes
+template <int W>
+__device__ __forceinline__ void store_hl(uint32_t tl, uint32_t chi, uint32_t clo, const float* x) {
+  float h[W], l[W];
+#pragma unroll
+  for (int i = 0; i < W; ++i) split2(x[i], h[i], l[i]);
+  if constexpr (W == 8) {
+    st8(tl + chi, h);
+    st8(tl + clo, l);
+  } else if constexpr (W == 16) {
+    st16(tl + chi, h);
+    st16(tl + clo, l);
+  } else {
+    static_assert(W == 32, "W");
+    st32(tl + chi, h);
+    st32(tl + clo, l);
+  }
+}
+template <int KS, uint32_t NN = 32>
+__device__ __forceinline__ void issue_at(uint32_t d, uint32_t ahi, uint32_t alo, uint32_t bh, uint32_t bl) {
+  constexpr uint32_t sbo = KS * 8 * 32;
+#pragma unroll
+  for (int kk = 0; kk < KS; ++kk) {
+    const uint32_t off = kk * 256;
+    mma_ts<NN>(d, alo + kk * 8, sdesc(bh + off, 128, sbo), kk > 0 ? 1u : 0u);
+    mma_ts<NN>(d, ahi + kk * 8, sdesc(bl + off, 128, sbo), 1u);
+    mma_ts<NN>(d, ahi + kk * 8, sdesc(bh + off, 128, sbo), 1u);
+  }
+}
+// column sums over the warp: lane l returns sum over lanes of v[l]
+__device__ __forceinline__ float warp_colsum32(float (&v)[32]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    const bool up = (lane & o) != 0;
+#pragma unroll
+    for (int i = 0; i < o; ++i) {
+      const float send = up ? v[i] : v[i + o];
+      v[i] = (up ? v[i + o] : v[i]) + __shfl_xor_sync(0xffffffffu, send, o);
+    }
+  }
+  return v[0];
+}
+
+template <class S>
+__global__ void __launch_bounds__(kTile, 2) k_bwd_geom_t5(Ws<float> w, Geo G, int M, int N,
+                                                         const double* __restrict__ dep,
+                                                         const float* __restrict__ spts, int nsp,
+                                                         int agg_levels) {
+  using F = tc::Fr<S>;
+  using U = tc::UmmaW;
+  using K = GeoT5;
+  constexpr int KG = F::KG, ROW = K::ROW;
+  static_assert(S::IN_G <= 16 && 8 * KG <= 16, "geometry input width");
+  extern __shared__ __align__(128) float t5_smem[];
+  float* sw = t5_smem;
+  const float* gvec = t5_smem + K::NW;
+  float* rows_all = t5_smem + K::NW + tc::GVec::N;
+  __shared__ __align__(8) uint64_t s_bar[2];
+  __shared__ uint32_t s_tmem;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&s_tmem)),
+                 "r"(K::kCols2)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  if (tid == 0) {
+    tc::mbar_init(&s_bar[0]);
+    tc::mbar_init(&s_bar[1]);
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  if (tid == 0) {
+    constexpr uint32_t wb = K::NW * 4, vb = tc::GVec::N * 4;
+    tc::mbar_expect(&s_bar[0], wb + vb);
+    tc::bulk_g2s(sw, w.wfrag + tc::kUmmaBaseU4, wb, &s_bar[0]);
+    tc::bulk_g2s(t5_smem + K::NW, reinterpret_cast<const float*>(w.wfrag + tc::kVecBase), vb, &s_bar[0]);
+  }
+  const uint32_t tmem = s_tmem;
+  const uint32_t tl = tmem + ((uint32_t)(warp * 32) << 16);
+  auto sa = [&](int off) { return smem_u32(sw + off); };
+  float* rows = rows_all + warp * 32 * ROW;
+  float* myrow = rows + lane * ROW;
+  const int64_t MN = (int64_t)M * N, NS = MN + nsp;
+  const int64_t s = (int64_t)blockIdx.x * kTile + tid;
+  const bool active = s < NS;
+  // ---- per sample: point, z and v in one pass over the corners
+  LocT<float> loc[S::NL];
+  float p = 0.f, u[3] = {0.f, 0.f, 0.f};
+  {
+    float pt[3];
+    if (active) {
+      p = w.pbar[s];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) u[a] = w.ubar[s * 3 + a];
+      if (s < MN) {
+        const int ray = (int)((uint32_t)s / (uint32_t)N);
+        taped_point<float>(w.o + ray * 3, w.r + ray * 3,
+                           dep[(int64_t)ray * w.ld + (int)((uint32_t)s % (uint32_t)N)], G.lo, G.hi, pt);
+      } else {
+#pragma unroll
+        for (int a = 0; a < 3; ++a) pt[a] = spts[(s - MN) * 3 + a];
+      }
+    } else {
+#pragma unroll
+      for (int a = 0; a < 3; ++a) pt[a] = (float)G.lo[a];
+    }
+    float z[16], v[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) z[i] = v[i] = 0.f;
+#pragma unroll
+    for (int l = 0; l < S::NL; ++l) {
+      const LevelDev& L = G.lv[l];
+      const LocT<float> lq = compact<float>(locate<false>(L, (double)pt[0], (double)pt[1], (double)pt[2], nullptr));
+      loc[l] = lq;
+      float wk[8], ju[8];
+      corner_w_ju(lq, (float)L.inv_vs, u, wk, ju);
+      const float* Fp = reinterpret_cast<const float*>(L.feat) + (int64_t)lq.base * S::CG;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        float row[S::CG];
+        load_row<float, S::CG>(Fp + corner_off(L, k) * S::CG, row);
+#pragma unroll
+        for (int c = 0; c < S::CG; ++c) {
+          z[l * S::CG + c] = fmaf(wk[k], row[c], z[l * S::CG + c]);
+          v[l * S::CG + c] = fmaf(ju[k], row[c], v[l * S::CG + c]);
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 16; i += 2)
+      *reinterpret_cast<float2*>(myrow + K::oA0 + i) = make_float2(fmaf(p, z[i], v[i]), fmaf(p, z[i + 1], v[i + 1]));
+    store_hl<8 * KG>(tl, 64, 96, z);
+    store_hl<8 * KG>(tl, 128, 160, v);
+  }
+  uint32_t phase = 0;
+  auto mma_round = [&](auto issue) {
+    cta_sync_tmem();
+    if (tid == 0) {
+      issue();
+      commit(&s_bar[1]);
+    }
+    tc::mbar_wait(&s_bar[1], phase);
+    phase ^= 1u;
+    fence_after();
+  };
+  tc::mbar_wait(&s_bar[0], 0);
+  // S1
+  mma_round([&] {
+    issue_at<KG>(tmem, tmem + 64, tmem + 96, sa(U::W0H), sa(U::W0L));
+    issue_at<KG>(tmem + 32, tmem + 128, tmem + 160, sa(U::W0H), sa(U::W0L));
+  });
+  float h[32], q[32];
+  uint32_t m0 = 0u, m1 = 0u;
+  ld32(tl, h);
+  ld32(tl + 32, q);
+#pragma unroll
+  for (int n = 0; n < 32; ++n) {
+    const float x = h[n] + gvec[tc::GVec::b0 + n];
+    const bool pos = x > 0.f;
+    h[n] = pos ? x : 0.f;
+    q[n] = pos ? q[n] : 0.f;
+    m0 |= (uint32_t)pos << n;
+  }
+#pragma unroll
+  for (int n = 0; n < 32; n += 2)
+    *reinterpret_cast<float2*>(myrow + K::oA1 + n) = make_float2(fmaf(p, h[n], q[n]), fmaf(p, h[n + 1], q[n + 1]));
+  store_hl<32>(tl, 64, 96, h);
+  store_hl<32>(tl, 128, 160, q);
+  // S2
+  mma_round([&] {
+    issue_at<4>(tmem, tmem + 64, tmem + 96, sa(U::W1H), sa(U::W1L));
+    issue_at<4>(tmem + 32, tmem + 128, tmem + 160, sa(U::W1H), sa(U::W1L));
+  });
+  ld32(tl, h);
+  ld32(tl + 32, q);
+  float acc_b0, acc_b1, acc_w2;
+#pragma unroll
+  for (int n = 0; n < 32; ++n) {
+    const float x = h[n] + gvec[tc::GVec::b1 + n];
+    const bool pos = x > 0.f;
+    m1 |= (uint32_t)pos << n;
+    q[n] = (pos ? p * x : 0.f) + (pos ? q[n] : 0.f);  // dW2: p relu(h1) + dd1
+    h[n] = pos ? gvec[tc::GVec::w2 + n] : 0.f;        // delta1
+  }
+  myrow[K::oM] = __uint_as_float(m1);
+  acc_w2 = warp_colsum32(q);
+  store_hl<32>(tl, 64, 96, h);
+#pragma unroll
+  for (int n = 0; n < 32; ++n) h[n] *= p;
+  acc_b1 = warp_colsum32(h);
+  // S3
+  mma_round([&] { issue_at<4>(tmem, tmem + 64, tmem + 96, sa(U::W1NH), sa(U::W1NL)); });
+  ld32(tl, h);
+#pragma unroll
+  for (int n = 0; n < 32; ++n) h[n] = ((m0 >> n) & 1u) ? h[n] : 0.f;
+#pragma unroll
+  for (int n = 0; n < 32; n += 2) *reinterpret_cast<float2*>(myrow + K::oB0 + n) = make_float2(h[n], h[n + 1]);
+  store_hl<32>(tl, 64, 96, h);
+#pragma unroll
+  for (int n = 0; n < 32; ++n) h[n] *= p;
+  acc_b0 = warp_colsum32(h);
+  // S4 (dphi/dz to D0 [0, 16)); the outer products overlap it
+  cta_sync_tmem();
+  if (tid == 0) {
+    issue_at<4, 16>(tmem, tmem + 64, tmem + 96, sa(U::W0NH), sa(U::W0NL));
+    commit(&s_bar[1]);
+  }
+  __syncwarp();
+  // ---- outer products over the warp's samples: dW0 += A0^T delta0, dW1 += A1^T delta1
+  const int g = lane >> 2, t = lane & 3;
+  float d0[1][4][4], d1[2][4][4];
+  tc::zero_d(d0);
+  tc::zero_d(d1);
+  const float w2l = gvec[tc::GVec::w2 + lane];
+#pragma unroll
+  for (int ks = 0; ks < 4; ++ks) {
+    const int k0 = ks * 8;
+    const uint32_t mk0 = __float_as_uint(rows[(k0 + t) * ROW + K::oM]);
+    const uint32_t mk1 = __float_as_uint(rows[(k0 + t + 4) * ROW + K::oM]);
+    uint32_t ah[2][4], al[2][4], bh0[4], bh1[4], bl0[4], bl1[4];
+    {
+      uint32_t a1h[1][4], a1l[1][4];
+      frag_a(rows, ROW, K::oA0, k0, 0, a1h[0], a1l[0]);
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) frag_b(rows, ROW, K::oB0, k0, nt * 8, bh0[nt], bh1[nt], bl0[nt], bl1[nt]);
+      tc::mma3_sweep(d0, a1h, a1l, bh0, bh1, bl0, bl1);
+    }
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) {
+      const int n = nt * 8 + g;
+      const float w2n = __shfl_sync(0xffffffffu, w2l, n);
+      split_fast(((mk0 >> n) & 1u) ? w2n : 0.f, bh0[nt], bl0[nt]);
+      split_fast(((mk1 >> n) & 1u) ? w2n : 0.f, bh1[nt], bl1[nt]);
+    }
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt) frag_a(rows, ROW, K::oA1, k0, mt * 16, ah[mt], al[mt]);
+    tc::mma3_sweep(d1, ah, al, bh0, bh1, bl0, bl1);
+  }
+  float accp = p;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) accp += __shfl_xor_sync(0xffffffffu, accp, o);
+  // ---- grid scatter: theta_l[idx_k] += g_l (p w_k + ju_k)
+  tc::mbar_wait(&s_bar[1], phase);
+  fence_after();
+  float gz[16];
+  ld16(tl, gz);
+#pragma unroll
+  for (int l = 0; l < S::NL; ++l) {
+    const LocT<float> lq = loc[l];
+    float wk[8], ju[8], coef[8];
+    corner_w_ju(lq, (float)G.lv[l].inv_vs, u, wk, ju);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) coef[k] = fmaf(p, wk[k], ju[k]);
+    scatter_level<float, S::CG>(G.lv[l], lq, gz + l * S::CG, coef, active, l < agg_levels, w.det_keys, w.det_vals,
+                                s * (S::NL + 1) + l);
+  }
+  // ---- CTA reduction -> MLP partial slot
+  fence_before();
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(K::kCols2) : "memory");
+  constexpr int NGP = S::NG;
+  float* red = rows_all;
+  {
+    float* mine = red + (size_t)warp * NGP;
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) frag_d_store(d0[0][nt], mine + S::oGW0, 0, nt * 8, S::IN_G);
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) frag_d_store(d1[mt][nt], mine + S::oGW1, mt * 16, nt * 8, GSB_HID);
+    mine[S::oGb0 + lane] = acc_b0;
+    mine[S::oGb1 + lane] = acc_b1;
+    mine[S::oGW2 + lane] = acc_w2;
+    if (lane == 0) mine[S::oGb2] = accp;
+  }
+  __syncthreads();
+  const int slot = w.mlp_slots > 0 ? (int)(blockIdx.x % (unsigned)w.mlp_slots) : (int)blockIdx.x;
+  float* out = w.mlp_part + (size_t)slot * S::NMLP;
+  for (int i = tid; i < NGP; i += kTile) {
+    float a = 0.f;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) a += red[(size_t)k * NGP + i];
+    if (w.mlp_slots > 0)
+      atomicAdd(out + i, a);
+    else
+      out[i] = a;
+  }
+}
+
 }  // namespace t5
 }  // namespace gsb
