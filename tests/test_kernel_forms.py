@@ -1,0 +1,31 @@
+"""The A/B kernel forms stay parity-green: the production step uses tcgen05
+for the coarse no-grad SDF, the taped forward and the geometry backward
+(gsb_step.cuh: GSB_T5=2, GSB_T5_FWD=4, GSB_T5_BWD=1).  The alternatives
+(mma.sync everywhere; tcgen05 everywhere with the 3-CTA forward) are read
+once per process from the environment, so each runs the float step parity
+tests of test_gpu_step.py in a child process against the same oracle
+goldens."""
+
+import os
+import subprocess
+import sys
+
+import pytest
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+FORMS = {
+    "mma_sync": {"GSB_T5": "0", "GSB_T5_FWD": "0", "GSB_T5_BWD": "0"},
+    "tcgen05_all": {"GSB_T5": "1", "GSB_T5_FWD": "3", "GSB_T5_BWD": "1"},
+}
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("form", sorted(FORMS))
+def test_alternative_kernel_forms_match_reference(form):
+    env = dict(os.environ, **FORMS[form])
+    cmd = [sys.executable, "-m", "pytest", os.path.join(HERE, "test_gpu_step.py"), "-m", "gpu", "-q", "-x",
+           "-p", "no:cacheprovider", "-k", "step_ or deterministic or two_iterations"]
+    r = subprocess.run(cmd, env=env, cwd=os.path.dirname(HERE), capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    assert " passed" in r.stdout
