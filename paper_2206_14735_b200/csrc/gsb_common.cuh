@@ -41,6 +41,7 @@ struct Shape {
   static constexpr int oCW2 = oCb1 + GSB_HID;
   static constexpr int oCb2 = oCW2 + GSB_HID * 3;
   static constexpr int NMLP = oCb2 + 3;
+  static constexpr int NMLPP = (NMLP + 3) / 4 * 4;  // stride of the MLP partial rows (16-byte aligned)
   static_assert(NMLP <= GSB_MLP_MAX, "MLP block exceeds constant buffer");
 };
 

@@ -102,8 +102,8 @@ Ws<T> carve(void* ws, const Sizes& z, size_t* bytes, int64_t* off_parts = nullpt
   // CTA per 128 samples), at least kNbMax for the persistent float64 kernels
   const int64_t nb = std::max<int64_t>(kNbMax, (z.NS + 127) / 128);
   w.nb_max = (int)nb;
-  w.mlp_part = c.template take<T>(nb * z.nmlp);
-  w.wfrag = c.template take<uint4>(4096 + 68 + 2304);  // tc::kFragBufU4: fragments + vector block
+  w.mlp_part = c.template take<T>(nb * ((z.nmlp + 3) / 4 * 4));
+  w.wfrag = c.template take<uint4>(4096 + 68 + 3072);  // tc::kFragBufU4: fragments + vector block
   w.fin_red = c.template take<double>((int64_t)16 * z.nmlp);  // FIN_SPLIT x NMLP
   w.fin_cnt = c.template take<unsigned>((z.nmlp + 31) / 32);
   w.loss_red = c.template take<double>((int64_t)((std::max(z.M, z.S) + 255) / 256 + 1) * 8);

@@ -1430,7 +1430,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_bwd_geom(Ws<T> w, Geo G, int M, 
     if (lane == 0) mine[S::oGb2] = accp;
   }
   __syncthreads();
-  T* out = w.mlp_part + (size_t)blockIdx.x * S::NMLP;
+  T* out = w.mlp_part + (size_t)blockIdx.x * S::NMLPP;
   for (int t = threadIdx.x; t < NGP; t += WARPS * 32) {
     T a = T(0);
 #pragma unroll
@@ -1592,7 +1592,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_bwd_color(Ws<T> w, Geo G, int M,
     if (lane < 3) mine[S::oCb2 - o + lane] = accb2;
   }
   __syncthreads();
-  T* out = w.mlp_part + (size_t)blockIdx.x * S::NMLP + S::NG;
+  T* out = w.mlp_part + (size_t)blockIdx.x * S::NMLPP + S::NG;
   for (int t = threadIdx.x; t < NCP; t += WARPS * 32) {
     T a = T(0);
 #pragma unroll
@@ -1616,7 +1616,7 @@ __global__ void __launch_bounds__(256) k_finalize_mlp(Ws<T> w, T* grads, int64_t
   double a = 0.0;
   if (t < S::NMLP) {
     const int nb = t < S::NG ? nb_geo : nb_col;
-    for (int b = wid; b < nb; b += 8) a += (double)w.mlp_part[(size_t)b * S::NMLP + t];
+    for (int b = wid; b < nb; b += 8) a += (double)w.mlp_part[(size_t)b * S::NMLPP + t];
   }
   red[wid][lane] = a;
   __syncthreads();
@@ -1648,12 +1648,12 @@ __global__ void __launch_bounds__(256) k_finalize_mlp2(Ws<T> w, T* grads, int64_
     const T* col = w.mlp_part + t;
     int b = b0 + wid;
     for (; b + 24 < b1; b += 32) {
-      a0 += (double)col[(size_t)b * S::NMLP];
-      a1 += (double)col[(size_t)(b + 8) * S::NMLP];
-      a2 += (double)col[(size_t)(b + 16) * S::NMLP];
-      a3 += (double)col[(size_t)(b + 24) * S::NMLP];
+      a0 += (double)col[(size_t)b * S::NMLPP];
+      a1 += (double)col[(size_t)(b + 8) * S::NMLPP];
+      a2 += (double)col[(size_t)(b + 16) * S::NMLPP];
+      a3 += (double)col[(size_t)(b + 24) * S::NMLPP];
     }
-    for (; b < b1; b += 8) a0 += (double)col[(size_t)b * S::NMLP];
+    for (; b < b1; b += 8) a0 += (double)col[(size_t)b * S::NMLPP];
   }
   red[wid][lane] = (a0 + a1) + (a2 + a3);
   __syncthreads();
@@ -1661,7 +1661,7 @@ __global__ void __launch_bounds__(256) k_finalize_mlp2(Ws<T> w, T* grads, int64_
     double tot = 0.0;
 #pragma unroll
     for (int k = 0; k < 8; ++k) tot += red[k][lane];
-    if (t < S::NMLP) w.fin_red[(size_t)y * S::NMLP + t] = tot;
+    if (t < S::NMLP) w.fin_red[(size_t)y * S::NMLPP + t] = tot;
     __threadfence();
     __syncwarp();
     if (lane == 0) last = atomicAdd(&w.fin_cnt[blockIdx.x], 1u) == FIN_SPLIT - 1;
@@ -1671,7 +1671,7 @@ __global__ void __launch_bounds__(256) k_finalize_mlp2(Ws<T> w, T* grads, int64_
     __threadfence();
     if (t < S::NMLP) {
       double tot = 0.0;
-      for (int k = 0; k < FIN_SPLIT; ++k) tot += __ldcg(&w.fin_red[(size_t)k * S::NMLP + t]);
+      for (int k = 0; k < FIN_SPLIT; ++k) tot += __ldcg(&w.fin_red[(size_t)k * S::NMLPP + t]);
       grads[mlp_off + t] += (T)tot;
     }
     if (lane == 0) w.fin_cnt[blockIdx.x] = 0u;  // ready for the next launch

@@ -50,6 +50,14 @@ inline bool use_t5_bwd() {
   }();
   return v;
 }
+// colour backward form: GSB_T5_COL=1 (default) tcgen05 (t5::k_bwd_color_t5), 0 mma.sync
+inline bool use_t5_col() {
+  static const bool v = [] {
+    const char* e = std::getenv("GSB_T5_COL");
+    return e ? std::atoi(e) != 0 : true;
+  }();
+  return v;
+}
 inline int t5_fwd_mode() {
   static const int v = [] {
     const char* e = std::getenv("GSB_T5_FWD");
@@ -144,7 +152,7 @@ int run_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step
       w.pose_g = reinterpret_cast<T*>(sc + PL.g);
       w.pose_fb = reinterpret_cast<T*>(sc + PL.fb);
     }
-    static_assert(tc::kFragBufU4 == 4096 + 68 + 2304, "workspace carve");
+    static_assert(tc::kFragBufU4 == 4096 + 68 + 3072, "workspace carve");
     tc::k_wfrag<S><<<tc::Fr<S>::NALL + 1 + tc::UmmaW::kTiles, 128, 0, stream>>>(mlp32, w.wfrag);
     GSB_LAUNCHED_T("k_wfrag");
   }
@@ -291,7 +299,7 @@ int run_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step
       w.mlp_slots = w.det_keys ? 0 : kMlpSlots;  // deterministic mode: per-CTA rows
       if (runA) {
         if (w.mlp_slots)
-          GSB_CHECK(cudaMemsetAsync(w.mlp_part, 0, (size_t)kMlpSlots * S::NMLP * sizeof(T), stream));
+          GSB_CHECK(cudaMemsetAsync(w.mlp_part, 0, (size_t)kMlpSlots * S::NMLPP * sizeof(T), stream));
         if (use_t5_bwd()) {
           const size_t smem_t5 = t5::GeoT5::smem();
           GSB_CHECK(cudaFuncSetAttribute(t5::k_bwd_geom_t5<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -305,7 +313,15 @@ int run_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step
         GSB_LAUNCHED_T("k_bwd_geom");
       }
       if (runB) {
-        tc::k_bwd_color_tc<S, WCOL><<<nb_col, WCOL * 32, smem_c, stream>>>(w, G, M, N, mlp32, dep_final);
+        if (use_t5_col()) {
+          const size_t smem_t5 = t5::ColT5::smem();
+          GSB_CHECK(cudaFuncSetAttribute(t5::k_bwd_color_t5<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem_t5));
+          t5::k_bwd_color_t5<S><<<(int)((z.MN + t5::kTile - 1) / t5::kTile), t5::kTile, smem_t5, stream>>>(
+              w, G, M, N, dep_final);
+        } else {
+          tc::k_bwd_color_tc<S, WCOL><<<nb_col, WCOL * 32, smem_c, stream>>>(w, G, M, N, mlp32, dep_final);
+        }
         GSB_LAUNCHED_T("k_bwd_color");
       }
       if (w.mlp_slots) {
@@ -383,8 +399,8 @@ Ws<T> carve_sdf(void* ws, int64_t n, int nmlp, size_t* bytes, bool grad = true) 
   w.ubar = c.template take<T>(grad ? n * 3 : 1);
   const int64_t nb = grad ? std::max<int64_t>(kNbMax, (n + 127) / 128) : 1;
   w.nb_max = (int)nb;
-  w.mlp_part = c.template take<T>(nb * nmlp);
-  w.wfrag = c.template take<uint4>(4096 + 68 + 2304);
+  w.mlp_part = c.template take<T>(nb * ((nmlp + 3) / 4 * 4));
+  w.wfrag = c.template take<uint4>(4096 + 68 + 3072);
   w.fin_red = c.template take<double>((int64_t)16 * nmlp);
   w.fin_cnt = c.template take<unsigned>((nmlp + 31) / 32);
   if (bytes) *bytes = c.off;

@@ -155,7 +155,8 @@ __device__ __forceinline__ void issue_layer(uint32_t tmem, uint32_t bh, uint32_t
 // persistent CTAs, one 128-sample tile per iteration
 
 struct SdfT5 {
-  static constexpr size_t smem() { return (size_t)(tc::UmmaW::N + tc::GVec::N) * 4; }
+  static constexpr int NW = tc::UmmaW::W1L + 1024;  // W0^T, W1^T tiles only
+  static constexpr size_t smem() { return (size_t)(NW + tc::GVec::N) * 4; }
 };
 
 template <class S>
@@ -168,7 +169,7 @@ __global__ void __launch_bounds__(kTile) k_sdf_eval_t5(Ws<float> w, Geo G, int M
   constexpr int KG = F::KG;
   extern __shared__ __align__(128) float t5_smem[];
   float* sw = t5_smem;                 // UmmaW block
-  float* svec = t5_smem + tc::UmmaW::N;  // GVec block
+  float* svec = t5_smem + SdfT5::NW;  // GVec block
   __shared__ __align__(8) uint64_t s_bar[2];  // [0] weight staging, [1] MMA completion
   __shared__ uint32_t s_tmem;
   const int64_t total = list ? (int64_t)(*list_count) : (int64_t)M * Nc;
@@ -189,7 +190,7 @@ __global__ void __launch_bounds__(kTile) k_sdf_eval_t5(Ws<float> w, Geo G, int M
   __syncthreads();
   fence_after();
   if (tid == 0) {
-    constexpr uint32_t wb = tc::UmmaW::N * 4, vb = tc::GVec::N * 4;
+    constexpr uint32_t wb = SdfT5::NW * 4, vb = tc::GVec::N * 4;
     tc::mbar_expect(&s_bar[0], wb + vb);
     tc::bulk_g2s(sw, w.wfrag + tc::kUmmaBaseU4, wb, &s_bar[0]);
     tc::bulk_g2s(svec, reinterpret_cast<const float*>(w.wfrag + tc::kVecBase), vb, &s_bar[0]);
@@ -290,7 +291,7 @@ __global__ void __launch_bounds__(kTile) k_sdf_eval_t5(Ws<float> w, Geo G, int M
 // overlap the last MMA.
 
 struct FwdT5 {
-  static constexpr size_t smem() { return (size_t)(tc::UmmaW::N + tc::GVec::N + tc::CVec::N) * 4; }
+  static constexpr size_t smem() { return (size_t)(tc::UmmaW::NFWD + tc::GVec::N + tc::CVec::N) * 4; }
 };
 
 template <class S, int CPS>
@@ -303,7 +304,7 @@ __global__ void __launch_bounds__(kTile, CPS) k_fwd_t5(Ws<float> w, Geo G, int M
   static_assert(8 * KG <= 16 && 8 * KC <= 16, "input widths");
   extern __shared__ __align__(128) float t5_smem[];
   float* sw = t5_smem;
-  const float* gvec = t5_smem + U::N;
+  const float* gvec = t5_smem + U::NFWD;
   const float* cvec = gvec + tc::GVec::N;
   __shared__ __align__(8) uint64_t s_bar[2];
   __shared__ uint32_t s_tmem;
@@ -325,10 +326,10 @@ __global__ void __launch_bounds__(kTile, CPS) k_fwd_t5(Ws<float> w, Geo G, int M
   __syncthreads();
   fence_after();
   if (tid == 0) {
-    constexpr uint32_t wb = U::N * 4, vb = (tc::GVec::N + tc::CVec::N) * 4;
+    constexpr uint32_t wb = U::NFWD * 4, vb = (tc::GVec::N + tc::CVec::N) * 4;
     tc::mbar_expect(&s_bar[0], wb + vb);
     tc::bulk_g2s(sw, w.wfrag + tc::kUmmaBaseU4, wb, &s_bar[0]);
-    tc::bulk_g2s(t5_smem + U::N, reinterpret_cast<const float*>(w.wfrag + tc::kVecBase), vb, &s_bar[0]);
+    tc::bulk_g2s(t5_smem + U::NFWD, reinterpret_cast<const float*>(w.wfrag + tc::kVecBase), vb, &s_bar[0]);
   }
   const uint32_t tmem = s_tmem;
   const uint32_t tl = tmem + ((uint32_t)(warp * 32) << 16);
@@ -774,7 +775,9 @@ __global__ void __launch_bounds__(kTile, 2) k_bwd_geom_t5(Ws<float> w, Geo G, in
   }
   __syncthreads();
   const int slot = w.mlp_slots > 0 ? (int)(blockIdx.x % (unsigned)w.mlp_slots) : (int)blockIdx.x;
-  float* out = w.mlp_part + (size_t)slot * S::NMLP;
+  float* out = w.mlp_part + (size_t)slot * S::NMLPP;
+  // (scalar reds: the 4-wide vector form measured slower here, 399 vs 371 us,
+  // while it pays in the colour backward)
   for (int i = tid; i < NGP; i += kTile) {
     float a = 0.f;
 #pragma unroll
@@ -783,6 +786,278 @@ __global__ void __launch_bounds__(kTile, 2) k_bwd_geom_t5(Ws<float> w, Geo G, in
       atomicAdd(out + i, a);
     else
       out[i] = a;
+  }
+}
+
+
+// ---------------------------------------------------------------------------
+// colour backward (same contract as tc::k_bwd_color_tc): the sample-major
+// colour layers on tcgen05, one 128-sample tile per CTA
+//   R1: [f_c, r] W0c -> h0c, m0
+//   R2: h0c W1c -> h1c, m1; 32 -> 3 head, sigmoid, y_bar, a1_bar per lane
+//   R3: a1_bar W1c^T -> a0_bar = (.) . m0
+//   R4: a0_bar W0c^T (N = 16) -> [f_bar, view-direction cotangent]
+// column sums (dW2c, db1c, db2c) as butterflies; the dW0c (+ db0c via the
+// ones column) and dW1c outer products stay on mma.sync over the rows.
+
+struct ColT5 {
+  static constexpr int ROW = 104;
+  static constexpr int oA0 = 0, oB0 = 16, oA1 = 48, oY = 80, oM = 88;
+  static constexpr int W0 = tc::UmmaW::C0H, NW = tc::UmmaW::N - tc::UmmaW::C0H;  // colour tiles
+  static constexpr size_t smem() { return (size_t)(NW + tc::CVec::N) * 4 + (size_t)kTile * ROW * 4; }
+};
+
+template <class S>
+__global__ void __launch_bounds__(kTile, 2) k_bwd_color_t5(Ws<float> w, Geo G, int M, int N,
+                                                          const double* __restrict__ dep) {
+  using F = tc::Fr<S>;
+  using U = tc::UmmaW;
+  using K = ColT5;
+  constexpr int KC = F::KC, ROW = K::ROW;
+  static_assert(S::IN_C + 1 <= 16 && 8 * KC <= 16 && S::CC <= 8, "colour input width");
+  extern __shared__ __align__(128) float t5_smem[];
+  float* sw = t5_smem - K::W0;  // indexed by UmmaW offsets
+  const float* cvec = t5_smem + K::NW;
+  float* rows_all = t5_smem + K::NW + tc::CVec::N;
+  __shared__ __align__(8) uint64_t s_bar[2];
+  __shared__ uint32_t s_tmem;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&s_tmem)),
+                 "r"(kCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  if (tid == 0) {
+    tc::mbar_init(&s_bar[0]);
+    tc::mbar_init(&s_bar[1]);
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  if (tid == 0) {
+    constexpr uint32_t wb = K::NW * 4, vb = tc::CVec::N * 4;
+    tc::mbar_expect(&s_bar[0], wb + vb);
+    tc::bulk_g2s(t5_smem, reinterpret_cast<const float*>(w.wfrag + tc::kUmmaBaseU4) + K::W0, wb, &s_bar[0]);
+    tc::bulk_g2s(t5_smem + K::NW, reinterpret_cast<const float*>(w.wfrag + tc::kVecBase) + tc::GVec::N, vb,
+                 &s_bar[0]);
+  }
+  const uint32_t tmem = s_tmem;
+  const uint32_t tl = tmem + ((uint32_t)(warp * 32) << 16);
+  auto sa = [&](int off) { return smem_u32(sw + off); };
+  float* rows = rows_all + warp * 32 * ROW;
+  float* myrow = rows + lane * ROW;
+  const int64_t NS = (int64_t)M * N;
+  const int64_t s = (int64_t)blockIdx.x * kTile + tid;
+  const bool active = s < NS;
+  const int ray = active ? (int)((uint32_t)s / (uint32_t)N) : 0;
+  LocT<float> q;
+  float cb[3];
+  {
+    float pt[3];
+    taped_point<float>(w.o + ray * 3, w.r + ray * 3,
+                       active ? dep[(int64_t)ray * w.ld + (int)((uint32_t)s % (uint32_t)N)] : 0.0, G.lo, G.hi, pt);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) cb[c] = active ? w.cbar[s * 3 + c] : 0.f;
+    q = compact<float>(locate<false>(G.col, (double)pt[0], (double)pt[1], (double)pt[2], nullptr));
+    float inp[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) inp[i] = 0.f;
+    gather_fast<float, S::CC>(G.col, q, inp);
+#pragma unroll
+    for (int a = 0; a < 3; ++a) inp[S::CC + a] = w.r[ray * 3 + a];
+    inp[S::IN_C] = 1.f;  // ones column: db0c rides on the dW0c outer product (zero weight row in W0c^T)
+#pragma unroll
+    for (int i = 0; i < 16; i += 2) *reinterpret_cast<float2*>(myrow + K::oA0 + i) = make_float2(inp[i], inp[i + 1]);
+    store_hl<8 * KC>(tl, 32, 64, inp);
+  }
+  uint32_t phase = 0;
+  auto mma_round = [&](auto issue) {
+    cta_sync_tmem();
+    if (tid == 0) {
+      issue();
+      commit(&s_bar[1]);
+    }
+    tc::mbar_wait(&s_bar[1], phase);
+    phase ^= 1u;
+    fence_after();
+  };
+  tc::mbar_wait(&s_bar[0], 0);
+  // R1
+  mma_round([&] { issue_at<KC>(tmem, tmem + 32, tmem + 64, sa(U::C0H), sa(U::C0L)); });
+  float h[32];
+  uint32_t m0 = 0u, m1 = 0u;
+  ld32(tl, h);
+#pragma unroll
+  for (int n = 0; n < 32; ++n) {
+    const float x = h[n] + cvec[tc::CVec::b0 + n];
+    const bool pos = x > 0.f;
+    h[n] = pos ? x : 0.f;
+    m0 |= (uint32_t)pos << n;
+  }
+#pragma unroll
+  for (int n = 0; n < 32; n += 2) *reinterpret_cast<float2*>(myrow + K::oA1 + n) = make_float2(h[n], h[n + 1]);
+  store_hl<32>(tl, 32, 64, h);
+  // R2
+  mma_round([&] { issue_at<4>(tmem, tmem + 32, tmem + 64, sa(U::C1H), sa(U::C1L)); });
+  ld32(tl, h);
+  float y[3] = {cvec[tc::CVec::b2], cvec[tc::CVec::b2 + 1], cvec[tc::CVec::b2 + 2]};
+#pragma unroll
+  for (int n = 0; n < 32; ++n) {
+    const float x = h[n] + cvec[tc::CVec::b1 + n];
+    const bool pos = x > 0.f;
+    h[n] = pos ? x : 0.f;
+    m1 |= (uint32_t)pos << n;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) y[c] = fmaf(h[n], cvec[tc::CVec::w2 + n * 3 + c], y[c]);
+  }
+  float yb[3];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    const float cc = sigmoid_fast(y[c]);
+    yb[c] = cb[c] * (cc * (1.f - cc));
+    myrow[K::oY + c] = yb[c];
+  }
+  myrow[K::oM] = __uint_as_float(m1);
+  float acc_w2[3], acc_b1, acc_b2[3];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {  // dW2c[n][c] = sum_s h1c[n] y_bar[c]
+    float v[32];
+#pragma unroll
+    for (int n = 0; n < 32; ++n) v[n] = h[n] * yb[c];
+    acc_w2[c] = warp_colsum32(v);
+  }
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    float a = yb[c];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    acc_b2[c] = a;
+  }
+  // a1_bar = (y_bar W2c^T) . m1
+#pragma unroll
+  for (int n = 0; n < 32; ++n) {
+    const float* w2 = cvec + tc::CVec::w2 + n * 3;
+    const float v = fmaf(w2[0], yb[0], fmaf(w2[1], yb[1], w2[2] * yb[2]));
+    h[n] = ((m1 >> n) & 1u) ? v : 0.f;
+  }
+  store_hl<32>(tl, 32, 64, h);
+  acc_b1 = warp_colsum32(h);
+  // R3
+  mma_round([&] { issue_at<4>(tmem, tmem + 32, tmem + 64, sa(U::C1NH), sa(U::C1NL)); });
+  ld32(tl, h);
+#pragma unroll
+  for (int n = 0; n < 32; ++n) h[n] = ((m0 >> n) & 1u) ? h[n] : 0.f;
+#pragma unroll
+  for (int n = 0; n < 32; n += 2) *reinterpret_cast<float2*>(myrow + K::oB0 + n) = make_float2(h[n], h[n + 1]);
+  store_hl<32>(tl, 32, 64, h);
+  // R4: [f_bar, r_bar] to D [0, 16); the outer products overlap it
+  cta_sync_tmem();
+  if (tid == 0) {
+    issue_at<4, 16>(tmem, tmem + 32, tmem + 64, sa(U::C0NH), sa(U::C0NL));
+    commit(&s_bar[1]);
+  }
+  __syncwarp();
+  // ---- outer products over the warp's samples: e0 = [inp,1]^T a0b, e1 = h0c^T a1b
+  const int g = lane >> 2, t = lane & 3;
+  float w2c[4][3];
+#pragma unroll
+  for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) w2c[nt][c] = cvec[tc::CVec::w2 + (8 * nt + g) * 3 + c];
+  float e0[1][4][4], e1[2][4][4];
+  tc::zero_d(e0);
+  tc::zero_d(e1);
+#pragma unroll
+  for (int ks = 0; ks < 4; ++ks) {
+    const int k0 = ks * 8;
+    uint32_t ah[2][4], al[2][4], bh0[4], bh1[4], bl0[4], bl1[4];
+    {
+      uint32_t a1h[1][4], a1l[1][4];
+      frag_a(rows, ROW, K::oA0, k0, 0, a1h[0], a1l[0]);
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) frag_b(rows, ROW, K::oB0, k0, nt * 8, bh0[nt], bh1[nt], bl0[nt], bl1[nt]);
+      tc::mma3_sweep(e0, a1h, a1l, bh0, bh1, bl0, bl1);
+    }
+    {
+      const float* r0 = rows + (k0 + t) * ROW;
+      const float* r1 = rows + (k0 + t + 4) * ROW;
+      const uint32_t mk0 = __float_as_uint(r0[K::oM]);
+      const uint32_t mk1 = __float_as_uint(r1[K::oM]);
+      const float y00 = r0[K::oY], y01 = r0[K::oY + 1], y02 = r0[K::oY + 2];
+      const float y10 = r1[K::oY], y11 = r1[K::oY + 1], y12 = r1[K::oY + 2];
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) {
+        const int n = nt * 8 + g;
+        const float v0 = fmaf(w2c[nt][0], y00, fmaf(w2c[nt][1], y01, w2c[nt][2] * y02));
+        const float v1 = fmaf(w2c[nt][0], y10, fmaf(w2c[nt][1], y11, w2c[nt][2] * y12));
+        split_fast(((mk0 >> n) & 1u) ? v0 : 0.f, bh0[nt], bl0[nt]);
+        split_fast(((mk1 >> n) & 1u) ? v1 : 0.f, bh1[nt], bl1[nt]);
+      }
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) frag_a(rows, ROW, K::oA1, k0, mt * 16, ah[mt], al[mt]);
+      tc::mma3_sweep(e1, ah, al, bh0, bh1, bl0, bl1);
+    }
+  }
+  // ---- colour grid scatter: theta_c[idx_k] += w_k f_bar
+  tc::mbar_wait(&s_bar[1], phase);
+  fence_after();
+  float fb[16];
+  ld16(tl, fb);
+  {
+    float wk[8];
+    corner_w(q, wk);
+    scatter_level<float, S::CC>(G.col, q, fb, wk, active, false, w.det_keys, w.det_vals, s * (S::NL + 1) + S::NL);
+  }
+  if (w.pose_fb && active) {  // pose refinement: f_bar and the view-direction cotangent
+    float* o = w.pose_fb + s * 12;
+#pragma unroll
+    for (int c = 0; c < S::IN_C; ++c) o[c] = fb[c];
+  }
+  // ---- CTA reduction -> MLP partial slot (colour block)
+  fence_before();
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kCols) : "memory");
+  constexpr int NCP = S::NMLP - S::NG;
+  float* red = rows_all;
+  {
+    float* mine = red + (size_t)warp * NCP;
+    const int o = S::NG;
+    if (lane < S::oCW0 - S::NG) mine[lane] = 0.f;  // alignment padding
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) frag_d_store(e0[0][nt], mine + (S::oCW0 - o), 0, nt * 8, S::IN_C + 1);
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) frag_d_store(e1[mt][nt], mine + (S::oCW1 - o), mt * 16, nt * 8, GSB_HID);
+    mine[S::oCb1 - o + lane] = acc_b1;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) mine[S::oCW2 - o + lane * 3 + c] = acc_w2[c];
+    if (lane == 0) {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) mine[S::oCb2 - o + c] = acc_b2[c];
+    }
+  }
+  __syncthreads();
+  const int slot = w.mlp_slots > 0 ? (int)(blockIdx.x % (unsigned)w.mlp_slots) : (int)blockIdx.x;
+  // from the 16-byte aligned colour block start, 4 parameters per vector red
+  float* out = w.mlp_part + (size_t)slot * S::NMLPP;
+  if (w.mlp_slots == 0 && tid < S::oCW0 - S::NG) out[S::NG + tid] = 0.f;  // per-CTA rows: padding
+  for (int i = S::oCW0 + tid * 4; i < S::NMLP; i += kTile * 4) {
+    float a[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      a[e] = 0.f;
+      if (i + e < S::NMLP) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) a[e] += red[(size_t)k * NCP + (i + e - S::NG)];
+      }
+    }
+    if (w.mlp_slots > 0)
+      red_add_v4(out + i, a[0], a[1], a[2], a[3]);
+    else
+      *reinterpret_cast<float4*>(out + i) = make_float4(a[0], a[1], a[2], a[3]);
   }
 }
 

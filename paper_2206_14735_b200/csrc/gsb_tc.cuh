@@ -45,8 +45,11 @@ struct UmmaW {
   static constexpr int W0H = 0, W0L = 512, W1H = 1024, W1L = 2048;
   static constexpr int W1NH = 3072, W1NL = 4096, W0NH = 5120, W0NL = 5632;
   static constexpr int C0H = 6144, C0L = 6656, C1H = 7168, C1L = 8192;
-  static constexpr int N = 9216;
-  static constexpr int kTiles = 12;
+  // colour backward chain: W1c (a1b -> a0b), W0c rows (a0b -> [f_bar, r_bar])
+  static constexpr int C1NH = 9216, C1NL = 10240, C0NH = 11264, C0NL = 11776;
+  static constexpr int N = 12288;
+  static constexpr int NFWD = 9216;  // geometry + colour forward tiles (k_fwd_t5)
+  static constexpr int kTiles = 16;
 };
 constexpr int kUmmaBaseU4 = kVecBase + (GVec::N + CVec::N) / 4;
 constexpr int kFragBufU4 = kUmmaBaseU4 + UmmaW::N / 4;
@@ -128,7 +131,7 @@ __global__ void __launch_bounds__(128) k_wfrag(const float* __restrict__ mlp, ui
   const int id = blockIdx.x, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   if (id > F::NALL) {  // tcgen05 B tiles (UmmaW), hi / lo per matrix
     const int tile = id - F::NALL - 1, lo = tile & 1, mat = tile >> 1;
-    // mat: 0 W0^T, 1 W1^T, 2 W1, 3 W0, 4 W0c^T, 5 W1c^T.  B[n][k] with K contiguous
+    // mat: 0 W0^T, 1 W1^T, 2 W1, 3 W0, 4 W0c^T, 5 W1c^T, 6 W1c, 7 W0c.  B[n][k], K contiguous
     int oW, K, Nn, rows, off;
     bool tr;  // true: B[n][k] = W[k][n] (W stored (in, out) row-major, 32 columns)
     switch (mat) {
@@ -137,7 +140,9 @@ __global__ void __launch_bounds__(128) k_wfrag(const float* __restrict__ mlp, ui
       case 2: oW = S::oGW1; K = GSB_HID; Nn = GSB_HID; rows = GSB_HID; tr = false; off = lo ? UmmaW::W1NL : UmmaW::W1NH; break;
       case 3: oW = S::oGW0; K = GSB_HID; Nn = 16; rows = S::IN_G; tr = false; off = lo ? UmmaW::W0NL : UmmaW::W0NH; break;
       case 4: oW = S::oCW0; K = 8 * F::KC; Nn = GSB_HID; rows = S::IN_C; tr = true; off = lo ? UmmaW::C0L : UmmaW::C0H; break;
-      default: oW = S::oCW1; K = GSB_HID; Nn = GSB_HID; rows = GSB_HID; tr = true; off = lo ? UmmaW::C1L : UmmaW::C1H; break;
+      case 5: oW = S::oCW1; K = GSB_HID; Nn = GSB_HID; rows = GSB_HID; tr = true; off = lo ? UmmaW::C1L : UmmaW::C1H; break;
+      case 6: oW = S::oCW1; K = GSB_HID; Nn = GSB_HID; rows = GSB_HID; tr = false; off = lo ? UmmaW::C1NL : UmmaW::C1NH; break;
+      default: oW = S::oCW0; K = GSB_HID; Nn = 16; rows = S::IN_C; tr = false; off = lo ? UmmaW::C0NL : UmmaW::C0NH; break;
     }
     float* o = reinterpret_cast<float*>(out + kUmmaBaseU4) + off;
     for (int i = threadIdx.x; i < Nn * K; i += blockDim.x) {
@@ -1010,7 +1015,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_bwd_geom_tc(Ws<float> w, Geo G, 
   }
   __syncthreads();
   const int slot = w.mlp_slots > 0 ? (int)(blockIdx.x % (unsigned)w.mlp_slots) : (int)blockIdx.x;
-  float* out = w.mlp_part + (size_t)slot * S::NMLP;
+  float* out = w.mlp_part + (size_t)slot * S::NMLPP;
   for (int i = threadIdx.x; i < NGP; i += WARPS * 32) {
     float a = 0.f;
 #pragma unroll
@@ -1272,7 +1277,7 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS <= 6 ? 2 : 1) k_bwd_color_tc
   }
   __syncthreads();
   const int slot = w.mlp_slots > 0 ? (int)(blockIdx.x % (unsigned)w.mlp_slots) : (int)blockIdx.x;
-  float* out = w.mlp_part + (size_t)slot * S::NMLP + S::NG;
+  float* out = w.mlp_part + (size_t)slot * S::NMLPP + S::NG;
   for (int i = threadIdx.x; i < NCP; i += WARPS * 32) {
     float a = 0.f;
 #pragma unroll

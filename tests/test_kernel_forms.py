@@ -1,6 +1,6 @@
 """The A/B kernel forms stay parity-green: the production step uses tcgen05
-for the coarse no-grad SDF, the taped forward and the geometry backward
-(gsb_step.cuh: GSB_T5=2, GSB_T5_FWD=4, GSB_T5_BWD=1).  The alternatives
+for the coarse no-grad SDF, the taped forward and both backward kernels
+(gsb_step.cuh: GSB_T5=2, GSB_T5_FWD=4, GSB_T5_BWD=1, GSB_T5_COL=1).  The alternatives
 (mma.sync everywhere; tcgen05 everywhere with the 3-CTA forward) are read
 once per process from the environment, so each runs the float step parity
 tests of test_gpu_step.py in a child process against the same oracle
@@ -15,8 +15,8 @@ import pytest
 HERE = os.path.dirname(os.path.abspath(__file__))
 
 FORMS = {
-    "mma_sync": {"GSB_T5": "0", "GSB_T5_FWD": "0", "GSB_T5_BWD": "0"},
-    "tcgen05_all": {"GSB_T5": "1", "GSB_T5_FWD": "3", "GSB_T5_BWD": "1"},
+    "mma_sync": {"GSB_T5": "0", "GSB_T5_FWD": "0", "GSB_T5_BWD": "0", "GSB_T5_COL": "0"},
+    "tcgen05_all": {"GSB_T5": "1", "GSB_T5_FWD": "3", "GSB_T5_BWD": "1", "GSB_T5_COL": "1"},
 }
 
 
