@@ -1711,11 +1711,22 @@ __global__ void __launch_bounds__(256) k_finalize_loss(Ws<T> w, int M, int S, T*
   __syncthreads();
   if (tid == 0) last = atomicAdd(w.loss_cnt, 1u) == gridDim.x - 1;
   __syncthreads();
-  if (!last || tid != 0) return;
+  if (!last) return;
   __threadfence();
-  double tot[7] = {0, 0, 0, 0, 0, 0, 0};
-  for (int blk = 0; blk < (int)gridDim.x; ++blk)
-    for (int k = 0; k < 7; ++k) tot[k] += __ldcg(&w.loss_red[blk * 8 + k]);
+  // block partials summed by warp k (part k): lane-strided, then a fixed
+  // butterfly -- deterministic, and 32-way parallel instead of one thread
+  // walking every block
+  if (wid < 7) {
+    double a = 0.0;
+    for (int blk = lane; blk < (int)gridDim.x; blk += 32) a += __ldcg(&w.loss_red[blk * 8 + wid]);
+    a = warp_sum(a);
+    if (lane == 0) red[wid][0] = a;
+  }
+  __syncthreads();
+  if (tid != 0) return;
+  double tot[7];
+#pragma unroll
+  for (int k = 0; k < 7; ++k) tot[k] = red[k][0];
   *w.loss_cnt = 0u;  // ready for the next launch
   const T sT = exp(params[log_s_off]);
   const double s = (double)sT;
