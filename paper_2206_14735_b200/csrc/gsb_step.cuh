@@ -294,8 +294,11 @@ int run_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step
       GSB_CHECK(cudaFuncSetAttribute(tc::k_bwd_color_tc<S, WCOL>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_c));
       // MLP partials: red.add into kMlpSlots L2-resident rows instead of one row per CTA
-      constexpr int kMlpSlots = 64;
-      static_assert(kMlpSlots <= kNbMax, "workspace carve");
+      static const int kMlpSlots = [] {
+        const char* e = std::getenv("GSB_MLP_SLOTS");
+        const int v = e ? std::atoi(e) : 64;
+        return v < 1 ? 1 : (v > kNbMax ? kNbMax : v);
+      }();
       w.mlp_slots = w.det_keys ? 0 : kMlpSlots;  // deterministic mode: per-CTA rows
       if (runA) {
         if (w.mlp_slots)
