@@ -226,6 +226,14 @@ int run_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step
     const T* spts = reinterpret_cast<const T*>(st->smooth_pts);
     int64_t ns = z.NS;
     int fb = (int)((ns + 127) / 128);
+    // tile sweep directions (Ws::sweep, GSB_SWEEP): the geometry backward runs
+    // its tiles last-to-first, so it starts on the grid cells the forward
+    // touched last (still in L2): 372 -> 369 us; the other bits measured neutral
+    static const int kSweep = [] {
+      const char* e = std::getenv("GSB_SWEEP");
+      return e ? std::atoi(e) : 2;
+    }();
+    w.sweep = kSweep;
     if (runA) {
     if constexpr (F32) {
       constexpr int FW = 4;  // warps per CTA of the taped forward

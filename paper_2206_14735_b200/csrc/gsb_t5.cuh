@@ -354,7 +354,7 @@ __global__ void __launch_bounds__(kTile, CPS) k_fwd_t5(Ws<float> w, Geo G, int M
   LocT<float> loc[S::NL];
   float z[8 * KG], inp[8 * KC];
   auto gather = [&](int64_t tile) {
-    s = tile * kTile + tid;
+    s = ((w.sweep & 1) ? ntiles - 1 - tile : tile) * kTile + tid;  // backward sweep: L2 reuse
     act = s < NS;
     ray = -1;
     float p[3];
@@ -580,7 +580,7 @@ __global__ void __launch_bounds__(kTile, 2) k_bwd_geom_t5(Ws<float> w, Geo G, in
   float* rows = rows_all + warp * 32 * ROW;
   float* myrow = rows + lane * ROW;
   const int64_t MN = (int64_t)M * N, NS = MN + nsp;
-  const int64_t s = (int64_t)blockIdx.x * kTile + tid;
+  const int64_t s = (int64_t)((w.sweep & 2) ? gridDim.x - 1 - blockIdx.x : blockIdx.x) * kTile + tid;
   const bool active = s < NS;
   // ---- per sample: point, z and v in one pass over the corners
   LocT<float> loc[S::NL];
@@ -848,7 +848,7 @@ __global__ void __launch_bounds__(kTile, 2) k_bwd_color_t5(Ws<float> w, Geo G, i
   float* rows = rows_all + warp * 32 * ROW;
   float* myrow = rows + lane * ROW;
   const int64_t NS = (int64_t)M * N;
-  const int64_t s = (int64_t)blockIdx.x * kTile + tid;
+  const int64_t s = (int64_t)((w.sweep & 4) ? gridDim.x - 1 - blockIdx.x : blockIdx.x) * kTile + tid;
   const bool active = s < NS;
   const int ray = active ? (int)((uint32_t)s / (uint32_t)N) : 0;
   LocT<float> q;
