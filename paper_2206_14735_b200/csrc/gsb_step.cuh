@@ -376,9 +376,13 @@ int run_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step
       GSB_LAUNCHED_T("k_det_reduce");
     }
     static_assert(FIN_SPLIT == 16, "workspace carve");
-    GSB_CHECK(cudaMemsetAsync(w.fin_cnt, 0, (S::NMLP + 31) / 32 * sizeof(unsigned), stream));
-    k_finalize_mlp2<T, S><<<dim3((S::NMLP + 31) / 32, FIN_SPLIT), 256, 0, stream>>>(w, grads, model->mlp_offset,
-                                                                    nb_geo, nb_col);
+    if (nb_geo <= 256 && nb_col <= 256) {  // few (slot) rows: one pass, 8 warps per 32 parameters
+      k_finalize_mlp<T, S><<<(S::NMLP + 31) / 32, 256, 0, stream>>>(w, grads, model->mlp_offset, nb_geo, nb_col);
+    } else {
+      GSB_CHECK(cudaMemsetAsync(w.fin_cnt, 0, (S::NMLP + 31) / 32 * sizeof(unsigned), stream));
+      k_finalize_mlp2<T, S><<<dim3((S::NMLP + 31) / 32, FIN_SPLIT), 256, 0, stream>>>(w, grads, model->mlp_offset,
+                                                                      nb_geo, nb_col);
+    }
     GSB_LAUNCHED_T("k_finalize_mlp");
     GSB_CHECK(cudaMemsetAsync(w.loss_cnt, 0, sizeof(unsigned), stream));
     k_finalize_loss<T><<<(std::max(M, z.S) + 255) / 256, 256, 0, stream>>>(w, M, z.S, grads, params,
