@@ -201,17 +201,21 @@ __device__ __forceinline__ PixelRay pixel_ray(const gsb_dataset_t& D, int64_t fl
   return R;
 }
 
+// rays per block of k_ray_setup: 16 rays x 8 threads (384 blocks at c2)
+constexpr int kRaySetupRays = 16;
+
 template <typename T>
 __global__ void __launch_bounds__(128) k_ray_setup(gsb_dataset_t D, const int64_t* __restrict__ ids, int M,
                                                    int ray_base, Ws<T> w, Geo G, int Nc, double nearv,
                                                    double max_depth, int has_ff, double ff, gsb_pcg64_t rng) {
-  // 32 rays per block: threads 0..31 set the rays up, then all 128 threads
-  // fill the stratified depths, 4 threads per ray (each jumps its own PCG
-  // stream to its first sample)
-  __shared__ double s_near[32], s_span[32];
+  // RPB rays per block: threads 0..RPB-1 set the rays up, then all 128
+  // threads fill the stratified depths, TPR threads per ray (each jumps its
+  // own PCG stream to its first sample)
+  constexpr int RPB = kRaySetupRays, TPR = 128 / RPB;  // rays per block, threads per ray
+  __shared__ double s_near[RPB], s_span[RPB];
   const int t = threadIdx.x;
-  const int i = blockIdx.x * 32 + t;
-  if (t < 32 && i < M) {
+  const int i = blockIdx.x * RPB + t;
+  if (t < RPB && i < M) {
     PixelRay P = pixel_ray(D, ids[i]);
     const double* pose = D.poses + P.frame * 12;
     T r[3];
@@ -257,9 +261,9 @@ __global__ void __launch_bounds__(128) k_ray_setup(gsb_dataset_t D, const int64_
   }
   __syncthreads();
   // stratified_coarse (gs/sampler.py:91-107) with uniform row (ray_base + ray)
-  const int rl = t >> 2, q = t & 3, ray = blockIdx.x * 32 + rl;
+  const int rl = t / TPR, q = t % TPR, ray = blockIdx.x * RPB + rl;
   if (ray >= M) return;
-  const int chunk = (Nc + 3) / 4, j0 = q * chunk, j1 = min(Nc, j0 + chunk);
+  const int chunk = (Nc + TPR - 1) / TPR, j0 = q * chunk, j1 = min(Nc, j0 + chunk);
   if (j0 >= j1) return;
   Pcg g;
   g.init(rng);

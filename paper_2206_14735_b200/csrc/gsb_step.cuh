@@ -164,7 +164,7 @@ int run_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step
   const T* log_s = params + model->log_s_offset;
   if (st->phases & 1) {
     GSB_CHECK(cudaMemsetAsync(w.counts, 0, 8 * sizeof(long long), stream));
-    k_ray_setup<T><<<(M + 31) / 32, 128, 0, stream>>>(
+    k_ray_setup<T><<<(M + kRaySetupRays - 1) / kRaySetupRays, 128, 0, stream>>>(
         *data, st->ray_ids, M, st->ray_base, w, G, Nc, st->near, st->max_depth,
         st->has_fixed_far, st->fixed_far, st->rng_stratify);
     GSB_LAUNCHED_T("k_ray_setup");
