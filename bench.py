@@ -238,51 +238,99 @@ def kernel_table(model, kt, K, M, N, S, P, peak_hbm):
 
 
 # ----------------------------------------------------------------------------
-# reference arm: the CPU oracle port of the reference step
+# reference arm: the unmodified reference package (baseline/ref_step.py)
+
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
 
 
-def cpu_step_sample(steps, warmup, m_sample, threads):
-    """Time the oracle's step (gs/optimizer.py:363-373 restated in numpy) on
-    the same workload with a bounded ray sample."""
+def reference_available():
+    return os.path.isdir(os.path.join(REF_DIR, "gridsurf"))
+
+
+def reference_step(steps, warmup, rays, frames, config, precision="single", timeout=1500):
+    """Time the reference's own training step (gs/optimizer.py:362-373) on
+    the host cores in a separate process (baseline/ref_step.py): the
+    reference's scenegen renders the dataset, nothing of this repository
+    (no _gsb.so) is loaded there.  Returns its JSON dict."""
+    threads = str(os.cpu_count() or 1)
+    env = dict(os.environ, OPENBLAS_NUM_THREADS=threads, OMP_NUM_THREADS=threads,
+               MKL_NUM_THREADS=threads, NUMBA_CACHE_DIR=os.path.join(
+                   os.environ.get("TMPDIR", "/tmp"), "gsb_ref_numba"),
+               PYTHONDONTWRITEBYTECODE="1")
+    env.pop("CUDA_VISIBLE_DEVICES", None)
+    cmd = [sys.executable, os.path.join(ROOT, "baseline", "ref_step.py"), "--steps", str(steps),
+           "--warmup", str(warmup), "--rays", str(rays), "--frames", str(frames),
+           "--config", str(config), "--precision", precision]
+    out = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=timeout)
+    if out.returncode != 0:
+        raise RuntimeError(f"reference step failed: {out.stderr[-2000:]}")
+    return json.loads(out.stdout.strip().splitlines()[-1])
+
+
+def port_step(steps, warmup, rays, frames, config, threads):
+    """Fallback when baseline/_ref is absent: the oracle port of the same step
+    (oracle/gridsurf_oracle.py, ~3x slower than gridsurf on the same cores),
+    on a dataset rendered by the oracle's host renderer (no repo .so)."""
     os.environ.setdefault("OMP_NUM_THREADS", str(threads))
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     from oracle import gridsurf_oracle as O
-    from _golden import OracleDataset, cfg_ns
-    from paper_2206_14735_b200 import scenes
-    ds = scenes.config2(frames=2, threads=threads)
-    ods = OracleDataset(ds.colors_u8, ds.depths_mm, ds.poses, ds.intrinsics)
-    cfg = cfg_ns(precision="single", batch_rays=m_sample, bounds=scenes.CONFIG2_BOUNDS)
-    P = O.create_params(*cfg.bounds, ds.poses, seed=0, dtype=np.float32)
+    from oracle import scene_host as SH
+    from _golden import cfg_ns
+    ds = SH.config_dataset(config, frames, threads)
+    bounds = SH.CONFIG2_BOUNDS if config == 2 else None
+    cfg = cfg_ns(precision="single", batch_rays=rays, bounds=bounds)
+    lo, hi = O.derive_bounds(ds, cfg)
+    P = O.create_params(lo, hi, ds.poses, seed=0, dtype=np.float32)
     opt = O.Adam(P.arrays(), P.lrs())
     times = []
     for it in range(warmup + steps):
         t0 = time.perf_counter()
-        O.train_step(P, opt, ods, cfg, it)
-        dt = time.perf_counter() - t0
+        O.train_step(P, opt, ds, cfg, it)
         if it >= warmup:
-            times.append(dt)
-    return float(np.median(times)), P
+            times.append(time.perf_counter() - t0)
+    tot = float(sum(times))
+    return {"value": rays * steps / tot, "ms_per_step": 1e3 * tot / steps, "steps": steps,
+            "warmup": warmup, "threads": threads, "rays": rays, "frames": frames,
+            "params": int(sum(a.size for a in P.arrays()))}
+
+
+def cpu_reference(steps, warmup, rays, frames, config):
+    """(result dict, kind): the reference itself when installed, else the port."""
+    threads = os.cpu_count() or 1
+    if reference_available():
+        return reference_step(steps, warmup, rays, frames, config), "reference"
+    return port_step(steps, warmup, rays, frames, config, threads), "port"
+
+
+def ref_sample_text(r, kind, config):
+    who = ("the unmodified reference package (gridsurf 0.1.0 from baseline/_ref): "
+           "draw_ray_batch + train_objective + dc.grad + Adam.step"
+           if kind == "reference" else "the oracle port of the reference step")
+    return (f"{who}, config{config}, {r['rays']} rays x 132 samples per step, {r['frames']} "
+            f"frames rendered by its own scenegen, dense Adam over {r['params']} parameters; "
+            f"{r['steps']} timed steps after {r['warmup']} warm-up (numba JIT), "
+            f"{r['threads']} host threads")
 
 
 def run_reference(args):
     ws, rank, _ = dist_env()
     if rank != 0:
         return 0
-    threads = os.cpu_count() or 1
-    # bounded sample per step so that K steps stay within a few minutes
-    m_sample = 512 if args.steps <= 20 else 256 if args.steps <= 50 else 128
-    t, P = cpu_step_sample(max(args.steps, 1), 0 if args.steps <= 1 else 1, m_sample, threads)
-    v = m_sample / t
+    rays = args.rays if args.config != 1 else 1024
+    frames = args.frames if args.config == 2 else 20
+    # full-size steps (the whole 6144-ray batch, same frames and bounds as the
+    # B200 arm); ~9 s per c2 step on 8 cores, so at most 20 are timed
+    steps = max(1, min(args.steps, 20))
+    r, kind = cpu_reference(steps, 1, rays, frames, args.config)
+    v = r["value"]
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "rays/s",
-            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
+            "n_gpus": args.gpus, "steps": r["steps"], "warmup": r["warmup"],
+            "ms_per_step": r["ms_per_step"], "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": "config2 ScanNet-shaped 640x480, 4-level grid, pinned "
-                                   "7x7x3.25 m box, 132 samples/ray", "sample_rays": m_sample},
-            "cpu_baseline": {"value": v, "unit": "rays/s", "cores": threads, "kind": "port",
-                             "sample": f"{m_sample} rays of the config2 batch + dense Adam over "
-                                       f"all {sum(a.size for a in P.arrays())} parameters, "
-                                       "median step"},
+            "config": {"workload": workload_name(args, 132), "rays_per_gpu": rays,
+                       "samples_per_ray": 132, "params": r["params"], "frames": frames},
+            "cpu_baseline": {"value": v, "unit": "rays/s", "cores": r["threads"], "kind": kind,
+                             "sample": ref_sample_text(r, kind, args.config)},
             "e2e": {"value": v, "unit": "rays/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -503,19 +551,21 @@ def main():
         roofline["traffic"] = tr
     cpu = None
     if not args.no_cpu_baseline and ws_ == 1:
-        threads = os.cpu_count() or 1
-        m_sample = 2048  # ~10-20 s of CPU work
-        t, _ = cpu_step_sample(1, 0, m_sample, threads)
-        cpu = {"value": m_sample / t, "unit": "rays/s", "cores": threads, "kind": "port",
-               "sample": f"one oracle step, {m_sample} rays of the config2 workload + dense "
-                         f"Adam over all {P} parameters"}
+        # one full-size reference step after one warm-up step (~10-30 s of CPU work)
+        r, kind = cpu_reference(1, 1, M if args.config != 1 else 1024,
+                                args.frames if args.config == 2 else 20, args.config)
+        cpu = {"value": r["value"], "unit": "rays/s", "cores": r["threads"], "kind": kind,
+               "sample": ref_sample_text(r, kind, args.config)}
     line = {"metric": METRIC, "value": value, "unit": "rays/s", "n_gpus": ws_, "steps": K,
             "warmup": W, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32" if args.precision == "single" else "f64",
             "data": "synthetic",
             "config": {"workload": workload_name(args, N),
                        "rays_per_gpu": M, "samples_per_ray": N, "params": P,
-                       "frames": args.frames, "l2": f"working set (params/grad/m/v arenas = {4 * P * model.arena.params.element_size() / 1e9:.2f} GB) "
+                       "frames": 20 if args.config == 1 else args.frames,
+                       "frames_note": "SURVEY 8(d) defines c2 at F = 300 frames; the step "
+                                      "cost does not depend on F (it only sets the ray-id range)",
+                       "l2": f"working set (params/grad/m/v arenas = {4 * P * model.arena.params.element_size() / 1e9:.2f} GB) "
                              "> L2 (126 MB); no explicit flush"},
             "samples_per_s": value * N,
             "e2e": {"value": e2e, "unit": "rays/s", "h2d_bytes_per_step": int(T.last_h2d),

@@ -23,6 +23,9 @@ PAIRS = {"optimizer": "optimizer", "renderer": "renderer", "sampler": "sampler",
 NOT_MIRRORED = {"renderer": {"alphas", "composite", "render_weights_data", "loss_rgb_depth", "loss_sdf_fs",
                              "loss_eikonal"},
                 "sampler": {"enforce_separation"},
+                # the host sphere tracer: frames render on the device (gsb_render_frames);
+                # the numpy form is the checker in oracle/scene_host.py
+                "scenegen": {"sphere_trace"},
                 "decoders": {"decode_sdf", "decode_color"},
                 # analysis helpers of the reference's own autodiff tests
                 "feature_grid": {"sample_jacobian", "sample_hessian_xx", "sample_hessian_xtheta"}}

@@ -2,7 +2,8 @@
 reference renderer's own output (gs/scenegen.py:290-368; fixtures from
 tests/golden/make_golden_scene.py, make_golden_c1.py, make_golden.py).
 
-* CPU: the numpy form (scenes.render_dataset_host) reproduces every pixel.
+* CPU: the oracle's numpy renderer (oracle/scene_host.py, the device's
+  postfix program evaluated with numpy) reproduces every pixel.
 * GPU: gsb_render_frames (one thread per pixel, the CSG tree as a postfix
   program) reproduces every pixel -- clean frames at c1 (20 x 160x120) and
   the small case, depth noise + all three dropouts, the thin slab."""
@@ -45,14 +46,15 @@ def _check(name, cols, deps, ref_c, ref_d):
     assert bad_c == 0 and bad_d == 0, (name, bad_c, bad_d, np.abs(deps.astype(int) - ref_d).max())
 
 
-@pytest.mark.parametrize("which", ["corrupt", "slab", "small_double"])
+@pytest.mark.parametrize("which", ["corrupt", "slab", "small_double", "c1_double"])
 def test_host_render_matches_reference(which):
+    from oracle import scene_host
     from paper_2206_14735_b200 import scenes
     for name, scene, intr, poses, kw, ref_c, ref_d in cases():
         if name != which:
             continue
-        ds = scenes.render_dataset_host(getattr(scenes, scene)(), poses, intr, max_t=8.0, **kw)
-        _check(name, ds.colors_u8, ds.depths_mm, ref_c, ref_d)
+        cols, deps = scene_host.render_sequence(getattr(scenes, scene)(), poses, intr, max_t=8.0, **kw)
+        _check(name, cols, deps, ref_c, ref_d)
 
 
 @pytest.mark.gpu
@@ -65,14 +67,15 @@ def test_device_render_matches_reference():
 
 @pytest.mark.gpu
 def test_device_render_dataset_is_a_dataset():
+    from oracle import scene_host
     from paper_2206_14735_b200 import scenes
     ds = scenes.render_dataset(scenes.sphere_in_box(), scenes.orbit_trajectory(3),
                                scenes.fov_intrinsics(40, 30))
-    host = scenes.render_dataset_host(scenes.sphere_in_box(), scenes.orbit_trajectory(3),
-                                      scenes.fov_intrinsics(40, 30))
-    np.testing.assert_array_equal(ds.colors_u8, host.colors_u8)
-    np.testing.assert_array_equal(ds.depths_mm, host.depths_mm)
-    assert ds.n_valid == host.n_valid
+    cols, deps = scene_host.render_sequence(scenes.sphere_in_box(), scenes.orbit_trajectory(3),
+                                            scenes.fov_intrinsics(40, 30))
+    np.testing.assert_array_equal(ds.colors_u8, cols)
+    np.testing.assert_array_equal(ds.depths_mm, deps)
+    assert ds.n_valid == int((deps > 0).sum())
 
 
 def test_scene_program_flattening_and_validation():
