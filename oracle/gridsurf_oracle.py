@@ -650,12 +650,19 @@ class GeomPass:
 
 
 def train_objective(P, dataset, batch, iteration, cfg, smooth_override=None,
-                    want_grads=True, inject_depths=None, shard=None):
+                    want_grads=True, inject_depths=None, shard=None, inject_rays=None,
+                    point_dtype=None):
     """One evaluation of the training objective and (optionally) all
     parameter gradients.  Returns a dict of every intermediate.
 
     ``inject_depths`` replaces the sampled depths (M, N) for component
     parity (the taped pass of another implementation given our samples).
+    ``inject_rays`` = (o, r) (M, 3) replaces the realised ray origins and
+    directions, and ``point_dtype`` forms the taped points x = o + d r (and
+    their clip to the box) in that dtype before the cast to the model dtype
+    (gs/renderer.py:348-351 forms them in the model dtype).  Together they
+    give the float64 evaluation of the taped pass at exactly the float32
+    points a float32 implementation used (conditioned kernel parity).
 
     ``shard`` (data-parallel restatement; not in the
     reference): dict with ``row_base`` and ``m_global`` (this batch is rows
@@ -677,6 +684,8 @@ def train_objective(P, dataset, batch, iteration, cfg, smooth_override=None,
     # ray setup: gs/renderer.py:302-317; R = R0 @ exp_so3(nu) in the model
     # dtype (gs/camera.py:68-70, exactly R0 for nu = 0)
     uniq, inv, pose_aux, o, r = realised_rays(P, batch)
+    if inject_rays is not None:
+        o, r = (np.asarray(a).astype(dt).reshape(m, 3) for a in inject_rays)
     o_data, r_data = o.astype(np.float64), r.astype(np.float64)
     if cfg.fixed_far is not None:
         far = np.full(m, float(cfg.fixed_far))
@@ -720,9 +729,11 @@ def train_objective(P, dataset, batch, iteration, cfg, smooth_override=None,
     R["depths"] = depths
 
     # taped pass: gs/renderer.py:348-370
-    x = o.reshape(m, 1, 3) + depths[:, :, None].astype(dt) * r.reshape(m, 1, 3)
+    pdt = dt if point_dtype is None else np.dtype(point_dtype)
+    x = o.astype(pdt).reshape(m, 1, 3) + depths[:, :, None].astype(pdt) * r.astype(pdt).reshape(m, 1, 3)
     xu = x.reshape(m * n, 3)
-    xf = np.minimum(np.maximum(xu, lo_c.astype(dt)), hi_c.astype(dt))
+    xf = np.minimum(np.maximum(xu, lo_c.astype(pdt)), hi_c.astype(pdt)).astype(dt)
+    xu = xu.astype(dt)
     G = GeomPass(P, xf)
     cs = LevelSample(P.color, xf)
     fc = cs.value()
