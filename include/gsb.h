@@ -276,14 +276,22 @@ int gsb_render_frames(const gsb_scene_t* scene, const double* poses, int32_t n_f
                       const double* noise, double sigma0, const gsb_render_opts_t* opts, uint8_t* colors,
                       uint16_t* depth_mm, void* stream);
 
-/* Dense Adam over the whole arena (gs/optimizer.py:38-55): per segment
- * learning rate; float64 register math; grads zeroed afterwards.  If
+/* Dense Adam over the whole arena (gs/optimizer.py:38-55, replaces
+ * Adam.step / _adam_kernel): per segment learning rate (n_seg <= 32 runs
+ * starting at seg_begin_host[i]); float64 register math; grads zeroed
+ * afterwards.  A segment with a negative learning rate is not owned by this
+ * launch (a data-parallel rank's foreign shards): its gradients are zeroed
+ * and p / m / v are untouched.  The update is skipped, and
+ * status[GSB_ST_DIVERGED] set (which skips every later guarded update), if
  * `guard` is non-null and guard[0] (total loss) is non-finite or
- * > guard_threshold, the update is skipped and status[GSB_ST_DIVERGED] set. */
+ * > guard_threshold (gs/optimizer.py:368-371), or `guard_status` (the step's
+ * status words) is non-null and carries a bounds / overflow / view-direction
+ * error (raised inside train_objective by the reference). */
 int gsb_adam_step(int32_t precision, void* params, void* grads, void* m, void* v,
                   int64_t n, const int64_t* seg_begin_host, const double* seg_lr_host,
                   int32_t n_seg, double beta1, double beta2, double eps, double c1, double c2,
-                  const double* guard, double guard_threshold, int32_t* status, void* stream);
+                  const double* guard, double guard_threshold, const int32_t* guard_status,
+                  int32_t* status, void* stream);
 
 /* Smoothness points (renderer.draw_smooth_points, gs/renderer.py:243-276) on
  * the device from the host's RNG draws, in the reference's call order:

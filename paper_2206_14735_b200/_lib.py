@@ -159,7 +159,7 @@ def lib():
         "gsb_importance_refine": ([I32, I32, I32, I32, P, P, P, P, P, P, P, P], I32),
         "gsb_train_step": ([C.POINTER(Model), C.POINTER(Dataset), C.POINTER(Step), P], I32),
         "gsb_adam_step": ([I32, P, P, P, P, I64, C.POINTER(I64), C.POINTER(D), I32, D, D, D, D, D,
-                           P, D, P, P], I32),
+                           P, D, P, P, P], I32),
         "gsb_pcg64_random": ([C.POINTER(Pcg64), I64, I64, P, P], I32),
         "gsb_ray_batch": ([C.POINTER(Dataset), P, I32, P, P], I32),
         "gsb_gather_weighted": ([I32, P, I32, P, P, I64, P, P], I32),

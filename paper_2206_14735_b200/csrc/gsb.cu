@@ -549,8 +549,9 @@ int gsb_train_step(const gsb_model_t* model, const gsb_dataset_t* data, const gs
 int gsb_adam_step(int32_t precision, void* params, void* grads, void* m, void* v, int64_t n,
                   const int64_t* seg_begin_host, const double* seg_lr_host, int32_t n_seg,
                   double beta1, double beta2, double eps, double c1, double c2,
-                  const double* guard, double guard_threshold, int32_t* status, void* stream) {
-  if (n_seg < 1 || n_seg > 16 || !status) return GSB_E_ARG;
+                  const double* guard, double guard_threshold, const int32_t* guard_status,
+                  int32_t* status, void* stream) {
+  if (n_seg < 1 || n_seg > GSB_ADAM_MAX_SEGS || !status) return GSB_E_ARG;
   AdamSegs sg;
   sg.n = n_seg;
   for (int i = 0; i < n_seg; ++i) {
@@ -582,10 +583,10 @@ int gsb_adam_step(int32_t precision, void* params, void* grads, void* m, void* v
   timing_point(nullptr, s);
   if (precision == 0)
     k_adam<float><<<blocks, 256, 0, s>>>((float*)params, (float*)grads, (float*)m, (float*)v, n, sg,
-                                         k, guard, guard_threshold, status);
+                                         k, guard, guard_threshold, guard_status, status);
   else
     k_adam<double><<<blocks, 256, 0, s>>>((double*)params, (double*)grads, (double*)m, (double*)v,
-                                          n, sg, k, guard, guard_threshold, status);
+                                          n, sg, k, guard, guard_threshold, guard_status, status);
   GSB_LAUNCHED();
   timing_point("k_adam", s);
   return GSB_OK;

@@ -1759,9 +1759,13 @@ __global__ void __launch_bounds__(256) k_finalize_loss(Ws<T> w, int M, int S, T*
 // Adam over the arena (gs/optimizer.py:38-55): float64 math, storage dtype,
 // non-finite gradients zeroed and counted, gradient cleared.
 
+// learning-rate runs over the arena; lr < 0 marks a run this launch does not
+// own (data-parallel ZeRO-1: another rank's shard): its gradients are only
+// zeroed, p / m / v are neither read nor written
+constexpr int GSB_ADAM_MAX_SEGS = 32;
 struct AdamSegs {
-  int64_t begin[16];
-  double lr[16];
+  int64_t begin[GSB_ADAM_MAX_SEGS];
+  double lr[GSB_ADAM_MAX_SEGS];
   int n;
 };
 
@@ -1806,7 +1810,7 @@ __device__ __forceinline__ void adam_fast(float& p, float& g, float& m, float& v
   double sq;
   if (q2 == 0.0) {  // never-touched parameter: sqrt(0) = 0 exactly
     sq = 0.0;
-  } else if (q2 > 1e-30) {
+  } else if (q2 > 1e-30 && q2 < 1e30) {  // rsqrtf seed in float range
     double t = (double)rsqrtf((float)q2);
     t = t * fma(-0.5 * q2, t * t, 1.5);
     t = t * fma(-0.5 * q2, t * t, 1.5);
@@ -1830,13 +1834,21 @@ template <typename T>
 __global__ void __launch_bounds__(256) k_adam(T* __restrict__ P, T* __restrict__ Gr, T* __restrict__ Mm,
                                               T* __restrict__ Vv, int64_t n, AdamSegs segs,
                                               AdamConst k, const double* guard, double thr,
-                                              int32_t* status) {
+                                              const int32_t* guard_status, int32_t* status) {
+  // halt (this and every later update) where the reference raises before
+  // its Adam step: a diverged total (gs/optimizer.py:368-371) or a step
+  // error flag (GridBoundsError etc., raised inside train_objective)
+  bool halt = guard && status[GSB_ST_DIVERGED];
   if (guard) {
     const double tot = guard[0];
-    if (!(tot == tot) || isinf(tot) || tot > thr || status[GSB_ST_DIVERGED]) {
-      if (blockIdx.x == 0 && threadIdx.x == 0) status[GSB_ST_DIVERGED] = 1;
-      return;
-    }
+    halt |= !(tot == tot) || isinf(tot) || tot > thr;
+  }
+  if (guard_status)
+    halt |= guard_status[GSB_ST_BOUNDS] | guard_status[GSB_ST_OVERFLOW] |
+            guard_status[GSB_ST_VIEWDIR];
+  if (halt) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) status[GSB_ST_DIVERGED] = 1;
+    return;
   }
   constexpr int V = 16 / sizeof(T);  // elements per 16-byte vector
   using Vec = typename std::conditional<sizeof(T) == 4, float4, double2>::type;
@@ -1856,6 +1868,7 @@ __global__ void __launch_bounds__(256) k_adam(T* __restrict__ P, T* __restrict__
       for (int q = 1; q < segs.n; ++q)
         if (e >= segs.begin[q]) sidx = q;
       lr[u] = segs.lr[sidx];
+      if (lr[u] < 0.0) continue;  // not owned: gradients zeroed below
       p[u] = __ldcs(reinterpret_cast<const Vec*>(P) + i);
       g[u] = __ldcs(reinterpret_cast<const Vec*>(Gr) + i);
       m[u] = __ldcs(reinterpret_cast<const Vec*>(Mm) + i);
@@ -1865,6 +1878,10 @@ __global__ void __launch_bounds__(256) k_adam(T* __restrict__ P, T* __restrict__
     for (int u = 0; u < 2; ++u) {
       const int64_t i = i0 + u * stride;
       if (i >= nvec) break;
+      if (lr[u] < 0.0) {
+        __stcs(reinterpret_cast<Vec*>(Gr) + i, Vec{});
+        continue;
+      }
       T* pp = reinterpret_cast<T*>(&p[u]);
       T* gg = reinterpret_cast<T*>(&g[u]);
       T* mm = reinterpret_cast<T*>(&m[u]);
@@ -1887,7 +1904,9 @@ __global__ void __launch_bounds__(256) k_adam(T* __restrict__ P, T* __restrict__
     int sidx = 0;
     for (int q = 1; q < segs.n; ++q)
       if (e >= segs.begin[q]) sidx = q;
-    if constexpr (sizeof(T) == 4)
+    if (segs.lr[sidx] < 0.0)
+      Gr[e] = T(0);
+    else if constexpr (sizeof(T) == 4)
       adam_fast(P[e], Gr[e], Mm[e], Vv[e], segs.lr[sidx], k, bad);
     else
       adam_exact(P[e], Gr[e], Mm[e], Vv[e], segs.lr[sidx], k, bad);

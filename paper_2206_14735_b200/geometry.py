@@ -99,7 +99,7 @@ class _RangeAdam:
             _lib.check(L.gsb_adam_step(
                 0 if a.dtype == np.float32 else 1, a.params.data_ptr() + b * esz,
                 a.grads.data_ptr() + b * esz, m.data_ptr(), v.data_ptr(), e - b, B, Lr, 1,
-                self.beta1, self.beta2, self.eps, c1, c2, None, 0.0, self.status.data_ptr(),
+                self.beta1, self.beta2, self.eps, c1, c2, None, 0.0, None, self.status.data_ptr(),
                 _lib.stream_handle()), "gsb_adam_step")
         a.grads_clean = True  # the kernel zeroes the gradients it consumed
 

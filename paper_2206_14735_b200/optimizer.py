@@ -22,6 +22,7 @@ __all__ = ["Adam", "TrainConfig", "DivergenceError", "train", "build_model", "ma
            "save_model", "load_model", "Trainer", "CSV_HEADER"]
 
 log = logging.getLogger("gridsurf_b200")
+MAX_ADAM_SEGMENTS = 32  # GSB_ADAM_MAX_SEGS (csrc/gsb_kernels.cuh)
 
 
 class DivergenceError(RuntimeError):
@@ -88,8 +89,6 @@ class Adam:
         if self.arena.n - up(pos) >= A and lrs[-1] != 0.0:
             begins.append(up(pos))
             lrs.append(0.0)
-        if len(begins) > 16:
-            raise ValueError("too many learning-rate segments")
         return begins, lrs
 
     def _segments_in(self, lo, hi):
@@ -104,9 +103,32 @@ class Adam:
                 lrs.append(lr)
         return begins, lrs
 
-    def _launch(self, guard=None, guard_threshold=0.0, stream=None, lo=0, hi=None):
-        """One fused update of arena range [lo, hi) (default: all of it;
-        a data-parallel rank updates its own shard, parallel.py)."""
+    def _segments_owned(self, owned):
+        """Runs over the whole arena where only the ``owned`` [lo, hi) ranges
+        keep their learning rates; the rest is marked not-owned (lr -1: the
+        kernel only zeroes those gradients)."""
+        b, l = self._segments()
+        cuts = sorted({0, self.arena.n} | set(b) | {x for r in owned for x in r})
+        begins, lrs = [], []
+        for x, y in zip(cuts[:-1], cuts[1:]):
+            if x == y:
+                continue
+            lr = l[max(i for i, s in enumerate(b) if s <= x)]
+            if not any(lo <= x and y <= hi for lo, hi in owned):
+                lr = -1.0
+            if lrs and lrs[-1] == lr:
+                continue
+            begins.append(x)
+            lrs.append(lr)
+        return begins, lrs
+
+    def _launch(self, guard=None, guard_threshold=0.0, stream=None, lo=0, hi=None,
+                guard_status=None, owned=None):
+        """One fused update of arena range [lo, hi) (default: all of it), or
+        of the whole arena where only the ``owned`` ranges are updated and the
+        other gradients zeroed (a data-parallel rank's shards, parallel.py).
+        ``guard`` / ``guard_status`` (the step's parts and status words) skip
+        the update where the reference raises before its Adam step."""
         ts = set(self.t)
         if len(ts) != 1:
             raise NotImplementedError("per-tensor step counts must agree for the fused update")
@@ -118,7 +140,16 @@ class Adam:
         lo = int(lo)
         if lo % mdl.ParamArena.ALIGN or (hi - lo) % mdl.ParamArena.ALIGN or not 0 <= lo <= hi <= a.n:
             raise ValueError("Adam range must be 16-byte aligned inside the arena")
-        b, l = self._segments_in(lo, hi) if (lo, hi) != (0, a.n) else self._segments()
+        if owned is not None:
+            if (lo, hi) != (0, a.n):
+                raise ValueError("owned ranges are given over the whole arena")
+            if any(x % mdl.ParamArena.ALIGN for r in owned for x in r):
+                raise ValueError("owned ranges must be 16-byte aligned")
+            b, l = self._segments_owned(owned)
+        else:
+            b, l = self._segments_in(lo, hi) if (lo, hi) != (0, a.n) else self._segments()
+        if len(b) > MAX_ADAM_SEGMENTS:
+            raise ValueError("too many learning-rate segments")
         B = (C.c_int64 * len(b))(*b)
         Lr = (C.c_double * len(l))(*l)
         esz = a.params.element_size()
@@ -127,6 +158,7 @@ class Adam:
             self.m_arena.data_ptr() + lo * esz, self.v_arena.data_ptr() + lo * esz, hi - lo, B, Lr, len(b),
             self.beta1, self.beta2, self.eps, c1, c2,
             None if guard is None else guard.data_ptr(), float(guard_threshold),
+            None if guard_status is None else guard_status.data_ptr(),
             self.status.data_ptr(), _lib.stream_handle(stream)), "gsb_adam_step")
         a.grads_clean = True
         a.generation = getattr(a, "generation", 0) + 1
@@ -391,6 +423,10 @@ class Trainer:
         self.dataset = Dataset.wrap(dataset)
         self.engine = engine_for(model, self.dataset)
         self.host_parts = torch.zeros((2, _lib.N_PARTS), dtype=torch.float64).pin_memory()
+        # the step's status words (grid bounds, importance overflow, view
+        # directions), read with the parts: the workspace copy is zeroed by
+        # the next launch
+        self.host_status = torch.zeros((2, _lib.N_STATUS), dtype=torch.int32).pin_memory()
         self.events = [torch.cuda.Event(), torch.cuda.Event()]
         self.rank, self.world = int(rank), int(world)
         self.dp = DataParallelStep(self.engine, dist) if dist is not None and world > 1 else None
@@ -428,12 +464,15 @@ class Trainer:
         else:
             ws = self.dp(self.cfg, d, ids, sm, **kw)
         self.host_parts[slot].copy_(ws["parts"], non_blocking=True)
+        self.host_status[slot].copy_(ws["status"], non_blocking=True)
         self.events[slot].record()
         self.opt.t = [t + 1 for t in self.opt.t]
         if self.dp is None:
-            self.opt._launch(guard=ws["parts"], guard_threshold=self.cfg.divergence_threshold)
+            self.opt._launch(guard=ws["parts"], guard_threshold=self.cfg.divergence_threshold,
+                             guard_status=ws["status"])
         else:
-            self.dp.adam(self.opt, guard=ws["parts"], guard_threshold=self.cfg.divergence_threshold)
+            self.dp.adam(self.opt, guard=ws["parts"], guard_threshold=self.cfg.divergence_threshold,
+                         guard_status=ws["status"])
         if self.engine.refine and (it + 1) % self.cfg.pose_refresh_every == 0:
             for p in self.model.poses:  # gs/optimizer.py:374-376
                 p.refresh()
@@ -443,6 +482,11 @@ class Trainer:
         self.events[slot].synchronize()
         p = self.host_parts[slot].numpy()
         return {k: float(p[i]) for i, k in enumerate(_lib.PART_NAMES)}
+
+    def status(self, slot):
+        """Host copy of the step's status words (valid after parts(slot))."""
+        self.events[slot].synchronize()
+        return self.host_status[slot].numpy().copy()
 
 
 def train(dataset, cfg, out_dir, initial_poses=None, resume=None):
@@ -467,9 +511,23 @@ def train(dataset, cfg, out_dir, initial_poses=None, resume=None):
     T = Trainer(model, dataset, cfg, opt)
     every = max(cfg.checkpoint_every, 1)
 
-    def finish(it, parts, csv):
-        if not np.isfinite(parts["total"]) or parts["total"] > cfg.divergence_threshold:
-            raise DivergenceError(f"loss diverged at iteration {it}: {parts}")
+    launched = []  # iterations whose Adam launch is enqueued but not yet checked
+
+    def finish(it, slot, csv):
+        parts = T.parts(slot)
+        # the reference raises inside train_objective (GridBoundsError, ...)
+        # or right after it (DivergenceError), before its Adam step: the
+        # device skipped this and every later Adam launch (guard), so only
+        # the host step counters run ahead and are rolled back
+        try:
+            check_status(T.status(slot), cfg.precision)
+            if not np.isfinite(parts["total"]) or parts["total"] > cfg.divergence_threshold:
+                raise DivergenceError(f"loss diverged at iteration {it}: {parts}")
+        except Exception:
+            k = len(launched) - launched.index(it)
+            opt.t = [t - k for t in opt.t]
+            raise
+        launched.remove(it)
         csv.write(f"{it},{parts['total']:.10g},{parts['rgb']:.10g},{parts['depth']:.10g},"
                   f"{parts['sdf']:.10g},{parts['fs']:.10g},{parts['eik']:.10g},"
                   f"{parts['smooth']:.10g},{parts['s']:.10g}\n")
@@ -481,21 +539,23 @@ def train(dataset, cfg, out_dir, initial_poses=None, resume=None):
             csv.write(CSV_HEADER)
         pending = None  # (iteration, slot)
         T.start_prefetch(start_it)
-        for it in range(start_it, cfg.iterations):
-            slot = it % 2
-            T.launch(it, slot=slot)
+        try:
+            for it in range(start_it, cfg.iterations):
+                slot = it % 2
+                T.launch(it, slot=slot)
+                launched.append(it)
+                if pending is not None:
+                    finish(pending[0], pending[1], csv)
+                pending = (it, slot)
+                if (it + 1) % every == 0:
+                    finish(it, slot, csv)
+                    pending = None
+                    save_model(os.path.join(out_dir, f"ckpt_{it + 1:06d}.gsck"), model, cfg,
+                               it + 1, opt)
             if pending is not None:
-                finish(pending[0], T.parts(pending[1]), csv)
-            pending = (it, slot)
-            if (it + 1) % every == 0:
-                finish(it, T.parts(slot), csv)
-                pending = None
-                check_status(T.opt.status)
-                save_model(os.path.join(out_dir, f"ckpt_{it + 1:06d}.gsck"), model, cfg, it + 1,
-                           opt)
-        if pending is not None:
-            finish(pending[0], T.parts(pending[1]), csv)
-        T.stop_prefetch()
-        csv.flush()
+                finish(pending[0], pending[1], csv)
+        finally:
+            T.stop_prefetch()
+            csv.flush()
     save_model(final_path, model, cfg, cfg.iterations, opt)
     return model, final_path

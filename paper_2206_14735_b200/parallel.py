@@ -69,7 +69,6 @@ class DataParallelStep:
         self.world = dist.get_world_size(group)
         self.nccl = dist.get_backend(group) == "nccl"
         self.shard_adam = bool(shard_adam) and self.world > 1
-        self._inplace_ok = True  # NCCL in-place reduce-scatter / all-gather accepted
         self.overlap = overlap
 
     def chunks(self, n):
@@ -130,20 +129,21 @@ class DataParallelStep:
         s = parts[S_SLOT].clone()
         self.dist.all_reduce(parts, group=self.group)
         parts[S_SLOT] = s
+        # every rank raises (and skips Adam) if any rank's step flagged an error
+        self.dist.all_reduce(ws["status"], op=self.dist.ReduceOp.MAX, group=self.group)
         return ws
 
     def _reduce_scatter(self, g, c0, c1, async_op=False):
-        """Sum of chunk [c0, c1) into this rank's shard of it (NCCL in place);
-        gloo has no reduce-scatter: the chunk's sum everywhere."""
+        """Sum of chunk [c0, c1) into this rank's shard of it (NCCL, in place:
+        the output is the rank's slice of the input).  gloo has no
+        reduce-scatter, so the CPU tests take the chunk's sum everywhere (a
+        superset of the shard).  NCCL errors propagate."""
         t = g[c0:c1]
-        if self.nccl and self._inplace_ok:
+        if self.nccl:
             chunk = (c1 - c0) // self.world
             lo = self.rank * chunk
-            try:
-                return self.dist.reduce_scatter_tensor(t[lo:lo + chunk], t, group=self.group,
-                                                       async_op=async_op)
-            except (RuntimeError, ValueError):  # argument check refused the aliasing
-                self._inplace_ok = False
+            return self.dist.reduce_scatter_tensor(t[lo:lo + chunk], t, group=self.group,
+                                                   async_op=async_op)
         return self.dist.all_reduce(t, group=self.group, async_op=async_op)
 
     def adam(self, opt, **kw):
@@ -153,23 +153,16 @@ class DataParallelStep:
             return
         a = opt.arena
         mine = self.shards(a.n)
-        for lo, hi in mine:  # Adam zeroes grads[lo:hi]; the divergence guard gates every range
-            opt._launch(lo=lo, hi=hi, **kw)
-        prev = 0
-        for lo, hi in mine:  # partial sums of the other ranks' shards
-            a.grads[prev:lo].zero_()
-            prev = hi
-        a.grads[prev:].zero_()
+        # one launch: Adam on this rank's shards, and the partial sums left in
+        # the other ranks' shards zeroed (the guard gates all of it)
+        opt._launch(owned=mine, **kw)
         for (c0, c1), (lo, hi) in zip(self.chunks(a.n), mine):
             self._all_gather(a.params[c0:c1], lo - c0, hi - c0)
 
     def _all_gather(self, t, lo, hi):
-        if self.nccl and self._inplace_ok:
-            try:
-                self.dist.all_gather_into_tensor(t, t[lo:hi], group=self.group)  # in place
-                return
-            except (RuntimeError, ValueError):
-                self._inplace_ok = False
+        if self.nccl:
+            self.dist.all_gather_into_tensor(t, t[lo:hi], group=self.group)  # in place
+            return
         n = hi - lo
         parts = [t[r * n:(r + 1) * n] for r in range(self.world)]
         self.dist.all_gather(parts, t[lo:hi].clone(), group=self.group)

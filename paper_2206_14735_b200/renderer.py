@@ -124,7 +124,9 @@ def engine_for(model, dataset):
 
 
 def check_status(status, precision="single"):
-    st = status.cpu().numpy()
+    """Raise the reference's exception for a step's device status words
+    (a device tensor or the host copy of one)."""
+    st = status.cpu().numpy() if hasattr(status, "cpu") else np.asarray(status)
     if st[_lib.ST_BOUNDS]:
         raise GridBoundsError("sample point(s) outside grid box")
     if st[_lib.ST_VIEWDIR]:

@@ -68,7 +68,9 @@ def _dataset(case):
                       camera.Intrinsics(i.fx, i.fy, i.cx, i.cy, i.width, i.height))
     kw = {k: v for k, v in G.meta["cfg"].items() if k not in ("precision", "bounds", "voxel_sizes")}
     kw["voxel_sizes"], kw["bounds"] = G.cfg.voxel_sizes, G.cfg.bounds
-    return ds, dict(kw, smooth_count=G.meta["smooth_count"])
+    # its pinned box is a flat slab: a sphere of half the smallest extent
+    # would touch the box faces
+    return ds, dict(kw, smooth_count=G.meta["smooth_count"], sphere_radius_scale=0.4)
 
 
 def oracle_from_model(model, poses, dtype):

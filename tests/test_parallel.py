@@ -65,7 +65,8 @@ class OracleEngine:
         n = sum(a.size for a in P.arrays())
         self.model = SimpleNamespace(arena=SimpleNamespace(grads=torch.zeros(n, dtype=torch.float64)))
         self.ws = dict(counts=torch.zeros(4, dtype=torch.int64),
-                       parts=torch.zeros(8, dtype=torch.float64))
+                       parts=torch.zeros(8, dtype=torch.float64),
+                       status=torch.zeros(8, dtype=torch.int32))
 
     def launch(self, cfg, draws, ids, sm, phases=3, fresh=True, ray_base=0, m_global=None,
                smooth_global=None):
@@ -220,8 +221,13 @@ class _TorchAdam:
         self.m_arena = torch.zeros_like(arena.params)
         self.v_arena = torch.zeros_like(arena.params)
 
-    def _launch(self, lo=0, hi=None, **kw):
+    def _launch(self, lo=0, hi=None, owned=None, **kw):
         a = self.arena
+        if owned is not None:  # the rank's shards; the rest is only zeroed
+            for x, y in owned:
+                self._launch(x, y)
+            a.grads.zero_()
+            return
         hi = a.n if hi is None else hi
         t = float(self.t[0])
         g = a.grads[lo:hi]
@@ -239,7 +245,8 @@ class _FakeStepEngine:
         self.torch, self.rank = torch, rank
         self.model = types.SimpleNamespace(arena=arena)
         self.split = 300  # "colorgrid" offset of the fake arena
-        self.ws = dict(counts=torch.zeros(4, dtype=torch.int64), parts=torch.zeros(8, dtype=torch.float64))
+        self.ws = dict(counts=torch.zeros(4, dtype=torch.int64), parts=torch.zeros(8, dtype=torch.float64),
+                       status=torch.zeros(8, dtype=torch.int32))
 
     def launch(self, cfg, draws, ids, sm, phases=3, fresh=True, it=0, **kw):
         if phases == 1:
@@ -308,6 +315,19 @@ def test_sharded_adam_gloo_world2_equals_replicated(tmp_path, overlap):
     np.testing.assert_allclose(z["v"], opt.v_arena.numpy(), rtol=0, atol=1e-15)
     assert list(z["counts"]) == [3, 6, 9, 12]
     assert z["parts"][0] == 3.0 and z["parts"][7] == 1.0  # s slot is not summed
+
+
+def test_adam_segments_owned():
+    """ZeRO-1 segments over the whole arena: the owned ranges keep their
+    learning-rate runs, everything else is marked not-owned (lr -1)."""
+    from types import SimpleNamespace
+    from paper_2206_14735_b200.optimizer import Adam
+    a = Adam.__new__(Adam)
+    a.arena = SimpleNamespace(n=256)
+    a._segments = lambda: ([0, 64, 128, 200], [0.01, 0.001, 0.0005, 0.0])
+    assert a._segments_owned([(0, 256)]) == ([0, 64, 128, 200], [0.01, 0.001, 0.0005, 0.0])
+    assert a._segments_owned([(32, 160)]) == ([0, 32, 64, 128, 160], [-1.0, 0.01, 0.001, 0.0005, -1.0])
+    assert a._segments_owned([(0, 64), (128, 192)]) == ([0, 64, 128, 192], [0.01, -1.0, 0.0005, -1.0])
 
 
 def test_adam_segments_in_range():
