@@ -3,8 +3,8 @@ for the coarse no-grad SDF, the taped forward and both backward kernels
 (gsb_step.cuh: GSB_T5=2, GSB_T5_FWD=4, GSB_T5_BWD=1, GSB_T5_COL=1).  The alternatives
 (mma.sync everywhere; tcgen05 everywhere with the 3-CTA forward) are read
 once per process from the environment, so each runs the float step parity
-tests of test_gpu_step.py in a child process against the same oracle
-goldens."""
+tests of test_gpu_step.py and the conditioned float32 parity of
+test_f32_parity.py in a child process against the same oracle goldens."""
 
 import os
 import subprocess
@@ -24,8 +24,11 @@ FORMS = {
 @pytest.mark.parametrize("form", sorted(FORMS))
 def test_alternative_kernel_forms_match_reference(form):
     env = dict(os.environ, **FORMS[form])
-    cmd = [sys.executable, "-m", "pytest", os.path.join(HERE, "test_gpu_step.py"), "-m", "gpu", "-q", "-x",
-           "-p", "no:cacheprovider", "-k", "step_ or deterministic or two_iterations"]
-    r = subprocess.run(cmd, env=env, cwd=os.path.dirname(HERE), capture_output=True, text=True, timeout=900)
-    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
-    assert " passed" in r.stdout
+    base = [sys.executable, "-m", "pytest", "-m", "gpu", "-q", "-x", "-p", "no:cacheprovider"]
+    for cmd in (base + [os.path.join(HERE, "test_gpu_step.py"), "-k",
+                        "step_ or deterministic or two_iterations"],
+                base + [os.path.join(HERE, "test_f32_parity.py")]):  # conditioned 1e-4 / 1e-5
+        r = subprocess.run(cmd, env=env, cwd=os.path.dirname(HERE), capture_output=True, text=True,
+                           timeout=900)
+        assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+        assert " passed" in r.stdout
