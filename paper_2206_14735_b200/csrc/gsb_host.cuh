@@ -58,6 +58,7 @@ Ws<T> carve(void* ws, const Sizes& z, size_t* bytes, int64_t* off_parts = nullpt
   Ws<T> w;
   w.mlp_slots = 0;
   w.sweep = 0;
+  w.dbg = 0;
   w.det_keys = nullptr;
   w.det_vals = nullptr;
   w.pose_g = nullptr;

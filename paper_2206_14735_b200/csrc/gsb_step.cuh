@@ -234,6 +234,11 @@ int run_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step
       return e ? std::atoi(e) : 2;
     }();
     w.sweep = kSweep;
+    static const int kDbg = [] {
+      const char* e = std::getenv("GSB_DBG");
+      return e ? std::atoi(e) : 0;
+    }();
+    w.dbg = kDbg;
     if (runA) {
     if constexpr (F32) {
       constexpr int FW = 4;  // warps per CTA of the taped forward

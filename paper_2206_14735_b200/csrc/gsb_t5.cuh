@@ -617,7 +617,12 @@ __global__ void __launch_bounds__(kTile, 2) k_bwd_geom_t5(Ws<float> w, Geo G, in
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         float row[S::CG];
-        load_row<float, S::CG>(Fp + corner_off(L, k) * S::CG, row);
+        if (w.dbg & 8) {
+#pragma unroll
+          for (int c = 0; c < S::CG; ++c) row[c] = 1e-3f * (float)(c + k);
+        } else {
+          load_row<float, S::CG>(Fp + corner_off(L, k) * S::CG, row);
+        }
 #pragma unroll
         for (int c = 0; c < S::CG; ++c) {
           z[l * S::CG + c] = fmaf(wk[k], row[c], z[l * S::CG + c]);
@@ -712,7 +717,7 @@ __global__ void __launch_bounds__(kTile, 2) k_bwd_geom_t5(Ws<float> w, Geo G, in
   tc::zero_d(d1);
   const float w2l = gvec[tc::GVec::w2 + lane];
 #pragma unroll
-  for (int ks = 0; ks < 4; ++ks) {
+  for (int ks = 0; ks < ((w.dbg & 2) ? 0 : 4); ++ks) {
     const int k0 = ks * 8;
     const uint32_t mk0 = __float_as_uint(rows[(k0 + t) * ROW + K::oM]);
     const uint32_t mk1 = __float_as_uint(rows[(k0 + t + 4) * ROW + K::oM]);
@@ -750,14 +755,16 @@ __global__ void __launch_bounds__(kTile, 2) k_bwd_geom_t5(Ws<float> w, Geo G, in
     corner_w_ju(lq, (float)G.lv[l].inv_vs, u, wk, ju);
 #pragma unroll
     for (int k = 0; k < 8; ++k) coef[k] = fmaf(p, wk[k], ju[k]);
-    scatter_level<float, S::CG>(G.lv[l], lq, gz + l * S::CG, coef, active, l < agg_levels, w.det_keys, w.det_vals,
-                                s * (S::NL + 1) + l);
+    if (!(w.dbg & 1))
+      scatter_level<float, S::CG>(G.lv[l], lq, gz + l * S::CG, coef, active, l < agg_levels, w.det_keys,
+                                  w.det_vals, s * (S::NL + 1) + l);
   }
   // ---- CTA reduction -> MLP partial slot
   fence_before();
   __syncthreads();
   if (warp == 0)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(K::kCols2) : "memory");
+  if (w.dbg & 4) return;
   constexpr int NGP = S::NG;
   float* red = rows_all;
   {
@@ -863,7 +870,12 @@ __global__ void __launch_bounds__(kTile, 2) k_bwd_color_t5(Ws<float> w, Geo G, i
     float inp[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) inp[i] = 0.f;
-    gather_fast<float, S::CC>(G.col, q, inp);
+    if (w.dbg & 8) {
+#pragma unroll
+      for (int c = 0; c < S::CC; ++c) inp[c] = 1e-3f * (float)c + q.fx;
+    } else {
+      gather_fast<float, S::CC>(G.col, q, inp);
+    }
 #pragma unroll
     for (int a = 0; a < 3; ++a) inp[S::CC + a] = w.r[ray * 3 + a];
     inp[S::IN_C] = 1.f;  // ones column: db0c rides on the dW0c outer product (zero weight row in W0c^T)
@@ -969,7 +981,7 @@ __global__ void __launch_bounds__(kTile, 2) k_bwd_color_t5(Ws<float> w, Geo G, i
   tc::zero_d(e0);
   tc::zero_d(e1);
 #pragma unroll
-  for (int ks = 0; ks < 4; ++ks) {
+  for (int ks = 0; ks < ((w.dbg & 2) ? 0 : 4); ++ks) {
     const int k0 = ks * 8;
     uint32_t ah[2][4], al[2][4], bh0[4], bh1[4], bl0[4], bl1[4];
     {
@@ -1007,7 +1019,9 @@ __global__ void __launch_bounds__(kTile, 2) k_bwd_color_t5(Ws<float> w, Geo G, i
   {
     float wk[8];
     corner_w(q, wk);
-    scatter_level<float, S::CC>(G.col, q, fb, wk, active, false, w.det_keys, w.det_vals, s * (S::NL + 1) + S::NL);
+    if (!(w.dbg & 1))
+      scatter_level<float, S::CC>(G.col, q, fb, wk, active, false, w.det_keys, w.det_vals,
+                                  s * (S::NL + 1) + S::NL);
   }
   if (w.pose_fb && active) {  // pose refinement: f_bar and the view-direction cotangent
     float* o = w.pose_fb + s * 12;
@@ -1019,6 +1033,7 @@ __global__ void __launch_bounds__(kTile, 2) k_bwd_color_t5(Ws<float> w, Geo G, i
   __syncthreads();
   if (warp == 0)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kCols) : "memory");
+  if (w.dbg & 4) return;
   constexpr int NCP = S::NMLP - S::NG;
   float* red = rows_all;
   {

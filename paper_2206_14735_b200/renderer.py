@@ -154,7 +154,7 @@ def train_objective(model, dataset, batch, iteration, cfg, smooth_override=None,
     if hasattr(batch, "near_value"):
         near, far = batch.near_value, batch.far_value
     else:
-        near, far = float(np.asarray(batch.near)[0]), float(np.asarray(batch.far)[0])
+        near, far = _check_foreign_batch(batch, dataset)
     if near != cfg.near or far != cfg.max_depth:
         cfg = _with(cfg, near=near, max_depth=far)
     eng = engine_for(model, dataset)
@@ -190,6 +190,24 @@ def train_objective(model, dataset, batch, iteration, cfg, smooth_override=None,
 
     total = Objective(parts["total"], model, arena.generation)
     return total, parts, _Extras(extras, fetch)
+
+
+def _check_foreign_batch(batch, dataset):
+    """A reference-shaped RayBatch (gs/sampler.py:35-55) carries per-ray
+    bounds and targets; the device step derives the targets from the ray ids
+    and takes one near / far for the batch (what draw_ray_batch produces).
+    Anything else would be trained on different inputs: refuse it."""
+    from .sampler import RayBatch
+    nr, fr = np.asarray(batch.near, dtype=np.float64), np.asarray(batch.far, dtype=np.float64)
+    if nr.size == 0:
+        raise ValueError("empty ray batch")
+    if np.any(nr != nr[0]) or np.any(fr != fr[0]):
+        raise ValueError("per-ray near/far bounds are not supported: the batch must share one near and far")
+    mine = RayBatch(dataset, batch_ray_ids(batch, dataset), nr[0], fr[0])
+    for k in ("color", "depth_ray", "valid", "dir_cam"):
+        if hasattr(batch, k) and not np.array_equal(np.asarray(getattr(batch, k)), getattr(mine, k)):
+            raise ValueError(f"batch.{k} differs from the dataset's values at the batch's pixels")
+    return float(nr[0]), float(fr[0])
 
 
 def _with(cfg, **kw):

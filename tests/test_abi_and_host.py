@@ -215,3 +215,29 @@ def test_build_model_refuses_cpu_device():
     ds = data.Dataset(G.a["colors_u8"], G.a["depths_u16"], G.a["poses"], G.ds.intrinsics)
     with pytest.raises(RuntimeError, match="CUDA"):
         optimizer.build_model(ds, cfg, skip_init=True)
+
+
+def test_foreign_batch_checks():
+    """A reference-shaped batch (per-ray arrays) is accepted only when its
+    bounds are uniform and its targets are the dataset's (renderer.py)."""
+    from types import SimpleNamespace
+    from _golden import load
+    from paper_2206_14735_b200 import camera, data, sampler
+    from paper_2206_14735_b200.renderer import _check_foreign_batch
+    G = load("tiny", "double")
+    i = G.ds.intrinsics
+    ds = data.Dataset(G.a["colors_u8"], G.a["depths_u16"], G.a["poses"],
+                      camera.Intrinsics(i.fx, i.fy, i.cx, i.cy, i.width, i.height))
+    b = sampler.draw_ray_batch(ds, np.random.default_rng(0), 16, near=0.01, far=8.0)
+    ref = SimpleNamespace(**{k: getattr(b, k) for k in ("frame_ids", "pixels", "color", "depth_ray",
+                                                        "valid", "dir_cam", "near", "far")})
+    assert _check_foreign_batch(ref, ds) == (0.01, 8.0)
+    bad = SimpleNamespace(**vars(ref))
+    bad.far = ref.far.copy()
+    bad.far[3] = 5.0
+    with pytest.raises(ValueError, match="near/far"):
+        _check_foreign_batch(bad, ds)
+    bad = SimpleNamespace(**vars(ref))
+    bad.color = ref.color + 0.01
+    with pytest.raises(ValueError, match="color"):
+        _check_foreign_batch(bad, ds)
