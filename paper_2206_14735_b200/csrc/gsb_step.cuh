@@ -40,8 +40,10 @@ inline int t5_mode() {
   return v;
 }
 inline bool use_t5(bool coarse = true) { return t5_mode() == 1 || (t5_mode() == 2 && coarse); }
-// taped forward form: GSB_T5_FWD=0 mma.sync (tc::k_fwd_tc); k > 0 tcgen05
-// (t5::k_fwd_t5) with k CTAs per SM (3 or 4; register cap 170 / 128)
+// taped forward form: GSB_T5_FWD=0 mma.sync (tc::k_fwd_tc); > 0 tcgen05
+// (t5::k_fwd_t5, 4 CTAs per SM, register cap 128).  (A 3-CTA / 170-register
+// variant measured slower, 201 vs 190 us, and failed the conditioned float32
+// gradient check intermittently; it was removed.)
 // geometry backward form: GSB_T5_BWD=1 (default) tcgen05 (t5::k_bwd_geom_t5), 0 mma.sync
 inline bool use_t5_bwd() {
   static const bool v = [] {
@@ -242,15 +244,11 @@ int run_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step
     if (runA) {
     if constexpr (F32) {
       constexpr int FW = 4;  // warps per CTA of the taped forward
-      if (const int cps = t5_fwd_mode(); cps > 0) {
+      if (t5_fwd_mode() > 0) {
         const int64_t tiles = (ns + t5::kTile - 1) / t5::kTile;
-        const int grid = (int)std::min<int64_t>(tiles, (int64_t)sm_count() * (cps == 3 ? 3 : 4));
-        if (grid > 0) {
-          if (cps == 3)
-            t5::k_fwd_t5<S, 3><<<grid, t5::kTile, t5::FwdT5::smem(), stream>>>(w, G, M, N, dep_final, spts, nsp);
-          else
-            t5::k_fwd_t5<S, 4><<<grid, t5::kTile, t5::FwdT5::smem(), stream>>>(w, G, M, N, dep_final, spts, nsp);
-        }
+        const int grid = (int)std::min<int64_t>(tiles, (int64_t)sm_count() * t5::kCtaPerSm);
+        if (grid > 0)
+          t5::k_fwd_t5<S><<<grid, t5::kTile, t5::FwdT5::smem(), stream>>>(w, G, M, N, dep_final, spts, nsp);
       } else {
         GSB_CHECK(cudaFuncSetAttribute(tc::k_fwd_tc<S, FW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)tc::FwdTc<S, FW>::smem()));
@@ -313,15 +311,20 @@ int run_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step
         return v < 1 ? 1 : (v > kNbMax ? kNbMax : v);
       }();
       w.mlp_slots = w.det_keys ? 0 : kMlpSlots;  // deterministic mode: per-CTA rows
+      if (use_t5_bwd())  // persistent: two CTAs per SM loop over the 128-sample tiles
+        nb_geo = (int)std::min<int64_t>((ns + t5::kTile - 1) / t5::kTile,
+                                        (int64_t)sm_count() * t5::GeoT5::kCtaPerSm);
+      if (use_t5_col())
+        nb_col = (int)std::min<int64_t>((z.MN + t5::kTile - 1) / t5::kTile,
+                                        (int64_t)sm_count() * t5::ColT5::kCtaPerSm);
       if (runA) {
         if (w.mlp_slots)
           GSB_CHECK(cudaMemsetAsync(w.mlp_part, 0, (size_t)kMlpSlots * S::NMLPP * sizeof(T), stream));
         if (use_t5_bwd()) {
-          const size_t smem_t5 = t5::GeoT5::smem();
+          const size_t smem_t5 = t5::GeoT5::smem<S>();
           GSB_CHECK(cudaFuncSetAttribute(t5::k_bwd_geom_t5<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem_t5));
-          t5::k_bwd_geom_t5<S><<<(int)((ns + t5::kTile - 1) / t5::kTile), t5::kTile, smem_t5, stream>>>(
-              w, G, M, N, dep_final, spts, nsp, 2);
+          t5::k_bwd_geom_t5<S><<<nb_geo, t5::kTile, smem_t5, stream>>>(w, G, M, N, dep_final, spts, nsp, 2);
         } else {
           tc::k_bwd_geom_tc<S, WGEO><<<nb_geo, WGEO * 32, smem_g, stream>>>(w, G, M, N, mlp32,
                                                                             dep_final, spts, nsp, 2);
@@ -330,11 +333,10 @@ int run_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step
       }
       if (runB) {
         if (use_t5_col()) {
-          const size_t smem_t5 = t5::ColT5::smem();
+          const size_t smem_t5 = t5::ColT5::smem<S>();
           GSB_CHECK(cudaFuncSetAttribute(t5::k_bwd_color_t5<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem_t5));
-          t5::k_bwd_color_t5<S><<<(int)((z.MN + t5::kTile - 1) / t5::kTile), t5::kTile, smem_t5, stream>>>(
-              w, G, M, N, dep_final);
+          t5::k_bwd_color_t5<S><<<nb_col, t5::kTile, smem_t5, stream>>>(w, G, M, N, dep_final);
         } else {
           tc::k_bwd_color_tc<S, WCOL><<<nb_col, WCOL * 32, smem_c, stream>>>(w, G, M, N, mlp32, dep_final);
         }

@@ -294,8 +294,8 @@ struct FwdT5 {
   static constexpr size_t smem() { return (size_t)(tc::UmmaW::NFWD + tc::GVec::N + tc::CVec::N) * 4; }
 };
 
-template <class S, int CPS>
-__global__ void __launch_bounds__(kTile, CPS) k_fwd_t5(Ws<float> w, Geo G, int M, int N,
+template <class S>
+__global__ void __launch_bounds__(kTile, kCtaPerSm) k_fwd_t5(Ws<float> w, Geo G, int M, int N,
                                                  const double* __restrict__ dep,
                                                  const float* __restrict__ spts, int nsp) {
   using F = tc::Fr<S>;
@@ -483,16 +483,41 @@ __global__ void __launch_bounds__(kTile, CPS) k_fwd_t5(Ws<float> w, Geo G, int M
 // weight-gradient outer products (contraction over samples) stay on
 // mma.sync over the sample-major rows, as in the tc kernel.  256 TMEM
 // columns: D0 [0,32), D1 [32,64), A1 hi/lo [64,128), A2 hi/lo [128,192);
-// 78 KB shared memory: 2 CTAs per SM (3 CTAs with 128 columns, 5 MMA rounds
-// and a 168-register cap measured slower: 432 vs 390 us).
+// 104 KB shared memory: 2 CTAs per SM (3 CTAs with 128 columns, 5 MMA rounds
+// and a 168-register cap measured slower: 432 vs 390 us).  Persistent: a CTA
+// loops over tiles and keeps its MLP-gradient sums (outer products in shared
+// memory, column sums in registers) across them, so the CTA reduction and
+// the L2 reds into the partial rows happen once per CTA instead of once per
+// 128-sample tile (GSB_DBG attribution: that per-tile reduction was 47 of
+// 376 us).
 
 struct GeoT5 {
   static constexpr int ROW = 104;  // 104 % 32 = 8: fragment loads conflict-free (88 measured slower)
   static constexpr int oA0 = 16, oM = 33, oB0 = 40, oA1 = 72;  // p z + v, m1 bits, delta0, p h0 + q0
   static constexpr int NW = tc::UmmaW::W0NL + 512;              // geometry tiles only
   static constexpr uint32_t kCols2 = 256;
-  static constexpr size_t smem() { return (size_t)(NW + tc::GVec::N) * 4 + (size_t)kTile * ROW * 4; }
+  static constexpr int kCtaPerSm = 2;
+  // weights + vectors, the per-warp sample rows, and the per-warp MLP-gradient
+  // accumulators that persist across the CTA's tiles
+  template <class S>
+  static constexpr size_t smem() {
+    return (size_t)(NW + tc::GVec::N) * 4 + (size_t)kTile * ROW * 4 + (size_t)4 * ((S::NG + 3) / 4 * 4) * 4;
+  }
 };
+
+// d (an m16n8 fp32 D fragment) added into a row-major [rows][GSB_HID] block
+__device__ __forceinline__ void frag_d_add(const float (&d)[4], float* out, int m0, int n0, int mrows) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const int r0 = m0 + g, r1 = m0 + g + 8, c = n0 + 2 * t;
+  if (r0 < mrows) {
+    out[r0 * GSB_HID + c] += d[0];
+    out[r0 * GSB_HID + c + 1] += d[1];
+  }
+  if (r1 < mrows) {
+    out[r1 * GSB_HID + c] += d[2];
+    out[r1 * GSB_HID + c + 1] += d[3];
+  }
+}
 
 // x (W columns) as tf32 hi / lo to TMEM columns chi / clo of this warp's lanes
 template <int W>
@@ -547,11 +572,13 @@ __global__ void __launch_bounds__(kTile, 2) k_bwd_geom_t5(Ws<float> w, Geo G, in
   using U = tc::UmmaW;
   using K = GeoT5;
   constexpr int KG = F::KG, ROW = K::ROW;
+  constexpr int NGP = (S::NG + 3) / 4 * 4;
   static_assert(S::IN_G <= 16 && 8 * KG <= 16, "geometry input width");
   extern __shared__ __align__(128) float t5_smem[];
   float* sw = t5_smem;
   const float* gvec = t5_smem + K::NW;
   float* rows_all = t5_smem + K::NW + tc::GVec::N;
+  float* acc_all = rows_all + (size_t)kTile * ROW;  // [4 warps][NGP], persists across tiles
   __shared__ __align__(8) uint64_t s_bar[2];
   __shared__ uint32_t s_tmem;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -565,6 +592,8 @@ __global__ void __launch_bounds__(kTile, 2) k_bwd_geom_t5(Ws<float> w, Geo G, in
     tc::mbar_init(&s_bar[0]);
     tc::mbar_init(&s_bar[1]);
   }
+  float* acc = acc_all + (size_t)warp * NGP;
+  for (int i = lane; i < NGP; i += 32) acc[i] = 0.f;
   fence_before();
   __syncthreads();
   fence_after();
@@ -580,62 +609,7 @@ __global__ void __launch_bounds__(kTile, 2) k_bwd_geom_t5(Ws<float> w, Geo G, in
   float* rows = rows_all + warp * 32 * ROW;
   float* myrow = rows + lane * ROW;
   const int64_t MN = (int64_t)M * N, NS = MN + nsp;
-  const int64_t s = (int64_t)((w.sweep & 2) ? gridDim.x - 1 - blockIdx.x : blockIdx.x) * kTile + tid;
-  const bool active = s < NS;
-  // ---- per sample: point, z and v in one pass over the corners
-  LocT<float> loc[S::NL];
-  float p = 0.f, u[3] = {0.f, 0.f, 0.f};
-  {
-    float pt[3];
-    if (active) {
-      p = w.pbar[s];
-#pragma unroll
-      for (int a = 0; a < 3; ++a) u[a] = w.ubar[s * 3 + a];
-      if (s < MN) {
-        const int ray = (int)((uint32_t)s / (uint32_t)N);
-        taped_point<float>(w.o + ray * 3, w.r + ray * 3,
-                           dep[(int64_t)ray * w.ld + (int)((uint32_t)s % (uint32_t)N)], G.lo, G.hi, pt);
-      } else {
-#pragma unroll
-        for (int a = 0; a < 3; ++a) pt[a] = spts[(s - MN) * 3 + a];
-      }
-    } else {
-#pragma unroll
-      for (int a = 0; a < 3; ++a) pt[a] = (float)G.lo[a];
-    }
-    float z[16], v[16];
-#pragma unroll
-    for (int i = 0; i < 16; ++i) z[i] = v[i] = 0.f;
-#pragma unroll
-    for (int l = 0; l < S::NL; ++l) {
-      const LevelDev& L = G.lv[l];
-      const LocT<float> lq = compact<float>(locate<false>(L, (double)pt[0], (double)pt[1], (double)pt[2], nullptr));
-      loc[l] = lq;
-      float wk[8], ju[8];
-      corner_w_ju(lq, (float)L.inv_vs, u, wk, ju);
-      const float* Fp = reinterpret_cast<const float*>(L.feat) + (int64_t)lq.base * S::CG;
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        float row[S::CG];
-        if (w.dbg & 8) {
-#pragma unroll
-          for (int c = 0; c < S::CG; ++c) row[c] = 1e-3f * (float)(c + k);
-        } else {
-          load_row<float, S::CG>(Fp + corner_off(L, k) * S::CG, row);
-        }
-#pragma unroll
-        for (int c = 0; c < S::CG; ++c) {
-          z[l * S::CG + c] = fmaf(wk[k], row[c], z[l * S::CG + c]);
-          v[l * S::CG + c] = fmaf(ju[k], row[c], v[l * S::CG + c]);
-        }
-      }
-    }
-#pragma unroll
-    for (int i = 0; i < 16; i += 2)
-      *reinterpret_cast<float2*>(myrow + K::oA0 + i) = make_float2(fmaf(p, z[i], v[i]), fmaf(p, z[i + 1], v[i + 1]));
-    store_hl<8 * KG>(tl, 64, 96, z);
-    store_hl<8 * KG>(tl, 128, 160, v);
-  }
+  const int64_t ntiles = (NS + kTile - 1) / kTile;
   uint32_t phase = 0;
   auto mma_round = [&](auto issue) {
     cta_sync_tmem();
@@ -647,148 +621,213 @@ __global__ void __launch_bounds__(kTile, 2) k_bwd_geom_t5(Ws<float> w, Geo G, in
     phase ^= 1u;
     fence_after();
   };
-  tc::mbar_wait(&s_bar[0], 0);
-  // S1
-  mma_round([&] {
-    issue_at<KG>(tmem, tmem + 64, tmem + 96, sa(U::W0H), sa(U::W0L));
-    issue_at<KG>(tmem + 32, tmem + 128, tmem + 160, sa(U::W0H), sa(U::W0L));
-  });
-  float h[32], q[32];
-  uint32_t m0 = 0u, m1 = 0u;
-  ld32(tl, h);
-  ld32(tl + 32, q);
-#pragma unroll
-  for (int n = 0; n < 32; ++n) {
-    const float x = h[n] + gvec[tc::GVec::b0 + n];
-    const bool pos = x > 0.f;
-    h[n] = pos ? x : 0.f;
-    q[n] = pos ? q[n] : 0.f;
-    m0 |= (uint32_t)pos << n;
-  }
-#pragma unroll
-  for (int n = 0; n < 32; n += 2)
-    *reinterpret_cast<float2*>(myrow + K::oA1 + n) = make_float2(fmaf(p, h[n], q[n]), fmaf(p, h[n + 1], q[n + 1]));
-  store_hl<32>(tl, 64, 96, h);
-  store_hl<32>(tl, 128, 160, q);
-  // S2
-  mma_round([&] {
-    issue_at<4>(tmem, tmem + 64, tmem + 96, sa(U::W1H), sa(U::W1L));
-    issue_at<4>(tmem + 32, tmem + 128, tmem + 160, sa(U::W1H), sa(U::W1L));
-  });
-  ld32(tl, h);
-  ld32(tl + 32, q);
-  float acc_b0, acc_b1, acc_w2;
-#pragma unroll
-  for (int n = 0; n < 32; ++n) {
-    const float x = h[n] + gvec[tc::GVec::b1 + n];
-    const bool pos = x > 0.f;
-    m1 |= (uint32_t)pos << n;
-    q[n] = (pos ? p * x : 0.f) + (pos ? q[n] : 0.f);  // dW2: p relu(h1) + dd1
-    h[n] = pos ? gvec[tc::GVec::w2 + n] : 0.f;        // delta1
-  }
-  myrow[K::oM] = __uint_as_float(m1);
-  acc_w2 = warp_colsum32(q);
-  store_hl<32>(tl, 64, 96, h);
-#pragma unroll
-  for (int n = 0; n < 32; ++n) h[n] *= p;
-  acc_b1 = warp_colsum32(h);
-  // S3
-  mma_round([&] { issue_at<4>(tmem, tmem + 64, tmem + 96, sa(U::W1NH), sa(U::W1NL)); });
-  ld32(tl, h);
-#pragma unroll
-  for (int n = 0; n < 32; ++n) h[n] = ((m0 >> n) & 1u) ? h[n] : 0.f;
-#pragma unroll
-  for (int n = 0; n < 32; n += 2) *reinterpret_cast<float2*>(myrow + K::oB0 + n) = make_float2(h[n], h[n + 1]);
-  store_hl<32>(tl, 64, 96, h);
-#pragma unroll
-  for (int n = 0; n < 32; ++n) h[n] *= p;
-  acc_b0 = warp_colsum32(h);
-  // S4 (dphi/dz to D0 [0, 16)); the outer products overlap it
-  cta_sync_tmem();
-  if (tid == 0) {
-    issue_at<4, 16>(tmem, tmem + 64, tmem + 96, sa(U::W0NH), sa(U::W0NL));
-    commit(&s_bar[1]);
-  }
-  __syncwarp();
-  // ---- outer products over the warp's samples: dW0 += A0^T delta0, dW1 += A1^T delta1
-  const int g = lane >> 2, t = lane & 3;
-  float d0[1][4][4], d1[2][4][4];
-  tc::zero_d(d0);
-  tc::zero_d(d1);
-  const float w2l = gvec[tc::GVec::w2 + lane];
-#pragma unroll
-  for (int ks = 0; ks < ((w.dbg & 2) ? 0 : 4); ++ks) {
-    const int k0 = ks * 8;
-    const uint32_t mk0 = __float_as_uint(rows[(k0 + t) * ROW + K::oM]);
-    const uint32_t mk1 = __float_as_uint(rows[(k0 + t + 4) * ROW + K::oM]);
-    uint32_t ah[2][4], al[2][4], bh0[4], bh1[4], bl0[4], bl1[4];
+  // column sums (db0, db1, dW2 per lane = column; db2) summed over the tiles
+  float sum_b0 = 0.f, sum_b1 = 0.f, sum_w2 = 0.f, sum_p = 0.f;
+  bool weights_ready = false;
+  // persistent: tiles blockIdx, blockIdx + grid, ... (the sweep maps them
+  // last-to-first: the cells the forward touched last are still in L2)
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t tt = (w.sweep & 2) ? ntiles - 1 - tile : tile;
+    const int64_t s = tt * kTile + tid;
+    const bool active = s < NS;
+    __syncwarp();  // the previous tile's outer products are done with this warp's rows
+    // ---- per sample: point, z and v in one pass over the corners
+    LocT<float> loc[S::NL];
+    float p = 0.f, u[3] = {0.f, 0.f, 0.f};
     {
-      uint32_t a1h[1][4], a1l[1][4];
-      frag_a(rows, ROW, K::oA0, k0, 0, a1h[0], a1l[0]);
+      float pt[3];
+      if (active) {
+        p = w.pbar[s];
 #pragma unroll
-      for (int nt = 0; nt < 4; ++nt) frag_b(rows, ROW, K::oB0, k0, nt * 8, bh0[nt], bh1[nt], bl0[nt], bl1[nt]);
-      tc::mma3_sweep(d0, a1h, a1l, bh0, bh1, bl0, bl1);
+        for (int a = 0; a < 3; ++a) u[a] = w.ubar[s * 3 + a];
+        if (s < MN) {
+          const int ray = (int)((uint32_t)s / (uint32_t)N);
+          taped_point<float>(w.o + ray * 3, w.r + ray * 3,
+                             dep[(int64_t)ray * w.ld + (int)((uint32_t)s % (uint32_t)N)], G.lo, G.hi, pt);
+        } else {
+#pragma unroll
+          for (int a = 0; a < 3; ++a) pt[a] = spts[(s - MN) * 3 + a];
+        }
+      } else {
+#pragma unroll
+        for (int a = 0; a < 3; ++a) pt[a] = (float)G.lo[a];
+      }
+      float z[16], v[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) z[i] = v[i] = 0.f;
+#pragma unroll
+      for (int l = 0; l < S::NL; ++l) {
+        const LevelDev& L = G.lv[l];
+        const LocT<float> lq = compact<float>(locate<false>(L, (double)pt[0], (double)pt[1], (double)pt[2], nullptr));
+        loc[l] = lq;
+        float wk[8], ju[8];
+        corner_w_ju(lq, (float)L.inv_vs, u, wk, ju);
+        const float* Fp = reinterpret_cast<const float*>(L.feat) + (int64_t)lq.base * S::CG;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          float row[S::CG];
+          if (w.dbg & 8) {
+#pragma unroll
+            for (int c = 0; c < S::CG; ++c) row[c] = 1e-3f * (float)(c + k);
+          } else {
+            load_row<float, S::CG>(Fp + corner_off(L, k) * S::CG, row);
+          }
+#pragma unroll
+          for (int c = 0; c < S::CG; ++c) {
+            z[l * S::CG + c] = fmaf(wk[k], row[c], z[l * S::CG + c]);
+            v[l * S::CG + c] = fmaf(ju[k], row[c], v[l * S::CG + c]);
+          }
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 16; i += 2)
+        *reinterpret_cast<float2*>(myrow + K::oA0 + i) = make_float2(fmaf(p, z[i], v[i]), fmaf(p, z[i + 1], v[i + 1]));
+      store_hl<8 * KG>(tl, 64, 96, z);
+      store_hl<8 * KG>(tl, 128, 160, v);
+    }
+    if (!weights_ready) {
+      tc::mbar_wait(&s_bar[0], 0);
+      weights_ready = true;
+    }
+    // S1
+    mma_round([&] {
+      issue_at<KG>(tmem, tmem + 64, tmem + 96, sa(U::W0H), sa(U::W0L));
+      issue_at<KG>(tmem + 32, tmem + 128, tmem + 160, sa(U::W0H), sa(U::W0L));
+    });
+    float h[32], q[32];
+    uint32_t m0 = 0u, m1 = 0u;
+    ld32(tl, h);
+    ld32(tl + 32, q);
+#pragma unroll
+    for (int n = 0; n < 32; ++n) {
+      const float x = h[n] + gvec[tc::GVec::b0 + n];
+      const bool pos = x > 0.f;
+      h[n] = pos ? x : 0.f;
+      q[n] = pos ? q[n] : 0.f;
+      m0 |= (uint32_t)pos << n;
     }
 #pragma unroll
-    for (int nt = 0; nt < 4; ++nt) {
-      const int n = nt * 8 + g;
-      const float w2n = __shfl_sync(0xffffffffu, w2l, n);
-      split_fast(((mk0 >> n) & 1u) ? w2n : 0.f, bh0[nt], bl0[nt]);
-      split_fast(((mk1 >> n) & 1u) ? w2n : 0.f, bh1[nt], bl1[nt]);
+    for (int n = 0; n < 32; n += 2)
+      *reinterpret_cast<float2*>(myrow + K::oA1 + n) = make_float2(fmaf(p, h[n], q[n]), fmaf(p, h[n + 1], q[n + 1]));
+    store_hl<32>(tl, 64, 96, h);
+    store_hl<32>(tl, 128, 160, q);
+    // S2
+    mma_round([&] {
+      issue_at<4>(tmem, tmem + 64, tmem + 96, sa(U::W1H), sa(U::W1L));
+      issue_at<4>(tmem + 32, tmem + 128, tmem + 160, sa(U::W1H), sa(U::W1L));
+    });
+    ld32(tl, h);
+    ld32(tl + 32, q);
+#pragma unroll
+    for (int n = 0; n < 32; ++n) {
+      const float x = h[n] + gvec[tc::GVec::b1 + n];
+      const bool pos = x > 0.f;
+      m1 |= (uint32_t)pos << n;
+      q[n] = (pos ? p * x : 0.f) + (pos ? q[n] : 0.f);  // dW2: p relu(h1) + dd1
+      h[n] = pos ? gvec[tc::GVec::w2 + n] : 0.f;        // delta1
     }
+    myrow[K::oM] = __uint_as_float(m1);
+    sum_w2 += warp_colsum32(q);
+    store_hl<32>(tl, 64, 96, h);
 #pragma unroll
-    for (int mt = 0; mt < 2; ++mt) frag_a(rows, ROW, K::oA1, k0, mt * 16, ah[mt], al[mt]);
-    tc::mma3_sweep(d1, ah, al, bh0, bh1, bl0, bl1);
+    for (int n = 0; n < 32; ++n) h[n] *= p;
+    sum_b1 += warp_colsum32(h);
+    // S3
+    mma_round([&] { issue_at<4>(tmem, tmem + 64, tmem + 96, sa(U::W1NH), sa(U::W1NL)); });
+    ld32(tl, h);
+#pragma unroll
+    for (int n = 0; n < 32; ++n) h[n] = ((m0 >> n) & 1u) ? h[n] : 0.f;
+#pragma unroll
+    for (int n = 0; n < 32; n += 2) *reinterpret_cast<float2*>(myrow + K::oB0 + n) = make_float2(h[n], h[n + 1]);
+    store_hl<32>(tl, 64, 96, h);
+#pragma unroll
+    for (int n = 0; n < 32; ++n) h[n] *= p;
+    sum_b0 += warp_colsum32(h);
+    // S4 (dphi/dz to D0 [0, 16)); the outer products overlap it
+    cta_sync_tmem();
+    if (tid == 0) {
+      issue_at<4, 16>(tmem, tmem + 64, tmem + 96, sa(U::W0NH), sa(U::W0NL));
+      commit(&s_bar[1]);
+    }
+    __syncwarp();
+    // ---- outer products over the warp's samples: dW0 += A0^T delta0, dW1 += A1^T delta1
+    if (!(w.dbg & 2)) {
+      const int g = lane >> 2, t = lane & 3;
+      float d0[1][4][4], d1[2][4][4];
+      tc::zero_d(d0);
+      tc::zero_d(d1);
+      const float w2l = gvec[tc::GVec::w2 + lane];
+#pragma unroll
+      for (int ks = 0; ks < 4; ++ks) {
+        const int k0 = ks * 8;
+        const uint32_t mk0 = __float_as_uint(rows[(k0 + t) * ROW + K::oM]);
+        const uint32_t mk1 = __float_as_uint(rows[(k0 + t + 4) * ROW + K::oM]);
+        uint32_t ah[2][4], al[2][4], bh0[4], bh1[4], bl0[4], bl1[4];
+        {
+          uint32_t a1h[1][4], a1l[1][4];
+          frag_a(rows, ROW, K::oA0, k0, 0, a1h[0], a1l[0]);
+#pragma unroll
+          for (int nt = 0; nt < 4; ++nt) frag_b(rows, ROW, K::oB0, k0, nt * 8, bh0[nt], bh1[nt], bl0[nt], bl1[nt]);
+          tc::mma3_sweep(d0, a1h, a1l, bh0, bh1, bl0, bl1);
+        }
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) {
+          const int n = nt * 8 + g;
+          const float w2n = __shfl_sync(0xffffffffu, w2l, n);
+          split_fast(((mk0 >> n) & 1u) ? w2n : 0.f, bh0[nt], bl0[nt]);
+          split_fast(((mk1 >> n) & 1u) ? w2n : 0.f, bh1[nt], bl1[nt]);
+        }
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) frag_a(rows, ROW, K::oA1, k0, mt * 16, ah[mt], al[mt]);
+        tc::mma3_sweep(d1, ah, al, bh0, bh1, bl0, bl1);
+      }
+      // this tile's products into the warp's running sums (lanes own disjoint entries)
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) frag_d_add(d0[0][nt], acc + S::oGW0, 0, nt * 8, S::IN_G);
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) frag_d_add(d1[mt][nt], acc + S::oGW1, mt * 16, nt * 8, GSB_HID);
+    }
+    float accp = p;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) accp += __shfl_xor_sync(0xffffffffu, accp, o);
+    sum_p += accp;
+    // ---- grid scatter: theta_l[idx_k] += g_l (p w_k + ju_k)
+    tc::mbar_wait(&s_bar[1], phase);
+    phase ^= 1u;
+    fence_after();
+    float gz[16];
+    ld16(tl, gz);
+#pragma unroll
+    for (int l = 0; l < S::NL; ++l) {
+      const LocT<float> lq = loc[l];
+      float wk[8], ju[8], coef[8];
+      corner_w_ju(lq, (float)G.lv[l].inv_vs, u, wk, ju);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) coef[k] = fmaf(p, wk[k], ju[k]);
+      if (!(w.dbg & 1))
+        scatter_level<float, S::CG>(G.lv[l], lq, gz + l * S::CG, coef, active, l < agg_levels, w.det_keys,
+                                    w.det_vals, s * (S::NL + 1) + l);
+    }
   }
-  float accp = p;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) accp += __shfl_xor_sync(0xffffffffu, accp, o);
-  // ---- grid scatter: theta_l[idx_k] += g_l (p w_k + ju_k)
-  tc::mbar_wait(&s_bar[1], phase);
-  fence_after();
-  float gz[16];
-  ld16(tl, gz);
-#pragma unroll
-  for (int l = 0; l < S::NL; ++l) {
-    const LocT<float> lq = loc[l];
-    float wk[8], ju[8], coef[8];
-    corner_w_ju(lq, (float)G.lv[l].inv_vs, u, wk, ju);
-#pragma unroll
-    for (int k = 0; k < 8; ++k) coef[k] = fmaf(p, wk[k], ju[k]);
-    if (!(w.dbg & 1))
-      scatter_level<float, S::CG>(G.lv[l], lq, gz + l * S::CG, coef, active, l < agg_levels, w.det_keys,
-                                  w.det_vals, s * (S::NL + 1) + l);
-  }
-  // ---- CTA reduction -> MLP partial slot
+  // ---- CTA reduction of the running sums -> MLP partial slot (once per CTA)
   fence_before();
   __syncthreads();
   if (warp == 0)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(K::kCols2) : "memory");
   if (w.dbg & 4) return;
-  constexpr int NGP = S::NG;
-  float* red = rows_all;
-  {
-    float* mine = red + (size_t)warp * NGP;
-#pragma unroll
-    for (int nt = 0; nt < 4; ++nt) frag_d_store(d0[0][nt], mine + S::oGW0, 0, nt * 8, S::IN_G);
-#pragma unroll
-    for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-      for (int nt = 0; nt < 4; ++nt) frag_d_store(d1[mt][nt], mine + S::oGW1, mt * 16, nt * 8, GSB_HID);
-    mine[S::oGb0 + lane] = acc_b0;
-    mine[S::oGb1 + lane] = acc_b1;
-    mine[S::oGW2 + lane] = acc_w2;
-    if (lane == 0) mine[S::oGb2] = accp;
-  }
+  acc[S::oGb0 + lane] += sum_b0;
+  acc[S::oGb1 + lane] += sum_b1;
+  acc[S::oGW2 + lane] += sum_w2;
+  if (lane == 0) acc[S::oGb2] += sum_p;
   __syncthreads();
   const int slot = w.mlp_slots > 0 ? (int)(blockIdx.x % (unsigned)w.mlp_slots) : (int)blockIdx.x;
   float* out = w.mlp_part + (size_t)slot * S::NMLPP;
-  // (scalar reds: the 4-wide vector form measured slower here, 399 vs 371 us,
-  // while it pays in the colour backward)
-  for (int i = tid; i < NGP; i += kTile) {
+  for (int i = tid; i < S::NG; i += kTile) {
     float a = 0.f;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) a += red[(size_t)k * NGP + i];
+    for (int k = 0; k < 4; ++k) a += acc_all[(size_t)k * NGP + i];
     if (w.mlp_slots > 0)
       atomicAdd(out + i, a);
     else
@@ -811,7 +850,13 @@ struct ColT5 {
   static constexpr int ROW = 104;
   static constexpr int oA0 = 0, oB0 = 16, oA1 = 48, oY = 80, oM = 88;
   static constexpr int W0 = tc::UmmaW::C0H, NW = tc::UmmaW::N - tc::UmmaW::C0H;  // colour tiles
-  static constexpr size_t smem() { return (size_t)(NW + tc::CVec::N) * 4 + (size_t)kTile * ROW * 4; }
+  static constexpr int kCtaPerSm = 2;
+  // weights + vectors, the per-warp sample rows, and the per-warp colour
+  // MLP-gradient sums that persist across the CTA's tiles
+  template <class S>
+  static constexpr size_t smem() {
+    return (size_t)(NW + tc::CVec::N) * 4 + (size_t)kTile * ROW * 4 + (size_t)4 * (S::NMLP - S::NG) * 4;
+  }
 };
 
 template <class S>
@@ -821,11 +866,14 @@ __global__ void __launch_bounds__(kTile, 2) k_bwd_color_t5(Ws<float> w, Geo G, i
   using U = tc::UmmaW;
   using K = ColT5;
   constexpr int KC = F::KC, ROW = K::ROW;
+  constexpr int NCP = S::NMLP - S::NG, o = S::NG;
   static_assert(S::IN_C + 1 <= 16 && 8 * KC <= 16 && S::CC <= 8, "colour input width");
+  static_assert(S::oCb0 == S::oCW0 + S::IN_C * GSB_HID, "db0c is the ones row of dW0c");
   extern __shared__ __align__(128) float t5_smem[];
   float* sw = t5_smem - K::W0;  // indexed by UmmaW offsets
   const float* cvec = t5_smem + K::NW;
   float* rows_all = t5_smem + K::NW + tc::CVec::N;
+  float* acc_all = rows_all + (size_t)kTile * ROW;  // [4 warps][NCP], persists across tiles
   __shared__ __align__(8) uint64_t s_bar[2];
   __shared__ uint32_t s_tmem;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -839,6 +887,8 @@ __global__ void __launch_bounds__(kTile, 2) k_bwd_color_t5(Ws<float> w, Geo G, i
     tc::mbar_init(&s_bar[0]);
     tc::mbar_init(&s_bar[1]);
   }
+  float* acc = acc_all + (size_t)warp * NCP;
+  for (int i = lane; i < NCP; i += 32) acc[i] = 0.f;
   fence_before();
   __syncthreads();
   fence_after();
@@ -855,34 +905,7 @@ __global__ void __launch_bounds__(kTile, 2) k_bwd_color_t5(Ws<float> w, Geo G, i
   float* rows = rows_all + warp * 32 * ROW;
   float* myrow = rows + lane * ROW;
   const int64_t NS = (int64_t)M * N;
-  const int64_t s = (int64_t)((w.sweep & 4) ? gridDim.x - 1 - blockIdx.x : blockIdx.x) * kTile + tid;
-  const bool active = s < NS;
-  const int ray = active ? (int)((uint32_t)s / (uint32_t)N) : 0;
-  LocT<float> q;
-  float cb[3];
-  {
-    float pt[3];
-    taped_point<float>(w.o + ray * 3, w.r + ray * 3,
-                       active ? dep[(int64_t)ray * w.ld + (int)((uint32_t)s % (uint32_t)N)] : 0.0, G.lo, G.hi, pt);
-#pragma unroll
-    for (int c = 0; c < 3; ++c) cb[c] = active ? w.cbar[s * 3 + c] : 0.f;
-    q = compact<float>(locate<false>(G.col, (double)pt[0], (double)pt[1], (double)pt[2], nullptr));
-    float inp[16];
-#pragma unroll
-    for (int i = 0; i < 16; ++i) inp[i] = 0.f;
-    if (w.dbg & 8) {
-#pragma unroll
-      for (int c = 0; c < S::CC; ++c) inp[c] = 1e-3f * (float)c + q.fx;
-    } else {
-      gather_fast<float, S::CC>(G.col, q, inp);
-    }
-#pragma unroll
-    for (int a = 0; a < 3; ++a) inp[S::CC + a] = w.r[ray * 3 + a];
-    inp[S::IN_C] = 1.f;  // ones column: db0c rides on the dW0c outer product (zero weight row in W0c^T)
-#pragma unroll
-    for (int i = 0; i < 16; i += 2) *reinterpret_cast<float2*>(myrow + K::oA0 + i) = make_float2(inp[i], inp[i + 1]);
-    store_hl<8 * KC>(tl, 32, 64, inp);
-  }
+  const int64_t ntiles = (NS + kTile - 1) / kTile;
   uint32_t phase = 0;
   auto mma_round = [&](auto issue) {
     cta_sync_tmem();
@@ -894,165 +917,200 @@ __global__ void __launch_bounds__(kTile, 2) k_bwd_color_t5(Ws<float> w, Geo G, i
     phase ^= 1u;
     fence_after();
   };
-  tc::mbar_wait(&s_bar[0], 0);
-  // R1
-  mma_round([&] { issue_at<KC>(tmem, tmem + 32, tmem + 64, sa(U::C0H), sa(U::C0L)); });
-  float h[32];
-  uint32_t m0 = 0u, m1 = 0u;
-  ld32(tl, h);
-#pragma unroll
-  for (int n = 0; n < 32; ++n) {
-    const float x = h[n] + cvec[tc::CVec::b0 + n];
-    const bool pos = x > 0.f;
-    h[n] = pos ? x : 0.f;
-    m0 |= (uint32_t)pos << n;
-  }
-#pragma unroll
-  for (int n = 0; n < 32; n += 2) *reinterpret_cast<float2*>(myrow + K::oA1 + n) = make_float2(h[n], h[n + 1]);
-  store_hl<32>(tl, 32, 64, h);
-  // R2
-  mma_round([&] { issue_at<4>(tmem, tmem + 32, tmem + 64, sa(U::C1H), sa(U::C1L)); });
-  ld32(tl, h);
-  float y[3] = {cvec[tc::CVec::b2], cvec[tc::CVec::b2 + 1], cvec[tc::CVec::b2 + 2]};
-#pragma unroll
-  for (int n = 0; n < 32; ++n) {
-    const float x = h[n] + cvec[tc::CVec::b1 + n];
-    const bool pos = x > 0.f;
-    h[n] = pos ? x : 0.f;
-    m1 |= (uint32_t)pos << n;
-#pragma unroll
-    for (int c = 0; c < 3; ++c) y[c] = fmaf(h[n], cvec[tc::CVec::w2 + n * 3 + c], y[c]);
-  }
-  float yb[3];
-#pragma unroll
-  for (int c = 0; c < 3; ++c) {
-    const float cc = sigmoid_fast(y[c]);
-    yb[c] = cb[c] * (cc * (1.f - cc));
-    myrow[K::oY + c] = yb[c];
-  }
-  myrow[K::oM] = __uint_as_float(m1);
-  float acc_w2[3], acc_b1, acc_b2[3];
-#pragma unroll
-  for (int c = 0; c < 3; ++c) {  // dW2c[n][c] = sum_s h1c[n] y_bar[c]
-    float v[32];
-#pragma unroll
-    for (int n = 0; n < 32; ++n) v[n] = h[n] * yb[c];
-    acc_w2[c] = warp_colsum32(v);
-  }
-#pragma unroll
-  for (int c = 0; c < 3; ++c) {
-    float a = yb[c];
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-    acc_b2[c] = a;
-  }
-  // a1_bar = (y_bar W2c^T) . m1
-#pragma unroll
-  for (int n = 0; n < 32; ++n) {
-    const float* w2 = cvec + tc::CVec::w2 + n * 3;
-    const float v = fmaf(w2[0], yb[0], fmaf(w2[1], yb[1], w2[2] * yb[2]));
-    h[n] = ((m1 >> n) & 1u) ? v : 0.f;
-  }
-  store_hl<32>(tl, 32, 64, h);
-  acc_b1 = warp_colsum32(h);
-  // R3
-  mma_round([&] { issue_at<4>(tmem, tmem + 32, tmem + 64, sa(U::C1NH), sa(U::C1NL)); });
-  ld32(tl, h);
-#pragma unroll
-  for (int n = 0; n < 32; ++n) h[n] = ((m0 >> n) & 1u) ? h[n] : 0.f;
-#pragma unroll
-  for (int n = 0; n < 32; n += 2) *reinterpret_cast<float2*>(myrow + K::oB0 + n) = make_float2(h[n], h[n + 1]);
-  store_hl<32>(tl, 32, 64, h);
-  // R4: [f_bar, r_bar] to D [0, 16); the outer products overlap it
-  cta_sync_tmem();
-  if (tid == 0) {
-    issue_at<4, 16>(tmem, tmem + 32, tmem + 64, sa(U::C0NH), sa(U::C0NL));
-    commit(&s_bar[1]);
-  }
-  __syncwarp();
-  // ---- outer products over the warp's samples: e0 = [inp,1]^T a0b, e1 = h0c^T a1b
-  const int g = lane >> 2, t = lane & 3;
-  float w2c[4][3];
-#pragma unroll
-  for (int nt = 0; nt < 4; ++nt)
-#pragma unroll
-    for (int c = 0; c < 3; ++c) w2c[nt][c] = cvec[tc::CVec::w2 + (8 * nt + g) * 3 + c];
-  float e0[1][4][4], e1[2][4][4];
-  tc::zero_d(e0);
-  tc::zero_d(e1);
-#pragma unroll
-  for (int ks = 0; ks < ((w.dbg & 2) ? 0 : 4); ++ks) {
-    const int k0 = ks * 8;
-    uint32_t ah[2][4], al[2][4], bh0[4], bh1[4], bl0[4], bl1[4];
+  // column sums (dW2c, db1c per lane = column; db2c) summed over the tiles
+  float sum_w2[3] = {0.f, 0.f, 0.f}, sum_b1 = 0.f, sum_b2[3] = {0.f, 0.f, 0.f};
+  bool weights_ready = false;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t tt = (w.sweep & 4) ? ntiles - 1 - tile : tile;
+    const int64_t s = tt * kTile + tid;
+    const bool active = s < NS;
+    const int ray = active ? (int)((uint32_t)s / (uint32_t)N) : 0;
+    __syncwarp();  // the previous tile's outer products are done with this warp's rows
+    LocT<float> q;
+    float cb[3];
     {
-      uint32_t a1h[1][4], a1l[1][4];
-      frag_a(rows, ROW, K::oA0, k0, 0, a1h[0], a1l[0]);
+      float pt[3];
+      taped_point<float>(w.o + ray * 3, w.r + ray * 3,
+                         active ? dep[(int64_t)ray * w.ld + (int)((uint32_t)s % (uint32_t)N)] : 0.0, G.lo, G.hi,
+                         pt);
 #pragma unroll
-      for (int nt = 0; nt < 4; ++nt) frag_b(rows, ROW, K::oB0, k0, nt * 8, bh0[nt], bh1[nt], bl0[nt], bl1[nt]);
-      tc::mma3_sweep(e0, a1h, a1l, bh0, bh1, bl0, bl1);
-    }
-    {
-      const float* r0 = rows + (k0 + t) * ROW;
-      const float* r1 = rows + (k0 + t + 4) * ROW;
-      const uint32_t mk0 = __float_as_uint(r0[K::oM]);
-      const uint32_t mk1 = __float_as_uint(r1[K::oM]);
-      const float y00 = r0[K::oY], y01 = r0[K::oY + 1], y02 = r0[K::oY + 2];
-      const float y10 = r1[K::oY], y11 = r1[K::oY + 1], y12 = r1[K::oY + 2];
+      for (int c = 0; c < 3; ++c) cb[c] = active ? w.cbar[s * 3 + c] : 0.f;
+      q = compact<float>(locate<false>(G.col, (double)pt[0], (double)pt[1], (double)pt[2], nullptr));
+      float inp[16];
 #pragma unroll
-      for (int nt = 0; nt < 4; ++nt) {
-        const int n = nt * 8 + g;
-        const float v0 = fmaf(w2c[nt][0], y00, fmaf(w2c[nt][1], y01, w2c[nt][2] * y02));
-        const float v1 = fmaf(w2c[nt][0], y10, fmaf(w2c[nt][1], y11, w2c[nt][2] * y12));
-        split_fast(((mk0 >> n) & 1u) ? v0 : 0.f, bh0[nt], bl0[nt]);
-        split_fast(((mk1 >> n) & 1u) ? v1 : 0.f, bh1[nt], bl1[nt]);
+      for (int i = 0; i < 16; ++i) inp[i] = 0.f;
+      if (w.dbg & 8) {
+#pragma unroll
+        for (int c = 0; c < S::CC; ++c) inp[c] = 1e-3f * (float)c + q.fx;
+      } else {
+        gather_fast<float, S::CC>(G.col, q, inp);
       }
 #pragma unroll
-      for (int mt = 0; mt < 2; ++mt) frag_a(rows, ROW, K::oA1, k0, mt * 16, ah[mt], al[mt]);
-      tc::mma3_sweep(e1, ah, al, bh0, bh1, bl0, bl1);
+      for (int a = 0; a < 3; ++a) inp[S::CC + a] = w.r[ray * 3 + a];
+      inp[S::IN_C] = 1.f;  // ones column: db0c rides on the dW0c outer product (zero weight row in W0c^T)
+#pragma unroll
+      for (int i = 0; i < 16; i += 2) *reinterpret_cast<float2*>(myrow + K::oA0 + i) = make_float2(inp[i], inp[i + 1]);
+      store_hl<8 * KC>(tl, 32, 64, inp);
+    }
+    if (!weights_ready) {
+      tc::mbar_wait(&s_bar[0], 0);
+      weights_ready = true;
+    }
+    // R1
+    mma_round([&] { issue_at<KC>(tmem, tmem + 32, tmem + 64, sa(U::C0H), sa(U::C0L)); });
+    float h[32];
+    uint32_t m0 = 0u, m1 = 0u;
+    ld32(tl, h);
+#pragma unroll
+    for (int n = 0; n < 32; ++n) {
+      const float x = h[n] + cvec[tc::CVec::b0 + n];
+      const bool pos = x > 0.f;
+      h[n] = pos ? x : 0.f;
+      m0 |= (uint32_t)pos << n;
+    }
+#pragma unroll
+    for (int n = 0; n < 32; n += 2) *reinterpret_cast<float2*>(myrow + K::oA1 + n) = make_float2(h[n], h[n + 1]);
+    store_hl<32>(tl, 32, 64, h);
+    // R2
+    mma_round([&] { issue_at<4>(tmem, tmem + 32, tmem + 64, sa(U::C1H), sa(U::C1L)); });
+    ld32(tl, h);
+    float y[3] = {cvec[tc::CVec::b2], cvec[tc::CVec::b2 + 1], cvec[tc::CVec::b2 + 2]};
+#pragma unroll
+    for (int n = 0; n < 32; ++n) {
+      const float x = h[n] + cvec[tc::CVec::b1 + n];
+      const bool pos = x > 0.f;
+      h[n] = pos ? x : 0.f;
+      m1 |= (uint32_t)pos << n;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) y[c] = fmaf(h[n], cvec[tc::CVec::w2 + n * 3 + c], y[c]);
+    }
+    float yb[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const float cc = sigmoid_fast(y[c]);
+      yb[c] = cb[c] * (cc * (1.f - cc));
+      myrow[K::oY + c] = yb[c];
+    }
+    myrow[K::oM] = __uint_as_float(m1);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {  // dW2c[n][c] = sum_s h1c[n] y_bar[c]
+      float v[32];
+#pragma unroll
+      for (int n = 0; n < 32; ++n) v[n] = h[n] * yb[c];
+      sum_w2[c] += warp_colsum32(v);
+    }
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      float a = yb[c];
+#pragma unroll
+      for (int sh = 1; sh < 32; sh <<= 1) a += __shfl_xor_sync(0xffffffffu, a, sh);
+      sum_b2[c] += a;
+    }
+    // a1_bar = (y_bar W2c^T) . m1
+#pragma unroll
+    for (int n = 0; n < 32; ++n) {
+      const float* w2 = cvec + tc::CVec::w2 + n * 3;
+      const float v = fmaf(w2[0], yb[0], fmaf(w2[1], yb[1], w2[2] * yb[2]));
+      h[n] = ((m1 >> n) & 1u) ? v : 0.f;
+    }
+    store_hl<32>(tl, 32, 64, h);
+    sum_b1 += warp_colsum32(h);
+    // R3
+    mma_round([&] { issue_at<4>(tmem, tmem + 32, tmem + 64, sa(U::C1NH), sa(U::C1NL)); });
+    ld32(tl, h);
+#pragma unroll
+    for (int n = 0; n < 32; ++n) h[n] = ((m0 >> n) & 1u) ? h[n] : 0.f;
+#pragma unroll
+    for (int n = 0; n < 32; n += 2) *reinterpret_cast<float2*>(myrow + K::oB0 + n) = make_float2(h[n], h[n + 1]);
+    store_hl<32>(tl, 32, 64, h);
+    // R4: [f_bar, r_bar] to D [0, 16); the outer products overlap it
+    cta_sync_tmem();
+    if (tid == 0) {
+      issue_at<4, 16>(tmem, tmem + 32, tmem + 64, sa(U::C0NH), sa(U::C0NL));
+      commit(&s_bar[1]);
+    }
+    __syncwarp();
+    // ---- outer products over the warp's samples: e0 = [inp,1]^T a0b, e1 = h0c^T a1b
+    if (!(w.dbg & 2)) {
+      const int g = lane >> 2, t = lane & 3;
+      float w2c[4][3];
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) w2c[nt][c] = cvec[tc::CVec::w2 + (8 * nt + g) * 3 + c];
+      float e0[1][4][4], e1[2][4][4];
+      tc::zero_d(e0);
+      tc::zero_d(e1);
+#pragma unroll
+      for (int ks = 0; ks < 4; ++ks) {
+        const int k0 = ks * 8;
+        uint32_t ah[2][4], al[2][4], bh0[4], bh1[4], bl0[4], bl1[4];
+        {
+          uint32_t a1h[1][4], a1l[1][4];
+          frag_a(rows, ROW, K::oA0, k0, 0, a1h[0], a1l[0]);
+#pragma unroll
+          for (int nt = 0; nt < 4; ++nt) frag_b(rows, ROW, K::oB0, k0, nt * 8, bh0[nt], bh1[nt], bl0[nt], bl1[nt]);
+          tc::mma3_sweep(e0, a1h, a1l, bh0, bh1, bl0, bl1);
+        }
+        {
+          const float* r0 = rows + (k0 + t) * ROW;
+          const float* r1 = rows + (k0 + t + 4) * ROW;
+          const uint32_t mk0 = __float_as_uint(r0[K::oM]);
+          const uint32_t mk1 = __float_as_uint(r1[K::oM]);
+          const float y00 = r0[K::oY], y01 = r0[K::oY + 1], y02 = r0[K::oY + 2];
+          const float y10 = r1[K::oY], y11 = r1[K::oY + 1], y12 = r1[K::oY + 2];
+#pragma unroll
+          for (int nt = 0; nt < 4; ++nt) {
+            const int n = nt * 8 + g;
+            const float v0 = fmaf(w2c[nt][0], y00, fmaf(w2c[nt][1], y01, w2c[nt][2] * y02));
+            const float v1 = fmaf(w2c[nt][0], y10, fmaf(w2c[nt][1], y11, w2c[nt][2] * y12));
+            split_fast(((mk0 >> n) & 1u) ? v0 : 0.f, bh0[nt], bl0[nt]);
+            split_fast(((mk1 >> n) & 1u) ? v1 : 0.f, bh1[nt], bl1[nt]);
+          }
+#pragma unroll
+          for (int mt = 0; mt < 2; ++mt) frag_a(rows, ROW, K::oA1, k0, mt * 16, ah[mt], al[mt]);
+          tc::mma3_sweep(e1, ah, al, bh0, bh1, bl0, bl1);
+        }
+      }
+      // this tile's products into the warp's running sums (lanes own disjoint entries)
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) frag_d_add(e0[0][nt], acc + (S::oCW0 - o), 0, nt * 8, S::IN_C + 1);
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) frag_d_add(e1[mt][nt], acc + (S::oCW1 - o), mt * 16, nt * 8, GSB_HID);
+    }
+    // ---- colour grid scatter: theta_c[idx_k] += w_k f_bar
+    tc::mbar_wait(&s_bar[1], phase);
+    phase ^= 1u;
+    fence_after();
+    float fb[16];
+    ld16(tl, fb);
+    {
+      float wk[8];
+      corner_w(q, wk);
+      if (!(w.dbg & 1))
+        scatter_level<float, S::CC>(G.col, q, fb, wk, active, false, w.det_keys, w.det_vals,
+                                    s * (S::NL + 1) + S::NL);
+    }
+    if (w.pose_fb && active) {  // pose refinement: f_bar and the view-direction cotangent
+      float* po = w.pose_fb + s * 12;
+#pragma unroll
+      for (int c = 0; c < S::IN_C; ++c) po[c] = fb[c];
     }
   }
-  // ---- colour grid scatter: theta_c[idx_k] += w_k f_bar
-  tc::mbar_wait(&s_bar[1], phase);
-  fence_after();
-  float fb[16];
-  ld16(tl, fb);
-  {
-    float wk[8];
-    corner_w(q, wk);
-    if (!(w.dbg & 1))
-      scatter_level<float, S::CC>(G.col, q, fb, wk, active, false, w.det_keys, w.det_vals,
-                                  s * (S::NL + 1) + S::NL);
-  }
-  if (w.pose_fb && active) {  // pose refinement: f_bar and the view-direction cotangent
-    float* o = w.pose_fb + s * 12;
-#pragma unroll
-    for (int c = 0; c < S::IN_C; ++c) o[c] = fb[c];
-  }
-  // ---- CTA reduction -> MLP partial slot (colour block)
+  // ---- CTA reduction of the running sums -> MLP partial slot (colour block, once per CTA)
   fence_before();
   __syncthreads();
   if (warp == 0)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kCols) : "memory");
   if (w.dbg & 4) return;
-  constexpr int NCP = S::NMLP - S::NG;
-  float* red = rows_all;
-  {
-    float* mine = red + (size_t)warp * NCP;
-    const int o = S::NG;
-    if (lane < S::oCW0 - S::NG) mine[lane] = 0.f;  // alignment padding
+  acc[S::oCb1 - o + lane] += sum_b1;
 #pragma unroll
-    for (int nt = 0; nt < 4; ++nt) frag_d_store(e0[0][nt], mine + (S::oCW0 - o), 0, nt * 8, S::IN_C + 1);
+  for (int c = 0; c < 3; ++c) acc[S::oCW2 - o + lane * 3 + c] += sum_w2[c];
+  if (lane == 0) {
 #pragma unroll
-    for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-      for (int nt = 0; nt < 4; ++nt) frag_d_store(e1[mt][nt], mine + (S::oCW1 - o), mt * 16, nt * 8, GSB_HID);
-    mine[S::oCb1 - o + lane] = acc_b1;
-#pragma unroll
-    for (int c = 0; c < 3; ++c) mine[S::oCW2 - o + lane * 3 + c] = acc_w2[c];
-    if (lane == 0) {
-#pragma unroll
-      for (int c = 0; c < 3; ++c) mine[S::oCb2 - o + c] = acc_b2[c];
-    }
+    for (int c = 0; c < 3; ++c) acc[S::oCb2 - o + c] += sum_b2[c];
   }
   __syncthreads();
   const int slot = w.mlp_slots > 0 ? (int)(blockIdx.x % (unsigned)w.mlp_slots) : (int)blockIdx.x;
@@ -1066,7 +1124,7 @@ __global__ void __launch_bounds__(kTile, 2) k_bwd_color_t5(Ws<float> w, Geo G, i
       a[e] = 0.f;
       if (i + e < S::NMLP) {
 #pragma unroll
-        for (int k = 0; k < 4; ++k) a[e] += red[(size_t)k * NCP + (i + e - S::NG)];
+        for (int k = 0; k < 4; ++k) a[e] += acc_all[(size_t)k * NCP + (i + e - o)];
       }
     }
     if (w.mlp_slots > 0)

@@ -1,7 +1,7 @@
 """The A/B kernel forms stay parity-green: the production step uses tcgen05
 for the coarse no-grad SDF, the taped forward and both backward kernels
 (gsb_step.cuh: GSB_T5=2, GSB_T5_FWD=4, GSB_T5_BWD=1, GSB_T5_COL=1).  The alternatives
-(mma.sync everywhere; tcgen05 everywhere with the 3-CTA forward) are read
+(mma.sync everywhere; tcgen05 everywhere, the importance-pass SDF included) are read
 once per process from the environment, so each runs the float step parity
 tests of test_gpu_step.py and the conditioned float32 parity of
 test_f32_parity.py in a child process against the same oracle goldens."""
@@ -16,7 +16,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 
 FORMS = {
     "mma_sync": {"GSB_T5": "0", "GSB_T5_FWD": "0", "GSB_T5_BWD": "0", "GSB_T5_COL": "0"},
-    "tcgen05_all": {"GSB_T5": "1", "GSB_T5_FWD": "3", "GSB_T5_BWD": "1", "GSB_T5_COL": "1"},
+    "tcgen05_all": {"GSB_T5": "1", "GSB_T5_FWD": "4", "GSB_T5_BWD": "1", "GSB_T5_COL": "1"},
 }
 
 
