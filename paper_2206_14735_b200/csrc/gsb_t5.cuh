@@ -485,8 +485,10 @@ __global__ void __launch_bounds__(kTile, kCtaPerSm) k_fwd_t5(Ws<float> w, Geo G,
 // columns: D0 [0,32), D1 [32,64), A1 hi/lo [64,128), A2 hi/lo [128,192);
 // 104 KB shared memory: 2 CTAs per SM (3 CTAs with 128 columns, 5 MMA rounds
 // and a 168-register cap measured slower: 432 vs 390 us).  Persistent: a CTA
-// loops over tiles and keeps its MLP-gradient sums (outer products in shared
-// memory, column sums in registers) across them, so the CTA reduction and
+// loops over tiles and keeps its MLP-gradient sums (outer-product fragments
+// in the lanes' spare TMEM columns, column sums in registers) across them
+// -- no extra shared memory, so L1 keeps its share for the gathers -- so
+// the CTA reduction and
 // the L2 reds into the partial rows happen once per CTA instead of once per
 // 128-sample tile (GSB_DBG attribution: that per-tile reduction was 47 of
 // 376 us).
@@ -497,26 +499,27 @@ struct GeoT5 {
   static constexpr int NW = tc::UmmaW::W0NL + 512;              // geometry tiles only
   static constexpr uint32_t kCols2 = 256;
   static constexpr int kCtaPerSm = 2;
-  // weights + vectors, the per-warp sample rows, and the per-warp MLP-gradient
-  // accumulators that persist across the CTA's tiles
+  static constexpr uint32_t kAcc = 192;  // TMEM columns [192, 240): the lane's dW0 / dW1 fragment sums
   template <class S>
-  static constexpr size_t smem() {
-    return (size_t)(NW + tc::GVec::N) * 4 + (size_t)kTile * ROW * 4 + (size_t)4 * ((S::NG + 3) / 4 * 4) * 4;
-  }
+  static constexpr size_t smem() { return (size_t)(NW + tc::GVec::N) * 4 + (size_t)kTile * ROW * 4; }
 };
 
-// d (an m16n8 fp32 D fragment) added into a row-major [rows][GSB_HID] block
-__device__ __forceinline__ void frag_d_add(const float (&d)[4], float* out, int m0, int n0, int mrows) {
-  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
-  const int r0 = m0 + g, r1 = m0 + g + 8, c = n0 + 2 * t;
-  if (r0 < mrows) {
-    out[r0 * GSB_HID + c] += d[0];
-    out[r0 * GSB_HID + c + 1] += d[1];
-  }
-  if (r1 < mrows) {
-    out[r1 * GSB_HID + c] += d[2];
-    out[r1 * GSB_HID + c + 1] += d[3];
-  }
+// running sums of a warp's mma.sync D fragments (tiles of m16n8) kept in the
+// lane's own TMEM row: 16 fragment values per call, columns [col, col + 16)
+__device__ __forceinline__ void tmem_acc16(uint32_t ta, float (&d)[4][4]) {
+  float cur[16];
+  ld16(ta, cur);
+#pragma unroll
+  for (int i = 0; i < 16; ++i) cur[i] += d[i >> 2][i & 3];
+  st16(ta, cur);
+}
+__device__ __forceinline__ void tmem_get16(uint32_t ta, float (&d)[4][4]) {
+  float cur[16];
+  ld16(ta, cur);
+#pragma unroll
+  for (int i = 0; i < 16; ++i) d[i >> 2][i & 3] = cur[i];
+}
+
 }
 
 // x (W columns) as tf32 hi / lo to TMEM columns chi / clo of this warp's lanes
@@ -578,7 +581,6 @@ __global__ void __launch_bounds__(kTile, 2) k_bwd_geom_t5(Ws<float> w, Geo G, in
   float* sw = t5_smem;
   const float* gvec = t5_smem + K::NW;
   float* rows_all = t5_smem + K::NW + tc::GVec::N;
-  float* acc_all = rows_all + (size_t)kTile * ROW;  // [4 warps][NGP], persists across tiles
   __shared__ __align__(8) uint64_t s_bar[2];
   __shared__ uint32_t s_tmem;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -592,8 +594,6 @@ __global__ void __launch_bounds__(kTile, 2) k_bwd_geom_t5(Ws<float> w, Geo G, in
     tc::mbar_init(&s_bar[0]);
     tc::mbar_init(&s_bar[1]);
   }
-  float* acc = acc_all + (size_t)warp * NGP;
-  for (int i = lane; i < NGP; i += 32) acc[i] = 0.f;
   fence_before();
   __syncthreads();
   fence_after();
@@ -605,6 +605,13 @@ __global__ void __launch_bounds__(kTile, 2) k_bwd_geom_t5(Ws<float> w, Geo G, in
   }
   const uint32_t tmem = s_tmem;
   const uint32_t tl = tmem + ((uint32_t)(warp * 32) << 16);
+  {  // zero the fragment sums (TMEM columns [kAcc, kAcc + 48) of this warp's lanes)
+    float zz[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) zz[i] = 0.f;
+#pragma unroll
+    for (int j = 0; j < 3; ++j) st16(tl + K::kAcc + 16 * j, zz);
+  }
   auto sa = [&](int off) { return smem_u32(sw + off); };
   float* rows = rows_all + warp * 32 * ROW;
   float* myrow = rows + lane * ROW;
@@ -781,13 +788,10 @@ __global__ void __launch_bounds__(kTile, 2) k_bwd_geom_t5(Ws<float> w, Geo G, in
         for (int mt = 0; mt < 2; ++mt) frag_a(rows, ROW, K::oA1, k0, mt * 16, ah[mt], al[mt]);
         tc::mma3_sweep(d1, ah, al, bh0, bh1, bl0, bl1);
       }
-      // this tile's products into the warp's running sums (lanes own disjoint entries)
-#pragma unroll
-      for (int nt = 0; nt < 4; ++nt) frag_d_add(d0[0][nt], acc + S::oGW0, 0, nt * 8, S::IN_G);
-#pragma unroll
-      for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-        for (int nt = 0; nt < 4; ++nt) frag_d_add(d1[mt][nt], acc + S::oGW1, mt * 16, nt * 8, GSB_HID);
+      // this tile's products into the lane's running sums in TMEM
+      tmem_acc16(tl + K::kAcc, d0[0]);
+      tmem_acc16(tl + K::kAcc + 16, d1[0]);
+      tmem_acc16(tl + K::kAcc + 32, d1[1]);
     }
     float accp = p;
 #pragma unroll
@@ -812,15 +816,30 @@ __global__ void __launch_bounds__(kTile, 2) k_bwd_geom_t5(Ws<float> w, Geo G, in
     }
   }
   // ---- CTA reduction of the running sums -> MLP partial slot (once per CTA)
+  float d0[1][4][4], d1[2][4][4];
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  tmem_get16(tl + K::kAcc, d0[0]);
+  tmem_get16(tl + K::kAcc + 16, d1[0]);
+  tmem_get16(tl + K::kAcc + 32, d1[1]);
   fence_before();
   __syncthreads();
   if (warp == 0)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(K::kCols2) : "memory");
   if (w.dbg & 4) return;
-  acc[S::oGb0 + lane] += sum_b0;
-  acc[S::oGb1 + lane] += sum_b1;
-  acc[S::oGW2 + lane] += sum_w2;
-  if (lane == 0) acc[S::oGb2] += sum_p;
+  float* acc_all = rows_all;  // [4 warps][NGP] over the (now idle) sample rows
+  {
+    float* acc = acc_all + (size_t)warp * NGP;
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) frag_d_store(d0[0][nt], acc + S::oGW0, 0, nt * 8, S::IN_G);
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) frag_d_store(d1[mt][nt], acc + S::oGW1, mt * 16, nt * 8, GSB_HID);
+    acc[S::oGb0 + lane] = sum_b0;
+    acc[S::oGb1 + lane] = sum_b1;
+    acc[S::oGW2 + lane] = sum_w2;
+    if (lane == 0) acc[S::oGb2] = sum_p;
+  }
   __syncthreads();
   const int slot = w.mlp_slots > 0 ? (int)(blockIdx.x % (unsigned)w.mlp_slots) : (int)blockIdx.x;
   float* out = w.mlp_part + (size_t)slot * S::NMLPP;
@@ -851,12 +870,10 @@ struct ColT5 {
   static constexpr int oA0 = 0, oB0 = 16, oA1 = 48, oY = 80, oM = 88;
   static constexpr int W0 = tc::UmmaW::C0H, NW = tc::UmmaW::N - tc::UmmaW::C0H;  // colour tiles
   static constexpr int kCtaPerSm = 2;
-  // weights + vectors, the per-warp sample rows, and the per-warp colour
-  // MLP-gradient sums that persist across the CTA's tiles
+  static constexpr uint32_t kCols = 256;  // D [0,32), A hi/lo [32,96), fragment sums [96, 144)
+  static constexpr uint32_t kAcc = 96;
   template <class S>
-  static constexpr size_t smem() {
-    return (size_t)(NW + tc::CVec::N) * 4 + (size_t)kTile * ROW * 4 + (size_t)4 * (S::NMLP - S::NG) * 4;
-  }
+  static constexpr size_t smem() { return (size_t)(NW + tc::CVec::N) * 4 + (size_t)kTile * ROW * 4; }
 };
 
 template <class S>
@@ -873,13 +890,12 @@ __global__ void __launch_bounds__(kTile, 2) k_bwd_color_t5(Ws<float> w, Geo G, i
   float* sw = t5_smem - K::W0;  // indexed by UmmaW offsets
   const float* cvec = t5_smem + K::NW;
   float* rows_all = t5_smem + K::NW + tc::CVec::N;
-  float* acc_all = rows_all + (size_t)kTile * ROW;  // [4 warps][NCP], persists across tiles
   __shared__ __align__(8) uint64_t s_bar[2];
   __shared__ uint32_t s_tmem;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&s_tmem)),
-                 "r"(kCols)
+                 "r"(K::kCols)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
@@ -887,8 +903,6 @@ __global__ void __launch_bounds__(kTile, 2) k_bwd_color_t5(Ws<float> w, Geo G, i
     tc::mbar_init(&s_bar[0]);
     tc::mbar_init(&s_bar[1]);
   }
-  float* acc = acc_all + (size_t)warp * NCP;
-  for (int i = lane; i < NCP; i += 32) acc[i] = 0.f;
   fence_before();
   __syncthreads();
   fence_after();
@@ -901,6 +915,13 @@ __global__ void __launch_bounds__(kTile, 2) k_bwd_color_t5(Ws<float> w, Geo G, i
   }
   const uint32_t tmem = s_tmem;
   const uint32_t tl = tmem + ((uint32_t)(warp * 32) << 16);
+  {  // zero the fragment sums (TMEM columns [kAcc, kAcc + 48) of this warp's lanes)
+    float zz[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) zz[i] = 0.f;
+#pragma unroll
+    for (int j = 0; j < 3; ++j) st16(tl + K::kAcc + 16 * j, zz);
+  }
   auto sa = [&](int off) { return smem_u32(sw + off); };
   float* rows = rows_all + warp * 32 * ROW;
   float* myrow = rows + lane * ROW;
@@ -1072,13 +1093,10 @@ __global__ void __launch_bounds__(kTile, 2) k_bwd_color_t5(Ws<float> w, Geo G, i
           tc::mma3_sweep(e1, ah, al, bh0, bh1, bl0, bl1);
         }
       }
-      // this tile's products into the warp's running sums (lanes own disjoint entries)
-#pragma unroll
-      for (int nt = 0; nt < 4; ++nt) frag_d_add(e0[0][nt], acc + (S::oCW0 - o), 0, nt * 8, S::IN_C + 1);
-#pragma unroll
-      for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-        for (int nt = 0; nt < 4; ++nt) frag_d_add(e1[mt][nt], acc + (S::oCW1 - o), mt * 16, nt * 8, GSB_HID);
+      // this tile's products into the lane's running sums in TMEM
+      tmem_acc16(tl + K::kAcc, e0[0]);
+      tmem_acc16(tl + K::kAcc + 16, e1[0]);
+      tmem_acc16(tl + K::kAcc + 32, e1[1]);
     }
     // ---- colour grid scatter: theta_c[idx_k] += w_k f_bar
     tc::mbar_wait(&s_bar[1], phase);
@@ -1100,17 +1118,33 @@ __global__ void __launch_bounds__(kTile, 2) k_bwd_color_t5(Ws<float> w, Geo G, i
     }
   }
   // ---- CTA reduction of the running sums -> MLP partial slot (colour block, once per CTA)
+  float e0[1][4][4], e1[2][4][4];
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  tmem_get16(tl + K::kAcc, e0[0]);
+  tmem_get16(tl + K::kAcc + 16, e1[0]);
+  tmem_get16(tl + K::kAcc + 32, e1[1]);
   fence_before();
   __syncthreads();
   if (warp == 0)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kCols) : "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(K::kCols) : "memory");
   if (w.dbg & 4) return;
-  acc[S::oCb1 - o + lane] += sum_b1;
+  float* acc_all = rows_all;  // [4 warps][NCP] over the (now idle) sample rows
+  {
+    float* acc = acc_all + (size_t)warp * NCP;
+    if (lane < S::oCW0 - S::NG) acc[lane] = 0.f;  // alignment padding
 #pragma unroll
-  for (int c = 0; c < 3; ++c) acc[S::oCW2 - o + lane * 3 + c] += sum_w2[c];
-  if (lane == 0) {
+    for (int nt = 0; nt < 4; ++nt) frag_d_store(e0[0][nt], acc + (S::oCW0 - o), 0, nt * 8, S::IN_C + 1);
 #pragma unroll
-    for (int c = 0; c < 3; ++c) acc[S::oCb2 - o + c] += sum_b2[c];
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) frag_d_store(e1[mt][nt], acc + (S::oCW1 - o), mt * 16, nt * 8, GSB_HID);
+    acc[S::oCb1 - o + lane] = sum_b1;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) acc[S::oCW2 - o + lane * 3 + c] = sum_w2[c];
+    if (lane == 0) {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) acc[S::oCb2 - o + c] = sum_b2[c];
+    }
   }
   __syncthreads();
   const int slot = w.mlp_slots > 0 ? (int)(blockIdx.x % (unsigned)w.mlp_slots) : (int)blockIdx.x;
