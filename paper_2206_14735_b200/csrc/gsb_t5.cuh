@@ -520,8 +520,6 @@ __device__ __forceinline__ void tmem_get16(uint32_t ta, float (&d)[4][4]) {
   for (int i = 0; i < 16; ++i) d[i >> 2][i & 3] = cur[i];
 }
 
-}
-
 // x (W columns) as tf32 hi / lo to TMEM columns chi / clo of this warp's lanes
 template <int W>
 __device__ __forceinline__ void store_hl(uint32_t tl, uint32_t chi, uint32_t clo, const float* x) {
