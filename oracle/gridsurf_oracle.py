@@ -606,6 +606,7 @@ class GeomPass:
         (a0, a1, a2), (h0, h1), out = mlp_forward(P.geom, self.z)
         self.phi = out[:, 0]
         self.h0, self.h1 = h0, h1
+        self.pre = (a0, a1)  # ReLU pre-activations (conditioned-parity kink margins)
         self.m0 = (a0 > 0).astype(dt)
         self.m1 = (a1 > 0).astype(dt)
         W0, W1, W2 = (P.geom[i][0] for i in range(3))
@@ -828,6 +829,7 @@ def train_objective(P, dataset, batch, iteration, cfg, smooth_override=None,
                    "empty_tr": bool(tr_cnt.sum() == 0), "empty_fs": bool(fs_cnt.sum() == 0)}
     R.update(phi=phis, gphi=gp.reshape(m, n, 3), colors=colors, alpha=al, weights=w,
              chat=chat, dhat=dhat, xf=xf)
+    R["pre"] = {"geom": G.pre, "color": (ca0, ca1), "smooth": None if S is None else S.pre}
     if not want_grads:
         return R
 

@@ -85,7 +85,36 @@ def oracle_from_model(model, poses, dtype):
     return P
 
 
-def run_case(case, iteration=3):
+# ReLU kinks: where a pre-activation is within float32 rounding of zero the
+# float32 step and the float64 oracle may take different sides, and the
+# derivative (dphi/dz, so grad-phi, and every gradient behind it) jumps while
+# the values stay continuous.  That is the measure-zero set on which the
+# derivative is not defined, not a kernel error, so the comparison is made at
+# a generic point: any layer bias whose unit has a sample within
+# KINK_MARGIN x (the layer's max |pre-activation|; the float32 error there
+# measured ~1e-7) of zero is moved by
+# 4 x that margin (both sides use the moved parameters) and the step re-run.
+KINK_MARGIN = 1e-6
+KINK_BIASES = {("geom", 0): "geom_b0", ("geom", 1): "geom_b1", ("smooth", 0): "geom_b0",
+               ("smooth", 1): "geom_b1", ("color", 0): "color_b0", ("color", 1): "color_b1"}
+
+
+def kink_nudges(R):
+    """{bias name: {unit: shift}} for the units with a near-zero pre-activation."""
+    out = {}
+    for net, pre in R["pre"].items():
+        if pre is None:
+            continue
+        for layer, a in enumerate(pre):
+            a = np.asarray(a, dtype=np.float64)
+            scale = float(np.abs(a).max())
+            units = np.unique(np.nonzero(np.abs(a) < KINK_MARGIN * scale)[1])
+            for u in units:
+                out.setdefault(KINK_BIASES[(net, layer)], {})[int(u)] = 4 * KINK_MARGIN * scale
+    return out
+
+
+def run_case(case, iteration=3, max_nudges=6):
     from paper_2206_14735_b200 import optimizer, renderer, sampler, seeds
     ds, kw = _dataset(case)
     smooth_count = kw.pop("smooth_count", None)
@@ -100,33 +129,47 @@ def run_case(case, iteration=3):
                   importance_rounds=cfg.importance_rounds, importance_add=cfg.importance_add,
                   near=cfg.near, max_depth=cfg.max_depth)
     ocfg.weights.smooth_count = cfg.weights.smooth_count
-    P32 = oracle_from_model(model, ds.poses, np.float32)
-    P64 = oracle_from_model(model, ds.poses, np.float64)
-    # smoothness points drawn as the step draws them, float32-representable
-    rng = O.substream(cfg.seed, O.SMOOTH, iteration)
-    xs, xe = O.draw_smooth_points(P32, ods, cfg.weights.smooth_count, cfg.weights.truncation,
-                                  cfg.weights.smooth_delta, rng)
-    sm = (xs.astype(np.float32).astype(np.float64), xe.astype(np.float32).astype(np.float64))
+    params = dict(zip(model.param_names(), model.parameters()))
+    nudged = 0
+    for attempt in range(max_nudges + 1):
+        P32 = oracle_from_model(model, ds.poses, np.float32)
+        P64 = oracle_from_model(model, ds.poses, np.float64)
+        # smoothness points drawn as the step draws them, float32-representable
+        rng = O.substream(cfg.seed, O.SMOOTH, iteration)
+        xs, xe = O.draw_smooth_points(P32, ods, cfg.weights.smooth_count, cfg.weights.truncation,
+                                      cfg.weights.smooth_delta, rng)
+        sm = (xs.astype(np.float32).astype(np.float64), xe.astype(np.float32).astype(np.float64))
 
-    batch = sampler.draw_ray_batch(ds, seeds.substream(cfg.seed, seeds.RAYS, iteration),
-                                   cfg.batch_rays, near=cfg.near, far=cfg.max_depth)
-    total, parts, extras = renderer.train_objective(model, ds, batch, iteration, cfg,
-                                                    smooth_override=sm)
-    grads = renderer.grad(total, model.parameters())
-    g = {n: t.cpu().numpy().copy() for n, t in zip(model.param_names(), grads)}
-    eng = renderer.engine_for(model, ds)
-    M, N = cfg.batch_rays, extras["samples_per_ray"]
-    ws = eng.workspace(M, cfg.coarse_samples, cfg.importance_rounds, cfg.importance_add,
-                       cfg.weights.smooth_count)
-    dev = {k: ws[k].cpu().numpy().astype(np.float64) for k in ("phi", "gphi", "color", "ray_o",
-                                                                 "ray_r")}
-    depths = extras["depths"]
+        batch = sampler.draw_ray_batch(ds, seeds.substream(cfg.seed, seeds.RAYS, iteration),
+                                       cfg.batch_rays, near=cfg.near, far=cfg.max_depth)
+        total, parts, extras = renderer.train_objective(model, ds, batch, iteration, cfg,
+                                                        smooth_override=sm)
+        grads = renderer.grad(total, model.parameters())
+        g = {n: t.cpu().numpy().copy() for n, t in zip(model.param_names(), grads)}
+        eng = renderer.engine_for(model, ds)
+        M, N = cfg.batch_rays, extras["samples_per_ray"]
+        ws = eng.workspace(M, cfg.coarse_samples, cfg.importance_rounds, cfg.importance_add,
+                           cfg.weights.smooth_count)
+        dev = {k: ws[k].cpu().numpy().astype(np.float64) for k in ("phi", "gphi", "color", "ray_o",
+                                                                     "ray_r")}
+        depths = extras["depths"]
 
-    ob = O.draw_ray_batch(ods, O.substream(cfg.seed, O.RAYS, iteration), cfg.batch_rays)
-    R = O.train_objective(P64, ods, ob, iteration, ocfg, smooth_override=sm,
-                          inject_depths=depths, inject_rays=(dev["ray_o"], dev["ray_r"]),
-                          point_dtype=np.float32)
-    return dict(model=model, parts=parts, extras=extras, g=g, dev=dev, R=R, M=M, N=N)
+        ob = O.draw_ray_batch(ods, O.substream(cfg.seed, O.RAYS, iteration), cfg.batch_rays)
+        R = O.train_objective(P64, ods, ob, iteration, ocfg, smooth_override=sm,
+                              inject_depths=depths, inject_rays=(dev["ray_o"], dev["ray_r"]),
+                              point_dtype=np.float32)
+        shifts = kink_nudges(R)
+        if not shifts:
+            break
+        assert attempt < max_nudges, f"ReLU kinks persist after {max_nudges} bias nudges: {shifts}"
+        for name, units in shifts.items():
+            b = params[name].numpy()
+            for u, d in units.items():
+                b[u] += d
+            params[name].set(b)
+            nudged += len(units)
+    return dict(model=model, parts=parts, extras=extras, g=g, dev=dev, R=R, M=M, N=N,
+                nudged=nudged)
 
 
 CASES = ["small", "c1", "c2"]
@@ -147,7 +190,7 @@ def test_per_sample_outputs(conditioned):
         "gphi": rel_maxnorm(dev["gphi"][:M * N], R["gphi"].reshape(-1, 3)),
         "color": rel_maxnorm(dev["color"], R["colors"].reshape(-1, 3)),
     }
-    print(case, "per-sample", errs)
+    print(case, "per-sample", errs, "kink nudges", r["nudged"])
     assert max(errs.values()) <= SAMPLE_TOL, errs
 
 
