@@ -110,6 +110,7 @@ Ws<T> carve(void* ws, const Sizes& z, size_t* bytes, int64_t* off_parts = nullpt
   w.fin_cnt = c.template take<unsigned>((z.nmlp + 31) / 32);
   w.loss_red = c.template take<double>((int64_t)((std::max(z.M, z.S) + 255) / 256 + 1) * 8);
   w.loss_cnt = c.template take<unsigned>(4);
+  w.imp_state = c.template take<uint64_t>((int64_t)GSB_MAX_ROUNDS * z.M * 2);
   if (bytes) *bytes = c.off;
   if (off_parts) *off_parts = (int64_t)o_parts;
   if (off_counts) *off_counts = (int64_t)o_counts;

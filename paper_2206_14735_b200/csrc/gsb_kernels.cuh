@@ -70,6 +70,14 @@ struct Ws {
   long long* counts;
   double* parts;
   int32_t* status;
+  uint64_t* imp_state;  // [GSB_MAX_ROUNDS][M][2]: importance-round PCG64 state at row (ray_base + ray) * A
+};
+
+// the importance rounds' generators (one substream per round) and A, for
+// k_ray_setup's per-row jump-ahead
+struct PcgRounds {
+  gsb_pcg64_t r[GSB_MAX_ROUNDS];
+  int n, A;
 };
 
 struct Geo {
@@ -209,11 +217,13 @@ constexpr int kRaySetupRays = 16;
 template <typename T>
 __global__ void __launch_bounds__(128) k_ray_setup(gsb_dataset_t D, const int64_t* __restrict__ ids, int M,
                                                    int ray_base, Ws<T> w, Geo G, int Nc, double nearv,
-                                                   double max_depth, int has_ff, double ff, gsb_pcg64_t rng) {
+                                                   double max_depth, int has_ff, double ff, gsb_pcg64_t rng,
+                                                   PcgRounds imp) {
   // RPB rays per block: threads 0..RPB-1 set the rays up, then all 128
   // threads fill the stratified depths, TPR threads per ray (each jumps its
   // own PCG stream to its first sample)
   constexpr int RPB = kRaySetupRays, TPR = 128 / RPB;  // rays per block, threads per ray
+  static_assert(TPR >= GSB_MAX_ROUNDS, "one thread per importance round");
   __shared__ double s_near[RPB], s_span[RPB];
   const int t = threadIdx.x;
   const int i = blockIdx.x * RPB + t;
@@ -265,6 +275,14 @@ __global__ void __launch_bounds__(128) k_ray_setup(gsb_dataset_t D, const int64_
   // stratified_coarse (gs/sampler.py:91-107) with uniform row (ray_base + ray)
   const int rl = t / TPR, q = t % TPR, ray = blockIdx.x * RPB + rl;
   if (ray >= M) return;
+  if (q < imp.n && w.imp_state) {  // importance round q: this row's first-uniform state
+    Pcg g;
+    g.init(imp.r[q]);
+    g.advance((uint64_t)(ray_base + ray) * (uint64_t)imp.A);
+    uint64_t* o = w.imp_state + ((int64_t)q * M + ray) * 2;
+    o[0] = (uint64_t)(g.state >> 64);
+    o[1] = (uint64_t)g.state;
+  }
   const int chunk = (Nc + TPR - 1) / TPR, j0 = q * chunk, j1 = min(Nc, j0 + chunk);
   if (j0 >= j1) return;
   Pcg g;
@@ -447,7 +465,7 @@ __global__ void k_smooth_points(gsb_dataset_t D, const double* __restrict__ pose
 // CDF normalisation, inverse-CDF draws, the stable merge (by rank), the
 // separation test and provenance.
 
-struct ImpSmem {
+struct __align__(16) ImpSmem {
   double om[GSB_KMAX];
   double cdf[GSB_KMAX];
   double out[GSB_KMAX];
@@ -457,11 +475,13 @@ struct ImpSmem {
 
 // d, ph: (K) input row; win: optional given weights (K); uni: optional
 // uniforms (A) else PCG64 advanced to row*A; writes out/src (K+A) in smem.
+// WOUT: also write the rendering weights to wout (the twin's output).
+template <bool WOUT>
 static __device__ void importance_warp(ImpSmem& S, int K, int A, const double* __restrict__ d,
                                 const double* __restrict__ ph, const double* __restrict__ win,
                                 double s, double nearv, double farv, const gsb_pcg64_t& rng,
                                 uint64_t row, const double* __restrict__ uni,
-                                double* __restrict__ wout) {
+                                double* __restrict__ wout, const uint64_t* __restrict__ row_state = nullptr) {
   const int lane = threadIdx.x & 31;
   const unsigned full = 0xffffffffu;
   double total;
@@ -485,15 +505,35 @@ static __device__ void importance_warp(ImpSmem& S, int K, int A, const double* _
     }
     __syncwarp();
     if (lane == 0) {  // sequential cumprod / cumsum, as numpy
+      // four steps per trip: the om loads (16-byte) are issued ahead of the
+      // two dependent float64 chains (trans *= om, c += w)
       double trans = 1.0, c = 0.0;
-      for (int i = 0; i < K - 1; ++i) {
-        const double wi = trans * (1.0 - S.om[i]);
-        if (wout) wout[i] = wi;
+      int i = 0;
+      for (; i + 4 <= K - 1; i += 4) {
+        const double2 o01 = *reinterpret_cast<const double2*>(S.om + i);
+        const double2 o23 = *reinterpret_cast<const double2*>(S.om + i + 2);
+        const double om4[4] = {o01.x, o01.y, o23.x, o23.y};
+        double c4[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const double wi = trans * (1.0 - om4[q]);
+          if constexpr (WOUT) wout[i + q] = wi;
+          c = (i + q == 0) ? wi : c + wi;
+          c4[q] = c;
+          trans = trans * om4[q];
+        }
+        *reinterpret_cast<double2*>(S.cdf + i) = make_double2(c4[0], c4[1]);
+        *reinterpret_cast<double2*>(S.cdf + i + 2) = make_double2(c4[2], c4[3]);
+      }
+      for (; i < K - 1; ++i) {
+        const double om = S.om[i];
+        const double wi = trans * (1.0 - om);
+        if constexpr (WOUT) wout[i] = wi;
         c = (i == 0) ? wi : c + wi;
         S.cdf[i] = c;
-        trans = trans * S.om[i];
+        trans = trans * om;
       }
-      if (wout) wout[K - 1] = trans * (1.0 - 1.0);
+      if constexpr (WOUT) wout[K - 1] = trans * (1.0 - 1.0);
       total = c;
     }
   }
@@ -515,7 +555,12 @@ static __device__ void importance_warp(ImpSmem& S, int K, int A, const double* _
     } else {
       Pcg g;
       g.init(rng);
-      g.advance(row * (uint64_t)A + (uint64_t)lane);
+      if (row_state) {  // state at row * A precomputed (k_ray_setup): a short jump
+        g.state = ((u128)row_state[0] << 64) | (u128)row_state[1];
+        g.advance((uint64_t)lane);
+      } else {
+        g.advance(row * (uint64_t)A + (uint64_t)lane);
+      }
       u = g.next_double();
     }
     int lo = 0, hi = K - 1;  // idx = #(cdf <= u): upper bound on a non-decreasing array
@@ -595,7 +640,8 @@ __global__ void __launch_bounds__(128) k_importance_dev(Ws<T> w, int M, int K, i
                                                         const T* __restrict__ log_s,
                                                         gsb_pcg64_t rng, int32_t* __restrict__ evl,
                                                         int32_t* __restrict__ evl_count, int64_t cap,
-                                                        int want_list, int count_final, double trunc) {
+                                                        int want_list, int count_final, double trunc,
+                                                        const uint64_t* __restrict__ row_states) {
   __shared__ ImpSmem smem[4];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int i = blockIdx.x * 4 + wid;
@@ -605,8 +651,9 @@ __global__ void __launch_bounds__(128) k_importance_dev(Ws<T> w, int M, int K, i
   const double s = (double)exp(log_s[0]);
   const double* d = dep + (int64_t)i * w.ld;
   const double* ph = phi + (int64_t)i * w.ld;
-  importance_warp(S, K, A, d, ph, nullptr, s, w.nearv[i], w.farv[i], rng,
-                  (uint64_t)(ray_base + i), nullptr, nullptr);
+  importance_warp<false>(S, K, A, d, ph, nullptr, s, w.nearv[i], w.farv[i], rng,
+                         (uint64_t)(ray_base + i), nullptr, nullptr,
+                         row_states ? row_states + (int64_t)i * 2 : nullptr);
   const int n = K + A;
   double* out = dep_out + (int64_t)i * w.ld;
   double* po = phi_out + (int64_t)i * w.ld;
@@ -675,9 +722,14 @@ static __global__ void __launch_bounds__(128) k_importance_twin(int M, int K, in
   const int i = blockIdx.x * 4 + wid;
   if (i >= M) return;
   ImpSmem& S = smem[wid];
-  importance_warp(S, K, A, dep + (int64_t)i * ld, phi ? phi + (int64_t)i * ld : nullptr,
-                  win ? win + (int64_t)i * ld : nullptr, s, nearv[i], farv[i], rng, (uint64_t)i,
-                  use_rng ? nullptr : uni + (int64_t)i * A, wts ? wts + (int64_t)i * ld : nullptr);
+  const double* d = dep + (int64_t)i * ld;
+  const double* ph = phi ? phi + (int64_t)i * ld : nullptr;
+  const double* wi = win ? win + (int64_t)i * ld : nullptr;
+  const double* ui = use_rng ? nullptr : uni + (int64_t)i * A;
+  if (wts)
+    importance_warp<true>(S, K, A, d, ph, wi, s, nearv[i], farv[i], rng, (uint64_t)i, ui, wts + (int64_t)i * ld);
+  else
+    importance_warp<false>(S, K, A, d, ph, wi, s, nearv[i], farv[i], rng, (uint64_t)i, ui, nullptr);
   for (int t = lane; t < K + A; t += 32) {
     out[(int64_t)i * ld + t] = S.out[t];
     src[(int64_t)i * ld + t] = S.src[t];

@@ -166,9 +166,13 @@ int run_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step
   const T* log_s = params + model->log_s_offset;
   if (st->phases & 1) {
     GSB_CHECK(cudaMemsetAsync(w.counts, 0, 8 * sizeof(long long), stream));
+    PcgRounds imp{};
+    imp.n = R;
+    imp.A = A;
+    for (int r = 0; r < R; ++r) imp.r[r] = st->rng_importance[r];
     k_ray_setup<T><<<(M + kRaySetupRays - 1) / kRaySetupRays, 128, 0, stream>>>(
         *data, st->ray_ids, M, st->ray_base, w, G, Nc, st->near, st->max_depth,
-        st->has_fixed_far, st->fixed_far, st->rng_stratify);
+        st->has_fixed_far, st->fixed_far, st->rng_stratify, imp);
     GSB_LAUNCHED_T("k_ray_setup");
     if (R > 0) {
       int64_t n0 = (int64_t)M * Nc;
@@ -194,7 +198,7 @@ int run_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step
         k_importance_dev<T><<<(M + 3) / 4, 128, 0, stream>>>(
             w, M, K, A, st->ray_base, w.dep[cur], w.phi[cur], w.dep[1 - cur], w.phi[1 - cur],
             log_s, st->rng_importance[rnd], w.evl, w.evl_count, w.evl_cap, need_phi ? 1 : 0,
-            rnd == R - 1 ? 1 : 0, st->truncation);
+            rnd == R - 1 ? 1 : 0, st->truncation, w.imp_state + (int64_t)rnd * M * 2);
         GSB_LAUNCHED_T("k_importance_dev");
         if (need_phi) {
           int64_t cap = (int64_t)M * A;
