@@ -599,7 +599,10 @@ class GeomPass:
     (ReLU masks a > 0, gs/diffcore.py:483-492) and each level adds
     J_l^T g_l (gs/diffcore.py:946-991)."""
 
-    def __init__(self, P, pts):
+    def __init__(self, P, pts, flips=()):
+        """``flips``: (layer, row, unit) whose ReLU derivative mask is taken on
+        the other side of the kink (test-only: a pre-activation within
+        rounding of zero, where a float32 run may have gone the other way)."""
         dt = P.dtype
         self.P = P
         self.ls, self.z = sample_multi(P, pts)
@@ -609,6 +612,9 @@ class GeomPass:
         self.pre = (a0, a1)  # ReLU pre-activations (conditioned-parity kink margins)
         self.m0 = (a0 > 0).astype(dt)
         self.m1 = (a1 > 0).astype(dt)
+        for layer, row, unit in flips:
+            m = self.m0 if layer == 0 else self.m1
+            m[row, unit] = 1 - m[row, unit]
         W0, W1, W2 = (P.geom[i][0] for i in range(3))
         ones = np.ones((self.z.shape[0], 1), dtype=dt)
         self.d1 = np.matmul(ones, W2.T) * self.m1
@@ -652,7 +658,7 @@ class GeomPass:
 
 def train_objective(P, dataset, batch, iteration, cfg, smooth_override=None,
                     want_grads=True, inject_depths=None, shard=None, inject_rays=None,
-                    point_dtype=None):
+                    point_dtype=None, relu_flips=None):
     """One evaluation of the training objective and (optionally) all
     parameter gradients.  Returns a dict of every intermediate.
 
@@ -664,6 +670,9 @@ def train_objective(P, dataset, batch, iteration, cfg, smooth_override=None,
     (gs/renderer.py:348-351 forms them in the model dtype).  Together they
     give the float64 evaluation of the taped pass at exactly the float32
     points a float32 implementation used (conditioned kernel parity).
+    ``relu_flips`` = {"geom" | "smooth" | "color": [(layer, row, unit)]}
+    takes those ReLU derivative masks on the other side of their kink
+    (GeomPass); test-only.
 
     ``shard`` (data-parallel restatement; not in the
     reference): dict with ``row_base`` and ``m_global`` (this batch is rows
@@ -735,7 +744,8 @@ def train_objective(P, dataset, batch, iteration, cfg, smooth_override=None,
     xu = x.reshape(m * n, 3)
     xf = np.minimum(np.maximum(xu, lo_c.astype(pdt)), hi_c.astype(pdt)).astype(dt)
     xu = xu.astype(dt)
-    G = GeomPass(P, xf)
+    flips = relu_flips or {}
+    G = GeomPass(P, xf, flips.get("geom", ()))
     cs = LevelSample(P.color, xf)
     fc = cs.value()
     vdir = np.broadcast_to(r.reshape(m, 1, 3), (m, n, 3)).reshape(m * n, 3)
@@ -813,7 +823,7 @@ def train_objective(P, dataset, batch, iteration, cfg, smooth_override=None,
         xs, xe = smooth_pts
         n_smooth = xs.shape[0]
         n_sm_norm = int(sh.get("n_smooth", n_smooth))
-        S = GeomPass(P, np.concatenate([xs, xe], axis=0).astype(dt))
+        S = GeomPass(P, np.concatenate([xs, xe], axis=0).astype(dt), flips.get("smooth", ()))
         dS = S.gphi[:n_smooth] - S.gphi[n_smooth:]
         l_smooth = (dS * dS).sum() / dt.type(n_sm_norm)
     R["smooth_pts"] = smooth_pts
@@ -830,6 +840,7 @@ def train_objective(P, dataset, batch, iteration, cfg, smooth_override=None,
     R.update(phi=phis, gphi=gp.reshape(m, n, 3), colors=colors, alpha=al, weights=w,
              chat=chat, dhat=dhat, xf=xf)
     R["pre"] = {"geom": G.pre, "color": (ca0, ca1), "smooth": None if S is None else S.pre}
+    R["smooth_gphi"] = None if S is None else S.gphi
     if not want_grads:
         return R
 
@@ -877,10 +888,14 @@ def train_objective(P, dataset, batch, iteration, cfg, smooth_override=None,
     cW = [P.color_net[i][0] for i in range(3)]
     grads["color_w2"] += np.matmul(ch1.T, y_bar)
     grads["color_b2"] += y_bar.sum(axis=0)
-    a1b = np.matmul(y_bar, cW[2].T) * (ca1 > 0)
+    cm0, cm1 = (ca0 > 0).astype(dt), (ca1 > 0).astype(dt)
+    for layer, row, unit in flips.get("color", ()):
+        cm = cm0 if layer == 0 else cm1
+        cm[row, unit] = 1 - cm[row, unit]
+    a1b = np.matmul(y_bar, cW[2].T) * cm1
     grads["color_w1"] += np.matmul(ch0.T, a1b)
     grads["color_b1"] += a1b.sum(axis=0)
-    a0b = np.matmul(a1b, cW[1].T) * (ca0 > 0)
+    a0b = np.matmul(a1b, cW[1].T) * cm0
     grads["color_w0"] += np.matmul(cin.T, a0b)
     grads["color_b0"] += a0b.sum(axis=0)
     in_bar = np.matmul(a0b, cW[0].T)

@@ -186,6 +186,16 @@ __device__ __forceinline__ void red_row(T* p, const T (&v)[C]) {
   if constexpr (sizeof(T) == 4 && C % 4 == 0) {
 #pragma unroll
     for (int c = 0; c < C; c += 4) red_add_v4(p + c, v[c], v[c + 1], v[c + 2], v[c + 3]);
+  } else if constexpr (sizeof(T) == 4 && C == 6) {
+    // 24-byte rows: a 16-byte and an 8-byte red, in the order the row's
+    // alignment allows (2 reds instead of 3)
+    if ((reinterpret_cast<uintptr_t>(p) & 15) == 0) {
+      red_add_v4(p, v[0], v[1], v[2], v[3]);
+      red_add_v2(p + 4, v[4], v[5]);
+    } else {
+      red_add_v2(p, v[0], v[1]);
+      red_add_v4(p + 2, v[2], v[3], v[4], v[5]);
+    }
   } else if constexpr (sizeof(T) == 4 && C % 2 == 0) {
 #pragma unroll
     for (int c = 0; c < C; c += 2) red_add_v2(p + c, v[c], v[c + 1]);
