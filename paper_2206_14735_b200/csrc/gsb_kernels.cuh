@@ -57,7 +57,7 @@ struct Ws {
   int mlp_slots;        // float32 taped backward: >0 = CTAs red.add into slot blockIdx % mlp_slots
   int sweep;            // tcgen05 taped kernels: bit 0 fwd, 1 geometry bwd, 2 colour bwd sweep the tiles backward
   int dbg;              // GSB_DBG time-attribution knobs (results invalid when set): 1 no scatter,
-                        // 2 no outer products, 4 no CTA reduction, 8 no feature loads
+                        // 2 no outer products, 4 no CTA reduction, 8 no feature loads, 16 no MMAs
   uint64_t* det_keys;   // deterministic scatter mode: [NS][NL+1][8] grad-row addresses, or null
   T* det_vals;          // ... and their [8] values (C used); reduced in sample order (k_det_reduce)
   T* pose_g;            // pose refinement, float32: [MN][IN_G] dphi/dz (k_fwd_tc), or null
@@ -1945,6 +1945,16 @@ __global__ void __launch_bounds__(256) k_adam(T* __restrict__ P, T* __restrict__
       if (lr[u] < 0.0) {
         __stcs(reinterpret_cast<Vec*>(Gr) + i, Vec{});
         continue;
+      }
+      {
+        // g = m = v = +0 everywhere in the vector (a parameter no step has
+        // touched yet): the update computes m = v = +0, p unchanged, g = +0
+        // -- exactly the stored bits -- so nothing is written back
+        const uint4 gb = *reinterpret_cast<const uint4*>(&g[u]);
+        const uint4 mb = *reinterpret_cast<const uint4*>(&m[u]);
+        const uint4 vb = *reinterpret_cast<const uint4*>(&v[u]);
+        if (((gb.x | gb.y | gb.z | gb.w) | (mb.x | mb.y | mb.z | mb.w) | (vb.x | vb.y | vb.z | vb.w)) == 0u)
+          continue;
       }
       T* pp = reinterpret_cast<T*>(&p[u]);
       T* gg = reinterpret_cast<T*>(&g[u]);

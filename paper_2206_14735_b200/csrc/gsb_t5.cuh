@@ -338,7 +338,7 @@ __global__ void __launch_bounds__(kTile, kCtaPerSm) k_fwd_t5(Ws<float> w, Geo G,
   auto run = [&](auto issue) {  // all lanes' A stores -> one thread issues -> wait for D
     cta_sync_tmem();
     if (tid == 0) {
-      issue();
+      if (!(w.dbg & 16)) issue();
       commit(&s_bar[1]);
     }
   };
@@ -375,13 +375,23 @@ __global__ void __launch_bounds__(kTile, kCtaPerSm) k_fwd_t5(Ws<float> w, Geo G,
     for (int l = 0; l < S::NL; ++l) {
       loc[l] = compact<float>(locate<false>(G.lv[l], (double)p[0], (double)p[1], (double)p[2],
                                             act ? w.status : nullptr));
-      gather_fast<float, S::CG>(G.lv[l], loc[l], z + l * S::CG);
+      if (w.dbg & 8) {
+#pragma unroll
+        for (int c = 0; c < S::CG; ++c) z[l * S::CG + c] = 1e-3f * (float)c + loc[l].fx;
+      } else {
+        gather_fast<float, S::CG>(G.lv[l], loc[l], z + l * S::CG);
+      }
     }
     const int cr = ray < 0 ? 0 : ray;  // smoothness points: harmless colour, not stored
     const Loc qc = locate<false>(G.col, (double)p[0], (double)p[1], (double)p[2], nullptr);
 #pragma unroll
     for (int i = 0; i < 8 * KC; ++i) inp[i] = 0.f;
-    gather_fast<float, S::CC>(G.col, compact<float>(qc), inp);
+    if (w.dbg & 8) {
+#pragma unroll
+      for (int c = 0; c < S::CC; ++c) inp[c] = 1e-3f * (float)c + (float)qc.fx;
+    } else {
+      gather_fast<float, S::CC>(G.col, compact<float>(qc), inp);
+    }
 #pragma unroll
     for (int a = 0; a < 3; ++a) inp[S::CC + a] = w.r[cr * 3 + a];
   };
@@ -428,7 +438,8 @@ __global__ void __launch_bounds__(kTile, kCtaPerSm) k_fwd_t5(Ws<float> w, Geo G,
     ld16(tl, gz);
     float gr[3] = {0.f, 0.f, 0.f};
 #pragma unroll
-    for (int l = 0; l < S::NL; ++l) level_dx_fast<float, S::CG>(G.lv[l], loc[l], gz + l * S::CG, gr);
+    for (int l = 0; l < S::NL; ++l)
+      if (!(w.dbg & 8)) level_dx_fast<float, S::CG>(G.lv[l], loc[l], gz + l * S::CG, gr);
     // ---- colour: sigmoid(MLP_c([f_c, r]))  (gs/decoders.py:86-99)
     store_a<KC>(tl, inp);
     run([&] { issue_layer<KC>(tmem, sa(U::C0H), sa(U::C0L)); });
@@ -619,7 +630,7 @@ __global__ void __launch_bounds__(kTile, 2) k_bwd_geom_t5(Ws<float> w, Geo G, in
   auto mma_round = [&](auto issue) {
     cta_sync_tmem();
     if (tid == 0) {
-      issue();
+      if (!(w.dbg & 16)) issue();
       commit(&s_bar[1]);
     }
     tc::mbar_wait(&s_bar[1], phase);
@@ -929,7 +940,7 @@ __global__ void __launch_bounds__(kTile, 2) k_bwd_color_t5(Ws<float> w, Geo G, i
   auto mma_round = [&](auto issue) {
     cta_sync_tmem();
     if (tid == 0) {
-      issue();
+      if (!(w.dbg & 16)) issue();
       commit(&s_bar[1]);
     }
     tc::mbar_wait(&s_bar[1], phase);
