@@ -58,7 +58,7 @@ struct Ws {
   int sweep;            // tcgen05 taped kernels: bit 0 fwd, 1 geometry bwd, 2 colour bwd sweep the tiles backward
   int dbg;              // GSB_DBG time-attribution knobs (results invalid when set): 1 no scatter,
                         // 2 no outer products, 4 no CTA reduction, 8 no feature loads, 16 no MMAs,
-                        // 32 no L2 prefetch of the next tile's corners
+                        // 64 no grad-phi corner re-reads (forward)
   uint64_t* det_keys;   // deterministic scatter mode: [NS][NL+1][8] grad-row addresses, or null
   T* det_vals;          // ... and their [8] values (C used); reduced in sample order (k_det_reduce)
   T* pose_g;            // pose refinement, float32: [MN][IN_G] dphi/dz (k_fwd_tc), or null

@@ -137,26 +137,6 @@ __device__ __forceinline__ void store_a(uint32_t tl, const float* x) {
   }
 }
 
-// L2 prefetch of the corner rows a sample at p gathers from level L (C
-// channels): the fine geometry level and the colour grid do not fit the L2
-// together (95 + 146 MB at config 2), so a tile's gathers otherwise wait on
-// HBM.  Issued one tile ahead; no registers are held.  The z-adjacent corner
-// rows are contiguous, so the first and last byte of each pair is touched.
-__device__ __forceinline__ void prefetch_l2(const void* a) {
-  asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
-}
-template <int C>
-__device__ __forceinline__ void prefetch_corners(const LevelDev& L, const float (&p)[3]) {
-  const Loc q = locate<false>(L, (double)p[0], (double)p[1], (double)p[2], nullptr);
-  const float* F = reinterpret_cast<const float*>(L.feat) + q.base * C;
-#pragma unroll
-  for (int k = 0; k < 8; k += 2) {
-    const float* r = F + corner_off(L, k) * C;
-    prefetch_l2(r);
-    prefetch_l2(r + 2 * C - 1);
-  }
-}
-
 // D[0, NN) = A (TMEM) x B (smem tiles bh / bl, NN x K, K = 8 KS), 3xTF32
 template <int KS, uint32_t NN = 32>
 __device__ __forceinline__ void issue_layer(uint32_t tmem, uint32_t bh, uint32_t bl) {
@@ -373,36 +353,22 @@ __global__ void __launch_bounds__(kTile, kCtaPerSm) k_fwd_t5(Ws<float> w, Geo G,
   bool act;
   LocT<float> loc[S::NL];
   float z[8 * KG], inp[8 * KC];
-  // sample of `tile` this thread owns, and its taped point
-  auto tile_point = [&](int64_t tile, int64_t& ss, int& rr, float (&p)[3]) {
-    ss = ((w.sweep & 1) ? ntiles - 1 - tile : tile) * kTile + tid;  // backward sweep: L2 reuse
-    rr = -1;
-    if (ss < NS && ss < MN) {
-      rr = (int)((uint32_t)ss / (uint32_t)N);
-      taped_point<float>(w.o + rr * 3, w.r + rr * 3,
-                         dep[(int64_t)rr * w.ld + (int)((uint32_t)ss % (uint32_t)N)], G.lo, G.hi, p);
-    } else if (ss < NS) {
+  auto gather = [&](int64_t tile) {
+    s = ((w.sweep & 1) ? ntiles - 1 - tile : tile) * kTile + tid;  // backward sweep: L2 reuse
+    act = s < NS;
+    ray = -1;
+    float p[3];
+    if (act && s < MN) {
+      ray = (int)((uint32_t)s / (uint32_t)N);
+      taped_point<float>(w.o + ray * 3, w.r + ray * 3,
+                         dep[(int64_t)ray * w.ld + (int)((uint32_t)s % (uint32_t)N)], G.lo, G.hi, p);
+    } else if (act) {
 #pragma unroll
-      for (int a = 0; a < 3; ++a) p[a] = spts[(ss - MN) * 3 + a];
+      for (int a = 0; a < 3; ++a) p[a] = spts[(s - MN) * 3 + a];
     } else {
 #pragma unroll
       for (int a = 0; a < 3; ++a) p[a] = (float)G.lo[a];
     }
-  };
-  auto prefetch = [&](int64_t tile) {
-    if (tile >= ntiles || (w.dbg & 32)) return;
-    int64_t ss;
-    int rr;
-    float p[3];
-    tile_point(tile, ss, rr, p);
-    if (ss >= NS) return;
-    prefetch_corners<S::CG>(G.lv[S::NL - 1], p);
-    if (rr >= 0) prefetch_corners<S::CC>(G.col, p);
-  };
-  auto gather = [&](int64_t tile) {
-    float p[3];
-    tile_point(tile, s, ray, p);
-    act = s < NS;
 #pragma unroll
     for (int i = 0; i < 8 * KG; ++i) z[i] = 0.f;
 #pragma unroll
@@ -432,7 +398,6 @@ __global__ void __launch_bounds__(kTile, kCtaPerSm) k_fwd_t5(Ws<float> w, Geo G,
   gather(blockIdx.x);
   tc::mbar_wait(&s_bar[0], 0);
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    prefetch(tile + gridDim.x);  // HBM -> L2 under this tile's MMA chain
     float h[32];
     uint32_t m0 = 0u;
     // ---- geometry layer 0 / 1 (gs/decoders.py:40-60)
@@ -474,7 +439,7 @@ __global__ void __launch_bounds__(kTile, kCtaPerSm) k_fwd_t5(Ws<float> w, Geo G,
     float gr[3] = {0.f, 0.f, 0.f};
 #pragma unroll
     for (int l = 0; l < S::NL; ++l)
-      if (!(w.dbg & 8)) level_dx_fast<float, S::CG>(G.lv[l], loc[l], gz + l * S::CG, gr);
+      if (!(w.dbg & 72)) level_dx_fast<float, S::CG>(G.lv[l], loc[l], gz + l * S::CG, gr);
     // ---- colour: sigmoid(MLP_c([f_c, r]))  (gs/decoders.py:86-99)
     store_a<KC>(tl, inp);
     run([&] { issue_layer<KC>(tmem, sa(U::C0H), sa(U::C0L)); });
@@ -681,22 +646,6 @@ __global__ void __launch_bounds__(kTile, 2) k_bwd_geom_t5(Ws<float> w, Geo G, in
     const int64_t tt = (w.sweep & 2) ? ntiles - 1 - tile : tile;
     const int64_t s = tt * kTile + tid;
     const bool active = s < NS;
-    if (tile + gridDim.x < ntiles && !(w.dbg & 32)) {  // next tile's fine-level corners: HBM -> L2
-      const int64_t tn = tile + gridDim.x;
-      const int64_t sn = ((w.sweep & 2) ? ntiles - 1 - tn : tn) * kTile + tid;
-      if (sn < NS) {
-        float pn[3];
-        if (sn < MN) {
-          const int ray = (int)((uint32_t)sn / (uint32_t)N);
-          taped_point<float>(w.o + ray * 3, w.r + ray * 3,
-                             dep[(int64_t)ray * w.ld + (int)((uint32_t)sn % (uint32_t)N)], G.lo, G.hi, pn);
-        } else {
-#pragma unroll
-          for (int a = 0; a < 3; ++a) pn[a] = spts[(sn - MN) * 3 + a];
-        }
-        prefetch_corners<S::CG>(G.lv[S::NL - 1], pn);
-      }
-    }
     __syncwarp();  // the previous tile's outer products are done with this warp's rows
     // ---- per sample: point, z and v in one pass over the corners
     LocT<float> loc[S::NL];
@@ -1006,17 +955,6 @@ __global__ void __launch_bounds__(kTile, 2) k_bwd_color_t5(Ws<float> w, Geo G, i
     const int64_t s = tt * kTile + tid;
     const bool active = s < NS;
     const int ray = active ? (int)((uint32_t)s / (uint32_t)N) : 0;
-    if (tile + gridDim.x < ntiles && !(w.dbg & 32)) {  // next tile's colour corners: HBM -> L2
-      const int64_t tn = tile + gridDim.x;
-      const int64_t sn = ((w.sweep & 4) ? ntiles - 1 - tn : tn) * kTile + tid;
-      if (sn < NS) {
-        const int rn = (int)((uint32_t)sn / (uint32_t)N);
-        float pn[3];
-        taped_point<float>(w.o + rn * 3, w.r + rn * 3, dep[(int64_t)rn * w.ld + (int)((uint32_t)sn % (uint32_t)N)],
-                           G.lo, G.hi, pn);
-        prefetch_corners<S::CC>(G.col, pn);
-      }
-    }
     __syncwarp();  // the previous tile's outer products are done with this warp's rows
     LocT<float> q;
     float cb[3];
