@@ -39,12 +39,14 @@ FRAMES = 8
 
 
 def peaks():
+    """(HBM GB/s, bf16 dense TFLOP/s burst, kind) from MEASURED_PEAKS.json
+    (driver-written), else the B200_PROFILING.md fallback."""
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
         with open(p) as f:
             d = json.load(f)
-        return float(d.get("hbm_gbs", 6650.0)), "measured"
-    return 6650.0, "fallback"
+        return float(d.get("hbm_gbs", 6650.0)), float(d.get("bf16_tflops", 1590.0)), "measured"
+    return 6650.0, 1590.0, "fallback"
 
 
 def make_cfg(precision="single", batch=M_PER_GPU, seed=0, config=2, coarse=96, smooth=True):
@@ -165,7 +167,6 @@ MAC_DELTA = HID * HID + HID * IN_G                                # dphi/dz chai
 MAC_COL_FWD = IN_C * HID + HID * HID + HID * 3
 MAC_GEO_BWD = MAC_GEO_FWD + MAC_DELTA + IN_G * HID + HID * HID + IN_G * HID + HID * HID + HID
 MAC_COL_BWD = MAC_COL_FWD + 3 * HID + HID * HID + HID * 6 + (IN_C + 1) * HID + HID * HID + HID * 3
-FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12                 # nominal FMA peak
 
 
 def workload_name(args, N):
@@ -202,8 +203,12 @@ def traffic_of(kernel, workload):
     return None
 
 
-def kernel_table(model, kt, K, M, N, S, P, peak_hbm):
-    """Per-kernel algorithmic work over live CUDA-event times."""
+def kernel_table(model, kt, K, M, N, S, P, peak_hbm, peak_bf16):
+    """Per-kernel algorithmic work over live CUDA-event times,
+    against both roofs: measured HBM bandwidth, and the 3xTF32 tensor rate
+    the float32 MLPs run at (tf32 is half the measured bf16 dense rate, and
+    3xTF32 spends three tf32 MMAs per fp32-accurate product).  `bound` is
+    the roof with the larger ideal time."""
     G_s = sum(8 * l.width * 4 for l in model.grid.levels if l.features.size * 4 > 32 * 2 ** 20)
     Cc_s = 8 * 6 * 4 if model.grid.color.features.size * 4 > 32 * 2 ** 20 else 0
     n_imp = N - 12  # coarse + 2 x 12 evaluated (the last round's 12 are not)
@@ -215,21 +220,21 @@ def kernel_table(model, kt, K, M, N, S, P, peak_hbm):
         "k_bwd_geom": (NS * G_s, NS * MAC_GEO_BWD),
         "k_bwd_color": (M * N * Cc_s, M * N * MAC_COL_BWD),
     }
+    tensor_peak = peak_bf16 / 2.0 / 3.0  # TFLOP/s of fp32-accurate 3xTF32 products
     rows = []
     for name, (ms, n) in sorted(kt.items(), key=lambda x: -x[1][0]):
         t = ms / K / 1e3
         b, mac = work.get(name, (0, 0))
         hbm = b / t / 1e9 if t > 0 else 0.0
         fl = 2 * mac / t / 1e12 if t > 0 else 0.0
-        compute = mac > 0 and 2 * mac / (FP32_PEAK_TFLOPS * 1e12) > b / (peak_hbm * 1e9)
+        t_hbm, t_ten = b / (peak_hbm * 1e9), 2 * mac / (tensor_peak * 1e12)
         r = {"kernel": name, "ms_per_step": ms / K, "launches_per_step": n / K,
-             "alg_bytes": b, "alg_flops": 2 * mac, "hbm_gbs": hbm, "tflops": fl}
-        if compute:
-            r.update(bound="tensor", achieved=fl, peak=FP32_PEAK_TFLOPS, unit="TFLOP/s",
-                     frac=fl / FP32_PEAK_TFLOPS,
-                     peak_kind="nominal fp32 FMA peak 148 SM x 128 FMA/clk x 2 x 1.965 GHz "
-                               "(fp32 MLP work; 3xTF32 mma.sync measured at the same "
-                               "effective rate, tools/mb_layers.cu)")
+             "alg_bytes": b, "alg_flops": 2 * mac, "hbm_gbs": hbm, "tflops": fl,
+             "hbm_frac": hbm / peak_hbm, "tensor_frac": fl / tensor_peak}
+        if t_ten > t_hbm:
+            r.update(bound="tensor", achieved=fl, peak=tensor_peak, unit="TFLOP/s", frac=fl / tensor_peak,
+                     peak_kind="3xTF32 rate derived from the measured bf16 dense peak "
+                               "(MEASURED_PEAKS.json bf16_tflops / 2 (tf32) / 3 (passes))")
         else:
             r.update(bound="hbm", achieved=hbm, peak=peak_hbm, unit="GB/s",
                      frac=hbm / peak_hbm, peak_kind="measured (MEASURED_PEAKS.json hbm_gbs)")
@@ -360,6 +365,9 @@ def main():
                     help="pose refinement on (refine_poses=True, frame 0 frozen; not the headline)")
     ap.add_argument("--prefetch", action="store_true",
                     help="host draws on a background thread in the e2e leg")
+    ap.add_argument("--strong", action="store_true",
+                    help="strong scaling (SURVEY 8d c3(i)): the global batch is --rays, split by rows "
+                         "across the ranks (default: weak, --rays per rank)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -385,8 +393,12 @@ def main():
         pg = dist
     W = max(args.warmup, 3)
     K = args.steps
-    M = args.rays
-    cfg = make_cfg(args.precision, batch=M * ws_, config=args.config, coarse=args.coarse,
+    # weak: --rays per rank (global batch rays x ranks); strong: --rays in total,
+    # rank g takes rows parallel.shard_rows(rays, g, N) of the one global batch
+    M_glob = args.rays if args.strong else args.rays * ws_
+    lo_r, hi_r = parallel.shard_rows(M_glob, rank, ws_)
+    M = hi_r - lo_r  # this rank's rays
+    cfg = make_cfg(args.precision, batch=M_glob, config=args.config, coarse=args.coarse,
                    smooth=not args.no_smooth)
     cfg.refine_poses = bool(args.refine_poses)
     if args.config == 4:
@@ -477,7 +489,7 @@ def main():
     ms_step = total_ms / K
     adam_ms = float(np.mean([x.elapsed_time(y) for x, y in t_adam]))
     obj_ms = float(np.mean([x.elapsed_time(y) for x, y in t_step]))
-    value = M * ws_ * K / (total_ms / 1e3)
+    value = M_glob * K / (total_ms / 1e3)
 
     # ---- per-kernel live timing (CUDA events between launches on the step
     # stream, gsb_timing_enable); a separate pass so `value` carries no markers
@@ -526,7 +538,7 @@ def main():
         tt = torch.tensor([e2e_s], device=dev)
         pg.all_reduce(tt, op=pg.ReduceOp.MAX)
         e2e_s = float(tt.item())
-    e2e = M * ws_ * K / e2e_s
+    e2e = M_glob * K / e2e_s
 
     if rank != 0:
         if pg:
@@ -534,9 +546,9 @@ def main():
         return 0
 
     # ---- roofline of the dominant kernel + per-kernel table
-    peak, peak_kind = peaks()
+    peak, peak_bf16, peak_kind = peaks()
     B, P = b_alg_bytes(model, M, N, S)
-    table = kernel_table(model, kt, K, M, N, S, P, peak)
+    table = kernel_table(model, kt, K, M, N, S, P, peak, peak_bf16)
     dom = max(table, key=lambda r: r["ms_per_step"])
     roofline = {"bound": dom["bound"], "kernel": dom["kernel"], "achieved": dom["achieved"],
                 "peak": dom["peak"], "unit": dom["unit"], "frac": dom["frac"],
@@ -557,11 +569,12 @@ def main():
         cpu = {"value": r["value"], "unit": "rays/s", "cores": r["threads"], "kind": kind,
                "sample": ref_sample_text(r, kind, args.config)}
     line = {"metric": METRIC, "value": value, "unit": "rays/s", "n_gpus": ws_, "steps": K,
-            "warmup": W, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": W, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "strong" if args.strong else "weak",
             "vs_baseline": None, "dtype": "f32" if args.precision == "single" else "f64",
             "data": "synthetic",
             "config": {"workload": workload_name(args, N),
-                       "rays_per_gpu": M, "samples_per_ray": N, "params": P,
+                       "rays_per_gpu": M, "global_rays": M_glob, "samples_per_ray": N, "params": P,
                        "frames": 20 if args.config == 1 else args.frames,
                        "frames_note": "SURVEY 8(d) defines c2 at F = 300 frames; the step "
                                       "cost does not depend on F (it only sets the ray-id range)",

@@ -786,7 +786,12 @@ int gsb_importance_round(int32_t n, int32_t K, int32_t A, int32_t ld, const doub
   if (n == 0) return GSB_OK;
   gsb_pcg64_t g = {0, 0, 0, 0};
   if (rng) g = *rng;
-  k_importance_twin<<<(n + 3) / 4, 128, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+  const size_t imp_smem = (size_t)kImpRaysPerBlock * imp_row_bytes(K + A, A);
+  if (cudaFuncSetAttribute(k_importance_twin, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)imp_smem) !=
+      cudaSuccess)
+    return GSB_E_CUDA;
+  k_importance_twin<<<(n + kImpRaysPerBlock - 1) / kImpRaysPerBlock, 128, imp_smem,
+                      reinterpret_cast<cudaStream_t>(stream)>>>(
       n, K, A, ld, depths, phi, nullptr, s, nearv, farv, uniforms, g, uniforms ? 0 : 1, depths_out,
       src_out, weights_out);
   GSB_LAUNCHED();
@@ -802,7 +807,12 @@ int gsb_importance_refine(int32_t n, int32_t K, int32_t A, int32_t ld, const dou
     return GSB_E_ARG;
   if (n == 0) return GSB_OK;
   gsb_pcg64_t g = {0, 0, 0, 0};
-  k_importance_twin<<<(n + 3) / 4, 128, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+  const size_t imp_smem = (size_t)kImpRaysPerBlock * imp_row_bytes(K + A, A);
+  if (cudaFuncSetAttribute(k_importance_twin, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)imp_smem) !=
+      cudaSuccess)
+    return GSB_E_CUDA;
+  k_importance_twin<<<(n + kImpRaysPerBlock - 1) / kImpRaysPerBlock, 128, imp_smem,
+                      reinterpret_cast<cudaStream_t>(stream)>>>(
       n, K, A, ld, depths, nullptr, weights, 0.0, nearv, farv, uniforms, g, 0, depths_out,
       src_out, nullptr);
   GSB_LAUNCHED();

@@ -458,61 +458,94 @@ __global__ void k_smooth_points(gsb_dataset_t D, const double* __restrict__ pose
 }
 
 // ---------------------------------------------------------------------------
-// one importance round, one warp per ray (render_weights_data +
-// importance_refine_with_sources + enforce_separation, gs/renderer.py:162-173,
-// gs/sampler.py:128-197).  The two float64 recurrences (cumprod of the
-// transmittance, cumsum of the CDF) run serially on lane 0 so they round
-// exactly like numpy; everything else is lane-parallel: sigmoid ratios,
-// CDF normalisation, inverse-CDF draws, the stable merge (by rank), the
-// separation test and provenance.
+// one importance round (render_weights_data + importance_refine_with_sources
+// + enforce_separation, gs/renderer.py:162-173, gs/sampler.py:128-197) for a
+// ray handled by a group of G lanes of a warp (32 / G rays per warp).  The
+// two float64 recurrences (cumprod of the transmittance, cumsum of the CDF)
+// run serially on the group's first lane so they round exactly like numpy;
+// the G-lane groups of a warp run their serial chains side by side, so a
+// warp retires 32 / G of them at once.  Everything else is lane-parallel
+// within the group: sigmoid ratios, CDF normalisation, inverse-CDF draws, the
+// stable merge (by rank), the separation test and provenance.
 
-struct __align__(16) ImpSmem {
-  double om[GSB_KMAX];
-  double cdf[GSB_KMAX];
-  double out[GSB_KMAX];
-  double nw[GSB_AMAX];
-  int32_t src[GSB_KMAX];
+// per-ray scratch in shared memory, `ld` >= K + A entries per array
+struct ImpRow {
+  double* a;    // sigmoid values, then om, then the CDF (in place)
+  double* out;  // merged depths
+  double* nw;   // new depths (A)
+  int32_t* src; // provenance (-1 = new / moved)
+};
+__host__ __device__ constexpr size_t imp_row_bytes(int ld, int A) {
+  return (size_t)ld * 8 * 2 + (size_t)((A + 1) / 2 * 2) * 8 + (size_t)(ld + 3) / 4 * 4 * 4;
+}
+__device__ __forceinline__ ImpRow imp_row(unsigned char* base, int ld, int A) {
+  ImpRow r;
+  r.a = reinterpret_cast<double*>(base);
+  r.out = r.a + ld;
+  r.nw = r.out + ld;
+  r.src = reinterpret_cast<int32_t*>(r.nw + (A + 1) / 2 * 2);
+  return r;
+}
+
+template <int G>
+struct LaneGroup {
+  int gl;        // lane in the group
+  unsigned gm;   // the group's lanes
+  __device__ __forceinline__ LaneGroup() {
+    const int lane = threadIdx.x & 31;
+    gl = lane % G;
+    gm = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (lane - gl));
+  }
+  __device__ __forceinline__ void sync() const { __syncwarp(gm); }
+  template <typename V>
+  __device__ __forceinline__ V bcast(V v) const { return __shfl_sync(gm, v, 0, G); }
+  __device__ __forceinline__ bool all(bool p) const { return (__ballot_sync(gm, p) & gm) == gm; }
+  __device__ __forceinline__ bool any(bool p) const { return (__ballot_sync(gm, p) & gm) != 0u; }
+  __device__ __forceinline__ int sum(int v) const {
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) v += __shfl_xor_sync(gm, v, o, G);
+    return v;
+  }
 };
 
 // d, ph: (K) input row; win: optional given weights (K); uni: optional
-// uniforms (A) else PCG64 advanced to row*A; writes out/src (K+A) in smem.
-// WOUT: also write the rendering weights to wout (the twin's output).
-template <bool WOUT>
-static __device__ void importance_warp(ImpSmem& S, int K, int A, const double* __restrict__ d,
-                                const double* __restrict__ ph, const double* __restrict__ win,
-                                double s, double nearv, double farv, const gsb_pcg64_t& rng,
-                                uint64_t row, const double* __restrict__ uni,
-                                double* __restrict__ wout, const uint64_t* __restrict__ row_state = nullptr) {
-  const int lane = threadIdx.x & 31;
-  const unsigned full = 0xffffffffu;
-  double total;
+// uniforms (A) else PCG64 at row * A (row_state: that state precomputed);
+// writes R.out / R.src (K + A).  WOUT: also the rendering weights to wout.
+template <int G, bool WOUT>
+static __device__ void importance_group(const LaneGroup<G>& grp, const ImpRow& R, int K, int A,
+                                        const double* __restrict__ d, const double* __restrict__ ph,
+                                        const double* __restrict__ win, double s, double nearv,
+                                        double farv, const gsb_pcg64_t& rng, uint64_t row,
+                                        const double* __restrict__ uni, double* __restrict__ wout,
+                                        const uint64_t* __restrict__ row_state = nullptr) {
+  const int gl = grp.gl;
+  double total = 0.0;
+  double* cdf = R.a;
   if (win) {
-    if (lane == 0) {
+    if (gl == 0) {
       double c = 0.0;
       for (int i = 0; i < K - 1; ++i) {
         c = (i == 0) ? win[i] : c + win[i];
-        S.cdf[i] = c;
+        cdf[i] = c;
       }
       total = c;
     }
   } else {
-    // om_i = min(sig_{i+1} / max(sig_i, 1e-12), 1)
-    for (int i = lane; i < K; i += 32) S.out[i] = sigmoid_raw(s * ph[i]);
-    __syncwarp();
-    for (int i = lane; i < K - 1; i += 32) {
-      const double den = S.out[i] >= 1e-12 ? S.out[i] : 1e-12;
-      const double ratio = S.out[i + 1] / den;
-      S.om[i] = ratio <= 1.0 ? ratio : 1.0;
+    // om_i = min(sig_{i+1} / max(sig_i, 1e-12), 1): sigmoids into out, om into a
+    for (int i = gl; i < K; i += G) R.out[i] = sigmoid_raw(s * ph[i]);
+    grp.sync();
+    for (int i = gl; i < K - 1; i += G) {
+      const double den = R.out[i] >= 1e-12 ? R.out[i] : 1e-12;
+      const double ratio = R.out[i + 1] / den;
+      R.a[i] = ratio <= 1.0 ? ratio : 1.0;
     }
-    __syncwarp();
-    if (lane == 0) {  // sequential cumprod / cumsum, as numpy
-      // four steps per trip: the om loads (16-byte) are issued ahead of the
-      // two dependent float64 chains (trans *= om, c += w)
+    grp.sync();
+    if (gl == 0) {  // sequential cumprod / cumsum, as numpy; the CDF overwrites om in place
       double trans = 1.0, c = 0.0;
       int i = 0;
       for (; i + 4 <= K - 1; i += 4) {
-        const double2 o01 = *reinterpret_cast<const double2*>(S.om + i);
-        const double2 o23 = *reinterpret_cast<const double2*>(S.om + i + 2);
+        const double2 o01 = *reinterpret_cast<const double2*>(R.a + i);
+        const double2 o23 = *reinterpret_cast<const double2*>(R.a + i + 2);
         const double om4[4] = {o01.x, o01.y, o23.x, o23.y};
         double c4[4];
 #pragma unroll
@@ -523,54 +556,54 @@ static __device__ void importance_warp(ImpSmem& S, int K, int A, const double* _
           c4[q] = c;
           trans = trans * om4[q];
         }
-        *reinterpret_cast<double2*>(S.cdf + i) = make_double2(c4[0], c4[1]);
-        *reinterpret_cast<double2*>(S.cdf + i + 2) = make_double2(c4[2], c4[3]);
+        *reinterpret_cast<double2*>(cdf + i) = make_double2(c4[0], c4[1]);
+        *reinterpret_cast<double2*>(cdf + i + 2) = make_double2(c4[2], c4[3]);
       }
       for (; i < K - 1; ++i) {
-        const double om = S.om[i];
+        const double om = R.a[i];
         const double wi = trans * (1.0 - om);
         if constexpr (WOUT) wout[i] = wi;
         c = (i == 0) ? wi : c + wi;
-        S.cdf[i] = c;
+        cdf[i] = c;
         trans = trans * om;
       }
       if constexpr (WOUT) wout[K - 1] = trans * (1.0 - 1.0);
       total = c;
     }
   }
-  total = __shfl_sync(full, total, 0);
-  __syncwarp();
+  total = grp.bcast(total);
+  grp.sync();
   const bool dead = total <= 0.0;
   if (dead)
-    for (int i = lane; i < K - 1; i += 32) S.cdf[i] = (double)(i + 1);
-  __syncwarp();
-  const double last = S.cdf[K - 2];
-  __syncwarp();
-  for (int i = lane; i < K - 1; i += 32) S.cdf[i] = S.cdf[i] / last;
-  __syncwarp();
-  // inverse-CDF draws, lane a < A
-  if (lane < A) {
+    for (int i = gl; i < K - 1; i += G) cdf[i] = (double)(i + 1);
+  grp.sync();
+  const double last = cdf[K - 2];
+  grp.sync();
+  for (int i = gl; i < K - 1; i += G) cdf[i] = cdf[i] / last;
+  grp.sync();
+  // inverse-CDF draws
+  for (int a = gl; a < A; a += G) {
     double u;
     if (uni) {
-      u = uni[lane];
+      u = uni[a];
     } else {
       Pcg g;
       g.init(rng);
       if (row_state) {  // state at row * A precomputed (k_ray_setup): a short jump
         g.state = ((u128)row_state[0] << 64) | (u128)row_state[1];
-        g.advance((uint64_t)lane);
+        g.advance((uint64_t)a);
       } else {
-        g.advance(row * (uint64_t)A + (uint64_t)lane);
+        g.advance(row * (uint64_t)A + (uint64_t)a);
       }
       u = g.next_double();
     }
     int lo = 0, hi = K - 1;  // idx = #(cdf <= u): upper bound on a non-decreasing array
     while (lo < hi) {
       const int mid = (lo + hi) >> 1;
-      if (S.cdf[mid] <= u) lo = mid + 1; else hi = mid;
+      if (cdf[mid] <= u) lo = mid + 1; else hi = mid;
     }
     const int idx = lo < K - 2 ? lo : K - 2;
-    const double clo = idx > 0 ? S.cdf[idx - 1] : 0.0, chi = S.cdf[idx];
+    const double clo = idx > 0 ? cdf[idx - 1] : 0.0, chi = cdf[idx];
     double frac;
     if (chi > clo) {
       double den = chi - clo;
@@ -581,56 +614,59 @@ static __device__ void importance_warp(ImpSmem& S, int K, int A, const double* _
     }
     double v = d[idx] + frac * (d[idx + 1] - d[idx]);
     if (dead) v = nearv + u * (farv - nearv);
-    S.nw[lane] = v;
+    R.nw[a] = v;
   }
-  __syncwarp();
+  grp.sync();
   // stable merge (np.argsort kind="stable": old columns precede new on ties)
   bool sorted = true;
-  for (int i = lane; i + 1 < K; i += 32)
+  for (int i = gl; i + 1 < K; i += G)
     if (!(d[i] <= d[i + 1])) sorted = false;
-  sorted = __all_sync(full, sorted);
+  sorted = grp.all(sorted);
   const int n = K + A;
   if (sorted) {
-    for (int i = lane; i < K; i += 32) {
+    for (int i = gl; i < K; i += G) {
       const double di = d[i];
       int c = 0;
-      for (int a = 0; a < A; ++a) c += S.nw[a] < di;
-      S.out[i + c] = di;
-      S.src[i + c] = i;
+      for (int a = 0; a < A; ++a) c += R.nw[a] < di;
+      R.out[i + c] = di;
+      R.src[i + c] = i;
     }
-    if (lane < A) {
-      const double v = S.nw[lane];
+    for (int a = gl; a < A; a += G) {
+      const double v = R.nw[a];
       int lo = 0, hi = K;  // #(old <= v)
       while (lo < hi) {
         const int mid = (lo + hi) >> 1;
         if (d[mid] <= v) lo = mid + 1; else hi = mid;
       }
       int r = 0;
-      for (int b = 0; b < A; ++b) r += (S.nw[b] < v) || (S.nw[b] == v && b < lane);
-      S.out[lo + r] = v;
-      S.src[lo + r] = -1;
+      for (int b = 0; b < A; ++b) r += (R.nw[b] < v) || (R.nw[b] == v && b < a);
+      R.out[lo + r] = v;
+      R.src[lo + r] = -1;
     }
-  } else if (lane == 0) {  // general stable insertion sort (unsorted input rows)
+  } else if (gl == 0) {  // general stable insertion sort (unsorted input rows)
     for (int t = 0; t < n; ++t) {
-      const double v = t < K ? d[t] : S.nw[t - K];
+      const double v = t < K ? d[t] : R.nw[t - K];
       const int sv = t < K ? t : -1;
       int q = t;
-      while (q > 0 && S.out[q - 1] > v) {
-        S.out[q] = S.out[q - 1];
-        S.src[q] = S.src[q - 1];
+      while (q > 0 && R.out[q - 1] > v) {
+        R.out[q] = R.out[q - 1];
+        R.src[q] = R.src[q - 1];
         --q;
       }
-      S.out[q] = v;
-      S.src[q] = sv;
+      R.out[q] = v;
+      R.src[q] = sv;
     }
   }
-  __syncwarp();
+  grp.sync();
   bool bad = false;
-  for (int i = lane; i + 1 < n; i += 32)
-    if (S.out[i + 1] - S.out[i] < 1e-9) bad = true;
-  if (__any_sync(full, bad) && lane == 0) separation_fallback(S.out, S.src, n);
-  __syncwarp();
+  for (int i = gl; i + 1 < n; i += G)
+    if (R.out[i + 1] - R.out[i] < 1e-9) bad = true;
+  if (grp.any(bad) && gl == 0) separation_fallback(R.out, R.src, n);
+  grp.sync();
 }
+
+constexpr int kImpG = 8;              // lanes per ray (4 rays per warp)
+constexpr int kImpRaysPerBlock = 16;  // 128 threads
 
 template <typename T>
 __global__ void __launch_bounds__(128) k_importance_dev(Ws<T> w, int M, int K, int A, int ray_base,
@@ -643,25 +679,28 @@ __global__ void __launch_bounds__(128) k_importance_dev(Ws<T> w, int M, int K, i
                                                         int32_t* __restrict__ evl_count, int64_t cap,
                                                         int want_list, int count_final, double trunc,
                                                         const uint64_t* __restrict__ row_states) {
-  __shared__ ImpSmem smem[4];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int i = blockIdx.x * 4 + wid;
-  if (i >= M) return;  // warp-uniform
-  ImpSmem& S = smem[wid];
+  constexpr int G = kImpG;
+  extern __shared__ __align__(16) unsigned char imp_smem[];
+  const LaneGroup<G> grp;
+  const int gid = threadIdx.x / G;  // ray slot in the block
+  const int i = blockIdx.x * kImpRaysPerBlock + gid;
+  const int n = K + A;
+  if (i >= M) return;  // group-uniform
+  const ImpRow R = imp_row(imp_smem + (size_t)gid * imp_row_bytes(n, A), n, A);
   // ModelState.s_value() = float(np.exp(log_s)) in the model dtype
   const double s = (double)exp(log_s[0]);
   const double* d = dep + (int64_t)i * w.ld;
   const double* ph = phi + (int64_t)i * w.ld;
-  importance_warp<false>(S, K, A, d, ph, nullptr, s, w.nearv[i], w.farv[i], rng,
-                         (uint64_t)(ray_base + i), nullptr, nullptr,
-                         row_states ? row_states + (int64_t)i * 2 : nullptr);
-  const int n = K + A;
+  importance_group<G, false>(grp, R, K, A, d, ph, nullptr, s, w.nearv[i], w.farv[i], rng,
+                             (uint64_t)(ray_base + i), nullptr, nullptr,
+                             row_states ? row_states + (int64_t)i * 2 : nullptr);
+  const int gl = grp.gl;
   double* out = dep_out + (int64_t)i * w.ld;
   double* po = phi_out + (int64_t)i * w.ld;
   int nnew = 0;
-  for (int t = lane; t < n; t += 32) {
-    out[t] = S.out[t];
-    const int sv = S.src[t];
+  for (int t = gl; t < n; t += G) {
+    out[t] = R.out[t];
+    const int sv = R.src[t];
     if (sv >= 0) po[t] = ph[sv];
     else ++nnew;
   }
@@ -669,8 +708,8 @@ __global__ void __launch_bounds__(128) k_importance_dev(Ws<T> w, int M, int K, i
     const int valid = w.valid[i];
     const double D = w.dray[i];
     int ntr = 0, nfs = 0, neik = 0;
-    for (int t = lane; t < n; t += 32) {
-      const double b = D - S.out[t];
+    for (int t = gl; t < n; t += G) {
+      const double b = D - R.out[t];
       const bool tr = valid && fabs(b) <= trunc;
       const bool fs = valid && b > trunc;
       const bool bh = valid && b < -trunc;
@@ -678,10 +717,10 @@ __global__ void __launch_bounds__(128) k_importance_dev(Ws<T> w, int M, int K, i
       nfs += fs;
       neik += (fs || bh || !valid);
     }
-    ntr = warp_sum(ntr);
-    nfs = warp_sum(nfs);
-    neik = warp_sum(neik);
-    if (lane == 0) {
+    ntr = grp.sum(ntr);
+    nfs = grp.sum(nfs);
+    neik = grp.sum(neik);
+    if (gl == 0) {
       w.cnt[i * 3 + 0] = ntr;
       w.cnt[i * 3 + 1] = nfs;
       w.cnt[i * 3 + 2] = neik;
@@ -692,25 +731,27 @@ __global__ void __launch_bounds__(128) k_importance_dev(Ws<T> w, int M, int K, i
     }
   }
   if (!want_list) return;
-  const int tot = warp_sum(nnew);
+  const int tot = grp.sum(nnew);
   int base = 0;
-  if (lane == 0) base = atomicAdd(evl_count, tot);
-  base = __shfl_sync(0xffffffffu, base, 0);
+  if (gl == 0) base = atomicAdd(evl_count, tot);
+  base = grp.bcast(base);
   if (base + tot > cap) {
-    if (lane == 0) atomicOr(w.status + GSB_ST_OVERFLOW, 1);
+    if (gl == 0) atomicOr(w.status + GSB_ST_OVERFLOW, 1);
     return;
   }
   // compact the new slots in order
-  for (int t0 = 0; t0 < n; t0 += 32) {
-    const int t = t0 + lane;
-    const bool isnew = t < n && S.src[t] < 0;
-    const unsigned bal = __ballot_sync(0xffffffffu, isnew);
-    if (isnew) evl[base + __popc(bal & ((1u << lane) - 1u))] = i * GSB_KMAX + t;
+  for (int t0 = 0; t0 < n; t0 += G) {
+    const int t = t0 + gl;
+    const bool isnew = t < n && R.src[t] < 0;
+    const unsigned bal = __ballot_sync(grp.gm, isnew) & grp.gm;
+    const unsigned below = bal & ((1u << (threadIdx.x & 31)) - 1u);
+    if (isnew) evl[base + __popc(below)] = i * GSB_KMAX + t;
     base += __popc(bal);
   }
 }
 
-// twin: explicit weights or phi, explicit uniforms or generator; one warp per row
+// twin: explicit weights or phi, explicit uniforms or generator; the same
+// G-lane groups as the step kernel
 static __global__ void __launch_bounds__(128) k_importance_twin(int M, int K, int A, int ld,
                                                          const double* dep, const double* phi,
                                                          const double* win, double s,
@@ -718,22 +759,26 @@ static __global__ void __launch_bounds__(128) k_importance_twin(int M, int K, in
                                                          const double* uni, gsb_pcg64_t rng,
                                                          int use_rng, double* out, int32_t* src,
                                                          double* wts) {
-  __shared__ ImpSmem smem[4];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int i = blockIdx.x * 4 + wid;
+  constexpr int G = kImpG;
+  extern __shared__ __align__(16) unsigned char imp_smem[];
+  const LaneGroup<G> grp;
+  const int gid = threadIdx.x / G;
+  const int i = blockIdx.x * kImpRaysPerBlock + gid;
   if (i >= M) return;
-  ImpSmem& S = smem[wid];
+  const int n = K + A;
+  const ImpRow R = imp_row(imp_smem + (size_t)gid * imp_row_bytes(n, A), n, A);
   const double* d = dep + (int64_t)i * ld;
   const double* ph = phi ? phi + (int64_t)i * ld : nullptr;
   const double* wi = win ? win + (int64_t)i * ld : nullptr;
   const double* ui = use_rng ? nullptr : uni + (int64_t)i * A;
   if (wts)
-    importance_warp<true>(S, K, A, d, ph, wi, s, nearv[i], farv[i], rng, (uint64_t)i, ui, wts + (int64_t)i * ld);
+    importance_group<G, true>(grp, R, K, A, d, ph, wi, s, nearv[i], farv[i], rng, (uint64_t)i, ui,
+                              wts + (int64_t)i * ld);
   else
-    importance_warp<false>(S, K, A, d, ph, wi, s, nearv[i], farv[i], rng, (uint64_t)i, ui, nullptr);
-  for (int t = lane; t < K + A; t += 32) {
-    out[(int64_t)i * ld + t] = S.out[t];
-    src[(int64_t)i * ld + t] = S.src[t];
+    importance_group<G, false>(grp, R, K, A, d, ph, wi, s, nearv[i], farv[i], rng, (uint64_t)i, ui, nullptr);
+  for (int t = grp.gl; t < n; t += G) {
+    out[(int64_t)i * ld + t] = R.out[t];
+    src[(int64_t)i * ld + t] = R.src[t];
   }
 }
 

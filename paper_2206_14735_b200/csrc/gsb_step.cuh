@@ -195,7 +195,10 @@ int run_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step
       for (int rnd = 0; rnd < R; ++rnd) {
         const bool need_phi = rnd < R - 1;
         GSB_CHECK(cudaMemsetAsync(w.evl_count, 0, sizeof(int32_t), stream));
-        k_importance_dev<T><<<(M + 3) / 4, 128, 0, stream>>>(
+        const size_t imp_smem = (size_t)kImpRaysPerBlock * imp_row_bytes(K + A, A);
+        GSB_CHECK(cudaFuncSetAttribute(k_importance_dev<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)imp_smem));
+        k_importance_dev<T><<<(M + kImpRaysPerBlock - 1) / kImpRaysPerBlock, 128, imp_smem, stream>>>(
             w, M, K, A, st->ray_base, w.dep[cur], w.phi[cur], w.dep[1 - cur], w.phi[1 - cur],
             log_s, st->rng_importance[rnd], w.evl, w.evl_count, w.evl_cap, need_phi ? 1 : 0,
             rnd == R - 1 ? 1 : 0, st->truncation, w.imp_state + (int64_t)rnd * M * 2);

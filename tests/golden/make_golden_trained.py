@@ -1,0 +1,111 @@
+"""Golden metrics of a mesh TRAINED by the reference (north-star mesh gate).
+
+    PYTHONPATH=/root/reference/pkg/src NUMBA_CACHE_DIR=/tmp/numba_cache \\
+        python tests/golden/make_golden_trained.py
+
+Runs the reference's own training loop (``gridsurf.optimizer.train``,
+gs/optimizer.py:334-391: sphere pre-fit, then K iterations of draw_ray_batch
+-> train_objective -> grad -> Adam) on the SPEC acceptance scene #3
+(sphere-in-box, 40 frames 160x120, clean depth,
+seed 0), float32, then extracts the zero level set at 2 cm with the
+reference mesher (gs/mesher.py:148-151), culls it with the dataset's cameras
+(gs/mesher.py:234-272) and evaluates it against the analytic scene surface
+(gs/mesher.py:368-400).  The ground truth is the analytic SDF of the scene
+on the same 2 cm lattice through the same extraction and culling.
+
+scikit-image is not installed here, so, as in make_golden_mesh.py, the
+reference mesher's marching cubes is the oracle's (the generated table of
+paper_2206_14735_b200/mc_table.py); the GPU side uses the same table.
+
+tests/test_trained_mesh.py trains the B200 build for the same K with the
+same seed and compares its metrics with these.
+"""
+
+from __future__ import annotations
+
+import json
+import os
+import sys
+import tempfile
+import time
+import types
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, HERE)
+sys.path.insert(0, ROOT)
+
+from oracle import gridsurf_oracle as O  # noqa: E402
+
+_sk = types.ModuleType("skimage")
+_measure = types.ModuleType("skimage.measure")
+
+
+def _marching_cubes(vol, level=0.0, spacing=(1.0, 1.0, 1.0), method="lorensen"):
+    v, f = O.marching_cubes(vol, level, spacing)
+    return v, f, None, None
+
+
+_measure.marching_cubes = _marching_cubes
+_sk.measure = _measure
+sys.modules["skimage"] = _sk
+sys.modules["skimage.measure"] = _measure
+
+from gridsurf import camera, mesher, optimizer, scenegen  # noqa: E402
+
+ITERS = 200
+RES = 0.02
+FRAMES, W, H = 40, 160, 120
+
+
+def dataset():
+    f = 0.5 * W / np.tan(np.radians(35.0))  # gs/cli.py:144-147 (70 degree FOV)
+    intr = camera.Intrinsics(f, f, W / 2.0, H / 2.0, W, H)
+    return scenegen.render_dataset(scenegen.sphere_in_box(), scenegen.orbit_trajectory(FRAMES), intr,
+                                   threads=8)
+
+
+def gt_mesh(scene, lo, hi, res):
+    """The analytic scene surface on the mesher's lattice (gs/mesher.py:114-133)."""
+    dims = np.maximum((np.floor((hi - lo) / res)).astype(int) + 1, 2)
+    axes = [lo[a] + np.arange(dims[a]) * res for a in range(3)]
+    X, Y, Z = np.meshgrid(*axes, indexing="ij")
+    vol = scene.sdf(np.stack([X.ravel(), Y.ravel(), Z.ravel()], axis=1)).reshape(tuple(dims))
+    return mesher.mesh_from_sdf(vol.astype(np.float32), lo, res)
+
+
+def main():
+    t0 = time.time()
+    ds = dataset()
+    cfg = optimizer.TrainConfig(precision="single", iterations=ITERS, batch_rays=1024, seed=0,
+                                checkpoint_every=10 ** 9)
+    with tempfile.TemporaryDirectory() as d:
+        model, _ = optimizer.train(ds, cfg, d)
+        with open(os.path.join(d, "loss_log.csv")) as f:
+            log = f.read().splitlines()
+    t_train = time.time() - t0
+    mesh = mesher.extract_mesh(model, resolution=RES)
+    culled = mesher.cull_mesh(mesh, ds)
+    margin = 0.5 * model.grid.finest_voxel
+    lo, hi = model.grid.lo + margin, model.grid.hi - margin
+    gt = mesher.cull_mesh(gt_mesh(scenegen.sphere_in_box(), lo, hi, RES), ds)
+    rep = mesher.evaluate(culled, gt)
+    print(rep.table())
+    last = log[-1].split(",")
+    meta = dict(iters=ITERS, res=RES, frames=FRAMES, width=W, height=H, batch_rays=1024, seed=0,
+                precision="single", metrics=json.loads(rep.to_json()),
+                final_total=float(last[1]), first_total=float(log[1].split(",")[1]),
+                lo=list(map(float, model.grid.lo)), hi=list(map(float, model.grid.hi)),
+                gt_vertex_sum=float(gt.vertices.sum()), gt_faces=int(len(gt.faces)),
+                mesh_faces=int(len(culled.faces)), train_seconds=t_train)
+    out = {"meta_json": np.frombuffer(json.dumps(meta).encode(), dtype=np.uint8),
+           "loss_log": np.array([[float(x) for x in ln.split(",")] for ln in log[1:]])}
+    path = os.path.join(HERE, "trained_c3.npz")
+    np.savez_compressed(path, **out)
+    print(path, json.dumps(meta, indent=1))
+
+
+if __name__ == "__main__":
+    main()

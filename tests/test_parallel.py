@@ -400,3 +400,27 @@ def test_sharded_adam_device_world2_equals_single(tmp_path):
     # last-bit differences of near-zero gradients only up to lr
     assert np.abs(z["p_sh"] - z["p_1"]).max() <= 1e-9
     assert np.abs(z["m_sh"] - z["m_1"]).max() <= 1e-9 * max(np.abs(z["m_1"]).max(), 1e-300)
+
+
+def test_strong_split_rows_cover_the_global_batch():
+    """bench.py --strong: the global batch (BASELINE c3(i), M = 6144) split by
+    rows over N ranks covers every row once, in order, sizes within one, and
+    each rank's ray_base is its first global row (so its device PCG streams
+    start where the 1-GPU batch's rows do)."""
+    import numpy as np
+    from paper_2206_14735_b200.engine import HostDraws
+    from paper_2206_14735_b200.parallel import shard_draws, shard_rows
+    for m, world in [(6144, 1), (6144, 2), (6144, 3), (6145, 4), (6144, 8), (7, 8)]:
+        spans = [shard_rows(m, r, world) for r in range(world)]
+        assert spans[0][0] == 0 and spans[-1][1] == m
+        assert all(a[1] == b[0] for a, b in zip(spans[:-1], spans[1:]))
+        sizes = [hi - lo for lo, hi in spans]
+        assert max(sizes) - min(sizes) <= 1
+        ids = np.arange(m, dtype=np.int64) * 3
+        d = HostDraws(0, ids, np.zeros((2, 3)), None, [])
+        got = []
+        for r in range(world):
+            dr, kw = shard_draws(d, r, world)
+            assert kw["ray_base"] == spans[r][0] and kw["m_global"] == m
+            got.append(dr.ray_ids)
+        np.testing.assert_array_equal(np.concatenate(got), ids)
