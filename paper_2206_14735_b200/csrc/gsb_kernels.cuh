@@ -665,10 +665,10 @@ static __device__ void importance_group(const LaneGroup<G>& grp, const ImpRow& R
   grp.sync();
 }
 
-constexpr int kImpG = 8;              // lanes per ray (4 rays per warp)
-constexpr int kImpRaysPerBlock = 16;  // 128 threads
+constexpr int kImpG = 8;              // lanes per ray of the twin (4 rays per warp)
+constexpr int kImpRaysPerBlock = 128 / kImpG;
 
-template <typename T>
+template <typename T, int G>
 __global__ void __launch_bounds__(128) k_importance_dev(Ws<T> w, int M, int K, int A, int ray_base,
                                                         const double* __restrict__ dep,
                                                         const double* __restrict__ phi,
@@ -679,11 +679,10 @@ __global__ void __launch_bounds__(128) k_importance_dev(Ws<T> w, int M, int K, i
                                                         int32_t* __restrict__ evl_count, int64_t cap,
                                                         int want_list, int count_final, double trunc,
                                                         const uint64_t* __restrict__ row_states) {
-  constexpr int G = kImpG;
   extern __shared__ __align__(16) unsigned char imp_smem[];
   const LaneGroup<G> grp;
   const int gid = threadIdx.x / G;  // ray slot in the block
-  const int i = blockIdx.x * kImpRaysPerBlock + gid;
+  const int i = blockIdx.x * (128 / G) + gid;
   const int n = K + A;
   if (i >= M) return;  // group-uniform
   const ImpRow R = imp_row(imp_smem + (size_t)gid * imp_row_bytes(n, A), n, A);

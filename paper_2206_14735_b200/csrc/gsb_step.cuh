@@ -106,6 +106,35 @@ inline DetLayout det_layout(const host::Sizes& z, int nl) {
   return L;
 }
 
+// lanes per ray of the importance rounds (GSB_IMP_G: 8, 16 or 32)
+inline int imp_group() {
+  static const int v = [] {
+    const char* e = std::getenv("GSB_IMP_G");
+    const int g = e ? std::atoi(e) : 32;
+    return (g == 8 || g == 16) ? g : 32;
+  }();
+  return v;
+}
+template <typename T>
+inline cudaError_t launch_importance(int G, Ws<T> w, int M, int K, int A, int ray_base, const double* dep,
+                                     const double* phi, double* dep_out, double* phi_out, const T* log_s,
+                                     gsb_pcg64_t rng, int want_list, int count_final, double trunc,
+                                     const uint64_t* row_states, cudaStream_t stream) {
+  const int rpb = 128 / G;
+  const size_t smem = (size_t)rpb * imp_row_bytes(K + A, A);
+  auto go = [&](auto kern) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    kern<<<(M + rpb - 1) / rpb, 128, smem, stream>>>(w, M, K, A, ray_base, dep, phi, dep_out, phi_out, log_s,
+                                                      rng, w.evl, w.evl_count, w.evl_cap, want_list,
+                                                      count_final, trunc, row_states);
+    return cudaGetLastError();
+  };
+  if (G == 8) return go(k_importance_dev<T, 8>);
+  if (G == 16) return go(k_importance_dev<T, 16>);
+  return go(k_importance_dev<T, 32>);
+}
+
 // persistent tcgen05 SDF evaluation over `cap` (upper bound of) samples
 template <class S>
 inline cudaError_t launch_sdf_t5(Ws<float> w, Geo G, int M, int Nc, const double* dep, double* phi,
@@ -195,13 +224,10 @@ int run_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step
       for (int rnd = 0; rnd < R; ++rnd) {
         const bool need_phi = rnd < R - 1;
         GSB_CHECK(cudaMemsetAsync(w.evl_count, 0, sizeof(int32_t), stream));
-        const size_t imp_smem = (size_t)kImpRaysPerBlock * imp_row_bytes(K + A, A);
-        GSB_CHECK(cudaFuncSetAttribute(k_importance_dev<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)imp_smem));
-        k_importance_dev<T><<<(M + kImpRaysPerBlock - 1) / kImpRaysPerBlock, 128, imp_smem, stream>>>(
-            w, M, K, A, st->ray_base, w.dep[cur], w.phi[cur], w.dep[1 - cur], w.phi[1 - cur],
-            log_s, st->rng_importance[rnd], w.evl, w.evl_count, w.evl_cap, need_phi ? 1 : 0,
-            rnd == R - 1 ? 1 : 0, st->truncation, w.imp_state + (int64_t)rnd * M * 2);
+        GSB_CHECK(launch_importance<T>(imp_group(), w, M, K, A, st->ray_base, w.dep[cur], w.phi[cur],
+                                       w.dep[1 - cur], w.phi[1 - cur], log_s, st->rng_importance[rnd],
+                                       need_phi ? 1 : 0, rnd == R - 1 ? 1 : 0, st->truncation,
+                                       w.imp_state + (int64_t)rnd * M * 2, stream));
         GSB_LAUNCHED_T("k_importance_dev");
         if (need_phi) {
           int64_t cap = (int64_t)M * A;
