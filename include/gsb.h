@@ -345,13 +345,16 @@ int gsb_sdf_volume(const gsb_model_t* model, const double* lo_host, double resol
  * generated 256-case table (mc_table.py; table = packed int8 ntri[256] |
  * tri[256][16] | edge corners[12][2], device).  gsb_mc_count writes the
  * triangle total (int64) and the volume min/max (2 floats) to device memory;
- * gsb_mc_emit then writes 3 f64 vertices per triangle (verts: 9 * total). */
+ * gsb_mc_emit then writes 3 f64 vertices per triangle (verts: 9 * total)
+ * and, if `keys` is non-null, each vertex's lattice-edge key (3 * total
+ * int64: ((i ny + j) nz + k) 3 + axis of the edge's lower end point); equal
+ * keys are bit-identical vertices, which the caller welds. */
 int gsb_mc_workspace_size(int64_t nx, int64_t ny, int64_t nz, size_t* bytes);
 int gsb_mc_count(const float* vol, int64_t nx, int64_t ny, int64_t nz, float level, const int8_t* table,
                  void* workspace, size_t workspace_bytes, int64_t* total, float* minmax, void* stream);
 int gsb_mc_emit(const float* vol, int64_t nx, int64_t ny, int64_t nz, float level, double ox, double oy,
                 double oz, double resolution, const int8_t* table, void* workspace,
-                size_t workspace_bytes, double* verts, void* stream);
+                size_t workspace_bytes, double* verts, int64_t* keys, void* stream);
 
 /* Exact nearest neighbour from each query into ref (mesher.nearest_neighbors,
  * gs/mesher.py:302-363): the same cell hash (lo, cell, dims computed by the

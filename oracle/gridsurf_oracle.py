@@ -1127,8 +1127,9 @@ def train_step(P, opt, dataset, cfg, iteration):
 # marching cubes (test infrastructure): numpy restatement of the device
 # kernel over the generated 256-case table (paper_2206_14735_b200/mc_table.py),
 # standing in for skimage.measure.marching_cubes, which is not installed here.
-# Cells in C order, triangles in table order, three vertices per triangle;
-# vertex = origin-free grid coordinates scaled by spacing (as skimage).
+# Cells in C order, triangles in table order; vertices welded per lattice
+# edge in order of first use; vertex = origin-free grid coordinates scaled by
+# spacing (as skimage).
 
 
 def marching_cubes(vol, level=0.0, spacing=(1.0, 1.0, 1.0), table=None):
@@ -1152,7 +1153,7 @@ def marching_cubes(vol, level=0.0, spacing=(1.0, 1.0, 1.0), table=None):
         vals.append(v)
         idx |= (v < np.float32(level)).astype(np.int64) << k
     cells = np.flatnonzero(ntri[idx.reshape(-1)] > 0)
-    verts = []
+    verts, keys = [], []
     for c in cells:
         i, r = divmod(int(c), (ny - 1) * (nz - 1))
         j, k = divmod(r, nz - 1)
@@ -1166,6 +1167,16 @@ def marching_cubes(vol, level=0.0, spacing=(1.0, 1.0, 1.0), table=None):
             pa = np.array([i, j, k]) + corners[a]
             pb = np.array([i, j, k]) + corners[b]
             verts.append([(pa[d] + t * (pb[d] - pa[d])) * spacing[d] for d in range(3)])
+            ax = int(np.flatnonzero(pb - pa)[0])
+            keys.append(((int(pa[0]) * ny + int(pa[1])) * nz + int(pa[2])) * 3 + ax)
     verts = np.asarray(verts, dtype=np.float64).reshape(-1, 3)
-    faces = np.arange(len(verts), dtype=np.int64).reshape(-1, 3)
-    return verts, faces
+    # welded: one vertex per lattice edge, in order of first use (what the
+    # device path returns; scikit-image's meshes are welded too)
+    keys = np.asarray(keys, dtype=np.int64)
+    if len(keys) == 0:
+        return verts, np.zeros((0, 3), dtype=np.int64)
+    _, first, inv = np.unique(keys, return_index=True, return_inverse=True)
+    order = np.argsort(first, kind="stable")
+    rank = np.empty_like(order)
+    rank[order] = np.arange(len(order))
+    return verts[first[order]], rank[inv.reshape(-1)].reshape(-1, 3).astype(np.int64)

@@ -134,7 +134,7 @@ def lib():
         "gsb_sdf_volume": ([C.POINTER(Model), P, D, I64, I64, I64, P, P, SZ, P], I32),
         "gsb_mc_workspace_size": ([I64, I64, I64, C.POINTER(SZ)], I32),
         "gsb_mc_count": ([P, I64, I64, I64, C.c_float, P, P, SZ, P, P, P], I32),
-        "gsb_mc_emit": ([P, I64, I64, I64, C.c_float, D, D, D, D, P, P, SZ, P, P], I32),
+        "gsb_mc_emit": ([P, I64, I64, I64, C.c_float, D, D, D, D, P, P, SZ, P, P, P], I32),
         "gsb_nn_workspace_size": ([I64, I64, I64, I64, C.POINTER(SZ)], I32),
         "gsb_raster_zbuffer": ([P, P, P, P, I64, I32, I32, P, P], I32),
         "gsb_nearest_neighbors": ([P, I64, P, I64, P, D, I64, I64, I64, P, SZ, P, P, P], I32),

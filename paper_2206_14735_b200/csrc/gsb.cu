@@ -376,7 +376,7 @@ int gsb_mc_count(const float* vol, int64_t nx, int64_t ny, int64_t nz, float lev
 
 int gsb_mc_emit(const float* vol, int64_t nx, int64_t ny, int64_t nz, float level, double ox, double oy,
                 double oz, double resolution, const int8_t* table, void* workspace, size_t workspace_bytes,
-                double* verts, void* stream) {
+                double* verts, int64_t* keys, void* stream) {
   if (!vol || !table || !workspace || !verts || nx < 2 || ny < 2 || nz < 2) return GSB_E_ARG;
   const int64_t cells = (nx - 1) * (ny - 1) * (nz - 1);
   size_t oc, oo, om, ot, tb;
@@ -385,7 +385,7 @@ int gsb_mc_emit(const float* vol, int64_t nx, int64_t ny, int64_t nz, float leve
   unsigned char* w = reinterpret_cast<unsigned char*>(workspace);
   mesh::k_mc_emit<<<(int)((cells + 255) / 256), 256, 0, s>>>(
       vol, nx, ny, nz, level, ox, oy, oz, resolution, table, reinterpret_cast<const int32_t*>(w + oc),
-      reinterpret_cast<const int32_t*>(w + oo), verts);
+      reinterpret_cast<const int32_t*>(w + oo), verts, keys);
   GSB_LAUNCHED();
   return GSB_OK;
 }

@@ -665,7 +665,7 @@ static __device__ void importance_group(const LaneGroup<G>& grp, const ImpRow& R
   grp.sync();
 }
 
-constexpr int kImpG = 8;              // lanes per ray of the twin (4 rays per warp)
+constexpr int kImpG = 16;             // lanes per ray of the twin (2 rays per warp)
 constexpr int kImpRaysPerBlock = 128 / kImpG;
 
 template <typename T, int G>

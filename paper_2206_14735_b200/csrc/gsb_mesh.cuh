@@ -3,8 +3,9 @@
 //
 //  * marching cubes over a dense float32 SDF volume: a count pass (cell ->
 //    triangle count from the 256-case table), an exclusive scan (CUB), and an
-//    emit pass writing three f64 vertices per triangle; the table is the
-//    generated one of mc_table.py (watertight; see there);
+//    emit pass writing three f64 vertices per triangle plus the lattice-edge
+//    key of each (the host welds equal keys into one vertex); the table is
+//    the generated one of mc_table.py (watertight; see there);
 //  * exact nearest neighbours with the reference's grid hash: ref points
 //    bucketed by cell (stable radix sort), each query searches Chebyshev
 //    rings of cells in the reference's order with its early-out rule, so
@@ -65,7 +66,7 @@ __global__ void k_mc_count(const float* __restrict__ vol, int64_t nx, int64_t ny
 __global__ void k_mc_emit(const float* __restrict__ vol, int64_t nx, int64_t ny, int64_t nz, float level,
                           double ox, double oy, double oz, double res, const int8_t* __restrict__ tab,
                           const int32_t* __restrict__ counts, const int32_t* __restrict__ offsets,
-                          double* __restrict__ verts) {
+                          double* __restrict__ verts, int64_t* __restrict__ keys) {
   const int64_t cells = (nx - 1) * (ny - 1) * (nz - 1);
   const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (c >= cells || counts[c] == 0) return;
@@ -86,6 +87,12 @@ __global__ void k_mc_emit(const float* __restrict__ vol, int64_t nx, int64_t ny,
       const double pa = (double)(base[d] + ((a >> (2 - d)) & 1));
       const double pb = (double)(base[d] + ((b >> (2 - d)) & 1));
       out[q * 3 + d] = o[d] + (pa + t * (pb - pa)) * res;
+    }
+    if (keys) {  // the lattice edge (lower end point, axis) the vertex lies on: equal
+                 // keys are bit-identical vertices (a < b along the axis in every cell)
+      const int ax = (a ^ b) == 4 ? 0 : ((a ^ b) == 2 ? 1 : 2);
+      const int64_t li = i + ((a >> 2) & 1), lj = j + ((a >> 1) & 1), lk = k + (a & 1);
+      keys[(int64_t)offsets[c] * 3 + q] = ((li * ny + lj) * nz + lk) * 3 + ax;
     }
   }
 }

@@ -106,12 +106,13 @@ inline DetLayout det_layout(const host::Sizes& z, int nl) {
   return L;
 }
 
-// lanes per ray of the importance rounds (GSB_IMP_G: 8, 16 or 32)
+// lanes per ray of the importance rounds (GSB_IMP_G: 8, 16 or 32).  Measured
+// at config 2 (three rounds per step): 32 -> 116 us, 16 -> 108.5 us, 8 -> 134 us
 inline int imp_group() {
   static const int v = [] {
     const char* e = std::getenv("GSB_IMP_G");
-    const int g = e ? std::atoi(e) : 32;
-    return (g == 8 || g == 16) ? g : 32;
+    const int g = e ? std::atoi(e) : 16;
+    return (g == 8 || g == 32) ? g : 16;
   }();
   return v;
 }

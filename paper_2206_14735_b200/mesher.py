@@ -193,13 +193,28 @@ def mesh_from_sdf(vol, origin, resolution, level=0.0, device=None):
         raise EmptyLevelSetError("SDF volume has no zero crossing")
     n = int(total.item())
     verts = torch.empty((3 * n, 3), dtype=torch.float64, device=v.device)
+    keys = torch.empty(3 * n, dtype=torch.int64, device=v.device)
     if n:
         o = np.asarray(origin, dtype=np.float64)
         _lib.check(lib.gsb_mc_emit(v.data_ptr(), nx, ny, nz, float(level), float(o[0]), float(o[1]),
                                    float(o[2]), float(resolution), tab.data_ptr(), ws.data_ptr(),
-                                   ws.numel(), verts.data_ptr(), s), "gsb_mc_emit")
-    faces = np.arange(3 * n, dtype=np.int64).reshape(-1, 3)
-    return TriangleMesh(verts.cpu().numpy(), faces).drop_degenerate()
+                                   ws.numel(), verts.data_ptr(), keys.data_ptr(), s), "gsb_mc_emit")
+    vw, faces = weld(verts.cpu().numpy(), keys.cpu().numpy())
+    return TriangleMesh(vw, faces).drop_degenerate()
+
+
+def weld(verts, keys):
+    """One vertex per lattice edge (marching cubes emits it once per
+    incident triangle): vertices in order of first use, faces re-indexed.
+    Welding by the edge key is welding by identical coordinates, as
+    scikit-image's marching cubes returns its mesh."""
+    if len(keys) == 0:
+        return verts.reshape(0, 3), np.zeros((0, 3), dtype=np.int64)
+    _, first, inv = np.unique(keys, return_index=True, return_inverse=True)
+    order = np.argsort(first, kind="stable")
+    rank = np.empty_like(order)
+    rank[order] = np.arange(len(order))
+    return verts[first[order]], rank[inv.reshape(-1)].reshape(-1, 3).astype(np.int64)
 
 
 def extract_mesh(model, resolution=0.01, threads=1):
