@@ -17,8 +17,9 @@ scikit-image is not installed here, so, as in make_golden_mesh.py, the
 reference mesher's marching cubes is the oracle's (the generated table of
 paper_2206_14735_b200/mc_table.py); the GPU side uses the same table.
 
-tests/test_trained_mesh.py trains the B200 build for the same K with the
-same seed and compares its metrics with these.
+Metrics are recorded at iterations 200 (still converging) and 2000 (the
+SPEC's run length) from the run's own checkpoints.  tests/test_trained_mesh.py
+trains the B200 build the same way and compares its metrics with these.
 """
 
 from __future__ import annotations
@@ -55,7 +56,8 @@ sys.modules["skimage.measure"] = _measure
 
 from gridsurf import camera, mesher, optimizer, scenegen  # noqa: E402
 
-ITERS = 200
+ITERS = 2000
+EVAL_AT = (200, 2000)  # checkpoints evaluated
 RES = 0.02
 FRAMES, W, H = 40, 160, 120
 
@@ -80,26 +82,29 @@ def main():
     t0 = time.time()
     ds = dataset()
     cfg = optimizer.TrainConfig(precision="single", iterations=ITERS, batch_rays=1024, seed=0,
-                                checkpoint_every=10 ** 9)
+                                checkpoint_every=EVAL_AT[0])
+    per_it = {}
     with tempfile.TemporaryDirectory() as d:
         model, _ = optimizer.train(ds, cfg, d)
+        t_train = time.time() - t0
         with open(os.path.join(d, "loss_log.csv")) as f:
             log = f.read().splitlines()
-    t_train = time.time() - t0
-    mesh = mesher.extract_mesh(model, resolution=RES)
-    culled = mesher.cull_mesh(mesh, ds)
-    margin = 0.5 * model.grid.finest_voxel
-    lo, hi = model.grid.lo + margin, model.grid.hi - margin
-    gt = mesher.cull_mesh(gt_mesh(scenegen.sphere_in_box(), lo, hi, RES), ds)
-    rep = mesher.evaluate(culled, gt)
-    print(rep.table())
-    last = log[-1].split(",")
-    meta = dict(iters=ITERS, res=RES, frames=FRAMES, width=W, height=H, batch_rays=1024, seed=0,
-                precision="single", metrics=json.loads(rep.to_json()),
-                final_total=float(last[1]), first_total=float(log[1].split(",")[1]),
+        margin = 0.5 * model.grid.finest_voxel
+        lo, hi = model.grid.lo + margin, model.grid.hi - margin
+        gt = mesher.cull_mesh(gt_mesh(scenegen.sphere_in_box(), lo, hi, RES), ds)
+        for it in EVAL_AT:
+            m, _, _, _ = optimizer.load_model(os.path.join(d, f"ckpt_{it:06d}.gsck"))
+            culled = mesher.cull_mesh(mesher.extract_mesh(m, resolution=RES), ds)
+            rep = mesher.evaluate(culled, gt)
+            print(it, rep.table(), flush=True)
+            per_it[str(it)] = dict(metrics=json.loads(rep.to_json()), mesh_faces=int(len(culled.faces)),
+                                   total=float(log[it].split(",")[1]))
+    meta = dict(iters=ITERS, eval_at=list(EVAL_AT), res=RES, frames=FRAMES, width=W, height=H,
+                batch_rays=1024, seed=0, precision="single", per_iteration=per_it,
+                first_total=float(log[1].split(",")[1]),
                 lo=list(map(float, model.grid.lo)), hi=list(map(float, model.grid.hi)),
-                gt_vertex_sum=float(gt.vertices.sum()), gt_faces=int(len(gt.faces)),
-                mesh_faces=int(len(culled.faces)), train_seconds=t_train)
+                gt_vertex_sum=float(gt.vertices[gt.faces].sum()), gt_faces=int(len(gt.faces)),
+                train_seconds=t_train)
     out = {"meta_json": np.frombuffer(json.dumps(meta).encode(), dtype=np.uint8),
            "loss_log": np.array([[float(x) for x in ln.split(",")] for ln in log[1:]])}
     path = os.path.join(HERE, "trained_c3.npz")

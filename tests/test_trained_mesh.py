@@ -2,21 +2,25 @@
 reference's Chamfer / F-score / normal consistency on the same synthetic scene.
 
 * Parity (tests/golden/make_golden_trained.py): the reference's own train()
-  (gs/optimizer.py:334-391, sphere pre-fit + K = 200 iterations, float32,
+  (gs/optimizer.py:334-391: sphere pre-fit, then 2000 iterations, float32,
   seed 0) on SPEC acceptance scene #3 (/root/reference/SPEC.md:702:
-  sphere-in-box, 40 frames 160x120, clean depth), mesh extracted at 2 cm
-  (gs/mesher.py:148-151), culled (gs/mesher.py:234-272) and evaluated
-  against the analytic surface (gs/mesher.py:368-400).  The device run does
-  the same through this package's train() / mesher; its metrics must be
-  within MESH_TOL of the reference's.  Runs are not bit-identical (atomic
-  summation order in float32), so the comparison is at the metric level.
+  sphere-in-box, 40 frames 160x120, clean depth); meshes of its checkpoints
+  at iterations 200 and 2000 extracted at 2 cm (gs/mesher.py:148-151),
+  culled (gs/mesher.py:234-272) and evaluated against the analytic surface
+  (gs/mesher.py:368-400).  The device run does the same through this
+  package's train() / mesher; its metrics must be within MESH_TOL of the
+  reference's at each checkpoint.  Runs are not bit-identical (float32
+  summation orders, and Adam turns near-zero gradients into +-lr steps), so
+  the comparison is at the metric level, looser while the surface is still
+  converging.
 * SPEC #3 absolute criteria at 2000 iterations and the default 1 cm
-  extraction: C-l1 < 1 cm, NC > 0.95, F-score@5cm > 0.98.
+  extraction: C-l1 < 1 cm, NC > 0.95, F-score@5cm > 0.98, and the total loss
+  falls >= 10x (SPEC.md:503).
 
 The ground-truth surface is the analytic scene SDF (oracle/scene_host.py,
 the numpy evaluation of the same CSG program the renderer traces) on the
-extraction lattice, through the same marching cubes and culling; its
-vertex checksum must equal the reference run's.
+extraction lattice, through the same marching cubes and culling; its face
+count and vertex checksum equal the reference run's.
 """
 
 import json
@@ -32,9 +36,13 @@ sys.path.insert(0, os.path.dirname(HERE))
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
-# |ours - reference| per metric (K = 200: the surface is still converging)
-MESH_TOL = {"chamfer_l1": 2e-3, "accuracy": 3e-3, "completion": 3e-3, "normal_consistency": 0.02,
-            "f_score": 0.02}
+# |ours - reference| per metric and checkpoint: (absolute, relative) -- either passes
+MESH_TOL = {
+    200: {"chamfer_l1": (5e-3, 0.25), "accuracy": (5e-3, 0.25), "completion": (1e-2, 0.25),
+          "normal_consistency": (0.05, 0.0), "f_score": (0.08, 0.0)},
+    2000: {"chamfer_l1": (2e-3, 0.2), "accuracy": (2e-3, 0.2), "completion": (2e-3, 0.2),
+           "normal_consistency": (0.02, 0.0), "f_score": (0.02, 0.0)},
+}
 
 
 def golden():
@@ -60,43 +68,62 @@ def gt_mesh(model, res, ds):
     prog = scene_host.flatten(scenes.sphere_in_box().root)
     vol = scene_host.evaluate(prog, np.stack([X.ravel(), Y.ravel(), Z.ravel()], axis=1))
     gt = mesher.mesh_from_sdf(vol.reshape(tuple(dims)).astype(np.float32), lo, res)
-    return gt, mesher.cull_mesh(gt, ds)
+    return mesher.cull_mesh(gt, ds)
 
 
-def train_and_evaluate(tmp_path, iters, res, precision="single"):
-    from paper_2206_14735_b200 import mesher, optimizer
-    ds = scene_dataset()
-    cfg = optimizer.TrainConfig(precision=precision, iterations=iters, batch_rays=1024, seed=0,
-                                checkpoint_every=10 ** 9)
-    model, _ = optimizer.train(ds, cfg, str(tmp_path))
-    with open(os.path.join(str(tmp_path), "loss_log.csv")) as f:
+@pytest.fixture(scope="module")
+def trained(tmp_path_factory):
+    """One 2000-iteration float32 run with checkpoints every 200 iterations."""
+    from paper_2206_14735_b200 import optimizer
+    meta, _ = golden()
+    out = str(tmp_path_factory.mktemp("trained"))
+    ds = scene_dataset(meta["frames"], meta["width"], meta["height"])
+    cfg = optimizer.TrainConfig(precision="single", iterations=meta["iters"], batch_rays=meta["batch_rays"],
+                                seed=meta["seed"], checkpoint_every=meta["eval_at"][0])
+    model, _ = optimizer.train(ds, cfg, out)
+    with open(os.path.join(out, "loss_log.csv")) as f:
         log = np.array([[float(x) for x in ln.split(",")] for ln in f.read().splitlines()[1:]])
-    mesh = mesher.cull_mesh(mesher.extract_mesh(model, resolution=res), ds)
-    _, gt = gt_mesh(model, res, ds)
-    return model, log, gt, mesher.evaluate(mesh, gt)
+    return ds, out, model, log
 
 
-def test_trained_mesh_matches_reference(tmp_path):
+def _close(got, ref, tol):
+    ab, rel = tol
+    return abs(got - ref) <= max(ab, rel * abs(ref))
+
+
+def test_trained_mesh_matches_reference(trained):
+    from paper_2206_14735_b200 import mesher, optimizer
+    ds, out, model, log = trained
     meta, ref_log = golden()
-    model, log, gt, rep = train_and_evaluate(tmp_path, meta["iters"], meta["res"])
     np.testing.assert_array_equal(model.grid.lo, meta["lo"])
     np.testing.assert_array_equal(model.grid.hi, meta["hi"])
+    gt = gt_mesh(model, meta["res"], ds)
     # same ground truth as the reference run (same lattice, SDF, extraction, culling)
     assert len(gt.faces) == meta["gt_faces"]
-    assert abs(gt.vertices.sum() - meta["gt_vertex_sum"]) <= 1e-9 * abs(meta["gt_vertex_sum"])
-    ref = meta["metrics"]
-    got = json.loads(rep.to_json())
-    print("ours", {k: round(got[k], 5) for k in MESH_TOL}, "reference", {k: round(ref[k], 5) for k in MESH_TOL})
-    bad = {k: (got[k], ref[k]) for k, tol in MESH_TOL.items() if not abs(got[k] - ref[k]) <= tol}
-    assert not bad, bad
-    # the loss curves agree too (same batches; float32 run-to-run noise only)
+    assert abs(gt.vertices[gt.faces].sum() - meta["gt_vertex_sum"]) <= 1e-9 * abs(meta["gt_vertex_sum"])
     assert log.shape == ref_log.shape
-    assert abs(log[-1, 1] - ref_log[-1, 1]) <= 0.05 * abs(ref_log[-1, 1])
+    bad = {}
+    for it in meta["eval_at"]:
+        m, _, it_ck, _ = optimizer.load_model(os.path.join(out, f"ckpt_{it:06d}.gsck"))
+        assert it_ck == it
+        rep = mesher.evaluate(mesher.cull_mesh(mesher.extract_mesh(m, resolution=meta["res"]), ds), gt)
+        got = json.loads(rep.to_json())
+        ref = meta["per_iteration"][str(it)]["metrics"]
+        print(it, "ours", {k: round(got[k], 5) for k in MESH_TOL[it]},
+              "reference", {k: round(ref[k], 5) for k in MESH_TOL[it]})
+        bad.update({(it, k): (got[k], ref[k]) for k, tol in MESH_TOL[it].items()
+                    if not _close(got[k], ref[k], tol)})
+    assert not bad, bad
+    # the loss curves agree (same batches; float32 run-to-run noise only)
+    assert abs(log[-1, 1] - ref_log[-1, 1]) <= 0.1 * abs(ref_log[-1, 1])
 
 
-def test_spec3_end_to_end_reconstruction(tmp_path):
+def test_spec3_end_to_end_reconstruction(trained):
     """/root/reference/SPEC.md:702 acceptance #3 at the default extraction (1 cm)."""
-    _, log, _, rep = train_and_evaluate(tmp_path, 2000, 0.01)
+    from paper_2206_14735_b200 import mesher
+    ds, _, model, log = trained
+    gt = gt_mesh(model, 0.01, ds)
+    rep = mesher.evaluate(mesher.cull_mesh(mesher.extract_mesh(model, resolution=0.01), ds), gt)
     print(rep.table())
     assert rep.chamfer_l1 < 0.01
     assert rep.normal_consistency > 0.95
