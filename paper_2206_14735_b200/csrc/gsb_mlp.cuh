@@ -151,6 +151,49 @@ __device__ __forceinline__ void gather_fast(const LevelDev& L, const LocT<T>& q,
   }
 }
 
+// gather_fast plus the level's spatial Jacobian of the features,
+// J[c][a] = d/dfrac_a sum_k w_k theta_k[c] (grid units; gs/diffcore.py:844-871
+// before the 1/vs), from the same corner rows: grad phi then needs
+// g . J instead of a second read of the corners
+template <typename T, int C>
+__device__ __forceinline__ void gather_jac(const LevelDev& L, const LocT<T>& q, T* out, T (&J)[3 * C]) {
+  const T* F = reinterpret_cast<const T*>(L.feat) + (int64_t)q.base * C;
+  T w[8];
+  corner_w(q, w);
+  T r[8][C];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) load_row<T, C>(F + corner_off(L, k) * C, r[k]);
+  const T x1 = q.fx, y1 = q.fy, z1 = q.fz;
+  const T x0 = T(1) - x1, y0 = T(1) - y1, z0 = T(1) - z1;
+#pragma unroll
+  for (int c = 0; c < C; ++c) {
+    T acc = T(0);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) acc = fma(w[k], r[k][c], acc);
+    out[c] = acc;
+    J[3 * c + 0] = (r[4][c] - r[0][c]) * (y0 * z0) + (r[5][c] - r[1][c]) * (y0 * z1) +
+                   (r[6][c] - r[2][c]) * (y1 * z0) + (r[7][c] - r[3][c]) * (y1 * z1);
+    J[3 * c + 1] = (r[2][c] - r[0][c]) * (x0 * z0) + (r[3][c] - r[1][c]) * (x0 * z1) +
+                   (r[6][c] - r[4][c]) * (x1 * z0) + (r[7][c] - r[5][c]) * (x1 * z1);
+    J[3 * c + 2] = (r[1][c] - r[0][c]) * (x0 * y0) + (r[3][c] - r[2][c]) * (x0 * y1) +
+                   (r[5][c] - r[4][c]) * (x1 * y0) + (r[7][c] - r[6][c]) * (x1 * y1);
+  }
+}
+
+// grad phi contribution g . J / vs of a level whose Jacobian was kept
+template <typename T, int C>
+__device__ __forceinline__ void level_dx_jac(const LevelDev& L, const T (&J)[3 * C], const T* gl,
+                                             T (&gr)[3]) {
+  const T iv = (T)L.inv_vs;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    T acc = T(0);
+#pragma unroll
+    for (int c = 0; c < C; ++c) acc = fma(gl[c], J[3 * c + a], acc);
+    gr[a] += acc * iv;
+  }
+}
+
 // d/dx <interp(theta, x), g>  (gs/diffcore.py:844-871)
 template <typename T, int C>
 __device__ __forceinline__ void level_dx_fast(const LevelDev& L, const LocT<T>& q, const T* gl,

@@ -25,6 +25,10 @@ using tc::smem_u32;
 constexpr int kTile = 128;         // samples per CTA = TMEM lanes
 constexpr int kCtaPerSm = 4;       // 128 TMEM columns each: 4 x 128 = 512
 constexpr uint32_t kCols = 128;
+// taped forward: TMEM columns D [0, 32), A hi / lo [32, 96), and the two
+// finest levels' spatial Jacobians [96, 128)
+constexpr int kJacLevels = 2;
+constexpr uint32_t kJacCol = 96;
 
 // kind::tf32, D f32, A/B K-major, M = 128, N = 32 (or 16)
 __host__ __device__ constexpr uint32_t idesc(uint32_t n) {
@@ -110,6 +114,16 @@ __device__ __forceinline__ void ld16(uint32_t ta, float (&v)[16]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ void ld8(uint32_t ta, float (&v)[8]) {
+  uint32_t r[8];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(ta)
+               : "memory");
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
 }
 // hi = x rounded to tf32 (half away at bit 13); lo = x - hi exact (the tensor
 // core reads its top 19 bits)
@@ -378,6 +392,15 @@ __global__ void __launch_bounds__(kTile, kCtaPerSm) k_fwd_t5(Ws<float> w, Geo G,
       if (w.dbg & 8) {
 #pragma unroll
         for (int c = 0; c < S::CG; ++c) z[l * S::CG + c] = 1e-3f * (float)c + loc[l].fx;
+      } else if (l >= S::NL - kJacLevels && S::CG == 4) {
+        // the two finest levels keep their spatial Jacobian (this lane's
+        // TMEM columns [96, 128), 16 per level, 12 used) so grad phi does
+        // not re-read their corners
+        float J[16];
+        gather_jac<float, S::CG>(G.lv[l], loc[l], z + l * S::CG, reinterpret_cast<float(&)[3 * S::CG]>(J));
+#pragma unroll
+        for (int i = 3 * S::CG; i < 16; ++i) J[i] = 0.f;
+        st16(tl + kJacCol + 16 * (l - (S::NL - kJacLevels)), J);
       } else {
         gather_fast<float, S::CG>(G.lv[l], loc[l], z + l * S::CG);
       }
@@ -438,8 +461,16 @@ __global__ void __launch_bounds__(kTile, kCtaPerSm) k_fwd_t5(Ws<float> w, Geo G,
     ld16(tl, gz);
     float gr[3] = {0.f, 0.f, 0.f};
 #pragma unroll
-    for (int l = 0; l < S::NL; ++l)
-      if (!(w.dbg & 72)) level_dx_fast<float, S::CG>(G.lv[l], loc[l], gz + l * S::CG, gr);
+    for (int l = 0; l < S::NL; ++l) {
+      if (w.dbg & 72) continue;
+      if (l >= S::NL - kJacLevels && S::CG == 4) {
+        float J[16];
+        ld16(tl + kJacCol + 16 * (l - (S::NL - kJacLevels)), J);
+        level_dx_jac<float, S::CG>(G.lv[l], reinterpret_cast<const float(&)[3 * S::CG]>(J), gz + l * S::CG, gr);
+      } else {
+        level_dx_fast<float, S::CG>(G.lv[l], loc[l], gz + l * S::CG, gr);
+      }
+    }
     // ---- colour: sigmoid(MLP_c([f_c, r]))  (gs/decoders.py:86-99)
     store_a<KC>(tl, inp);
     run([&] { issue_layer<KC>(tmem, sa(U::C0H), sa(U::C0L)); });
