@@ -93,6 +93,7 @@ Ws<T> carve(void* ws, const Sizes& z, size_t* bytes, int64_t* off_parts = nullpt
   w.sphi = c.template take<T>(z.NS);
   w.sgphi = c.template take<T>(z.NS * 3);
   w.scol = c.template take<T>(z.MN * 3);
+  w.scolf = c.template take<T>(z.MN * 8);  // colour features (CC <= 8)
   w.pbar = c.template take<T>(z.NS);
   w.ubar = c.template take<T>(z.NS * 3);
   w.cbar = c.template take<T>(z.MN * 3);

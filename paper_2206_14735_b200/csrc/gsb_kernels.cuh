@@ -46,6 +46,8 @@ struct Ws {
   T* sphi;
   T* sgphi;
   T* scol;
+  T* scolf;             // float32 tcgen05 path: [MN][CC] colour-grid features of the taped samples
+                        // (k_fwd_t5 writes them, k_bwd_color_t5 reads them instead of re-gathering)
   T* pbar;
   T* ubar;
   T* cbar;

@@ -161,6 +161,9 @@ int run_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step
   size_t need = 0;
   Ws<T> w = carve<T>(st->workspace, z, &need);
   if (need > st->workspace_bytes) return GSB_E_ARG;
+  // the colour backward reads the colour features the taped forward kept
+  // only when both are the tcgen05 kernels (the A/B forms re-gather)
+  if (!(sizeof(T) == 4 && t5_fwd_mode() > 0 && use_t5_col())) w.scolf = nullptr;
   Geo G = geo_of(model, esz);
   T* params = reinterpret_cast<T*>(model->params);
   T* grads = reinterpret_cast<T*>(model->grads);
@@ -631,6 +634,9 @@ int run_pose_grad(const gsb_model_t* model, const gsb_dataset_t* data, const gsb
   size_t need = 0;
   Ws<T> w = carve<T>(st->workspace, z, &need);
   if (need > st->workspace_bytes) return GSB_E_ARG;
+  // the colour backward reads the colour features the taped forward kept
+  // only when both are the tcgen05 kernels (the A/B forms re-gather)
+  if (!(sizeof(T) == 4 && t5_fwd_mode() > 0 && use_t5_col())) w.scolf = nullptr;
   if (z.M == 0) return GSB_OK;
   const Geo G = geo_of(model, sizeof(T));
   const T* params = reinterpret_cast<const T*>(model->params);

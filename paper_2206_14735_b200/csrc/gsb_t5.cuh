@@ -472,6 +472,11 @@ __global__ void __launch_bounds__(kTile, kCtaPerSm) k_fwd_t5(Ws<float> w, Geo G,
       }
     }
     // ---- colour: sigmoid(MLP_c([f_c, r]))  (gs/decoders.py:86-99)
+    if (act && ray >= 0 && w.scolf) {  // the colour features, for the colour backward
+#pragma unroll
+      for (int c = 0; c < S::CC; c += 2)
+        *reinterpret_cast<float2*>(w.scolf + s * S::CC + c) = make_float2(inp[c], inp[c + 1]);
+    }
     store_a<KC>(tl, inp);
     run([&] { issue_layer<KC>(tmem, sa(U::C0H), sa(U::C0L)); });
     wait_d();
@@ -924,7 +929,7 @@ __global__ void __launch_bounds__(kTile, 2) k_bwd_color_t5(Ws<float> w, Geo G, i
   using K = ColT5;
   constexpr int KC = F::KC, ROW = K::ROW;
   constexpr int NCP = S::NMLP - S::NG, o = S::NG;
-  static_assert(S::IN_C + 1 <= 16 && 8 * KC <= 16 && S::CC <= 8, "colour input width");
+  static_assert(S::IN_C + 1 <= 16 && 8 * KC <= 16 && S::CC <= 8 && S::CC % 2 == 0, "colour input width");
   static_assert(S::oCb0 == S::oCW0 + S::IN_C * GSB_HID, "db0c is the ones row of dW0c");
   extern __shared__ __align__(128) float t5_smem[];
   float* sw = t5_smem - K::W0;  // indexed by UmmaW offsets
@@ -1003,6 +1008,14 @@ __global__ void __launch_bounds__(kTile, 2) k_bwd_color_t5(Ws<float> w, Geo G, i
       if (w.dbg & 8) {
 #pragma unroll
         for (int c = 0; c < S::CC; ++c) inp[c] = 1e-3f * (float)c + q.fx;
+      } else if (w.scolf) {  // kept by the taped forward (the same gather, bit for bit)
+#pragma unroll
+        for (int c = 0; c < S::CC; c += 2) {
+          const float2 f = active ? *reinterpret_cast<const float2*>(w.scolf + s * S::CC + c)
+                                  : make_float2(0.f, 0.f);
+          inp[c] = f.x;
+          inp[c + 1] = f.y;
+        }
       } else {
         gather_fast<float, S::CC>(G.col, q, inp);
       }
