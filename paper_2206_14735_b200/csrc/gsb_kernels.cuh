@@ -1211,7 +1211,7 @@ __device__ __forceinline__ void det_put(uint64_t* keys, T* vals, int64_t slot, c
 
 template <typename T, int C>
 __device__ __forceinline__ void scatter_level(const LevelDev& L, const LocT<T>& q, const T* gl,
-                                              const T (&coef)[8], bool active, bool /*unused*/,
+                                              const T (&coef)[8], bool active, bool no_merge,
                                               uint64_t* dkeys = nullptr, T* dvals = nullptr,
                                               int64_t dslot = 0) {
   if (dkeys) {
@@ -1223,9 +1223,9 @@ __device__ __forceinline__ void scatter_level(const LevelDev& L, const LocT<T>& 
   const int key = active ? q.base : (-2 - lane);
   const int prev = __shfl_up_sync(full, key, 1);
   const bool head = lane == 0 || key != prev;
-  const unsigned heads = __ballot_sync(full, head);
+  const unsigned heads = no_merge ? full : __ballot_sync(full, head);
   T* Gp = reinterpret_cast<T*>(L.grad) + (int64_t)q.base * C;
-  if (heads == full) {  // no shared cells in this warp: one red per lane
+  if (heads == full) {  // no shared cells in this warp (or no_merge): one red per lane
     if (!active) return;
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
@@ -1464,7 +1464,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_bwd_geom(Ws<T> w, Geo G, int M, 
       corner_w_ju(loc[l], (T)G.lv[l].inv_vs, u, wk, ju);
 #pragma unroll
       for (int k = 0; k < 8; ++k) coef[k] = fma(p, wk[k], ju[k]);
-      scatter_level<T, S::CG>(G.lv[l], loc[l], gz + l * S::CG, coef, active, l < agg_levels, w.det_keys,
+      scatter_level<T, S::CG>(G.lv[l], loc[l], gz + l * S::CG, coef, active, false, w.det_keys,
                               w.det_vals, s * (S::NL + 1) + l);
     }
     // ---- A0 = [p z + v, p]; q0 = (v W0) (.) m0; A1 = [p h0 + q0, p]; V2 += dd1 (.) m1

@@ -856,7 +856,8 @@ __global__ void __launch_bounds__(kTile, 2) k_bwd_geom_t5(Ws<float> w, Geo G, in
 #pragma unroll
       for (int k = 0; k < 8; ++k) coef[k] = fmaf(p, wk[k], ju[k]);
       if (!(w.dbg & 1))
-        scatter_level<float, S::CG>(G.lv[l], lq, gz + l * S::CG, coef, active, l < agg_levels, w.det_keys,
+        scatter_level<float, S::CG>(G.lv[l], lq, gz + l * S::CG, coef, active,
+                                    (w.dbg & 128) && l == S::NL - 1, w.det_keys,
                                     w.det_vals, s * (S::NL + 1) + l);
     }
   }

@@ -942,7 +942,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_bwd_geom_tc(Ws<float> w, Geo G, 
     corner_w_ju(lq, (float)G.lv[l].inv_vs, u, wk, ju);
 #pragma unroll
     for (int k = 0; k < 8; ++k) coef[k] = fmaf(p, wk[k], ju[k]);
-    scatter_level<float, S::CG>(G.lv[l], lq, myrow + K::oZ + l * S::CG, coef, active, l < agg_levels,
+    scatter_level<float, S::CG>(G.lv[l], lq, myrow + K::oZ + l * S::CG, coef, active, false,
                                 w.det_keys, w.det_vals, s * (S::NL + 1) + l);
   }
   // ---- outer products over the warp's samples: dW0 += A0^T delta0, dW1 += A1^T delta1
