@@ -558,6 +558,11 @@ def main():
                 "step_hbm_frac": B / (ms_step / 1e3) / 1e9 / peak,
                 "objective_ms": obj_ms, "adam_ms": adam_ms,
                 "kernels": table}
+    roofline["note"] = ("k_adam reads all 32 B/param of state but writes nothing back for 16-byte "
+                        "vectors whose g, m and v are all +0 (never-touched parameters: the update "
+                        "would rewrite the same bits), so early in training or on large mostly-empty "
+                        "grids (config 4) its algorithmic-byte rate can exceed the copy peak; "
+                        "`traffic` is the measured DRAM bytes")
     tr = traffic_of(dom["kernel"], f"config{args.config}" + ("-pose" if args.refine_poses else ""))
     if tr is not None:
         roofline["traffic"] = tr
