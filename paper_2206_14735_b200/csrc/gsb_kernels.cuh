@@ -474,18 +474,22 @@ __global__ void k_smooth_points(gsb_dataset_t D, const double* __restrict__ pose
 struct ImpRow {
   double* a;    // sigmoid values, then om, then the CDF (in place)
   double* out;  // merged depths
-  double* nw;   // new depths (A)
+  double* d;    // the input depth row, staged once
+  double* nw;   // new depths (A), in draw order
+  double* ns;   // the same, sorted (stable)
   int32_t* src; // provenance (-1 = new / moved)
 };
 __host__ __device__ constexpr size_t imp_row_bytes(int ld, int A) {
-  return (size_t)ld * 8 * 2 + (size_t)((A + 1) / 2 * 2) * 8 + (size_t)(ld + 3) / 4 * 4 * 4;
+  return (size_t)ld * 8 * 3 + (size_t)((A + 1) / 2 * 2) * 8 * 2 + (size_t)(ld + 3) / 4 * 4 * 4;
 }
 __device__ __forceinline__ ImpRow imp_row(unsigned char* base, int ld, int A) {
   ImpRow r;
   r.a = reinterpret_cast<double*>(base);
   r.out = r.a + ld;
-  r.nw = r.out + ld;
-  r.src = reinterpret_cast<int32_t*>(r.nw + (A + 1) / 2 * 2);
+  r.d = r.out + ld;
+  r.nw = r.d + ld;
+  r.ns = r.nw + (A + 1) / 2 * 2;
+  r.src = reinterpret_cast<int32_t*>(r.ns + (A + 1) / 2 * 2);
   return r;
 }
 
@@ -523,6 +527,8 @@ static __device__ void importance_group(const LaneGroup<G>& grp, const ImpRow& R
   const int gl = grp.gl;
   double total = 0.0;
   double* cdf = R.a;
+  for (int i = gl; i < K; i += G) R.d[i] = d[i];  // read the row once
+  d = R.d;
   if (win) {
     if (gl == 0) {
       double c = 0.0;
@@ -626,13 +632,8 @@ static __device__ void importance_group(const LaneGroup<G>& grp, const ImpRow& R
   sorted = grp.all(sorted);
   const int n = K + A;
   if (sorted) {
-    for (int i = gl; i < K; i += G) {
-      const double di = d[i];
-      int c = 0;
-      for (int a = 0; a < A; ++a) c += R.nw[a] < di;
-      R.out[i + c] = di;
-      R.src[i + c] = i;
-    }
+    // new samples: stable rank among themselves (the draw index breaks
+    // ties) and #(old <= v); then the sorted copy for the old samples' counts
     for (int a = gl; a < A; a += G) {
       const double v = R.nw[a];
       int lo = 0, hi = K;  // #(old <= v)
@@ -642,8 +643,20 @@ static __device__ void importance_group(const LaneGroup<G>& grp, const ImpRow& R
       }
       int r = 0;
       for (int b = 0; b < A; ++b) r += (R.nw[b] < v) || (R.nw[b] == v && b < a);
+      R.ns[r] = v;
       R.out[lo + r] = v;
       R.src[lo + r] = -1;
+    }
+    grp.sync();
+    for (int i = gl; i < K; i += G) {
+      const double di = d[i];
+      int lo = 0, hi = A;  // #(new < di) over the sorted new samples
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (R.ns[mid] < di) lo = mid + 1; else hi = mid;
+      }
+      R.out[i + lo] = di;
+      R.src[i + lo] = i;
     }
   } else if (gl == 0) {  // general stable insertion sort (unsorted input rows)
     for (int t = 0; t < n; ++t) {
