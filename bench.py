@@ -365,6 +365,8 @@ def main():
                     help="pose refinement on (refine_poses=True, frame 0 frozen; not the headline)")
     ap.add_argument("--prefetch", action="store_true",
                     help="host draws on a background thread in the e2e leg")
+    ap.add_argument("--no-overlap", action="store_true",
+                    help="fused Adam launch (no side-stream colour-grid update under the next sampling)")
     ap.add_argument("--strong", action="store_true",
                     help="strong scaling (SURVEY 8d c3(i)): the global batch is --rays, split by rows "
                          "across the ranks (default: weak, --rays per rank)")
@@ -434,9 +436,21 @@ def main():
         else:
             dp.adam(opt)  # sharded Adam + all-gather (parallel.py)
 
+    # single GPU: step k's colour-grid Adam on a side stream under step k+1's
+    # sampling phase (optimizer.AdamOverlap; bit-identical to the fused launch)
+    ov = optimizer.AdamOverlap(opt, model) if (dp is None and not args.no_overlap) else None
+
     def one_step(d, kw, ids, sm):
-        w = objective(d, kw, ids, sm)
-        adam_step()
+        if ov is None:
+            w = objective(d, kw, ids, sm)
+            adam_step()
+            return w
+        if isinstance(sm, tuple):
+            sm = eng.smooth_points_dev(*sm)
+        eng.launch(cfg, d, ids, sm, phases=1, **kw)
+        ov.wait_colour()
+        w = eng.launch(cfg, d, ids, sm, phases=2, fresh=False, **kw)
+        ov.step(w, cfg.divergence_threshold)
         return w
 
     # ---- device-resident inputs for warmup + timed steps
@@ -469,12 +483,24 @@ def main():
         b = torch.cuda.Event(enable_timing=True)
         c = torch.cuda.Event(enable_timing=True)
         a.record()
-        objective(*pre[W + k])
-        b.record()
-        adam_step()
+        if ov is None:
+            objective(*pre[W + k])
+            b.record()
+            adam_step()
+        else:  # b: after phase 2; c: after the main-stream part of Adam
+            d_, kw_, ids_, sm_ = pre[W + k]
+            if isinstance(sm_, tuple):
+                sm_ = eng.smooth_points_dev(*sm_)
+            eng.launch(cfg, d_, ids_, sm_, phases=1, **kw_)
+            ov.wait_colour()
+            w_ = eng.launch(cfg, d_, ids_, sm_, phases=2, fresh=False, **kw_)
+            b.record()
+            ov.step(w_, cfg.divergence_threshold)
         c.record()
         t_step.append((a, b))
         t_adam.append((b, c))
+    if ov is not None:
+        ov.drain()  # the timed region ends after the last colour-grid update
     ev1.record()
     torch.cuda.synchronize()
     launches = int(eng.lib.gsb_launch_count() - launches0)
@@ -494,15 +520,17 @@ def main():
     # ---- per-kernel live timing (CUDA events between launches on the step
     # stream, gsb_timing_enable); a separate pass so `value` carries no markers
     eng.lib.gsb_timing_enable(1)
-    for k in range(K):
-        one_step(*pre[W + k])
+    for k in range(K):  # fused Adam here: the per-kernel events live on one stream
+        objective(*pre[W + k])
+        adam_step()
     torch.cuda.synchronize()
     eng.lib.gsb_timing_enable(0)
     kt = _lib.kernel_times()
 
     # ---- e2e through the public API (host draws + H2D + D2H of parts);
     # the Trainer prefetches host draws on a background thread
-    T = optimizer.Trainer(model, ds, cfg, opt, dist=pg, rank=rank, world=ws_)
+    T = optimizer.Trainer(model, ds, cfg, opt, dist=pg, rank=rank, world=ws_,
+                          overlap_adam=not args.no_overlap)
     base_it = W + K
     if args.prefetch:
         T.start_prefetch(base_it)

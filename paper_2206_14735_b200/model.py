@@ -76,7 +76,11 @@ class Param:
         return self.arena.grads[self.offset:self.offset + self.size].view(self.shape)
 
     def numpy(self):
-        return self.data.detach().cpu().numpy().copy()
+        d = self.data
+        if d.is_cuda:  # every stream (the Trainer updates the colour grid on a side stream)
+            import torch
+            torch.cuda.synchronize(d.device)
+        return d.detach().cpu().numpy().copy()
 
     def set(self, values):
         import torch

@@ -180,6 +180,70 @@ class Adam:
         self._launch(guard=guard, guard_threshold=guard_threshold)
 
 
+class AdamOverlap:
+    """Step k's colour-grid update on a side stream, under step k+1's
+    sampling phase.
+
+    The sampling phase (ray setup, coarse + importance SDF evaluations and
+    importance rounds, gs/renderer.py:302-346) reads the geometry grids, the
+    geometry MLP and log_s, never the colour grid; the colour grid is next
+    read by the taped forward of phase 2.  So each step's Adam is split into
+    the colour-grid range [lo, hi) of the arena, launched on `side` once the
+    step's gradients are final, and the rest, on the step's own stream; the
+    next step's phase 2 waits for the colour range.  Every element is still
+    updated exactly once per step, from the same gradients, with the same
+    guard (a device snapshot of the step's parts and status words, since the
+    next phase 1 resets them): results are bit-identical to the fused launch.
+    Single-GPU only (the data-parallel path shards Adam instead)."""
+
+    def __init__(self, opt, model):
+        import torch
+        self.torch = torch
+        self.opt = opt
+        cg = model.arena["colorgrid"]
+        A = mdl.ParamArena.ALIGN
+        self.lo = cg.offset // A * A
+        self.hi = min(-(-(cg.offset + cg.size) // A) * A, opt.arena.n)
+        dev = opt.arena.device
+        self.side = torch.cuda.Stream(device=dev)
+        self.snap_parts = torch.zeros(_lib.N_PARTS, dtype=torch.float64, device=dev)
+        self.snap_status = torch.zeros(_lib.N_STATUS, dtype=torch.int32, device=dev)
+        self.ev_grads = torch.cuda.Event()
+        self.ev_done = torch.cuda.Event()
+        self.pending = False
+
+    def wait_colour(self, stream=None):
+        """Before a phase 2: the previous step's colour-grid update is done."""
+        if self.pending:
+            (stream or self.torch.cuda.current_stream()).wait_event(self.ev_done)
+
+    def step(self, ws, guard_threshold, stream=None):
+        """Step k's Adam, after its phase 2 (ws: its workspace views)."""
+        torch = self.torch
+        cur = stream or torch.cuda.current_stream()
+        opt = self.opt
+        with torch.cuda.stream(cur):
+            self.wait_colour(cur)  # the snapshot buffers are reused
+            self.snap_parts.copy_(ws["parts"])
+            self.snap_status.copy_(ws["status"])
+        opt.t = [t + 1 for t in opt.t]
+        kw = dict(guard=self.snap_parts, guard_threshold=guard_threshold, guard_status=self.snap_status)
+        if self.lo > 0:
+            opt._launch(lo=0, hi=self.lo, stream=cur, **kw)
+        if self.hi < opt.arena.n:
+            opt._launch(lo=self.hi, hi=opt.arena.n, stream=cur, **kw)
+        self.ev_grads.record(cur)
+        self.side.wait_event(self.ev_grads)
+        opt._launch(lo=self.lo, hi=self.hi, stream=self.side, **kw)
+        self.ev_done.record(self.side)
+        self.pending = True
+
+    def drain(self, stream=None):
+        """Make the current stream wait for the last colour-grid update."""
+        self.wait_colour(stream)
+        self.pending = False
+
+
 @dataclass
 class TrainConfig:
     """All knobs of a reconstruction run (gs/optimizer.py:94-143)."""
@@ -282,6 +346,9 @@ def make_optimizer(model, cfg):
 
 
 def save_model(path, model, cfg, iteration, opt=None):
+    if model.arena.params.is_cuda:  # all streams, the side-stream Adam included
+        import torch
+        torch.cuda.synchronize(model.arena.params.device)
     names = model.param_names()
     arrays = {n: p.numpy() for n, p in zip(names, model.parameters())}
     # the reference stores log_s as a 0-d array
@@ -415,7 +482,7 @@ class Trainer:
     its row shard of the global batch and the step runs as
     parallel.DataParallelStep."""
 
-    def __init__(self, model, dataset, cfg, opt, dist=None, rank=0, world=1):
+    def __init__(self, model, dataset, cfg, opt, dist=None, rank=0, world=1, overlap_adam=True):
         import torch
         from .parallel import DataParallelStep
         self.torch = torch
@@ -430,6 +497,8 @@ class Trainer:
         self.events = [torch.cuda.Event(), torch.cuda.Event()]
         self.rank, self.world = int(rank), int(world)
         self.dp = DataParallelStep(self.engine, dist) if dist is not None and world > 1 else None
+        # single GPU: the colour-grid Adam of step k runs under step k+1's sampling
+        self.overlap = AdamOverlap(opt, model) if (overlap_adam and self.dp is None) else None
         self.prefetcher = None
         self.last_h2d = 0
 
@@ -459,24 +528,37 @@ class Trainer:
             d, kw = self.draws(it)
         self.last_h2d = d.h2d_bytes
         ids, sm = self.engine.upload(d)
-        if self.dp is None:
+        if self.overlap is not None:
+            self.engine.launch(self.cfg, d, ids, sm, phases=1, **kw)
+            self.overlap.wait_colour()
+            ws = self.engine.launch(self.cfg, d, ids, sm, phases=2, fresh=False, **kw)
+        elif self.dp is None:
             ws = self.engine.launch(self.cfg, d, ids, sm, **kw)
         else:
             ws = self.dp(self.cfg, d, ids, sm, **kw)
         self.host_parts[slot].copy_(ws["parts"], non_blocking=True)
         self.host_status[slot].copy_(ws["status"], non_blocking=True)
         self.events[slot].record()
-        self.opt.t = [t + 1 for t in self.opt.t]
-        if self.dp is None:
+        if self.overlap is not None:
+            self.overlap.step(ws, self.cfg.divergence_threshold)
+        elif self.dp is None:
+            self.opt.t = [t + 1 for t in self.opt.t]
             self.opt._launch(guard=ws["parts"], guard_threshold=self.cfg.divergence_threshold,
                              guard_status=ws["status"])
         else:
+            self.opt.t = [t + 1 for t in self.opt.t]
             self.dp.adam(self.opt, guard=ws["parts"], guard_threshold=self.cfg.divergence_threshold,
                          guard_status=ws["status"])
         if self.engine.refine and (it + 1) % self.cfg.pose_refresh_every == 0:
             for p in self.model.poses:  # gs/optimizer.py:374-376
                 p.refresh()
         return ws
+
+    def drain(self):
+        """Order every later read of the parameters (host copies, checkpoints)
+        after the side-stream colour-grid update of the last step."""
+        if self.overlap is not None:
+            self.overlap.drain()
 
     def parts(self, slot):
         self.events[slot].synchronize()
@@ -550,12 +632,14 @@ def train(dataset, cfg, out_dir, initial_poses=None, resume=None):
                 if (it + 1) % every == 0:
                     finish(it, slot, csv)
                     pending = None
+                    T.drain()
                     save_model(os.path.join(out_dir, f"ckpt_{it + 1:06d}.gsck"), model, cfg,
                                it + 1, opt)
             if pending is not None:
                 finish(pending[0], pending[1], csv)
         finally:
             T.stop_prefetch()
+            T.drain()
             csv.flush()
     save_model(final_path, model, cfg, cfg.iterations, opt)
     return model, final_path

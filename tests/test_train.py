@@ -149,3 +149,32 @@ def test_trainer_guard_skips_update_and_rolls_back():
     for a, b in zip(before, model.parameters()):
         np.testing.assert_array_equal(a, b.numpy())
     assert int(opt.status[5].item()) == 1  # GSB_ST_DIVERGED
+
+
+@pytest.mark.gpu
+def test_trainer_overlapped_adam_is_bit_identical():
+    """The side-stream colour-grid Adam (optimizer.AdamOverlap, under the
+    next step's sampling phase) gives the fused launch's parameters and
+    moments bit for bit (deterministic scatter mode on both, so the
+    gradients themselves are run-to-run identical)."""
+    from paper_2206_14735_b200 import optimizer
+    from paper_2206_14735_b200.renderer import engine_for
+    ds, cfg = small_setup()
+    out = []
+    for overlap in (False, True):
+        model = optimizer.build_model(ds, cfg, skip_init=True)
+        opt = optimizer.make_optimizer(model, cfg)
+        T = optimizer.Trainer(model, ds, cfg, opt, overlap_adam=overlap)
+        T.engine.deterministic = True
+        assert engine_for(model, T.dataset) is T.engine
+        for it in range(4):
+            T.launch(it, slot=it % 2)
+            T.parts(it % 2)
+        T.drain()
+        out.append(([p.numpy() for p in model.parameters()],
+                    opt.m_arena.cpu().numpy(), opt.v_arena.cpu().numpy()))
+    (p0, m0, v0), (p1, m1, v1) = out
+    for a, b in zip(p0, p1):
+        np.testing.assert_array_equal(a, b)
+    np.testing.assert_array_equal(m0, m1)
+    np.testing.assert_array_equal(v0, v1)
