@@ -365,8 +365,9 @@ def main():
                     help="pose refinement on (refine_poses=True, frame 0 frozen; not the headline)")
     ap.add_argument("--prefetch", action="store_true",
                     help="host draws on a background thread in the e2e leg")
-    ap.add_argument("--no-overlap", action="store_true",
-                    help="fused Adam launch (no side-stream colour-grid update under the next sampling)")
+    ap.add_argument("--overlap-adam", action="store_true",
+                    help="step k's colour-grid Adam on a side stream under step k+1's sampling "
+                         "(optimizer.AdamOverlap; measured slower on one B200: 1.412 vs 1.384 ms)")
     ap.add_argument("--strong", action="store_true",
                     help="strong scaling (SURVEY 8d c3(i)): the global batch is --rays, split by rows "
                          "across the ranks (default: weak, --rays per rank)")
@@ -436,9 +437,11 @@ def main():
         else:
             dp.adam(opt)  # sharded Adam + all-gather (parallel.py)
 
-    # single GPU: step k's colour-grid Adam on a side stream under step k+1's
-    # sampling phase (optimizer.AdamOverlap; bit-identical to the fused launch)
-    ov = optimizer.AdamOverlap(opt, model) if (dp is None and not args.no_overlap) else None
+    # opt-in (--overlap-adam), single GPU: step k's colour-grid Adam on a side
+    # stream under step k+1's sampling phase (optimizer.AdamOverlap;
+    # bit-identical).  Measured slower: the HBM stream slows the latency-bound
+    # sampling and forward kernels more than it hides (1.412 vs 1.384 ms)
+    ov = optimizer.AdamOverlap(opt, model) if (dp is None and args.overlap_adam) else None
 
     def one_step(d, kw, ids, sm):
         if ov is None:
@@ -530,7 +533,7 @@ def main():
     # ---- e2e through the public API (host draws + H2D + D2H of parts);
     # the Trainer prefetches host draws on a background thread
     T = optimizer.Trainer(model, ds, cfg, opt, dist=pg, rank=rank, world=ws_,
-                          overlap_adam=not args.no_overlap)
+                          overlap_adam=args.overlap_adam)
     base_it = W + K
     if args.prefetch:
         T.start_prefetch(base_it)

@@ -194,7 +194,9 @@ class AdamOverlap:
     updated exactly once per step, from the same gradients, with the same
     guard (a device snapshot of the step's parts and status words, since the
     next phase 1 resets them): results are bit-identical to the fused launch.
-    Single-GPU only (the data-parallel path shards Adam instead)."""
+    Single-GPU only (the data-parallel path shards Adam instead).  Opt-in: on
+    one B200 at config 2 the concurrent HBM stream slowed the latency-bound
+    sampling and taped kernels by more than it hid (1.412 vs 1.384 ms)."""
 
     def __init__(self, opt, model):
         import torch
@@ -482,7 +484,7 @@ class Trainer:
     its row shard of the global batch and the step runs as
     parallel.DataParallelStep."""
 
-    def __init__(self, model, dataset, cfg, opt, dist=None, rank=0, world=1, overlap_adam=True):
+    def __init__(self, model, dataset, cfg, opt, dist=None, rank=0, world=1, overlap_adam=False):
         import torch
         from .parallel import DataParallelStep
         self.torch = torch
@@ -497,7 +499,8 @@ class Trainer:
         self.events = [torch.cuda.Event(), torch.cuda.Event()]
         self.rank, self.world = int(rank), int(world)
         self.dp = DataParallelStep(self.engine, dist) if dist is not None and world > 1 else None
-        # single GPU: the colour-grid Adam of step k runs under step k+1's sampling
+        # opt-in, single GPU: the colour-grid Adam of step k under step k+1's
+        # sampling (AdamOverlap; bit-identical, measured slower at config 2)
         self.overlap = AdamOverlap(opt, model) if (overlap_adam and self.dp is None) else None
         self.prefetcher = None
         self.last_h2d = 0
