@@ -71,7 +71,7 @@ Ws<T> carve(void* ws, const Sizes& z, size_t* bytes, int64_t* off_parts = nullpt
   w.counts = c.template take<long long>(8);
   size_t o_status = c.off;
   w.status = c.template take<int32_t>(GSB_N_STATUS);
-  w.evl_count = c.template take<int32_t>(4);
+  w.evl_count = c.template take<int32_t>(GSB_MAX_ROUNDS);  // one list counter per importance round
   w.o = c.template take<T>(z.M * 3);
   w.r = c.template take<T>(z.M * 3);
   w.od = c.template take<double>(z.M * 3);

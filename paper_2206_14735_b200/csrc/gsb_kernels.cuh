@@ -230,6 +230,11 @@ __global__ void __launch_bounds__(128) k_ray_setup(gsb_dataset_t D, const int64_
   __shared__ double s_near[RPB], s_span[RPB];
   const int t = threadIdx.x;
   const int i = blockIdx.x * RPB + t;
+  if (blockIdx.x == 0) {  // the step's counters (first kernel of the step): no memset launches
+    if (t < 8) w.counts[t] = 0;
+    if (t < GSB_MAX_ROUNDS) w.evl_count[t] = 0;
+    if (t == 0) *w.loss_cnt = 0u;
+  }
   if (t < RPB && i < M) {
     PixelRay P = pixel_ray(D, ids[i]);
     const double* pose = D.poses + P.frame * 12;

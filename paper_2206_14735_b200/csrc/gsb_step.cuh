@@ -120,14 +120,14 @@ template <typename T>
 inline cudaError_t launch_importance(int G, Ws<T> w, int M, int K, int A, int ray_base, const double* dep,
                                      const double* phi, double* dep_out, double* phi_out, const T* log_s,
                                      gsb_pcg64_t rng, int want_list, int count_final, double trunc,
-                                     const uint64_t* row_states, cudaStream_t stream) {
+                                     const uint64_t* row_states, int32_t* evl_count, cudaStream_t stream) {
   const int rpb = 128 / G;
   const size_t smem = (size_t)rpb * imp_row_bytes(K + A, A);
   auto go = [&](auto kern) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     kern<<<(M + rpb - 1) / rpb, 128, smem, stream>>>(w, M, K, A, ray_base, dep, phi, dep_out, phi_out, log_s,
-                                                      rng, w.evl, w.evl_count, w.evl_cap, want_list,
+                                                      rng, w.evl, evl_count, w.evl_cap, want_list,
                                                       count_final, trunc, row_states);
     return cudaGetLastError();
   };
@@ -198,7 +198,6 @@ int run_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step
   double* dep_final = w.dep[R % 2];
   const T* log_s = params + model->log_s_offset;
   if (st->phases & 1) {
-    GSB_CHECK(cudaMemsetAsync(w.counts, 0, 8 * sizeof(long long), stream));
     PcgRounds imp{};
     imp.n = R;
     imp.A = A;
@@ -227,25 +226,25 @@ int run_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step
       int cur = 0, K = Nc;
       for (int rnd = 0; rnd < R; ++rnd) {
         const bool need_phi = rnd < R - 1;
-        GSB_CHECK(cudaMemsetAsync(w.evl_count, 0, sizeof(int32_t), stream));
+        int32_t* evl_n = w.evl_count + rnd;  // zeroed by k_ray_setup
         GSB_CHECK(launch_importance<T>(imp_group(), w, M, K, A, st->ray_base, w.dep[cur], w.phi[cur],
                                        w.dep[1 - cur], w.phi[1 - cur], log_s, st->rng_importance[rnd],
                                        need_phi ? 1 : 0, rnd == R - 1 ? 1 : 0, st->truncation,
-                                       w.imp_state + (int64_t)rnd * M * 2, stream));
+                                       w.imp_state + (int64_t)rnd * M * 2, evl_n, stream));
         GSB_LAUNCHED_T("k_importance_dev");
         if (need_phi) {
           int64_t cap = (int64_t)M * A;
           int b2 = (int)((cap + 127) / 128);
           if constexpr (F32) {
             if (use_t5(false))
-              GSB_CHECK(launch_sdf_t5<S>(w, G, M, Nc, w.dep[1 - cur], w.phi[1 - cur], w.evl, w.evl_count,
+              GSB_CHECK(launch_sdf_t5<S>(w, G, M, Nc, w.dep[1 - cur], w.phi[1 - cur], w.evl, evl_n,
                                          cap, stream));
             else
               tc::k_sdf_eval_tc<S, TW><<<b2, TW * 32, tc::SdfTc<S, TW>::smem(), stream>>>(
-                  w, G, M, Nc, mlp32, w.dep[1 - cur], w.phi[1 - cur], w.evl, w.evl_count);
+                  w, G, M, Nc, mlp32, w.dep[1 - cur], w.phi[1 - cur], w.evl, evl_n);
           } else
             k_sdf_eval<T, S, false><<<b2, 128, smem_sdf, stream>>>(
-                w, G, M, Nc, w.dep[1 - cur], w.phi[1 - cur], w.evl, w.evl_count, mlp);
+                w, G, M, Nc, w.dep[1 - cur], w.phi[1 - cur], w.evl, evl_n, mlp);
           GSB_LAUNCHED_T("k_sdf_eval");
         }
         cur = 1 - cur;
@@ -428,7 +427,6 @@ int run_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step
                                                                       nb_geo, nb_col);
     }
     GSB_LAUNCHED_T("k_finalize_mlp");
-    GSB_CHECK(cudaMemsetAsync(w.loss_cnt, 0, sizeof(unsigned), stream));
     k_finalize_loss<T><<<(std::max(M, z.S) + 255) / 256, 256, 0, stream>>>(w, M, z.S, grads, params,
                                                                          model->log_s_offset, L);
     GSB_LAUNCHED_T("k_finalize_loss");
