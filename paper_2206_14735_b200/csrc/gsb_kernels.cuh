@@ -279,11 +279,11 @@ __global__ void __launch_bounds__(128) k_ray_setup(gsb_dataset_t D, const int64_
     s_near[t] = nearv;
     s_span[t] = farv - nearv;
   }
-  __syncthreads();
-  // stratified_coarse (gs/sampler.py:91-107) with uniform row (ray_base + ray)
+  // the generator work does not depend on the rays: it runs before the
+  // barrier, under the setup threads' dataset reads and float64 math
   const int rl = t / TPR, q = t % TPR, ray = blockIdx.x * RPB + rl;
-  if (ray >= M) return;
-  if (q < imp.n && w.imp_state) {  // importance round q: this row's first-uniform state
+  const bool live = ray < M;
+  if (live && q < imp.n && w.imp_state) {  // importance round q: this row's first-uniform state
     Pcg g;
     g.init(imp.r[q]);
     g.advance((uint64_t)(ray_base + ray) * (uint64_t)imp.A);
@@ -291,16 +291,28 @@ __global__ void __launch_bounds__(128) k_ray_setup(gsb_dataset_t D, const int64_
     o[0] = (uint64_t)(g.state >> 64);
     o[1] = (uint64_t)g.state;
   }
+  // stratified_coarse (gs/sampler.py:91-107) with uniform row (ray_base + ray)
+  constexpr int kU = 16;  // uniforms drawn ahead of the barrier
   const int chunk = (Nc + TPR - 1) / TPR, j0 = q * chunk, j1 = min(Nc, j0 + chunk);
-  if (j0 >= j1) return;
   Pcg g;
-  g.init(rng);
-  g.advance((uint64_t)(ray_base + ray) * (uint64_t)Nc + (uint64_t)j0);
+  double u[kU];
+  if (live && j0 < j1) {
+    g.init(rng);
+    g.advance((uint64_t)(ray_base + ray) * (uint64_t)Nc + (uint64_t)j0);
+#pragma unroll
+    for (int k = 0; k < kU; ++k)
+      if (j0 + k < j1) u[k] = g.next_double();
+  }
+  __syncthreads();
+  if (!live || j0 >= j1) return;
   const double nv = s_near[rl], span = s_span[rl];
   double* dep = w.dep[0] + (int64_t)ray * w.ld;
-  for (int j = j0; j < j1; ++j) {
-    double u = g.next_double();
-    dep[j] = nv + span * (((double)j + u) / (double)Nc);
+#pragma unroll
+  for (int k = 0; k < kU; ++k)
+    if (j0 + k < j1) dep[j0 + k] = nv + span * (((double)(j0 + k) + u[k]) / (double)Nc);
+  for (int j = j0 + kU; j < j1; ++j) {  // long rows (Nc > 8 kU): the rest after the barrier
+    const double uu = g.next_double();
+    dep[j] = nv + span * (((double)j + uu) / (double)Nc);
   }
 }
 
