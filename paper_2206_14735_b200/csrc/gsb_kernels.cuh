@@ -998,16 +998,20 @@ __device__ __forceinline__ T warp_allsum(T v) {
   return warp_sum(v);
 }
 
+constexpr int kRenderRows = 6;  // per-warp shared arrays of N values
+
 template <typename T>
 __global__ void __launch_bounds__(128, 11) k_render(Ws<T> w, int M, int N, const double* __restrict__ dep,
                                                 const T* __restrict__ params, int64_t log_s_off,
                                                 LossW L) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  T* sig = reinterpret_cast<T*>(smem_raw) + (size_t)wid * 4 * N;
+  T* sig = reinterpret_cast<T*>(smem_raw) + (size_t)wid * kRenderRows * N;
   T* trn = sig + N;
   T* xb = trn + N;
   T* yb = xb + N;
+  T* alp = yb + N;  // alpha_j, kept from the forward pass
+  T* rat = alp + N; // sigma_{j+1} / max(sigma_j, 1e-12), kept from the forward pass
   const int ray = blockIdx.x * (blockDim.x >> 5) + wid;
   if (ray >= M) return;  // warp-uniform
   const T s = exp(params[log_s_off]);  // ModelState.s_tensor (gs/renderer.py:83-84)
@@ -1020,15 +1024,17 @@ __global__ void __launch_bounds__(128, 11) k_render(Ws<T> w, int M, int N, const
   T carry = T(0), ch0 = T(0), ch1 = T(0), ch2 = T(0), dh = T(0);
   for (int j0 = 0; j0 < N; j0 += 32) {
     const int j = j0 + lane;
-    T al = T(0), Lj = T(0);
+    T al = T(0), Lj = T(0), ratio = T(0);
     if (j < N - 1) {
       const T den = sig[j] >= SF ? sig[j] : SF;
-      const T ratio = sig[j + 1] / den;
+      ratio = sig[j + 1] / den;
       al = T(1) - (ratio <= T(1) ? ratio : T(1));
     }
     if (j < N) {
       const T om = T(1) - al;
       Lj = log(om >= TF ? om : TF);
+      alp[j] = al;
+      rat[j] = ratio;
     }
     const T incl = warp_incl_scan(Lj);
     const T Tj = (j == 0) ? T(1) : exp(carry + (incl - Lj));
@@ -1099,12 +1105,7 @@ __global__ void __launch_bounds__(128, 11) k_render(Ws<T> w, int M, int N, const
     const int j = j0 + lane;
     T tt = T(0);
     if (j < N) {
-      T al = T(0);
-      if (j < N - 1) {
-        const T den = sig[j] >= SF ? sig[j] : SF;
-        const T ratio = sig[j + 1] / den;
-        al = T(1) - (ratio <= T(1) ? ratio : T(1));
-      }
+      const T al = alp[j];
       const T Tj = trn[j];
       const T wj = Tj * al;
       const T* cj = w.scol + (s0 + j) * 3;
@@ -1126,12 +1127,8 @@ __global__ void __launch_bounds__(128, 11) k_render(Ws<T> w, int M, int N, const
     const int j = j0 + lane;
     T own = T(0), fwd = T(0);
     if (j < N) {
-      T al = T(0), ratio = T(0), den = T(1);
-      if (j < N - 1) {
-        den = sig[j] >= SF ? sig[j] : SF;
-        ratio = sig[j + 1] / den;
-        al = T(1) - (ratio <= T(1) ? ratio : T(1));
-      }
+      const T al = alp[j], ratio = rat[j];
+      const T den = (j < N - 1) ? (sig[j] >= SF ? sig[j] : SF) : T(1);
       const T om = T(1) - al;
       const T Lbar = tot - yb[j];
       const T ombar = om >= TF ? Lbar / om : T(0);

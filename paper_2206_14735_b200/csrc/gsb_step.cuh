@@ -315,7 +315,9 @@ int run_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step
         k_smooth<T><<<(z.S + 127) / 128, 128, 0, stream>>>(w, z.MN, z.S, scale);
         GSB_LAUNCHED_T("k_smooth");
       }
-      k_render<T><<<(M + 3) / 4, 128, (size_t)4 * 4 * N * esz, stream>>>(w, M, N, dep_final, params,
+      const size_t smem_render = (size_t)4 * kRenderRows * N * esz;
+      GSB_CHECK(cudaFuncSetAttribute(k_render<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_render));
+      k_render<T><<<(M + 3) / 4, 128, smem_render, stream>>>(w, M, N, dep_final, params,
                                                                          model->log_s_offset, L);
       GSB_LAUNCHED_T("k_render");
       if (w.det_keys)  // every slot starts empty (~0 sorts last and is skipped)

@@ -385,18 +385,6 @@ __global__ void __launch_bounds__(kTile, kCtaPerSm) k_fwd_t5(Ws<float> w, Geo G,
     }
 #pragma unroll
     for (int i = 0; i < 8 * KG; ++i) z[i] = 0.f;
-    if (w.dbg & 256) {  // A/B: L1 prefetch of the finest level's and the colour corners first
-      const Loc qf = locate<false>(G.lv[S::NL - 1], (double)p[0], (double)p[1], (double)p[2], nullptr);
-      const Loc qcp = locate<false>(G.col, (double)p[0], (double)p[1], (double)p[2], nullptr);
-      const float* Ff = reinterpret_cast<const float*>(G.lv[S::NL - 1].feat) + qf.base * S::CG;
-      const float* Fc = reinterpret_cast<const float*>(G.col.feat) + qcp.base * S::CC;
-#pragma unroll
-      for (int k = 0; k < 8; k += 2) {
-        asm volatile("prefetch.global.L1 [%0];" ::"l"(Ff + corner_off(G.lv[S::NL - 1], k) * S::CG));
-        asm volatile("prefetch.global.L1 [%0];" ::"l"(Fc + corner_off(G.col, k) * S::CC));
-        asm volatile("prefetch.global.L1 [%0];" ::"l"(Fc + corner_off(G.col, k) * S::CC + 2 * S::CC - 1));
-      }
-    }
 #pragma unroll
     for (int l = 0; l < S::NL; ++l) {
       loc[l] = compact<float>(locate<false>(G.lv[l], (double)p[0], (double)p[1], (double)p[2],
