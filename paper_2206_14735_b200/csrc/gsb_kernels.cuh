@@ -2020,15 +2020,16 @@ __global__ void __launch_bounds__(256) k_adam(T* __restrict__ P, T* __restrict__
         __stcs(reinterpret_cast<Vec*>(Gr) + i, Vec{});
         continue;
       }
+      // a gradient vector that is already +0 (no sample touched these
+      // parameters this step: ~3/4 of the rows at config 2) needs no zeroing
+      // store; if m and v are +0 too (never touched), the update rewrites the
+      // same bits everywhere and nothing is written back
+      const uint4 gb = *reinterpret_cast<const uint4*>(&g[u]);
+      const bool g_zero = (gb.x | gb.y | gb.z | gb.w) == 0u;
       {
-        // g = m = v = +0 everywhere in the vector (a parameter no step has
-        // touched yet): the update computes m = v = +0, p unchanged, g = +0
-        // -- exactly the stored bits -- so nothing is written back
-        const uint4 gb = *reinterpret_cast<const uint4*>(&g[u]);
         const uint4 mb = *reinterpret_cast<const uint4*>(&m[u]);
         const uint4 vb = *reinterpret_cast<const uint4*>(&v[u]);
-        if (((gb.x | gb.y | gb.z | gb.w) | (mb.x | mb.y | mb.z | mb.w) | (vb.x | vb.y | vb.z | vb.w)) == 0u)
-          continue;
+        if (g_zero && ((mb.x | mb.y | mb.z | mb.w) | (vb.x | vb.y | vb.z | vb.w)) == 0u) continue;
       }
       T* pp = reinterpret_cast<T*>(&p[u]);
       T* gg = reinterpret_cast<T*>(&g[u]);
@@ -2042,7 +2043,7 @@ __global__ void __launch_bounds__(256) k_adam(T* __restrict__ P, T* __restrict__
           adam_exact(pp[q], gg[q], mm[q], vv[q], lr[u], k, bad);
       }
       __stcs(reinterpret_cast<Vec*>(P) + i, p[u]);
-      __stcs(reinterpret_cast<Vec*>(Gr) + i, g[u]);
+      if (!g_zero) __stcs(reinterpret_cast<Vec*>(Gr) + i, g[u]);
       __stcs(reinterpret_cast<Vec*>(Mm) + i, m[u]);
       __stcs(reinterpret_cast<Vec*>(Vv) + i, v[u]);
     }
