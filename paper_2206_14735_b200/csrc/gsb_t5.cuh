@@ -916,8 +916,9 @@ struct ColT5 {
   static constexpr int oA0 = 0, oB0 = 16, oA1 = 48, oY = 80, oM = 88;
   static constexpr int W0 = tc::UmmaW::C0H, NW = tc::UmmaW::N - tc::UmmaW::C0H;  // colour tiles
   static constexpr int kCtaPerSm = 2;
-  static constexpr uint32_t kCols = 256;  // D [0,32), A hi/lo [32,96), fragment sums [96, 144)
-  static constexpr uint32_t kAcc = 96;
+  static constexpr uint32_t kCols = 256;  // D [0,32), A hi/lo [32,96), fragment sums [96, 144),
+  static constexpr uint32_t kAcc = 96;    // dW2c lane partials [144, 240)
+  static constexpr uint32_t kW2 = 144;
   template <class S>
   static constexpr size_t smem() { return (size_t)(NW + tc::CVec::N) * 4 + (size_t)kTile * ROW * 4; }
 };
@@ -967,6 +968,8 @@ __global__ void __launch_bounds__(kTile, 2) k_bwd_color_t5(Ws<float> w, Geo G, i
     for (int i = 0; i < 16; ++i) zz[i] = 0.f;
 #pragma unroll
     for (int j = 0; j < 3; ++j) st16(tl + K::kAcc + 16 * j, zz);
+#pragma unroll
+    for (int j = 0; j < 6; ++j) st16(tl + K::kW2 + 16 * j, zz);
   }
   auto sa = [&](int off) { return smem_u32(sw + off); };
   float* rows = rows_all + warp * 32 * ROW;
@@ -1068,11 +1071,12 @@ __global__ void __launch_bounds__(kTile, 2) k_bwd_color_t5(Ws<float> w, Geo G, i
     }
     myrow[K::oM] = __uint_as_float(m1);
 #pragma unroll
-    for (int c = 0; c < 3; ++c) {  // dW2c[n][c] = sum_s h1c[n] y_bar[c]
-      float v[32];
+    for (int c = 0; c < 3; ++c) {  // dW2c[n][c] = sum_s h1c[n] y_bar[c]: the lane's own
+      float v[32];                 // running vector in TMEM, reduced over lanes once per CTA
+      ld32(tl + K::kW2 + 32 * c, v);
 #pragma unroll
-      for (int n = 0; n < 32; ++n) v[n] = h[n] * yb[c];
-      sum_w2[c] += warp_colsum32(v);
+      for (int n = 0; n < 32; ++n) v[n] = fmaf(h[n], yb[c], v[n]);
+      st32(tl + K::kW2 + 32 * c, v);
     }
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
@@ -1174,6 +1178,12 @@ __global__ void __launch_bounds__(kTile, 2) k_bwd_color_t5(Ws<float> w, Geo G, i
   // ---- CTA reduction of the running sums -> MLP partial slot (colour block, once per CTA)
   float e0[1][4][4], e1[2][4][4];
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    float v[32];
+    ld32(tl + K::kW2 + 32 * c, v);
+    sum_w2[c] = warp_colsum32(v);
+  }
   tmem_get16(tl + K::kAcc, e0[0]);
   tmem_get16(tl + K::kAcc + 16, e1[0]);
   tmem_get16(tl + K::kAcc + 32, e1[1]);
