@@ -1968,7 +1968,8 @@ __device__ __forceinline__ void adam_fast(float& p, float& g, float& m, float& v
   g = 0.0f;
 }
 
-template <typename T>
+// kAdamU: vectors in flight per thread per trip
+template <typename T, int kAdamU = 2>
 __global__ void __launch_bounds__(256) k_adam(T* __restrict__ P, T* __restrict__ Gr, T* __restrict__ Mm,
                                               T* __restrict__ Vv, int64_t n, AdamSegs segs,
                                               AdamConst k, const double* guard, double thr,
@@ -1993,12 +1994,12 @@ __global__ void __launch_bounds__(256) k_adam(T* __restrict__ P, T* __restrict__
   int bad = 0;
   const int64_t nvec = n / V;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i0 < nvec; i0 += 2 * stride) {
-    // two independent vectors per iteration: more bytes in flight
-    Vec p[2], g[2], m[2], v[2];
-    double lr[2];
+  for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i0 < nvec; i0 += kAdamU * stride) {
+    // kAdamU independent vectors per iteration: more bytes in flight
+    Vec p[kAdamU], g[kAdamU], m[kAdamU], v[kAdamU];
+    double lr[kAdamU];
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
+    for (int u = 0; u < kAdamU; ++u) {
       const int64_t i = i0 + u * stride;
       if (i >= nvec) break;
       const int64_t e = i * V;
@@ -2013,7 +2014,7 @@ __global__ void __launch_bounds__(256) k_adam(T* __restrict__ P, T* __restrict__
       v[u] = __ldcs(reinterpret_cast<const Vec*>(Vv) + i);
     }
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
+    for (int u = 0; u < kAdamU; ++u) {
       const int64_t i = i0 + u * stride;
       if (i >= nvec) break;
       if (lr[u] < 0.0) {
