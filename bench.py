@@ -363,8 +363,9 @@ def main():
     ap.add_argument("--no-smooth", action="store_true", help="lambda_smooth = 0 (c5 sweep)")
     ap.add_argument("--refine-poses", action="store_true",
                     help="pose refinement on (refine_poses=True, frame 0 frozen; not the headline)")
-    ap.add_argument("--prefetch", action="store_true",
-                    help="host draws on a background thread in the e2e leg")
+    ap.add_argument("--no-prefetch", action="store_true",
+                    help="host draws on the main thread in the e2e leg (default: a background "
+                         "thread, as train() does)")
     ap.add_argument("--overlap-adam", action="store_true",
                     help="step k's colour-grid Adam on a side stream under step k+1's sampling "
                          "(optimizer.AdamOverlap; measured slower on one B200: 1.412 vs 1.384 ms)")
@@ -535,7 +536,7 @@ def main():
     T = optimizer.Trainer(model, ds, cfg, opt, dist=pg, rank=rank, world=ws_,
                           overlap_adam=args.overlap_adam)
     base_it = W + K
-    if args.prefetch:
+    if not args.no_prefetch:  # as train() runs (optimizer.py: T.start_prefetch)
         T.start_prefetch(base_it)
     # untimed e2e warm-up: prefetch thread start, pinned staging, first draws
     pending = None
