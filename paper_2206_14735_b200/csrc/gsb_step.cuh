@@ -280,11 +280,16 @@ int run_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step
     if (runA) {
     if constexpr (F32) {
       constexpr int FW = 4;  // warps per CTA of the taped forward
-      if (t5_fwd_mode() > 0) {
+      if (const int cps = t5_fwd_mode(); cps > 0) {
+        // 4 CTAs per SM (128 registers) by default; GSB_T5_FWD=3: 3 CTAs, 170 registers (A/B)
         const int64_t tiles = (ns + t5::kTile - 1) / t5::kTile;
-        const int grid = (int)std::min<int64_t>(tiles, (int64_t)sm_count() * t5::kCtaPerSm);
-        if (grid > 0)
-          t5::k_fwd_t5<S><<<grid, t5::kTile, t5::FwdT5::smem(), stream>>>(w, G, M, N, dep_final, spts, nsp);
+        const int grid = (int)std::min<int64_t>(tiles, (int64_t)sm_count() * (cps == 3 ? 3 : t5::kCtaPerSm));
+        if (grid > 0) {
+          if (cps == 3)
+            t5::k_fwd_t5<S, 3><<<grid, t5::kTile, t5::FwdT5::smem(), stream>>>(w, G, M, N, dep_final, spts, nsp);
+          else
+            t5::k_fwd_t5<S><<<grid, t5::kTile, t5::FwdT5::smem(), stream>>>(w, G, M, N, dep_final, spts, nsp);
+        }
       } else {
         GSB_CHECK(cudaFuncSetAttribute(tc::k_fwd_tc<S, FW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)tc::FwdTc<S, FW>::smem()));

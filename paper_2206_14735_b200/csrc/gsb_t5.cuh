@@ -308,8 +308,8 @@ struct FwdT5 {
   static constexpr size_t smem() { return (size_t)(tc::UmmaW::NFWD + tc::GVec::N + tc::CVec::N) * 4; }
 };
 
-template <class S>
-__global__ void __launch_bounds__(kTile, kCtaPerSm) k_fwd_t5(Ws<float> w, Geo G, int M, int N,
+template <class S, int CPS = kCtaPerSm>
+__global__ void __launch_bounds__(kTile, CPS) k_fwd_t5(Ws<float> w, Geo G, int M, int N,
                                                  const double* __restrict__ dep,
                                                  const float* __restrict__ spts, int nsp) {
   using F = tc::Fr<S>;
