@@ -156,13 +156,9 @@ __device__ __forceinline__ void gather_fast(const LevelDev& L, const LocT<T>& q,
 // before the 1/vs), from the same corner rows: grad phi then needs
 // g . J instead of a second read of the corners
 template <typename T, int C>
-__device__ __forceinline__ void gather_jac(const LevelDev& L, const LocT<T>& q, T* out, T (&J)[3 * C]) {
-  const T* F = reinterpret_cast<const T*>(L.feat) + (int64_t)q.base * C;
+__device__ __forceinline__ void jac_from_rows(const LocT<T>& q, const T (&r)[8][C], T* out, T (&J)[3 * C]) {
   T w[8];
   corner_w(q, w);
-  T r[8][C];
-#pragma unroll
-  for (int k = 0; k < 8; ++k) load_row<T, C>(F + corner_off(L, k) * C, r[k]);
   const T x1 = q.fx, y1 = q.fy, z1 = q.fz;
   const T x0 = T(1) - x1, y0 = T(1) - y1, z0 = T(1) - z1;
 #pragma unroll
@@ -178,6 +174,14 @@ __device__ __forceinline__ void gather_jac(const LevelDev& L, const LocT<T>& q, 
     J[3 * c + 2] = (r[1][c] - r[0][c]) * (x0 * y0) + (r[3][c] - r[2][c]) * (x0 * y1) +
                    (r[5][c] - r[4][c]) * (x1 * y0) + (r[7][c] - r[6][c]) * (x1 * y1);
   }
+}
+template <typename T, int C>
+__device__ __forceinline__ void gather_jac(const LevelDev& L, const LocT<T>& q, T* out, T (&J)[3 * C]) {
+  const T* F = reinterpret_cast<const T*>(L.feat) + (int64_t)q.base * C;
+  T r[8][C];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) load_row<T, C>(F + corner_off(L, k) * C, r[k]);
+  jac_from_rows<T, C>(q, r, out, J);
 }
 
 // grad phi contribution g . J / vs of a level whose Jacobian was kept

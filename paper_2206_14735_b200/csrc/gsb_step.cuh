@@ -41,9 +41,11 @@ inline int t5_mode() {
 }
 inline bool use_t5(bool coarse = true) { return t5_mode() == 1 || (t5_mode() == 2 && coarse); }
 // taped forward form: GSB_T5_FWD=0 mma.sync (tc::k_fwd_tc); > 0 tcgen05
-// (t5::k_fwd_t5, 4 CTAs per SM, register cap 128).  (A 3-CTA / 170-register
-// variant measured slower, 201 vs 190 us, and failed the conditioned float32
-// gradient check intermittently; it was removed.)
+// (t5::k_fwd_t5, 4 CTAs per SM, register cap 128); 3: 3 CTAs per SM, 170
+// registers (A/B, measured slower: 196 vs 181 us); 5: finest-level corners
+// staged in shared memory with cp.async one tile ahead (A/B, measured
+// slower: 221 vs 182 us -- the 4 x 56 KB carve-out leaves L1 28 KB for the
+// coarse-level gathers).
 // geometry backward form: GSB_T5_BWD=1 (default) tcgen05 (t5::k_bwd_geom_t5), 0 mma.sync
 inline bool use_t5_bwd() {
   static const bool v = [] {
@@ -285,10 +287,23 @@ int run_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step
         const int64_t tiles = (ns + t5::kTile - 1) / t5::kTile;
         const int grid = (int)std::min<int64_t>(tiles, (int64_t)sm_count() * (cps == 3 ? 3 : t5::kCtaPerSm));
         if (grid > 0) {
-          if (cps == 3)
+          bool staged = false;
+          if constexpr (S::CG == 4 && S::NL >= 2) {
+            if (cps == 5) {
+              GSB_CHECK(cudaFuncSetAttribute(t5::k_fwd_t5<S, t5::kCtaPerSm, true>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)t5::FwdT5::smem(true)));
+              t5::k_fwd_t5<S, t5::kCtaPerSm, true>
+                  <<<grid, t5::kTile, t5::FwdT5::smem(true), stream>>>(w, G, M, N, dep_final, spts, nsp);
+              staged = true;
+            }
+          }
+          if (staged) {
+          } else if (cps == 3) {
             t5::k_fwd_t5<S, 3><<<grid, t5::kTile, t5::FwdT5::smem(), stream>>>(w, G, M, N, dep_final, spts, nsp);
-          else
+          } else {
             t5::k_fwd_t5<S><<<grid, t5::kTile, t5::FwdT5::smem(), stream>>>(w, G, M, N, dep_final, spts, nsp);
+          }
         }
       } else {
         GSB_CHECK(cudaFuncSetAttribute(tc::k_fwd_tc<S, FW>, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -304,11 +304,27 @@ __global__ void __launch_bounds__(kTile) k_sdf_eval_t5(Ws<float> w, Geo G, int M
 // grid-space gradient are per-lane epilogues.  The next tile's gathers
 // overlap the last MMA.
 
+// Staged form (STG): the finest level's 8 corner rows of the NEXT tile are
+// copied HBM -> shared memory with cp.async (16 B per row, thread-private
+// slots [corner][lane]) while this tile's six MMA rounds run, so its gather
+// reads them from shared memory; the next tile's point is formed during this
+// tile's gather (its depth / ray loads overlap the coarse-level loads) and
+// parked in shared memory.  16 KB + 1.5 KB per CTA: still 4 CTAs per SM.
 struct FwdT5 {
-  static constexpr size_t smem() { return (size_t)(tc::UmmaW::NFWD + tc::GVec::N + tc::CVec::N) * 4; }
+  static constexpr int kVecEnd = tc::UmmaW::NFWD + tc::GVec::N + tc::CVec::N;  // floats
+  static constexpr int kStg = kVecEnd;                 // float4 [8][kTile]
+  static constexpr int kPt = kStg + 8 * kTile * 4;     // float [3][kTile]
+  static constexpr size_t smem(bool stg = false) { return (size_t)(stg ? kPt + 3 * kTile : kVecEnd) * 4; }
 };
+static_assert(FwdT5::kVecEnd % 4 == 0, "staging rows 16-byte aligned");
 
-template <class S, int CPS = kCtaPerSm>
+__device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(sdst)), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+template <class S, int CPS = kCtaPerSm, bool STG = false>
 __global__ void __launch_bounds__(kTile, CPS) k_fwd_t5(Ws<float> w, Geo G, int M, int N,
                                                  const double* __restrict__ dep,
                                                  const float* __restrict__ spts, int nsp) {
@@ -316,16 +332,18 @@ __global__ void __launch_bounds__(kTile, CPS) k_fwd_t5(Ws<float> w, Geo G, int M
   using U = tc::UmmaW;
   constexpr int KG = F::KG, KC = F::KC;
   static_assert(8 * KG <= 16 && 8 * KC <= 16, "input widths");
+  static_assert(!STG || (S::CG == 4 && S::NL >= kJacLevels), "staged form: 16-byte finest rows");
   extern __shared__ __align__(128) float t5_smem[];
   float* sw = t5_smem;
   const float* gvec = t5_smem + U::NFWD;
   const float* cvec = gvec + tc::GVec::N;
-  __shared__ __align__(8) uint64_t s_bar[2];
+  __shared__ __align__(8) uint64_t s_bar[2];  // [0] weight staging, [1] MMA completion
   __shared__ uint32_t s_tmem;
   const int64_t MN = (int64_t)M * N, NS = MN + nsp;
   const int64_t ntiles = (NS + kTile - 1) / kTile;
   if ((int64_t)blockIdx.x >= ntiles) return;
   const int tid = threadIdx.x, warp = tid >> 5;
+  const int64_t first = blockIdx.x, stride = gridDim.x;
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&s_tmem)),
                  "r"(kCols)
@@ -347,17 +365,18 @@ __global__ void __launch_bounds__(kTile, CPS) k_fwd_t5(Ws<float> w, Geo G, int M
   }
   const uint32_t tmem = s_tmem;
   const uint32_t tl = tmem + ((uint32_t)(warp * 32) << 16);
+  uint64_t* bar_d = &s_bar[1];
   auto sa = [&](int off) { return smem_u32(sw + off); };
   uint32_t phase = 0;
   auto run = [&](auto issue) {  // all lanes' A stores -> one thread issues -> wait for D
     cta_sync_tmem();
     if (tid == 0) {
       if (!(w.dbg & 16)) issue();
-      commit(&s_bar[1]);
+      commit(bar_d);
     }
   };
   auto wait_d = [&]() {
-    tc::mbar_wait(&s_bar[1], phase);
+    tc::mbar_wait(bar_d, phase);
     phase ^= 1u;
     fence_after();
   };
@@ -367,21 +386,58 @@ __global__ void __launch_bounds__(kTile, CPS) k_fwd_t5(Ws<float> w, Geo G, int M
   bool act;
   LocT<float> loc[S::NL];
   float z[8 * KG], inp[8 * KC];
-  auto gather = [&](int64_t tile) {
-    s = ((w.sweep & 1) ? ntiles - 1 - tile : tile) * kTile + tid;  // backward sweep: L2 reuse
-    act = s < NS;
-    ray = -1;
-    float p[3];
-    if (act && s < MN) {
-      ray = (int)((uint32_t)s / (uint32_t)N);
-      taped_point<float>(w.o + ray * 3, w.r + ray * 3,
-                         dep[(int64_t)ray * w.ld + (int)((uint32_t)s % (uint32_t)N)], G.lo, G.hi, p);
-    } else if (act) {
+  auto sample_of = [&](int64_t tile, int64_t& s_, int& ray_, bool& act_) {
+    s_ = ((w.sweep & 1) ? ntiles - 1 - tile : tile) * kTile + tid;  // backward sweep: L2 reuse
+    act_ = s_ < NS;
+    ray_ = act_ && s_ < MN ? (int)((uint32_t)s_ / (uint32_t)N) : -1;
+  };
+  auto point_of = [&](int64_t s_, int ray_, bool act_, float (&p)[3]) {
+    if (ray_ >= 0) {
+      taped_point<float>(w.o + ray_ * 3, w.r + ray_ * 3,
+                         dep[(int64_t)ray_ * w.ld + (int)((uint32_t)s_ % (uint32_t)N)], G.lo, G.hi, p);
+    } else if (act_) {
 #pragma unroll
-      for (int a = 0; a < 3; ++a) p[a] = spts[(s - MN) * 3 + a];
+      for (int a = 0; a < 3; ++a) p[a] = spts[(s_ - MN) * 3 + a];
     } else {
 #pragma unroll
       for (int a = 0; a < 3; ++a) p[a] = (float)G.lo[a];
+    }
+  };
+  float4* stg = reinterpret_cast<float4*>(t5_smem + FwdT5::kStg);
+  float* spt = t5_smem + FwdT5::kPt;
+  // STG: issue the finest level's corner copies for the point p (this
+  // thread's slots), park p
+  auto stage = [&](const float (&p)[3]) {
+    cp_async_wait_all();  // (no-op: the previous copies were consumed)
+    const LevelDev& L = G.lv[S::NL - 1];
+    const LocT<float> q = compact<float>(locate<false>(L, (double)p[0], (double)p[1], (double)p[2], nullptr));
+    const float* F = reinterpret_cast<const float*>(L.feat) + (int64_t)q.base * S::CG;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) cp_async16(stg + k * kTile + tid, F + corner_off(L, k) * S::CG);
+    cp_async_commit();
+#pragma unroll
+    for (int a = 0; a < 3; ++a) spt[a * kTile + tid] = p[a];
+  };
+  auto gather = [&](int64_t tile) {
+    sample_of(tile, s, ray, act);
+    float p[3];
+    if constexpr (STG) {
+#pragma unroll
+      for (int a = 0; a < 3; ++a) p[a] = spt[a * kTile + tid];
+    } else {
+      point_of(s, ray, act, p);
+    }
+    // STG: the next tile's point (its loads overlap this tile's gathers)
+    const int64_t nt = tile + stride;
+    float pn[3];
+    if constexpr (STG) {
+      if (nt < ntiles) {
+        int64_t sn;
+        int rn;
+        bool an;
+        sample_of(nt, sn, rn, an);
+        point_of(sn, rn, an, pn);
+      }
     }
 #pragma unroll
     for (int i = 0; i < 8 * KG; ++i) z[i] = 0.f;
@@ -397,7 +453,21 @@ __global__ void __launch_bounds__(kTile, CPS) k_fwd_t5(Ws<float> w, Geo G, int M
         // TMEM columns [96, 128), 16 per level, 12 used) so grad phi does
         // not re-read their corners
         float J[16];
-        gather_jac<float, S::CG>(G.lv[l], loc[l], z + l * S::CG, reinterpret_cast<float(&)[3 * S::CG]>(J));
+        if (STG && l == S::NL - 1) {
+          cp_async_wait_all();
+          float r[8][S::CG];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const float4 x = stg[k * kTile + tid];
+            r[k][0] = x.x;
+            r[k][1] = x.y;
+            r[k][2] = x.z;
+            r[k][3] = x.w;
+          }
+          jac_from_rows<float, S::CG>(loc[l], r, z + l * S::CG, reinterpret_cast<float(&)[3 * S::CG]>(J));
+        } else {
+          gather_jac<float, S::CG>(G.lv[l], loc[l], z + l * S::CG, reinterpret_cast<float(&)[3 * S::CG]>(J));
+        }
 #pragma unroll
         for (int i = 3 * S::CG; i < 16; ++i) J[i] = 0.f;
         st16(tl + kJacCol + 16 * (l - (S::NL - kJacLevels)), J);
@@ -417,10 +487,22 @@ __global__ void __launch_bounds__(kTile, CPS) k_fwd_t5(Ws<float> w, Geo G, int M
     }
 #pragma unroll
     for (int a = 0; a < 3; ++a) inp[S::CC + a] = w.r[cr * 3 + a];
+    if constexpr (STG) {
+      if (nt < ntiles) stage(pn);
+    }
   };
-  gather(blockIdx.x);
+  if constexpr (STG) {
+    int64_t s0;
+    int r0;
+    bool a0;
+    sample_of(first, s0, r0, a0);
+    float p0[3];
+    point_of(s0, r0, a0, p0);
+    stage(p0);
+  }
+  if (first < ntiles) gather(first);
   tc::mbar_wait(&s_bar[0], 0);
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  for (int64_t tile = first; tile < ntiles; tile += stride) {
     float h[32];
     uint32_t m0 = 0u;
     // ---- geometry layer 0 / 1 (gs/decoders.py:40-60)
@@ -488,7 +570,7 @@ __global__ void __launch_bounds__(kTile, CPS) k_fwd_t5(Ws<float> w, Geo G, int M
     const int64_t cs = s;
     const int cray = ray;
     const bool cact = act;
-    if (tile + gridDim.x < ntiles) gather(tile + gridDim.x);  // overlaps the last MMA
+    if (tile + stride < ntiles) gather(tile + stride);  // overlaps the last MMA
     wait_d();
     ld32(tl, h);
     float y[3] = {cvec[tc::CVec::b2], cvec[tc::CVec::b2 + 1], cvec[tc::CVec::b2 + 2]};
@@ -512,6 +594,7 @@ __global__ void __launch_bounds__(kTile, CPS) k_fwd_t5(Ws<float> w, Geo G, int M
       }
     }
   }
+  if constexpr (STG) cp_async_wait_all();
   fence_before();
   __syncthreads();
   if (warp == 0)
