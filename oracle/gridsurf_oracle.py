@@ -672,7 +672,9 @@ def train_objective(P, dataset, batch, iteration, cfg, smooth_override=None,
     points a float32 implementation used (conditioned kernel parity).
     ``relu_flips`` = {"geom" | "smooth" | "color": [(layer, row, unit)]}
     takes those ReLU derivative masks on the other side of their kink
-    (GeomPass); test-only.
+    (GeomPass); ``relu_flips["ratio"]`` = [(ray, j)] does the same for the
+    derivative of min(ratio, 1) in the alphas (gs/renderer.py:112-134) at
+    sigma_{j+1} / sigma_j = 1; test-only.
 
     ``shard`` (data-parallel restatement; not in the
     reference): dict with ``row_base`` and ``m_global`` (this batch is rows
@@ -763,6 +765,7 @@ def train_objective(P, dataset, batch, iteration, cfg, smooth_override=None,
     sig = sigmoid_raw(phis * s_t)
     Dden = np.maximum(sig[:, :-1], dt.type(SIGMA_FLOOR))
     ratio = sig[:, 1:] / Dden
+    R["ratio"] = ratio
     head = 1.0 - np.minimum(ratio, 1.0)
     al = np.concatenate([head, np.zeros((m, 1), dtype=dt)], axis=1)
     # composite: gs/renderer.py:137-159
@@ -861,7 +864,12 @@ def train_objective(P, dataset, batch, iteration, cfg, smooth_override=None,
     L_bar[:, :n - 1] = np.flip(np.cumsum(np.flip(tt[:, 1:], axis=1), axis=1), axis=1)
     om_bar = np.where(om >= dt.type(TRANS_FLOOR), L_bar / omc, 0.0).astype(dt)
     al_bar = al_bar - om_bar
-    r_bar = np.where(ratio <= 1.0, -al_bar[:, :n - 1], 0.0).astype(dt)
+    r_take = ratio <= 1.0
+    for row, j in flips.get("ratio", ()):
+        r_take[row, j] = not r_take[row, j]
+    r_bar = np.where(r_take, -al_bar[:, :n - 1], 0.0).astype(dt)
+    # size of the phi_bar jump at sample j + 1 if the ratio branch flips (test-only diagnostics)
+    R["ratio_jump"] = np.abs(al_bar[:, :n - 1] / Dden * (sig[:, 1:] * (1.0 - sig[:, 1:]))) * s_t
     sig_bar = np.zeros_like(sig)
     sig_bar[:, 1:] += r_bar / Dden
     D_bar = -(r_bar * sig[:, 1:]) / (Dden * Dden)
