@@ -3,16 +3,17 @@
 //
 // Step data flow (all on one stream, no host round trips):
 //   k_ray_setup      rays + stratified depths      gs/sampler.py:58-107, gs/renderer.py:302-321
+//                    (float32: k_setup, with the decoder weight tiles in its trailing blocks)
 //   k_sdf_eval       no-grad phi at listed samples gs/renderer.py:323-326, 236-240
 //   k_importance     one importance round per ray  gs/renderer.py:329-342, gs/sampler.py:128-197
 //   k_counts         tr/fs/eik partition counts    gs/renderer.py:384-412
 //   k_fwd            phi, grad phi, colour          gs/renderer.py:348-365
-//   k_smooth         smoothness loss + adjoints     gs/renderer.py:416-434
-//   k_render         alphas/composite/losses/adjoints (warp-free, thread per ray)
+//   k_render         alphas/composite/losses/adjoints (warp per ray)
 //                                                  gs/renderer.py:112-159, 372-414
+//                    + smoothness loss/adjoints in its trailing blocks  gs/renderer.py:416-434
 //   k_bwd_geom       grid scatter + geometry MLP grads
 //   k_bwd_color      colour grid scatter + colour MLP grads
-//   k_finalize_*     deterministic reductions of the per-CTA partials
+//   k_finalize       deterministic reductions of the per-CTA MLP partials and the losses
 //   k_adam           dense Adam over the arena       gs/optimizer.py:38-55
 #pragma once
 
@@ -218,10 +219,10 @@ __device__ __forceinline__ PixelRay pixel_ray(const gsb_dataset_t& D, int64_t fl
 constexpr int kRaySetupRays = 16;
 
 template <typename T>
-__global__ void __launch_bounds__(128) k_ray_setup(gsb_dataset_t D, const int64_t* __restrict__ ids, int M,
-                                                   int ray_base, Ws<T> w, Geo G, int Nc, double nearv,
-                                                   double max_depth, int has_ff, double ff, gsb_pcg64_t rng,
-                                                   PcgRounds imp) {
+__device__ __forceinline__ void ray_setup_block(const gsb_dataset_t& D, const int64_t* __restrict__ ids, int M,
+                                                int ray_base, const Ws<T>& w, const Geo& G, int Nc, double nearv,
+                                                double max_depth, int has_ff, double ff, const gsb_pcg64_t& rng,
+                                                const PcgRounds& imp, int blk, int nfin) {
   // RPB rays per block: threads 0..RPB-1 set the rays up, then all 128
   // threads fill the stratified depths, TPR threads per ray (each jumps its
   // own PCG stream to its first sample)
@@ -229,11 +230,12 @@ __global__ void __launch_bounds__(128) k_ray_setup(gsb_dataset_t D, const int64_
   static_assert(TPR >= GSB_MAX_ROUNDS, "one thread per importance round");
   __shared__ double s_near[RPB], s_span[RPB];
   const int t = threadIdx.x;
-  const int i = blockIdx.x * RPB + t;
-  if (blockIdx.x == 0) {  // the step's counters (first kernel of the step): no memset launches
+  const int i = blk * RPB + t;
+  if (blk == 0) {  // the step's counters (first kernel of the step): no memset launches
     if (t < 8) w.counts[t] = 0;
     if (t < GSB_MAX_ROUNDS) w.evl_count[t] = 0;
     if (t == 0) *w.loss_cnt = 0u;
+    for (int k = t; k < nfin; k += 128) w.fin_cnt[k] = 0u;  // k_finalize_mlp2 tickets
   }
   if (t < RPB && i < M) {
     PixelRay P = pixel_ray(D, ids[i]);
@@ -281,7 +283,7 @@ __global__ void __launch_bounds__(128) k_ray_setup(gsb_dataset_t D, const int64_
   }
   // the generator work does not depend on the rays: it runs before the
   // barrier, under the setup threads' dataset reads and float64 math
-  const int rl = t / TPR, q = t % TPR, ray = blockIdx.x * RPB + rl;
+  const int rl = t / TPR, q = t % TPR, ray = blk * RPB + rl;
   const bool live = ray < M;
   if (live && q < imp.n && w.imp_state) {  // importance round q: this row's first-uniform state
     Pcg g;
@@ -314,6 +316,13 @@ __global__ void __launch_bounds__(128) k_ray_setup(gsb_dataset_t D, const int64_
     const double uu = g.next_double();
     dep[j] = nv + span * (((double)j + uu) / (double)Nc);
   }
+}
+template <typename T>
+__global__ void __launch_bounds__(128) k_ray_setup(gsb_dataset_t D, const int64_t* __restrict__ ids, int M,
+                                                   int ray_base, Ws<T> w, Geo G, int Nc, double nearv,
+                                                   double max_depth, int has_ff, double ff, gsb_pcg64_t rng,
+                                                   PcgRounds imp, int nfin) {
+  ray_setup_block<T>(D, ids, M, ray_base, w, G, Nc, nearv, max_depth, has_ff, ff, rng, imp, blockIdx.x, nfin);
 }
 
 // ---------------------------------------------------------------------------
@@ -954,8 +963,7 @@ __global__ void __launch_bounds__(128) k_fwd(Ws<T> w, Geo G, int M, int N,
 // smoothness (gs/renderer.py:428-434): loss partial + grad-phi adjoints
 
 template <typename T>
-__global__ void k_smooth(Ws<T> w, int64_t MN, int S, T scale) {
-  int j = blockIdx.x * blockDim.x + threadIdx.x;
+__device__ __forceinline__ void smooth_item(Ws<T> w, int64_t MN, int S, T scale, int j) {
   if (j >= S) return;
   int64_t a = MN + j, b = MN + S + j;
   T acc = T(0);
@@ -1000,11 +1008,19 @@ __device__ __forceinline__ T warp_allsum(T v) {
 
 constexpr int kRenderRows = 6;  // per-warp shared arrays of N values
 
+// The smoothness pairs (k_smooth's work, nsm > 0) ride in trailing blocks
+// of the same launch: one launch fewer per step.
 template <typename T>
 __global__ void __launch_bounds__(128, 11) k_render(Ws<T> w, int M, int N, const double* __restrict__ dep,
                                                 const T* __restrict__ params, int64_t log_s_off,
-                                                LossW L) {
+                                                LossW L, int nsm = 0, int64_t MN = 0) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int rblocks = (M + 3) / 4;
+  if ((int)blockIdx.x >= rblocks) {  // block-uniform
+    const T scale = (T)(2.0 * L.smooth) / (T)L.smooth_global;
+    smooth_item<T>(w, MN, nsm, scale, ((int)blockIdx.x - rblocks) * 128 + (int)threadIdx.x);
+    return;
+  }
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   T* sig = reinterpret_cast<T*>(smem_raw) + (size_t)wid * kRenderRows * N;
   T* trn = sig + N;
@@ -1751,11 +1767,11 @@ __global__ void __launch_bounds__(WARPS * 32) k_bwd_color(Ws<T> w, Geo G, int M,
 // block = 32 parameters x 8 warps; warp w sums slots w, w+8, ...; then the 8
 // warp partials are added in warp order
 template <typename T, class S>
-__global__ void __launch_bounds__(256) k_finalize_mlp(Ws<T> w, T* grads, int64_t mlp_off,
-                                                      int nb_geo, int nb_col) {
+__device__ __forceinline__ void finalize_mlp_block(const Ws<T>& w, T* grads, int64_t mlp_off, int nb_geo,
+                                                   int nb_col, int bx) {
   __shared__ double red[8][33];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int t = blockIdx.x * 32 + lane;
+  const int t = bx * 32 + lane;
   double a = 0.0;
   if (t < S::NMLP) {
     const int nb = t < S::NG ? nb_geo : nb_col;
@@ -1778,12 +1794,12 @@ __global__ void __launch_bounds__(256) k_finalize_mlp(Ws<T> w, T* grads, int64_t
 constexpr int FIN_SPLIT = 16;
 
 template <typename T, class S>
-__global__ void __launch_bounds__(256) k_finalize_mlp2(Ws<T> w, T* grads, int64_t mlp_off,
-                                                       int nb_geo, int nb_col) {
+__device__ __forceinline__ void finalize_mlp2_block(const Ws<T>& w, T* grads, int64_t mlp_off, int nb_geo,
+                                                    int nb_col, int bx, int y) {
   __shared__ double red[8][33];
   __shared__ bool last;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int t = blockIdx.x * 32 + lane, y = blockIdx.y;
+  const int t = bx * 32 + lane;
   double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
   if (t < S::NMLP) {
     const int nb = t < S::NG ? nb_geo : nb_col;
@@ -1807,7 +1823,7 @@ __global__ void __launch_bounds__(256) k_finalize_mlp2(Ws<T> w, T* grads, int64_
     if (t < S::NMLP) w.fin_red[(size_t)y * S::NMLPP + t] = tot;
     __threadfence();
     __syncwarp();
-    if (lane == 0) last = atomicAdd(&w.fin_cnt[blockIdx.x], 1u) == FIN_SPLIT - 1;
+    if (lane == 0) last = atomicAdd(&w.fin_cnt[bx], 1u) == FIN_SPLIT - 1;
   }
   __syncthreads();
   if (last && wid == 0) {
@@ -1817,20 +1833,25 @@ __global__ void __launch_bounds__(256) k_finalize_mlp2(Ws<T> w, T* grads, int64_
       for (int k = 0; k < FIN_SPLIT; ++k) tot += __ldcg(&w.fin_red[(size_t)k * S::NMLPP + t]);
       grads[mlp_off + t] += (T)tot;
     }
-    if (lane == 0) w.fin_cnt[blockIdx.x] = 0u;  // ready for the next launch
+    if (lane == 0) w.fin_cnt[bx] = 0u;  // ready for the next launch
   }
+}
+template <typename T, class S>
+__global__ void __launch_bounds__(256) k_finalize_mlp2(Ws<T> w, T* grads, int64_t mlp_off,
+                                                       int nb_geo, int nb_col) {
+  finalize_mlp2_block<T, S>(w, grads, mlp_off, nb_geo, nb_col, blockIdx.x, blockIdx.y);
 }
 
 // Loss parts and the log_s gradient from the per-ray / per-smoothness-pair
 // partials: one thread per item over many blocks, block partials in a
 // scratch array, and the last block (atomic ticket) sums them in block order.
 template <typename T>
-__global__ void __launch_bounds__(256) k_finalize_loss(Ws<T> w, int M, int S, T* grads, const T* params,
-                                                       int64_t log_s_off, LossW L) {
+__device__ __forceinline__ void finalize_loss_block(const Ws<T>& w, int M, int S, T* grads, const T* params,
+                                                    int64_t log_s_off, const LossW& L, int blk, int nblk) {
   __shared__ double red[7][8];
   __shared__ bool last;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int i = blockIdx.x * 256 + tid;
+  const int i = blk * 256 + tid;
   double acc[7] = {0, 0, 0, 0, 0, 0, 0};
   if (i < M) {
     const double* p = w.ray_part + (int64_t)i * 8;
@@ -1848,11 +1869,11 @@ __global__ void __launch_bounds__(256) k_finalize_loss(Ws<T> w, int M, int S, T*
     double t = 0.0;
 #pragma unroll
     for (int q = 0; q < 8; ++q) t += red[tid][q];
-    w.loss_red[blockIdx.x * 8 + tid] = t;
+    w.loss_red[blk * 8 + tid] = t;
   }
   __threadfence();
   __syncthreads();
-  if (tid == 0) last = atomicAdd(w.loss_cnt, 1u) == gridDim.x - 1;
+  if (tid == 0) last = atomicAdd(w.loss_cnt, 1u) == (unsigned)nblk - 1;
   __syncthreads();
   if (!last) return;
   __threadfence();
@@ -1861,7 +1882,7 @@ __global__ void __launch_bounds__(256) k_finalize_loss(Ws<T> w, int M, int S, T*
   // walking every block
   if (wid < 7) {
     double a = 0.0;
-    for (int blk = lane; blk < (int)gridDim.x; blk += 32) a += __ldcg(&w.loss_red[blk * 8 + wid]);
+    for (int b = lane; b < nblk; b += 32) a += __ldcg(&w.loss_red[b * 8 + wid]);
     a = warp_sum(a);
     if (lane == 0) red[wid][0] = a;
   }
@@ -1891,6 +1912,21 @@ __global__ void __launch_bounds__(256) k_finalize_loss(Ws<T> w, int M, int S, T*
                          L.smooth * sm;
   // d total / d log_s = s * sum z_bar phi (exp vjp)
   grads[log_s_off] += (T)(tot[5] * s);
+}
+// the MLP reduction (blocks [0, ncol) one pass, or [0, ncol x FIN_SPLIT)
+// split) and the loss reduction (the blocks after them) in one launch
+template <typename T, class S, bool SPLIT>
+__global__ void __launch_bounds__(256) k_finalize(Ws<T> w, T* grads, int64_t mlp_off, int nb_geo, int nb_col,
+                                                  int M, int nsm, const T* params, int64_t log_s_off, LossW L,
+                                                  int nloss) {
+  constexpr int ncol = (S::NMLP + 31) / 32, nmlp = SPLIT ? ncol * FIN_SPLIT : ncol;
+  const int b = blockIdx.x;
+  if (b >= nmlp)
+    finalize_loss_block<T>(w, M, nsm, grads, params, log_s_off, L, b - nmlp, nloss);
+  else if constexpr (SPLIT)
+    finalize_mlp2_block<T, S>(w, grads, mlp_off, nb_geo, nb_col, b % ncol, b / ncol);
+  else
+    finalize_mlp_block<T, S>(w, grads, mlp_off, nb_geo, nb_col, b);
 }
 
 // ---------------------------------------------------------------------------

@@ -151,6 +151,19 @@ inline cudaError_t launch_sdf_t5(Ws<float> w, Geo G, int M, int Nc, const double
   return cudaGetLastError();
 }
 
+// float32 step start: ray setup (blocks [0, nrb)) and the decoder weight
+// tiles / fragments (k_wfrag's blocks after them) in one launch
+template <typename T, class S>
+__global__ void __launch_bounds__(128) k_setup(gsb_dataset_t D, const int64_t* __restrict__ ids, int M,
+                                               int ray_base, Ws<T> w, Geo G, int Nc, double nearv,
+                                               double max_depth, int has_ff, double ff, gsb_pcg64_t rng,
+                                               PcgRounds imp, int nfin, int nrb, const float* __restrict__ mlp) {
+  if ((int)blockIdx.x < nrb)
+    ray_setup_block<T>(D, ids, M, ray_base, w, G, Nc, nearv, max_depth, has_ff, ff, rng, imp, blockIdx.x, nfin);
+  else
+    tc::wfrag_block<S>(mlp, w.wfrag, (int)blockIdx.x - nrb);
+}
+
 namespace host {
 
 template <typename T, class S>
@@ -190,8 +203,10 @@ int run_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step
       w.pose_fb = reinterpret_cast<T*>(sc + PL.fb);
     }
     static_assert(tc::kFragBufU4 == 4096 + 68 + 3072, "workspace carve");
-    tc::k_wfrag<S><<<tc::Fr<S>::NALL + 1 + tc::UmmaW::kTiles, 128, 0, stream>>>(mlp32, w.wfrag);
-    GSB_LAUNCHED_T("k_wfrag");
+    if (!(st->phases & 1)) {  // otherwise k_setup builds them with the rays
+      tc::k_wfrag<S><<<tc::wfrag_blocks<S>(), 128, 0, stream>>>(mlp32, w.wfrag);
+      GSB_LAUNCHED_T("k_wfrag");
+    }
   }
   const size_t smem_sdf = (size_t)S::NG * esz;
   const size_t smem_fwd = ((size_t)(S::NMLP + 3) / 4 * 4 + 128 * FwdRow<T, S>::ROW) * esz;
@@ -204,9 +219,16 @@ int run_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step
     imp.n = R;
     imp.A = A;
     for (int r = 0; r < R; ++r) imp.r[r] = st->rng_importance[r];
-    k_ray_setup<T><<<(M + kRaySetupRays - 1) / kRaySetupRays, 128, 0, stream>>>(
-        *data, st->ray_ids, M, st->ray_base, w, G, Nc, st->near, st->max_depth,
-        st->has_fixed_far, st->fixed_far, st->rng_stratify, imp);
+    const int nrb = (M + kRaySetupRays - 1) / kRaySetupRays, nfin = (S::NMLP + 31) / 32;
+    if constexpr (F32) {
+      k_setup<T, S><<<nrb + tc::wfrag_blocks<S>(), 128, 0, stream>>>(
+          *data, st->ray_ids, M, st->ray_base, w, G, Nc, st->near, st->max_depth, st->has_fixed_far,
+          st->fixed_far, st->rng_stratify, imp, nfin, nrb, mlp32);
+    } else {
+      k_ray_setup<T><<<nrb, 128, 0, stream>>>(*data, st->ray_ids, M, st->ray_base, w, G, Nc, st->near,
+                                              st->max_depth, st->has_fixed_far, st->fixed_far,
+                                              st->rng_stratify, imp, nfin);
+    }
     GSB_LAUNCHED_T("k_ray_setup");
     if (R > 0) {
       int64_t n0 = (int64_t)M * Nc;
@@ -330,15 +352,11 @@ int run_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step
     L.m_global = st->m_global;
     L.smooth_global = st->smooth_global;
     if (runA) {
-      if (z.S > 0) {
-        T scale = (T)(2.0 * st->w_smooth) / (T)st->smooth_global;
-        k_smooth<T><<<(z.S + 127) / 128, 128, 0, stream>>>(w, z.MN, z.S, scale);
-        GSB_LAUNCHED_T("k_smooth");
-      }
+      // the smoothness pairs ride in k_render's trailing blocks
       const size_t smem_render = (size_t)4 * kRenderRows * N * esz;
       GSB_CHECK(cudaFuncSetAttribute(k_render<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_render));
-      k_render<T><<<(M + 3) / 4, 128, smem_render, stream>>>(w, M, N, dep_final, params,
-                                                                         model->log_s_offset, L);
+      k_render<T><<<(M + 3) / 4 + (z.S + 127) / 128, 128, smem_render, stream>>>(
+          w, M, N, dep_final, params, model->log_s_offset, L, z.S, z.MN);
       GSB_LAUNCHED_T("k_render");
       if (w.det_keys)  // every slot starts empty (~0 sorts last and is skipped)
         GSB_CHECK(cudaMemsetAsync(w.det_keys, 0xff, (size_t)DL.n * 8, stream));
@@ -441,17 +459,19 @@ int run_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step
       GSB_LAUNCHED_T("k_det_reduce");
     }
     static_assert(FIN_SPLIT == 16, "workspace carve");
+    const int nloss = (std::max(M, z.S) + 255) / 256;
+    // MLP-partial reduction and loss reduction in one launch
     if (nb_geo <= 256 && nb_col <= 256) {  // few (slot) rows: one pass, 8 warps per 32 parameters
-      k_finalize_mlp<T, S><<<(S::NMLP + 31) / 32, 256, 0, stream>>>(w, grads, model->mlp_offset, nb_geo, nb_col);
+      k_finalize<T, S, false><<<(S::NMLP + 31) / 32 + nloss, 256, 0, stream>>>(
+          w, grads, model->mlp_offset, nb_geo, nb_col, M, z.S, params, model->log_s_offset, L, nloss);
     } else {
-      GSB_CHECK(cudaMemsetAsync(w.fin_cnt, 0, (S::NMLP + 31) / 32 * sizeof(unsigned), stream));
-      k_finalize_mlp2<T, S><<<dim3((S::NMLP + 31) / 32, FIN_SPLIT), 256, 0, stream>>>(w, grads, model->mlp_offset,
-                                                                      nb_geo, nb_col);
+      // tickets: zeroed by the step's ray setup, and each launch leaves them zero
+      if (!(st->phases & 1))
+        GSB_CHECK(cudaMemsetAsync(w.fin_cnt, 0, (S::NMLP + 31) / 32 * sizeof(unsigned), stream));
+      k_finalize<T, S, true><<<(S::NMLP + 31) / 32 * FIN_SPLIT + nloss, 256, 0, stream>>>(
+          w, grads, model->mlp_offset, nb_geo, nb_col, M, z.S, params, model->log_s_offset, L, nloss);
     }
-    GSB_LAUNCHED_T("k_finalize_mlp");
-    k_finalize_loss<T><<<(std::max(M, z.S) + 255) / 256, 256, 0, stream>>>(w, M, z.S, grads, params,
-                                                                         model->log_s_offset, L);
-    GSB_LAUNCHED_T("k_finalize_loss");
+    GSB_LAUNCHED_T("k_finalize");
   }
   return GSB_OK;
 }

@@ -126,9 +126,9 @@ struct Fr {
 // One block per fragment id, one thread per lane.  Contraction index k of
 // fragment (kk, nn): b0 <-> k = 8kk+2t, b1 <-> k = 8kk+2t+1; output n = 8nn+g.
 template <class S>
-__global__ void __launch_bounds__(128) k_wfrag(const float* __restrict__ mlp, uint4* __restrict__ out) {
+__device__ __forceinline__ void wfrag_block(const float* __restrict__ mlp, uint4* __restrict__ out, int id) {
   using F = Fr<S>;
-  const int id = blockIdx.x, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   if (id > F::NALL) {  // tcgen05 B tiles (UmmaW), hi / lo per matrix
     const int tile = id - F::NALL - 1, lo = tile & 1, mat = tile >> 1;
     // mat: 0 W0^T, 1 W1^T, 2 W1, 3 W0, 4 W0c^T, 5 W1c^T, 6 W1c, 7 W0c.  B[n][k], K contiguous
@@ -222,6 +222,13 @@ __global__ void __launch_bounds__(128) k_wfrag(const float* __restrict__ mlp, ui
   split_tf32(b[1], h1, l1);
   out[id * 32 + lane] = make_uint4(h0, h1, l0, l1);
 }
+template <class S>
+__global__ void __launch_bounds__(128) k_wfrag(const float* __restrict__ mlp, uint4* __restrict__ out) {
+  wfrag_block<S>(mlp, out, blockIdx.x);
+}
+// blocks of k_wfrag
+template <class S>
+constexpr int wfrag_blocks() { return Fr<S>::NALL + 1 + UmmaW::kTiles; }
 
 // ---------------------------------------------------------------------------
 // fragment helpers

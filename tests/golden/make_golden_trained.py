@@ -79,9 +79,13 @@ def gt_mesh(scene, lo, hi, res):
 
 
 def main():
+    # --seed S (default 0): the reference's run with another batch / sampling
+    # seed, written to trained_c3_seed{S}.npz -- its spread over seeds is the
+    # scale the device runs' metrics are compared on
+    seed = int(sys.argv[sys.argv.index("--seed") + 1]) if "--seed" in sys.argv else 0
     t0 = time.time()
     ds = dataset()
-    cfg = optimizer.TrainConfig(precision="single", iterations=ITERS, batch_rays=1024, seed=0,
+    cfg = optimizer.TrainConfig(precision="single", iterations=ITERS, batch_rays=1024, seed=seed,
                                 checkpoint_every=EVAL_AT[0])
     per_it = {}
     with tempfile.TemporaryDirectory() as d:
@@ -100,14 +104,14 @@ def main():
             per_it[str(it)] = dict(metrics=json.loads(rep.to_json()), mesh_faces=int(len(culled.faces)),
                                    total=float(log[it].split(",")[1]))
     meta = dict(iters=ITERS, eval_at=list(EVAL_AT), res=RES, frames=FRAMES, width=W, height=H,
-                batch_rays=1024, seed=0, precision="single", per_iteration=per_it,
+                batch_rays=1024, seed=seed, precision="single", per_iteration=per_it,
                 first_total=float(log[1].split(",")[1]),
                 lo=list(map(float, model.grid.lo)), hi=list(map(float, model.grid.hi)),
                 gt_vertex_sum=float(gt.vertices[gt.faces].sum()), gt_faces=int(len(gt.faces)),
                 train_seconds=t_train)
     out = {"meta_json": np.frombuffer(json.dumps(meta).encode(), dtype=np.uint8),
            "loss_log": np.array([[float(x) for x in ln.split(",")] for ln in log[1:]])}
-    path = os.path.join(HERE, "trained_c3.npz")
+    path = os.path.join(HERE, "trained_c3.npz" if seed == 0 else f"trained_c3_seed{seed}.npz")
     np.savez_compressed(path, **out)
     print(path, json.dumps(meta, indent=1))
 

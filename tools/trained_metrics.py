@@ -1,7 +1,7 @@
 """Train SPEC scene #3 on the device (2000 iterations, float32, seed 0) and
 print the culled-mesh metrics at 200 / 2000 iterations (2 cm) and at 2000
 (1 cm): the numbers tests/test_trained_mesh.py checks.  Usage: python
-tools/trained_metrics.py [runs]"""
+tools/trained_metrics.py [runs] [seed ...]"""
 import json
 import os
 import sys
@@ -14,10 +14,12 @@ sys.path.insert(0, os.path.join(ROOT, "tests"))
 from test_trained_mesh import gt_mesh, scene_dataset  # noqa: E402
 from paper_2206_14735_b200 import mesher, optimizer  # noqa: E402
 
-for run in range(int(sys.argv[1]) if len(sys.argv) > 1 else 1):
+seeds = [int(a) for a in sys.argv[2:]] or [0]
+for run in range((int(sys.argv[1]) if len(sys.argv) > 1 else 1) * len(seeds)):
+    seed = seeds[run % len(seeds)]
     with tempfile.TemporaryDirectory() as d:
         ds = scene_dataset()
-        cfg = optimizer.TrainConfig(precision="single", iterations=2000, batch_rays=1024, seed=0,
+        cfg = optimizer.TrainConfig(precision="single", iterations=2000, batch_rays=1024, seed=seed,
                                     checkpoint_every=200)
         t0 = time.time()
         model, _ = optimizer.train(ds, cfg, d)
@@ -29,4 +31,4 @@ for run in range(int(sys.argv[1]) if len(sys.argv) > 1 else 1):
             rep = mesher.evaluate(mesher.cull_mesh(mesher.extract_mesh(m, resolution=r), ds), gt)
             res[f"{it}@{r}"] = {k: round(v, 5) for k, v in json.loads(rep.to_json()).items()
                                if k in ("chamfer_l1", "accuracy", "completion", "normal_consistency", "f_score")}
-        print(json.dumps({"run": run, "train_s": round(t, 2), **res}), flush=True)
+        print(json.dumps({"run": run, "seed": seed, "train_s": round(t, 2), **res}), flush=True)
