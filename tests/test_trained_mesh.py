@@ -2,22 +2,24 @@
 reference's Chamfer / F-score / normal consistency on the same synthetic scene.
 
 * Parity (tests/golden/make_golden_trained.py): the reference's own train()
-  (gs/optimizer.py:334-391: sphere pre-fit, then 2000 iterations, float32,
-  seed 0) on SPEC acceptance scene #3 (/root/reference/SPEC.md:702:
-  sphere-in-box, 40 frames 160x120, clean depth); meshes of its checkpoints
-  at iterations 200 and 2000 extracted at 2 cm (gs/mesher.py:148-151),
-  culled (gs/mesher.py:234-272) and evaluated against the analytic surface
-  (gs/mesher.py:368-400).  The device run does the same through this
-  package's train() / mesher; the median of RUNS device runs must be within
-  MESH_TOL of the reference's metrics at each checkpoint.  Runs are not
-  bit-identical (float32 summation orders, and Adam turns near-zero gradients
-  into +-lr steps): single device runs of this configuration measured C-l1
-  1.53-2.09 cm at 2000 iterations around the reference's 1.70 cm, so the
-  comparison is of medians at the metric level.
+  (gs/optimizer.py:334-391: sphere pre-fit, then 2000 iterations, float32)
+  on SPEC acceptance scene #3 (sphere-in-box,
+  40 frames 160x120, clean depth), once per batch / sampling seed (0, 1, 2:
+  trained_c3.npz, trained_c3_seed{1,2}.npz); meshes of its checkpoints at
+  iterations 200 and 2000 extracted at 2 cm (gs/mesher.py:148-151), culled
+  (gs/mesher.py:234-272) and evaluated against the analytic surface
+  (gs/mesher.py:368-400).  The device trains RUNS_PER_SEED runs per seed
+  through this package's train() / mesher, and the median over its runs must
+  be within MESH_TOL of the median over the reference's seeds at each
+  checkpoint.  Device runs are not bit-identical (float32 atomics; Adam turns
+  near-zero gradients into +-lr steps) and the dynamics amplify that: at one
+  seed, device runs measured C-l1 1.50-2.13 cm at 2000 iterations; over 15
+  runs (3 seeds) the median was 1.71 cm against the reference's 1.70 / 1.72
+  (seeds 0 / 1).  Hence medians over several runs and seeds.
 * SPEC #3 at 2000 iterations and the default 1 cm extraction: NC > 0.95 and
-  the >= 10x loss drop (SPEC.md:503), which the reference's own run meets;
+  the >= 10x loss drop (SPEC.md:503), which the reference's own runs meet;
   its C-l1 < 1 cm and F-score@5cm > 0.98 targets the reference itself misses
-  (1.70 cm, 0.911), so those are held to the reference's values.
+  (1.70 cm, 0.911 at seed 0), so those are held to the reference's values.
 
 The ground-truth surface is the analytic scene SDF (oracle/scene_host.py,
 the numpy evaluation of the same CSG program the renderer traces) on the
@@ -25,6 +27,7 @@ extraction lattice, through the same marching cubes and culling; its face
 count and vertex checksum equal the reference run's.
 """
 
+import glob
 import json
 import os
 import sys
@@ -47,9 +50,17 @@ MESH_TOL = {
 }
 
 
+def goldens():
+    """[(meta, loss_log)] of the reference runs, seed 0 first."""
+    out = []
+    for f in sorted(glob.glob(os.path.join(HERE, "golden", "trained_c3*.npz"))):
+        z = np.load(f)
+        out.append((json.loads(z["meta_json"].tobytes().decode()), z["loss_log"]))
+    return sorted(out, key=lambda g: g[0]["seed"])
+
+
 def golden():
-    z = np.load(os.path.join(HERE, "golden", "trained_c3.npz"))
-    return json.loads(z["meta_json"].tobytes().decode()), z["loss_log"]
+    return goldens()[0]
 
 
 def scene_dataset(frames=40, w=160, h=120):
@@ -73,26 +84,33 @@ def gt_mesh(model, res, ds):
     return mesher.cull_mesh(gt, ds)
 
 
-RUNS = 3  # device runs (float32 atomics: run-to-run chaos); their median is compared
+RUNS_PER_SEED = 2  # device runs per reference seed (float32 atomics: run-to-run chaos)
 
 
 @pytest.fixture(scope="module")
 def trained(tmp_path_factory):
-    """RUNS 2000-iteration float32 runs with checkpoints every 200 iterations."""
+    """2000-iteration float32 runs, RUNS_PER_SEED per reference seed, with
+    checkpoints every 200 iterations."""
     from paper_2206_14735_b200 import optimizer
     meta, _ = golden()
     ds = scene_dataset(meta["frames"], meta["width"], meta["height"])
     runs = []
-    for _ in range(RUNS):
-        out = str(tmp_path_factory.mktemp("trained"))
-        cfg = optimizer.TrainConfig(precision="single", iterations=meta["iters"],
-                                    batch_rays=meta["batch_rays"], seed=meta["seed"],
-                                    checkpoint_every=meta["eval_at"][0])
-        model, _ = optimizer.train(ds, cfg, out)
-        with open(os.path.join(out, "loss_log.csv")) as f:
-            log = np.array([[float(x) for x in ln.split(",")] for ln in f.read().splitlines()[1:]])
-        runs.append((out, model, log))
+    for gm, _ in goldens():
+        for _ in range(RUNS_PER_SEED):
+            out = str(tmp_path_factory.mktemp("trained"))
+            cfg = optimizer.TrainConfig(precision="single", iterations=gm["iters"],
+                                        batch_rays=gm["batch_rays"], seed=gm["seed"],
+                                        checkpoint_every=gm["eval_at"][0])
+            model, _ = optimizer.train(ds, cfg, out)
+            with open(os.path.join(out, "loss_log.csv")) as f:
+                log = np.array([[float(x) for x in ln.split(",")] for ln in f.read().splitlines()[1:]])
+            runs.append((out, model, log))
     return ds, runs
+
+
+def ref_median(it, key):
+    """Median over the reference's seeds of one checkpoint metric."""
+    return float(np.median([gm["per_iteration"][str(it)]["metrics"][key] for gm, _ in goldens()]))
 
 
 def _close(got, ref, tol):
@@ -121,16 +139,17 @@ def test_trained_mesh_matches_reference(trained):
             rep = mesher.evaluate(mesher.cull_mesh(mesher.extract_mesh(m, resolution=meta["res"]), ds), gt)
             per_run.append(json.loads(rep.to_json()))
         got = {k: float(np.median([r[k] for r in per_run])) for k in MESH_TOL[it]}
-        ref = meta["per_iteration"][str(it)]["metrics"]
-        print(it, "ours (median of", RUNS, "runs)", {k: round(v, 5) for k, v in got.items()},
+        ref = {k: ref_median(it, k) for k in MESH_TOL[it]}
+        print(it, "ours (median of", len(per_run), "runs)", {k: round(v, 5) for k, v in got.items()},
               "runs", [round(r["chamfer_l1"], 5) for r in per_run],
-              "reference", {k: round(ref[k], 5) for k in MESH_TOL[it]})
+              "reference (median of", len(goldens()), "seeds)", {k: round(ref[k], 5) for k in MESH_TOL[it]})
         bad.update({(it, k): (got[k], ref[k]) for k, tol in MESH_TOL[it].items()
                     if not _close(got[k], ref[k], tol)})
     assert not bad, bad
     # the loss curves agree (same batches; float32 run-to-run noise only)
     final = float(np.median([log[-1, 1] for _, _, log in runs]))
-    assert abs(final - ref_log[-1, 1]) <= 0.1 * abs(ref_log[-1, 1])
+    ref_final = float(np.median([lg[-1, 1] for _, lg in goldens()]))
+    assert abs(final - ref_final) <= 0.1 * abs(ref_final), (final, ref_final)
 
 
 def test_spec3_end_to_end_reconstruction(trained):
@@ -143,7 +162,7 @@ def test_spec3_end_to_end_reconstruction(trained):
     checked against the reference's own values (the parity tolerances of
     test_trained_mesh_matches_reference) instead of the SPEC's numbers."""
     from paper_2206_14735_b200 import mesher
-    meta, ref_log = golden()
+    meta, _ = golden()
     ds, runs = trained
     gt = gt_mesh(runs[0][1], 0.01, ds)
     reps = [mesher.evaluate(mesher.cull_mesh(mesher.extract_mesh(m, resolution=0.01), ds), gt)
@@ -151,10 +170,11 @@ def test_spec3_end_to_end_reconstruction(trained):
     for rep in reps:
         print(rep.table())
     med = lambda k: float(np.median([getattr(r, k) for r in reps]))
-    ref = meta["per_iteration"][str(meta["iters"])]["metrics"]
     assert med("normal_consistency") > 0.95  # SPEC #3 (the reference: 0.966)
     for _, _, log in runs:
         assert log[0, 1] / log[-1, 1] >= 10.0  # SPEC.md:503 (the reference: 51x)
-    assert ref_log[0, 1] / ref_log[-1, 1] >= 10.0
-    assert _close(med("chamfer_l1"), ref["chamfer_l1"], MESH_TOL[2000]["chamfer_l1"])
-    assert _close(med("f_score"), ref["f_score"], MESH_TOL[2000]["f_score"])
+    for _, lg in goldens():
+        assert lg[0, 1] / lg[-1, 1] >= 10.0
+    it = meta["iters"]
+    assert _close(med("chamfer_l1"), ref_median(it, "chamfer_l1"), MESH_TOL[2000]["chamfer_l1"])
+    assert _close(med("f_score"), ref_median(it, "f_score"), MESH_TOL[2000]["f_score"])
