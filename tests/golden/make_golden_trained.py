@@ -83,6 +83,23 @@ def main():
     # seed, written to trained_c3_seed{S}.npz -- its spread over seeds is the
     # scale the device runs' metrics are compared on
     seed = int(sys.argv[sys.argv.index("--seed") + 1]) if "--seed" in sys.argv else 0
+    # --perturb EPS (diagnostic): the pre-fit model's grid features times
+    # (1 + EPS u), u ~ U(-1, 1) -- the reference's own sensitivity to
+    # rounding-sized changes of its starting point; --out PATH for the result
+    eps = float(sys.argv[sys.argv.index("--perturb") + 1]) if "--perturb" in sys.argv else 0.0
+    if eps > 0:
+        build0 = optimizer.build_model
+
+        def build_perturbed(*a, **k):
+            m = build0(*a, **k)
+            rng = np.random.default_rng(int(sys.argv[sys.argv.index("--pseed") + 1]) if "--pseed" in sys.argv
+                                        else 12345)
+            for lv in list(m.grid.levels) + [m.grid.color]:
+                f = lv.features.data
+                f *= (1.0 + eps * rng.uniform(-1.0, 1.0, size=f.shape)).astype(f.dtype)
+            return m
+
+        optimizer.build_model = build_perturbed
     t0 = time.time()
     ds = dataset()
     cfg = optimizer.TrainConfig(precision="single", iterations=ITERS, batch_rays=1024, seed=seed,
@@ -112,6 +129,8 @@ def main():
     out = {"meta_json": np.frombuffer(json.dumps(meta).encode(), dtype=np.uint8),
            "loss_log": np.array([[float(x) for x in ln.split(",")] for ln in log[1:]])}
     path = os.path.join(HERE, "trained_c3.npz" if seed == 0 else f"trained_c3_seed{seed}.npz")
+    if "--out" in sys.argv:
+        path = sys.argv[sys.argv.index("--out") + 1]
     np.savez_compressed(path, **out)
     print(path, json.dumps(meta, indent=1))
 
