@@ -20,6 +20,15 @@ paper_2206_14735_b200/mc_table.py); the GPU side uses the same table.
 Metrics are recorded at iterations 200 (still converging) and 2000 (the
 SPEC's run length) from the run's own checkpoints.  tests/test_trained_mesh.py
 trains the B200 build the same way and compares its metrics with these.
+
+The goldens (the training dynamics amplify rounding-sized differences, so
+the gate compares distributions, not one run):
+    trained_c3.npz               seed 0
+    trained_c3_seed{1,2}.npz     --seed 1 / --seed 2
+    trained_c3_seed0_p{1,2}.npz  --perturb 1e-6 --pseed 1 / 2 --out ...: seed 0
+                                 from the pre-fit model's grid features times
+                                 (1 + 1e-6 u) -- a rounding-sized change of the
+                                 starting point (C-l1 at 2000: 1.53 vs 1.70 cm)
 """
 
 from __future__ import annotations
@@ -122,6 +131,8 @@ def main():
                                    total=float(log[it].split(",")[1]))
     meta = dict(iters=ITERS, eval_at=list(EVAL_AT), res=RES, frames=FRAMES, width=W, height=H,
                 batch_rays=1024, seed=seed, precision="single", per_iteration=per_it,
+                perturb=eps, pseed=(int(sys.argv[sys.argv.index("--pseed") + 1]) if "--pseed" in sys.argv
+                                    else 12345) if eps > 0 else None,
                 first_total=float(log[1].split(",")[1]),
                 lo=list(map(float, model.grid.lo)), hi=list(map(float, model.grid.hi)),
                 gt_vertex_sum=float(gt.vertices[gt.faces].sum()), gt_faces=int(len(gt.faces)),

@@ -5,17 +5,22 @@ reference's Chamfer / F-score / normal consistency on the same synthetic scene.
   (gs/optimizer.py:334-391: sphere pre-fit, then 2000 iterations, float32)
   on SPEC acceptance scene #3 (sphere-in-box,
   40 frames 160x120, clean depth), once per batch / sampling seed (0, 1, 2:
-  trained_c3.npz, trained_c3_seed{1,2}.npz); meshes of its checkpoints at
+  trained_c3.npz, trained_c3_seed{1,2}.npz) and at seed 0 from starting
+  points perturbed by 1e-6 relative (trained_c3_seed0_p*.npz: the
+  reference's own sensitivity to rounding-sized differences, C-l1 at 2000
+  1.53 vs 1.70 cm); meshes of its checkpoints at
   iterations 200 and 2000 extracted at 2 cm (gs/mesher.py:148-151), culled
   (gs/mesher.py:234-272) and evaluated against the analytic surface
-  (gs/mesher.py:368-400).  The device trains RUNS_PER_SEED runs per seed
-  through this package's train() / mesher, and the median over its runs must
-  be within MESH_TOL of the median over the reference's seeds at each
-  checkpoint.  Device runs are not bit-identical (float32 atomics; Adam turns
-  near-zero gradients into +-lr steps) and the dynamics amplify that: at one
-  seed, device runs measured C-l1 1.50-2.13 cm at 2000 iterations; over 15
-  runs (3 seeds) the median was 1.71 cm against the reference's 1.70 / 1.72
-  (seeds 0 / 1).  Hence medians over several runs and seeds.
+  (gs/mesher.py:368-400).  The device trains RUNS_PER_SEED runs per
+  reference run at its seed through this package's train() / mesher, and
+  the median over its runs must be within MESH_TOL of the median over the
+  reference's runs at each checkpoint.  Device runs are not bit-identical
+  (float32 atomics; Adam turns near-zero gradients into +-lr steps) and the
+  dynamics amplify that, as they amplify the 1e-6 perturbation on the
+  reference side: device runs measured C-l1 1.48-2.50 cm at 2000 iterations
+  (the spread is the floor's reconstruction, tools/diag_trained.py), median
+  1.71-1.85 cm, against the reference's 1.53-1.77 cm.  Hence medians over
+  several runs and seeds.
 * SPEC #3 at 2000 iterations and the default 1 cm extraction: NC > 0.95 and
   the >= 10x loss drop (SPEC.md:503), which the reference's own runs meet;
   its C-l1 < 1 cm and F-score@5cm > 0.98 targets the reference itself misses
@@ -56,7 +61,7 @@ def goldens():
     for f in sorted(glob.glob(os.path.join(HERE, "golden", "trained_c3*.npz"))):
         z = np.load(f)
         out.append((json.loads(z["meta_json"].tobytes().decode()), z["loss_log"]))
-    return sorted(out, key=lambda g: g[0]["seed"])
+    return sorted(out, key=lambda g: (g[0]["seed"], g[0].get("perturb") or 0.0, g[0].get("pseed") or 0))
 
 
 def golden():
