@@ -55,6 +55,7 @@ def build(force=False, verbose=False):
         return OUT
     os.makedirs(OBJDIR, exist_ok=True)
     extra = ["-Xptxas", "-v"] if verbose else []
+    extra += os.environ.get("GSB_NVCC_EXTRA", "").split()  # A/B builds (e.g. -DGSB_SPLIT_TRUNC)
     jobs = [([nvcc()] + NVCC_FLAGS + extra + ["-c", "-o", os.path.join(OBJDIR, "gsb.o"), SRC])]
     for tag, t, nl, cg, cc in STEP_UNITS:
         jobs.append([nvcc()] + NVCC_FLAGS + extra + [

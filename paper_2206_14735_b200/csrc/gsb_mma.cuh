@@ -17,12 +17,12 @@ __device__ __forceinline__ void split_tf32(float x, uint32_t& hi, uint32_t& lo) 
   hi = tf32_of(x);
   lo = tf32_of(x - __uint_as_float(hi));
 }
-// per-use split (3 integer/FP ops instead of two emulated cvt.rna): hi rounds
-// the mantissa half-away at bit 13, lo = x - hi is exact and goes to the MMA
-// raw (the tensor core ignores its low 13 bits): |x - hi - lo_tf32| <= 2^-21 |x|
+// per-use split: hi = x as is (mma.sync reads the top 19 bits of a tf32
+// operand, i.e. trunc(x)), lo = x - trunc(x) exact, also passed raw:
+// |x - trunc(x) - trunc(lo)| <= 2^-21 |x|
 __device__ __forceinline__ void split_fast(float x, uint32_t& hi, uint32_t& lo) {
-  hi = (__float_as_uint(x) + 0x1000u) & 0xffffe000u;
-  lo = __float_as_uint(x - __uint_as_float(hi));
+  hi = __float_as_uint(x);
+  lo = __float_as_uint(x - __uint_as_float(hi & 0xffffe000u));
 }
 __device__ __forceinline__ void mma_tf32(float (&d)[4], const uint32_t (&a)[4], uint32_t b0,
                                          uint32_t b1) {
