@@ -323,6 +323,9 @@ int run_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step
           if (staged) {
           } else if (cps == 3) {
             t5::k_fwd_t5<S, 3><<<grid, t5::kTile, t5::FwdT5::smem(), stream>>>(w, G, M, N, dep_final, spts, nsp);
+          } else if (w.dbg) {  // GSB_DBG attribution knobs (measurement only)
+            t5::k_fwd_t5<S, t5::kCtaPerSm, false, true>
+                <<<grid, t5::kTile, t5::FwdT5::smem(), stream>>>(w, G, M, N, dep_final, spts, nsp);
           } else {
             t5::k_fwd_t5<S><<<grid, t5::kTile, t5::FwdT5::smem(), stream>>>(w, G, M, N, dep_final, spts, nsp);
           }
@@ -398,9 +401,12 @@ int run_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step
           GSB_CHECK(cudaMemsetAsync(w.mlp_part, 0, (size_t)kMlpSlots * S::NMLPP * sizeof(T), stream));
         if (use_t5_bwd()) {
           const size_t smem_t5 = t5::GeoT5::smem<S>();
-          GSB_CHECK(cudaFuncSetAttribute(t5::k_bwd_geom_t5<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem_t5));
-          t5::k_bwd_geom_t5<S><<<nb_geo, t5::kTile, smem_t5, stream>>>(w, G, M, N, dep_final, spts, nsp, 2);
+          // the runtime-knob instantiation in production too: without the
+          // knob branches the compiler schedules the gather differently (255
+          // vs 236 registers) and the kernel measured slower, 311 vs 297 us
+          auto kern = t5::k_bwd_geom_t5<S, true>;
+          GSB_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_t5));
+          kern<<<nb_geo, t5::kTile, smem_t5, stream>>>(w, G, M, N, dep_final, spts, nsp, 2);
         } else {
           tc::k_bwd_geom_tc<S, WGEO><<<nb_geo, WGEO * 32, smem_g, stream>>>(w, G, M, N, mlp32,
                                                                             dep_final, spts, nsp, 2);
@@ -410,9 +416,9 @@ int run_step(const gsb_model_t* model, const gsb_dataset_t* data, const gsb_step
       if (runB) {
         if (use_t5_col()) {
           const size_t smem_t5 = t5::ColT5::smem<S>();
-          GSB_CHECK(cudaFuncSetAttribute(t5::k_bwd_color_t5<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem_t5));
-          t5::k_bwd_color_t5<S><<<nb_col, t5::kTile, smem_t5, stream>>>(w, G, M, N, dep_final);
+          auto kern = w.dbg ? t5::k_bwd_color_t5<S, true> : t5::k_bwd_color_t5<S>;
+          GSB_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_t5));
+          kern<<<nb_col, t5::kTile, smem_t5, stream>>>(w, G, M, N, dep_final);
         } else {
           tc::k_bwd_color_tc<S, WCOL><<<nb_col, WCOL * 32, smem_c, stream>>>(w, G, M, N, mlp32, dep_final);
         }

@@ -327,7 +327,7 @@ __device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
-template <class S, int CPS = kCtaPerSm, bool STG = false>
+template <class S, int CPS = kCtaPerSm, bool STG = false, bool DBG = false>
 __global__ void __launch_bounds__(kTile, CPS) k_fwd_t5(Ws<float> w, Geo G, int M, int N,
                                                  const double* __restrict__ dep,
                                                  const float* __restrict__ spts, int nsp) {
@@ -374,7 +374,7 @@ __global__ void __launch_bounds__(kTile, CPS) k_fwd_t5(Ws<float> w, Geo G, int M
   auto run = [&](auto issue) {  // all lanes' A stores -> one thread issues -> wait for D
     cta_sync_tmem();
     if (tid == 0) {
-      if (!(w.dbg & 16)) issue();
+      if (!(DBG && (w.dbg & 16))) issue();
       commit(bar_d);
     }
   };
@@ -448,7 +448,7 @@ __global__ void __launch_bounds__(kTile, CPS) k_fwd_t5(Ws<float> w, Geo G, int M
     for (int l = 0; l < S::NL; ++l) {
       loc[l] = compact<float>(locate<false>(G.lv[l], (double)p[0], (double)p[1], (double)p[2],
                                             act ? w.status : nullptr));
-      if (w.dbg & 8) {
+      if (DBG && (w.dbg & 8)) {
 #pragma unroll
         for (int c = 0; c < S::CG; ++c) z[l * S::CG + c] = 1e-3f * (float)c + loc[l].fx;
       } else if (l >= S::NL - kJacLevels && S::CG == 4) {
@@ -482,7 +482,7 @@ __global__ void __launch_bounds__(kTile, CPS) k_fwd_t5(Ws<float> w, Geo G, int M
     const Loc qc = locate<false>(G.col, (double)p[0], (double)p[1], (double)p[2], nullptr);
 #pragma unroll
     for (int i = 0; i < 8 * KC; ++i) inp[i] = 0.f;
-    if (w.dbg & 8) {
+    if (DBG && (w.dbg & 8)) {
 #pragma unroll
       for (int c = 0; c < S::CC; ++c) inp[c] = 1e-3f * (float)c + (float)qc.fx;
     } else {
@@ -547,7 +547,7 @@ __global__ void __launch_bounds__(kTile, CPS) k_fwd_t5(Ws<float> w, Geo G, int M
     float gr[3] = {0.f, 0.f, 0.f};
 #pragma unroll
     for (int l = 0; l < S::NL; ++l) {
-      if (w.dbg & 72) continue;
+      if (DBG && (w.dbg & 72)) continue;
       if (l >= S::NL - kJacLevels && S::CG == 4) {
         float J[16];
         ld16(tl + kJacCol + 16 * (l - (S::NL - kJacLevels)), J);
@@ -697,7 +697,7 @@ __device__ __forceinline__ float warp_colsum32(float (&v)[32]) {
   return v[0];
 }
 
-template <class S>
+template <class S, bool DBG = false>
 __global__ void __launch_bounds__(kTile, 2) k_bwd_geom_t5(Ws<float> w, Geo G, int M, int N,
                                                          const double* __restrict__ dep,
                                                          const float* __restrict__ spts, int nsp,
@@ -752,7 +752,7 @@ __global__ void __launch_bounds__(kTile, 2) k_bwd_geom_t5(Ws<float> w, Geo G, in
   auto mma_round = [&](auto issue) {
     cta_sync_tmem();
     if (tid == 0) {
-      if (!(w.dbg & 16)) issue();
+      if (!(DBG && (w.dbg & 16))) issue();
       commit(&s_bar[1]);
     }
     tc::mbar_wait(&s_bar[1], phase);
@@ -804,7 +804,7 @@ __global__ void __launch_bounds__(kTile, 2) k_bwd_geom_t5(Ws<float> w, Geo G, in
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
           float row[S::CG];
-          if (w.dbg & 8) {
+          if (DBG && (w.dbg & 8)) {
 #pragma unroll
             for (int c = 0; c < S::CG; ++c) row[c] = 1e-3f * (float)(c + k);
           } else {
@@ -889,7 +889,7 @@ __global__ void __launch_bounds__(kTile, 2) k_bwd_geom_t5(Ws<float> w, Geo G, in
     }
     __syncwarp();
     // ---- outer products over the warp's samples: dW0 += A0^T delta0, dW1 += A1^T delta1
-    if (!(w.dbg & 2)) {
+    if (!(DBG && (w.dbg & 2))) {
       const int g = lane >> 2, t = lane & 3;
       float d0[1][4][4], d1[2][4][4];
       tc::zero_d(d0);
@@ -941,9 +941,9 @@ __global__ void __launch_bounds__(kTile, 2) k_bwd_geom_t5(Ws<float> w, Geo G, in
       corner_w_ju(lq, (float)G.lv[l].inv_vs, u, wk, ju);
 #pragma unroll
       for (int k = 0; k < 8; ++k) coef[k] = fmaf(p, wk[k], ju[k]);
-      if (!(w.dbg & 1))
+      if (!(DBG && (w.dbg & 1)))
         scatter_level<float, S::CG>(G.lv[l], lq, gz + l * S::CG, coef, active,
-                                    (w.dbg & 128) && l == S::NL - 1, w.det_keys,
+                                    (DBG && (w.dbg & 128)) && l == S::NL - 1, w.det_keys,
                                     w.det_vals, s * (S::NL + 1) + l);
     }
   }
@@ -957,7 +957,7 @@ __global__ void __launch_bounds__(kTile, 2) k_bwd_geom_t5(Ws<float> w, Geo G, in
   __syncthreads();
   if (warp == 0)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(K::kCols2) : "memory");
-  if (w.dbg & 4) return;
+  if (DBG && (w.dbg & 4)) return;
   float* acc_all = rows_all;  // [4 warps][NGP] over the (now idle) sample rows
   {
     float* acc = acc_all + (size_t)warp * NGP;
@@ -1009,7 +1009,7 @@ struct ColT5 {
   static constexpr size_t smem() { return (size_t)(NW + tc::CVec::N) * 4 + (size_t)kTile * ROW * 4; }
 };
 
-template <class S>
+template <class S, bool DBG = false>
 __global__ void __launch_bounds__(kTile, 2) k_bwd_color_t5(Ws<float> w, Geo G, int M, int N,
                                                           const double* __restrict__ dep) {
   using F = tc::Fr<S>;
@@ -1066,7 +1066,7 @@ __global__ void __launch_bounds__(kTile, 2) k_bwd_color_t5(Ws<float> w, Geo G, i
   auto mma_round = [&](auto issue) {
     cta_sync_tmem();
     if (tid == 0) {
-      if (!(w.dbg & 16)) issue();
+      if (!(DBG && (w.dbg & 16))) issue();
       commit(&s_bar[1]);
     }
     tc::mbar_wait(&s_bar[1], phase);
@@ -1095,7 +1095,7 @@ __global__ void __launch_bounds__(kTile, 2) k_bwd_color_t5(Ws<float> w, Geo G, i
       float inp[16];
 #pragma unroll
       for (int i = 0; i < 16; ++i) inp[i] = 0.f;
-      if (w.dbg & 8) {
+      if (DBG && (w.dbg & 8)) {
 #pragma unroll
         for (int c = 0; c < S::CC; ++c) inp[c] = 1e-3f * (float)c + q.fx;
       } else if (w.scolf) {  // kept by the taped forward (the same gather, bit for bit)
@@ -1196,7 +1196,7 @@ __global__ void __launch_bounds__(kTile, 2) k_bwd_color_t5(Ws<float> w, Geo G, i
     }
     __syncwarp();
     // ---- outer products over the warp's samples: e0 = [inp,1]^T a0b, e1 = h0c^T a1b
-    if (!(w.dbg & 2)) {
+    if (!(DBG && (w.dbg & 2))) {
       const int g = lane >> 2, t = lane & 3;
       float w2c[4][3];
 #pragma unroll
@@ -1251,7 +1251,7 @@ __global__ void __launch_bounds__(kTile, 2) k_bwd_color_t5(Ws<float> w, Geo G, i
     {
       float wk[8];
       corner_w(q, wk);
-      if (!(w.dbg & 1))
+      if (!(DBG && (w.dbg & 1)))
         scatter_level<float, S::CC>(G.col, q, fb, wk, active, false, w.det_keys, w.det_vals,
                                     s * (S::NL + 1) + S::NL);
     }
@@ -1277,7 +1277,7 @@ __global__ void __launch_bounds__(kTile, 2) k_bwd_color_t5(Ws<float> w, Geo G, i
   __syncthreads();
   if (warp == 0)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(K::kCols) : "memory");
-  if (w.dbg & 4) return;
+  if (DBG && (w.dbg & 4)) return;
   float* acc_all = rows_all;  // [4 warps][NCP] over the (now idle) sample rows
   {
     float* acc = acc_all + (size_t)warp * NCP;
