@@ -28,7 +28,7 @@ the gate compares distributions, not one run):
     trained_c3_seed0_p{1,2}.npz  --perturb 1e-6 --pseed 1 / 2 --out ...: seed 0
                                  from the pre-fit model's grid features times
                                  (1 + 1e-6 u) -- a rounding-sized change of the
-                                 starting point (C-l1 at 2000: 1.53 vs 1.70 cm)
+                                 starting point (C-l1 at 2000: 1.53 and 1.67 vs 1.70 cm)
 """
 
 from __future__ import annotations
