@@ -573,10 +573,20 @@ int gsb_adam_step(int32_t precision, void* params, void* grads, void* m, void* v
   // persistent grid: exactly the resident blocks (no partial last wave).
   // (Four vectors in flight per thread instead of two measured slower:
   // 437 vs 351 us at config 2.)
-  static int resident[2] = {0, 0};
-  int& res = resident[precision == 0 ? 0 : 1];
+  // float32: 256-bit accesses (k_adam8) unless GSB_ADAM_V8=0 (A/B)
+  static const bool v8 = [] {
+    const char* e = std::getenv("GSB_ADAM_V8");
+    return e ? std::atoi(e) != 0 : true;
+  }();
+  const bool use8 = precision == 0 && v8 &&
+                    ((reinterpret_cast<uintptr_t>(params) | reinterpret_cast<uintptr_t>(grads) |
+                      reinterpret_cast<uintptr_t>(m) | reinterpret_cast<uintptr_t>(v)) & 31u) == 0;
+  static int resident[3] = {0, 0, 0};
+  int& res = resident[use8 ? 2 : (precision == 0 ? 0 : 1)];
   if (res == 0) {
-    if (precision == 0)
+    if (use8)
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&res, k_adam8<>, 256, 0);
+    else if (precision == 0)
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&res, k_adam<float>, 256, 0);
     else
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&res, k_adam<double>, 256, 0);
@@ -584,7 +594,10 @@ int gsb_adam_step(int32_t precision, void* params, void* grads, void* m, void* v
   }
   int blocks = num_sms() * res;
   timing_point(nullptr, s);
-  if (precision == 0)
+  if (use8)
+    k_adam8<><<<blocks, 256, 0, s>>>((float*)params, (float*)grads, (float*)m, (float*)v, n, sg,
+                                     k, guard, guard_threshold, guard_status, status);
+  else if (precision == 0)
     k_adam<float><<<blocks, 256, 0, s>>>((float*)params, (float*)grads, (float*)m, (float*)v, n, sg,
                                          k, guard, guard_threshold, guard_status, status);
   else
