@@ -203,7 +203,7 @@ def traffic_of(kernel, workload):
     return None
 
 
-def kernel_table(model, kt, K, M, N, S, P, peak_hbm, peak_bf16):
+def kernel_table(model, kt, K, M, N, S, P, peak_hbm, peak_bf16, workload=None):
     """Per-kernel algorithmic work over live CUDA-event times,
     against both roofs: measured HBM bandwidth, and the 3xTF32 tensor rate
     the float32 MLPs run at (tf32 is half the measured bf16 dense rate, and
@@ -231,6 +231,10 @@ def kernel_table(model, kt, K, M, N, S, P, peak_hbm, peak_bf16):
         r = {"kernel": name, "ms_per_step": ms / K, "launches_per_step": n / K,
              "alg_bytes": b, "alg_flops": 2 * mac, "hbm_gbs": hbm, "tflops": fl,
              "hbm_frac": hbm / peak_hbm, "tensor_frac": fl / tensor_peak}
+        tr = traffic_of(name, workload) if workload else None
+        if tr is not None and t > 0:  # measured DRAM bytes per launch (ncu) over this launch time
+            r["traffic_bytes"] = tr
+            r["dram_frac"] = tr * (n / K) / t / 1e9 / peak_hbm
         if t_ten > t_hbm:
             r.update(bound="tensor", achieved=fl, peak=tensor_peak, unit="TFLOP/s", frac=fl / tensor_peak,
                      peak_kind="3xTF32 rate derived from the measured bf16 dense peak "
@@ -580,7 +584,8 @@ def main():
     # ---- roofline of the dominant kernel + per-kernel table
     peak, peak_bf16, peak_kind = peaks()
     B, P = b_alg_bytes(model, M, N, S)
-    table = kernel_table(model, kt, K, M, N, S, P, peak, peak_bf16)
+    table = kernel_table(model, kt, K, M, N, S, P, peak, peak_bf16,
+                         f"config{args.config}" + ("-pose" if args.refine_poses else ""))
     dom = max(table, key=lambda r: r["ms_per_step"])
     roofline = {"bound": dom["bound"], "kernel": dom["kernel"], "achieved": dom["achieved"],
                 "peak": dom["peak"], "unit": dom["unit"], "frac": dom["frac"],
@@ -590,11 +595,12 @@ def main():
                 "step_hbm_frac": B / (ms_step / 1e3) / 1e9 / peak,
                 "objective_ms": obj_ms, "adam_ms": adam_ms,
                 "kernels": table}
-    roofline["note"] = ("k_adam reads all 32 B/param of state but writes nothing back for 16-byte "
-                        "vectors whose g, m and v are all +0 (never-touched parameters: the update "
-                        "would rewrite the same bits), so early in training or on large mostly-empty "
-                        "grids (config 4) its algorithmic-byte rate can exceed the copy peak; "
-                        "`traffic` is the measured DRAM bytes")
+    roofline["note"] = ("k_adam's algorithmic bytes are 32 B/param (p, g, m, v read and written); it "
+                        "reads all 16 B/param but skips the gradient-zeroing store where g is already "
+                        "+0 and every store where g, m and v are all +0 (never-touched parameters: the "
+                        "update would rewrite the same bits), so its algorithmic-byte rate can exceed "
+                        "the copy peak; `traffic` / the table's dram_frac use the measured DRAM bytes "
+                        "per launch (profiles/traffic.json, ncu)")
     tr = traffic_of(dom["kernel"], f"config{args.config}" + ("-pose" if args.refine_poses else ""))
     if tr is not None:
         roofline["traffic"] = tr
