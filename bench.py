@@ -232,9 +232,9 @@ def kernel_table(model, kt, K, M, N, S, P, peak_hbm, peak_bf16, workload=None):
              "alg_bytes": b, "alg_flops": 2 * mac, "hbm_gbs": hbm, "tflops": fl,
              "hbm_frac": hbm / peak_hbm, "tensor_frac": fl / tensor_peak}
         tr = traffic_of(name, workload) if workload else None
-        if tr is not None and t > 0:  # measured DRAM bytes per launch (ncu) over this launch time
+        if tr is not None and t > 0 and n == K:  # one launch per step: ncu DRAM bytes over its time
             r["traffic_bytes"] = tr
-            r["dram_frac"] = tr * (n / K) / t / 1e9 / peak_hbm
+            r["dram_frac"] = tr / t / 1e9 / peak_hbm
         if t_ten > t_hbm:
             r.update(bound="tensor", achieved=fl, peak=tensor_peak, unit="TFLOP/s", frac=fl / tensor_peak,
                      peak_kind="3xTF32 rate derived from the measured bf16 dense peak "
