@@ -358,15 +358,35 @@ class StepEngine:
         return self.smooth_points_dev(self.upload_smooth_raw(raw), len(raw[0]), delta, stream)
 
     def upload(self, draws, stream=None):
+        """Host draws -> device inputs.  On the default path the host-to-device
+        copies go on a copy stream the step's stream then waits for, so the
+        copies of step k+1 overlap step k's kernels (the caller runs ahead)."""
         torch = self.torch
         self.pose_tables(stream)
-        ids = torch.from_numpy(draws.ray_ids).pin_memory().to(self.device, non_blocking=True)
-        sm = None
-        if draws.smooth is not None:
-            sm = torch.from_numpy(np.ascontiguousarray(draws.smooth)).pin_memory().to(
-                self.device, non_blocking=True)
-        elif draws.smooth_raw is not None:
-            sm = self.smooth_points(draws.smooth_raw, draws.smooth_delta, stream)
+        side = stream is None and self.device.type == "cuda"
+        cur = torch.cuda.current_stream(self.device) if side else None
+        if side:
+            if getattr(self, "_copy_stream", None) is None:
+                self._copy_stream = torch.cuda.Stream(device=self.device)
+            ctx = torch.cuda.stream(self._copy_stream)
+        else:
+            import contextlib
+            ctx = contextlib.nullcontext()
+        raw_dev = sm = None
+        with ctx:
+            ids = torch.from_numpy(draws.ray_ids).pin_memory().to(self.device, non_blocking=True)
+            if draws.smooth is not None:
+                sm = torch.from_numpy(np.ascontiguousarray(draws.smooth)).pin_memory().to(
+                    self.device, non_blocking=True)
+            elif draws.smooth_raw is not None:
+                raw_dev = self.upload_smooth_raw(draws.smooth_raw)
+        if side:
+            cur.wait_stream(self._copy_stream)
+            for t in (ids, sm, raw_dev):
+                if t is not None:
+                    t.record_stream(cur)
+        if raw_dev is not None:
+            sm = self.smooth_points_dev(raw_dev, len(draws.smooth_raw[0]), draws.smooth_delta, stream)
         return ids, sm
 
     def launch(self, cfg, draws, ray_ids_dev, smooth_dev, stream=None, fresh=True, **kw):
