@@ -15,6 +15,8 @@ from __future__ import annotations
 import ctypes as C
 from dataclasses import dataclass
 
+import os
+
 import numpy as np
 
 from . import _lib
@@ -363,7 +365,10 @@ class StepEngine:
         copies of step k+1 overlap step k's kernels (the caller runs ahead)."""
         torch = self.torch
         self.pose_tables(stream)
-        side = stream is None and self.device.type == "cuda"
+        # (large batches only: at 1024 rays the step is host-bound and the
+        # extra stream bookkeeping costs more than the copy it hides)
+        side = (stream is None and self.device.type == "cuda" and len(draws.ray_ids) >= 4096
+                and os.environ.get("GSB_COPY_STREAM", "1") != "0")
         cur = torch.cuda.current_stream(self.device) if side else None
         if side:
             if getattr(self, "_copy_stream", None) is None:
