@@ -1097,14 +1097,19 @@ __global__ void __launch_bounds__(kTile, 2) k_bwd_color_t5(Ws<float> w, Geo G, i
     const int ray = active ? (int)((uint32_t)s / (uint32_t)N) : 0;
     __syncwarp();  // the previous tile's outer products are done with this warp's rows
     LocT<float> q;
-    float cb[3];
+    float cb[3], cc3[3];
     {
       float pt[3];
       taped_point<float>(w.o + ray * 3, w.r + ray * 3,
                          active ? dep[(int64_t)ray * w.ld + (int)((uint32_t)s % (uint32_t)N)] : 0.0, G.lo, G.hi,
                          pt);
 #pragma unroll
-      for (int c = 0; c < 3; ++c) cb[c] = active ? w.cbar[s * 3 + c] : 0.f;
+      for (int c = 0; c < 3; ++c) {
+        cb[c] = active ? w.cbar[s * 3 + c] : 0.f;
+        // the colour the taped forward stored: sigmoid of the same head
+        // (same MMA operands and order, so the same bits as recomputing it)
+        cc3[c] = active ? w.scol[s * 3 + c] : 0.f;
+      }
       q = compact<float>(locate<false>(G.col, (double)pt[0], (double)pt[1], (double)pt[2], nullptr));
       float inp[16];
 #pragma unroll
@@ -1152,21 +1157,17 @@ __global__ void __launch_bounds__(kTile, 2) k_bwd_color_t5(Ws<float> w, Geo G, i
     // R2
     mma_round([&] { issue_at<4>(tmem, tmem + 32, tmem + 64, sa(U::C1H), sa(U::C1L)); });
     ld32(tl, h);
-    float y[3] = {cvec[tc::CVec::b2], cvec[tc::CVec::b2 + 1], cvec[tc::CVec::b2 + 2]};
 #pragma unroll
     for (int n = 0; n < 32; ++n) {
       const float x = h[n] + cvec[tc::CVec::b1 + n];
       const bool pos = x > 0.f;
       h[n] = pos ? x : 0.f;
       m1 |= (uint32_t)pos << n;
-#pragma unroll
-      for (int c = 0; c < 3; ++c) y[c] = fmaf(h[n], cvec[tc::CVec::w2 + n * 3 + c], y[c]);
     }
     float yb[3];
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-      const float cc = sigmoid_fast(y[c]);
-      yb[c] = cb[c] * (cc * (1.f - cc));
+      yb[c] = cb[c] * (cc3[c] * (1.f - cc3[c]));
       myrow[K::oY + c] = yb[c];
     }
     myrow[K::oM] = __uint_as_float(m1);
