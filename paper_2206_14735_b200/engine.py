@@ -12,6 +12,7 @@ the PCG64 states of the uniform streams, which the device regenerates.
 
 from __future__ import annotations
 
+import contextlib
 import ctypes as C
 from dataclasses import dataclass
 
@@ -375,7 +376,6 @@ class StepEngine:
                 self._copy_stream = torch.cuda.Stream(device=self.device)
             ctx = torch.cuda.stream(self._copy_stream)
         else:
-            import contextlib
             ctx = contextlib.nullcontext()
         raw_dev = sm = None
         with ctx:
