@@ -14,9 +14,8 @@ from __future__ import annotations
 
 import contextlib
 import ctypes as C
-from dataclasses import dataclass
-
 import os
+from dataclasses import dataclass
 
 import numpy as np
 
