@@ -208,7 +208,9 @@ def kernel_table(model, kt, K, M, N, S, P, peak_hbm, peak_bf16, workload=None):
     against both roofs: measured HBM bandwidth, and the 3xTF32 tensor rate
     the float32 MLPs run at (tf32 is half the measured bf16 dense rate, and
     3xTF32 spends three tf32 MMAs per fp32-accurate product).  `bound` is
-    the roof with the larger ideal time."""
+    the roof with the larger ideal time.  Kernels launched once per step
+    also carry `dram_frac`: the measured DRAM bytes of one launch
+    (profiles/traffic.json, ncu) over its live time, against the copy peak."""
     G_s = sum(8 * l.width * 4 for l in model.grid.levels if l.features.size * 4 > 32 * 2 ** 20)
     Cc_s = 8 * 6 * 4 if model.grid.color.features.size * 4 > 32 * 2 ** 20 else 0
     n_imp = N - 12  # coarse + 2 x 12 evaluated (the last round's 12 are not)
