@@ -402,6 +402,64 @@ def test_sharded_adam_device_world2_equals_single(tmp_path):
     assert np.abs(z["m_sh"] - z["m_1"]).max() <= 1e-9 * max(np.abs(z["m_1"]).max(), 1e-300)
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("precision", ["single", "double"])
+def test_adam_owned_ranges_on_device(precision):
+    """One Adam launch over the whole arena with owned ranges (a data-parallel
+    rank's shards): the owned parameters, moments and cleared gradients are
+    bit-identical to a plain update, the foreign ones keep their parameters
+    and moments and get their gradients zeroed -- including ranges that start
+    and end half-way into an 8-float vector (the float32 kernel moves 32-byte
+    vectors, the ranges are 16-byte aligned)."""
+    import torch
+    from paper_2206_14735_b200 import optimizer
+    from test_train import small_setup
+    ds, cfg = small_setup(precision=precision)
+    model = optimizer.build_model(ds, cfg, skip_init=True, device=torch.device("cuda", 0))
+    a = model.arena
+    n = a.n
+    tdt = a.params.dtype
+
+    def init(opt):
+        a.params.copy_(torch.randn(n, generator=g0, dtype=torch.float64).to(tdt))
+        a.grads.copy_(torch.randn(n, generator=g0, dtype=torch.float64).to(tdt))
+        a.grads[: n // 3].zero_()  # untouched gradients too
+        opt.m_arena.copy_(torch.randn(n, generator=g0, dtype=torch.float64).to(tdt) * 0.1)
+        opt.v_arena.copy_(torch.rand(n, generator=g0, dtype=torch.float64).to(tdt) * 0.01)
+        opt.t = [4] * len(opt.t)
+
+    lo, hi = (n // 16) * 8 + 4, (n // 2) // 8 * 8 - 4  # both 4 floats off the 8-float grid
+    owned = [(lo, hi), (hi + 8, n)]
+    out = []
+    for ranges in (None, owned):
+        g0 = torch.Generator().manual_seed(11)
+        opt = optimizer.make_optimizer(model, cfg)
+        init(opt)
+        before = (a.params.cpu().numpy().copy(), opt.m_arena.cpu().numpy().copy(),
+                  opt.v_arena.cpu().numpy().copy())
+        opt.t = [5] * len(opt.t)
+        if ranges is None:
+            opt._launch()
+        else:
+            opt._launch(owned=ranges)
+        torch.cuda.synchronize()
+        out.append((before, a.params.cpu().numpy().copy(), opt.m_arena.cpu().numpy().copy(),
+                    opt.v_arena.cpu().numpy().copy(), a.grads.cpu().numpy().copy()))
+    (b0, p_full, m_full, v_full, _), (b1, p_own, m_own, v_own, g_own) = out
+    for x, y in zip(b0, b1):
+        np.testing.assert_array_equal(x, y)  # same starting state
+    mine = np.zeros(n, dtype=bool)
+    for x, y in owned:
+        mine[x:y] = True
+    np.testing.assert_array_equal(p_own[mine], p_full[mine])
+    np.testing.assert_array_equal(m_own[mine], m_full[mine])
+    np.testing.assert_array_equal(v_own[mine], v_full[mine])
+    np.testing.assert_array_equal(p_own[~mine], b1[0][~mine])
+    np.testing.assert_array_equal(m_own[~mine], b1[1][~mine])
+    np.testing.assert_array_equal(v_own[~mine], b1[2][~mine])
+    assert not np.any(g_own)
+
+
 def test_strong_split_rows_cover_the_global_batch():
     """bench.py --strong: the global batch (BASELINE c3(i), M = 6144) split by
     rows over N ranks covers every row once, in order, sizes within one, and
