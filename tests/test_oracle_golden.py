@@ -101,3 +101,27 @@ def test_two_iterations_double(run):
         assert R["parts"][k] == pytest.approx(v, rel=1e-9, abs=1e-14), k
     for i, n in enumerate(P1.names()):
         assert rel_maxnorm(P1.arrays()[i], G.a[f"final_{n}"]) <= 1e-8, n
+
+
+def test_relu_flips_ratio_semantics():
+    """The oracle's alpha-ratio kink switch (relu_flips["ratio"], used by
+    tests/test_f32_parity.py): flipping the branch of min(ratio, 1) at one
+    interval leaves every value and loss part unchanged and changes the
+    gradients only through that interval's two samples."""
+    G = load("tiny", "double")
+    P = oracle_params(G)
+    it = G.meta["iteration"]
+    batch = O.draw_ray_batch(G.ds, O.substream(G.cfg.seed, O.RAYS, it), G.cfg.batch_rays,
+                             near=G.cfg.near, far=G.cfg.max_depth)
+    R0 = O.train_objective(P, G.ds, batch, it, G.cfg)
+    # the interval with the largest phi_bar jump if flipped
+    row, j = np.unravel_index(np.argmax(R0["ratio_jump"]), R0["ratio_jump"].shape)
+    R1 = O.train_objective(P, G.ds, batch, it, G.cfg, relu_flips={"ratio": [(int(row), int(j))]})
+    assert R1["parts"] == R0["parts"]
+    np.testing.assert_array_equal(R1["phi"], R0["phi"])
+    assert any(not np.array_equal(R1["grads"][n], R0["grads"][n]) for n in R0["grads"])
+    # and flipping it back is the identity
+    R2 = O.train_objective(P, G.ds, batch, it, G.cfg,
+                           relu_flips={"ratio": [(int(row), int(j)), (int(row), int(j))]})
+    for n in R0["grads"]:
+        np.testing.assert_array_equal(R2["grads"][n], R0["grads"][n])
