@@ -263,7 +263,11 @@ __global__ void __launch_bounds__(kTile) k_sdf_eval_t5(Ws<float> w, Geo G, int M
     for (int i = S::IN_G; i < 8 * KG; ++i) z[i] = 0.f;
 #pragma unroll
     for (int l = 0; l < S::NL; ++l) {
-      const Loc q = locate<false>(G.lv[l], (double)p[0], (double)p[1], (double)p[2], act ? w.status : nullptr);
+      // bounds / NaN flag from the finest level only: the points are clipped
+      // into the box, so every level passes unless the point is NaN, which
+      // every level catches alike (the other levels' compares compile away)
+      const Loc q = locate<false>(G.lv[l], (double)p[0], (double)p[1], (double)p[2],
+                                  (act && l == S::NL - 1) ? w.status : nullptr);
       gather_fast<float, S::CG>(G.lv[l], compact<float>(q), z + l * S::CG);
     }
   };
@@ -463,7 +467,7 @@ __global__ void __launch_bounds__(kTile, CPS) k_fwd_t5(Ws<float> w, Geo G, int M
 #pragma unroll
     for (int l = 0; l < S::NL; ++l) {
       loc[l] = compact<float>(locate<false>(G.lv[l], (double)p[0], (double)p[1], (double)p[2],
-                                            act ? w.status : nullptr));
+                                            (act && l == S::NL - 1) ? w.status : nullptr));  // as in the SDF pass
       if (DBG && (w.dbg & 8)) {
 #pragma unroll
         for (int c = 0; c < S::CG; ++c) z[l * S::CG + c] = 1e-3f * (float)c + loc[l].fx;
