@@ -264,8 +264,9 @@ __global__ void __launch_bounds__(kTile) k_sdf_eval_t5(Ws<float> w, Geo G, int M
 #pragma unroll
     for (int l = 0; l < S::NL; ++l) {
       // bounds / NaN flag from the finest level only: the points are clipped
-      // into the box, so every level passes unless the point is NaN, which
-      // every level catches alike (the other levels' compares compile away)
+      // to the clamp box (half a finest voxel inside the grid box on every
+      // side), so every level passes unless the point is NaN, which every
+      // level catches alike (the other levels' compares compile away)
       const Loc q = locate<false>(G.lv[l], (double)p[0], (double)p[1], (double)p[2],
                                   (act && l == S::NL - 1) ? w.status : nullptr);
       gather_fast<float, S::CG>(G.lv[l], compact<float>(q), z + l * S::CG);

@@ -561,7 +561,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_sdf_eval_tc(Ws<float> w, Geo G, 
 #pragma unroll
     for (int l = 0; l < S::NL; ++l) {
       const Loc q = locate<false>(G.lv[l], (double)p[0], (double)p[1], (double)p[2],
-                                  act ? w.status : nullptr);
+                                  (act && l == S::NL - 1) ? w.status : nullptr);  // as t5::k_sdf_eval_t5
       gather_fast<float, S::CG>(G.lv[l], compact<float>(q), z + l * S::CG);
     }
     float* my = rows + lane * ROW;
@@ -659,7 +659,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_fwd_tc(Ws<float> w, Geo G, int M
 #pragma unroll
     for (int l = 0; l < S::NL; ++l) {
       loc[l] = compact<float>(locate<false>(G.lv[l], (double)p[0], (double)p[1], (double)p[2],
-                                            act ? w.status : nullptr));
+                                            (act && l == S::NL - 1) ? w.status : nullptr));
       gather_fast<float, S::CG>(G.lv[l], loc[l], z + l * S::CG);
     }
 #pragma unroll
