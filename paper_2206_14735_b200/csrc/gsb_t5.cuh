@@ -22,6 +22,23 @@ namespace t5 {
 
 using tc::smem_u32;
 
+// division by a loop-invariant divisor (samples per ray): multiply-high
+// with a precomputed magic number (round-up method, exact for every 32-bit
+// n and d >= 1) instead of the generic ~20-instruction sequence per sample
+struct FastDiv {
+  uint32_t d, m, sh;
+  __device__ __forceinline__ explicit FastDiv(uint32_t d_) : d(d_) {
+    sh = d_ > 1 ? 32u - (uint32_t)__clz(d_ - 1u) : 0u;  // ceil(log2 d)
+    m = d_ > 1 ? (uint32_t)((((1ull << 32) * ((1ull << sh) - d_)) / d_) + 1ull) : 0u;
+  }
+  __device__ __forceinline__ uint32_t div(uint32_t n) const {
+    if (sh == 0) return n;
+    const uint32_t t = __umulhi(n, m);
+    return (t + ((n - t) >> 1)) >> (sh - 1);
+  }
+  __device__ __forceinline__ uint32_t mod(uint32_t n, uint32_t q) const { return n - q * d; }
+};
+
 constexpr int kTile = 128;         // samples per CTA = TMEM lanes
 constexpr int kCtaPerSm = 4;       // 128 TMEM columns each: 4 x 128 = 512
 constexpr uint32_t kCols = 128;
@@ -200,6 +217,7 @@ __global__ void __launch_bounds__(kTile) k_sdf_eval_t5(Ws<float> w, Geo G, int M
                                                       const int32_t* __restrict__ list_count) {
   using F = tc::Fr<S>;
   constexpr int KG = F::KG;
+  const FastDiv fdc((uint32_t)Nc);
   extern __shared__ __align__(128) float t5_smem[];
   float* sw = t5_smem;                 // UmmaW block
   float* svec = t5_smem + SdfT5::NW;  // GVec block
@@ -246,8 +264,9 @@ __global__ void __launch_bounds__(kTile) k_sdf_eval_t5(Ws<float> w, Geo G, int M
         ray = e / GSB_KMAX;
         slot = e % GSB_KMAX;
       } else {
-        ray = (int)((uint32_t)s / (uint32_t)Nc);
-        slot = (int)((uint32_t)s % (uint32_t)Nc);
+        const uint32_t q = fdc.div((uint32_t)s);
+        ray = (int)q;
+        slot = (int)fdc.mod((uint32_t)s, q);
       }
     }
     const double d = act ? dep[(int64_t)ray * w.ld + slot] : 0.0;
@@ -357,6 +376,7 @@ __global__ void __launch_bounds__(kTile, CPS) k_fwd_t5(Ws<float> w, Geo G, int M
   constexpr int KG = F::KG, KC = F::KC;
   static_assert(8 * KG <= 16 && 8 * KC <= 16, "input widths");
   static_assert(!STG || (S::CG == 4 && S::NL >= kJacLevels), "staged form: 16-byte finest rows");
+  const FastDiv fdn((uint32_t)N);
   extern __shared__ __align__(128) float t5_smem[];
   float* sw = t5_smem;
   const float* gvec = t5_smem + U::NFWD;
@@ -413,12 +433,12 @@ __global__ void __launch_bounds__(kTile, CPS) k_fwd_t5(Ws<float> w, Geo G, int M
   auto sample_of = [&](int64_t tile, int64_t& s_, int& ray_, bool& act_) {
     s_ = ((w.sweep & 1) ? ntiles - 1 - tile : tile) * kTile + tid;  // backward sweep: L2 reuse
     act_ = s_ < NS;
-    ray_ = act_ && s_ < MN ? (int)((uint32_t)s_ / (uint32_t)N) : -1;
+    ray_ = act_ && s_ < MN ? (int)fdn.div((uint32_t)s_) : -1;
   };
   auto point_of = [&](int64_t s_, int ray_, bool act_, float (&p)[3]) {
     if (ray_ >= 0) {
       taped_point<float>(w.o + ray_ * 3, w.r + ray_ * 3,
-                         dep[(int64_t)ray_ * w.ld + (int)((uint32_t)s_ % (uint32_t)N)], G.lo, G.hi, p);
+                         dep[(int64_t)ray_ * w.ld + (int)fdn.mod((uint32_t)s_, (uint32_t)ray_)], G.lo, G.hi, p);
     } else if (act_) {
 #pragma unroll
       for (int a = 0; a < 3; ++a) p[a] = spts[(s_ - MN) * 3 + a];
@@ -729,6 +749,7 @@ __global__ void __launch_bounds__(kTile, 2) k_bwd_geom_t5(Ws<float> w, Geo G, in
   constexpr int KG = F::KG, ROW = K::ROW;
   constexpr int NGP = (S::NG + 3) / 4 * 4;
   static_assert(S::IN_G <= 16 && 8 * KG <= 16, "geometry input width");
+  const FastDiv fdn((uint32_t)N);
   extern __shared__ __align__(128) float t5_smem[];
   float* sw = t5_smem;
   const float* gvec = t5_smem + K::NW;
@@ -800,9 +821,9 @@ __global__ void __launch_bounds__(kTile, 2) k_bwd_geom_t5(Ws<float> w, Geo G, in
 #pragma unroll
         for (int a = 0; a < 3; ++a) u[a] = w.ubar[s * 3 + a];
         if (s < MN) {
-          const int ray = (int)((uint32_t)s / (uint32_t)N);
+          const int ray = (int)fdn.div((uint32_t)s);
           taped_point<float>(w.o + ray * 3, w.r + ray * 3,
-                             dep[(int64_t)ray * w.ld + (int)((uint32_t)s % (uint32_t)N)], G.lo, G.hi, pt);
+                             dep[(int64_t)ray * w.ld + (int)fdn.mod((uint32_t)s, (uint32_t)ray)], G.lo, G.hi, pt);
         } else {
 #pragma unroll
           for (int a = 0; a < 3; ++a) pt[a] = spts[(s - MN) * 3 + a];
@@ -1038,6 +1059,7 @@ __global__ void __launch_bounds__(kTile, 2) k_bwd_color_t5(Ws<float> w, Geo G, i
   constexpr int NCP = S::NMLP - S::NG, o = S::NG;
   static_assert(S::IN_C + 1 <= 16 && 8 * KC <= 16 && S::CC <= 8 && S::CC % 2 == 0, "colour input width");
   static_assert(S::oCb0 == S::oCW0 + S::IN_C * GSB_HID, "db0c is the ones row of dW0c");
+  const FastDiv fdn((uint32_t)N);
   extern __shared__ __align__(128) float t5_smem[];
   float* sw = t5_smem - K::W0;  // indexed by UmmaW offsets
   const float* cvec = t5_smem + K::NW;
@@ -1099,14 +1121,14 @@ __global__ void __launch_bounds__(kTile, 2) k_bwd_color_t5(Ws<float> w, Geo G, i
     const int64_t tt = (w.sweep & 4) ? ntiles - 1 - tile : tile;
     const int64_t s = tt * kTile + tid;
     const bool active = s < NS;
-    const int ray = active ? (int)((uint32_t)s / (uint32_t)N) : 0;
+    const int ray = active ? (int)fdn.div((uint32_t)s) : 0;
     __syncwarp();  // the previous tile's outer products are done with this warp's rows
     LocT<float> q;
     float cb[3], cc3[3];
     {
       float pt[3];
       taped_point<float>(w.o + ray * 3, w.r + ray * 3,
-                         active ? dep[(int64_t)ray * w.ld + (int)((uint32_t)s % (uint32_t)N)] : 0.0, G.lo, G.hi,
+                         active ? dep[(int64_t)ray * w.ld + (int)fdn.mod((uint32_t)s, (uint32_t)ray)] : 0.0, G.lo, G.hi,
                          pt);
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
